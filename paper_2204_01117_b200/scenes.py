@@ -1,0 +1,171 @@
+"""Synthetic scene generators in the reference's scenario-JSON schema v1.
+
+The reference's schema is parsed by ``citywind.scenario.scenario_from_dict``
+(/root/reference/pkg/src/citywind/scenario.py:132-301); these builders emit
+plain dicts in that schema so the oracle, the reference itself (when it is
+importable) and this package all consume byte-identical inputs.  The recipes
+follow SURVEY.md Appendix D (C1 cuboid, C2 street canyon, C3/C5 block city,
+C4 16-parameter design on the block-city generator).
+"""
+from __future__ import annotations
+
+import copy
+
+import numpy as np
+
+_NUMERICS = {"subdiv": 4, "ai_omega": 1.65, "ai_order": 1, "init": "inflow"}
+
+
+def cuboid(nx: int = 64, ny: int = 64, nz: int = 32, h: float = 2.0,
+           dt: float = 0.3, steps: int = 200) -> dict:
+    """C1: one opaque box building in uniform 3 m/s inflow along +x."""
+    return {
+        "version": 1, "name": f"cuboid-{nx}x{ny}x{nz}",
+        "grid": {"nx": nx, "ny": ny, "nz": nz, "dx": h, "dy": h, "dz": h},
+        "boundaries": {"x_min": "inlet", "x_max": "outlet", "y_min": "outlet",
+                       "y_max": "outlet", "z_min": "solid_wall", "z_max": "outlet"},
+        "inlet": {"kind": "uniform", "speed": 3.0, "direction": [1, 0]},
+        "solver": {"dt": dt, "turbulence": True, "turb_intensity": 0.1,
+                   "u_ref": 3.0, "length_scale": 20.0},
+        "objects": [{"name": "building", "kind": "building", "shape": "box",
+                     "lo": [0.35 * nx * h, 0.40 * ny * h, 0.0],
+                     "hi": [0.45 * nx * h, 0.60 * ny * h, 0.5 * nz * h], "phi": 0.0}],
+        "run": {"steps": steps, "snapshot_every": 0},
+        "numerics": dict(_NUMERICS),
+    }
+
+
+def canyon(nx: int = 128, ny: int = 128, nz: int = 64, h: float = 1.0,
+           dt: float = 0.2, steps: int = 500, n_trees: int = 8) -> dict:
+    """C2: two opaque slabs with a row of porous tree cylinders between them."""
+    L, W = nx * h, ny * h
+    objs = [
+        {"name": "slab_s", "kind": "building", "shape": "box",
+         "lo": [0.2 * L, 0.30 * W, 0.0], "hi": [0.8 * L, 0.42 * W, 18.0 * h], "phi": 0.0},
+        {"name": "slab_n", "kind": "building", "shape": "box",
+         "lo": [0.2 * L, 0.58 * W, 0.0], "hi": [0.8 * L, 0.70 * W, 18.0 * h], "phi": 0.0},
+    ]
+    for i in range(n_trees):
+        objs.append({"name": f"tree{i}", "kind": "tree", "shape": "cylinder",
+                     "center": [0.25 * L + 0.075 * L * i, 0.5 * W], "radius": 3.0 * h,
+                     "z0": 3.0 * h, "z1": 11.0 * h, "lad": 1.0})
+    return {
+        "version": 1, "name": f"canyon-{nx}x{ny}x{nz}",
+        "grid": {"nx": nx, "ny": ny, "nz": nz, "dx": h, "dy": h, "dz": h},
+        "boundaries": {"x_min": "inlet", "x_max": "outlet", "y_min": "outlet",
+                       "y_max": "outlet", "z_min": "solid_wall", "z_max": "outlet"},
+        "inlet": {"kind": "logarithmic", "u_star": 0.4, "z0": 0.5, "direction": [0.8, 0.6]},
+        "solver": {"dt": dt, "turbulence": True, "turb_intensity": 0.1,
+                   "u_ref": 4.0, "length_scale": 20.0},
+        "objects": objs,
+        "run": {"steps": steps, "snapshot_every": 0},
+        "numerics": dict(_NUMERICS),
+    }
+
+
+def block_city(nx: int = 256, ny: int = 256, nz: int = 64, h: float = 2.0,
+               seed: int = 0, nb: int = 6, dt: float = 0.5, steps: int = 100,
+               trees: bool = True) -> dict:
+    """C3 (and C5 at 512x512x128): an nb x nb lattice of random blocks.
+
+    RNG call order follows SURVEY.md Appendix D exactly so seed 0 at
+    256x256x64 yields the survey's 52-object city (36 buildings, 16 trees).
+    """
+    rng = np.random.default_rng(seed)
+    px = 0.7 * nx * h / nb
+    py = 0.7 * ny * h / nb
+    objs = []
+    for i in range(nb):
+        for j in range(nb):
+            x0 = 0.15 * nx * h + i * px
+            y0 = 0.15 * ny * h + j * py
+            fx, fy = rng.uniform(0.45, 0.75, 2)
+            ht = rng.uniform(8.0, 0.6 * nz * h)
+            phi = float(rng.choice([0.0, 0.0, 0.0, 0.3]))
+            objs.append({"name": f"b{i}_{j}", "kind": "building", "shape": "box",
+                         "lo": [x0, y0, 0.0],
+                         "hi": [x0 + fx * px, y0 + fy * py, float(ht)], "phi": phi})
+            if rng.random() < 0.5 and trees:
+                objs.append({"name": f"t{i}_{j}", "kind": "tree", "shape": "cylinder",
+                             "center": [x0 + 0.9 * px, y0 + 0.9 * py],
+                             "radius": 0.08 * px, "z0": 2.0, "z1": 12.0, "lad": 1.2})
+    return {
+        "version": 1, "name": f"block-city-{nx}x{ny}x{nz}-s{seed}",
+        "grid": {"nx": nx, "ny": ny, "nz": nz, "dx": h, "dy": h, "dz": h},
+        "boundaries": {"x_min": "inlet", "y_min": "inlet", "x_max": "outlet",
+                       "y_max": "outlet", "z_min": "solid_wall", "z_max": "outlet"},
+        "inlet": {"kind": "logarithmic", "u_star": 0.53, "z0": 0.5, "direction": [1, 1]},
+        "solver": {"dt": dt, "turbulence": True, "turb_intensity": 0.1,
+                   "u_ref": 5.0, "length_scale": 35.0},
+        "objects": objs,
+        "run": {"steps": steps, "snapshot_every": 0},
+        "numerics": dict(_NUMERICS),
+    }
+
+
+def block_city_design(nx: int = 256, ny: int = 256, nz: int = 64, h: float = 2.0,
+                      seed: int = 0, nb: int = 6, dt: float = 0.5,
+                      settle_steps: int = 300) -> dict:
+    """C4: block city plus 16 design parameters (extent_z of 8 blocks and
+    extent_x of 8 blocks, scenario.py:394-398 bindings) and 6 objective
+    regions (3 courtyards, 3 corner gaps)."""
+    doc = block_city(nx, ny, nz, h, seed, nb, dt)
+    blocks = [o for o in doc["objects"] if o["kind"] == "building"]
+    design = []
+    for n, o in enumerate(blocks[:8]):
+        span = 0.25 * (o["hi"][2] - o["lo"][2])
+        design.append({"name": f"h_{o['name']}", "lo": -span, "hi": span, "initial": 0.0,
+                       "object": o["name"], "transform": "extent_z"})
+    for n, o in enumerate(blocks[8:16]):
+        span = 0.2 * (o["hi"][0] - o["lo"][0])
+        design.append({"name": f"w_{o['name']}", "lo": -span, "hi": span, "initial": 0.0,
+                       "object": o["name"], "transform": "extent_x"})
+    Lx, Ly = nx * h, ny * h
+    px, py = 0.7 * Lx / nb, 0.7 * Ly / nb
+    regions = []
+    for r in range(3):  # sheltered gaps between blocks (heat pockets)
+        cx = 0.15 * Lx + (1.5 + r) * px - 0.05 * px
+        cy = 0.15 * Ly + (1.5 + r) * py - 0.05 * py
+        regions.append({"name": f"court{r}", "lo": [cx - 0.1 * px, cy - 0.1 * py, 0.0],
+                        "hi": [cx + 0.1 * px, cy + 0.1 * py, 6.0]})
+    for r in range(3):  # corner gaps (wind comfort)
+        cx = 0.15 * Lx + (r + 1) * px - 0.1 * px
+        cy = 0.15 * Ly + 0.5 * py
+        regions.append({"name": f"gap{r}", "lo": [cx - 0.08 * px, cy - 0.1 * py, 0.0],
+                        "hi": [cx + 0.08 * px, cy + 0.1 * py, 6.0]})
+    doc["design"] = design
+    doc["objective"] = {"regions": regions, "target_speed": 0.55,
+                        "settle_steps": settle_steps, "avg_fraction": 0.25}
+    doc["name"] = doc["name"].replace("block-city", "block-city-design")
+    return doc
+
+
+def channel_2d(nx: int = 24, ny: int = 16, dt: float = 0.1, speed: float = 2.0) -> dict:
+    """2D walled channel (the reference tests' `channel()` helper geometry)."""
+    return {
+        "version": 1, "name": f"channel2d-{nx}x{ny}",
+        "grid": {"nx": nx, "ny": ny, "nz": 1, "dx": 1.0, "dy": 1.0, "dz": 1.0},
+        "boundaries": {"x_min": "inlet", "x_max": "outlet",
+                       "y_min": "solid_wall", "y_max": "solid_wall"},
+        "inlet": {"kind": "uniform", "speed": speed, "direction": [1, 0]},
+        "solver": {"dt": dt, "turbulence": True, "u_ref": speed},
+        "objects": [],
+        "run": {"steps": 50},
+        "numerics": dict(_NUMERICS),
+    }
+
+
+def scaled(doc: dict, **grid) -> dict:
+    """Copy of ``doc`` with grid entries replaced (used to shrink scenes)."""
+    out = copy.deepcopy(doc)
+    out["grid"].update(grid)
+    return out
+
+
+CONFIGS = {
+    "C1": lambda: cuboid(64, 64, 32, 2.0, 0.3, 200),
+    "C2": lambda: canyon(128, 128, 64, 1.0, 0.2, 500),
+    "C3": lambda: block_city(256, 256, 64, 2.0, 0, 6, 0.5),
+    "C4": lambda: block_city_design(256, 256, 64, 2.0, 0, 6, 0.5),
+    "C5": lambda: block_city(512, 512, 128, 2.0, 0, 6, 0.5),
+}
