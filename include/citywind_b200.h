@@ -1,0 +1,170 @@
+/*
+ * citywind_b200 -- C ABI of the B200-native RANS step path.
+ *
+ * Drop-in boundary for the reference's Python step path
+ * (/root/reference/pkg/src/citywind/, "ref" below).  The reference has no
+ * native FFI of its own: its hot path is the Python call
+ *     solver.step(state, params, psys, preconditioner, profile, advector, pcg_tol)
+ * (ref solver.py:407-461) plus the per-design precompute of
+ * CompiledScenario (ref scenario.py:364-445).  Each entry point below
+ * replaces one of those Python-level interfaces; the Python mirror
+ * (paper_2204_01117_b200/_native.py) binds them with ctypes.
+ *
+ * Conventions
+ *  - plain C types only; device buffers are passed as raw device pointers
+ *    (void*), streams as cudaStream_t cast to void*.
+ *  - every field is x-fastest: a cell field has nx*ny*nz entries with x
+ *    fastest; u has (nx+1)*ny*nz, v nx*(ny+1)*nz, w nx*ny*(nz+1).
+ *  - "real" buffers are float or double according to the precision the
+ *    context was created with (4 or 8).
+ *  - functions return CW_OK or an error code; cw_last_error() gives a
+ *    thread-local message.  Error codes map to the reference's exceptions
+ *    (see the CW_ERR_* comments).
+ */
+#ifndef CITYWIND_B200_H
+#define CITYWIND_B200_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CW_ABI_VERSION 1
+
+#define CW_OK 0
+#define CW_ERR_INVALID 1       /* ValueError: bad argument / shape */
+#define CW_ERR_CUDA 2          /* CUDA runtime failure */
+#define CW_ERR_SINGULAR 3      /* SingularSystemError, ref linalg.py:23,114-117 */
+#define CW_ERR_PCG 4           /* ProjectionError, ref solver.py:113-116,275-276 */
+#define CW_ERR_NONFINITE 5     /* FloatingPointError, ref turbulence.py:123-127 */
+#define CW_ERR_TIMEOUT 6       /* device grid barrier timed out (never expected) */
+#define CW_ERR_RHS 7           /* ValueError non-finite rhs, ref linalg.py:326-327 */
+#define CW_ERR_GEOMETRY 8      /* ClassificationError, ref geometry.py:31,236-240 */
+
+typedef struct cw_ctx cw_ctx;
+
+/* GridSpec, ref grid.py:33-84 */
+typedef struct {
+  int nx, ny, nz;
+  double dx, dy, dz;
+  double origin[3];
+} cw_grid;
+
+/* SolverParams, ref solver.py:26-50 (inlet k/omega derived host-side) */
+typedef struct {
+  double dt, nu, cd_tree, cd_building, drag_a, drag_b, drag_eps;
+  double c_mu, alpha, beta, sigma, sigma_star, c_lim;
+  double k_in, omega_in;       /* SolverParams.inlet_k_omega(), ref solver.py:48-50 */
+  int turbulence;
+} cw_params;
+
+/* InletProfile, ref solver.py:54-97: speed_at() sampled at cell-centre heights */
+typedef struct {
+  int kind;                    /* 0 uniform, 1 logarithmic */
+  double speed, u_star, z0, kappa;
+  double dir_x, dir_y;         /* already normalised (ref solver.py:69-75) */
+} cw_inlet;
+
+/* FlowState device buffers, ref grid.py:492-571 */
+typedef struct {
+  void *u, *v, *w, *p, *k, *omega, *nu_t;   /* real */
+  const signed char *labels;                /* int8 CellLabel, ref grid.py:19-29 */
+  const void *g;                            /* real per-cell drag coefficient C_d*G */
+  int has_drag;                             /* any(g != 0), ref solver.py:157-158 */
+} cw_fields;
+
+/* StepReport + PcgReport, ref solver.py:101-110, linalg.py:27-31 */
+typedef struct {
+  int iterations, converged, status;        /* status: CW_OK or a CW_ERR_* code */
+  int bad_field;                            /* 0 k, 1 omega when status == CW_ERR_NONFINITE */
+  double criterion, cfl, div_before, div_after;
+  long long bad_cell;                       /* ref C-order (i*ny+j)*nz+k of first non-finite */
+  float ms_total;                           /* device time of the step, when timed */
+} cw_report;
+
+int cw_abi_version(void);
+const char *cw_last_error(void);
+
+/* Context = one grid on one device. Replaces CompiledScenario's per-grid
+ * state (ref scenario.py:364-381). precision: 4 (fp32) or 8 (fp64). */
+int cw_ctx_create(const cw_grid *grid, int precision, int device, cw_ctx **out);
+void cw_ctx_destroy(cw_ctx *ctx);
+
+/* build_pressure_matrix + build_ai_preconditioner(A, omega, 1, truncate=False)
+ * (ref linalg.py:57-126, 201-232; called from scenario.py:377-379), matrix-free:
+ * derives the per-cell operator code from labels (device int8).  Returns the
+ * unknown count and default_projection_tol (ref solver.py:235-243). */
+int cw_set_operator(cw_ctx *ctx, const signed char *d_labels, double ai_omega,
+                    long long *n_unknown, double *tol_default, void *stream);
+
+/* Select the preconditioner of the projection: 0 identity (plain CG),
+ * 1 Jacobi (build_jacobi, ref linalg.py:194-198), 2 untruncated AI1 (default).
+ * Returns the matching default_projection_tol. */
+int cw_set_preconditioner(cw_ctx *ctx, int kind, double *tol_default);
+
+/* Drag coefficient per cell, drag_factor_cells (ref solver.py:123-135), from
+ * float64 phi/lad (device) into the context-precision buffer g. */
+int cw_drag_coefficient(cw_ctx *ctx, const double *d_phi, const double *d_lad,
+                        const signed char *d_labels, const cw_params *prm, void *d_g,
+                        int *has_drag, void *stream);
+
+/* apply_boundary_conditions (ref solver.py:330-400) on a state. */
+int cw_apply_boundary(cw_ctx *ctx, const cw_fields *f, const cw_params *prm,
+                      const cw_inlet *inl, void *stream);
+
+/* Enqueue nsteps calls of step() (ref solver.py:407-461) without any host
+ * synchronisation; pcg_tol < 0 selects default_projection_tol.  Reports are
+ * collected on the device; read them with cw_read_reports. */
+int cw_step(cw_ctx *ctx, const cw_fields *f, const cw_params *prm, const cw_inlet *inl,
+            double pcg_tol, int nsteps, void *stream);
+
+/* Run ONE stage function of the reference on a state, with dt = prm->dt:
+ * advect (advect_velocity + upwind_scalar k/omega, advection.py:125-173),
+ * diffuse (solver.py:193-208), apply_drag (:150-168), apply_boundary_conditions
+ * (:330-400), project (:246-304, incl. div before/after), update_turbulence
+ * (turbulence.py:100-132).  Uses one report slot like a step. */
+#define CW_STAGE_ADVECT 1
+#define CW_STAGE_DIFFUSE 2
+#define CW_STAGE_DRAG 3
+#define CW_STAGE_BOUNDARY 4
+#define CW_STAGE_PROJECT 5
+#define CW_STAGE_TURBULENCE 6
+int cw_run_stage(cw_ctx *ctx, const cw_fields *f, const cw_params *prm, const cw_inlet *inl,
+                 int stage, double pcg_tol, void *stream);
+
+/* Synchronise `stream`, copy up to n pending step reports (oldest first) into
+ * out, clear them and the error latch.  *n_out = number written.  Returns
+ * the status of the first failed step (CW_OK if none). */
+int cw_read_reports(cw_ctx *ctx, cw_report *out, int n, int *n_out, void *stream);
+
+/* Per-stage device timings of the next cw_step call (ms per stage, keys of
+ * StepReport.timings, ref solver.py:418-454): enable before, read after. */
+int cw_set_stage_timing(cw_ctx *ctx, int enabled);
+int cw_read_stage_timings(cw_ctx *ctx, float out_ms[7]);
+
+/* region_average_speed (ref solver.py:535-549) for n boxes in one pass:
+ * mean cell-centred speed over AIR cells whose centres lie in [lo, hi];
+ * count_out[b] = 0 means "region contains no air cells". Deterministic. */
+int cw_region_speed(cw_ctx *ctx, const cw_fields *f, int n, const double *lo3n,
+                    const double *hi3n, double *mean_out, long long *count_out, void *stream);
+
+/* Voxelizer, ref grid.py:233-325 + scenario.py:327-360 (bit-exact float64).
+ * Objects in order; kind 1 building / 2 tree; shape 0 box (lo, hi), shape 1
+ * closed triangle mesh given by (verts, tris) slices of the packed arrays.
+ * Outputs device buffers: labels (int8, merged with boundary labels), phi, lad
+ * (float64).  Returns CW_ERR_GEOMETRY if a point cannot be classified. */
+typedef struct {
+  int kind, shape;
+  double phi, lad;
+  double lo[3], hi[3];
+  int vert_offset, n_verts, tri_offset, n_tris;
+} cw_object;
+
+int cw_voxelize(cw_ctx *ctx, const cw_object *objs, int n_obj, const double *verts,
+                const int *tris, int subdiv, const signed char *d_boundary_labels,
+                signed char *d_labels, double *d_phi, double *d_lad, int *n_overlap_warnings,
+                void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,679 @@
+// C ABI of the B200 RANS step path (declared in include/citywind_b200.h).
+// Host orchestration: one context per grid owns the workspace, the operator
+// code field, the device report ring and the error latch; cw_step enqueues
+// whole steps (no host synchronisation inside a step or between steps).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/citywind_b200.h"
+#include "cw_common.cuh"
+#include "cw_pcg.cuh"
+#include "cw_step.cuh"
+#include "cw_aux.cuh"
+
+using namespace cw;
+
+static thread_local std::string g_err;
+static int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+#define CW_CUDA(call)                                                                   \
+  do {                                                                                  \
+    cudaError_t e_ = (call);                                                            \
+    if (e_ != cudaSuccess)                                                              \
+      return fail(CW_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_));     \
+  } while (0)
+
+static constexpr int TX = 32, TY = 8;
+static constexpr int RING = 4096;
+
+struct cw_ctx {
+  int prec = 4;
+  int device = 0;
+  int num_sms = 148;
+  Dims d{};
+  cw_grid grid{};
+  size_t esz = 4;
+  long long ncell = 0, nu_ = 0, nv_ = 0, nw_ = 0;
+  // workspace (context precision)
+  void *tk = nullptr, *tw = nullptr, *speed = nullptr;
+  void *ahead[3] = {nullptr, nullptr, nullptr}, *adv[3] = {nullptr, nullptr, nullptr};
+  void *r0 = nullptr, *r1 = nullptr, *p0 = nullptr, *p1 = nullptr, *z = nullptr, *Ap = nullptr;
+  void *lut = nullptr, *uzx = nullptr, *uzy = nullptr;
+  uint8_t* code = nullptr;
+  double* part = nullptr;
+  unsigned* bar = nullptr;
+  int* gate = nullptr;
+  DevReport* rep = nullptr;
+  double* reg_part = nullptr;   // region partials
+  long long* reg_cnt = nullptr;
+  double* reg_out = nullptr;
+  long long* reg_cout = nullptr;
+  int* flag = nullptr;
+  // operator
+  bool have_op = false;
+  double omega = 1.65, tol_default = 0.0;
+  double tol_kind[3] = {1e-8, 0.0, 0.0};   // default_projection_tol per preconditioner kind
+  int precond = 2;
+  long long n_unknown = 0;
+  int U = 0, ntx = 0, nty = 0, zc = 1, pcg_blocks = 0;
+  // pending reports
+  int head = 0;
+  std::vector<double> slot_dt;
+  // inlet cache
+  cw_inlet inl_cache{};
+  bool inl_valid = false;
+  // stage timing
+  bool timing = false;
+  cudaEvent_t ev[8] = {};
+  bool ev_made = false;
+  float stage_ms[7] = {0, 0, 0, 0, 0, 0, 0};
+};
+
+extern "C" int cw_abi_version(void) { return CW_ABI_VERSION; }
+extern "C" const char* cw_last_error(void) { return g_err.c_str(); }
+
+static int alloc(void** p, size_t bytes) {
+  cudaError_t e = cudaMalloc(p, bytes);
+  if (e != cudaSuccess) return fail(CW_ERR_CUDA, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+  e = cudaMemset(*p, 0, bytes);
+  if (e != cudaSuccess) return fail(CW_ERR_CUDA, std::string("cudaMemset: ") + cudaGetErrorString(e));
+  return CW_OK;
+}
+
+template <typename T>
+static int pcg_occupancy(int* blocks_per_sm) {
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_pcg<T, TX, TY>, TX * TY, 0);
+  if (e != cudaSuccess) return fail(CW_ERR_CUDA, std::string("occupancy: ") + cudaGetErrorString(e));
+  return CW_OK;
+}
+
+extern "C" int cw_ctx_create(const cw_grid* g, int precision, int device, cw_ctx** out) {
+  if (!g || !out) return fail(CW_ERR_INVALID, "null argument");
+  if (precision != 4 && precision != 8) return fail(CW_ERR_INVALID, "precision must be 4 or 8");
+  if (g->nx < 1 || g->ny < 1 || g->nz < 1) return fail(CW_ERR_INVALID, "cell counts must be >= 1");
+  if (!(g->dx > 0 && g->dy > 0 && g->dz > 0)) return fail(CW_ERR_INVALID, "cell spacings must be > 0");
+  CW_CUDA(cudaSetDevice(device));
+  cw_ctx* c = new cw_ctx();
+  c->prec = precision;
+  c->esz = precision;
+  c->device = device;
+  c->grid = *g;
+  cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
+  Dims& d = c->d;
+  d.nx = g->nx; d.ny = g->ny; d.nz = g->nz;
+  d.dx = (float)g->dx; d.dy = (float)g->dy; d.dz = (float)g->dz;
+  d.ddx = g->dx; d.ddy = g->dy; d.ddz = g->dz;
+  d.is2d = g->nz == 1;
+  c->ncell = d.ncell();
+  c->nu_ = (long long)(d.nx + 1) * d.ny * d.nz;
+  c->nv_ = (long long)d.nx * (d.ny + 1) * d.nz;
+  c->nw_ = (long long)d.nx * d.ny * (d.nz + 1);
+  const size_t cb = c->ncell * c->esz;
+  size_t fb[3] = {c->nu_ * c->esz, c->nv_ * c->esz, c->nw_ * c->esz};
+  int rc = CW_OK;
+  rc |= alloc(&c->tk, cb); rc |= alloc(&c->tw, cb); rc |= alloc(&c->speed, cb);
+  for (int a = 0; a < 3; ++a) { rc |= alloc(&c->ahead[a], fb[a]); rc |= alloc(&c->adv[a], fb[a]); }
+  rc |= alloc(&c->r0, cb); rc |= alloc(&c->r1, cb); rc |= alloc(&c->p0, cb);
+  rc |= alloc(&c->p1, cb); rc |= alloc(&c->z, cb); rc |= alloc(&c->Ap, cb);
+  rc |= alloc(&c->lut, 64 * 4 * c->esz);
+  rc |= alloc(&c->uzx, d.nz * c->esz); rc |= alloc(&c->uzy, d.nz * c->esz);
+  rc |= alloc((void**)&c->code, c->ncell);
+  rc |= alloc((void**)&c->bar, 64 * sizeof(unsigned));
+  rc |= alloc((void**)&c->gate, sizeof(int));
+  rc |= alloc((void**)&c->flag, 4 * sizeof(int));
+  rc |= alloc((void**)&c->rep, RING * sizeof(DevReport));
+  if (rc != CW_OK) { cw_ctx_destroy(c); return CW_ERR_CUDA; }
+  // PCG work decomposition: tiles TX x TY over (x, y), z-chunks of zc planes;
+  // each co-resident block owns at most one unit when the grid allows it.
+  int per_sm = 0;
+  rc = precision == 4 ? pcg_occupancy<float>(&per_sm) : pcg_occupancy<double>(&per_sm);
+  if (rc != CW_OK || per_sm < 1) { cw_ctx_destroy(c); return rc != CW_OK ? rc : fail(CW_ERR_CUDA, "pcg kernel cannot be resident"); }
+  const int maxb = per_sm * c->num_sms;
+  c->ntx = (d.nx + TX - 1) / TX;
+  c->nty = (d.ny + TY - 1) / TY;
+  const int tiles = c->ntx * c->nty;
+  int zc = std::max(4, (d.nz * tiles + maxb - 1) / maxb);
+  zc = std::min(zc, d.nz);
+  c->zc = zc;
+  c->U = tiles * ((d.nz + zc - 1) / zc);
+  c->pcg_blocks = std::min(c->U, maxb);
+  rc = alloc((void**)&c->part, 6 * (size_t)c->U * sizeof(double));
+  rc |= alloc((void**)&c->reg_part, (size_t)1024 * 64 * sizeof(double));
+  rc |= alloc((void**)&c->reg_cnt, (size_t)1024 * 64 * sizeof(long long));
+  rc |= alloc((void**)&c->reg_out, 64 * sizeof(double));
+  rc |= alloc((void**)&c->reg_cout, 64 * sizeof(long long));
+  if (rc != CW_OK) { cw_ctx_destroy(c); return CW_ERR_CUDA; }
+  c->slot_dt.assign(RING, 0.0);
+  *out = c;
+  return CW_OK;
+}
+
+extern "C" void cw_ctx_destroy(cw_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  void* ptrs[] = {c->tk, c->tw, c->speed, c->ahead[0], c->ahead[1], c->ahead[2], c->adv[0], c->adv[1],
+                  c->adv[2], c->r0, c->r1, c->p0, c->p1, c->z, c->Ap, c->lut, c->uzx, c->uzy, c->code,
+                  c->part, c->bar, c->gate, c->rep, c->reg_part, c->reg_cnt, c->reg_out, c->reg_cout,
+                  c->flag};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  if (c->ev_made)
+    for (auto& e : c->ev) cudaEventDestroy(e);
+  delete c;
+}
+
+static inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+static inline int nblk(long long n, int bs = 256) {
+  long long b = (n + bs - 1) / bs;
+  return (int)std::max<long long>(1, std::min<long long>(b, 148LL * 32));
+}
+
+// ---------------------------------------------------------------------------
+// operator setup
+
+extern "C" int cw_set_operator(cw_ctx* c, const signed char* lab, double ai_omega, long long* n_unknown,
+                               double* tol_default, void* stream) {
+  if (!c || !lab) return fail(CW_ERR_INVALID, "null argument");
+  if (!(ai_omega > 0.0 && ai_omega < 2.0)) return fail(CW_ERR_INVALID, "omega must lie in (0, 2)");
+  CW_CUDA(cudaSetDevice(c->device));
+  const Dims& d = c->d;
+  const double w[3] = {1.0 / (c->grid.dx * c->grid.dx), 1.0 / (c->grid.dy * c->grid.dy),
+                       1.0 / (c->grid.dz * c->grid.dz)};
+  // LUT: d, 1/d, s=(2-omega)*omega/d for each neighbour-bit pattern.
+  // Neighbour order +x,-x,+y,-y,+z,-z (ref linalg.py:20 offsets order).
+  std::vector<double> lut(64 * 4, 0.0);
+  for (int b = 1; b < 64; ++b) {
+    double dd = 0.0;
+    for (int q = 0; q < 6; ++q)
+      if (b & (1 << q)) dd += w[q / 2];
+    lut[b * 4 + 0] = dd;
+    lut[b * 4 + 1] = 1.0 / dd;
+    lut[b * 4 + 2] = (2.0 - ai_omega) * ai_omega / dd;
+  }
+  if (c->prec == 4) {
+    std::vector<float> lf(lut.begin(), lut.end());
+    CW_CUDA(cudaMemcpyAsync(c->lut, lf.data(), lf.size() * 4, cudaMemcpyHostToDevice, S(stream)));
+  } else {
+    CW_CUDA(cudaMemcpyAsync(c->lut, lut.data(), lut.size() * 8, cudaMemcpyHostToDevice, S(stream)));
+  }
+  CW_CUDA(cudaMemsetAsync(c->flag, 0, 4 * sizeof(int), S(stream)));
+  const int nb = std::min(nblk(c->ncell), 1024);
+  k_build_code<<<nb, 256, 0, S(stream)>>>(d, (const int8_t*)lab, c->code, c->flag);
+  CW_CUDA(cudaGetLastError());
+  k_wdiag_partials<<<nb, 256, 0, S(stream)>>>(d, c->code, w[0], w[1], w[2], ai_omega, c->reg_part, c->reg_cnt,
+                                               c->reg_part + 1024);
+  CW_CUDA(cudaGetLastError());
+  std::vector<double> parts(nb), jparts(nb);
+  std::vector<long long> cnts(nb);
+  int flags[4];
+  CW_CUDA(cudaMemcpyAsync(parts.data(), c->reg_part, nb * sizeof(double), cudaMemcpyDeviceToHost, S(stream)));
+  CW_CUDA(cudaMemcpyAsync(jparts.data(), c->reg_part + 1024, nb * sizeof(double), cudaMemcpyDeviceToHost, S(stream)));
+  CW_CUDA(cudaMemcpyAsync(cnts.data(), c->reg_cnt, nb * sizeof(long long), cudaMemcpyDeviceToHost, S(stream)));
+  CW_CUDA(cudaMemcpyAsync(flags, c->flag, sizeof(flags), cudaMemcpyDeviceToHost, S(stream)));
+  CW_CUDA(cudaStreamSynchronize(S(stream)));
+  double sum = 0.0, jsum = 0.0;
+  long long n = 0;
+  for (int b = 0; b < nb; ++b) { sum += parts[b]; jsum += jparts[b]; n += cnts[b]; }
+  if (n == 0) return fail(CW_ERR_INVALID, "no flow cells to solve for");
+  if (flags[0] == 0) return fail(CW_ERR_SINGULAR, "no outlet cells: pressure defined only up to a constant");
+  if (flags[1] != 0) return fail(CW_ERR_INVALID, "AI preconditioner requires a positive diagonal");
+  c->omega = ai_omega;
+  c->n_unknown = n;
+  const double mean = sum / (double)n;
+  c->tol_kind[0] = 1e-8;                                           // no W: mscale 1
+  c->tol_kind[1] = 1e-8 * std::max(jsum / (double)n, 1e-300);      // Jacobi W = diag(1/d)
+  c->tol_kind[2] = 1e-8 * std::max(mean, 1e-300);                  // AI1
+  c->tol_default = c->tol_kind[c->precond];
+  c->have_op = true;
+  if (n_unknown) *n_unknown = n;
+  if (tol_default) *tol_default = c->tol_default;
+  return CW_OK;
+}
+
+// ---------------------------------------------------------------------------
+// drag coefficient
+
+extern "C" int cw_drag_coefficient(cw_ctx* c, const double* phi, const double* lad, const signed char* lab,
+                                   const cw_params* prm, void* g, int* has_drag, void* stream) {
+  if (!c || !phi || !lad || !lab || !prm || !g) return fail(CW_ERR_INVALID, "null argument");
+  CW_CUDA(cudaSetDevice(c->device));
+  CW_CUDA(cudaMemsetAsync(c->flag, 0, sizeof(int), S(stream)));
+  if (c->prec == 4)
+    k_drag_coef<float><<<nblk(c->ncell), 256, 0, S(stream)>>>(c->ncell, phi, lad, (const int8_t*)lab, *prm, (float*)g, c->flag);
+  else
+    k_drag_coef<double><<<nblk(c->ncell), 256, 0, S(stream)>>>(c->ncell, phi, lad, (const int8_t*)lab, *prm, (double*)g, c->flag);
+  CW_CUDA(cudaGetLastError());
+  int f = 0;
+  CW_CUDA(cudaMemcpyAsync(&f, c->flag, sizeof(int), cudaMemcpyDeviceToHost, S(stream)));
+  CW_CUDA(cudaStreamSynchronize(S(stream)));
+  if (has_drag) *has_drag = f != 0;
+  return CW_OK;
+}
+
+// ---------------------------------------------------------------------------
+// boundary conditions
+
+static int upload_inlet(cw_ctx* c, const cw_inlet* inl, cudaStream_t st) {
+  if (c->inl_valid && std::memcmp(&c->inl_cache, inl, sizeof(cw_inlet)) == 0) return CW_OK;
+  const int nz = c->d.nz;
+  std::vector<double> ux(nz), uy(nz);
+  for (int k = 0; k < nz; ++k) {
+    const double zc = c->grid.origin[2] + ((double)k + 0.5) * c->grid.dz;   // solver.py:384
+    double s;
+    if (inl->kind == 0) s = inl->speed;
+    else s = zc > inl->z0 ? inl->u_star / inl->kappa * std::log(zc / inl->z0) : 0.0;   // solver.py:75-82
+    ux[k] = s * inl->dir_x;
+    uy[k] = s * inl->dir_y;
+  }
+  if (c->prec == 4) {
+    std::vector<float> fx(ux.begin(), ux.end()), fy(uy.begin(), uy.end());
+    CW_CUDA(cudaMemcpyAsync(c->uzx, fx.data(), nz * 4, cudaMemcpyHostToDevice, st));
+    CW_CUDA(cudaMemcpyAsync(c->uzy, fy.data(), nz * 4, cudaMemcpyHostToDevice, st));
+    CW_CUDA(cudaStreamSynchronize(st));   // host vectors go out of scope
+  } else {
+    CW_CUDA(cudaMemcpyAsync(c->uzx, ux.data(), nz * 8, cudaMemcpyHostToDevice, st));
+    CW_CUDA(cudaMemcpyAsync(c->uzy, uy.data(), nz * 8, cudaMemcpyHostToDevice, st));
+    CW_CUDA(cudaStreamSynchronize(st));
+  }
+  c->inl_cache = *inl;
+  c->inl_valid = true;
+  return CW_OK;
+}
+
+template <typename T>
+static void launch_bc(cw_ctx* c, BcFields<T> F, const int8_t* lab, const cw_params* prm, cudaStream_t st) {
+  const Dims& d = c->d;
+  const int sides = d.is2d ? 4 : 6;
+  for (int s = 0; s < sides; ++s) {
+    const int axis = s / 2;
+    const int ext = axis == 0 ? d.nx : (axis == 1 ? d.ny : d.nz);
+    const int pos = (s & 1) ? ext - 1 : 0;
+    const int e1 = axis == 0 ? d.ny : d.nx, e2 = axis == 2 ? d.ny : d.nz;
+    k_bc_outlet_side<T><<<nblk((long long)(e1 + 1) * (e2 + 1)), 256, 0, st>>>(d, axis, pos, F, lab, c->gate);
+  }
+  const long long n = c->ncell + c->nu_ + c->nv_ + (d.is2d ? 0 : c->nw_);
+  k_bc_inlet_wall<T><<<nblk(n), 256, 0, st>>>(d, F, lab, (const T*)c->uzx, (const T*)c->uzy, (T)prm->k_in,
+                                              (T)prm->omega_in, (T)(prm->k_in / prm->omega_in), c->gate);
+}
+
+extern "C" int cw_apply_boundary(cw_ctx* c, const cw_fields* f, const cw_params* prm, const cw_inlet* inl,
+                                 void* stream) {
+  if (!c || !f || !prm || !inl) return fail(CW_ERR_INVALID, "null argument");
+  CW_CUDA(cudaSetDevice(c->device));
+  int rc = upload_inlet(c, inl, S(stream));
+  if (rc) return rc;
+  if (c->prec == 4) {
+    BcFields<float> F{(float*)f->u, (float*)f->v, (float*)f->w, (float*)f->p, (float*)f->k, (float*)f->omega, (float*)f->nu_t};
+    launch_bc<float>(c, F, (const int8_t*)f->labels, prm, S(stream));
+  } else {
+    BcFields<double> F{(double*)f->u, (double*)f->v, (double*)f->w, (double*)f->p, (double*)f->k, (double*)f->omega, (double*)f->nu_t};
+    launch_bc<double>(c, F, (const int8_t*)f->labels, prm, S(stream));
+  }
+  CW_CUDA(cudaGetLastError());
+  return CW_OK;
+}
+
+// ---------------------------------------------------------------------------
+// the step
+
+template <typename T>
+static int launch_pcg(cw_ctx* c, const cw_fields* f, DevReport* rep, double dt, double tol, cudaStream_t st) {
+  PcgArgs<T> A;
+  A.d = c->d;
+  A.code = c->code;
+  A.x = (T*)f->p;
+  A.u = (const T*)f->u; A.v = (const T*)f->v; A.w = (const T*)f->w;
+  A.r0 = (T*)c->r0; A.r1 = (T*)c->r1; A.p0 = (T*)c->p0; A.p1 = (T*)c->p1; A.z = (T*)c->z; A.Ap = (T*)c->Ap;
+  A.part = c->part;
+  A.bar = c->bar;
+  A.gate = c->gate;
+  A.rep = rep;
+  A.lut = (const T*)c->lut;
+  A.wx = (T)(1.0 / (c->grid.dx * c->grid.dx));
+  A.wy = (T)(1.0 / (c->grid.dy * c->grid.dy));
+  A.wz = c->d.is2d ? (T)0 : (T)(1.0 / (c->grid.dz * c->grid.dz));
+  A.om = (T)c->omega;
+  A.dt = dt;
+  A.tol = tol;
+  A.res_factor = std::pow(10.0, -4.5);   // DIV_REDUCTION_TARGET, solver.py:232
+  A.max_iter = 10000;                    // project(max_iter=10_000), solver.py:249
+  A.precond = c->precond;
+  A.ntx = c->ntx; A.nty = c->nty; A.zc = c->zc; A.U = c->U;
+  A.timeout_ns = 20LL * 1000 * 1000 * 1000;
+  CW_CUDA(cudaMemsetAsync(c->bar, 0, 64 * sizeof(unsigned), st));
+  void* args[] = {&A};
+  CW_CUDA(cudaLaunchCooperativeKernel((const void*)k_pcg<T, TX, TY>, dim3(c->pcg_blocks), dim3(TX * TY), args, 0, st));
+  return CW_OK;
+}
+
+// stage building blocks ------------------------------------------------------
+template <typename T>
+struct StepPtrs {
+  T *u, *v, *w, *p, *k, *om, *nut;
+  const int8_t* lab;
+  const T* g;
+};
+
+template <typename T>
+static double nu_stable(const cw_ctx* c, double dt) {   // turbulence.py:18-23
+  double s = 1.0 / (c->grid.dx * c->grid.dx) + 1.0 / (c->grid.dy * c->grid.dy);
+  if (!c->d.is2d) s += 1.0 / (c->grid.dz * c->grid.dz);
+  return 1.0 / (2.0 * dt * s);
+}
+
+// upwind k/omega into (kout, wout); MacCormack u, v, w into the adv buffers
+template <typename T>
+static void st_advect(cw_ctx* c, const StepPtrs<T>& P, const cw_params* prm, T* kout, T* wout, cudaStream_t st) {
+  const Dims& d = c->d;
+  const T dt = (T)prm->dt;
+  const long long nf[3] = {c->nu_, c->nv_, c->nw_};
+  const int ncomp = d.is2d ? 2 : 3;
+  if (prm->turbulence)
+    k_upwind<T><<<nblk(c->ncell), 256, 0, st>>>(d, P.u, P.v, P.w, P.k, P.om, kout, wout, dt, c->gate);
+  for (int a = 0; a < ncomp; ++a)
+    k_mac_predict<T><<<nblk(nf[a]), 256, 0, st>>>(d, a, P.u, P.v, P.w, (T*)c->ahead[a], dt, c->gate);
+  for (int a = 0; a < ncomp; ++a)
+    k_mac_correct<T><<<nblk(nf[a]), 256, 0, st>>>(d, a, P.u, P.v, P.w, (const T*)c->ahead[a], (T*)c->adv[a], dt, c->gate);
+}
+
+template <typename T>
+static void st_diffuse(cw_ctx* c, const StepPtrs<T>& P, const cw_params* prm, cudaStream_t st) {
+  const Dims& d = c->d;
+  const long long nf[3] = {c->nu_, c->nv_, c->nw_};
+  T* cu[3] = {P.u, P.v, P.w};
+  double cap = nu_stable<T>(c, prm->dt) - prm->nu;
+  if (cap <= 0) cap = 0.0;                               // solver.py:195-201
+  for (int a = 0; a < (d.is2d ? 2 : 3); ++a)
+    k_diffuse<T><<<nblk(nf[a]), 256, 0, st>>>(d, a, (const T*)c->adv[a], cu[a], P.nut, (T)prm->dt,
+                                               (T)prm->nu, (T)cap, c->gate);
+}
+
+template <typename T>
+static void st_drag(cw_ctx* c, const StepPtrs<T>& P, const cw_params* prm, int has_drag, cudaStream_t st) {
+  if (!has_drag) return;                                 // solver.py:157-158
+  const Dims& d = c->d;
+  const long long nf[3] = {c->nu_, c->nv_, c->nw_};
+  T* cu[3] = {P.u, P.v, P.w};
+  k_cell_speed<T><<<nblk(c->ncell), 256, 0, st>>>(d, P.u, P.v, P.w, (T*)c->speed, c->gate);
+  for (int a = 0; a < (d.is2d ? 2 : 3); ++a)
+    k_drag<T><<<nblk(nf[a]), 256, 0, st>>>(d, a, cu[a], P.g, (const T*)c->speed, (T)prm->dt, c->gate);
+}
+
+template <typename T>
+static int st_project(cw_ctx* c, const StepPtrs<T>& P, const cw_fields* f, const cw_params* prm, double tol,
+                      DevReport* rep, cudaStream_t st) {
+  const Dims& d = c->d;
+  const long long nf[3] = {c->nu_, c->nv_, c->nw_};
+  T* cu[3] = {P.u, P.v, P.w};
+  int rc = launch_pcg<T>(c, f, rep, prm->dt, tol, st);
+  if (rc) return rc;
+  for (int a = 0; a < (d.is2d ? 2 : 3); ++a)
+    k_gradient<T><<<nblk(nf[a]), 256, 0, st>>>(d, a, cu[a], P.p, P.lab, (T)prm->dt, c->gate);
+  k_div_max<T><<<nblk(c->ncell), 256, 0, st>>>(d, P.u, P.v, P.w, P.lab, rep, SLOT_DIV_AFTER, c->gate);
+  return CW_OK;
+}
+
+template <typename T>
+static void st_turb(cw_ctx* c, const StepPtrs<T>& P, const cw_params* prm, const T* kin, const T* win,
+                    DevReport* rep, cudaStream_t st) {
+  StepConsts sc;
+  const double nus = nu_stable<T>(c, prm->dt);
+  sc.dt = prm->dt; sc.nu = prm->nu; sc.cap_diffuse = 0.0;
+  sc.cap_turb = std::max(nus - prm->nu, 0.0);            // turbulence.py:110
+  sc.c_mu = prm->c_mu; sc.alpha = prm->alpha; sc.beta = prm->beta;
+  sc.sigma = prm->sigma; sc.sigma_star = prm->sigma_star; sc.c_lim = prm->c_lim;
+  sc.k_in = prm->k_in; sc.om_in = prm->omega_in; sc.nut_in = prm->k_in / prm->omega_in;
+  k_turbulence<T><<<nblk(c->ncell), 256, 0, st>>>(c->d, P.u, P.v, P.w, kin, win, P.k, P.om, P.nut, sc, rep, c->gate);
+  k_turb_check<<<1, 1, 0, st>>>(rep, c->gate);
+}
+
+template <typename T>
+static StepPtrs<T> ptrs_of(const cw_fields* f) {
+  StepPtrs<T> P;
+  P.u = (T*)f->u; P.v = (T*)f->v; P.w = (T*)f->w; P.p = (T*)f->p;
+  P.k = (T*)f->k; P.om = (T*)f->omega; P.nut = (T*)f->nu_t;
+  P.lab = (const int8_t*)f->labels; P.g = (const T*)f->g;
+  return P;
+}
+
+// one full step (solver.py:407-461): no copies, stage temporaries chained
+template <typename T>
+static int enqueue_step(cw_ctx* c, const cw_fields* f, const cw_params* prm, double tol, int slot, cudaStream_t st) {
+  DevReport* rep = c->rep + slot;
+  const StepPtrs<T> P = ptrs_of<T>(f);
+  const bool turb = prm->turbulence != 0;
+  auto mark = [&](int i) { if (c->timing) cudaEventRecord(c->ev[i], st); };
+  k_report_init<<<1, 1, 0, st>>>(rep);
+  mark(0);
+  st_advect<T>(c, P, prm, (T*)c->tk, (T*)c->tw, st);        // "advect"
+  mark(1);
+  st_diffuse<T>(c, P, prm, st);                               // "diffuse"
+  mark(2);
+  st_drag<T>(c, P, prm, f->has_drag, st);                     // "drag"
+  mark(3);
+  StepPtrs<T> B = P;                                          // k, omega after upwind live in tk, tw
+  if (turb) { B.k = (T*)c->tk; B.om = (T*)c->tw; }
+  BcFields<T> F1{B.u, B.v, B.w, B.p, B.k, B.om, B.nut};
+  launch_bc<T>(c, F1, P.lab, prm, st);                        // "boundary"
+  mark(4);
+  int rc = st_project<T>(c, P, f, prm, tol, rep, st);         // "project"
+  if (rc) return rc;
+  mark(5);
+  if (turb) st_turb<T>(c, P, prm, B.k, B.om, rep, st);        // "turbulence"
+  mark(6);
+  BcFields<T> F2{P.u, P.v, P.w, P.p, P.k, P.om, P.nut};
+  launch_bc<T>(c, F2, P.lab, prm, st);                        // "boundary2"
+  k_speed_max<T><<<nblk(c->nu_ + c->nv_ + c->nw_), 256, 0, st>>>(c->nu_, c->nv_, c->nw_, P.u, P.v, P.w, rep, c->gate);
+  mark(7);
+  CW_CUDA(cudaGetLastError());
+  return CW_OK;
+}
+
+// a single reference stage function on a state (tests / stage-level API)
+template <typename T>
+static int enqueue_stage(cw_ctx* c, const cw_fields* f, const cw_params* prm, int stage, double tol, int slot,
+                         cudaStream_t st) {
+  DevReport* rep = c->rep + slot;
+  const StepPtrs<T> P = ptrs_of<T>(f);
+  const Dims& d = c->d;
+  const size_t cb = c->ncell * sizeof(T);
+  const size_t fb[3] = {c->nu_ * sizeof(T), c->nv_ * sizeof(T), c->nw_ * sizeof(T)};
+  T* cu[3] = {P.u, P.v, P.w};
+  const int ncomp = d.is2d ? 2 : 3;
+  k_report_init<<<1, 1, 0, st>>>(rep);
+  switch (stage) {
+    case CW_STAGE_ADVECT:
+      st_advect<T>(c, P, prm, (T*)c->tk, (T*)c->tw, st);
+      if (prm->turbulence) {
+        CW_CUDA(cudaMemcpyAsync(P.k, c->tk, cb, cudaMemcpyDeviceToDevice, st));
+        CW_CUDA(cudaMemcpyAsync(P.om, c->tw, cb, cudaMemcpyDeviceToDevice, st));
+      }
+      for (int a = 0; a < ncomp; ++a) CW_CUDA(cudaMemcpyAsync(cu[a], c->adv[a], fb[a], cudaMemcpyDeviceToDevice, st));
+      break;
+    case CW_STAGE_DIFFUSE:
+      for (int a = 0; a < ncomp; ++a) CW_CUDA(cudaMemcpyAsync(c->adv[a], cu[a], fb[a], cudaMemcpyDeviceToDevice, st));
+      st_diffuse<T>(c, P, prm, st);
+      break;
+    case CW_STAGE_DRAG:
+      st_drag<T>(c, P, prm, f->has_drag, st);
+      break;
+    case CW_STAGE_BOUNDARY: {
+      BcFields<T> F{P.u, P.v, P.w, P.p, P.k, P.om, P.nut};
+      launch_bc<T>(c, F, P.lab, prm, st);
+      break;
+    }
+    case CW_STAGE_PROJECT: {
+      if (!c->have_op) return fail(CW_ERR_INVALID, "cw_set_operator has not been called");
+      int rc = st_project<T>(c, P, f, prm, tol, rep, st);
+      if (rc) return rc;
+      break;
+    }
+    case CW_STAGE_TURBULENCE:
+      CW_CUDA(cudaMemcpyAsync(c->tk, P.k, cb, cudaMemcpyDeviceToDevice, st));
+      CW_CUDA(cudaMemcpyAsync(c->tw, P.om, cb, cudaMemcpyDeviceToDevice, st));
+      st_turb<T>(c, P, prm, (const T*)c->tk, (const T*)c->tw, rep, st);
+      break;
+    default:
+      return fail(CW_ERR_INVALID, "unknown stage");
+  }
+  CW_CUDA(cudaGetLastError());
+  return CW_OK;
+}
+
+extern "C" int cw_run_stage(cw_ctx* c, const cw_fields* f, const cw_params* prm, const cw_inlet* inl, int stage,
+                            double pcg_tol, void* stream) {
+  if (!c || !f || !prm || !inl) return fail(CW_ERR_INVALID, "null argument");
+  if (c->head + 1 > RING) return fail(CW_ERR_INVALID, "report ring full: call cw_read_reports");
+  if (stage == CW_STAGE_DRAG && f->has_drag && !f->g) return fail(CW_ERR_INVALID, "has_drag without g");
+  CW_CUDA(cudaSetDevice(c->device));
+  int rc = upload_inlet(c, inl, S(stream));
+  if (rc) return rc;
+  const double tol = pcg_tol < 0 || std::isnan(pcg_tol) ? c->tol_default : pcg_tol;
+  const int slot = c->head++;
+  c->slot_dt[slot] = prm->dt;
+  return c->prec == 4 ? enqueue_stage<float>(c, f, prm, stage, tol, slot, S(stream))
+                      : enqueue_stage<double>(c, f, prm, stage, tol, slot, S(stream));
+}
+
+extern "C" int cw_step(cw_ctx* c, const cw_fields* f, const cw_params* prm, const cw_inlet* inl, double pcg_tol,
+                       int nsteps, void* stream) {
+  if (!c || !f || !prm || !inl) return fail(CW_ERR_INVALID, "null argument");
+  if (!c->have_op) return fail(CW_ERR_INVALID, "cw_set_operator has not been called");
+  if (nsteps < 0) return fail(CW_ERR_INVALID, "nsteps < 0");
+  if (c->head + nsteps > RING) return fail(CW_ERR_INVALID, "report ring full: call cw_read_reports");
+  if (f->has_drag && !f->g) return fail(CW_ERR_INVALID, "has_drag without a drag-coefficient buffer");
+  CW_CUDA(cudaSetDevice(c->device));
+  int rc = upload_inlet(c, inl, S(stream));
+  if (rc) return rc;
+  if (c->timing && !c->ev_made) {
+    for (auto& e : c->ev) CW_CUDA(cudaEventCreate(&e));
+    c->ev_made = true;
+  }
+  const double tol = pcg_tol < 0 || std::isnan(pcg_tol) ? c->tol_default : pcg_tol;
+  for (int s = 0; s < nsteps; ++s) {
+    const int slot = c->head++;
+    c->slot_dt[slot] = prm->dt;
+    rc = c->prec == 4 ? enqueue_step<float>(c, f, prm, tol, slot, S(stream))
+                      : enqueue_step<double>(c, f, prm, tol, slot, S(stream));
+    if (rc) return rc;
+  }
+  return CW_OK;
+}
+
+extern "C" int cw_read_reports(cw_ctx* c, cw_report* out, int n, int* n_out, void* stream) {
+  if (!c) return fail(CW_ERR_INVALID, "null argument");
+  CW_CUDA(cudaSetDevice(c->device));
+  CW_CUDA(cudaStreamSynchronize(S(stream)));
+  const int m = std::min(n, c->head);
+  std::vector<DevReport> dr(std::max(c->head, 1));
+  if (c->head > 0)
+    CW_CUDA(cudaMemcpy(dr.data(), c->rep, c->head * sizeof(DevReport), cudaMemcpyDeviceToHost));
+  if (c->timing && c->ev_made && c->head > 0) {
+    for (int i = 0; i < 7; ++i) cudaEventElapsedTime(&c->stage_ms[i], c->ev[i], c->ev[i + 1]);
+  }
+  const double hmin = std::min(c->grid.dx, std::min(c->grid.dy, c->grid.dz));
+  int first_err = CW_OK;
+  for (int i = 0; i < c->head; ++i) {
+    const DevReport& r = dr[i];
+    cw_report o{};
+    o.iterations = r.iterations;
+    o.converged = r.converged;
+    o.criterion = r.criterion;
+    double smax, db, da;
+    if (c->prec == 4) {
+      float t;
+      std::memcpy(&t, &r.fmax[SLOT_SPEED], 4); smax = t;
+      std::memcpy(&t, &r.fmax[SLOT_DIV_BEFORE], 4); db = t;
+      std::memcpy(&t, &r.fmax[SLOT_DIV_AFTER], 4); da = t;
+    } else {
+      std::memcpy(&smax, &r.dmax[SLOT_SPEED], 8);
+      std::memcpy(&db, &r.dmax[SLOT_DIV_BEFORE], 8);
+      std::memcpy(&da, &r.dmax[SLOT_DIV_AFTER], 8);
+    }
+    o.cfl = std::max(smax, 1e-300) * c->slot_dt[i] / hmin;
+    o.div_before = db;
+    o.div_after = da;
+    o.bad_cell = -1;
+    switch (r.status) {
+      case 0: o.status = CW_OK; break;
+      case 1: o.status = CW_ERR_PCG; break;
+      case 2:
+        o.status = CW_ERR_NONFINITE;
+        o.bad_field = r.bad_index[0] != 0x7fffffffffffffffLL ? 0 : 1;
+        o.bad_cell = r.bad_index[o.bad_field];
+        break;
+      case 3: o.status = CW_ERR_TIMEOUT; break;
+      case 4: o.status = CW_ERR_RHS; break;
+      default: o.status = CW_ERR_CUDA; break;
+    }
+    if (o.status != CW_OK && first_err == CW_OK) first_err = o.status;
+    if (i < m && out) out[i] = o;
+  }
+  if (n_out) *n_out = m;
+  c->head = 0;
+  CW_CUDA(cudaMemset(c->gate, 0, sizeof(int)));
+  CW_CUDA(cudaMemset(c->bar, 0, 64 * sizeof(unsigned)));
+  if (first_err != CW_OK) {
+    const char* what = first_err == CW_ERR_PCG ? "pressure solve did not converge"
+                       : first_err == CW_ERR_NONFINITE ? "turbulence update produced non-finite values"
+                       : first_err == CW_ERR_RHS ? "right-hand side contains non-finite entries"
+                       : first_err == CW_ERR_TIMEOUT ? "device grid barrier timed out"
+                                                     : "device error";
+    g_err = what;
+  }
+  return first_err;
+}
+
+extern "C" int cw_set_preconditioner(cw_ctx* c, int kind, double* tol_default) {
+  if (!c || kind < 0 || kind > 2) return fail(CW_ERR_INVALID, "preconditioner kind must be 0, 1 or 2");
+  c->precond = kind;
+  c->tol_default = c->tol_kind[kind];
+  if (tol_default) *tol_default = c->tol_default;
+  return CW_OK;
+}
+
+extern "C" int cw_set_stage_timing(cw_ctx* c, int enabled) {
+  if (!c) return fail(CW_ERR_INVALID, "null argument");
+  c->timing = enabled != 0;
+  return CW_OK;
+}
+
+extern "C" int cw_read_stage_timings(cw_ctx* c, float out_ms[7]) {
+  if (!c || !out_ms) return fail(CW_ERR_INVALID, "null argument");
+  for (int i = 0; i < 7; ++i) out_ms[i] = c->stage_ms[i];
+  return CW_OK;
+}
+
+// ---------------------------------------------------------------------------
+// region averages
+
+extern "C" int cw_region_speed(cw_ctx* c, const cw_fields* f, int n, const double* lo, const double* hi,
+                               double* mean_out, long long* count_out, void* stream) {
+  if (!c || !f || n < 1 || n > 16 || !lo || !hi) return fail(CW_ERR_INVALID, "bad region arguments (1..16 boxes)");
+  CW_CUDA(cudaSetDevice(c->device));
+  RegionBoxes B;
+  B.n = n;
+  for (int b = 0; b < n; ++b)
+    for (int a = 0; a < 3; ++a) { B.lo[b][a] = lo[3 * b + a]; B.hi[b][a] = hi[3 * b + a]; }
+  const int nb = std::min(nblk(c->ncell), 1024);
+  if (c->prec == 4)
+    k_region_partials<float><<<nb, 256, 0, S(stream)>>>(c->d, c->grid.origin[0], c->grid.origin[1], c->grid.origin[2],
+        (const float*)f->u, (const float*)f->v, (const float*)f->w, (const int8_t*)f->labels, B, c->reg_part, c->reg_cnt);
+  else
+    k_region_partials<double><<<nb, 256, 0, S(stream)>>>(c->d, c->grid.origin[0], c->grid.origin[1], c->grid.origin[2],
+        (const double*)f->u, (const double*)f->v, (const double*)f->w, (const int8_t*)f->labels, B, c->reg_part, c->reg_cnt);
+  k_region_fold<<<1, 64, 0, S(stream)>>>(nb, n, c->reg_part, c->reg_cnt, c->reg_out, c->reg_cout);
+  CW_CUDA(cudaGetLastError());
+  CW_CUDA(cudaMemcpyAsync(mean_out, c->reg_out, n * sizeof(double), cudaMemcpyDeviceToHost, S(stream)));
+  CW_CUDA(cudaMemcpyAsync(count_out, c->reg_cout, n * sizeof(long long), cudaMemcpyDeviceToHost, S(stream)));
+  CW_CUDA(cudaStreamSynchronize(S(stream)));
+  return CW_OK;
+}

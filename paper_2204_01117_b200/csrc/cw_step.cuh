@@ -1,0 +1,515 @@
+// Per-stage kernels of one RANS step (everything except the pressure solve).
+// Each kernel restates one reference stage on the x-fastest device layout;
+// the reference file:line each one follows is given at the kernel.
+#pragma once
+#include "cw_common.cuh"
+
+namespace cw {
+
+struct StepConsts {
+  double dt, nu, cap_diffuse, cap_turb;   // cap_diffuse: solver.py:195-201; cap_turb: turbulence.py:110
+  double c_mu, alpha, beta, sigma, sigma_star, c_lim;
+  double k_in, om_in, nut_in;             // inlet turbulence (turbulence.py:26-33)
+};
+
+// Per-step device report (one slot per step in a batch).
+struct DevReport {
+  int iterations;
+  int converged;
+  int status;            // 0 ok, 1 pcg not converged, 2 non-finite turbulence, 3 barrier timeout, 4 non-finite rhs
+  int pad;
+  double criterion;
+  unsigned int fmax[4];  // float max slots: 0 div_before, 1 div_after, 2 max|vel| (bit patterns)
+  unsigned long long dmax[4];
+  long long bad_index[2];  // first non-finite k / omega cell, reference C order (i*ny+j)*nz+k
+};
+
+enum MaxSlot { SLOT_DIV_BEFORE = 0, SLOT_DIV_AFTER = 1, SLOT_SPEED = 2 };
+
+template <typename T> __device__ __forceinline__ void report_max(DevReport* r, int slot, T v);
+template <> __device__ __forceinline__ void report_max<float>(DevReport* r, int slot, float v) {
+  atomicMax(&r->fmax[slot], __float_as_uint(v));
+}
+template <> __device__ __forceinline__ void report_max<double>(DevReport* r, int slot, double v) {
+  atomicMax(&r->dmax[slot], (unsigned long long)__double_as_longlong(v));
+}
+
+#define CW_GRID_STRIDE(idx, n) \
+  for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < (n); \
+       idx += (long long)gridDim.x * blockDim.x)
+
+__device__ __forceinline__ int clampi(int a, int lo, int hi) { return a < lo ? lo : (a > hi ? hi : a); }
+
+// ---------------------------------------------------------------------------
+// upwind k and omega (advection.py:154-173), old velocity, axes x,y,z in turn
+template <typename T>
+__global__ void k_upwind(Dims d, const T* __restrict__ u, const T* __restrict__ v,
+                         const T* __restrict__ w, const T* __restrict__ kin,
+                         const T* __restrict__ win, T* __restrict__ kout, T* __restrict__ wout,
+                         T dt, const int* gate) {
+  if (*gate) return;
+  const long long n = d.ncell();
+  CW_GRID_STRIDE(c, n) {
+    const int i = (int)(c % d.nx), j = (int)((c / d.nx) % d.ny), k = (int)(c / ((long long)d.nx * d.ny));
+    T a[3];
+    a[0] = (T)0.5 * (u[((long long)k * d.ny + j) * (d.nx + 1) + i] + u[((long long)k * d.ny + j) * (d.nx + 1) + i + 1]);
+    a[1] = (T)0.5 * (v[((long long)k * (d.ny + 1) + j) * d.nx + i] + v[((long long)k * (d.ny + 1) + j + 1) * d.nx + i]);
+    a[2] = (T)0.5 * (w[c] + w[c + (long long)d.nx * d.ny]);
+    const int pos[3] = {i, j, k};
+    const int ext[3] = {d.nx, d.ny, d.nz};
+    const long long str[3] = {1, d.nx, (long long)d.nx * d.ny};
+    const T h[3] = {(T)d.dx, (T)d.dy, (T)d.dz};
+#pragma unroll
+    for (int f = 0; f < 2; ++f) {
+      const T* fld = f ? win : kin;
+      const T fc = fld[c];
+      T out = fc;
+#pragma unroll
+      for (int ax = 0; ax < 3; ++ax) {
+        if (ext[ax] == 1) continue;
+        const T bwd = pos[ax] > 0 ? (fc - fld[c - str[ax]]) / h[ax] : (T)0;
+        const T fwd = pos[ax] < ext[ax] - 1 ? (fld[c + str[ax]] - fc) / h[ax] : (T)0;
+        const T ap = a[ax] > (T)0 ? a[ax] : (T)0;
+        const T am = a[ax] < (T)0 ? a[ax] : (T)0;
+        out -= dt * (ap * bwd + am * fwd);
+      }
+      (f ? wout : kout)[c] = out;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// MacCormack predictor / corrector (advection.py:125-142)
+__device__ __forceinline__ void comp_offset(int comp, float& ox, float& oy, float& oz) {
+  ox = comp == 0 ? 0.f : 0.5f;
+  oy = comp == 1 ? 0.f : 0.5f;
+  oz = comp == 2 ? 0.f : 0.5f;
+}
+
+template <typename T>
+__device__ __forceinline__ void velocity_at(const Dims& d, const T* u, const T* v, const T* w,
+                                            T X, T Y, T Z, T& us, T& vs, T& ws) {
+  us = gather<T>(u, d.nx + 1, d.ny, d.nz, X, Y - (T)0.5, Z - (T)0.5, nullptr, nullptr);
+  vs = gather<T>(v, d.nx, d.ny + 1, d.nz, X - (T)0.5, Y, Z - (T)0.5, nullptr, nullptr);
+  ws = gather<T>(w, d.nx, d.ny, d.nz + 1, X - (T)0.5, Y - (T)0.5, Z, nullptr, nullptr);
+}
+
+template <typename T>
+__global__ void k_mac_predict(Dims d, int comp, const T* __restrict__ u, const T* __restrict__ v,
+                              const T* __restrict__ w, T* __restrict__ ahead, T dt, const int* gate) {
+  if (*gate) return;
+  int ex, ey, ez;
+  comp_extent(d, comp, ex, ey, ez);
+  float fox, foy, foz;
+  comp_offset(comp, fox, foy, foz);
+  const T ox = (T)fox, oy = (T)foy, oz = (T)foz;
+  const T* arr = comp == 0 ? u : (comp == 1 ? v : w);
+  const long long n = (long long)ex * ey * ez;
+  CW_GRID_STRIDE(c, n) {
+    const int i = (int)(c % ex), j = (int)((c / ex) % ey), k = (int)(c / ((long long)ex * ey));
+    const T X = (T)i + ox, Y = (T)j + oy, Z = (T)k + oz;
+    T us, vs, ws;
+    velocity_at(d, u, v, w, X, Y, Z, us, vs, ws);
+    const T bx = X - dt * us / (T)d.dx, by = Y - dt * vs / (T)d.dy, bz = Z - dt * ws / (T)d.dz;
+    ahead[c] = gather<T>(arr, ex, ey, ez, bx - ox, by - oy, bz - oz, nullptr, nullptr);
+  }
+}
+
+template <typename T>
+__global__ void k_mac_correct(Dims d, int comp, const T* __restrict__ u, const T* __restrict__ v,
+                              const T* __restrict__ w, const T* __restrict__ ahead,
+                              T* __restrict__ out, T dt, const int* gate) {
+  if (*gate) return;
+  int ex, ey, ez;
+  comp_extent(d, comp, ex, ey, ez);
+  float fox, foy, foz;
+  comp_offset(comp, fox, foy, foz);
+  const T ox = (T)fox, oy = (T)foy, oz = (T)foz;
+  const T* arr = comp == 0 ? u : (comp == 1 ? v : w);
+  const long long n = (long long)ex * ey * ez;
+  CW_GRID_STRIDE(c, n) {
+    const int i = (int)(c % ex), j = (int)((c / ex) % ey), k = (int)(c / ((long long)ex * ey));
+    const T X = (T)i + ox, Y = (T)j + oy, Z = (T)k + oz;
+    T us, vs, ws;
+    velocity_at(d, u, v, w, X, Y, Z, us, vs, ws);
+    T mn, mx;
+    const T bx = X - dt * us / (T)d.dx, by = Y - dt * vs / (T)d.dy, bz = Z - dt * ws / (T)d.dz;
+    (void)gather<T>(arr, ex, ey, ez, bx - ox, by - oy, bz - oz, &mn, &mx);
+    const T fx = X + dt * us / (T)d.dx, fy = Y + dt * vs / (T)d.dy, fz = Z + dt * ws / (T)d.dz;
+    const T back = gather<T>(ahead, ex, ey, ez, fx - ox, fy - oy, fz - oz, nullptr, nullptr);
+    T cor = ahead[c] + (T)0.5 * (arr[c] - back);
+    cor = cor < mn ? mn : cor;
+    cor = cor > mx ? mx : cor;
+    out[c] = cor;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// explicit diffusion with the capped eddy viscosity (solver.py:175-208)
+template <typename T>
+__device__ __forceinline__ T nu_eff(const T* nut, long long c, T nu, T cap) {
+  T t = nut[c];
+  t = t < (T)0 ? (T)0 : t;
+  t = t > cap ? cap : t;
+  return nu + t;
+}
+
+template <typename T>
+__global__ void k_diffuse(Dims d, int comp, const T* __restrict__ src, T* __restrict__ dst,
+                          const T* __restrict__ nut, T dt, T nu, T cap, const int* gate) {
+  if (*gate) return;
+  int ex, ey, ez;
+  comp_extent(d, comp, ex, ey, ez);
+  const long long n = (long long)ex * ey * ez;
+  const int ext[3] = {ex, ey, ez};
+  const long long str[3] = {1, ex, (long long)ex * ey};
+  const T h[3] = {(T)d.dx, (T)d.dy, (T)d.dz};
+  CW_GRID_STRIDE(c, n) {
+    const int pos[3] = {(int)(c % ex), (int)((c / ex) % ey), (int)(c / ((long long)ex * ey))};
+    const T mid = src[c];
+    T lap = (T)0;
+#pragma unroll
+    for (int ax = 0; ax < 3; ++ax) {
+      if (ext[ax] == 1 || (d.is2d && ax == 2)) continue;
+      const T lo = pos[ax] > 0 ? src[c - str[ax]] : mid;
+      const T hi = pos[ax] < ext[ax] - 1 ? src[c + str[ax]] : mid;
+      lap += (lo - (T)2 * mid + hi) / (h[ax] * h[ax]);
+    }
+    // face viscosity along the component's own axis, edge faces copy the cell
+    int ci[3] = {pos[0], pos[1], pos[2]};
+    const int nc = comp == 0 ? d.nx : (comp == 1 ? d.ny : d.nz);
+    const int f = pos[comp];
+    ci[comp] = clampi(f - 1, 0, nc - 1);
+    const T a = nu_eff(nut, d.cidx(ci[0], ci[1], ci[2]), nu, cap);
+    ci[comp] = clampi(f, 0, nc - 1);
+    const T b = nu_eff(nut, d.cidx(ci[0], ci[1], ci[2]), nu, cap);
+    dst[c] = mid + dt * ((T)0.5 * (a + b)) * lap;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// porosity drag (solver.py:123-168)
+template <typename T>
+__global__ void k_cell_speed(Dims d, const T* __restrict__ u, const T* __restrict__ v,
+                             const T* __restrict__ w, T* __restrict__ speed, const int* gate) {
+  if (*gate) return;
+  const long long n = d.ncell();
+  CW_GRID_STRIDE(c, n) {
+    const int i = (int)(c % d.nx), j = (int)((c / d.nx) % d.ny), k = (int)(c / ((long long)d.nx * d.ny));
+    const long long ui = ((long long)k * d.ny + j) * (d.nx + 1) + i;
+    const long long vi = ((long long)k * (d.ny + 1) + j) * d.nx + i;
+    const T uc = (T)0.5 * (u[ui] + u[ui + 1]);
+    const T vc = (T)0.5 * (v[vi] + v[vi + d.nx]);
+    const T wc = (T)0.5 * (w[c] + w[c + (long long)d.nx * d.ny]);
+    speed[c] = sqrt(uc * uc + vc * vc + wc * wc);
+  }
+}
+
+template <typename T>
+__global__ void k_drag(Dims d, int comp, T* __restrict__ arr, const T* __restrict__ g,
+                       const T* __restrict__ speed, T dt, const int* gate) {
+  if (*gate) return;
+  int ex, ey, ez;
+  comp_extent(d, comp, ex, ey, ez);
+  const long long n = (long long)ex * ey * ez;
+  const int nc = comp == 0 ? d.nx : (comp == 1 ? d.ny : d.nz);
+  CW_GRID_STRIDE(c, n) {
+    int p[3] = {(int)(c % ex), (int)((c / ex) % ey), (int)(c / ((long long)ex * ey))};
+    const int f = p[comp];
+    p[comp] = clampi(f - 1, 0, nc - 1);
+    const long long lo = d.cidx(p[0], p[1], p[2]);
+    p[comp] = clampi(f, 0, nc - 1);
+    const long long hi = d.cidx(p[0], p[1], p[2]);
+    const T gf = (T)0.5 * (g[lo] + g[hi]);
+    const T sf = (T)0.5 * (speed[lo] + speed[hi]);
+    T fac = (T)1 - dt * gf * sf;
+    fac = fac > (T)0 ? fac : (T)0;
+    arr[c] *= fac;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// boundary conditions (solver.py:330-400): ordered outlet copies, one launch
+// per domain side in the reference's side order, then inlet and wall writes.
+template <typename T>
+struct BcFields {
+  T* u; T* v; T* w; T* p; T* k; T* om; T* nut;
+};
+
+template <typename T>
+__global__ void k_bc_outlet_side(Dims d, int axis, int pos, BcFields<T> F,
+                                 const int8_t* __restrict__ lab, const int* gate) {
+  if (*gate) return;
+  const int ext[3] = {d.nx, d.ny, d.nz};
+  const int a1 = axis == 0 ? 1 : 0, a2 = axis == 2 ? 1 : 2;   // in-plane axes
+  const int n1 = ext[a1] + 1, n2 = ext[a2] + 1;
+  const int inner = pos == 0 ? pos + 1 : pos - 1;
+  const long long n = (long long)n1 * n2;
+  CW_GRID_STRIDE(t, n) {
+    const int q1 = (int)(t % n1), q2 = (int)(t / n1);
+    int c[3];
+    // cells (scalars) and the normal velocity component
+    if (q1 < ext[a1] && q2 < ext[a2]) {
+      c[axis] = pos; c[a1] = q1; c[a2] = q2;
+      const long long cc = d.cidx(c[0], c[1], c[2]);
+      if (lab[cc] == OUTLET) {
+        c[axis] = inner;
+        const long long ci = d.cidx(c[0], c[1], c[2]);
+        F.k[cc] = F.k[ci]; F.om[cc] = F.om[ci]; F.nut[cc] = F.nut[ci]; F.p[cc] = F.p[ci];
+        if (!(d.is2d && axis == 2)) {
+          int ex, ey, ez;
+          comp_extent(d, axis, ex, ey, ez);
+          int f[3];
+          f[a1] = q1; f[a2] = q2;
+          f[axis] = pos > 0 ? pos + 1 : 0;
+          const long long fo = ((long long)f[2] * ey + f[1]) * ex + f[0];
+          f[axis] = pos > 0 ? pos : 1;
+          const long long fs = ((long long)f[2] * ey + f[1]) * ex + f[0];
+          T* arr = axis == 0 ? F.u : (axis == 1 ? F.v : F.w);
+          arr[fo] = arr[fs];
+        }
+      }
+    }
+    // tangential components: face index q along its own axis, mask = either
+    // adjacent outlet-slab cell is an outlet (_face_adjacent_mask)
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+      const int caxis = s == 0 ? a1 : a2;
+      if (d.is2d && caxis == 2) continue;
+      const int qa = s == 0 ? q1 : q2, qb = s == 0 ? q2 : q1;
+      const int oth = s == 0 ? a2 : a1;
+      if (qa > ext[caxis] || qb >= ext[oth]) continue;
+      c[axis] = pos; c[oth] = qb;
+      c[caxis] = clampi(qa - 1, 0, ext[caxis] - 1);
+      bool m = lab[d.cidx(c[0], c[1], c[2])] == OUTLET;
+      c[caxis] = clampi(qa, 0, ext[caxis] - 1);
+      m = m || lab[d.cidx(c[0], c[1], c[2])] == OUTLET;
+      if (!m) continue;
+      int ex, ey, ez;
+      comp_extent(d, caxis, ex, ey, ez);
+      int f[3];
+      f[axis] = pos; f[caxis] = qa; f[oth] = qb;
+      const long long fo = ((long long)f[2] * ey + f[1]) * ex + f[0];
+      f[axis] = inner;
+      const long long fs = ((long long)f[2] * ey + f[1]) * ex + f[0];
+      T* arr = caxis == 0 ? F.u : (caxis == 1 ? F.v : F.w);
+      arr[fo] = arr[fs];
+    }
+  }
+}
+
+// inlet scalars, inlet face velocities, then walls zero all touching faces
+template <typename T>
+__global__ void k_bc_inlet_wall(Dims d, BcFields<T> F, const int8_t* __restrict__ lab,
+                                const T* __restrict__ uz_dirx, const T* __restrict__ uz_diry,
+                                T k_in, T om_in, T nut_in, const int* gate) {
+  if (*gate) return;
+  const long long nc = d.ncell();
+  const long long nu = (long long)(d.nx + 1) * d.ny * d.nz;
+  const long long nv = (long long)d.nx * (d.ny + 1) * d.nz;
+  const long long nw = d.is2d ? 0 : (long long)d.nx * d.ny * (d.nz + 1);
+  const long long n = nc + nu + nv + nw;
+  const int ext[3] = {d.nx, d.ny, d.nz};
+  CW_GRID_STRIDE(t, n) {
+    if (t < nc) {
+      if (lab[t] == INLET) { F.k[t] = k_in; F.om[t] = om_in; F.nut[t] = nut_in; }
+      continue;
+    }
+    long long r = t - nc;
+    int comp = 0;
+    if (r >= nu) { r -= nu; comp = 1; if (r >= nv) { r -= nv; comp = 2; } }
+    int ex, ey, ez;
+    comp_extent(d, comp, ex, ey, ez);
+    int p[3] = {(int)(r % ex), (int)((r / ex) % ey), (int)(r / ((long long)ex * ey))};
+    const int f = p[comp];
+    p[comp] = clampi(f - 1, 0, ext[comp] - 1);
+    const int8_t la = lab[d.cidx(p[0], p[1], p[2])];
+    p[comp] = clampi(f, 0, ext[comp] - 1);
+    const int8_t lb = lab[d.cidx(p[0], p[1], p[2])];
+    T* arr = comp == 0 ? F.u : (comp == 1 ? F.v : F.w);
+    if (la == SOLID_WALL || lb == SOLID_WALL) {
+      arr[r] = (T)0;
+    } else if (la == INLET || lb == INLET) {
+      const int kk = p[2];
+      arr[r] = comp == 0 ? uz_dirx[kk] : (comp == 1 ? uz_diry[kk] : (T)0);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// pressure-gradient update (solver.py:282-303)
+template <typename T>
+__global__ void k_gradient(Dims d, int comp, T* __restrict__ arr, const T* __restrict__ p,
+                           const int8_t* __restrict__ lab, T dt, const int* gate) {
+  if (*gate) return;
+  int ex, ey, ez;
+  comp_extent(d, comp, ex, ey, ez);
+  const long long n = (long long)ex * ey * ez;
+  const T h = comp == 0 ? (T)d.dx : (comp == 1 ? (T)d.dy : (T)d.dz);
+  const int nc = comp == 0 ? d.nx : (comp == 1 ? d.ny : d.nz);
+  CW_GRID_STRIDE(c, n) {
+    int q[3] = {(int)(c % ex), (int)((c / ex) % ey), (int)(c / ((long long)ex * ey))};
+    const int f = q[comp];
+    if (f < 1 || f > nc - 1) continue;
+    q[comp] = f - 1;
+    const long long lo = d.cidx(q[0], q[1], q[2]);
+    q[comp] = f;
+    const long long hi = d.cidx(q[0], q[1], q[2]);
+    const int8_t la = lab[lo], lb = lab[hi];
+    const bool au = is_unknown(la), bu = is_unknown(lb);
+    T grad = (T)0;
+    if (au && bu) grad = (p[hi] - p[lo]) / h;
+    else if (au && lb == OUTLET) grad = -p[lo] / h;
+    else if (bu && la == OUTLET) grad = p[hi] / h;
+    else continue;
+    arr[c] -= dt * grad;
+  }
+}
+
+// max |div| over unknown cells (solver.py:215-229)
+template <typename T>
+__global__ void k_div_max(Dims d, const T* __restrict__ u, const T* __restrict__ v,
+                          const T* __restrict__ w, const int8_t* __restrict__ lab,
+                          DevReport* rep, int slot, const int* gate) {
+  if (*gate) return;
+  __shared__ T scratch[32];
+  const long long n = d.ncell();
+  T m = (T)0;
+  CW_GRID_STRIDE(c, n) {
+    if (!is_unknown(lab[c])) continue;
+    const int i = (int)(c % d.nx), j = (int)((c / d.nx) % d.ny), k = (int)(c / ((long long)d.nx * d.ny));
+    const long long ui = ((long long)k * d.ny + j) * (d.nx + 1) + i;
+    const long long vi = ((long long)k * (d.ny + 1) + j) * d.nx + i;
+    T div = (u[ui + 1] - u[ui]) / (T)d.dx + (v[vi + d.nx] - v[vi]) / (T)d.dy;
+    if (!d.is2d) div = div + (w[c + (long long)d.nx * d.ny] - w[c]) / (T)d.dz;
+    const T a = fabs(div);
+    m = (a > m || a != a) ? a : m;
+  }
+  m = block_max(m, scratch);
+  if (threadIdx.x == 0) report_max<T>(rep, slot, m);
+}
+
+// max |u|,|v|,|w| for the CFL number (solver.py:456-458)
+template <typename T>
+__global__ void k_speed_max(long long nu, long long nv, long long nw, const T* __restrict__ u,
+                            const T* __restrict__ v, const T* __restrict__ w, DevReport* rep,
+                            const int* gate) {
+  if (*gate) return;
+  __shared__ T scratch[32];
+  T m = (T)0;
+  const long long n = nu + nv + nw;
+  CW_GRID_STRIDE(t, n) {
+    const T a = t < nu ? fabs(u[t]) : (t < nu + nv ? fabs(v[t - nu]) : fabs(w[t - nu - nv]));
+    m = (a > m || a != a) ? a : m;
+  }
+  m = block_max(m, scratch);
+  if (threadIdx.x == 0) report_max<T>(rep, SLOT_SPEED, m);
+}
+
+// ---------------------------------------------------------------------------
+// k-omega sources, diffusion, limiter (turbulence.py:36-132)
+template <typename T>
+__device__ __forceinline__ T cell_vel(const Dims& d, int comp, const T* u, const T* v, const T* w,
+                                      int i, int j, int k) {
+  if (comp == 0) {
+    const long long ui = ((long long)k * d.ny + j) * (d.nx + 1) + i;
+    return (T)0.5 * (u[ui] + u[ui + 1]);
+  }
+  if (comp == 1) {
+    const long long vi = ((long long)k * (d.ny + 1) + j) * d.nx + i;
+    return (T)0.5 * (v[vi] + v[vi + d.nx]);
+  }
+  const long long c = d.cidx(i, j, k);
+  return (T)0.5 * (w[c] + w[c + (long long)d.nx * d.ny]);
+}
+
+// np.gradient of the cell-centred component `comp` along `ax` (edge_order 1)
+template <typename T>
+__device__ __forceinline__ T cgrad(const Dims& d, int comp, int ax, const T* u, const T* v,
+                                   const T* w, int i, int j, int k) {
+  const int n = ax == 0 ? d.nx : (ax == 1 ? d.ny : d.nz);
+  if (n == 1) return (T)0;
+  const int q = ax == 0 ? i : (ax == 1 ? j : k);
+  const T h = ax == 0 ? (T)d.dx : (ax == 1 ? (T)d.dy : (T)d.dz);
+  int p0[3] = {i, j, k}, p1[3] = {i, j, k};
+  if (q == 0) { p1[ax] = 1; p0[ax] = 0; }
+  else if (q == n - 1) { p1[ax] = n - 1; p0[ax] = n - 2; }
+  else { p1[ax] = q + 1; p0[ax] = q - 1; }
+  const T f1 = cell_vel(d, comp, u, v, w, p1[0], p1[1], p1[2]);
+  const T f0 = cell_vel(d, comp, u, v, w, p0[0], p0[1], p0[2]);
+  if (q == 0 || q == n - 1) return (f1 - f0) / h;
+  return (f1 - f0) / ((T)2 * h);
+}
+
+template <typename T>
+__device__ __forceinline__ T pad_lap(const Dims& d, const T* f, long long c, int i, int j, int k) {
+  const int pos[3] = {i, j, k}, ext[3] = {d.nx, d.ny, d.nz};
+  const long long str[3] = {1, d.nx, (long long)d.nx * d.ny};
+  const T h[3] = {(T)d.dx, (T)d.dy, (T)d.dz};
+  const T fc = f[c];
+  T out = (T)0;
+#pragma unroll
+  for (int ax = 0; ax < 3; ++ax) {
+    const int n = ext[ax];
+    if (n == 1) continue;
+    const T h2 = h[ax] * h[ax];
+    if (pos[ax] == 0) out += (f[c + str[ax]] - fc) / h2;
+    else if (pos[ax] == n - 1) out += (f[c - str[ax]] - fc) / h2;
+    else out += (f[c - str[ax]] - (T)2 * fc + f[c + str[ax]]) / h2;
+  }
+  return out;
+}
+
+template <typename T>
+__global__ void k_turbulence(Dims d, const T* __restrict__ u, const T* __restrict__ v,
+                             const T* __restrict__ w, const T* __restrict__ kin,
+                             const T* __restrict__ win, T* __restrict__ kout, T* __restrict__ wout,
+                             T* __restrict__ nut, StepConsts sc, DevReport* rep, const int* gate) {
+  if (*gate) return;
+  const long long n = d.ncell();
+  const T dt = (T)sc.dt, nu = (T)sc.nu, cap = (T)sc.cap_turb;
+  CW_GRID_STRIDE(c, n) {
+    const int i = (int)(c % d.nx), j = (int)((c / d.nx) % d.ny), k = (int)(c / ((long long)d.nx * d.ny));
+    const long long ui = ((long long)k * d.ny + j) * (d.nx + 1) + i;
+    const long long vi = ((long long)k * (d.ny + 1) + j) * d.nx + i;
+    const T dudx = (u[ui + 1] - u[ui]) / (T)d.dx;
+    const T dvdy = (v[vi + d.nx] - v[vi]) / (T)d.dy;
+    const T dwdz = (w[c + (long long)d.nx * d.ny] - w[c]) / (T)d.dz;
+    const T dudy = cgrad(d, 0, 1, u, v, w, i, j, k), dudz = cgrad(d, 0, 2, u, v, w, i, j, k);
+    const T dvdx = cgrad(d, 1, 0, u, v, w, i, j, k), dvdz = cgrad(d, 1, 2, u, v, w, i, j, k);
+    const T dwdx = cgrad(d, 2, 0, u, v, w, i, j, k), dwdy = cgrad(d, 2, 1, u, v, w, i, j, k);
+    const T a = dudy + dvdx, b = dudz + dwdx, e = dvdz + dwdy;
+    const T s2 = (dudx * dudx + dvdy * dvdy + dwdz * dwdz) + (T)0.5 * (a * a + b * b + e * e);
+    const T nt = nut[c];
+    const T kc = kin[c], wc = win[c];
+    const T pk = (T)2 * nt * s2;
+    T sk = (T)sc.sigma_star * nt; sk = sk < cap ? sk : cap;
+    T sw = (T)sc.sigma * nt; sw = sw < cap ? sw : cap;
+    const T dk = nu + sk, dw = nu + sw;
+    const T kn = (kc + dt * (pk + dk * pad_lap(d, kin, c, i, j, k))) / ((T)1 + dt * (T)sc.c_mu * wc);
+    const T wn = (wc + dt * ((T)2 * (T)sc.alpha * s2 + dw * pad_lap(d, win, c, i, j, k)))
+                 / ((T)1 + dt * (T)sc.beta * wc);
+    const long long ref = ((long long)i * d.ny + j) * d.nz + k;
+    if (!isfinite(kn)) atomicMin(&rep->bad_index[0], ref);
+    if (!isfinite(wn)) atomicMin(&rep->bad_index[1], ref);
+    const T kf = kn > (T)1e-12 ? kn : (T)1e-12;
+    const T wf = wn > (T)1e-8 ? wn : (T)1e-8;
+    T omt = (T)sc.c_lim * sqrt(s2) / ((T)sc.c_mu / (T)2);
+    omt = wf > omt ? wf : omt;
+    omt = omt > (T)1e-8 ? omt : (T)1e-8;
+    kout[c] = kf;
+    wout[c] = wf;
+    nut[c] = kf / omt;
+  }
+}
+
+// turbulence error latch: runs after k_turbulence, sets the step status/gate
+__global__ void k_turb_check(DevReport* rep, int* gate) {
+  if (*gate) return;
+  if (rep->bad_index[0] != 0x7fffffffffffffffLL || rep->bad_index[1] != 0x7fffffffffffffffLL) {
+    rep->status = 2;
+    *gate = 2;
+  }
+}
+
+}  // namespace cw

@@ -1,0 +1,284 @@
+"""Grid, labels, porosity and the device-resident flow state.
+
+Mirrors the reference's ``citywind.grid`` interface (grid.py:19-130,
+439-571): ``GridSpec``, ``CellLabel``, ``PorosityField``, ``classify_boundary``,
+``merge_labels``, ``interior_mask`` and ``FlowState``.  The difference is
+where the fields live: ``FlowState`` keeps u, v, w, p, k, omega, nu_t as
+CUDA tensors in the x-fastest layout (torch shapes (nz, ny, nx[+1])); its
+``u``/``v``/... attributes return host copies in the reference's C-order
+(nx[+1], ny, nz) float64 layout and accept assignment of such arrays.
+In-place edits of a returned host copy do not reach the device -- assign
+the array back (``state.u = arr``) or edit ``state.fields['u']`` directly.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from enum import IntEnum
+
+import numpy as np
+import torch
+
+
+class CellLabel(IntEnum):
+    AIR = 0
+    BUILDING = 1
+    TREE = 2
+    INLET = 3
+    OUTLET = 4
+    SOLID_WALL = 5
+
+
+INTERIOR_LABELS = (CellLabel.AIR, CellLabel.BUILDING, CellLabel.TREE)
+BOUNDARY_LABELS = (CellLabel.INLET, CellLabel.OUTLET, CellLabel.SOLID_WALL)
+FIELDS = ("u", "v", "w", "p", "k", "omega", "nu_t")
+
+
+@dataclass(frozen=True)
+class GridSpec:
+    """Uniform staggered Cartesian grid; nz = 1 selects 2D mode (grid.py:33-84)."""
+
+    nx: int
+    ny: int
+    nz: int
+    dx: float
+    dy: float
+    dz: float
+    origin: tuple = (0.0, 0.0, 0.0)
+
+    def __post_init__(self):
+        if min(self.nx, self.ny, self.nz) < 1:
+            raise ValueError("cell counts must be >= 1")
+        if min(self.dx, self.dy, self.dz) <= 0:
+            raise ValueError("cell spacings must be > 0")
+
+    @property
+    def shape(self):
+        return (self.nx, self.ny, self.nz)
+
+    @property
+    def n_cells(self):
+        return self.nx * self.ny * self.nz
+
+    @property
+    def is_2d(self):
+        return self.nz == 1
+
+    @property
+    def cell_volume(self):
+        return self.dx * self.dy * self.dz
+
+    @property
+    def spacing(self):
+        return np.array([self.dx, self.dy, self.dz])
+
+    def axis_centers(self, axis):
+        return self.origin[axis] + (np.arange(self.shape[axis]) + 0.5) * self.spacing[axis]
+
+    def cell_centers(self):
+        x, y, z = (self.axis_centers(a) for a in range(3))
+        return np.stack(np.meshgrid(x, y, z, indexing="ij"), axis=-1)
+
+    def extent(self):
+        lo = np.asarray(self.origin, dtype=float)
+        return lo, lo + self.spacing * np.array(self.shape)
+
+    # device layout helpers -------------------------------------------------
+    def dshape(self, name: str):
+        nx, ny, nz = self.shape
+        return {"u": (nz, ny, nx + 1), "v": (nz, ny + 1, nx), "w": (nz + 1, ny, nx)}.get(
+            name, (nz, ny, nx))
+
+
+@dataclass
+class PorosityField:
+    """phi in [0, 1] per cell (1 = open air) and LAD >= 0 (grid.py:87-105),
+    host float64 in the reference layout (nx, ny, nz)."""
+
+    phi: np.ndarray
+    lad: np.ndarray
+
+    @classmethod
+    def open_air(cls, grid: GridSpec):
+        return cls(np.ones(grid.shape), np.zeros(grid.shape))
+
+    def validate(self):
+        if np.any(self.phi < 0) or np.any(self.phi > 1):
+            raise ValueError("phi outside [0, 1]")
+        if np.any(self.lad < 0):
+            raise ValueError("LAD must be >= 0")
+
+    def copy(self):
+        return PorosityField(self.phi.copy(), self.lad.copy())
+
+
+def to_device_layout(a: np.ndarray) -> np.ndarray:
+    """reference C-order (nx, ny, nz) -> x-fastest (nz, ny, nx)."""
+    return np.ascontiguousarray(np.asarray(a).transpose(2, 1, 0))
+
+
+def to_ref_layout(a: np.ndarray) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(a).transpose(2, 1, 0))
+
+
+_FACE_KEYS = ("x_min", "x_max", "y_min", "y_max", "z_min", "z_max")
+
+
+def classify_boundary(grid: GridSpec, faces: dict) -> np.ndarray:
+    """One-cell boundary layer from per-face assignments; edge/corner cells
+    take the priority Inlet > SolidWall > Outlet (grid.py:439-470).  Host
+    int8 labels in the reference layout."""
+    required = _FACE_KEYS[:4] if grid.is_2d else _FACE_KEYS
+    missing = [k for k in required if k not in faces]
+    if missing:
+        raise ValueError(f"missing boundary face assignment(s): {missing}")
+    for key, lab in faces.items():
+        if key not in _FACE_KEYS:
+            raise ValueError(f"unknown face {key!r}")
+        if CellLabel(lab) not in BOUNDARY_LABELS:
+            raise ValueError(f"face {key} must be Inlet/Outlet/SolidWall, got {lab}")
+    labels = np.zeros(grid.shape, dtype=np.int8)
+    sel = {"x_min": np.s_[0:1, :, :], "x_max": np.s_[grid.nx - 1:, :, :],
+           "y_min": np.s_[:, 0:1, :], "y_max": np.s_[:, grid.ny - 1:, :],
+           "z_min": np.s_[:, :, 0:1], "z_max": np.s_[:, :, grid.nz - 1:]}
+    for want in (CellLabel.OUTLET, CellLabel.SOLID_WALL, CellLabel.INLET):
+        for key in required:
+            if CellLabel(faces[key]) == want:
+                labels[sel[key]] = int(want)
+    return labels
+
+
+def merge_labels(boundary: np.ndarray, interior: np.ndarray) -> np.ndarray:
+    """Interior object labels under the boundary frame (grid.py:473-478)."""
+    out = boundary.copy()
+    m = (boundary == int(CellLabel.AIR)) & (interior != int(CellLabel.AIR))
+    out[m] = interior[m]
+    return out
+
+
+def interior_mask(labels: np.ndarray) -> np.ndarray:
+    """Cells that take part in the pressure solve (grid.py:481-484)."""
+    return (labels == 0) | (labels == 1) | (labels == 2)
+
+
+def default_device():
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2204_01117_b200 needs a CUDA device (B200); there is no CPU path")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+class FlowState:
+    """Device-resident simulation state (grid.py:492-571).
+
+    ``fields[name]`` are CUDA tensors in the x-fastest layout; ``labels_dev``
+    is int8, ``phi_dev``/``lad_dev`` float64 (bit-exact voxelizer output).
+    """
+
+    def __init__(self, grid: GridSpec, fields: dict, labels_dev, phi_dev, lad_dev,
+                 time: float = 0.0, step_count: int = 0):
+        self.grid = grid
+        self.fields = fields
+        self.labels_dev = labels_dev
+        self.phi_dev = phi_dev
+        self.lad_dev = lad_dev
+        self.time = time
+        self.step_count = step_count
+        self._drag_key = None
+        self._g = None
+        self._has_drag = False
+
+    # construction ----------------------------------------------------------
+    @classmethod
+    def zeros(cls, grid: GridSpec, labels=None, porosity=None, k0: float = 1e-6,
+              omega0: float = 1.0, dtype=torch.float32, device=None):
+        device = device or default_device()
+        f = {}
+        for n in FIELDS:
+            t = torch.zeros(grid.dshape(n), dtype=dtype, device=device)
+            f[n] = t
+        f["k"].fill_(k0)
+        f["omega"].fill_(omega0)
+        f["nu_t"].fill_(k0 / omega0)
+        lab = np.zeros(grid.shape, np.int8) if labels is None else np.asarray(labels, np.int8)
+        por = PorosityField.open_air(grid) if porosity is None else porosity
+        return cls(grid, f,
+                   torch.from_numpy(to_device_layout(lab)).to(device),
+                   torch.from_numpy(to_device_layout(np.asarray(por.phi, np.float64))).to(device),
+                   torch.from_numpy(to_device_layout(np.asarray(por.lad, np.float64))).to(device))
+
+    @property
+    def device(self):
+        return self.fields["u"].device
+
+    @property
+    def dtype(self):
+        return self.fields["u"].dtype
+
+    # reference-layout host views ---------------------------------------------
+    def _get(self, name):
+        return to_ref_layout(self.fields[name].detach().cpu().numpy().astype(np.float64))
+
+    def _set(self, name, value):
+        value = np.asarray(value, dtype=np.float64)
+        shp = self.grid.dshape(name)[::-1]
+        if value.shape != shp:
+            value = np.broadcast_to(value, shp)
+        self.fields[name].copy_(torch.from_numpy(to_device_layout(value)).to(self.dtype))
+
+    def __getattr__(self, name):
+        if name in FIELDS:
+            return self._get(name)
+        raise AttributeError(name)
+
+    def __setattr__(self, name, value):
+        if name in FIELDS and "fields" in self.__dict__:
+            self._set(name, value)
+        else:
+            object.__setattr__(self, name, value)
+
+    @property
+    def labels(self) -> np.ndarray:
+        return to_ref_layout(self.labels_dev.cpu().numpy())
+
+    @labels.setter
+    def labels(self, value):
+        self.labels_dev.copy_(torch.from_numpy(to_device_layout(np.asarray(value, np.int8))))
+        self._drag_key = None
+
+    @property
+    def porosity(self) -> PorosityField:
+        return PorosityField(to_ref_layout(self.phi_dev.cpu().numpy()),
+                             to_ref_layout(self.lad_dev.cpu().numpy()))
+
+    @porosity.setter
+    def porosity(self, por: PorosityField):
+        self.phi_dev.copy_(torch.from_numpy(to_device_layout(np.asarray(por.phi, np.float64))))
+        self.lad_dev.copy_(torch.from_numpy(to_device_layout(np.asarray(por.lad, np.float64))))
+        self._drag_key = None
+
+    def copy(self) -> "FlowState":
+        return FlowState(self.grid, {n: t.clone() for n, t in self.fields.items()},
+                         self.labels_dev.clone(), self.phi_dev.clone(), self.lad_dev.clone(),
+                         self.time, self.step_count)
+
+    def validate(self):
+        f = self.fields
+        if bool((f["k"] < 0).any()):
+            raise ValueError("negative turbulent kinetic energy")
+        if bool((f["omega"] <= 0).any()):
+            raise ValueError("non-positive specific dissipation")
+        if bool((f["nu_t"] < 0).any()):
+            raise ValueError("negative eddy viscosity")
+        self.porosity.validate()
+
+    def cell_velocity(self) -> np.ndarray:
+        u, v, w = self.u, self.v, self.w
+        return np.stack([0.5 * (u[:-1] + u[1:]), 0.5 * (v[:, :-1] + v[:, 1:]),
+                         0.5 * (w[:, :, :-1] + w[:, :, 1:])], axis=-1)
+
+    def speed(self) -> np.ndarray:
+        vel = self.cell_velocity()
+        return np.sqrt(np.sum(vel * vel, axis=-1))
+
+    def to_host(self) -> dict:
+        """All fields as reference-layout float64 arrays (one D2H per field)."""
+        return {n: self._get(n) for n in FIELDS}
