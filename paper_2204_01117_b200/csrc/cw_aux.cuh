@@ -22,13 +22,14 @@ __global__ void k_report_init(DevReport* r) {
 // +x,-x,+y,-y,+z,-z) = that neighbour is an unknown (off-diagonal -1/h^2 and
 // +1/h^2 on the diagonal) or an outlet (Dirichlet: +1/h^2 on the diagonal).
 // flag[0]: some unknown touches an outlet; flag[1]: an unknown has d = 0.
-__global__ void k_build_code(Dims d, const int8_t* __restrict__ lab, uint8_t* __restrict__ code,
+__global__ void k_build_code(Dims d, int nxp, const int8_t* __restrict__ lab, uint8_t* __restrict__ code,
                              int* flag) {
   const long long n = d.ncell();
   CW_GRID_STRIDE(c, n) {
     const int8_t l = lab[c];
-    if (!is_unknown(l)) { code[c] = 0; continue; }
     const int i = (int)(c % d.nx), j = (int)((c / d.nx) % d.ny), k = (int)(c / ((long long)d.nx * d.ny));
+    const long long pc = ((long long)k * d.ny + j) * nxp + i;   // pitched (PCG layout)
+    if (!is_unknown(l)) { code[pc] = 0; continue; }
     const int pos[3] = {i, j, k}, ext[3] = {d.nx, d.ny, d.nz};
     const long long str[3] = {1, d.nx, (long long)d.nx * d.ny};
     uint8_t cd = 64;
@@ -42,7 +43,7 @@ __global__ void k_build_code(Dims d, const int8_t* __restrict__ lab, uint8_t* __
       if (is_unknown(nl)) cd |= (uint8_t)(1 << q);
       else if (nl == OUTLET) { cd |= (uint8_t)(1 << q); outl = true; }
     }
-    code[c] = cd;
+    code[pc] = cd;
     if (outl) atomicOr(&flag[0], 1);
     if ((cd & 63) == 0) atomicOr(&flag[1], 1);
   }
@@ -59,19 +60,20 @@ __device__ __forceinline__ double code_d(uint8_t cd, double wx, double wy, doubl
 
 // sum over unknowns of diag(W) (closed form of K^T K) for
 // default_projection_tol (solver.py:235-243); fixed grid => deterministic.
-__global__ void k_wdiag_partials(Dims d, const uint8_t* __restrict__ code, double wx, double wy, double wz,
+__global__ void k_wdiag_partials(Dims d, int nxp, const uint8_t* __restrict__ code, double wx, double wy, double wz,
                                  double om, double* part, long long* cnt, double* jpart) {
   __shared__ double red[32];
   const long long n = d.ncell();
   double acc = 0.0, jacc = 0.0;
   long long m = 0;
   const double w[3] = {wx, wy, wz};
-  CW_GRID_STRIDE(c, n) {
+  CW_GRID_STRIDE(c0, n) {
+    const int pos[3] = {(int)(c0 % d.nx), (int)((c0 / d.nx) % d.ny), (int)(c0 / ((long long)d.nx * d.ny))};
+    const long long c = ((long long)pos[2] * d.ny + pos[1]) * nxp + pos[0];
     const uint8_t cd = code[c];
     if (!(cd & 64)) continue;
-    const int pos[3] = {(int)(c % d.nx), (int)((c / d.nx) % d.ny), (int)(c / ((long long)d.nx * d.ny))};
     const int ext[3] = {d.nx, d.ny, d.nz};
-    const long long str[3] = {1, d.nx, (long long)d.nx * d.ny};
+    const long long str[3] = {1, nxp, (long long)nxp * d.ny};
     const double di = code_d(cd, wx, wy, wz);
     jacc += 1.0 / di;
     double wii = (2.0 - om) * om / di;

@@ -2,11 +2,14 @@
 // Host orchestration: one context per grid owns the workspace, the operator
 // code field, the device report ring and the error latch; cw_step enqueues
 // whole steps (no host synchronisation inside a step or between steps).
+#include <cuda.h>
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -31,7 +34,7 @@ static int fail(int code, const std::string& msg) {
       return fail(CW_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_));     \
   } while (0)
 
-static constexpr int TX = 32, TY = 8;
+static constexpr int TX = PCG_TX, TY = PCG_TY;
 static constexpr int RING = 4096;
 
 struct cw_ctx {
@@ -42,6 +45,11 @@ struct cw_ctx {
   cw_grid grid{};
   size_t esz = 4;
   long long ncell = 0, nu_ = 0, nv_ = 0, nw_ = 0;
+  int nxp = 0;                 // row pitch of the PCG vectors (multiple of 16 elements)
+  long long ncellp = 0;
+  void* xw = nullptr;          // pitched PCG solution vector
+  CUtensorMap tm[9];           // z, p0, p1, x, ap, r0, r1, code, code_own
+  size_t pcg_smem = 0;
   // workspace (context precision)
   void *tk = nullptr, *tw = nullptr, *speed = nullptr;
   void *ahead[3] = {nullptr, nullptr, nullptr}, *adv[3] = {nullptr, nullptr, nullptr};
@@ -89,9 +97,34 @@ static int alloc(void** p, size_t bytes) {
 }
 
 template <typename T>
-static int pcg_occupancy(int* blocks_per_sm) {
-  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_pcg<T, TX, TY>, TX * TY, 0);
+static int pcg_occupancy(int* blocks_per_sm, size_t* smem) {
+  *smem = pcg_smem_bytes<T>();
+  cudaError_t e = cudaFuncSetAttribute(k_pcg<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)*smem);
+  if (e != cudaSuccess) return fail(CW_ERR_CUDA, std::string("smem attribute: ") + cudaGetErrorString(e));
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_pcg<T>, TX * TY, *smem);
   if (e != cudaSuccess) return fail(CW_ERR_CUDA, std::string("occupancy: ") + cudaGetErrorString(e));
+  return CW_OK;
+}
+
+// TMA descriptors for the pitched PCG vectors (3D: x, y, z; OOB -> zero fill)
+static int make_tmap(CUtensorMap* m, CUtensorMapDataType dt, size_t esz, void* base, const cw_ctx* c,
+                     unsigned bx, unsigned by) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!encode) {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+    if (e != cudaSuccess || !fn) return fail(CW_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    encode = (PFN_cuTensorMapEncodeTiled_v12000)fn;
+  }
+  cuuint64_t dims[3] = {(cuuint64_t)c->d.nx, (cuuint64_t)c->d.ny, (cuuint64_t)c->d.nz};
+  cuuint64_t strides[2] = {(cuuint64_t)c->nxp * esz, (cuuint64_t)c->nxp * c->d.ny * esz};
+  cuuint32_t box[3] = {bx, by, 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = encode(m, dt, 3, base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                      CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(CW_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
   return CW_OK;
 }
 
@@ -121,11 +154,15 @@ extern "C" int cw_ctx_create(const cw_grid* g, int precision, int device, cw_ctx
   int rc = CW_OK;
   rc |= alloc(&c->tk, cb); rc |= alloc(&c->tw, cb); rc |= alloc(&c->speed, cb);
   for (int a = 0; a < 3; ++a) { rc |= alloc(&c->ahead[a], fb[a]); rc |= alloc(&c->adv[a], fb[a]); }
-  rc |= alloc(&c->r0, cb); rc |= alloc(&c->r1, cb); rc |= alloc(&c->p0, cb);
-  rc |= alloc(&c->p1, cb); rc |= alloc(&c->z, cb); rc |= alloc(&c->Ap, cb);
+  c->nxp = (d.nx + 15) / 16 * 16;
+  c->ncellp = (long long)c->nxp * d.ny * d.nz;
+  const size_t pb = c->ncellp * c->esz;
+  rc |= alloc(&c->r0, c->ncellp * sizeof(double)); rc |= alloc(&c->r1, c->ncellp * sizeof(double));
+  rc |= alloc(&c->p0, pb); rc |= alloc(&c->p1, pb); rc |= alloc(&c->z, pb); rc |= alloc(&c->Ap, pb);
+  rc |= alloc(&c->xw, pb);
   rc |= alloc(&c->lut, 64 * 4 * c->esz);
   rc |= alloc(&c->uzx, d.nz * c->esz); rc |= alloc(&c->uzy, d.nz * c->esz);
-  rc |= alloc((void**)&c->code, c->ncell);
+  rc |= alloc((void**)&c->code, c->ncellp);
   rc |= alloc((void**)&c->bar, 64 * sizeof(unsigned));
   rc |= alloc((void**)&c->gate, sizeof(int));
   rc |= alloc((void**)&c->flag, 4 * sizeof(int));
@@ -134,17 +171,41 @@ extern "C" int cw_ctx_create(const cw_grid* g, int precision, int device, cw_ctx
   // PCG work decomposition: tiles TX x TY over (x, y), z-chunks of zc planes;
   // each co-resident block owns at most one unit when the grid allows it.
   int per_sm = 0;
-  rc = precision == 4 ? pcg_occupancy<float>(&per_sm) : pcg_occupancy<double>(&per_sm);
+  rc = precision == 4 ? pcg_occupancy<float>(&per_sm, &c->pcg_smem) : pcg_occupancy<double>(&per_sm, &c->pcg_smem);
   if (rc != CW_OK || per_sm < 1) { cw_ctx_destroy(c); return rc != CW_OK ? rc : fail(CW_ERR_CUDA, "pcg kernel cannot be resident"); }
   const int maxb = per_sm * c->num_sms;
   c->ntx = (d.nx + TX - 1) / TX;
   c->nty = (d.ny + TY - 1) / TY;
   const int tiles = c->ntx * c->nty;
-  int zc = std::max(4, (d.nz * tiles + maxb - 1) / maxb);
-  zc = std::min(zc, d.nz);
-  c->zc = zc;
-  c->U = tiles * ((d.nz + zc - 1) / zc);
+  // choose the z-chunk: each block streams ceil(U/B) units of zc+2 planes;
+  // minimise that critical path (halo planes included).  CW_PCG_ZC overrides.
+  int best_zc = d.nz, best_cost = 1 << 30;
+  for (int zc = 1; zc <= d.nz; ++zc) {
+    const int U = tiles * ((d.nz + zc - 1) / zc);
+    const int B = std::min(U, maxb);
+    const int m = (U + B - 1) / B;
+    const int cost = m * (zc + 2);
+    if (cost < best_cost) { best_cost = cost; best_zc = zc; }
+  }
+  if (const char* ev = std::getenv("CW_PCG_ZC")) best_zc = std::max(1, std::min(d.nz, std::atoi(ev)));
+  c->zc = best_zc;
+  c->U = tiles * ((d.nz + best_zc - 1) / best_zc);
   c->pcg_blocks = std::min(c->U, maxb);
+  if (const char* eb = std::getenv("CW_PCG_BLOCKS")) c->pcg_blocks = std::max(1, std::min(c->pcg_blocks, std::atoi(eb)));
+  {
+    const CUtensorMapDataType tdt = precision == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64;
+    const size_t e = c->esz;
+    int r2 = make_tmap(&c->tm[0], tdt, e, c->z, c, BOX_X, BOX_Y);
+    r2 |= make_tmap(&c->tm[1], tdt, e, c->p0, c, BOX_X, BOX_Y);
+    r2 |= make_tmap(&c->tm[2], tdt, e, c->p1, c, BOX_X, BOX_Y);
+    r2 |= make_tmap(&c->tm[3], tdt, e, c->xw, c, TX, TY);
+    r2 |= make_tmap(&c->tm[4], tdt, e, c->Ap, c, BOX_X, BOX_Y);
+    r2 |= make_tmap(&c->tm[5], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, c->r0, c, BOX_X, BOX_Y);
+    r2 |= make_tmap(&c->tm[6], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, c->r1, c, BOX_X, BOX_Y);
+    r2 |= make_tmap(&c->tm[7], CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, c->code, c, BOXC_X, BOX_Y);
+    r2 |= make_tmap(&c->tm[8], CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, c->code, c, TX, TY);
+    if (r2 != CW_OK) { cw_ctx_destroy(c); return CW_ERR_CUDA; }
+  }
   rc = alloc((void**)&c->part, 6 * (size_t)c->U * sizeof(double));
   rc |= alloc((void**)&c->reg_part, (size_t)1024 * 64 * sizeof(double));
   rc |= alloc((void**)&c->reg_cnt, (size_t)1024 * 64 * sizeof(long long));
@@ -160,7 +221,7 @@ extern "C" void cw_ctx_destroy(cw_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
   void* ptrs[] = {c->tk, c->tw, c->speed, c->ahead[0], c->ahead[1], c->ahead[2], c->adv[0], c->adv[1],
-                  c->adv[2], c->r0, c->r1, c->p0, c->p1, c->z, c->Ap, c->lut, c->uzx, c->uzy, c->code,
+                  c->adv[2], c->r0, c->r1, c->p0, c->p1, c->z, c->Ap, c->xw, c->lut, c->uzx, c->uzy, c->code,
                   c->part, c->bar, c->gate, c->rep, c->reg_part, c->reg_cnt, c->reg_out, c->reg_cout,
                   c->flag};
   for (void* p : ptrs)
@@ -206,9 +267,9 @@ extern "C" int cw_set_operator(cw_ctx* c, const signed char* lab, double ai_omeg
   }
   CW_CUDA(cudaMemsetAsync(c->flag, 0, 4 * sizeof(int), S(stream)));
   const int nb = std::min(nblk(c->ncell), 1024);
-  k_build_code<<<nb, 256, 0, S(stream)>>>(d, (const int8_t*)lab, c->code, c->flag);
+  k_build_code<<<nb, 256, 0, S(stream)>>>(d, c->nxp, (const int8_t*)lab, c->code, c->flag);
   CW_CUDA(cudaGetLastError());
-  k_wdiag_partials<<<nb, 256, 0, S(stream)>>>(d, c->code, w[0], w[1], w[2], ai_omega, c->reg_part, c->reg_cnt,
+  k_wdiag_partials<<<nb, 256, 0, S(stream)>>>(d, c->nxp, c->code, w[0], w[1], w[2], ai_omega, c->reg_part, c->reg_cnt,
                                                c->reg_part + 1024);
   CW_CUDA(cudaGetLastError());
   std::vector<double> parts(nb), jparts(nb);
@@ -327,11 +388,15 @@ extern "C" int cw_apply_boundary(cw_ctx* c, const cw_fields* f, const cw_params*
 template <typename T>
 static int launch_pcg(cw_ctx* c, const cw_fields* f, DevReport* rep, double dt, double tol, cudaStream_t st) {
   PcgArgs<T> A;
+  A.tm_z = c->tm[0]; A.tm_p0 = c->tm[1]; A.tm_p1 = c->tm[2]; A.tm_x = c->tm[3]; A.tm_ap = c->tm[4];
+  A.tm_r0 = c->tm[5]; A.tm_r1 = c->tm[6]; A.tm_code = c->tm[7]; A.tm_code_own = c->tm[8];
   A.d = c->d;
+  A.nxp = c->nxp;
   A.code = c->code;
-  A.x = (T*)f->p;
+  A.state_p = (T*)f->p;
   A.u = (const T*)f->u; A.v = (const T*)f->v; A.w = (const T*)f->w;
-  A.r0 = (T*)c->r0; A.r1 = (T*)c->r1; A.p0 = (T*)c->p0; A.p1 = (T*)c->p1; A.z = (T*)c->z; A.Ap = (T*)c->Ap;
+  A.r0 = (double*)c->r0; A.r1 = (double*)c->r1; A.p0 = (T*)c->p0; A.p1 = (T*)c->p1; A.z = (T*)c->z; A.Ap = (T*)c->Ap;
+  A.x = (T*)c->xw;
   A.part = c->part;
   A.bar = c->bar;
   A.gate = c->gate;
@@ -350,7 +415,7 @@ static int launch_pcg(cw_ctx* c, const cw_fields* f, DevReport* rep, double dt, 
   A.timeout_ns = 20LL * 1000 * 1000 * 1000;
   CW_CUDA(cudaMemsetAsync(c->bar, 0, 64 * sizeof(unsigned), st));
   void* args[] = {&A};
-  CW_CUDA(cudaLaunchCooperativeKernel((const void*)k_pcg<T, TX, TY>, dim3(c->pcg_blocks), dim3(TX * TY), args, 0, st));
+  CW_CUDA(cudaLaunchCooperativeKernel((const void*)k_pcg<T>, dim3(c->pcg_blocks), dim3(TX * TY), args, c->pcg_smem, st));
   return CW_OK;
 }
 

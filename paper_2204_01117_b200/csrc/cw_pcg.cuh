@@ -12,31 +12,49 @@
 // +x,-x,+y,-y,+z,-z is an unknown or an outlet) and a 64-entry table of
 // (d, 1/d, s) -- no CSR, no stored coefficients.
 //
-// PCG vectors live on the full grid with exact zeros at non-unknown cells,
-// so stencils need no masks.  Each iteration is two grid phases separated
-// by a grid barrier that also completes a deterministic fp64 reduction:
+// Data movement (B200): the PCG vectors live on a pitched copy of the grid
+// (row pitch nxp = nx rounded up to 16 elements, exact zeros off the
+// unknowns) so that every (x,y)-tile-with-halo of one z-plane is a single
+// TMA box (cp.async.bulk.tensor.3d; out-of-range elements are zero-filled by
+// the hardware, which is exactly the operator's boundary rule).  Each block
+// marches its tiles through z; one thread keeps a DEPTH-stage shared-memory
+// ring of planes in flight (mbarrier complete_tx), so a block has DEPTH
+// planes of loads outstanding instead of one.
+//
+// Each PCG iteration is two grid phases separated by a grid barrier that
+// also completes a deterministic fp64 reduction:
 //   phase A: p' = z + beta p  (recomputed on the tile halo), x += alpha_prev p,
 //            Ap = A p', partial p'.Ap
 //   phase B: r' = r - alpha Ap (recomputed on the halo), z = W r',
 //            partials r'.z and max|r'|
-// (x's update is deferred by one phase so phase B streams 16 B/unknown and
-// phase A 24 B/unknown in fp32.)  Partial sums are kept per work unit and
-// every block folds them in the same fixed order, so all blocks agree
-// bit-for-bit on alpha/beta and the result is run-to-run deterministic.
+// Storage: p, z, Ap, x in the state precision; r in float64 (a float32
+// recursive residual drifts by ~eps*|b| per iteration, several percent of the
+// max-norm target 10^-4.5 max|b|, which flips stopping decisions).  Partials
+// are kept per block over a fixed unit->block map and every block folds them
+// in the same fixed order: all blocks agree bit-for-bit on alpha/beta and
+// runs are deterministic.
 #pragma once
+#include <cuda.h>
+
 #include "cw_common.cuh"
 #include "cw_step.cuh"
 
 namespace cw {
 
+constexpr int PCG_TX = 32, PCG_TY = 8;
+constexpr int BOX_X = 36, BOX_Y = PCG_TY + 2, BOXC_X = 48;   // halo boxes (16-byte rows)
+
 template <typename T>
 struct PcgArgs {
+  CUtensorMap tm_z, tm_p0, tm_p1, tm_x, tm_ap, tm_r0, tm_r1, tm_code, tm_code_own;
   Dims d;
-  const uint8_t* code;
-  T* x;                      // state p (in: warm start, out: solution; 0 off the unknowns)
+  int nxp;                   // row pitch of the PCG vectors
+  const uint8_t* code;       // pitched
+  T* state_p;                // state pressure (unpitched): warm start in, solution out
   const T* u; const T* v; const T* w;
-  T* r0; T* r1; T* p0; T* p1; T* z; T* Ap;
-  double* part;              // [2][3][U] per-unit partials (two alternating sets)
+  double* r0; double* r1;    // pitched, float64
+  T* p0; T* p1; T* z; T* Ap; T* x;   // pitched
+  double* part;              // [2][3][U] partials (two alternating sets)
   unsigned int* bar;         // [0] arrival count, [32] generation
   int* gate;
   DevReport* rep;
@@ -48,6 +66,38 @@ struct PcgArgs {
   int ntx, nty, zc, U;
   long long timeout_ns;
 };
+
+// ---------------------------------------------------------------------------
+// PTX helpers: mbarrier + TMA
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
+  asm volatile(
+      "{\n\t.reg .pred P;\n"
+      "CW_WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t"
+      "@!P bra CW_WAIT_%=;\n}" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* b, int x, int y,
+                                            int z) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
+      "l"((unsigned long long)map), "r"(x), "r"(y), "r"(z), "r"(smem_u32(b))
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async;" ::: "memory"); }
 
 __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
   unsigned v;
@@ -62,8 +112,7 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 
 // Grid barrier for a cooperative launch (all blocks co-resident).  Times out
 // (status 3) instead of hanging if the co-residency assumption is ever broken.
-__device__ __forceinline__ void grid_barrier(unsigned* bar, int* gate, DevReport* rep,
-                                             long long timeout_ns) {
+__device__ __forceinline__ void grid_barrier(unsigned* bar, int* gate, DevReport* rep, long long timeout_ns) {
   __syncthreads();
   if (threadIdx.x == 0) {
     unsigned* count = bar;
@@ -79,7 +128,7 @@ __device__ __forceinline__ void grid_barrier(unsigned* bar, int* gate, DevReport
       const unsigned long long t0 = globaltimer();
       unsigned spins = 0;
       while (ld_acquire(gen) == g) {
-        __nanosleep(64);
+        __nanosleep(32);
         if ((++spins & 1023u) == 0 && (long long)(globaltimer() - t0) > timeout_ns) {
           rep->status = 3;
           *gate = 3;
@@ -88,16 +137,17 @@ __device__ __forceinline__ void grid_barrier(unsigned* bar, int* gate, DevReport
       }
     }
     __threadfence();
+    fence_proxy_async();   // the next phase's TMA (async proxy) reads see this phase's writes
   }
   __syncthreads();
 }
 
-// Fold U per-unit partials in a fixed order; every block computes the same
-// bits.  mode 0: sum, 1: max.  Result broadcast to all threads.
-__device__ __forceinline__ double fold_partials(const double* part, int U, int mode, double* sh) {
+// Fold n partials in a fixed order; every block computes the same bits.
+// mode 0: sum, 1: max.  Result broadcast to all threads.
+__device__ __forceinline__ double fold_partials(const double* part, int n, int mode, double* sh) {
   if (threadIdx.x < 32) {
     double a = 0.0;
-    for (int q = threadIdx.x; q < U; q += 32) {
+    for (int q = threadIdx.x; q < n; q += 32) {
       const double v = __ldcg(part + q);
       if (mode == 0) a += v;
       else a = (v > a || v != v) ? v : a;
@@ -116,52 +166,140 @@ __device__ __forceinline__ double fold_partials(const double* part, int U, int m
   return r;
 }
 
-template <typename T, int TX, int TY>
-struct PcgSmem {
-  T lut[64 * 4];
-  T pa[3][TY + 2][TX + 2];
-  T rb[2][TY + 2][TX + 2];
-  T qb[2][TY + 2][TX + 2];
-  uint8_t cb[2][TY + 2][TX + 2];
-  T yb[2][TY + 1][TX + 1];
-  double red[32];
-  T redt[32];
-  double bc[4];
+// ---------------------------------------------------------------------------
+// shared memory layout
+
+__host__ __device__ constexpr int align128(int b) { return (b + 127) & ~127; }
+
+template <typename T>
+struct StageLayout {
+  // phase A: z, p (halo boxes), x (own box)
+  static constexpr int A_Z = 0;
+  static constexpr int A_P = align128(BOX_X * BOX_Y * (int)sizeof(T));
+  static constexpr int A_X = A_P + align128(BOX_X * BOX_Y * (int)sizeof(T));
+  static constexpr int A_C = A_X + align128(PCG_TX * PCG_TY * (int)sizeof(T));
+  static constexpr int A_END = A_C + align128(PCG_TX * PCG_TY);
+  // phase B: r (float64), Ap, code (halo boxes)
+  static constexpr int B_R = 0;
+  static constexpr int B_AP = align128(BOX_X * BOX_Y * 8);
+  static constexpr int B_C = B_AP + align128(BOX_X * BOX_Y * (int)sizeof(T));
+  static constexpr int B_END = B_C + align128(BOXC_X * BOX_Y);
+  static constexpr int STAGE = A_END > B_END ? A_END : B_END;
+  static constexpr int DEPTH = sizeof(T) == 4 ? 6 : 4;
+  static constexpr unsigned BYTES_A_HALO = 2u * BOX_X * BOX_Y * sizeof(T);
+  static constexpr unsigned BYTES_A_X = PCG_TX * PCG_TY * (sizeof(T) + 1);   // x + code, own box
+  static constexpr unsigned BYTES_B = BOX_X * BOX_Y * 8u + BOX_X * BOX_Y * sizeof(T) + BOXC_X * BOX_Y;
 };
+
+template <typename T>
+struct PcgShared {
+  T lut[64 * 4];
+  T pa[2][PCG_TY + 2][PCG_TX + 2];          // phase 0 planes
+  double rb[3][PCG_TY + 2][PCG_TX + 2];     // phase B converted planes (3 = hazard-free ring)
+  T qb[3][PCG_TY + 2][PCG_TX + 2];
+  uint8_t cb[3][PCG_TY + 2][PCG_TX + 2];
+  T yb[2][PCG_TY + 1][PCG_TX + 1];
+  double red[32];
+  double bc[4];
+  alignas(8) uint64_t full[8];
+};
+
+template <typename T>
+__host__ __device__ constexpr size_t pcg_smem_bytes() {
+  return 128 + (size_t)StageLayout<T>::STAGE * StageLayout<T>::DEPTH + sizeof(PcgShared<T>);
+}
 
 struct Unit {
   int i0, j0, k0, k1;
 };
 
-template <typename T, int TX, int TY>
+template <typename T>
 __device__ __forceinline__ Unit unit_of(const PcgArgs<T>& A, int u) {
   const int per = A.ntx * A.nty;
   const int tz = u / per, rem = u - tz * per;
   Unit t;
-  t.i0 = (rem % A.ntx) * TX;
-  t.j0 = (rem / A.ntx) * TY;
+  t.i0 = (rem % A.ntx) * PCG_TX;
+  t.j0 = (rem / A.ntx) * PCG_TY;
   t.k0 = tz * A.zc;
   t.k1 = min(t.k0 + A.zc, A.d.nz);
   return t;
 }
 
+// Jobs of one ring phase for this block: its units in order (unit
+// blockIdx.x + m*gridDim.x), each contributing planes k0-1 .. k1.
+struct JobCursor {
+  int unit;
+  Unit t;
+  int kk;
+};
+
+template <typename T>
+__device__ __forceinline__ bool cursor_begin(const PcgArgs<T>& A, JobCursor& c) {
+  c.unit = blockIdx.x;
+  if (c.unit >= A.U) return false;
+  c.t = unit_of<T>(A, c.unit);
+  c.kk = c.t.k0 - 1;
+  return true;
+}
+template <typename T>
+__device__ __forceinline__ bool cursor_next(const PcgArgs<T>& A, JobCursor& c) {
+  if (c.kk < c.t.k1) { ++c.kk; return true; }
+  c.unit += gridDim.x;
+  if (c.unit >= A.U) return false;
+  c.t = unit_of<T>(A, c.unit);
+  c.kk = c.t.k0 - 1;
+  return true;
+}
+
+// Producer: thread 0 issues job `ticket` (numbered across the whole kernel,
+// which fixes every stage's mbarrier parity).
+template <typename T>
+__device__ __forceinline__ void issue_A(const PcgArgs<T>& A, uint8_t* ring, uint64_t* full, unsigned ticket,
+                                        const JobCursor& c, const CUtensorMap* tp) {
+  using L = StageLayout<T>;
+  const int s = ticket % L::DEPTH;
+  uint8_t* st = ring + (size_t)s * L::STAGE;
+  const bool own = c.kk >= c.t.k0 && c.kk < c.t.k1;
+  mbar_expect_tx(&full[s], L::BYTES_A_HALO + (own ? L::BYTES_A_X : 0u));
+  tma_load_3d(st + L::A_Z, &A.tm_z, &full[s], c.t.i0 - 1, c.t.j0 - 1, c.kk);
+  tma_load_3d(st + L::A_P, tp, &full[s], c.t.i0 - 1, c.t.j0 - 1, c.kk);
+  if (own) {
+    tma_load_3d(st + L::A_X, &A.tm_x, &full[s], c.t.i0, c.t.j0, c.kk);
+    tma_load_3d(st + L::A_C, &A.tm_code_own, &full[s], c.t.i0, c.t.j0, c.kk);
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ void issue_B(const PcgArgs<T>& A, uint8_t* ring, uint64_t* full, unsigned ticket,
+                                        const JobCursor& c, const CUtensorMap* tr) {
+  using L = StageLayout<T>;
+  const int s = ticket % L::DEPTH;
+  uint8_t* st = ring + (size_t)s * L::STAGE;
+  mbar_expect_tx(&full[s], L::BYTES_B);
+  tma_load_3d(st + L::B_R, tr, &full[s], c.t.i0 - 1, c.t.j0 - 1, c.kk);
+  tma_load_3d(st + L::B_AP, &A.tm_ap, &full[s], c.t.i0 - 1, c.t.j0 - 1, c.kk);
+  tma_load_3d(st + L::B_C, &A.tm_code, &full[s], c.t.i0 - 1, c.t.j0 - 1, c.kk);
+}
+
 // ---- phase 0: b = -div/dt, r0 = b - A x0 with x0 = p on the unknowns ------
-template <typename T, int TX, int TY>
-__device__ void phase0(const PcgArgs<T>& A, double* part, int unit, PcgSmem<T, TX, TY>& S) {
+// (once per projection; plain loads)
+template <typename T>
+__device__ void phase0(const PcgArgs<T>& A, double* part, int unit, PcgShared<T>& S) {
   const Dims& d = A.d;
-  const Unit t = unit_of<T, TX, TY>(A, unit);
-  const int lx = threadIdx.x % TX, ly = threadIdx.x / TX;
+  const Unit t = unit_of<T>(A, unit);
+  const int lx = threadIdx.x % PCG_TX, ly = threadIdx.x / PCG_TX;
   const int i = t.i0 + lx, j = t.j0 + ly;
   const bool own = i < d.nx && j < d.ny;
   const long long plane = (long long)d.nx * d.ny;
+  const long long pplane = (long long)A.nxp * d.ny;
   auto load = [&](int kk, int b) {
-    for (int e = threadIdx.x; e < (TX + 2) * (TY + 2); e += TX * TY) {
-      const int hx = e % (TX + 2), hy = e / (TX + 2);
+    for (int e = threadIdx.x; e < (PCG_TX + 2) * (PCG_TY + 2); e += PCG_TX * PCG_TY) {
+      const int hx = e % (PCG_TX + 2), hy = e / (PCG_TX + 2);
       const int gi = t.i0 + hx - 1, gj = t.j0 + hy - 1;
       T val = (T)0;
       if (kk >= 0 && kk < d.nz && gi >= 0 && gi < d.nx && gj >= 0 && gj < d.ny) {
-        const long long c = kk * plane + (long long)gj * d.nx + gi;
-        if (A.code[c] & 64) val = __ldcg(A.x + c);
+        if (A.code[kk * pplane + (long long)gj * A.nxp + gi] & 64)
+          val = A.state_p[kk * plane + (long long)gj * d.nx + gi];
       }
       S.pa[b][hy][hx] = val;
     }
@@ -169,8 +307,8 @@ __device__ void phase0(const PcgArgs<T>& A, double* part, int unit, PcgSmem<T, T
   double b2 = 0.0, bmax = 0.0, dmax = 0.0;
   T pm = (T)0;
   if (own && t.k0 - 1 >= 0) {
-    const long long c = (t.k0 - 1) * plane + (long long)j * d.nx + i;
-    pm = (A.code[c] & 64) ? __ldcg(A.x + c) : (T)0;
+    if (A.code[(t.k0 - 1) * pplane + (long long)j * A.nxp + i] & 64)
+      pm = A.state_p[(t.k0 - 1) * plane + (long long)j * d.nx + i];
   }
   int bc = 0, bn = 1;
   load(t.k0, bc);
@@ -179,30 +317,33 @@ __device__ void phase0(const PcgArgs<T>& A, double* part, int unit, PcgSmem<T, T
     __syncthreads();
     if (own) {
       const long long c = k * plane + (long long)j * d.nx + i;
-      const uint8_t cd = A.code[c];
+      const long long pc_ = k * pplane + (long long)j * A.nxp + i;
+      const uint8_t cd = A.code[pc_];
       const T pc = S.pa[bc][ly + 1][lx + 1];
       const T pn = S.pa[bn][ly + 1][lx + 1];
       if (cd & 64) {
         const long long ui = ((long long)k * d.ny + j) * (d.nx + 1) + i;
         const long long vi = ((long long)k * (d.ny + 1) + j) * d.nx + i;
-        T div = (A.u[ui + 1] - A.u[ui]) / (T)d.dx + (A.v[vi + d.nx] - A.v[vi]) / (T)d.dy;
-        if (!d.is2d) div = div + (A.w[c + plane] - A.w[c]) / (T)d.dz;
-        const T b = -div / (T)A.dt;
-        const T ax = S.lut[(cd & 63) * 4] * pc -
-                     (A.wx * (S.pa[bc][ly + 1][lx] + S.pa[bc][ly + 1][lx + 2]) +
-                      A.wy * (S.pa[bc][ly][lx + 1] + S.pa[bc][ly + 2][lx + 1]) + A.wz * (pm + pn));
-        A.r0[c] = b - ax;
-        b2 += (double)b * (double)b;
-        const double ab = fabs((double)b), ad = fabs((double)div);
+        // divergence and A x0 in float64 from the stored fields
+        double div = ((double)A.u[ui + 1] - (double)A.u[ui]) / d.ddx +
+                     ((double)A.v[vi + d.nx] - (double)A.v[vi]) / d.ddy;
+        if (!d.is2d) div = div + ((double)A.w[c + plane] - (double)A.w[c]) / d.ddz;
+        const double b = -div / A.dt;
+        const double ax = (double)S.lut[(cd & 63) * 4] * (double)pc -
+                          ((double)A.wx * ((double)S.pa[bc][ly + 1][lx] + (double)S.pa[bc][ly + 1][lx + 2]) +
+                           (double)A.wy * ((double)S.pa[bc][ly][lx + 1] + (double)S.pa[bc][ly + 2][lx + 1]) +
+                           (double)A.wz * ((double)pm + (double)pn));
+        A.r0[pc_] = b - ax;
+        A.x[pc_] = pc;
+        b2 += b * b;
+        const double ab = fabs(b), ad = fabs(div);
         bmax = (ab > bmax || ab != ab) ? ab : bmax;
         dmax = (ad > dmax || ad != ad) ? ad : dmax;
       } else {
-        A.x[c] = (T)0;
+        A.state_p[c] = (T)0;   // project() sets p = 0 off the unknowns (solver.py:278-280)
       }
       pm = pc;
     }
-    // rotate: next plane becomes current; the old current buffer is free
-    // once every thread has passed the barrier at the top of the next pass
     __syncthreads();
     const int tmp = bc; bc = bn; bn = tmp;
   }
@@ -219,186 +360,256 @@ __device__ void phase0(const PcgArgs<T>& A, double* part, int unit, PcgSmem<T, T
 }
 
 // ---- phase A: p' = z + beta p, x += alpha_prev p, Ap = A p' ---------------
-template <typename T, int TX, int TY>
-__device__ void phaseA(const PcgArgs<T>& A, double* part, int unit, PcgSmem<T, TX, TY>& S, bool first, T beta,
-                       bool upd_x, T alpha_prev, const T* __restrict__ pin, T* __restrict__ pout) {
+template <typename T>
+__device__ void phaseA(const PcgArgs<T>& A, double* part, PcgShared<T>& S, uint8_t* ring, unsigned& ticket,
+                       bool first, T beta, bool upd_x, T alpha_prev, int pin_sel) {
+  using L = StageLayout<T>;
+  static_assert(L::DEPTH >= 3, "ring too shallow");
   const Dims& d = A.d;
-  const Unit t = unit_of<T, TX, TY>(A, unit);
-  const int lx = threadIdx.x % TX, ly = threadIdx.x / TX;
-  const int i = t.i0 + lx, j = t.j0 + ly;
-  const bool own = i < d.nx && j < d.ny;
-  const long long plane = (long long)d.nx * d.ny;
-  auto pnew = [&](long long c) -> T {
-    const T zz = __ldcg(A.z + c);
-    return first ? zz : zz + beta * __ldcg(pin + c);
-  };
-  auto load = [&](int kk, int b) {
-    for (int e = threadIdx.x; e < (TX + 2) * (TY + 2); e += TX * TY) {
-      const int hx = e % (TX + 2), hy = e / (TX + 2);
-      const int gi = t.i0 + hx - 1, gj = t.j0 + hy - 1;
-      T val = (T)0;
-      if (kk >= 0 && kk < d.nz && gi >= 0 && gi < d.nx && gj >= 0 && gj < d.ny)
-        val = pnew(kk * plane + (long long)gj * d.nx + gi);
-      S.pa[b][hy][hx] = val;
-    }
-  };
+  const CUtensorMap* tp = pin_sel == 0 ? &A.tm_p0 : &A.tm_p1;
+  T* __restrict__ pout = pin_sel == 0 ? A.p1 : A.p0;
+  const int lx = threadIdx.x % PCG_TX, ly = threadIdx.x / PCG_TX;
+  const long long pplane = (long long)A.nxp * d.ny;
+  JobCursor prod, cons;
   double acc = 0.0;
-  T pm = (T)0;
-  if (own && t.k0 - 1 >= 0) pm = pnew((t.k0 - 1) * plane + (long long)j * d.nx + i);
-  int bc = 0, bn = 1;
-  load(t.k0, bc);
-  for (int k = t.k0; k < t.k1; ++k) {
-    load(k + 1, bn);
-    __syncthreads();
-    if (own) {
-      const long long c = k * plane + (long long)j * d.nx + i;
-      const uint8_t cd = A.code[c];
-      const T pc = S.pa[bc][ly + 1][lx + 1];
-      const T pn = S.pa[bn][ly + 1][lx + 1];
-      if (cd & 64) {
-        const T ap = S.lut[(cd & 63) * 4] * pc -
-                     (A.wx * (S.pa[bc][ly + 1][lx] + S.pa[bc][ly + 1][lx + 2]) +
-                      A.wy * (S.pa[bc][ly][lx + 1] + S.pa[bc][ly + 2][lx + 1]) + A.wz * (pm + pn));
-        pout[c] = pc;
-        A.Ap[c] = ap;
-        if (upd_x) A.x[c] += alpha_prev * __ldcg(pin + c);
-        acc += (double)pc * (double)ap;
+  if (cursor_begin<T>(A, cons)) {
+    prod = cons;
+    const unsigned t0 = ticket;
+    unsigned issued = 0;
+    bool more = true;   // producer state, meaningful in thread 0 only
+    if (threadIdx.x == 0) {
+      while (more && issued < (unsigned)L::DEPTH) {
+        issue_A<T>(A, ring, S.full, t0 + issued, prod, tp);
+        ++issued;
+        more = cursor_next<T>(A, prod);
       }
-      pm = pc;
     }
-    __syncthreads();
-    const int tmp = bc; bc = bn; bn = tmp;
+    auto pnew = [&](const uint8_t* st, int hy, int hx) -> T {
+      const T* zz = reinterpret_cast<const T*>(st + L::A_Z);
+      const T* pp = reinterpret_cast<const T*>(st + L::A_P);
+      const T zv = zz[hy * BOX_X + hx];
+      return first ? zv : zv + beta * pp[hy * BOX_X + hx];
+    };
+    unsigned j = 0;     // consumer job number in this phase
+    int cur_s = 0;      // stage holding plane kk-1 of the current unit
+    T pm = (T)0;
+    bool live = true;
+    while (live) {
+      const unsigned tk = t0 + j;
+      const int s = tk % L::DEPTH;
+      const uint8_t* st = ring + (size_t)s * L::STAGE;
+      mbar_wait(&S.full[s], (tk / L::DEPTH) & 1u);
+      const Unit u = cons.t;
+      const int i = u.i0 + lx, jj = u.j0 + ly;
+      if (cons.kk == u.k0 - 1) {
+        pm = pnew(st, ly + 1, lx + 1);           // own value of plane k0-1
+      } else if (cons.kk > u.k0) {
+        // plane k = kk-1: 5-point from the held stage, own k+1 from this one
+        const int k = cons.kk - 1;
+        const uint8_t* cs = ring + (size_t)cur_s * L::STAGE;
+        const T pc = pnew(cs, ly + 1, lx + 1);
+        if (i < d.nx && jj < d.ny) {
+          const long long pc_ = k * pplane + (long long)jj * A.nxp + i;
+          const uint8_t cd = (cs + L::A_C)[ly * PCG_TX + lx];
+          if (cd & 64) {
+            const T pn = pnew(st, ly + 1, lx + 1);
+            const T ap = S.lut[(cd & 63) * 4] * pc -
+                         (A.wx * (pnew(cs, ly + 1, lx) + pnew(cs, ly + 1, lx + 2)) +
+                          A.wy * (pnew(cs, ly, lx + 1) + pnew(cs, ly + 2, lx + 1)) + A.wz * (pm + pn));
+            pout[pc_] = pc;
+            A.Ap[pc_] = ap;
+            if (upd_x) {
+              const T* xx = reinterpret_cast<const T*>(cs + L::A_X);
+              const T* pp = reinterpret_cast<const T*>(cs + L::A_P);
+              A.x[pc_] = xx[ly * PCG_TX + lx] + alpha_prev * pp[(ly + 1) * BOX_X + lx + 1];
+            }
+            acc += (double)pc * (double)ap;
+          }
+        }
+        pm = pc;
+      }
+      cur_s = s;
+      live = cursor_next<T>(A, cons);
+      ++j;
+      __syncthreads();   // everyone is done with stage j-2's data; job j-1's stage stays held
+      if (threadIdx.x == 0) {
+        while (more && issued < j + L::DEPTH - 1) {
+          fence_proxy_async();
+          issue_A<T>(A, ring, S.full, t0 + issued, prod, tp);
+          ++issued;
+          more = cursor_next<T>(A, prod);
+        }
+      }
+    }
+    ticket = t0 + j;
   }
-  const double s = block_sum(acc, S.red);
-  if (threadIdx.x == 0) part[unit] = s;
+  const double sum = block_sum(acc, S.red);
+  if (threadIdx.x == 0) part[blockIdx.x] = sum;
 }
 
 // ---- phase B: r' = r - alpha Ap, z = W r' ----------------------------------
-template <typename T, int TX, int TY>
-__device__ void phaseB(const PcgArgs<T>& A, double* part, int unit, PcgSmem<T, TX, TY>& S, bool use_ap, T alpha,
-                       const T* __restrict__ rin, T* __restrict__ rout) {
+template <typename T>
+__device__ void phaseB(const PcgArgs<T>& A, double* part, PcgShared<T>& S, uint8_t* ring, unsigned& ticket,
+                       bool use_ap, double alpha, int rin_sel, bool write_r) {
+  using L = StageLayout<T>;
   const Dims& d = A.d;
-  const Unit t = unit_of<T, TX, TY>(A, unit);
-  const int lx = threadIdx.x % TX, ly = threadIdx.x / TX;
-  const int i = t.i0 + lx, j = t.j0 + ly;
-  const bool own = i < d.nx && j < d.ny;
-  const long long plane = (long long)d.nx * d.ny;
+  const CUtensorMap* tr = rin_sel == 0 ? &A.tm_r0 : &A.tm_r1;
+  double* __restrict__ rout = rin_sel == 0 ? A.r1 : A.r0;
   const T om = A.om;
-  auto load = [&](int kk, int b) {
-    for (int e = threadIdx.x; e < (TX + 2) * (TY + 2); e += TX * TY) {
-      const int hx = e % (TX + 2), hy = e / (TX + 2);
-      const int gi = t.i0 + hx - 1, gj = t.j0 + hy - 1;
-      T rr = (T)0;
-      uint8_t cd = 0;
-      if (kk >= 0 && kk < d.nz && gi >= 0 && gi < d.nx && gj >= 0 && gj < d.ny) {
-        const long long c = kk * plane + (long long)gj * d.nx + gi;
-        cd = A.code[c];
-        rr = __ldcg(rin + c);
-        if (use_ap) rr = rr - alpha * __ldcg(A.Ap + c);
-      }
-      S.rb[b][hy][hx] = rr;
-      S.qb[b][hy][hx] = rr * S.lut[(cd & 63) * 4 + 1];
-      S.cb[b][hy][hx] = cd;
-    }
-  };
+  const int lx = threadIdx.x % PCG_TX, ly = threadIdx.x / PCG_TX;
+  const long long pplane = (long long)A.nxp * d.ny;
+  JobCursor prod, cons;
   double acc = 0.0, rmax = 0.0;
-  T rprev = (T)0;
-  for (int kk = t.k0 - 1; kk <= t.k1; ++kk) {
-    const int b = kk & 1, bp = (kk - 1) & 1;
-    load(kk, b);
-    __syncthreads();
-    const T rown = S.rb[b][ly + 1][lx + 1];
-    if (kk >= t.k0) {
-      for (int e = threadIdx.x; e < (TX + 1) * (TY + 1); e += TX * TY) {
-        const int hx = e % (TX + 1), hy = e / (TX + 1);
-        const uint8_t cd = S.cb[b][hy + 1][hx + 1];
-        const T s = S.lut[(cd & 63) * 4 + 2];
-        S.yb[b][hy][hx] = s * (S.rb[b][hy + 1][hx + 1] +
-                               om * (A.wx * S.qb[b][hy + 1][hx] + A.wy * S.qb[b][hy][hx + 1] +
-                                     A.wz * S.qb[bp][hy + 1][hx + 1]));
+  if (cursor_begin<T>(A, cons)) {
+    prod = cons;
+    const unsigned t0 = ticket;
+    unsigned issued = 0;
+    bool more = true;
+    if (threadIdx.x == 0) {
+      while (more && issued < (unsigned)L::DEPTH) {
+        issue_B<T>(A, ring, S.full, t0 + issued, prod, tr);
+        ++issued;
+        more = cursor_next<T>(A, prod);
       }
     }
-    __syncthreads();
-    if (kk >= t.k0 + 1 && own) {
-      const int k = kk - 1;
-      const long long c = k * plane + (long long)j * d.nx + i;
-      const uint8_t cd = S.cb[bp][ly + 1][lx + 1];
-      if (cd & 64) {
-        T zv;
-        if (A.precond == 2)
-          zv = S.yb[bp][ly][lx] + om * S.lut[(cd & 63) * 4 + 1] *
-               (A.wx * S.yb[bp][ly][lx + 1] + A.wy * S.yb[bp][ly + 1][lx] + A.wz * S.yb[b][ly][lx]);
-        else if (A.precond == 1)
-          zv = S.qb[bp][ly + 1][lx + 1];
-        else
-          zv = rprev;
-        A.z[c] = zv;
-        if (use_ap) rout[c] = rprev;
-        acc += (double)rprev * (double)zv;
-        const double ar = fabs((double)rprev);
-        rmax = (ar > rmax || ar != ar) ? ar : rmax;
+    unsigned j = 0;
+    double rprev = 0.0;
+    bool live = true;
+    while (live) {
+      const unsigned tk = t0 + j;
+      const int s = tk % L::DEPTH;
+      const uint8_t* st = ring + (size_t)s * L::STAGE;
+      mbar_wait(&S.full[s], (tk / L::DEPTH) & 1u);
+      const Unit u = cons.t;
+      const int kk = cons.kk;
+      const int b = j % 3, bp = (j + 2) % 3;      // work-plane ring (job order)
+      const int yb_ = j & 1, ybp = (j + 1) & 1;
+      // convert the landed stage: r' = r - alpha Ap, q = r'/d, code
+      {
+        const double* rr = reinterpret_cast<const double*>(st + L::B_R);
+        const T* aa = reinterpret_cast<const T*>(st + L::B_AP);
+        const uint8_t* cc = st + L::B_C;
+        for (int e = threadIdx.x; e < (PCG_TX + 2) * (PCG_TY + 2); e += PCG_TX * PCG_TY) {
+          const int hx = e % (PCG_TX + 2), hy = e / (PCG_TX + 2);
+          double r = rr[hy * BOX_X + hx];
+          if (use_ap) r = r - alpha * (double)aa[hy * BOX_X + hx];
+          const uint8_t cd = cc[hy * BOXC_X + hx];
+          S.rb[b][hy][hx] = r;
+          S.qb[b][hy][hx] = (T)r * S.lut[(cd & 63) * 4 + 1];
+          S.cb[b][hy][hx] = cd;
+        }
       }
+      __syncthreads();
+      if (threadIdx.x == 0 && more) {     // the raw stage is free: refill it
+        fence_proxy_async();
+        issue_B<T>(A, ring, S.full, t0 + issued, prod, tr);
+        ++issued;
+        more = cursor_next<T>(A, prod);
+      }
+      const double rown = S.rb[b][ly + 1][lx + 1];
+      if (kk >= u.k0 && A.precond == 2) {
+        for (int e = threadIdx.x; e < (PCG_TX + 1) * (PCG_TY + 1); e += PCG_TX * PCG_TY) {
+          const int hx = e % (PCG_TX + 1), hy = e / (PCG_TX + 1);
+          const uint8_t cd = S.cb[b][hy + 1][hx + 1];
+          const T sv = S.lut[(cd & 63) * 4 + 2];
+          S.yb[yb_][hy][hx] = sv * ((T)S.rb[b][hy + 1][hx + 1] +
+                                    om * (A.wx * S.qb[b][hy + 1][hx] + A.wy * S.qb[b][hy][hx + 1] +
+                                          A.wz * S.qb[bp][hy + 1][hx + 1]));
+        }
+      }
+      __syncthreads();
+      const int i = u.i0 + lx, jj = u.j0 + ly;
+      if (kk >= u.k0 + 1 && i < d.nx && jj < d.ny) {
+        const int k = kk - 1;
+        const long long pc_ = k * pplane + (long long)jj * A.nxp + i;
+        const uint8_t cd = S.cb[bp][ly + 1][lx + 1];
+        if (cd & 64) {
+          T zv;
+          if (A.precond == 2)
+            zv = S.yb[ybp][ly][lx] + om * S.lut[(cd & 63) * 4 + 1] *
+                 (A.wx * S.yb[ybp][ly][lx + 1] + A.wy * S.yb[ybp][ly + 1][lx] + A.wz * S.yb[yb_][ly][lx]);
+          else if (A.precond == 1)
+            zv = S.qb[bp][ly + 1][lx + 1];
+          else
+            zv = (T)rprev;
+          A.z[pc_] = zv;
+          if (write_r) rout[pc_] = rprev;
+          acc += rprev * (double)zv;
+          const double ar = fabs(rprev);
+          rmax = (ar > rmax || ar != ar) ? ar : rmax;
+        }
+      }
+      rprev = rown;
+      live = cursor_next<T>(A, cons);
+      ++j;
     }
-    rprev = rown;
+    ticket = t0 + j;
   }
-  const double s = block_sum(acc, S.red);
+  const double sm = block_sum(acc, S.red);
   __syncthreads();
-  const double m = block_max(rmax, S.red);
+  const double mx = block_max(rmax, S.red);
   if (threadIdx.x == 0) {
-    part[unit] = s;
-    part[A.U + unit] = m;
+    part[blockIdx.x] = sm;
+    part[A.U + blockIdx.x] = mx;
   }
 }
 
-template <typename T, int TX, int TY>
-__device__ void x_update(const PcgArgs<T>& A, int unit, T alpha, const T* __restrict__ p) {
+// final: state p = x (+ alpha p pending) on the unknowns
+template <typename T>
+__device__ void finish_x(const PcgArgs<T>& A, int unit, T alpha, const T* __restrict__ p, bool zero) {
   const Dims& d = A.d;
-  const Unit t = unit_of<T, TX, TY>(A, unit);
-  const int lx = threadIdx.x % TX, ly = threadIdx.x / TX;
+  const Unit t = unit_of<T>(A, unit);
+  const int lx = threadIdx.x % PCG_TX, ly = threadIdx.x / PCG_TX;
   const int i = t.i0 + lx, j = t.j0 + ly;
   if (i >= d.nx || j >= d.ny) return;
-  const long long plane = (long long)d.nx * d.ny;
+  const long long plane = (long long)d.nx * d.ny, pplane = (long long)A.nxp * d.ny;
   for (int k = t.k0; k < t.k1; ++k) {
     const long long c = k * plane + (long long)j * d.nx + i;
-    if (A.code[c] & 64) A.x[c] += alpha * __ldcg(p + c);
+    const long long pc_ = k * pplane + (long long)j * A.nxp + i;
+    if (zero) { A.state_p[c] = (T)0; continue; }
+    if (A.code[pc_] & 64) A.state_p[c] = alpha != (T)0 ? A.x[pc_] + alpha * p[pc_] : A.x[pc_];
   }
 }
 
-template <typename T, int TX, int TY>
-__device__ void x_zero(const PcgArgs<T>& A, int unit) {
-  const Dims& d = A.d;
-  const Unit t = unit_of<T, TX, TY>(A, unit);
-  const int lx = threadIdx.x % TX, ly = threadIdx.x / TX;
-  const int i = t.i0 + lx, j = t.j0 + ly;
-  if (i >= d.nx || j >= d.ny) return;
-  const long long plane = (long long)d.nx * d.ny;
-  for (int k = t.k0; k < t.k1; ++k) A.x[k * plane + (long long)j * d.nx + i] = (T)0;
-}
-
-template <typename T, int TX, int TY>
-__global__ void __launch_bounds__(TX * TY) k_pcg(PcgArgs<T> A) {
-  __shared__ PcgSmem<T, TX, TY> S;
+template <typename T>
+__global__ void __launch_bounds__(PCG_TX * PCG_TY) k_pcg(const __grid_constant__ PcgArgs<T> A) {
+  extern __shared__ uint8_t dyn[];
+  uint8_t* base = reinterpret_cast<uint8_t*>(((uintptr_t)dyn + 127) & ~(uintptr_t)127);
+  uint8_t* ring = base;
+  PcgShared<T>& S =
+      *reinterpret_cast<PcgShared<T>*>(base + (size_t)StageLayout<T>::STAGE * StageLayout<T>::DEPTH);
   if (*(volatile int*)A.gate) return;  // uniform across blocks: set before launch
   for (int e = threadIdx.x; e < 64 * 4; e += blockDim.x) S.lut[e] = A.lut[e];
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < StageLayout<T>::DEPTH; ++s) mbar_init(&S.full[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    fence_proxy_async();
+  }
   __syncthreads();
   DevReport* rep = A.rep;
   const int U = A.U;
-  // two partial sets, alternated by phase, so one barrier per phase suffices
+  const int B = gridDim.x;
+  unsigned ticket = 0;
+  // two partial sets, alternated by phase, so one barrier per phase suffices;
+  // phase 0 writes per unit, the ring phases per block (fixed unit->block map)
   double* P[2] = {A.part, A.part + 3 * U};
 
-  for (int u = blockIdx.x; u < U; u += gridDim.x) phase0<T, TX, TY>(A, P[0], u, S);
+  for (int u = blockIdx.x; u < U; u += B) phase0<T>(A, P[0], u, S);
   grid_barrier(A.bar, A.gate, rep, A.timeout_ns);
   const double b2 = fold_partials(P[0], U, 0, S.bc);
   const double bmax = fold_partials(P[0] + U, U, 1, S.bc);
   const double divmax = fold_partials(P[0] + 2 * U, U, 1, S.bc);
   if (blockIdx.x == 0 && threadIdx.x == 0) report_max<T>(rep, SLOT_DIV_BEFORE, (T)divmax);
-  if (*(volatile int*)A.gate == 3) { if (blockIdx.x == 0 && threadIdx.x == 0) rep->status = 3; return; }
+  if (*(volatile int*)A.gate == 3) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) rep->status = 3;
+    return;
+  }
   if (!isfinite(bmax)) {                     // pcg_solve raises on a non-finite rhs
     if (blockIdx.x == 0 && threadIdx.x == 0) { rep->status = 4; *A.gate = 4; }
     return;
   }
   if (b2 == 0.0) {                           // linalg.py:329-330: x = 0, 0 iterations
-    for (int u = blockIdx.x; u < U; u += gridDim.x) x_zero<T, TX, TY>(A, u);
+    for (int u = blockIdx.x; u < U; u += B) finish_x<T>(A, u, (T)0, A.p0, true);
     if (blockIdx.x == 0 && threadIdx.x == 0) { rep->iterations = 0; rep->converged = 1; rep->criterion = 0.0; }
     return;
   }
@@ -406,37 +617,34 @@ __global__ void __launch_bounds__(TX * TY) k_pcg(PcgArgs<T> A) {
   const double tol = A.tol;
 
   // z = W r0, rz, max|r0|  (pcg_solve:342-345)
-  for (int u = blockIdx.x; u < U; u += gridDim.x)
-    phaseB<T, TX, TY>(A, P[1], u, S, false, (T)0, A.r0, A.r0);
+  phaseB<T>(A, P[1], S, ring, ticket, false, 0.0, 0, false);
   grid_barrier(A.bar, A.gate, rep, A.timeout_ns);
-  double rz = fold_partials(P[1], U, 0, S.bc);
-  double rmax = fold_partials(P[1] + U, U, 1, S.bc);
+  double rz = fold_partials(P[1], B, 0, S.bc);
+  double rmax = fold_partials(P[1] + U, B, 1, S.bc);
   double crit = rz / b2;
   int it = 0, converged = 0, status = 0;
   bool finished = false;
   if (0.0 <= crit && crit < tol && rmax <= res_target) { converged = 1; finished = true; }
   else if (rz < 0.0) { finished = true; }
-  T* rc = A.r0; T* rn = A.r1;
-  T* pc = A.p1; T* pn = A.p0;     // pc: previous direction (unused on the first pass)
+  int rsel = 0;       // r lives in r0 (0) or r1 (1)
+  int psel = 1;       // previous p lives in p0 (0) or p1 (1); the first pass ignores it
   double alpha = 0.0, beta = 0.0;
   while (!finished) {
     if (it >= A.max_iter) break;
     ++it;
     const bool first = it == 1;
-    for (int u = blockIdx.x; u < U; u += gridDim.x)
-      phaseA<T, TX, TY>(A, P[0], u, S, first, (T)beta, !first, (T)alpha, pc, pn);
+    phaseA<T>(A, P[0], S, ring, ticket, first, (T)beta, !first, (T)alpha, psel);
     grid_barrier(A.bar, A.gate, rep, A.timeout_ns);
-    const double pAp = fold_partials(P[0], U, 0, S.bc);
-    { T* tmp = pc; pc = pn; pn = tmp; }      // pc now holds this iteration's p
+    const double pAp = fold_partials(P[0], B, 0, S.bc);
+    psel ^= 1;                                // the new p went to the other buffer
     if (*(volatile int*)A.gate == 3) { status = 3; alpha = 0.0; break; }
     if (pAp <= 0.0) { it -= 1; alpha = 0.0; break; }   // linalg.py:354-355
     alpha = rz / pAp;
-    for (int u = blockIdx.x; u < U; u += gridDim.x)
-      phaseB<T, TX, TY>(A, P[1], u, S, true, (T)alpha, rc, rn);
+    phaseB<T>(A, P[1], S, ring, ticket, true, alpha, rsel, true);
     grid_barrier(A.bar, A.gate, rep, A.timeout_ns);
-    const double rz_new = fold_partials(P[1], U, 0, S.bc);
-    rmax = fold_partials(P[1] + U, U, 1, S.bc);
-    { T* tmp = rc; rc = rn; rn = tmp; }
+    const double rz_new = fold_partials(P[1], B, 0, S.bc);
+    rmax = fold_partials(P[1] + U, B, 1, S.bc);
+    rsel ^= 1;
     crit = rz_new / b2;
     if (*(volatile int*)A.gate == 3) { status = 3; break; }
     if (0.0 <= crit && crit < tol && rmax <= res_target) { converged = 1; break; }
@@ -444,9 +652,9 @@ __global__ void __launch_bounds__(TX * TY) k_pcg(PcgArgs<T> A) {
     beta = rz_new / rz;
     rz = rz_new;
   }
-  // x += alpha p of the last completed iteration is still pending
-  if (alpha != 0.0)
-    for (int u = blockIdx.x; u < U; u += gridDim.x) x_update<T, TX, TY>(A, u, (T)alpha, pc);
+  // state p = x, plus the alpha p of the last completed iteration if pending
+  const T* plast = psel == 0 ? A.p0 : A.p1;
+  for (int u = blockIdx.x; u < U; u += B) finish_x<T>(A, u, (T)alpha, plast, false);
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     rep->iterations = it;
     rep->converged = converged;

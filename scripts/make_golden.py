@@ -44,7 +44,7 @@ def digest(a):
 SCENES = {
     "cuboid_32": (scenes.cuboid(32, 32, 16, 2.0, 0.3), 40),
     "canyon_48": (scenes.canyon(48, 48, 24, 1.0, 0.2, n_trees=4), 25),
-    "city_64": (scenes.block_city(64, 64, 24, 2.0, seed=3, nb=3, dt=0.4), 20),
+    "city_64": (scenes.block_city(64, 64, 24, 2.0, seed=3, nb=3, dt=0.25), 30),
     "channel2d": (scenes.channel_2d(24, 16, 0.1, 2.0), 60),
 }
 VOXEL_ONLY = {

@@ -16,7 +16,7 @@ GOLD = os.path.join(os.path.dirname(__file__), "golden")
 STEP_SCENES = {
     "cuboid_32": lambda: scenes.cuboid(32, 32, 16, 2.0, 0.3),
     "canyon_48": lambda: scenes.canyon(48, 48, 24, 1.0, 0.2, n_trees=4),
-    "city_64": lambda: scenes.block_city(64, 64, 24, 2.0, seed=3, nb=3, dt=0.4),
+    "city_64": lambda: scenes.block_city(64, 64, 24, 2.0, seed=3, nb=3, dt=0.25),
     "channel2d": lambda: scenes.channel_2d(24, 16, 0.1, 2.0),
 }
 
