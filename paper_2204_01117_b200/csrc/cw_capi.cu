@@ -195,14 +195,15 @@ extern "C" int cw_ctx_create(const cw_grid* g, int precision, int device, cw_ctx
   {
     const CUtensorMapDataType tdt = precision == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64;
     const size_t e = c->esz;
-    int r2 = make_tmap(&c->tm[0], tdt, e, c->z, c, BOX_X, BOX_Y);
-    r2 |= make_tmap(&c->tm[1], tdt, e, c->p0, c, BOX_X, BOX_Y);
-    r2 |= make_tmap(&c->tm[2], tdt, e, c->p1, c, BOX_X, BOX_Y);
+    const unsigned hbw = precision == 4 ? Halo<float>::BW : Halo<double>::BW;
+    int r2 = make_tmap(&c->tm[0], tdt, e, c->z, c, hbw, BOX_Y);
+    r2 |= make_tmap(&c->tm[1], tdt, e, c->p0, c, hbw, BOX_Y);
+    r2 |= make_tmap(&c->tm[2], tdt, e, c->p1, c, hbw, BOX_Y);
     r2 |= make_tmap(&c->tm[3], tdt, e, c->xw, c, TX, TY);
-    r2 |= make_tmap(&c->tm[4], tdt, e, c->Ap, c, BOX_X, BOX_Y);
-    r2 |= make_tmap(&c->tm[5], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, c->r0, c, BOX_X, BOX_Y);
-    r2 |= make_tmap(&c->tm[6], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, c->r1, c, BOX_X, BOX_Y);
-    r2 |= make_tmap(&c->tm[7], CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, c->code, c, BOXC_X, BOX_Y);
+    r2 |= make_tmap(&c->tm[4], tdt, e, c->Ap, c, hbw, BOX_Y);
+    r2 |= make_tmap(&c->tm[5], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, c->r0, c, Halo<double>::BW, BOX_Y);
+    r2 |= make_tmap(&c->tm[6], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, c->r1, c, Halo<double>::BW, BOX_Y);
+    r2 |= make_tmap(&c->tm[7], CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, c->code, c, Halo<uint8_t>::BW, BOX_Y);
     r2 |= make_tmap(&c->tm[8], CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, c->code, c, TX, TY);
     if (r2 != CW_OK) { cw_ctx_destroy(c); return CW_ERR_CUDA; }
   }

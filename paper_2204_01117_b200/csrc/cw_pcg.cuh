@@ -42,7 +42,20 @@
 namespace cw {
 
 constexpr int PCG_TX = 32, PCG_TY = 8;
-constexpr int BOX_X = 36, BOX_Y = PCG_TY + 2, BOXC_X = 48;   // halo boxes (16-byte rows)
+constexpr int BOX_Y = PCG_TY + 2;
+
+// Halo box geometry per element type.  A TMA box must START on a 16-byte
+// boundary in x, so the box begins SH elements left of the tile (SH = 16 B /
+// element) and is BW elements wide; halo column hx (hx = 0 is x = i0-1)
+// lives at box column hx + OFF.
+template <typename E>
+struct Halo {
+  static constexpr int SH = 16 / (int)sizeof(E);
+  static constexpr int BW = ((SH + PCG_TX + 1) + SH - 1) / SH * SH;
+  static constexpr int OFF = SH - 1;
+  static constexpr unsigned BYTES = (unsigned)(BW * BOX_Y * (int)sizeof(E));
+  __device__ __forceinline__ static int at(int hy, int hx) { return hy * BW + hx + OFF; }
+};
 
 template <typename T>
 struct PcgArgs {
@@ -175,20 +188,20 @@ template <typename T>
 struct StageLayout {
   // phase A: z, p (halo boxes), x (own box)
   static constexpr int A_Z = 0;
-  static constexpr int A_P = align128(BOX_X * BOX_Y * (int)sizeof(T));
-  static constexpr int A_X = A_P + align128(BOX_X * BOX_Y * (int)sizeof(T));
+  static constexpr int A_P = align128((int)Halo<T>::BYTES);
+  static constexpr int A_X = A_P + align128((int)Halo<T>::BYTES);
   static constexpr int A_C = A_X + align128(PCG_TX * PCG_TY * (int)sizeof(T));
   static constexpr int A_END = A_C + align128(PCG_TX * PCG_TY);
   // phase B: r (float64), Ap, code (halo boxes)
   static constexpr int B_R = 0;
-  static constexpr int B_AP = align128(BOX_X * BOX_Y * 8);
-  static constexpr int B_C = B_AP + align128(BOX_X * BOX_Y * (int)sizeof(T));
-  static constexpr int B_END = B_C + align128(BOXC_X * BOX_Y);
+  static constexpr int B_AP = align128((int)Halo<double>::BYTES);
+  static constexpr int B_C = B_AP + align128((int)Halo<T>::BYTES);
+  static constexpr int B_END = B_C + align128((int)Halo<uint8_t>::BYTES);
   static constexpr int STAGE = A_END > B_END ? A_END : B_END;
   static constexpr int DEPTH = sizeof(T) == 4 ? 6 : 4;
-  static constexpr unsigned BYTES_A_HALO = 2u * BOX_X * BOX_Y * sizeof(T);
+  static constexpr unsigned BYTES_A_HALO = 2u * Halo<T>::BYTES;
   static constexpr unsigned BYTES_A_X = PCG_TX * PCG_TY * (sizeof(T) + 1);   // x + code, own box
-  static constexpr unsigned BYTES_B = BOX_X * BOX_Y * 8u + BOX_X * BOX_Y * sizeof(T) + BOXC_X * BOX_Y;
+  static constexpr unsigned BYTES_B = Halo<double>::BYTES + Halo<T>::BYTES + Halo<uint8_t>::BYTES;
 };
 
 template <typename T>
@@ -261,8 +274,8 @@ __device__ __forceinline__ void issue_A(const PcgArgs<T>& A, uint8_t* ring, uint
   uint8_t* st = ring + (size_t)s * L::STAGE;
   const bool own = c.kk >= c.t.k0 && c.kk < c.t.k1;
   mbar_expect_tx(&full[s], L::BYTES_A_HALO + (own ? L::BYTES_A_X : 0u));
-  tma_load_3d(st + L::A_Z, &A.tm_z, &full[s], c.t.i0 - 1, c.t.j0 - 1, c.kk);
-  tma_load_3d(st + L::A_P, tp, &full[s], c.t.i0 - 1, c.t.j0 - 1, c.kk);
+  tma_load_3d(st + L::A_Z, &A.tm_z, &full[s], c.t.i0 - Halo<T>::SH, c.t.j0 - 1, c.kk);
+  tma_load_3d(st + L::A_P, tp, &full[s], c.t.i0 - Halo<T>::SH, c.t.j0 - 1, c.kk);
   if (own) {
     tma_load_3d(st + L::A_X, &A.tm_x, &full[s], c.t.i0, c.t.j0, c.kk);
     tma_load_3d(st + L::A_C, &A.tm_code_own, &full[s], c.t.i0, c.t.j0, c.kk);
@@ -276,9 +289,9 @@ __device__ __forceinline__ void issue_B(const PcgArgs<T>& A, uint8_t* ring, uint
   const int s = ticket % L::DEPTH;
   uint8_t* st = ring + (size_t)s * L::STAGE;
   mbar_expect_tx(&full[s], L::BYTES_B);
-  tma_load_3d(st + L::B_R, tr, &full[s], c.t.i0 - 1, c.t.j0 - 1, c.kk);
-  tma_load_3d(st + L::B_AP, &A.tm_ap, &full[s], c.t.i0 - 1, c.t.j0 - 1, c.kk);
-  tma_load_3d(st + L::B_C, &A.tm_code, &full[s], c.t.i0 - 1, c.t.j0 - 1, c.kk);
+  tma_load_3d(st + L::B_R, tr, &full[s], c.t.i0 - Halo<double>::SH, c.t.j0 - 1, c.kk);
+  tma_load_3d(st + L::B_AP, &A.tm_ap, &full[s], c.t.i0 - Halo<T>::SH, c.t.j0 - 1, c.kk);
+  tma_load_3d(st + L::B_C, &A.tm_code, &full[s], c.t.i0 - Halo<uint8_t>::SH, c.t.j0 - 1, c.kk);
 }
 
 // ---- phase 0: b = -div/dt, r0 = b - A x0 with x0 = p on the unknowns ------
@@ -387,8 +400,9 @@ __device__ void phaseA(const PcgArgs<T>& A, double* part, PcgShared<T>& S, uint8
     auto pnew = [&](const uint8_t* st, int hy, int hx) -> T {
       const T* zz = reinterpret_cast<const T*>(st + L::A_Z);
       const T* pp = reinterpret_cast<const T*>(st + L::A_P);
-      const T zv = zz[hy * BOX_X + hx];
-      return first ? zv : zv + beta * pp[hy * BOX_X + hx];
+      const int o = Halo<T>::at(hy, hx);
+      const T zv = zz[o];
+      return first ? zv : zv + beta * pp[o];
     };
     unsigned j = 0;     // consumer job number in this phase
     int cur_s = 0;      // stage holding plane kk-1 of the current unit
@@ -421,7 +435,7 @@ __device__ void phaseA(const PcgArgs<T>& A, double* part, PcgShared<T>& S, uint8
             if (upd_x) {
               const T* xx = reinterpret_cast<const T*>(cs + L::A_X);
               const T* pp = reinterpret_cast<const T*>(cs + L::A_P);
-              A.x[pc_] = xx[ly * PCG_TX + lx] + alpha_prev * pp[(ly + 1) * BOX_X + lx + 1];
+              A.x[pc_] = xx[ly * PCG_TX + lx] + alpha_prev * pp[Halo<T>::at(ly + 1, lx + 1)];
             }
             acc += (double)pc * (double)ap;
           }
@@ -491,9 +505,9 @@ __device__ void phaseB(const PcgArgs<T>& A, double* part, PcgShared<T>& S, uint8
         const uint8_t* cc = st + L::B_C;
         for (int e = threadIdx.x; e < (PCG_TX + 2) * (PCG_TY + 2); e += PCG_TX * PCG_TY) {
           const int hx = e % (PCG_TX + 2), hy = e / (PCG_TX + 2);
-          double r = rr[hy * BOX_X + hx];
-          if (use_ap) r = r - alpha * (double)aa[hy * BOX_X + hx];
-          const uint8_t cd = cc[hy * BOXC_X + hx];
+          double r = rr[Halo<double>::at(hy, hx)];
+          if (use_ap) r = r - alpha * (double)aa[Halo<T>::at(hy, hx)];
+          const uint8_t cd = cc[Halo<uint8_t>::at(hy, hx)];
           S.rb[b][hy][hx] = r;
           S.qb[b][hy][hx] = (T)r * S.lut[(cd & 63) * 4 + 1];
           S.cb[b][hy][hx] = cd;

@@ -268,6 +268,8 @@ def step_many(state: FlowState, params: SolverParams, psys: PressureSystem, prec
                 done += chunk
                 continue
             rc, reps = ctx.read_reports(chunk)
+            if rc != N.CW_OK and not reps:
+                N.check(rc)
             wall = (time.perf_counter() - t0) / chunk
             timings = {"step": wall}
             if stage_timings:
@@ -321,6 +323,8 @@ def _stage(state, params, profile, stage, dt, psys=None, preconditioner=None, to
                                      -1.0 if tol is None else float(tol), ctx.stream))
         rc, reps = ctx.read_reports(1)
         if rc != N.CW_OK:
+            if not reps:
+                N.check(rc)
             _raise_for(rc, reps[0], state.grid)
         return reps[0]
     finally:
