@@ -427,17 +427,21 @@ __device__ void phaseA(const PcgArgs<T>& A, double* part, PcgShared<T>& S, uint8
           const uint8_t cd = (cs + L::A_C)[ly * PCG_TX + lx];
           if (cd & 64) {
             const T pn = pnew(st, ly + 1, lx + 1);
-            const T ap = S.lut[(cd & 63) * 4] * pc -
-                         (A.wx * (pnew(cs, ly + 1, lx) + pnew(cs, ly + 1, lx + 2)) +
-                          A.wy * (pnew(cs, ly, lx + 1) + pnew(cs, ly + 2, lx + 1)) + A.wz * (pm + pn));
+            // A p in float64 from the stored p: the 7-point difference of a
+            // smooth p cancels d*p almost entirely, so float32 arithmetic would
+            // leave a relative error of ~eps*d|p|/|Ap| in Ap (and in r)
+            const double ap = (double)S.lut[(cd & 63) * 4] * (double)pc -
+                              ((double)A.wx * ((double)pnew(cs, ly + 1, lx) + (double)pnew(cs, ly + 1, lx + 2)) +
+                               (double)A.wy * ((double)pnew(cs, ly, lx + 1) + (double)pnew(cs, ly + 2, lx + 1)) +
+                               (double)A.wz * ((double)pm + (double)pn));
             pout[pc_] = pc;
-            A.Ap[pc_] = ap;
+            A.Ap[pc_] = (T)ap;
             if (upd_x) {
               const T* xx = reinterpret_cast<const T*>(cs + L::A_X);
               const T* pp = reinterpret_cast<const T*>(cs + L::A_P);
               A.x[pc_] = xx[ly * PCG_TX + lx] + alpha_prev * pp[Halo<T>::at(ly + 1, lx + 1)];
             }
-            acc += (double)pc * (double)ap;
+            acc += (double)pc * ap;
           }
         }
         pm = pc;
@@ -448,7 +452,7 @@ __device__ void phaseA(const PcgArgs<T>& A, double* part, PcgShared<T>& S, uint8
       __syncthreads();   // everyone is done with stage j-2's data; job j-1's stage stays held
       if (threadIdx.x == 0) {
         while (more && issued < j + L::DEPTH - 1) {
-          fence_proxy_async();
+
           issue_A<T>(A, ring, S.full, t0 + issued, prod, tp);
           ++issued;
           more = cursor_next<T>(A, prod);
@@ -515,7 +519,7 @@ __device__ void phaseB(const PcgArgs<T>& A, double* part, PcgShared<T>& S, uint8
       }
       __syncthreads();
       if (threadIdx.x == 0 && more) {     // the raw stage is free: refill it
-        fence_proxy_async();
+
         issue_B<T>(A, ring, S.full, t0 + issued, prod, tr);
         ++issued;
         more = cursor_next<T>(A, prod);
