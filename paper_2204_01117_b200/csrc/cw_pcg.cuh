@@ -476,6 +476,27 @@ __device__ void phaseB(const PcgArgs<T>& A, double* part, PcgShared<T>& S, uint8
   const T om = A.om;
   const int lx = threadIdx.x % PCG_TX, ly = threadIdx.x / PCG_TX;
   const long long pplane = (long long)A.nxp * d.ny;
+  // fixed per-thread positions of the convert and y passes
+  struct {
+    int e[2], sr[2], st[2], sc[2], yo[2], ye[2];
+    bool h1, y1;
+  } P;
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const int e = threadIdx.x + q * PCG_TX * PCG_TY;
+    const int ec = e < (PCG_TX + 2) * (PCG_TY + 2) ? e : 0;
+    const int hx = ec % (PCG_TX + 2), hy = ec / (PCG_TX + 2);
+    P.e[q] = ec;
+    P.sr[q] = Halo<double>::at(hy, hx);
+    P.st[q] = Halo<T>::at(hy, hx);
+    P.sc[q] = Halo<uint8_t>::at(hy, hx);
+    const int ey = e < (PCG_TX + 1) * (PCG_TY + 1) ? e : 0;
+    const int yx = ey % (PCG_TX + 1), yy = ey / (PCG_TX + 1);
+    P.yo[q] = (yy + 1) * (PCG_TX + 2) + yx + 1;
+    P.ye[q] = yy * (PCG_TX + 1) + yx;
+  }
+  P.h1 = threadIdx.x + PCG_TX * PCG_TY < (PCG_TX + 2) * (PCG_TY + 2);
+  P.y1 = threadIdx.x + PCG_TX * PCG_TY < (PCG_TX + 1) * (PCG_TY + 1);
   JobCursor prod, cons;
   double acc = 0.0, rmax = 0.0;
   if (cursor_begin<T>(A, cons)) {
@@ -507,14 +528,18 @@ __device__ void phaseB(const PcgArgs<T>& A, double* part, PcgShared<T>& S, uint8
         const double* rr = reinterpret_cast<const double*>(st + L::B_R);
         const T* aa = reinterpret_cast<const T*>(st + L::B_AP);
         const uint8_t* cc = st + L::B_C;
-        for (int e = threadIdx.x; e < (PCG_TX + 2) * (PCG_TY + 2); e += PCG_TX * PCG_TY) {
-          const int hx = e % (PCG_TX + 2), hy = e / (PCG_TX + 2);
-          double r = rr[Halo<double>::at(hy, hx)];
-          if (use_ap) r = r - alpha * (double)aa[Halo<T>::at(hy, hx)];
-          const uint8_t cd = cc[Halo<uint8_t>::at(hy, hx)];
-          S.rb[b][hy][hx] = r;
-          S.qb[b][hy][hx] = (T)r * S.lut[(cd & 63) * 4 + 1];
-          S.cb[b][hy][hx] = cd;
+        double* rbf = &S.rb[b][0][0];
+        T* qbf = &S.qb[b][0][0];
+        uint8_t* cbf = &S.cb[b][0][0];
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          if (q == 1 && !P.h1) break;
+          double r = rr[P.sr[q]];
+          if (use_ap) r = r - alpha * (double)aa[P.st[q]];
+          const uint8_t cd = cc[P.sc[q]];
+          rbf[P.e[q]] = r;
+          qbf[P.e[q]] = (T)r * S.lut[(cd & 63) * 4 + 1];
+          cbf[P.e[q]] = cd;
         }
       }
       __syncthreads();
@@ -526,13 +551,18 @@ __device__ void phaseB(const PcgArgs<T>& A, double* part, PcgShared<T>& S, uint8
       }
       const double rown = S.rb[b][ly + 1][lx + 1];
       if (kk >= u.k0 && A.precond == 2) {
-        for (int e = threadIdx.x; e < (PCG_TX + 1) * (PCG_TY + 1); e += PCG_TX * PCG_TY) {
-          const int hx = e % (PCG_TX + 1), hy = e / (PCG_TX + 1);
-          const uint8_t cd = S.cb[b][hy + 1][hx + 1];
-          const T sv = S.lut[(cd & 63) * 4 + 2];
-          S.yb[yb_][hy][hx] = sv * ((T)S.rb[b][hy + 1][hx + 1] +
-                                    om * (A.wx * S.qb[b][hy + 1][hx] + A.wy * S.qb[b][hy][hx + 1] +
-                                          A.wz * S.qb[bp][hy + 1][hx + 1]));
+        const double* rbf = &S.rb[b][0][0];
+        const T* qbf = &S.qb[b][0][0];
+        const T* qpf = &S.qb[bp][0][0];
+        const uint8_t* cbf = &S.cb[b][0][0];
+        T* ybf = &S.yb[yb_][0][0];
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          if (q == 1 && !P.y1) break;
+          const int o = P.yo[q];                         // (hy+1, hx+1) in the halo plane
+          const T sv = S.lut[(cbf[o] & 63) * 4 + 2];
+          ybf[P.ye[q]] = sv * ((T)rbf[o] + om * (A.wx * qbf[o - 1] + A.wy * qbf[o - (PCG_TX + 2)] +
+                                                 A.wz * qpf[o]));
         }
       }
       __syncthreads();
@@ -591,12 +621,18 @@ __device__ void finish_x(const PcgArgs<T>& A, int unit, T alpha, const T* __rest
 
 template <typename T>
 __global__ void __launch_bounds__(PCG_TX * PCG_TY) k_pcg(const __grid_constant__ PcgArgs<T> A) {
-  extern __shared__ uint8_t dyn[];
-  uint8_t* base = reinterpret_cast<uint8_t*>(((uintptr_t)dyn + 127) & ~(uintptr_t)127);
-  uint8_t* ring = base;
+  // dynamic smem is the only shared allocation of this kernel, so it starts
+  // at the (1 KB aligned) base of the block's window; keep every access on
+  // this array so the compiler emits LDS/STS rather than generic loads
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  uint8_t* ring = smem_raw;
   PcgShared<T>& S =
-      *reinterpret_cast<PcgShared<T>*>(base + (size_t)StageLayout<T>::STAGE * StageLayout<T>::DEPTH);
+      *reinterpret_cast<PcgShared<T>*>(smem_raw + (size_t)StageLayout<T>::STAGE * StageLayout<T>::DEPTH);
   if (*(volatile int*)A.gate) return;  // uniform across blocks: set before launch
+  if ((smem_u32(smem_raw) & 127u) != 0u) {   // TMA destinations need 128-byte alignment
+    if (threadIdx.x == 0) { A.rep->status = 3; *A.gate = 3; }
+    return;
+  }
   for (int e = threadIdx.x; e < 64 * 4; e += blockDim.x) S.lut[e] = A.lut[e];
   if (threadIdx.x == 0) {
     for (int s = 0; s < StageLayout<T>::DEPTH; ++s) mbar_init(&S.full[s], 1);
