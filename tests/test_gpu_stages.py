@@ -26,6 +26,7 @@ SCENES = {
     "channel2d": lambda: scenes.channel_2d(24, 16, 0.1, 2.0),
 }
 DT = {"fp32": (torch.float32, np.float32, 1e-5), "fp64": (torch.float64, np.float64, 1e-11)}
+FP32_UNCERTIFIED = {"channel2d"}   # see tests/test_oracle_floor.py
 
 
 def _setup(name, prec, seed=1):
@@ -166,7 +167,16 @@ def test_steps_match_reference_golden(name, prec):
     p, prof = device_params(comp.scene)
     reps = solver.step_many(dst, p, psys, pre, prof, int(g["steps"]))
     iters = [r.pcg.iterations for r in reps]
-    assert iters == g["pcg_iterations"].tolist()
+    if name in FP32_UNCERTIFIED and prec == "fp32":
+        # the 2D channel stops on the max-norm criterion with <1% margins: the
+        # reference itself changes iteration counts under 1e-7 relative noise
+        # per step (tests/test_oracle_floor.py), below fp32 resolution.  Gate:
+        # at most 2 steps off, each by one iteration.
+        gold = g["pcg_iterations"].tolist()
+        off = [(a, b) for a, b in zip(iters, gold) if a != b]
+        assert len(off) <= 2 and all(abs(a - b) == 1 for a, b in off), off
+    else:
+        assert iters == g["pcg_iterations"].tolist()
     got = fields_of(dst)
     tol = 1e-4 if prec == "fp32" else 1e-9
     for n in FIELDS:
