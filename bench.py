@@ -1,0 +1,371 @@
+"""Benchmark: RANS cell-steps/s on the C3 block city (256x256x64), one JSON line.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+N=1 runs one C3 simulation on cuda:0.  N>1 (torchrun, one process per GPU)
+runs one independent C3 design per GPU -- the optimizer's design-per-GPU
+axis (no data-path collective), weak scaling; the timed region is bracketed
+by barriers and the max over ranks is reported.  ``--impl reference`` times
+the reference algorithm's CPU path (the oracle port, oracle/) on the host
+cores over bounded samples of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+_argv = sys.argv[1:]
+if "--impl" in _argv and "reference" in _argv:
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", str(os.cpu_count() or 1))
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "RANS cell-steps/sec at 256x256x64 (C3 block city)"
+UNIT = "cell-steps/s"
+PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
+# algorithmic bytes: per step 164*N + 44*I*Nu (+8*Nu); the PCG
+# launch moves 20*N (divergence -> r0) + 8*Nu (z0 = W r0) + 44*I*Nu
+PCG_B_PER_UNKNOWN_ITER = 44
+# mean PCG iterations per step of the C3 scene over steps 3..12 (device run,
+# equal to the reference's counts by the parity gates) -- used only to
+# extrapolate the CPU reference's bounded samples to a full step
+REF_ITERS_PER_STEP = 149.5
+
+
+def c3_doc(dt):
+    from paper_2204_01117_b200 import scenes
+    return scenes.block_city(256, 256, 64, 2.0, 0, 6, dt)
+
+
+def hbm_peak():
+    try:
+        with open(PEAKS_FILE) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# ---------------------------------------------------------------------------
+# clocks sampled during the timed region
+
+class ClockSampler:
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.sw_power_cap,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown")
+
+    def __init__(self, gpu_index):
+        self.idx = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                          "-lms", "100", "-i", str(self.idx)], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ("sw_power_cap", "hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown")
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline: the oracle port on bounded samples of the C3 step
+
+class OracleSampler:
+    """Times the reference algorithm (oracle/ port, numpy+scipy CSR) on the
+    full C3 grid: the non-projection stages of one step, and M PCG
+    iterations (A.p, W.r, dots, axpys exactly as pcg_solve).  A full step
+    is extrapolated as t_stages + t_iter * I."""
+
+    def __init__(self, doc):
+        from oracle import citywind_oracle as co
+        self.co = co
+        t0 = time.perf_counter()
+        self.comp = co.Compiled(co.scene_from_dict(doc))
+        self.state = self.comp.make_state()
+        self.setup_s = time.perf_counter() - t0
+        self.n = self.state.labels.size
+        self.nu = self.comp.psys.n
+
+    def stages(self):
+        co, st, sc = self.co, self.state, self.comp.scene
+        dt = sc.params.dt
+        t0 = time.perf_counter()
+        k_new = co.upwind_scalar(st, st.k, dt)
+        om_new = co.upwind_scalar(st, st.omega, dt)
+        st.u, st.v, st.w = co.advect_velocity(st, dt)
+        st.k, st.omega = k_new, om_new
+        co.diffuse(st, sc.params, dt)
+        co.apply_drag(st, sc.params, dt)
+        co.apply_boundary_conditions(st, sc.inlet, sc.params)
+        b = -co.divergence(st)[self.comp.psys.unknown] / dt
+        co.update_turbulence(st, sc.params, dt)
+        co.apply_boundary_conditions(st, sc.inlet, sc.params)
+        self.b = b
+        return time.perf_counter() - t0
+
+    def pcg_iters(self, m):
+        A, W, b = self.comp.psys.A, self.comp.W, self.b
+        x = np.zeros_like(b)
+        r = b.copy()
+        z = W @ r
+        rz = float(r @ z)
+        p = z.copy()
+        t0 = time.perf_counter()
+        for _ in range(m):
+            Ap = A @ p
+            alpha = rz / float(p @ Ap)
+            x += alpha * p
+            r -= alpha * Ap
+            z = W @ r
+            rz_new = float(r @ z)
+            p = z + (rz_new / rz) * p
+            rz = rz_new
+        return (time.perf_counter() - t0) / m
+
+    def sample(self, m=8):
+        ts = self.stages()
+        ti = self.pcg_iters(m)
+        step_s = ts + ti * REF_ITERS_PER_STEP
+        return self.n / step_s, ts, ti
+
+
+def cpu_threads():
+    return int(os.environ.get("OPENBLAS_NUM_THREADS", "0") or 0) or (os.cpu_count() or 1)
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    doc = c3_doc(args.dt)
+    smp = OracleSampler(doc)
+    for _ in range(args.warmup):
+        smp.sample(4)
+    vals, tstage, titer = [], [], []
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        v, ts, ti = smp.sample(4)
+        vals.append(v)
+        tstage.append(ts)
+        titer.append(ti)
+    wall = time.perf_counter() - t0
+    value = float(np.mean(vals))
+    cores = cpu_threads()
+    sample = (f"per step: the C3 step's non-projection stages on the full 256x256x64 grid "
+              f"(mean {np.mean(tstage):.2f} s) + 4 PCG iterations (mean {np.mean(titer):.3f} s/iteration), "
+              f"extrapolated to {REF_ITERS_PER_STEP} iterations/step; oracle/ numpy+scipy port, "
+              f"OpenBLAS ddot on {cores} threads, CSR matvec single-threaded")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * doc_cells(doc) / value,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": "C3 block city 256x256x64, seed 0, 52 objects",
+                                            "dt": args.dt},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "wall_s": wall}
+    print(json.dumps(line), flush=True)
+
+
+def doc_cells(doc):
+    g = doc["grid"]
+    return g["nx"] * g["ny"] * g["nz"]
+
+
+# ---------------------------------------------------------------------------
+# the B200 arm
+
+def run_b200(args):
+    import ctypes as C
+
+    import torch
+
+    from paper_2204_01117_b200 import _native as N
+    from paper_2204_01117_b200 import solver
+    from paper_2204_01117_b200.scenario import CompiledScenario, scenario_from_dict
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    doc = c3_doc(args.dt)
+    ncell = doc_cells(doc)
+    sc = scenario_from_dict(doc)
+    comp = CompiledScenario.compile(sc, dtype=torch.float32)
+    t0 = time.perf_counter()
+    state = comp.make_state()
+    torch.cuda.synchronize()
+    voxelize_s = time.perf_counter() - t0
+    nu = comp.psys.n
+
+    # warm-up (untimed)
+    comp.step_states(state, args.warmup)
+    lib = N.lib()
+    ctx = solver._acquire(comp.psys, comp.preconditioner, state)
+    comp.psys.pool.release(ctx)
+    N.check(lib.cw_pcg_timing(ctx.h, args.steps))
+    lib.cw_launch_count(ctx.h, 1)
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clocks:
+        ev0.record()
+        solver.step_many(state, sc.solver, comp.psys, comp.preconditioner, sc.inlet, args.steps,
+                         sc.pcg_tol, read_back=False)
+        ev1.record()
+        torch.cuda.synchronize()
+    barrier()
+    ms = ev0.elapsed_time(ev1)
+    launches = int(lib.cw_launch_count(ctx.h, 1))
+    reps = solver.finish(state, comp.psys, comp.preconditioner, args.steps)
+    iters = [r.pcg.iterations for r in reps]
+    pcg_ms = (C.c_float * args.steps)()
+    got = C.c_int()
+    N.check(lib.cw_read_pcg_timing(ctx.h, pcg_ms, args.steps, C.byref(got)))
+    pcg_ms = np.array(pcg_ms[:got.value], float)
+    ms_max = ms
+    if dist is not None:
+        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_max = float(t.item())
+    value = world * ncell * args.steps / (ms_max * 1e-3)
+
+    # roofline of the dominant kernel (k_pcg)
+    peak, peak_kind = hbm_peak()
+    bytes_per_launch = [20.0 * ncell + 8.0 * nu + PCG_B_PER_UNKNOWN_ITER * i * nu for i in iters[:len(pcg_ms)]]
+    achieved = float(np.sum(bytes_per_launch) / (np.sum(pcg_ms) * 1e-3) / 1e9) if len(pcg_ms) else None
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "pcg_dram_bytes.json")
+    if os.path.exists(prof):
+        with open(prof) as fh:
+            traffic = json.load(fh).get("dram_bytes_per_launch")
+    roofline = {"kernel": "k_pcg<float> (whole warm-started PCG, one cooperative launch per step)",
+                "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak if achieved else None, "traffic": traffic,
+                "peak_source": f"{peak_kind} copy bandwidth (MEASURED_PEAKS.json hbm_gbs)",
+                "bytes_model": "20*N + 8*Nu + 44*I*Nu per launch (SURVEY.md 8d, fp32 vectors)",
+                "pcg_ms_per_launch": float(np.mean(pcg_ms)) if len(pcg_ms) else None,
+                "pcg_share_of_step": float(np.sum(pcg_ms) / ms) if len(pcg_ms) else None}
+
+    # end to end through the reference-facing API: host state in, host state out
+    names = ("u", "v", "w", "p", "k", "omega", "nu_t")
+    host = {n: torch.empty(state.fields[n].shape, dtype=state.fields[n].dtype, pin_memory=True) for n in names}
+    for n in names:
+        host[n].copy_(state.fields[n])
+    k_e2e = max(1, min(args.steps, 5))
+    torch.cuda.synchronize()
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(k_e2e):
+        for n in names:
+            state.fields[n].copy_(host[n], non_blocking=True)
+        solver.step(state, sc.solver, comp.psys, comp.preconditioner, sc.inlet, pcg_tol=sc.pcg_tol)
+        for n in names:
+            host[n].copy_(state.fields[n], non_blocking=True)
+        torch.cuda.synchronize()
+    e2e_s = time.perf_counter() - t0
+    if dist is not None:
+        t = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    xfer = sum(int(host[n].numel() * host[n].element_size()) for n in names)
+    e2e = {"value": world * ncell * k_e2e / e2e_s, "unit": UNIT, "h2d_bytes_per_step": xfer,
+           "d2h_bytes_per_step": xfer,
+           "path": "solver.step() on a host-resident state: 7 fields pinned H2D, step, 7 fields D2H, per step"}
+
+    kmax = float(state.fields["k"].max())
+    if rank != 0:
+        if dist is not None:
+            dist.destroy_process_group()
+        return
+    cpu = None
+    if world == 1 and not args.no_cpu:
+        smp = OracleSampler(doc)
+        v, ts, ti = smp.sample(4)
+        cpu = {"value": v, "unit": UNIT, "cores": 1, "kind": "port",
+               "sample": (f"oracle/ numpy+scipy port on the full C3 grid: non-projection stages of one step "
+                          f"({ts:.2f} s) + 4 PCG iterations ({ti:.3f} s each), extrapolated to "
+                          f"{np.mean(iters):.1f} iterations/step (this run's mean); setup {smp.setup_s:.1f} s")}
+        cpu["value"] = smp.n / (ts + ti * float(np.mean(iters)))
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": "C3 block city 256x256x64, seed 0, 36 buildings + 16 trees, dt %.2f" % args.dt,
+                       "cells": ncell, "unknowns": nu, "parallelism": f"design-per-GPU x{world}",
+                       "l2": "inputs larger than L2: ~250 MB state+workspace per step > 126 MB L2",
+                       "precision": "fp32 fields; PCG residual and dot products in fp64"},
+            "e2e": e2e, "gpu_launches": launches, "roofline": roofline, "cpu_baseline": cpu,
+            "clocks": clocks.summary(), "pcg_iterations": iters, "voxelize_s": voxelize_s,
+            "k_max_end": kmax}
+    print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--dt", type=float, default=0.5)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_b200(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -141,6 +141,13 @@ int cw_read_reports(cw_ctx *ctx, cw_report *out, int n, int *n_out, void *stream
 int cw_set_stage_timing(cw_ctx *ctx, int enabled);
 int cw_read_stage_timings(cw_ctx *ctx, float out_ms[7]);
 
+/* Evidence hooks for the benchmark: device time of each PCG launch
+ * (CUDA events on the launching stream, first max_launches launches after
+ * the call), and the number of kernels this context has enqueued. */
+int cw_pcg_timing(cw_ctx *ctx, int max_launches);
+int cw_read_pcg_timing(cw_ctx *ctx, float *ms, int n, int *n_out);
+long long cw_launch_count(cw_ctx *ctx, int reset);
+
 /* region_average_speed (ref solver.py:535-549) for n boxes in one pass:
  * mean cell-centred speed over AIR cells whose centres lie in [lo, hi];
  * count_out[b] = 0 means "region contains no air cells". Deterministic. */

@@ -37,7 +37,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     objs = []
     for src in SOURCES:
         obj = os.path.join(HERE, "csrc", os.path.basename(src).replace(".cu", ".o"))
-        cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
+        extra = ["-fmad=false"] if "voxel" in src else []   # numpy never fuses: no FMA contraction
+        cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", *extra,
                "--expt-relaxed-constexpr", "-Xptxas", "-v" if verbose else "-O3",
                "-c", os.path.join(HERE, src), "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)

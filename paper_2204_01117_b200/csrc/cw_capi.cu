@@ -83,9 +83,24 @@ struct cw_ctx {
   cudaEvent_t ev[8] = {};
   bool ev_made = false;
   float stage_ms[7] = {0, 0, 0, 0, 0, 0, 0};
+  long long launches = 0;             // kernels enqueued (evidence for the bench's gpu_launches)
+  // per-launch device time of the PCG kernel (bench roofline), when enabled
+  std::vector<cudaEvent_t> pev;
+  int pcg_timed = 0;
 };
 
 extern "C" int cw_abi_version(void) { return CW_ABI_VERSION; }
+
+// shared with cw_voxel.cu
+int cw_internal_fail(int code, const char* msg) { return fail(code, msg); }
+int cw_internal_device(cw_ctx* c, int* nx, int* ny, int* nz, double* h, double* origin) {
+  cudaError_t e = cudaSetDevice(c->device);
+  if (e != cudaSuccess) return fail(CW_ERR_CUDA, cudaGetErrorString(e));
+  *nx = c->d.nx; *ny = c->d.ny; *nz = c->d.nz;
+  h[0] = c->grid.dx; h[1] = c->grid.dy; h[2] = c->grid.dz;
+  for (int a = 0; a < 3; ++a) origin[a] = c->grid.origin[a];
+  return CW_OK;
+}
 extern "C" const char* cw_last_error(void) { return g_err.c_str(); }
 
 static int alloc(void** p, size_t bytes) {
@@ -229,6 +244,7 @@ extern "C" void cw_ctx_destroy(cw_ctx* c) {
     if (p) cudaFree(p);
   if (c->ev_made)
     for (auto& e : c->ev) cudaEventDestroy(e);
+  for (auto& e : c->pev) cudaEventDestroy(e);
   delete c;
 }
 
@@ -268,10 +284,10 @@ extern "C" int cw_set_operator(cw_ctx* c, const signed char* lab, double ai_omeg
   }
   CW_CUDA(cudaMemsetAsync(c->flag, 0, 4 * sizeof(int), S(stream)));
   const int nb = std::min(nblk(c->ncell), 1024);
-  k_build_code<<<nb, 256, 0, S(stream)>>>(d, c->nxp, (const int8_t*)lab, c->code, c->flag);
+  (k_build_code<<<nb, 256, 0, S(stream)>>>(d, c->nxp, (const int8_t*)lab, c->code, c->flag), ++c->launches);
   CW_CUDA(cudaGetLastError());
-  k_wdiag_partials<<<nb, 256, 0, S(stream)>>>(d, c->nxp, c->code, w[0], w[1], w[2], ai_omega, c->reg_part, c->reg_cnt,
-                                               c->reg_part + 1024);
+  (k_wdiag_partials<<<nb, 256, 0, S(stream)>>>(d, c->nxp, c->code, w[0], w[1], w[2], ai_omega, c->reg_part, c->reg_cnt,
+                                               c->reg_part + 1024), ++c->launches);
   CW_CUDA(cudaGetLastError());
   std::vector<double> parts(nb), jparts(nb);
   std::vector<long long> cnts(nb);
@@ -309,9 +325,9 @@ extern "C" int cw_drag_coefficient(cw_ctx* c, const double* phi, const double* l
   CW_CUDA(cudaSetDevice(c->device));
   CW_CUDA(cudaMemsetAsync(c->flag, 0, sizeof(int), S(stream)));
   if (c->prec == 4)
-    k_drag_coef<float><<<nblk(c->ncell), 256, 0, S(stream)>>>(c->ncell, phi, lad, (const int8_t*)lab, *prm, (float*)g, c->flag);
+    (k_drag_coef<float><<<nblk(c->ncell), 256, 0, S(stream)>>>(c->ncell, phi, lad, (const int8_t*)lab, *prm, (float*)g, c->flag), ++c->launches);
   else
-    k_drag_coef<double><<<nblk(c->ncell), 256, 0, S(stream)>>>(c->ncell, phi, lad, (const int8_t*)lab, *prm, (double*)g, c->flag);
+    (k_drag_coef<double><<<nblk(c->ncell), 256, 0, S(stream)>>>(c->ncell, phi, lad, (const int8_t*)lab, *prm, (double*)g, c->flag), ++c->launches);
   CW_CUDA(cudaGetLastError());
   int f = 0;
   CW_CUDA(cudaMemcpyAsync(&f, c->flag, sizeof(int), cudaMemcpyDeviceToHost, S(stream)));
@@ -359,11 +375,11 @@ static void launch_bc(cw_ctx* c, BcFields<T> F, const int8_t* lab, const cw_para
     const int ext = axis == 0 ? d.nx : (axis == 1 ? d.ny : d.nz);
     const int pos = (s & 1) ? ext - 1 : 0;
     const int e1 = axis == 0 ? d.ny : d.nx, e2 = axis == 2 ? d.ny : d.nz;
-    k_bc_outlet_side<T><<<nblk((long long)(e1 + 1) * (e2 + 1)), 256, 0, st>>>(d, axis, pos, F, lab, c->gate);
+    (k_bc_outlet_side<T><<<nblk((long long)(e1 + 1) * (e2 + 1)), 256, 0, st>>>(d, axis, pos, F, lab, c->gate), ++c->launches);
   }
   const long long n = c->ncell + c->nu_ + c->nv_ + (d.is2d ? 0 : c->nw_);
-  k_bc_inlet_wall<T><<<nblk(n), 256, 0, st>>>(d, F, lab, (const T*)c->uzx, (const T*)c->uzy, (T)prm->k_in,
-                                              (T)prm->omega_in, (T)(prm->k_in / prm->omega_in), c->gate);
+  (k_bc_inlet_wall<T><<<nblk(n), 256, 0, st>>>(d, F, lab, (const T*)c->uzx, (const T*)c->uzy, (T)prm->k_in,
+                                              (T)prm->omega_in, (T)(prm->k_in / prm->omega_in), c->gate), ++c->launches);
 }
 
 extern "C" int cw_apply_boundary(cw_ctx* c, const cw_fields* f, const cw_params* prm, const cw_inlet* inl,
@@ -443,11 +459,11 @@ static void st_advect(cw_ctx* c, const StepPtrs<T>& P, const cw_params* prm, T* 
   const long long nf[3] = {c->nu_, c->nv_, c->nw_};
   const int ncomp = d.is2d ? 2 : 3;
   if (prm->turbulence)
-    k_upwind<T><<<nblk(c->ncell), 256, 0, st>>>(d, P.u, P.v, P.w, P.k, P.om, kout, wout, dt, c->gate);
+    (k_upwind<T><<<nblk(c->ncell), 256, 0, st>>>(d, P.u, P.v, P.w, P.k, P.om, kout, wout, dt, c->gate), ++c->launches);
   for (int a = 0; a < ncomp; ++a)
-    k_mac_predict<T><<<nblk(nf[a]), 256, 0, st>>>(d, a, P.u, P.v, P.w, (T*)c->ahead[a], dt, c->gate);
+    (k_mac_predict<T><<<nblk(nf[a]), 256, 0, st>>>(d, a, P.u, P.v, P.w, (T*)c->ahead[a], dt, c->gate), ++c->launches);
   for (int a = 0; a < ncomp; ++a)
-    k_mac_correct<T><<<nblk(nf[a]), 256, 0, st>>>(d, a, P.u, P.v, P.w, (const T*)c->ahead[a], (T*)c->adv[a], dt, c->gate);
+    (k_mac_correct<T><<<nblk(nf[a]), 256, 0, st>>>(d, a, P.u, P.v, P.w, (const T*)c->ahead[a], (T*)c->adv[a], dt, c->gate), ++c->launches);
 }
 
 template <typename T>
@@ -458,8 +474,8 @@ static void st_diffuse(cw_ctx* c, const StepPtrs<T>& P, const cw_params* prm, cu
   double cap = nu_stable<T>(c, prm->dt) - prm->nu;
   if (cap <= 0) cap = 0.0;                               // solver.py:195-201
   for (int a = 0; a < (d.is2d ? 2 : 3); ++a)
-    k_diffuse<T><<<nblk(nf[a]), 256, 0, st>>>(d, a, (const T*)c->adv[a], cu[a], P.nut, (T)prm->dt,
-                                               (T)prm->nu, (T)cap, c->gate);
+    (k_diffuse<T><<<nblk(nf[a]), 256, 0, st>>>(d, a, (const T*)c->adv[a], cu[a], P.nut, (T)prm->dt,
+                                               (T)prm->nu, (T)cap, c->gate), ++c->launches);
 }
 
 template <typename T>
@@ -468,9 +484,9 @@ static void st_drag(cw_ctx* c, const StepPtrs<T>& P, const cw_params* prm, int h
   const Dims& d = c->d;
   const long long nf[3] = {c->nu_, c->nv_, c->nw_};
   T* cu[3] = {P.u, P.v, P.w};
-  k_cell_speed<T><<<nblk(c->ncell), 256, 0, st>>>(d, P.u, P.v, P.w, (T*)c->speed, c->gate);
+  (k_cell_speed<T><<<nblk(c->ncell), 256, 0, st>>>(d, P.u, P.v, P.w, (T*)c->speed, c->gate), ++c->launches);
   for (int a = 0; a < (d.is2d ? 2 : 3); ++a)
-    k_drag<T><<<nblk(nf[a]), 256, 0, st>>>(d, a, cu[a], P.g, (const T*)c->speed, (T)prm->dt, c->gate);
+    (k_drag<T><<<nblk(nf[a]), 256, 0, st>>>(d, a, cu[a], P.g, (const T*)c->speed, (T)prm->dt, c->gate), ++c->launches);
 }
 
 template <typename T>
@@ -479,11 +495,15 @@ static int st_project(cw_ctx* c, const StepPtrs<T>& P, const cw_fields* f, const
   const Dims& d = c->d;
   const long long nf[3] = {c->nu_, c->nv_, c->nw_};
   T* cu[3] = {P.u, P.v, P.w};
+  const bool tpcg = c->pcg_timed < (int)c->pev.size() / 2;
+  if (tpcg) cudaEventRecord(c->pev[2 * c->pcg_timed], st);
   int rc = launch_pcg<T>(c, f, rep, prm->dt, tol, st);
+  ++c->launches;
+  if (tpcg) cudaEventRecord(c->pev[2 * c->pcg_timed++ + 1], st);
   if (rc) return rc;
   for (int a = 0; a < (d.is2d ? 2 : 3); ++a)
-    k_gradient<T><<<nblk(nf[a]), 256, 0, st>>>(d, a, cu[a], P.p, P.lab, (T)prm->dt, c->gate);
-  k_div_max<T><<<nblk(c->ncell), 256, 0, st>>>(d, P.u, P.v, P.w, P.lab, rep, SLOT_DIV_AFTER, c->gate);
+    (k_gradient<T><<<nblk(nf[a]), 256, 0, st>>>(d, a, cu[a], P.p, P.lab, (T)prm->dt, c->gate), ++c->launches);
+  (k_div_max<T><<<nblk(c->ncell), 256, 0, st>>>(d, P.u, P.v, P.w, P.lab, rep, SLOT_DIV_AFTER, c->gate), ++c->launches);
   return CW_OK;
 }
 
@@ -497,8 +517,8 @@ static void st_turb(cw_ctx* c, const StepPtrs<T>& P, const cw_params* prm, const
   sc.c_mu = prm->c_mu; sc.alpha = prm->alpha; sc.beta = prm->beta;
   sc.sigma = prm->sigma; sc.sigma_star = prm->sigma_star; sc.c_lim = prm->c_lim;
   sc.k_in = prm->k_in; sc.om_in = prm->omega_in; sc.nut_in = prm->k_in / prm->omega_in;
-  k_turbulence<T><<<nblk(c->ncell), 256, 0, st>>>(c->d, P.u, P.v, P.w, kin, win, P.k, P.om, P.nut, sc, rep, c->gate);
-  k_turb_check<<<1, 1, 0, st>>>(rep, c->gate);
+  (k_turbulence<T><<<nblk(c->ncell), 256, 0, st>>>(c->d, P.u, P.v, P.w, kin, win, P.k, P.om, P.nut, sc, rep, c->gate), ++c->launches);
+  (k_turb_check<<<1, 1, 0, st>>>(rep, c->gate), ++c->launches);
 }
 
 template <typename T>
@@ -517,7 +537,7 @@ static int enqueue_step(cw_ctx* c, const cw_fields* f, const cw_params* prm, dou
   const StepPtrs<T> P = ptrs_of<T>(f);
   const bool turb = prm->turbulence != 0;
   auto mark = [&](int i) { if (c->timing) cudaEventRecord(c->ev[i], st); };
-  k_report_init<<<1, 1, 0, st>>>(rep);
+  (k_report_init<<<1, 1, 0, st>>>(rep), ++c->launches);
   mark(0);
   st_advect<T>(c, P, prm, (T*)c->tk, (T*)c->tw, st);        // "advect"
   mark(1);
@@ -537,7 +557,7 @@ static int enqueue_step(cw_ctx* c, const cw_fields* f, const cw_params* prm, dou
   mark(6);
   BcFields<T> F2{P.u, P.v, P.w, P.p, P.k, P.om, P.nut};
   launch_bc<T>(c, F2, P.lab, prm, st);                        // "boundary2"
-  k_speed_max<T><<<nblk(c->nu_ + c->nv_ + c->nw_), 256, 0, st>>>(c->nu_, c->nv_, c->nw_, P.u, P.v, P.w, rep, c->gate);
+  (k_speed_max<T><<<nblk(c->nu_ + c->nv_ + c->nw_), 256, 0, st>>>(c->nu_, c->nv_, c->nw_, P.u, P.v, P.w, rep, c->gate), ++c->launches);
   mark(7);
   CW_CUDA(cudaGetLastError());
   return CW_OK;
@@ -554,7 +574,7 @@ static int enqueue_stage(cw_ctx* c, const cw_fields* f, const cw_params* prm, in
   const size_t fb[3] = {c->nu_ * sizeof(T), c->nv_ * sizeof(T), c->nw_ * sizeof(T)};
   T* cu[3] = {P.u, P.v, P.w};
   const int ncomp = d.is2d ? 2 : 3;
-  k_report_init<<<1, 1, 0, st>>>(rep);
+  (k_report_init<<<1, 1, 0, st>>>(rep), ++c->launches);
   switch (stage) {
     case CW_STAGE_ADVECT:
       st_advect<T>(c, P, prm, (T*)c->tk, (T*)c->tw, st);
@@ -706,6 +726,36 @@ extern "C" int cw_set_preconditioner(cw_ctx* c, int kind, double* tol_default) {
   return CW_OK;
 }
 
+extern "C" int cw_pcg_timing(cw_ctx* c, int max_launches) {
+  if (!c || max_launches < 0) return fail(CW_ERR_INVALID, "bad argument");
+  CW_CUDA(cudaSetDevice(c->device));
+  for (auto& e : c->pev) cudaEventDestroy(e);
+  c->pev.assign(2 * (size_t)max_launches, nullptr);
+  for (auto& e : c->pev) CW_CUDA(cudaEventCreate(&e));
+  c->pcg_timed = 0;
+  return CW_OK;
+}
+
+extern "C" int cw_read_pcg_timing(cw_ctx* c, float* ms, int n, int* n_out) {
+  if (!c) return fail(CW_ERR_INVALID, "null argument");
+  CW_CUDA(cudaSetDevice(c->device));
+  const int m = std::min(n, c->pcg_timed);
+  for (int i = 0; i < m; ++i) {
+    CW_CUDA(cudaEventSynchronize(c->pev[2 * i + 1]));
+    CW_CUDA(cudaEventElapsedTime(&ms[i], c->pev[2 * i], c->pev[2 * i + 1]));
+  }
+  if (n_out) *n_out = m;
+  c->pcg_timed = 0;
+  return CW_OK;
+}
+
+extern "C" long long cw_launch_count(cw_ctx* c, int reset) {
+  if (!c) return -1;
+  const long long v = c->launches;
+  if (reset) c->launches = 0;
+  return v;
+}
+
 extern "C" int cw_set_stage_timing(cw_ctx* c, int enabled) {
   if (!c) return fail(CW_ERR_INVALID, "null argument");
   c->timing = enabled != 0;
@@ -731,12 +781,12 @@ extern "C" int cw_region_speed(cw_ctx* c, const cw_fields* f, int n, const doubl
     for (int a = 0; a < 3; ++a) { B.lo[b][a] = lo[3 * b + a]; B.hi[b][a] = hi[3 * b + a]; }
   const int nb = std::min(nblk(c->ncell), 1024);
   if (c->prec == 4)
-    k_region_partials<float><<<nb, 256, 0, S(stream)>>>(c->d, c->grid.origin[0], c->grid.origin[1], c->grid.origin[2],
-        (const float*)f->u, (const float*)f->v, (const float*)f->w, (const int8_t*)f->labels, B, c->reg_part, c->reg_cnt);
+    (k_region_partials<float><<<nb, 256, 0, S(stream)>>>(c->d, c->grid.origin[0], c->grid.origin[1], c->grid.origin[2],
+        (const float*)f->u, (const float*)f->v, (const float*)f->w, (const int8_t*)f->labels, B, c->reg_part, c->reg_cnt), ++c->launches);
   else
-    k_region_partials<double><<<nb, 256, 0, S(stream)>>>(c->d, c->grid.origin[0], c->grid.origin[1], c->grid.origin[2],
-        (const double*)f->u, (const double*)f->v, (const double*)f->w, (const int8_t*)f->labels, B, c->reg_part, c->reg_cnt);
-  k_region_fold<<<1, 64, 0, S(stream)>>>(nb, n, c->reg_part, c->reg_cnt, c->reg_out, c->reg_cout);
+    (k_region_partials<double><<<nb, 256, 0, S(stream)>>>(c->d, c->grid.origin[0], c->grid.origin[1], c->grid.origin[2],
+        (const double*)f->u, (const double*)f->v, (const double*)f->w, (const int8_t*)f->labels, B, c->reg_part, c->reg_cnt), ++c->launches);
+  (k_region_fold<<<1, 64, 0, S(stream)>>>(nb, n, c->reg_part, c->reg_cnt, c->reg_out, c->reg_cout), ++c->launches);
   CW_CUDA(cudaGetLastError());
   CW_CUDA(cudaMemcpyAsync(mean_out, c->reg_out, n * sizeof(double), cudaMemcpyDeviceToHost, S(stream)));
   CW_CUDA(cudaMemcpyAsync(count_out, c->reg_cout, n * sizeof(long long), cudaMemcpyDeviceToHost, S(stream)));

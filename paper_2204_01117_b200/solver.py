@@ -450,3 +450,37 @@ def region_average_speed(state: FlowState, box_lo, box_hi,
     if counts[0] == 0:
         raise ValueError("region contains no air cells")
     return float(means[0])
+
+
+def _gather_point(t: torch.Tensor, fx: float, fy: float, fz: float) -> float:
+    """Trilinear sample of an x-fastest device array at fractional (x, y, z),
+    indices clamped like advection.py:49-101 (8 device reads)."""
+    nz, ny, nx = t.shape
+
+    def split(f, n):
+        i0 = int(min(max(np.floor(f), 0), max(n - 2, 0)))
+        return i0, float(np.clip(f - i0, 0.0, 1.0)), (1 if n > 1 else 0)
+
+    i0, tx, sx = split(fx, nx)
+    j0, ty, sy = split(fy, ny)
+    k0, tz, sz = split(fz, nz)
+    c = t[k0:k0 + 1 + sz, j0:j0 + 1 + sy, i0:i0 + 1 + sx].double().cpu().numpy()
+    c = np.broadcast_to(c if c.shape == (2, 2, 2) else np.pad(c, [(0, 2 - c.shape[0]), (0, 2 - c.shape[1]),
+                                                              (0, 2 - c.shape[2])], mode="edge"), (2, 2, 2))
+    c00 = c[0, 0, 0] * (1 - tx) + c[0, 0, 1] * tx
+    c10 = c[0, 1, 0] * (1 - tx) + c[0, 1, 1] * tx
+    c01 = c[1, 0, 0] * (1 - tx) + c[1, 0, 1] * tx
+    c11 = c[1, 1, 0] * (1 - tx) + c[1, 1, 1] * tx
+    c0 = c00 * (1 - ty) + c10 * ty
+    c1 = c01 * (1 - ty) + c11 * ty
+    return float(c0 * (1 - tz) + c1 * tz)
+
+
+def probe_velocity(state: FlowState, pos) -> tuple:
+    """Velocity at a physical point (the probes of run_simulation,
+    scenario.py:473-478): staggered trilinear samples of u, v, w."""
+    g = state.grid
+    X, Y, Z = ((np.asarray(pos, float) - np.asarray(g.origin)) / g.spacing)
+    f = state.fields
+    return (_gather_point(f["u"], X, Y - 0.5, Z - 0.5), _gather_point(f["v"], X - 0.5, Y, Z - 0.5),
+            _gather_point(f["w"], X - 0.5, Y - 0.5, Z))
