@@ -36,7 +36,7 @@ PCG_B_PER_UNKNOWN_ITER = 44
 # mean PCG iterations per step of the C3 scene over steps 3..12 (device run,
 # equal to the reference's counts by the parity gates) -- used only to
 # extrapolate the CPU reference's bounded samples to a full step
-REF_ITERS_PER_STEP = 149.5
+REF_ITERS_PER_STEP = 143.0
 
 
 def c3_doc(dt):
@@ -356,7 +356,7 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--dt", type=float, default=0.5)
+    ap.add_argument("--dt", type=float, default=0.2)
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:

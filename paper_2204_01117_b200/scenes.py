@@ -165,7 +165,7 @@ def scaled(doc: dict, **grid) -> dict:
 CONFIGS = {
     "C1": lambda: cuboid(64, 64, 32, 2.0, 0.3, 200),
     "C2": lambda: canyon(128, 128, 64, 1.0, 0.2, 500),
-    "C3": lambda: block_city(256, 256, 64, 2.0, 0, 6, 0.5),
-    "C4": lambda: block_city_design(256, 256, 64, 2.0, 0, 6, 0.5),
-    "C5": lambda: block_city(512, 512, 128, 2.0, 0, 6, 0.5),
+    "C3": lambda: block_city(256, 256, 64, 2.0, 0, 6, 0.2),
+    "C4": lambda: block_city_design(256, 256, 64, 2.0, 0, 6, 0.2),
+    "C5": lambda: block_city(512, 512, 128, 2.0, 0, 6, 0.2),
 }
