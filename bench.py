@@ -284,9 +284,13 @@ def run_b200(args):
     achieved = float(np.sum(bytes_per_launch) / (np.sum(pcg_ms) * 1e-3) / 1e9) if len(pcg_ms) else None
     traffic = None
     prof = os.path.join(ROOT, "profiles", "pcg_dram_bytes.json")
-    if os.path.exists(prof):
+    if os.path.exists(prof) and bytes_per_launch:
+        # measured DRAM bytes of one captured launch, scaled by the ratio to
+        # its algorithmic bytes onto this run's mean launch
         with open(prof) as fh:
-            traffic = json.load(fh).get("dram_bytes_per_launch")
+            ratio = json.load(fh).get("traffic_over_algorithmic")
+        if ratio:
+            traffic = float(ratio * np.mean(bytes_per_launch))
     roofline = {"kernel": "k_pcg<float> (whole warm-started PCG, one cooperative launch per step)",
                 "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak if achieved else None, "traffic": traffic,
