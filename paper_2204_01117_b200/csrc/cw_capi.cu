@@ -116,7 +116,7 @@ static int pcg_occupancy(int* blocks_per_sm, size_t* smem) {
   *smem = pcg_smem_bytes<T>();
   cudaError_t e = cudaFuncSetAttribute(k_pcg<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)*smem);
   if (e != cudaSuccess) return fail(CW_ERR_CUDA, std::string("smem attribute: ") + cudaGetErrorString(e));
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_pcg<T>, TX * TY, *smem);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_pcg<T>, PCG_THREADS, *smem);
   if (e != cudaSuccess) return fail(CW_ERR_CUDA, std::string("occupancy: ") + cudaGetErrorString(e));
   return CW_OK;
 }
@@ -432,7 +432,7 @@ static int launch_pcg(cw_ctx* c, const cw_fields* f, DevReport* rep, double dt, 
   A.timeout_ns = 20LL * 1000 * 1000 * 1000;
   CW_CUDA(cudaMemsetAsync(c->bar, 0, 64 * sizeof(unsigned), st));
   void* args[] = {&A};
-  CW_CUDA(cudaLaunchCooperativeKernel((const void*)k_pcg<T>, dim3(c->pcg_blocks), dim3(TX * TY), args, c->pcg_smem, st));
+  CW_CUDA(cudaLaunchCooperativeKernel((const void*)k_pcg<T>, dim3(c->pcg_blocks), dim3(PCG_THREADS), args, c->pcg_smem, st));
   return CW_OK;
 }
 

@@ -17,9 +17,8 @@
 // unknowns) so that every (x,y)-tile-with-halo of one z-plane is a single
 // TMA box (cp.async.bulk.tensor.3d; out-of-range elements are zero-filled by
 // the hardware, which is exactly the operator's boundary rule).  Each block
-// marches its tiles through z; one thread keeps a DEPTH-stage shared-memory
-// ring of planes in flight (mbarrier complete_tx), so a block has DEPTH
-// planes of loads outstanding instead of one.
+// marches 32x32 tiles through z (4 rows per thread); one thread keeps a
+// DEPTH-stage shared-memory ring of planes in flight (mbarrier complete_tx).
 //
 // Each PCG iteration is two grid phases separated by a grid barrier that
 // also completes a deterministic fp64 reduction:
@@ -29,10 +28,10 @@
 //            partials r'.z and max|r'|
 // Storage: p, z, Ap, x in the state precision; r in float64 (a float32
 // recursive residual drifts by ~eps*|b| per iteration, several percent of the
-// max-norm target 10^-4.5 max|b|, which flips stopping decisions).  Partials
-// are kept per block over a fixed unit->block map and every block folds them
-// in the same fixed order: all blocks agree bit-for-bit on alpha/beta and
-// runs are deterministic.
+// max-norm target 10^-4.5 max|b|, which flips stopping decisions); A p is
+// evaluated in float64 arithmetic.  Partials are kept per block over a fixed
+// unit->block map and every block folds them in the same fixed order: all
+// blocks agree bit-for-bit on alpha/beta and runs are deterministic.
 #pragma once
 #include <cuda.h>
 
@@ -41,8 +40,13 @@
 
 namespace cw {
 
-constexpr int PCG_TX = 32, PCG_TY = 8;
+constexpr int PCG_TX = 32, PCG_TY = 32;                 // tile (cells)
+constexpr int PCG_THREADS = 256;
+constexpr int PCG_RSTEP = PCG_THREADS / PCG_TX;         // 8 rows per thread sweep
+constexpr int PCG_RPT = PCG_TY / PCG_RSTEP;             // 4 rows per thread
 constexpr int BOX_Y = PCG_TY + 2;
+constexpr int HW = PCG_TX + 2, HH = PCG_TY + 2;         // halo tile (34 x 34)
+constexpr int YW = PCG_TX + 1, YH = PCG_TY + 1;         // y tile (33 x 33)
 
 // Halo box geometry per element type.  A TMA box must START on a 16-byte
 // boundary in x, so the box begins SH elements left of the tile (SH = 16 B /
@@ -186,7 +190,7 @@ __host__ __device__ constexpr int align128(int b) { return (b + 127) & ~127; }
 
 template <typename T>
 struct StageLayout {
-  // phase A: z, p (halo boxes), x (own box)
+  // phase A: z, p (halo boxes), x and code (own boxes)
   static constexpr int A_Z = 0;
   static constexpr int A_P = align128((int)Halo<T>::BYTES);
   static constexpr int A_X = A_P + align128((int)Halo<T>::BYTES);
@@ -198,20 +202,27 @@ struct StageLayout {
   static constexpr int B_C = B_AP + align128((int)Halo<T>::BYTES);
   static constexpr int B_END = B_C + align128((int)Halo<uint8_t>::BYTES);
   static constexpr int STAGE = A_END > B_END ? A_END : B_END;
-  static constexpr int DEPTH = sizeof(T) == 4 ? 6 : 4;
+  static constexpr int DEPTH = 3;
   static constexpr unsigned BYTES_A_HALO = 2u * Halo<T>::BYTES;
   static constexpr unsigned BYTES_A_X = PCG_TX * PCG_TY * (sizeof(T) + 1);   // x + code, own box
   static constexpr unsigned BYTES_B = Halo<double>::BYTES + Halo<T>::BYTES + Halo<uint8_t>::BYTES;
 };
 
 template <typename T>
+struct PcgWork {          // phase-B work planes (3 = hazard-free ring in job order)
+  T rb[3][HH][HW];
+  T qb[3][HH][HW];
+  uint8_t cb[3][HH][HW];
+  T yb[2][YH][YW];
+};
+
+template <typename T>
 struct PcgShared {
   T lut[64 * 4];
-  T pa[2][PCG_TY + 2][PCG_TX + 2];          // phase 0 planes
-  double rb[3][PCG_TY + 2][PCG_TX + 2];     // phase B converted planes (3 = hazard-free ring)
-  T qb[3][PCG_TY + 2][PCG_TX + 2];
-  uint8_t cb[3][PCG_TY + 2][PCG_TX + 2];
-  T yb[2][PCG_TY + 1][PCG_TX + 1];
+  union {
+    T pa[2][HH][HW];      // phase 0 planes
+    PcgWork<T> wk;        // phase B
+  };
   double red[32];
   double bc[4];
   alignas(8) uint64_t full[8];
@@ -300,35 +311,34 @@ template <typename T>
 __device__ void phase0(const PcgArgs<T>& A, double* part, int unit, PcgShared<T>& S) {
   const Dims& d = A.d;
   const Unit t = unit_of<T>(A, unit);
-  const int lx = threadIdx.x % PCG_TX, ly = threadIdx.x / PCG_TX;
-  const int i = t.i0 + lx, j = t.j0 + ly;
-  const bool own = i < d.nx && j < d.ny;
+  const int lx = threadIdx.x % PCG_TX, ly0 = threadIdx.x / PCG_TX;
+  const int i = t.i0 + lx;
   const long long plane = (long long)d.nx * d.ny;
   const long long pplane = (long long)A.nxp * d.ny;
+  auto xval = [&](int kk, int gi, int gj) -> T {
+    if (kk < 0 || kk >= d.nz || gi < 0 || gi >= d.nx || gj < 0 || gj >= d.ny) return (T)0;
+    if (!(A.code[kk * pplane + (long long)gj * A.nxp + gi] & 64)) return (T)0;
+    return A.state_p[kk * plane + (long long)gj * d.nx + gi];
+  };
   auto load = [&](int kk, int b) {
-    for (int e = threadIdx.x; e < (PCG_TX + 2) * (PCG_TY + 2); e += PCG_TX * PCG_TY) {
-      const int hx = e % (PCG_TX + 2), hy = e / (PCG_TX + 2);
-      const int gi = t.i0 + hx - 1, gj = t.j0 + hy - 1;
-      T val = (T)0;
-      if (kk >= 0 && kk < d.nz && gi >= 0 && gi < d.nx && gj >= 0 && gj < d.ny) {
-        if (A.code[kk * pplane + (long long)gj * A.nxp + gi] & 64)
-          val = A.state_p[kk * plane + (long long)gj * d.nx + gi];
-      }
-      S.pa[b][hy][hx] = val;
+    for (int e = threadIdx.x; e < HH * HW; e += PCG_THREADS) {
+      const int hx = e % HW, hy = e / HW;
+      S.pa[b][hy][hx] = xval(kk, t.i0 + hx - 1, t.j0 + hy - 1);
     }
   };
   double b2 = 0.0, bmax = 0.0, dmax = 0.0;
-  T pm = (T)0;
-  if (own && t.k0 - 1 >= 0) {
-    if (A.code[(t.k0 - 1) * pplane + (long long)j * A.nxp + i] & 64)
-      pm = A.state_p[(t.k0 - 1) * plane + (long long)j * d.nx + i];
-  }
+  T pm[PCG_RPT];
+#pragma unroll
+  for (int q = 0; q < PCG_RPT; ++q) pm[q] = xval(t.k0 - 1, i, t.j0 + ly0 + q * PCG_RSTEP);
   int bc = 0, bn = 1;
   load(t.k0, bc);
   for (int k = t.k0; k < t.k1; ++k) {
     load(k + 1, bn);
     __syncthreads();
-    if (own) {
+#pragma unroll
+    for (int q = 0; q < PCG_RPT; ++q) {
+      const int ly = ly0 + q * PCG_RSTEP, j = t.j0 + ly;
+      if (i >= d.nx || j >= d.ny) continue;
       const long long c = k * plane + (long long)j * d.nx + i;
       const long long pc_ = k * pplane + (long long)j * A.nxp + i;
       const uint8_t cd = A.code[pc_];
@@ -345,7 +355,7 @@ __device__ void phase0(const PcgArgs<T>& A, double* part, int unit, PcgShared<T>
         const double ax = (double)S.lut[(cd & 63) * 4] * (double)pc -
                           ((double)A.wx * ((double)S.pa[bc][ly + 1][lx] + (double)S.pa[bc][ly + 1][lx + 2]) +
                            (double)A.wy * ((double)S.pa[bc][ly][lx + 1] + (double)S.pa[bc][ly + 2][lx + 1]) +
-                           (double)A.wz * ((double)pm + (double)pn));
+                           (double)A.wz * ((double)pm[q] + (double)pn));
         A.r0[pc_] = b - ax;
         A.x[pc_] = pc;
         b2 += b * b;
@@ -355,7 +365,7 @@ __device__ void phase0(const PcgArgs<T>& A, double* part, int unit, PcgShared<T>
       } else {
         A.state_p[c] = (T)0;   // project() sets p = 0 off the unknowns (solver.py:278-280)
       }
-      pm = pc;
+      pm[q] = pc;
     }
     __syncthreads();
     const int tmp = bc; bc = bn; bn = tmp;
@@ -370,6 +380,7 @@ __device__ void phase0(const PcgArgs<T>& A, double* part, int unit, PcgShared<T>
     part[A.U + unit] = m1;
     part[2 * A.U + unit] = m2;
   }
+  __syncthreads();
 }
 
 // ---- phase A: p' = z + beta p, x += alpha_prev p, Ap = A p' ---------------
@@ -377,11 +388,11 @@ template <typename T>
 __device__ void phaseA(const PcgArgs<T>& A, double* part, PcgShared<T>& S, uint8_t* ring, unsigned& ticket,
                        bool first, T beta, bool upd_x, T alpha_prev, int pin_sel) {
   using L = StageLayout<T>;
-  static_assert(L::DEPTH >= 3, "ring too shallow");
+  static_assert(L::DEPTH >= 3, "phase A holds two stages");
   const Dims& d = A.d;
   const CUtensorMap* tp = pin_sel == 0 ? &A.tm_p0 : &A.tm_p1;
   T* __restrict__ pout = pin_sel == 0 ? A.p1 : A.p0;
-  const int lx = threadIdx.x % PCG_TX, ly = threadIdx.x / PCG_TX;
+  const int lx = threadIdx.x % PCG_TX, ly0 = threadIdx.x / PCG_TX;
   const long long pplane = (long long)A.nxp * d.ny;
   JobCursor prod, cons;
   double acc = 0.0;
@@ -406,7 +417,9 @@ __device__ void phaseA(const PcgArgs<T>& A, double* part, PcgShared<T>& S, uint8
     };
     unsigned j = 0;     // consumer job number in this phase
     int cur_s = 0;      // stage holding plane kk-1 of the current unit
-    T pm = (T)0;
+    T pm[PCG_RPT];
+#pragma unroll
+    for (int q = 0; q < PCG_RPT; ++q) pm[q] = (T)0;
     bool live = true;
     while (live) {
       const unsigned tk = t0 + j;
@@ -414,37 +427,39 @@ __device__ void phaseA(const PcgArgs<T>& A, double* part, PcgShared<T>& S, uint8
       const uint8_t* st = ring + (size_t)s * L::STAGE;
       mbar_wait(&S.full[s], (tk / L::DEPTH) & 1u);
       const Unit u = cons.t;
-      const int i = u.i0 + lx, jj = u.j0 + ly;
+      const int i = u.i0 + lx;
       if (cons.kk == u.k0 - 1) {
-        pm = pnew(st, ly + 1, lx + 1);           // own value of plane k0-1
+#pragma unroll
+        for (int q = 0; q < PCG_RPT; ++q) pm[q] = pnew(st, ly0 + q * PCG_RSTEP + 1, lx + 1);
       } else if (cons.kk > u.k0) {
         // plane k = kk-1: 5-point from the held stage, own k+1 from this one
         const int k = cons.kk - 1;
         const uint8_t* cs = ring + (size_t)cur_s * L::STAGE;
-        const T pc = pnew(cs, ly + 1, lx + 1);
-        if (i < d.nx && jj < d.ny) {
-          const long long pc_ = k * pplane + (long long)jj * A.nxp + i;
-          const uint8_t cd = (cs + L::A_C)[ly * PCG_TX + lx];
-          if (cd & 64) {
+        const T* xx = reinterpret_cast<const T*>(cs + L::A_X);
+        const T* pp = reinterpret_cast<const T*>(cs + L::A_P);
+        const uint8_t* cc = cs + L::A_C;
+#pragma unroll
+        for (int q = 0; q < PCG_RPT; ++q) {
+          const int ly = ly0 + q * PCG_RSTEP, jj = u.j0 + ly;
+          const T pc = pnew(cs, ly + 1, lx + 1);
+          const uint8_t cd = cc[ly * PCG_TX + lx];
+          if ((cd & 64) && i < d.nx && jj < d.ny) {
+            const long long pc_ = k * pplane + (long long)jj * A.nxp + i;
             const T pn = pnew(st, ly + 1, lx + 1);
             // A p in float64 from the stored p: the 7-point difference of a
-            // smooth p cancels d*p almost entirely, so float32 arithmetic would
-            // leave a relative error of ~eps*d|p|/|Ap| in Ap (and in r)
+            // smooth p cancels d*p almost entirely, so float32 arithmetic
+            // would leave a relative error ~eps*d|p|/|Ap| in Ap (and in r)
             const double ap = (double)S.lut[(cd & 63) * 4] * (double)pc -
                               ((double)A.wx * ((double)pnew(cs, ly + 1, lx) + (double)pnew(cs, ly + 1, lx + 2)) +
                                (double)A.wy * ((double)pnew(cs, ly, lx + 1) + (double)pnew(cs, ly + 2, lx + 1)) +
-                               (double)A.wz * ((double)pm + (double)pn));
+                               (double)A.wz * ((double)pm[q] + (double)pn));
             pout[pc_] = pc;
             A.Ap[pc_] = (T)ap;
-            if (upd_x) {
-              const T* xx = reinterpret_cast<const T*>(cs + L::A_X);
-              const T* pp = reinterpret_cast<const T*>(cs + L::A_P);
-              A.x[pc_] = xx[ly * PCG_TX + lx] + alpha_prev * pp[Halo<T>::at(ly + 1, lx + 1)];
-            }
+            if (upd_x) A.x[pc_] = xx[ly * PCG_TX + lx] + alpha_prev * pp[Halo<T>::at(ly + 1, lx + 1)];
             acc += (double)pc * ap;
           }
+          pm[q] = pc;
         }
-        pm = pc;
       }
       cur_s = s;
       live = cursor_next<T>(A, cons);
@@ -452,7 +467,6 @@ __device__ void phaseA(const PcgArgs<T>& A, double* part, PcgShared<T>& S, uint8
       __syncthreads();   // everyone is done with stage j-2's data; job j-1's stage stays held
       if (threadIdx.x == 0) {
         while (more && issued < j + L::DEPTH - 1) {
-
           issue_A<T>(A, ring, S.full, t0 + issued, prod, tp);
           ++issued;
           more = cursor_next<T>(A, prod);
@@ -474,29 +488,9 @@ __device__ void phaseB(const PcgArgs<T>& A, double* part, PcgShared<T>& S, uint8
   const CUtensorMap* tr = rin_sel == 0 ? &A.tm_r0 : &A.tm_r1;
   double* __restrict__ rout = rin_sel == 0 ? A.r1 : A.r0;
   const T om = A.om;
-  const int lx = threadIdx.x % PCG_TX, ly = threadIdx.x / PCG_TX;
+  const int lx = threadIdx.x % PCG_TX, ly0 = threadIdx.x / PCG_TX;
   const long long pplane = (long long)A.nxp * d.ny;
-  // fixed per-thread positions of the convert and y passes
-  struct {
-    int e[2], sr[2], st[2], sc[2], yo[2], ye[2];
-    bool h1, y1;
-  } P;
-#pragma unroll
-  for (int q = 0; q < 2; ++q) {
-    const int e = threadIdx.x + q * PCG_TX * PCG_TY;
-    const int ec = e < (PCG_TX + 2) * (PCG_TY + 2) ? e : 0;
-    const int hx = ec % (PCG_TX + 2), hy = ec / (PCG_TX + 2);
-    P.e[q] = ec;
-    P.sr[q] = Halo<double>::at(hy, hx);
-    P.st[q] = Halo<T>::at(hy, hx);
-    P.sc[q] = Halo<uint8_t>::at(hy, hx);
-    const int ey = e < (PCG_TX + 1) * (PCG_TY + 1) ? e : 0;
-    const int yx = ey % (PCG_TX + 1), yy = ey / (PCG_TX + 1);
-    P.yo[q] = (yy + 1) * (PCG_TX + 2) + yx + 1;
-    P.ye[q] = yy * (PCG_TX + 1) + yx;
-  }
-  P.h1 = threadIdx.x + PCG_TX * PCG_TY < (PCG_TX + 2) * (PCG_TY + 2);
-  P.y1 = threadIdx.x + PCG_TX * PCG_TY < (PCG_TX + 1) * (PCG_TY + 1);
+  PcgWork<T>& W = S.wk;
   JobCursor prod, cons;
   double acc = 0.0, rmax = 0.0;
   if (cursor_begin<T>(A, cons)) {
@@ -512,7 +506,9 @@ __device__ void phaseB(const PcgArgs<T>& A, double* part, PcgShared<T>& S, uint8
       }
     }
     unsigned j = 0;
-    double rprev = 0.0;
+    double rprev[PCG_RPT], rown[PCG_RPT];
+#pragma unroll
+    for (int q = 0; q < PCG_RPT; ++q) rprev[q] = 0.0;
     bool live = true;
     while (live) {
       const unsigned tk = t0 + j;
@@ -522,72 +518,82 @@ __device__ void phaseB(const PcgArgs<T>& A, double* part, PcgShared<T>& S, uint8
       const Unit u = cons.t;
       const int kk = cons.kk;
       const int b = j % 3, bp = (j + 2) % 3;      // work-plane ring (job order)
-      const int yb_ = j & 1, ybp = (j + 1) & 1;
-      // convert the landed stage: r' = r - alpha Ap, q = r'/d, code
+      const int yb = j & 1, ybp = (j + 1) & 1;
       {
+        // convert the landed stage: r' = r - alpha Ap, q = r'/d, code
         const double* rr = reinterpret_cast<const double*>(st + L::B_R);
         const T* aa = reinterpret_cast<const T*>(st + L::B_AP);
         const uint8_t* cc = st + L::B_C;
-        double* rbf = &S.rb[b][0][0];
-        T* qbf = &S.qb[b][0][0];
-        uint8_t* cbf = &S.cb[b][0][0];
+        T* rbf = &W.rb[b][0][0];
+        T* qbf = &W.qb[b][0][0];
+        uint8_t* cbf = &W.cb[b][0][0];
+        for (int e = threadIdx.x; e < HH * HW; e += PCG_THREADS) {
+          const int hx = e % HW, hy = e / HW;
+          double r = rr[Halo<double>::at(hy, hx)];
+          if (use_ap) r = r - alpha * (double)aa[Halo<T>::at(hy, hx)];
+          const uint8_t cd = cc[Halo<uint8_t>::at(hy, hx)];
+          rbf[e] = (T)r;
+          qbf[e] = (T)r * S.lut[(cd & 63) * 4 + 1];
+          cbf[e] = cd;
+        }
+        // own residuals in float64 straight from the stage
 #pragma unroll
-        for (int q = 0; q < 2; ++q) {
-          if (q == 1 && !P.h1) break;
-          double r = rr[P.sr[q]];
-          if (use_ap) r = r - alpha * (double)aa[P.st[q]];
-          const uint8_t cd = cc[P.sc[q]];
-          rbf[P.e[q]] = r;
-          qbf[P.e[q]] = (T)r * S.lut[(cd & 63) * 4 + 1];
-          cbf[P.e[q]] = cd;
+        for (int q = 0; q < PCG_RPT; ++q) {
+          const int hy = ly0 + q * PCG_RSTEP + 1, hx = lx + 1;
+          double r = rr[Halo<double>::at(hy, hx)];
+          if (use_ap) r = r - alpha * (double)aa[Halo<T>::at(hy, hx)];
+          rown[q] = r;
         }
       }
       __syncthreads();
       if (threadIdx.x == 0 && more) {     // the raw stage is free: refill it
-
         issue_B<T>(A, ring, S.full, t0 + issued, prod, tr);
         ++issued;
         more = cursor_next<T>(A, prod);
       }
-      const double rown = S.rb[b][ly + 1][lx + 1];
       if (kk >= u.k0 && A.precond == 2) {
-        const double* rbf = &S.rb[b][0][0];
-        const T* qbf = &S.qb[b][0][0];
-        const T* qpf = &S.qb[bp][0][0];
-        const uint8_t* cbf = &S.cb[b][0][0];
-        T* ybf = &S.yb[yb_][0][0];
-#pragma unroll
-        for (int q = 0; q < 2; ++q) {
-          if (q == 1 && !P.y1) break;
-          const int o = P.yo[q];                         // (hy+1, hx+1) in the halo plane
+        const T* rbf = &W.rb[b][0][0];
+        const T* qbf = &W.qb[b][0][0];
+        const T* qpf = &W.qb[bp][0][0];
+        const uint8_t* cbf = &W.cb[b][0][0];
+        T* ybf = &W.yb[yb][0][0];
+        for (int e = threadIdx.x; e < YH * YW; e += PCG_THREADS) {
+          const int yx = e % YW, yy = e / YW;
+          const int o = (yy + 1) * HW + yx + 1;     // (hy+1, hx+1) in the halo plane
           const T sv = S.lut[(cbf[o] & 63) * 4 + 2];
-          ybf[P.ye[q]] = sv * ((T)rbf[o] + om * (A.wx * qbf[o - 1] + A.wy * qbf[o - (PCG_TX + 2)] +
-                                                 A.wz * qpf[o]));
+          ybf[e] = sv * (rbf[o] + om * (A.wx * qbf[o - 1] + A.wy * qbf[o - HW] + A.wz * qpf[o]));
         }
       }
       __syncthreads();
-      const int i = u.i0 + lx, jj = u.j0 + ly;
-      if (kk >= u.k0 + 1 && i < d.nx && jj < d.ny) {
+      if (kk >= u.k0 + 1) {
         const int k = kk - 1;
-        const long long pc_ = k * pplane + (long long)jj * A.nxp + i;
-        const uint8_t cd = S.cb[bp][ly + 1][lx + 1];
-        if (cd & 64) {
-          T zv;
-          if (A.precond == 2)
-            zv = S.yb[ybp][ly][lx] + om * S.lut[(cd & 63) * 4 + 1] *
-                 (A.wx * S.yb[ybp][ly][lx + 1] + A.wy * S.yb[ybp][ly + 1][lx] + A.wz * S.yb[yb_][ly][lx]);
-          else if (A.precond == 1)
-            zv = S.qb[bp][ly + 1][lx + 1];
-          else
-            zv = (T)rprev;
-          A.z[pc_] = zv;
-          if (write_r) rout[pc_] = rprev;
-          acc += rprev * (double)zv;
-          const double ar = fabs(rprev);
-          rmax = (ar > rmax || ar != ar) ? ar : rmax;
+        const int i = u.i0 + lx;
+        const T* y0 = &W.yb[ybp][0][0];
+        const T* y1 = &W.yb[yb][0][0];
+#pragma unroll
+        for (int q = 0; q < PCG_RPT; ++q) {
+          const int ly = ly0 + q * PCG_RSTEP, jj = u.j0 + ly;
+          const uint8_t cd = W.cb[bp][ly + 1][lx + 1];
+          if ((cd & 64) && i < d.nx && jj < d.ny) {
+            const long long pc_ = k * pplane + (long long)jj * A.nxp + i;
+            T zv;
+            const int o = ly * YW + lx;
+            if (A.precond == 2)
+              zv = y0[o] + om * S.lut[(cd & 63) * 4 + 1] * (A.wx * y0[o + 1] + A.wy * y0[o + YW] + A.wz * y1[o]);
+            else if (A.precond == 1)
+              zv = W.qb[bp][ly + 1][lx + 1];
+            else
+              zv = (T)rprev[q];
+            A.z[pc_] = zv;
+            if (write_r) rout[pc_] = rprev[q];
+            acc += rprev[q] * (double)zv;
+            const double ar = fabs(rprev[q]);
+            rmax = (ar > rmax || ar != ar) ? ar : rmax;
+          }
         }
       }
-      rprev = rown;
+#pragma unroll
+      for (int q = 0; q < PCG_RPT; ++q) rprev[q] = rown[q];
       live = cursor_next<T>(A, cons);
       ++j;
     }
@@ -600,6 +606,7 @@ __device__ void phaseB(const PcgArgs<T>& A, double* part, PcgShared<T>& S, uint8
     part[blockIdx.x] = sm;
     part[A.U + blockIdx.x] = mx;
   }
+  __syncthreads();
 }
 
 // final: state p = x (+ alpha p pending) on the unknowns
@@ -607,20 +614,24 @@ template <typename T>
 __device__ void finish_x(const PcgArgs<T>& A, int unit, T alpha, const T* __restrict__ p, bool zero) {
   const Dims& d = A.d;
   const Unit t = unit_of<T>(A, unit);
-  const int lx = threadIdx.x % PCG_TX, ly = threadIdx.x / PCG_TX;
-  const int i = t.i0 + lx, j = t.j0 + ly;
-  if (i >= d.nx || j >= d.ny) return;
+  const int lx = threadIdx.x % PCG_TX, ly0 = threadIdx.x / PCG_TX;
+  const int i = t.i0 + lx;
+  if (i >= d.nx) return;
   const long long plane = (long long)d.nx * d.ny, pplane = (long long)A.nxp * d.ny;
-  for (int k = t.k0; k < t.k1; ++k) {
-    const long long c = k * plane + (long long)j * d.nx + i;
-    const long long pc_ = k * pplane + (long long)j * A.nxp + i;
-    if (zero) { A.state_p[c] = (T)0; continue; }
-    if (A.code[pc_] & 64) A.state_p[c] = alpha != (T)0 ? A.x[pc_] + alpha * p[pc_] : A.x[pc_];
+  for (int q = 0; q < PCG_RPT; ++q) {
+    const int j = t.j0 + ly0 + q * PCG_RSTEP;
+    if (j >= d.ny) continue;
+    for (int k = t.k0; k < t.k1; ++k) {
+      const long long c = k * plane + (long long)j * d.nx + i;
+      const long long pc_ = k * pplane + (long long)j * A.nxp + i;
+      if (zero) { A.state_p[c] = (T)0; continue; }
+      if (A.code[pc_] & 64) A.state_p[c] = alpha != (T)0 ? A.x[pc_] + alpha * p[pc_] : A.x[pc_];
+    }
   }
 }
 
 template <typename T>
-__global__ void __launch_bounds__(PCG_TX * PCG_TY) k_pcg(const __grid_constant__ PcgArgs<T> A) {
+__global__ void __launch_bounds__(PCG_THREADS) k_pcg(const __grid_constant__ PcgArgs<T> A) {
   // dynamic smem is the only shared allocation of this kernel, so it starts
   // at the (1 KB aligned) base of the block's window; keep every access on
   // this array so the compiler emits LDS/STS rather than generic loads
