@@ -202,7 +202,7 @@ struct StageLayout {
   static constexpr int B_C = B_AP + align128((int)Halo<T>::BYTES);
   static constexpr int B_END = B_C + align128((int)Halo<uint8_t>::BYTES);
   static constexpr int STAGE = A_END > B_END ? A_END : B_END;
-  static constexpr int DEPTH = 3;
+  static constexpr int DEPTH = sizeof(T) == 4 ? 4 : 3;
   static constexpr unsigned BYTES_A_HALO = 2u * Halo<T>::BYTES;
   static constexpr unsigned BYTES_A_X = PCG_TX * PCG_TY * (sizeof(T) + 1);   // x + code, own box
   static constexpr unsigned BYTES_B = Halo<double>::BYTES + Halo<T>::BYTES + Halo<uint8_t>::BYTES;
@@ -210,7 +210,6 @@ struct StageLayout {
 
 template <typename T>
 struct PcgWork {          // phase-B work planes (3 = hazard-free ring in job order)
-  T rb[3][HH][HW];
   T qb[3][HH][HW];
   uint8_t cb[3][HH][HW];
   T yb[2][YH][YW];
@@ -416,10 +415,13 @@ __device__ void phaseA(const PcgArgs<T>& A, double* part, PcgShared<T>& S, uint8
       return first ? zv : zv + beta * pp[o];
     };
     unsigned j = 0;     // consumer job number in this phase
-    int cur_s = 0;      // stage holding plane kk-1 of the current unit
-    T pm[PCG_RPT];
+    // per own row: the previous plane's p', and plane kk-1's pending result
+    // (A p without its +z term, new x, own flag) finished once plane kk lands
+    T pm[PCG_RPT], pcur[PCG_RPT], xn[PCG_RPT];
+    double part_ap[PCG_RPT];
+    bool pend[PCG_RPT];
 #pragma unroll
-    for (int q = 0; q < PCG_RPT; ++q) pm[q] = (T)0;
+    for (int q = 0; q < PCG_RPT; ++q) { pm[q] = (T)0; pend[q] = false; }
     bool live = true;
     while (live) {
       const unsigned tk = t0 + j;
@@ -428,45 +430,46 @@ __device__ void phaseA(const PcgArgs<T>& A, double* part, PcgShared<T>& S, uint8
       mbar_wait(&S.full[s], (tk / L::DEPTH) & 1u);
       const Unit u = cons.t;
       const int i = u.i0 + lx;
-      if (cons.kk == u.k0 - 1) {
+      const int kk = cons.kk;
+      const T* xx = reinterpret_cast<const T*>(st + L::A_X);
+      const T* pp = reinterpret_cast<const T*>(st + L::A_P);
+      const uint8_t* cc = st + L::A_C;
 #pragma unroll
-        for (int q = 0; q < PCG_RPT; ++q) pm[q] = pnew(st, ly0 + q * PCG_RSTEP + 1, lx + 1);
-      } else if (cons.kk > u.k0) {
-        // plane k = kk-1: 5-point from the held stage, own k+1 from this one
-        const int k = cons.kk - 1;
-        const uint8_t* cs = ring + (size_t)cur_s * L::STAGE;
-        const T* xx = reinterpret_cast<const T*>(cs + L::A_X);
-        const T* pp = reinterpret_cast<const T*>(cs + L::A_P);
-        const uint8_t* cc = cs + L::A_C;
-#pragma unroll
-        for (int q = 0; q < PCG_RPT; ++q) {
-          const int ly = ly0 + q * PCG_RSTEP, jj = u.j0 + ly;
-          const T pc = pnew(cs, ly + 1, lx + 1);
+      for (int q = 0; q < PCG_RPT; ++q) {
+        const int ly = ly0 + q * PCG_RSTEP, jj = u.j0 + ly;
+        const T pn = pnew(st, ly + 1, lx + 1);     // own p' on plane kk
+        if (pend[q]) {
+          // finish plane kk-1: add the +z neighbour (this plane) and store.
+          // A p is accumulated in float64 from the stored p: the 7-point
+          // difference of a smooth p cancels d*p almost entirely, so float32
+          // arithmetic would leave a relative error ~eps*d|p|/|Ap|
+          const long long pc_ = (long long)(kk - 1) * pplane + (long long)jj * A.nxp + i;
+          const double ap = part_ap[q] - (double)A.wz * (double)pn;
+          pout[pc_] = pcur[q];
+          A.Ap[pc_] = (T)ap;
+          if (upd_x) A.x[pc_] = xn[q];
+          acc += (double)pcur[q] * ap;
+          pend[q] = false;
+        }
+        if (kk >= u.k0 && kk < u.k1) {
           const uint8_t cd = cc[ly * PCG_TX + lx];
           if ((cd & 64) && i < d.nx && jj < d.ny) {
-            const long long pc_ = k * pplane + (long long)jj * A.nxp + i;
-            const T pn = pnew(st, ly + 1, lx + 1);
-            // A p in float64 from the stored p: the 7-point difference of a
-            // smooth p cancels d*p almost entirely, so float32 arithmetic
-            // would leave a relative error ~eps*d|p|/|Ap| in Ap (and in r)
-            const double ap = (double)S.lut[(cd & 63) * 4] * (double)pc -
-                              ((double)A.wx * ((double)pnew(cs, ly + 1, lx) + (double)pnew(cs, ly + 1, lx + 2)) +
-                               (double)A.wy * ((double)pnew(cs, ly, lx + 1) + (double)pnew(cs, ly + 2, lx + 1)) +
-                               (double)A.wz * ((double)pm[q] + (double)pn));
-            pout[pc_] = pc;
-            A.Ap[pc_] = (T)ap;
-            if (upd_x) A.x[pc_] = xx[ly * PCG_TX + lx] + alpha_prev * pp[Halo<T>::at(ly + 1, lx + 1)];
-            acc += (double)pc * ap;
+            part_ap[q] = (double)S.lut[(cd & 63) * 4] * (double)pn -
+                         ((double)A.wx * ((double)pnew(st, ly + 1, lx) + (double)pnew(st, ly + 1, lx + 2)) +
+                          (double)A.wy * ((double)pnew(st, ly, lx + 1) + (double)pnew(st, ly + 2, lx + 1)) +
+                          (double)A.wz * (double)pm[q]);
+            pcur[q] = pn;
+            if (upd_x) xn[q] = xx[ly * PCG_TX + lx] + alpha_prev * pp[Halo<T>::at(ly + 1, lx + 1)];
+            pend[q] = true;
           }
-          pm[q] = pc;
         }
+        pm[q] = pn;
       }
-      cur_s = s;
       live = cursor_next<T>(A, cons);
       ++j;
-      __syncthreads();   // everyone is done with stage j-2's data; job j-1's stage stays held
+      __syncthreads();   // every thread is done with this job's stage: refill it
       if (threadIdx.x == 0) {
-        while (more && issued < j + L::DEPTH - 1) {
+        while (more && issued < j + L::DEPTH) {
           issue_A<T>(A, ring, S.full, t0 + issued, prod, tp);
           ++issued;
           more = cursor_next<T>(A, prod);
@@ -524,7 +527,6 @@ __device__ void phaseB(const PcgArgs<T>& A, double* part, PcgShared<T>& S, uint8
         const double* rr = reinterpret_cast<const double*>(st + L::B_R);
         const T* aa = reinterpret_cast<const T*>(st + L::B_AP);
         const uint8_t* cc = st + L::B_C;
-        T* rbf = &W.rb[b][0][0];
         T* qbf = &W.qb[b][0][0];
         uint8_t* cbf = &W.cb[b][0][0];
         for (int e = threadIdx.x; e < HH * HW; e += PCG_THREADS) {
@@ -532,7 +534,6 @@ __device__ void phaseB(const PcgArgs<T>& A, double* part, PcgShared<T>& S, uint8
           double r = rr[Halo<double>::at(hy, hx)];
           if (use_ap) r = r - alpha * (double)aa[Halo<T>::at(hy, hx)];
           const uint8_t cd = cc[Halo<uint8_t>::at(hy, hx)];
-          rbf[e] = (T)r;
           qbf[e] = (T)r * S.lut[(cd & 63) * 4 + 1];
           cbf[e] = cd;
         }
@@ -552,16 +553,17 @@ __device__ void phaseB(const PcgArgs<T>& A, double* part, PcgShared<T>& S, uint8
         more = cursor_next<T>(A, prod);
       }
       if (kk >= u.k0 && A.precond == 2) {
-        const T* rbf = &W.rb[b][0][0];
+        // y = s (r + w sum_a w_a q_{-a}) with s r = (2-w) w q  (s = (2-w) w / d, q = r / d)
         const T* qbf = &W.qb[b][0][0];
         const T* qpf = &W.qb[bp][0][0];
         const uint8_t* cbf = &W.cb[b][0][0];
         T* ybf = &W.yb[yb][0][0];
+        const T c0 = ((T)2 - om) * om;
         for (int e = threadIdx.x; e < YH * YW; e += PCG_THREADS) {
           const int yx = e % YW, yy = e / YW;
           const int o = (yy + 1) * HW + yx + 1;     // (hy+1, hx+1) in the halo plane
           const T sv = S.lut[(cbf[o] & 63) * 4 + 2];
-          ybf[e] = sv * (rbf[o] + om * (A.wx * qbf[o - 1] + A.wy * qbf[o - HW] + A.wz * qpf[o]));
+          ybf[e] = c0 * qbf[o] + sv * (om * (A.wx * qbf[o - 1] + A.wy * qbf[o - HW] + A.wz * qpf[o]));
         }
       }
       __syncthreads();
