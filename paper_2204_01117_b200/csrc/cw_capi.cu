@@ -430,6 +430,13 @@ static int launch_pcg(cw_ctx* c, const cw_fields* f, DevReport* rep, double dt, 
   A.precond = c->precond;
   A.ntx = c->ntx; A.nty = c->nty; A.zc = c->zc; A.U = c->U;
   A.timeout_ns = 20LL * 1000 * 1000 * 1000;
+  A.probe_mode = 0;
+  A.probe_iters = 0;
+  if (const char* pe = std::getenv("CW_PCG_PROBE")) {   // developer timing probe "mode,iters"
+    A.probe_mode = std::atoi(pe);
+    const char* comma = std::strchr(pe, 0x2c);
+    A.probe_iters = comma ? std::atoi(comma + 1) : 100;
+  }
   CW_CUDA(cudaMemsetAsync(c->bar, 0, 64 * sizeof(unsigned), st));
   void* args[] = {&A};
   CW_CUDA(cudaLaunchCooperativeKernel((const void*)k_pcg<T>, dim3(c->pcg_blocks), dim3(PCG_THREADS), args, c->pcg_smem, st));

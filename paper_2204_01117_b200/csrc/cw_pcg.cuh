@@ -82,6 +82,7 @@ struct PcgArgs {
   int precond;               // 0 identity, 1 jacobi (diag(1/d)), 2 AI1 (K^T K)
   int ntx, nty, zc, U;
   long long timeout_ns;
+  int probe_mode, probe_iters;   // developer timing probe (CW_PCG_PROBE), 0 = off
 };
 
 // ---------------------------------------------------------------------------
@@ -691,6 +692,17 @@ __global__ void __launch_bounds__(PCG_THREADS) k_pcg(const __grid_constant__ Pcg
   double crit = rz / b2;
   int it = 0, converged = 0, status = 0;
   bool finished = false;
+  if (A.probe_mode) {
+    // timing probe: repeat one phase (1: A, 2: B, 3: barrier only) with its
+    // grid barrier; the state's p is not meaningful afterwards
+    for (int q = 0; q < A.probe_iters; ++q) {
+      if (A.probe_mode == 1) phaseA<T>(A, P[0], S, ring, ticket, false, (T)0.5, true, (T)0.0, q & 1);
+      if (A.probe_mode == 2) phaseB<T>(A, P[1], S, ring, ticket, true, 0.0, q & 1, true);
+      grid_barrier(A.bar, A.gate, rep, A.timeout_ns);
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) { rep->iterations = A.probe_iters; rep->converged = 1; }
+    return;
+  }
   if (0.0 <= crit && crit < tol && rmax <= res_target) { converged = 1; finished = true; }
   else if (rz < 0.0) { finished = true; }
   int rsel = 0;       // r lives in r0 (0) or r1 (1)
