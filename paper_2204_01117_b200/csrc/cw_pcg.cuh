@@ -210,10 +210,9 @@ struct StageLayout {
 };
 
 template <typename T>
-struct PcgWork {          // phase-B work planes (3 = hazard-free ring in job order)
-  T qb[3][HH][HW];
-  uint8_t cb[3][HH][HW];
-  T yb[2][YH][YW];
+struct PcgWork {          // phase-B work planes
+  T qb[2][YH][YW];        // q = r'/d on the y-tile, planes kk and kk-1
+  T yb[3][YH][YW];        // y, planes kk and kk-1 (+1 for a hazard-free ring)
 };
 
 template <typename T>
@@ -484,6 +483,9 @@ __device__ void phaseA(const PcgArgs<T>& A, double* part, PcgShared<T>& S, uint8
 }
 
 // ---- phase B: r' = r - alpha Ap, z = W r' ----------------------------------
+// One pass per landed plane kk computes q = r'/d on the y-tile (recomputing
+// the two in-plane lower neighbours from the stage instead of staging q) and
+// y(kk); after one barrier the own cells finish z on plane kk-1.
 template <typename T>
 __device__ void phaseB(const PcgArgs<T>& A, double* part, PcgShared<T>& S, uint8_t* ring, unsigned& ticket,
                        bool use_ap, double alpha, int rin_sel, bool write_r) {
@@ -492,6 +494,7 @@ __device__ void phaseB(const PcgArgs<T>& A, double* part, PcgShared<T>& S, uint8
   const CUtensorMap* tr = rin_sel == 0 ? &A.tm_r0 : &A.tm_r1;
   double* __restrict__ rout = rin_sel == 0 ? A.r1 : A.r0;
   const T om = A.om;
+  const T c0 = ((T)2 - om) * om;          // s * d
   const int lx = threadIdx.x % PCG_TX, ly0 = threadIdx.x / PCG_TX;
   const long long pplane = (long long)A.nxp * d.ny;
   PcgWork<T>& W = S.wk;
@@ -511,8 +514,9 @@ __device__ void phaseB(const PcgArgs<T>& A, double* part, PcgShared<T>& S, uint8
     }
     unsigned j = 0;
     double rprev[PCG_RPT], rown[PCG_RPT];
+    uint8_t cprev[PCG_RPT], cown[PCG_RPT];
 #pragma unroll
-    for (int q = 0; q < PCG_RPT; ++q) rprev[q] = 0.0;
+    for (int q = 0; q < PCG_RPT; ++q) { rprev[q] = 0.0; cprev[q] = 0; }
     bool live = true;
     while (live) {
       const unsigned tk = t0 + j;
@@ -521,30 +525,41 @@ __device__ void phaseB(const PcgArgs<T>& A, double* part, PcgShared<T>& S, uint8
       mbar_wait(&S.full[s], (tk / L::DEPTH) & 1u);
       const Unit u = cons.t;
       const int kk = cons.kk;
-      const int b = j % 3, bp = (j + 2) % 3;      // work-plane ring (job order)
-      const int yb = j & 1, ybp = (j + 1) & 1;
-      {
-        // convert the landed stage: r' = r - alpha Ap, q = r'/d, code
-        const double* rr = reinterpret_cast<const double*>(st + L::B_R);
-        const T* aa = reinterpret_cast<const T*>(st + L::B_AP);
-        const uint8_t* cc = st + L::B_C;
-        T* qbf = &W.qb[b][0][0];
-        uint8_t* cbf = &W.cb[b][0][0];
-        for (int e = threadIdx.x; e < HH * HW; e += PCG_THREADS) {
-          const int hx = e % HW, hy = e / HW;
-          double r = rr[Halo<double>::at(hy, hx)];
-          if (use_ap) r = r - alpha * (double)aa[Halo<T>::at(hy, hx)];
-          const uint8_t cd = cc[Halo<uint8_t>::at(hy, hx)];
-          qbf[e] = (T)r * S.lut[(cd & 63) * 4 + 1];
-          cbf[e] = cd;
-        }
-        // own residuals in float64 straight from the stage
+      const int qb = j & 1, qbp = (j + 1) & 1;       // q planes (kk, kk-1)
+      const int yb = j % 3, ybp = (j + 2) % 3;       // y planes (kk, kk-1), 3 = hazard-free
+      const double* rr = reinterpret_cast<const double*>(st + L::B_R);
+      const T* aa = reinterpret_cast<const T*>(st + L::B_AP);
+      const uint8_t* cc = st + L::B_C;
+      auto rnew = [&](int hy, int hx) -> double {
+        double r = rr[Halo<double>::at(hy, hx)];
+        if (use_ap) r = r - alpha * (double)aa[Halo<T>::at(hy, hx)];
+        return r;
+      };
+      auto qval = [&](int hy, int hx) -> T {
+        return (T)rnew(hy, hx) * S.lut[(cc[Halo<uint8_t>::at(hy, hx)] & 63) * 4 + 1];
+      };
 #pragma unroll
-        for (int q = 0; q < PCG_RPT; ++q) {
-          const int hy = ly0 + q * PCG_RSTEP + 1, hx = lx + 1;
-          double r = rr[Halo<double>::at(hy, hx)];
-          if (use_ap) r = r - alpha * (double)aa[Halo<T>::at(hy, hx)];
-          rown[q] = r;
+      for (int q = 0; q < PCG_RPT; ++q) {            // own residuals (float64) and codes
+        const int hy = ly0 + q * PCG_RSTEP + 1;
+        rown[q] = rnew(hy, lx + 1);
+        cown[q] = cc[Halo<uint8_t>::at(hy, lx + 1)];
+      }
+      {
+        T* qcur = &W.qb[qb][0][0];
+        const T* qprv = &W.qb[qbp][0][0];
+        T* ycur = &W.yb[yb][0][0];
+        const bool do_y = kk >= u.k0 && A.precond == 2;
+        for (int e = threadIdx.x; e < YH * YW; e += PCG_THREADS) {
+          const int yx = e % YW, yy = e / YW;
+          const int hy = yy + 1, hx = yx + 1;
+          const uint8_t cd = cc[Halo<uint8_t>::at(hy, hx)];
+          const T qp = (T)rnew(hy, hx) * S.lut[(cd & 63) * 4 + 1];
+          qcur[e] = qp;
+          if (do_y) {
+            // y = s (r + w sum_a w_a q_{-a}) with s r = (2-w) w q
+            const T sv = S.lut[(cd & 63) * 4 + 2];
+            ycur[e] = c0 * qp + sv * (om * (A.wx * qval(hy, hx - 1) + A.wy * qval(hy - 1, hx) + A.wz * qprv[e]));
+          }
         }
       }
       __syncthreads();
@@ -553,21 +568,6 @@ __device__ void phaseB(const PcgArgs<T>& A, double* part, PcgShared<T>& S, uint8
         ++issued;
         more = cursor_next<T>(A, prod);
       }
-      if (kk >= u.k0 && A.precond == 2) {
-        // y = s (r + w sum_a w_a q_{-a}) with s r = (2-w) w q  (s = (2-w) w / d, q = r / d)
-        const T* qbf = &W.qb[b][0][0];
-        const T* qpf = &W.qb[bp][0][0];
-        const uint8_t* cbf = &W.cb[b][0][0];
-        T* ybf = &W.yb[yb][0][0];
-        const T c0 = ((T)2 - om) * om;
-        for (int e = threadIdx.x; e < YH * YW; e += PCG_THREADS) {
-          const int yx = e % YW, yy = e / YW;
-          const int o = (yy + 1) * HW + yx + 1;     // (hy+1, hx+1) in the halo plane
-          const T sv = S.lut[(cbf[o] & 63) * 4 + 2];
-          ybf[e] = c0 * qbf[o] + sv * (om * (A.wx * qbf[o - 1] + A.wy * qbf[o - HW] + A.wz * qpf[o]));
-        }
-      }
-      __syncthreads();
       if (kk >= u.k0 + 1) {
         const int k = kk - 1;
         const int i = u.i0 + lx;
@@ -576,15 +576,16 @@ __device__ void phaseB(const PcgArgs<T>& A, double* part, PcgShared<T>& S, uint8
 #pragma unroll
         for (int q = 0; q < PCG_RPT; ++q) {
           const int ly = ly0 + q * PCG_RSTEP, jj = u.j0 + ly;
-          const uint8_t cd = W.cb[bp][ly + 1][lx + 1];
+          const uint8_t cd = cprev[q];
           if ((cd & 64) && i < d.nx && jj < d.ny) {
             const long long pc_ = k * pplane + (long long)jj * A.nxp + i;
             T zv;
             const int o = ly * YW + lx;
+            const T invd = S.lut[(cd & 63) * 4 + 1];
             if (A.precond == 2)
-              zv = y0[o] + om * S.lut[(cd & 63) * 4 + 1] * (A.wx * y0[o + 1] + A.wy * y0[o + YW] + A.wz * y1[o]);
+              zv = y0[o] + om * invd * (A.wx * y0[o + 1] + A.wy * y0[o + YW] + A.wz * y1[o]);
             else if (A.precond == 1)
-              zv = W.qb[bp][ly + 1][lx + 1];
+              zv = (T)rprev[q] * invd;
             else
               zv = (T)rprev[q];
             A.z[pc_] = zv;
@@ -596,7 +597,7 @@ __device__ void phaseB(const PcgArgs<T>& A, double* part, PcgShared<T>& S, uint8
         }
       }
 #pragma unroll
-      for (int q = 0; q < PCG_RPT; ++q) rprev[q] = rown[q];
+      for (int q = 0; q < PCG_RPT; ++q) { rprev[q] = rown[q]; cprev[q] = cown[q]; }
       live = cursor_next<T>(A, cons);
       ++j;
     }
