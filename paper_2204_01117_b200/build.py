@@ -1,9 +1,7 @@
 """Build recipe for the sm_100a extension (plain nvcc, no torch JIT cache).
 
 The shared library is written in-tree (paper_2204_01117_b200/libcitywind_b200.so)
-so that it travels with the repo snapshot to the GPU box.  Developer
-variants: ``python build.py --out libX.so -DCW_PCG_TY=16`` (load one with
-CW_LIB=/path/libX.so).
+so that it travels with the repo snapshot to the GPU box.
 """
 from __future__ import annotations
 
@@ -23,26 +21,24 @@ def nvcc():
     return cand if os.path.exists(cand) else "nvcc"
 
 
-def _stale(lib) -> bool:
-    if not os.path.exists(lib):
+def _stale() -> bool:
+    if not os.path.exists(LIB):
         return True
-    t = os.path.getmtime(lib)
+    t = os.path.getmtime(LIB)
     deps = [os.path.join(HERE, "csrc", f) for f in os.listdir(os.path.join(HERE, "csrc"))]
     deps.append(os.path.join(ROOT, "include", "citywind_b200.h"))
     deps.append(os.path.abspath(__file__))
     return any(os.path.getmtime(p) > t for p in deps)
 
 
-def build(force: bool = False, verbose: bool = False, out: str | None = None, defines=()) -> str:
-    lib = out or LIB
-    if not force and not defines and not _stale(lib):
-        return lib
+def build(force: bool = False, verbose: bool = False) -> str:
+    if not force and not _stale():
+        return LIB
     objs = []
-    tag = os.path.basename(lib).replace(".so", "")
     for src in SOURCES:
-        obj = os.path.join(HERE, "csrc", tag + "_" + os.path.basename(src).replace(".cu", ".o"))
+        obj = os.path.join(HERE, "csrc", os.path.basename(src).replace(".cu", ".o"))
         extra = ["-fmad=false"] if "voxel" in src else []   # numpy never fuses: no FMA contraction
-        cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", *extra, *defines,
+        cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", *extra,
                "--expt-relaxed-constexpr", "-Xptxas", "-v" if verbose else "-O3",
                "-c", os.path.join(HERE, src), "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
@@ -52,20 +48,15 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None, de
         if verbose:
             sys.stderr.write(r.stderr)
         objs.append(obj)
-    cmd = [nvcc(), *ARCH, "-shared", "-cudart", "static", "-o", lib, *objs]
+    cmd = [nvcc(), *ARCH, "-shared", "-cudart", "static", "-o", LIB, *objs]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
         raise RuntimeError("nvcc link failed")
     for o in objs:
         os.remove(o)
-    return lib
+    return LIB
 
 
 if __name__ == "__main__":
-    args = sys.argv[1:]
-    out = None
-    if "--out" in args:
-        out = os.path.join(HERE, args[args.index("--out") + 1])
-    defs = [a for a in args if a.startswith("-D")]
-    print(build(force="--force" in args or bool(defs), verbose="-v" in args, out=out, defines=defs))
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))

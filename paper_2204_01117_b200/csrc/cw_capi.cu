@@ -205,7 +205,7 @@ extern "C" int cw_ctx_create(const cw_grid* g, int precision, int device, cw_ctx
   if (const char* ev = std::getenv("CW_PCG_ZC")) best_zc = std::max(1, std::min(d.nz, std::atoi(ev)));
   c->zc = best_zc;
   c->U = tiles * ((d.nz + best_zc - 1) / best_zc);
-  c->pcg_blocks = maxb;   // every resident block: the ring phases balance planes exactly over them
+  c->pcg_blocks = std::min(c->U, maxb);
   if (const char* eb = std::getenv("CW_PCG_BLOCKS")) c->pcg_blocks = std::max(1, std::min(c->pcg_blocks, std::atoi(eb)));
   {
     const CUtensorMapDataType tdt = precision == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64;
@@ -222,7 +222,7 @@ extern "C" int cw_ctx_create(const cw_grid* g, int precision, int device, cw_ctx
     r2 |= make_tmap(&c->tm[8], CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, c->code, c, TX, TY);
     if (r2 != CW_OK) { cw_ctx_destroy(c); return CW_ERR_CUDA; }
   }
-  rc = alloc((void**)&c->part, 6 * (size_t)std::max(c->U, maxb) * sizeof(double));
+  rc = alloc((void**)&c->part, 6 * (size_t)c->U * sizeof(double));
   rc |= alloc((void**)&c->reg_part, (size_t)1024 * 64 * sizeof(double));
   rc |= alloc((void**)&c->reg_cnt, (size_t)1024 * 64 * sizeof(long long));
   rc |= alloc((void**)&c->reg_out, 64 * sizeof(double));
@@ -429,7 +429,6 @@ static int launch_pcg(cw_ctx* c, const cw_fields* f, DevReport* rep, double dt, 
   A.max_iter = 10000;                    // project(max_iter=10_000), solver.py:249
   A.precond = c->precond;
   A.ntx = c->ntx; A.nty = c->nty; A.zc = c->zc; A.U = c->U;
-  A.PS = std::max(c->U, c->pcg_blocks);
   A.timeout_ns = 20LL * 1000 * 1000 * 1000;
   A.probe_mode = 0;
   A.probe_iters = 0;

@@ -40,13 +40,7 @@
 
 namespace cw {
 
-#ifndef CW_PCG_TY
-#define CW_PCG_TY 32
-#endif
-#ifndef CW_PCG_MINB
-#define CW_PCG_MINB 1
-#endif
-constexpr int PCG_TX = 32, PCG_TY = CW_PCG_TY;           // tile (cells)
+constexpr int PCG_TX = 32, PCG_TY = 32;                 // tile (cells)
 constexpr int PCG_THREADS = 256;
 constexpr int PCG_RSTEP = PCG_THREADS / PCG_TX;         // 8 rows per thread sweep
 constexpr int PCG_RPT = PCG_TY / PCG_RSTEP;             // 4 rows per thread
@@ -87,7 +81,6 @@ struct PcgArgs {
   int max_iter;
   int precond;               // 0 identity, 1 jacobi (diag(1/d)), 2 AI1 (K^T K)
   int ntx, nty, zc, U;
-  int PS;                    // partial-slot stride = max(U, gridDim.x)
   long long timeout_ns;
   int probe_mode, probe_iters;   // developer timing probe (CW_PCG_PROBE), 0 = off
 };
@@ -257,42 +250,27 @@ __device__ __forceinline__ Unit unit_of(const PcgArgs<T>& A, int u) {
 
 // Jobs of one ring phase for this block: its units in order (unit
 // blockIdx.x + m*gridDim.x), each contributing planes k0-1 .. k1.
-// The ring phases balance work exactly: the (tile, z-plane) pairs are laid
-// out tile-major, z-minor, and block b owns the contiguous range
-// [b*J/B, (b+1)*J/B) of them (J = tiles * nz).  Each maximal run inside one
-// tile is a segment marched from k0-1 to k1 (one halo plane each side).
 struct JobCursor {
-  long long g1;     // end of this block's range
-  Unit t;           // current segment
-  int tile;
+  int unit;
+  Unit t;
   int kk;
 };
 
 template <typename T>
-__device__ __forceinline__ void cursor_seg(const PcgArgs<T>& A, JobCursor& c, long long g) {
-  const int nz = A.d.nz;
-  c.tile = (int)(g / nz);
-  c.t.i0 = (c.tile % A.ntx) * PCG_TX;
-  c.t.j0 = (c.tile / A.ntx) * PCG_TY;
-  c.t.k0 = (int)(g % nz);
-  c.t.k1 = (int)min((long long)nz, (long long)c.t.k0 + (c.g1 - g));
-  c.kk = c.t.k0 - 1;
-}
-template <typename T>
 __device__ __forceinline__ bool cursor_begin(const PcgArgs<T>& A, JobCursor& c) {
-  const long long J = (long long)A.ntx * A.nty * A.d.nz;
-  const long long g0 = J * blockIdx.x / gridDim.x;
-  c.g1 = J * (blockIdx.x + 1) / gridDim.x;
-  if (g0 >= c.g1) return false;
-  cursor_seg<T>(A, c, g0);
+  c.unit = blockIdx.x;
+  if (c.unit >= A.U) return false;
+  c.t = unit_of<T>(A, c.unit);
+  c.kk = c.t.k0 - 1;
   return true;
 }
 template <typename T>
 __device__ __forceinline__ bool cursor_next(const PcgArgs<T>& A, JobCursor& c) {
   if (c.kk < c.t.k1) { ++c.kk; return true; }
-  const long long g = (long long)c.tile * A.d.nz + c.t.k1;
-  if (g >= c.g1) return false;
-  cursor_seg<T>(A, c, g);
+  c.unit += gridDim.x;
+  if (c.unit >= A.U) return false;
+  c.t = unit_of<T>(A, c.unit);
+  c.kk = c.t.k0 - 1;
   return true;
 }
 
@@ -398,8 +376,8 @@ __device__ void phase0(const PcgArgs<T>& A, double* part, int unit, PcgShared<T>
   const double m2 = block_max(dmax, S.red);
   if (threadIdx.x == 0) {
     part[unit] = s0;
-    part[A.PS + unit] = m1;
-    part[2 * A.PS + unit] = m2;
+    part[A.U + unit] = m1;
+    part[2 * A.U + unit] = m2;
   }
   __syncthreads();
 }
@@ -630,7 +608,7 @@ __device__ void phaseB(const PcgArgs<T>& A, double* part, PcgShared<T>& S, uint8
   const double mx = block_max(rmax, S.red);
   if (threadIdx.x == 0) {
     part[blockIdx.x] = sm;
-    part[A.PS + blockIdx.x] = mx;
+    part[A.U + blockIdx.x] = mx;
   }
   __syncthreads();
 }
@@ -657,7 +635,7 @@ __device__ void finish_x(const PcgArgs<T>& A, int unit, T alpha, const T* __rest
 }
 
 template <typename T>
-__global__ void __launch_bounds__(PCG_THREADS, CW_PCG_MINB) k_pcg(const __grid_constant__ PcgArgs<T> A) {
+__global__ void __launch_bounds__(PCG_THREADS) k_pcg(const __grid_constant__ PcgArgs<T> A) {
   // dynamic smem is the only shared allocation of this kernel, so it starts
   // at the (1 KB aligned) base of the block's window; keep every access on
   // this array so the compiler emits LDS/STS rather than generic loads
@@ -683,13 +661,13 @@ __global__ void __launch_bounds__(PCG_THREADS, CW_PCG_MINB) k_pcg(const __grid_c
   unsigned ticket = 0;
   // two partial sets, alternated by phase, so one barrier per phase suffices;
   // phase 0 writes per unit, the ring phases per block (fixed unit->block map)
-  double* P[2] = {A.part, A.part + 3 * A.PS};
+  double* P[2] = {A.part, A.part + 3 * U};
 
   for (int u = blockIdx.x; u < U; u += B) phase0<T>(A, P[0], u, S);
   grid_barrier(A.bar, A.gate, rep, A.timeout_ns);
   const double b2 = fold_partials(P[0], U, 0, S.bc);
-  const double bmax = fold_partials(P[0] + A.PS, U, 1, S.bc);
-  const double divmax = fold_partials(P[0] + 2 * A.PS, U, 1, S.bc);
+  const double bmax = fold_partials(P[0] + U, U, 1, S.bc);
+  const double divmax = fold_partials(P[0] + 2 * U, U, 1, S.bc);
   if (blockIdx.x == 0 && threadIdx.x == 0) report_max<T>(rep, SLOT_DIV_BEFORE, (T)divmax);
   if (*(volatile int*)A.gate == 3) {
     if (blockIdx.x == 0 && threadIdx.x == 0) rep->status = 3;
@@ -711,7 +689,7 @@ __global__ void __launch_bounds__(PCG_THREADS, CW_PCG_MINB) k_pcg(const __grid_c
   phaseB<T>(A, P[1], S, ring, ticket, false, 0.0, 0, false);
   grid_barrier(A.bar, A.gate, rep, A.timeout_ns);
   double rz = fold_partials(P[1], B, 0, S.bc);
-  double rmax = fold_partials(P[1] + A.PS, B, 1, S.bc);
+  double rmax = fold_partials(P[1] + U, B, 1, S.bc);
   double crit = rz / b2;
   int it = 0, converged = 0, status = 0;
   bool finished = false;
@@ -745,7 +723,7 @@ __global__ void __launch_bounds__(PCG_THREADS, CW_PCG_MINB) k_pcg(const __grid_c
     phaseB<T>(A, P[1], S, ring, ticket, true, alpha, rsel, true);
     grid_barrier(A.bar, A.gate, rep, A.timeout_ns);
     const double rz_new = fold_partials(P[1], B, 0, S.bc);
-    rmax = fold_partials(P[1] + A.PS, B, 1, S.bc);
+    rmax = fold_partials(P[1] + U, B, 1, S.bc);
     rsel ^= 1;
     crit = rz_new / b2;
     if (*(volatile int*)A.gate == 3) { status = 3; break; }
