@@ -1,0 +1,99 @@
+"""GPU: the reference-facing pipeline (CompiledScenario, run_simulation,
+evaluate_objective, finite-difference gradients, snapshots) against the
+oracle on the same scenario JSON -- device voxelizer included."""
+import os
+
+import numpy as np
+import pytest
+
+from helpers import FIELDS, fields_of, oracle_compiled, rel_l2
+from paper_2204_01117_b200 import scenes
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+
+def _design_doc():
+    doc = scenes.block_city_design(48, 48, 16, 2.0, seed=5, nb=3, dt=0.25, settle_steps=12)
+    doc["design"] = doc["design"][:2]        # two parameters keep the oracle's N+1 runs short
+    return doc
+
+
+def test_run_simulation_matches_oracle():
+    from paper_2204_01117_b200.scenario import run_simulation, scenario_from_dict
+    doc = scenes.cuboid(24, 24, 12, 2.0, 0.3, steps=20)
+    out = run_simulation(scenario_from_dict(doc), steps=20)
+    comp = oracle_compiled(doc)
+    ost = comp.make_state()
+    iters = [comp.step_state(ost).pcg.iterations for _ in range(20)]
+    assert out["pcg_iterations"] == iters
+    got = fields_of(out["state"])
+    for n in FIELDS:
+        assert rel_l2(got[n], getattr(ost, n)) <= 1e-4, n
+    assert set(out["timings"]) >= {"advect", "project", "turbulence"}
+
+
+def test_evaluate_objective_matches_oracle():
+    from oracle import citywind_oracle as co
+    from paper_2204_01117_b200.optimize import evaluate_objective
+    from paper_2204_01117_b200.scenario import CompiledScenario, scenario_from_dict
+    doc = _design_doc()
+    comp = CompiledScenario.compile(scenario_from_dict(doc))
+    theta = np.array([d["initial"] + 0.5 * (d["hi"] - d["initial"]) for d in doc["design"]])
+    ev = evaluate_objective(comp, theta)
+    oloss, ospeeds = co.evaluate_objective(oracle_compiled(doc), theta)
+    assert abs(ev.loss - oloss) <= 1e-4 * abs(oloss)
+    np.testing.assert_allclose(ev.region_speeds, ospeeds, rtol=1e-4)
+
+
+def test_fd_gradient_matches_oracle():
+    from oracle import citywind_oracle as co
+    from paper_2204_01117_b200.optimize import DesignVector, ObjectiveSpec, finite_diff_gradient
+    from paper_2204_01117_b200.scenario import CompiledScenario, scenario_from_dict
+    doc = _design_doc()
+    sc = scenario_from_dict(doc)
+    comp = CompiledScenario.compile(sc)
+    theta = np.array([d["initial"] for d in doc["design"]])
+    grad, base = finite_diff_gradient(comp, theta, ObjectiveSpec.from_scenario(sc), eps=0.5)
+    oc = oracle_compiled(doc)
+    design = DesignVector.from_scenario(sc)
+    l0, _ = co.evaluate_objective(oc, theta)
+    og = []
+    for i in range(len(theta)):
+        h = 0.5 if theta[i] + 0.5 <= design.hi[i] else -0.5
+        t = theta.copy()
+        t[i] += h
+        og.append((co.evaluate_objective(oc, t)[0] - l0) / h)
+    assert abs(base.loss - l0) <= 1e-4 * abs(l0)
+    np.testing.assert_allclose(grad, og, rtol=2e-2, atol=1e-4 * abs(l0))
+
+
+def test_snapshot_roundtrip(tmp_path):
+    from paper_2204_01117_b200.io import read_snapshot, snapshot_to_state, write_snapshot
+    from paper_2204_01117_b200.scenario import CompiledScenario, scenario_from_dict
+    comp = CompiledScenario.compile(scenario_from_dict(scenes.cuboid(16, 12, 8, 2.0, 0.3)))
+    st = comp.make_state()
+    comp.step_states(st, 3)
+    path = os.path.join(tmp_path, "s.bin")
+    write_snapshot(path, st)
+    snap = read_snapshot(path)
+    assert snap.step == 3 and snap.arrays["u"].shape == (17, 12, 8)
+    back = snapshot_to_state(snap)
+    a, b = fields_of(st), fields_of(back)
+    for n in FIELDS:
+        np.testing.assert_array_equal(a[n], b[n])
+    assert torch.equal(back.labels_dev.cpu(), st.labels_dev.cpu())
+
+
+def test_snapshot_format_matches_oracle_layout(tmp_path):
+    """Payload is x-fastest float32 (io.py:30-31): the reference layout
+    transposed -- compare against the oracle's own field arrays."""
+    from paper_2204_01117_b200.io import read_snapshot, write_snapshot
+    from helpers import device_state
+    comp = oracle_compiled(scenes.cuboid(16, 12, 8, 2.0, 0.3))
+    ost = comp.make_state()
+    path = os.path.join(tmp_path, "s.bin")
+    write_snapshot(path, device_state(ost, torch.float32))
+    snap = read_snapshot(path)
+    for n in ("u", "v", "w", "k"):
+        np.testing.assert_array_equal(snap.arrays[n], getattr(ost, n).astype(np.float32).transpose(2, 1, 0))
