@@ -122,17 +122,23 @@ def block_city_design(nx: int = 256, ny: int = 256, nz: int = 64, h: float = 2.0
                        "object": o["name"], "transform": "extent_x"})
     Lx, Ly = nx * h, ny * h
     px, py = 0.7 * Lx / nb, 0.7 * Ly / nb
+    x0, y0 = 0.15 * Lx, 0.15 * Ly
+    zt = max(6.0, 3.0 * h)
     regions = []
-    for r in range(3):  # sheltered gaps between blocks (heat pockets)
-        cx = 0.15 * Lx + (1.5 + r) * px - 0.05 * px
-        cy = 0.15 * Ly + (1.5 + r) * py - 0.05 * py
-        regions.append({"name": f"court{r}", "lo": [cx - 0.1 * px, cy - 0.1 * py, 0.0],
-                        "hi": [cx + 0.1 * px, cy + 0.1 * py, 6.0]})
-    for r in range(3):  # corner gaps (wind comfort)
-        cx = 0.15 * Lx + (r + 1) * px - 0.1 * px
-        cy = 0.15 * Ly + 0.5 * py
-        regions.append({"name": f"gap{r}", "lo": [cx - 0.08 * px, cy - 0.1 * py, 0.0],
-                        "hi": [cx + 0.08 * px, cy + 0.1 * py, 6.0]})
+    # pedestrian-level street slabs between block columns / rows: a block
+    # covers at most 0.75 of its pitch (0.9 with the extent design range) and
+    # trees start at 0.82, so [0.76, 0.81] of a pitch is open street for most
+    # of the slab's length
+    for r in range(3):  # streets along y, behind block column r (sheltered: heat pockets)
+        c = r % nb
+        regions.append({"name": f"street_y{r}",
+                        "lo": [x0 + c * px + 0.76 * px, y0, 0.0],
+                        "hi": [x0 + c * px + 0.81 * px + h, y0 + nb * py, zt]})
+    for r in range(3):  # streets along x (wind comfort)
+        c = r % nb
+        regions.append({"name": f"street_x{r}",
+                        "lo": [x0, y0 + c * py + 0.76 * py, 0.0],
+                        "hi": [x0 + nb * px, y0 + c * py + 0.81 * py + h, zt]})
     doc["design"] = design
     doc["objective"] = {"regions": regions, "target_speed": 0.55,
                         "settle_steps": settle_steps, "avg_fraction": 0.25}

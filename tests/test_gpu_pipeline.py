@@ -19,6 +19,17 @@ def _design_doc():
     return doc
 
 
+def test_design_regions_contain_air():
+    from paper_2204_01117_b200.scenario import CompiledScenario, scenario_from_dict
+    from paper_2204_01117_b200.solver import region_average_speeds
+    doc = _design_doc()
+    comp = CompiledScenario.compile(scenario_from_dict(doc))
+    st = comp.make_state()
+    regs = doc["objective"]["regions"]
+    _, counts = region_average_speeds(st, [r["lo"] for r in regs], [r["hi"] for r in regs])
+    assert np.all(counts > 0), counts
+
+
 def test_run_simulation_matches_oracle():
     from paper_2204_01117_b200.scenario import run_simulation, scenario_from_dict
     doc = scenes.cuboid(24, 24, 12, 2.0, 0.3, steps=20)

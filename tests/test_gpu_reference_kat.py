@@ -207,14 +207,19 @@ def test_walled_channel_core_near_inflow():
     np.testing.assert_allclose(st.u[2:-2, 4:-4, :], 2.0, atol=1e-2)
 
 
-def test_divergence_reduced_every_step_and_invariants():
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+def test_divergence_reduced_every_step_and_invariants(dtype):
+    """test_solver.py:273-283 (fp64: the reference's 1e-4 drop).  A float32
+    field of O(2 m/s) velocities resolves divergence only to ~eps32*|u|/h,
+    so the fp32 run gates on max(1e-4 * before, 100 * eps32 * |u|max / h)."""
     g, lab = channel(24, 16)
     psys, pre = system(g, lab)
     params, prof = SolverParams(dt=0.1, u_ref=2.0), InletProfile(speed=2.0)
-    st = solver.make_initial_state(g, lab, None, params, prof, mode="rest")
+    st = solver.make_initial_state(g, lab, None, params, prof, mode="rest", dtype=dtype)
+    floor = 0.0 if dtype == torch.float64 else 100 * np.finfo(np.float32).eps * 2.5 / g.dx
     for rep in solver.step_many(st, params, psys, pre, prof, 50):
-        if rep.div_before > 1e-6:
-            assert rep.div_after <= 1e-4 * rep.div_before
+        if rep.div_before > 1e-12:
+            assert rep.div_after <= max(1e-4 * rep.div_before, floor)
     st.validate()
 
 
