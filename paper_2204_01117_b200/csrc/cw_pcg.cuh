@@ -164,26 +164,11 @@ __device__ __forceinline__ void grid_barrier(unsigned* bar, int* gate, DevReport
 // mode 0: sum, 1: max.  Result broadcast to all threads.
 __device__ __forceinline__ double fold_partials(const double* part, int n, int mode, double* sh) {
   if (threadIdx.x < 32) {
-    // issue every load of this lane before the first add (one L2 round trip
-    // instead of n/32 dependent ones), then fold in index order
-    constexpr int MAXL = 12;                  // first 384 partials in one round trip
-    double v[MAXL];
-#pragma unroll
-    for (int t = 0; t < MAXL; ++t) {
-      const int q = threadIdx.x + 32 * t;
-      v[t] = q < n ? __ldcg(part + q) : 0.0;
-    }
     double a = 0.0;
-#pragma unroll
-    for (int t = 0; t < MAXL; ++t) {
-      if (threadIdx.x + 32 * t >= n) break;
-      if (mode == 0) a += v[t];
-      else a = (v[t] > a || v[t] != v[t]) ? v[t] : a;
-    }
-    for (int q = threadIdx.x + 32 * MAXL; q < n; q += 32) {   // rest, same order
-      const double w = __ldcg(part + q);
-      if (mode == 0) a += w;
-      else a = (w > a || w != w) ? w : a;
+    for (int q = threadIdx.x; q < n; q += 32) {
+      const double v = __ldcg(part + q);
+      if (mode == 0) a += v;
+      else a = (v > a || v != v) ? v : a;
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
