@@ -326,6 +326,34 @@ def run_b200(args):
            "path": "solver.step() on a host-resident state: 7 fields pinned H2D, step, 7 fields D2H, per step"}
 
     kmax = float(state.fields["k"].max())
+
+    # seconds per design evaluation (C4 recipe on the C3 city: 16 extent
+    # parameters, 6 street regions), one design per GPU, voxelize + settle +
+    # trailing-window region sums through optimize.evaluate_objective
+    design = None
+    if not args.no_design:
+        from paper_2204_01117_b200 import scenes as _sc
+        from paper_2204_01117_b200.optimize import evaluate_objective
+        ddoc = _sc.block_city_design(256, 256, 64, 2.0, 0, 6, args.dt, settle_steps=args.settle)
+        dcomp = CompiledScenario.compile(scenario_from_dict(ddoc), dtype=torch.float32)
+        theta = np.array([d["initial"] for d in ddoc["design"]])
+        theta[rank % len(theta)] += 0.1 * (ddoc["design"][rank % len(theta)]["hi"]
+                                           - ddoc["design"][rank % len(theta)]["initial"])
+        barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        ev = evaluate_objective(dcomp, theta)
+        torch.cuda.synchronize()
+        t_eval = time.perf_counter() - t0
+        if dist is not None:
+            t = torch.tensor([t_eval], device="cuda", dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            t_eval = float(t.item())
+        design = {"seconds_per_evaluation": t_eval, "evaluations_per_hour": 3600.0 * world / t_eval,
+                  "settle_steps": args.settle, "n_params": len(theta), "designs_in_parallel": world,
+                  "loss": ev.loss,
+                  "note": "C4 recipe (16 params, 6 regions) on the C3 city; settle kept inside the "
+                          "reference model's stable window at dt 0.2"}
     if rank != 0:
         if dist is not None:
             dist.destroy_process_group()
@@ -348,6 +376,7 @@ def run_b200(args):
                        "precision": "fp32 fields; PCG residual and dot products in fp64"},
             "e2e": e2e, "gpu_launches": launches, "roofline": roofline, "cpu_baseline": cpu,
             "clocks": clocks.summary(), "pcg_iterations": iters, "voxelize_s": voxelize_s,
+            "design_eval": design,
             "k_max_end": kmax}
     print(json.dumps(line), flush=True)
     if dist is not None:
@@ -362,6 +391,8 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--dt", type=float, default=0.2)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-design", action="store_true")
+    ap.add_argument("--settle", type=int, default=120)
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
