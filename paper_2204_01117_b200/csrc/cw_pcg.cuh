@@ -220,6 +220,7 @@ struct PcgShared {
   T lut[64 * 4];
   union {
     T pa[2][HH][HW];      // phase 0 planes
+    PcgWork<T> wk;        // phase B
   };
   double red[32];
   double bc[4];
@@ -381,25 +382,16 @@ __device__ void phase0(const PcgArgs<T>& A, double* part, int unit, PcgShared<T>
   __syncthreads();
 }
 
-// ---- register-tiled thread mapping of the ring phases ----------------------
-// Thread (lx, w) owns column lx and the 4 consecutive rows 4w..4w+3 of the
-// 32x32 tile: row neighbours come from its own registers (plus one extra row
-// each side), column neighbours from warp shuffles (lane 0 / lane 31 read the
-// halo columns of the stage themselves).  No shared work planes and no
-// barrier besides the one that releases the stage.
-constexpr int RT = 4;   // rows per thread
-static_assert(PCG_TY == RT * (PCG_THREADS / PCG_TX), "tile rows = 4 x warps");
-
 // ---- phase A: p' = z + beta p, x += alpha_prev p, Ap = A p' ---------------
 template <typename T>
 __device__ void phaseA(const PcgArgs<T>& A, double* part, PcgShared<T>& S, uint8_t* ring, unsigned& ticket,
                        bool first, T beta, bool upd_x, T alpha_prev, int pin_sel) {
   using L = StageLayout<T>;
+  static_assert(L::DEPTH >= 3, "phase A holds two stages");
   const Dims& d = A.d;
   const CUtensorMap* tp = pin_sel == 0 ? &A.tm_p0 : &A.tm_p1;
   T* __restrict__ pout = pin_sel == 0 ? A.p1 : A.p0;
-  const int lx = threadIdx.x % PCG_TX, w = threadIdx.x / PCG_TX;
-  const int r0 = RT * w;                       // first own row
+  const int lx = threadIdx.x % PCG_TX, ly0 = threadIdx.x / PCG_TX;
   const long long pplane = (long long)A.nxp * d.ny;
   JobCursor prod, cons;
   double acc = 0.0;
@@ -415,14 +407,21 @@ __device__ void phaseA(const PcgArgs<T>& A, double* part, PcgShared<T>& S, uint8
         more = cursor_next<T>(A, prod);
       }
     }
-    unsigned j = 0;
-    // per own row: previous plane's p', plane kk-1's pending A p (without its
-    // +z term), its p' and new x
-    T pm[RT], pcur[RT], xn[RT];
-    double part_ap[RT];
-    bool pend[RT];
+    auto pnew = [&](const uint8_t* st, int hy, int hx) -> T {
+      const T* zz = reinterpret_cast<const T*>(st + L::A_Z);
+      const T* pp = reinterpret_cast<const T*>(st + L::A_P);
+      const int o = Halo<T>::at(hy, hx);
+      const T zv = zz[o];
+      return first ? zv : zv + beta * pp[o];
+    };
+    unsigned j = 0;     // consumer job number in this phase
+    // per own row: the previous plane's p', and plane kk-1's pending result
+    // (A p without its +z term, new x, own flag) finished once plane kk lands
+    T pm[PCG_RPT], pcur[PCG_RPT], xn[PCG_RPT];
+    double part_ap[PCG_RPT];
+    bool pend[PCG_RPT];
 #pragma unroll
-    for (int t = 0; t < RT; ++t) { pm[t] = (T)0; pend[t] = false; }
+    for (int q = 0; q < PCG_RPT; ++q) { pm[q] = (T)0; pend[q] = false; }
     bool live = true;
     while (live) {
       const unsigned tk = t0 + j;
@@ -432,63 +431,39 @@ __device__ void phaseA(const PcgArgs<T>& A, double* part, PcgShared<T>& S, uint8
       const Unit u = cons.t;
       const int i = u.i0 + lx;
       const int kk = cons.kk;
-      const T* zz = reinterpret_cast<const T*>(st + L::A_Z);
-      const T* pp = reinterpret_cast<const T*>(st + L::A_P);
-      auto pnew = [&](int hy, int hx) -> T {
-        const int o = Halo<T>::at(hy, hx);
-        return first ? zz[o] : zz[o] + beta * pp[o];
-      };
-      // own rows r0..r0+3 (halo rows r0+1..r0+4), plus rows below / above
-      T P[RT];
-#pragma unroll
-      for (int t = 0; t < RT; ++t) P[t] = pnew(r0 + t + 1, lx + 1);
-      const T Pb = pnew(r0, lx + 1), Pa = pnew(r0 + RT + 1, lx + 1);
-      const bool own_plane = kk >= u.k0 && kk < u.k1;
-      T Lf[RT], Rt[RT];
-#pragma unroll
-      for (int t = 0; t < RT; ++t) {
-        Lf[t] = __shfl_up_sync(0xffffffffu, P[t], 1);
-        Rt[t] = __shfl_down_sync(0xffffffffu, P[t], 1);
-      }
-      if (own_plane) {
-        if (lx == 0)
-#pragma unroll
-          for (int t = 0; t < RT; ++t) Lf[t] = pnew(r0 + t + 1, 0);
-        if (lx == PCG_TX - 1)
-#pragma unroll
-          for (int t = 0; t < RT; ++t) Rt[t] = pnew(r0 + t + 1, PCG_TX + 1);
-      }
       const T* xx = reinterpret_cast<const T*>(st + L::A_X);
+      const T* pp = reinterpret_cast<const T*>(st + L::A_P);
       const uint8_t* cc = st + L::A_C;
 #pragma unroll
-      for (int t = 0; t < RT; ++t) {
-        const int ly = r0 + t, jj = u.j0 + ly;
-        if (pend[t]) {
-          // finish plane kk-1 with its +z neighbour.  A p is accumulated in
-          // float64 from the stored p: the 7-point difference of a smooth p
-          // cancels d*p almost entirely, so float32 arithmetic would leave a
-          // relative error ~eps*d|p|/|Ap|
-          const long long q = (long long)(kk - 1) * pplane + (long long)jj * A.nxp + i;
-          const double ap = part_ap[t] - (double)A.wz * (double)P[t];
-          pout[q] = pcur[t];
-          A.Ap[q] = (T)ap;
-          if (upd_x) A.x[q] = xn[t];
-          acc += (double)pcur[t] * ap;
-          pend[t] = false;
+      for (int q = 0; q < PCG_RPT; ++q) {
+        const int ly = ly0 + q * PCG_RSTEP, jj = u.j0 + ly;
+        const T pn = pnew(st, ly + 1, lx + 1);     // own p' on plane kk
+        if (pend[q]) {
+          // finish plane kk-1: add the +z neighbour (this plane) and store.
+          // A p is accumulated in float64 from the stored p: the 7-point
+          // difference of a smooth p cancels d*p almost entirely, so float32
+          // arithmetic would leave a relative error ~eps*d|p|/|Ap|
+          const long long pc_ = (long long)(kk - 1) * pplane + (long long)jj * A.nxp + i;
+          const double ap = part_ap[q] - (double)A.wz * (double)pn;
+          pout[pc_] = pcur[q];
+          A.Ap[pc_] = (T)ap;
+          if (upd_x) A.x[pc_] = xn[q];
+          acc += (double)pcur[q] * ap;
+          pend[q] = false;
         }
-        if (own_plane) {
+        if (kk >= u.k0 && kk < u.k1) {
           const uint8_t cd = cc[ly * PCG_TX + lx];
           if ((cd & 64) && i < d.nx && jj < d.ny) {
-            const T dn = t > 0 ? P[t - 1] : Pb, up = t < RT - 1 ? P[t + 1] : Pa;
-            part_ap[t] = (double)S.lut[(cd & 63) * 4] * (double)P[t] -
-                         ((double)A.wx * ((double)Lf[t] + (double)Rt[t]) +
-                          (double)A.wy * ((double)dn + (double)up) + (double)A.wz * (double)pm[t]);
-            pcur[t] = P[t];
-            if (upd_x) xn[t] = xx[ly * PCG_TX + lx] + alpha_prev * pp[Halo<T>::at(ly + 1, lx + 1)];
-            pend[t] = true;
+            part_ap[q] = (double)S.lut[(cd & 63) * 4] * (double)pn -
+                         ((double)A.wx * ((double)pnew(st, ly + 1, lx) + (double)pnew(st, ly + 1, lx + 2)) +
+                          (double)A.wy * ((double)pnew(st, ly, lx + 1) + (double)pnew(st, ly + 2, lx + 1)) +
+                          (double)A.wz * (double)pm[q]);
+            pcur[q] = pn;
+            if (upd_x) xn[q] = xx[ly * PCG_TX + lx] + alpha_prev * pp[Halo<T>::at(ly + 1, lx + 1)];
+            pend[q] = true;
           }
         }
-        pm[t] = P[t];
+        pm[q] = pn;
       }
       live = cursor_next<T>(A, cons);
       ++j;
@@ -508,10 +483,9 @@ __device__ void phaseA(const PcgArgs<T>& A, double* part, PcgShared<T>& S, uint8
 }
 
 // ---- phase B: r' = r - alpha Ap, z = W r' ----------------------------------
-// Per landed plane kk each thread forms q = r'/d on its rows (+ the row
-// above), y = s (r' + w sum_a w_a q_{-a}) on its rows (+ the row above, and
-// lane 31 the column right of the tile), and finishes z on plane kk-1 from
-// the y it kept in registers.
+// One pass per landed plane kk computes q = r'/d on the y-tile (recomputing
+// the two in-plane lower neighbours from the stage instead of staging q) and
+// y(kk); after one barrier the own cells finish z on plane kk-1.
 template <typename T>
 __device__ void phaseB(const PcgArgs<T>& A, double* part, PcgShared<T>& S, uint8_t* ring, unsigned& ticket,
                        bool use_ap, double alpha, int rin_sel, bool write_r) {
@@ -521,10 +495,9 @@ __device__ void phaseB(const PcgArgs<T>& A, double* part, PcgShared<T>& S, uint8
   double* __restrict__ rout = rin_sel == 0 ? A.r1 : A.r0;
   const T om = A.om;
   const T c0 = ((T)2 - om) * om;          // s * d
-  const int lx = threadIdx.x % PCG_TX, w = threadIdx.x / PCG_TX;
-  const int r0 = RT * w;
-  const bool last = lx == PCG_TX - 1;
+  const int lx = threadIdx.x % PCG_TX, ly0 = threadIdx.x / PCG_TX;
   const long long pplane = (long long)A.nxp * d.ny;
+  PcgWork<T>& W = S.wk;
   JobCursor prod, cons;
   double acc = 0.0, rmax = 0.0;
   if (cursor_begin<T>(A, cons)) {
@@ -540,14 +513,10 @@ __device__ void phaseB(const PcgArgs<T>& A, double* part, PcgShared<T>& S, uint8
       }
     }
     unsigned j = 0;
-    // plane kk-1 state: q on own rows + the row above (+ lane 31: column 33),
-    // y, its +x / +y neighbours, residual and code of the own cells
-    T qm[RT + 1], qm33[RT + 1];
-    T yprev[RT], yRprev[RT], yUprev[RT];
-    double rprev[RT];
-    uint8_t cprev[RT];
+    double rprev[PCG_RPT], rown[PCG_RPT];
+    uint8_t cprev[PCG_RPT], cown[PCG_RPT];
 #pragma unroll
-    for (int t = 0; t < RT; ++t) { rprev[t] = 0.0; cprev[t] = 0; }
+    for (int q = 0; q < PCG_RPT; ++q) { rprev[q] = 0.0; cprev[q] = 0; }
     bool live = true;
     while (live) {
       const unsigned tk = t0 + j;
@@ -556,6 +525,8 @@ __device__ void phaseB(const PcgArgs<T>& A, double* part, PcgShared<T>& S, uint8
       mbar_wait(&S.full[s], (tk / L::DEPTH) & 1u);
       const Unit u = cons.t;
       const int kk = cons.kk;
+      const int qb = j & 1, qbp = (j + 1) & 1;       // q planes (kk, kk-1)
+      const int yb = j % 3, ybp = (j + 2) % 3;       // y planes (kk, kk-1), 3 = hazard-free
       const double* rr = reinterpret_cast<const double*>(st + L::B_R);
       const T* aa = reinterpret_cast<const T*>(st + L::B_AP);
       const uint8_t* cc = st + L::B_C;
@@ -564,108 +535,69 @@ __device__ void phaseB(const PcgArgs<T>& A, double* part, PcgShared<T>& S, uint8
         if (use_ap) r = r - alpha * (double)aa[Halo<T>::at(hy, hx)];
         return r;
       };
-      auto code = [&](int hy, int hx) -> uint8_t { return cc[Halo<uint8_t>::at(hy, hx)]; };
-      // q and codes: halo rows r0 .. r0+RT+1 (row below, own rows, row above)
-      T Q[RT + 2];
-      uint8_t C[RT + 2];
-      double rown[RT];
+      auto qval = [&](int hy, int hx) -> T {
+        return (T)rnew(hy, hx) * S.lut[(cc[Halo<uint8_t>::at(hy, hx)] & 63) * 4 + 1];
+      };
 #pragma unroll
-      for (int t = 0; t < RT + 2; ++t) {
-        const int hy = r0 + t;
-        C[t] = code(hy, lx + 1);
-        const double r = rnew(hy, lx + 1);
-        if (t >= 1 && t <= RT) rown[t - 1] = r;
-        Q[t] = (T)r * S.lut[(C[t] & 63) * 4 + 1];
+      for (int q = 0; q < PCG_RPT; ++q) {            // own residuals (float64) and codes
+        const int hy = ly0 + q * PCG_RSTEP + 1;
+        rown[q] = rnew(hy, lx + 1);
+        cown[q] = cc[Halo<uint8_t>::at(hy, lx + 1)];
       }
-      // lane 31: column hx = 33 (the y column right of the tile), rows r0..r0+RT+1
-      T Q33[RT + 2];
-      uint8_t C33[RT + 2];
-      if (last) {
-#pragma unroll
-        for (int t = 0; t < RT + 2; ++t) {
-          C33[t] = code(r0 + t, PCG_TX + 1);
-          Q33[t] = (T)rnew(r0 + t, PCG_TX + 1) * S.lut[(C33[t] & 63) * 4 + 1];
+      {
+        T* qcur = &W.qb[qb][0][0];
+        const T* qprv = &W.qb[qbp][0][0];
+        T* ycur = &W.yb[yb][0][0];
+        const bool do_y = kk >= u.k0 && A.precond == 2;
+        for (int e = threadIdx.x; e < YH * YW; e += PCG_THREADS) {
+          const int yx = e % YW, yy = e / YW;
+          const int hy = yy + 1, hx = yx + 1;
+          const uint8_t cd = cc[Halo<uint8_t>::at(hy, hx)];
+          const T qp = (T)rnew(hy, hx) * S.lut[(cd & 63) * 4 + 1];
+          qcur[e] = qp;
+          if (do_y) {
+            // y = s (r + w sum_a w_a q_{-a}) with s r = (2-w) w q
+            const T sv = S.lut[(cd & 63) * 4 + 2];
+            ycur[e] = c0 * qp + sv * (om * (A.wx * qval(hy, hx - 1) + A.wy * qval(hy - 1, hx) + A.wz * qprv[e]));
+          }
         }
       }
-      // left neighbours of q on rows 1..RT+1 (lane 0 reads halo column 0)
-      T QL[RT + 1];
-#pragma unroll
-      for (int t = 0; t < RT + 1; ++t) QL[t] = __shfl_up_sync(0xffffffffu, Q[t + 1], 1);
-      if (lx == 0)
-#pragma unroll
-        for (int t = 0; t < RT + 1; ++t) {
-          const int hy = r0 + t + 1;
-          QL[t] = (T)rnew(hy, 0) * S.lut[(code(hy, 0) & 63) * 4 + 1];
-        }
       __syncthreads();
       if (threadIdx.x == 0 && more) {     // the raw stage is free: refill it
         issue_B<T>(A, ring, S.full, t0 + issued, prod, tr);
         ++issued;
         more = cursor_next<T>(A, prod);
       }
-      const bool do_y = kk >= u.k0 && A.precond == 2;
-      T Y[RT + 1], Y33[RT];
-      if (do_y) {
-        // y on own rows and the row above: q own, left, below, and plane kk-1
-#pragma unroll
-        for (int t = 0; t < RT + 1; ++t) {
-          const T sv = S.lut[(C[t + 1] & 63) * 4 + 2];
-          Y[t] = c0 * Q[t + 1] + sv * (om * (A.wx * QL[t] + A.wy * Q[t] + A.wz * qm[t]));
-        }
-        if (last)
-#pragma unroll
-          for (int t = 0; t < RT; ++t) {
-            const T sv = S.lut[(C33[t + 1] & 63) * 4 + 2];
-            Y33[t] = c0 * Q33[t + 1] + sv * (om * (A.wx * Q[t + 1] + A.wy * Q33[t] + A.wz * qm33[t]));
-          }
-      }
-      // finish z on plane kk-1 (needs y of plane kk on the own rows)
       if (kk >= u.k0 + 1) {
         const int k = kk - 1;
         const int i = u.i0 + lx;
+        const T* y0 = &W.yb[ybp][0][0];
+        const T* y1 = &W.yb[yb][0][0];
 #pragma unroll
-        for (int t = 0; t < RT; ++t) {
-          const int jj = u.j0 + r0 + t;
-          const uint8_t cd = cprev[t];
+        for (int q = 0; q < PCG_RPT; ++q) {
+          const int ly = ly0 + q * PCG_RSTEP, jj = u.j0 + ly;
+          const uint8_t cd = cprev[q];
           if ((cd & 64) && i < d.nx && jj < d.ny) {
-            const long long q = k * pplane + (long long)jj * A.nxp + i;
+            const long long pc_ = k * pplane + (long long)jj * A.nxp + i;
             T zv;
+            const int o = ly * YW + lx;
             const T invd = S.lut[(cd & 63) * 4 + 1];
             if (A.precond == 2)
-              zv = yprev[t] + om * invd * (A.wx * yRprev[t] + A.wy * yUprev[t] + A.wz * Y[t]);
+              zv = y0[o] + om * invd * (A.wx * y0[o + 1] + A.wy * y0[o + YW] + A.wz * y1[o]);
             else if (A.precond == 1)
-              zv = (T)rprev[t] * invd;
+              zv = (T)rprev[q] * invd;
             else
-              zv = (T)rprev[t];
-            A.z[q] = zv;
-            if (write_r) rout[q] = rprev[t];
-            acc += rprev[t] * (double)zv;
-            const double ar = fabs(rprev[t]);
+              zv = (T)rprev[q];
+            A.z[pc_] = zv;
+            if (write_r) rout[pc_] = rprev[q];
+            acc += rprev[q] * (double)zv;
+            const double ar = fabs(rprev[q]);
             rmax = (ar > rmax || ar != ar) ? ar : rmax;
           }
         }
       }
-      // roll: plane kk becomes plane kk-1
-      if (do_y) {
 #pragma unroll
-        for (int t = 0; t < RT; ++t) {
-          const T yr = __shfl_down_sync(0xffffffffu, Y[t], 1);
-          yprev[t] = Y[t];
-          yRprev[t] = last ? Y33[t] : yr;
-          yUprev[t] = Y[t + 1];
-        }
-      } else {
-        // keep the warp converged for the shuffles above in later jobs
-#pragma unroll
-        for (int t = 0; t < RT; ++t) (void)__shfl_down_sync(0xffffffffu, (T)0, 1);
-      }
-#pragma unroll
-      for (int t = 0; t < RT + 1; ++t) {
-        qm[t] = Q[t + 1];
-        if (last) qm33[t] = Q33[t + 1];
-      }
-#pragma unroll
-      for (int t = 0; t < RT; ++t) { rprev[t] = rown[t]; cprev[t] = C[t + 1]; }
+      for (int q = 0; q < PCG_RPT; ++q) { rprev[q] = rown[q]; cprev[q] = cown[q]; }
       live = cursor_next<T>(A, cons);
       ++j;
     }
@@ -703,7 +635,7 @@ __device__ void finish_x(const PcgArgs<T>& A, int unit, T alpha, const T* __rest
 }
 
 template <typename T>
-__global__ void __launch_bounds__(PCG_THREADS, 2) k_pcg(const __grid_constant__ PcgArgs<T> A) {
+__global__ void __launch_bounds__(PCG_THREADS) k_pcg(const __grid_constant__ PcgArgs<T> A) {
   // dynamic smem is the only shared allocation of this kernel, so it starts
   // at the (1 KB aligned) base of the block's window; keep every access on
   // this array so the compiler emits LDS/STS rather than generic loads
