@@ -38,6 +38,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     for src in SOURCES:
         obj = os.path.join(HERE, "csrc", os.path.basename(src).replace(".cu", ".o"))
         extra = ["-fmad=false"] if "voxel" in src else []   # numpy never fuses: no FMA contraction
+        extra += os.environ.get("CW_NVCC_DEFS", "").split()     # developer variants, e.g. -DCW_PCG_MINB=2
         cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", *extra,
                "--expt-relaxed-constexpr", "-Xptxas", "-v" if verbose else "-O3",
                "-c", os.path.join(HERE, src), "-o", obj]

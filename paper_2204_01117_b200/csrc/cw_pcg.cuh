@@ -41,7 +41,13 @@
 namespace cw {
 
 constexpr int PCG_TX = 32, PCG_TY = 32;                 // tile (cells)
-constexpr int PCG_THREADS = 256;
+#ifndef CW_PCG_THREADS
+#define CW_PCG_THREADS 256
+#endif
+#ifndef CW_PCG_MINB
+#define CW_PCG_MINB 2
+#endif
+constexpr int PCG_THREADS = CW_PCG_THREADS;
 constexpr int PCG_RSTEP = PCG_THREADS / PCG_TX;         // 8 rows per thread sweep
 constexpr int PCG_RPT = PCG_TY / PCG_RSTEP;             // 4 rows per thread
 constexpr int BOX_Y = PCG_TY + 2;
@@ -211,8 +217,8 @@ struct StageLayout {
 
 template <typename T>
 struct PcgWork {          // phase-B work planes
-  T qb[2][YH][YW];        // q = r'/d on the y-tile, planes kk and kk-1
-  T yb[3][YH][YW];        // y, planes kk and kk-1 (+1 for a hazard-free ring)
+  T qb[3][HH][HW];        // q = r'/d on the halo tile, planes kk, kk-1 (+1 hazard-free)
+  T yb[2][YH][YW];        // y on the y tile, planes kk and kk-1
 };
 
 template <typename T>
@@ -428,6 +434,18 @@ __device__ void phaseA(const PcgArgs<T>& A, double* part, PcgShared<T>& S, uint8
       const int s = tk % L::DEPTH;
       const uint8_t* st = ring + (size_t)s * L::STAGE;
       mbar_wait(&S.full[s], (tk / L::DEPTH) & 1u);
+      if (A.probe_mode == 4 || A.probe_mode == 7) {   // timing probe: stream the stages only
+        live = cursor_next<T>(A, cons);
+        ++j;
+        __syncthreads();
+        if (threadIdx.x == 0)
+          while (more && issued < j + L::DEPTH) {
+            issue_A<T>(A, ring, S.full, t0 + issued, prod, tp);
+            ++issued;
+            more = cursor_next<T>(A, prod);
+          }
+        continue;
+      }
       const Unit u = cons.t;
       const int i = u.i0 + lx;
       const int kk = cons.kk;
@@ -523,10 +541,23 @@ __device__ void phaseB(const PcgArgs<T>& A, double* part, PcgShared<T>& S, uint8
       const int s = tk % L::DEPTH;
       const uint8_t* st = ring + (size_t)s * L::STAGE;
       mbar_wait(&S.full[s], (tk / L::DEPTH) & 1u);
+      if (A.probe_mode == 7) {   // timing probe: stream the stages only
+        __syncthreads();
+        if (threadIdx.x == 0 && more) {
+          issue_B<T>(A, ring, S.full, t0 + issued, prod, tr);
+          ++issued;
+          more = cursor_next<T>(A, prod);
+        }
+        live = cursor_next<T>(A, cons);
+        ++j;
+        continue;
+      }
       const Unit u = cons.t;
       const int kk = cons.kk;
-      const int qb = j & 1, qbp = (j + 1) & 1;       // q planes (kk, kk-1)
-      const int yb = j % 3, ybp = (j + 2) % 3;       // y planes (kk, kk-1), 3 = hazard-free
+      T* qcur = &W.qb[j % 3][0][0];                  // q planes kk, kk-1 (ring of 3)
+      const T* qprv = &W.qb[(j + 2) % 3][0][0];
+      T* ycur = &W.yb[j & 1][0][0];                  // y planes kk, kk-1 (ring of 2)
+      const T* yprv = &W.yb[(j + 1) & 1][0][0];
       const double* rr = reinterpret_cast<const double*>(st + L::B_R);
       const T* aa = reinterpret_cast<const T*>(st + L::B_AP);
       const uint8_t* cc = st + L::B_C;
@@ -535,44 +566,48 @@ __device__ void phaseB(const PcgArgs<T>& A, double* part, PcgShared<T>& S, uint8
         if (use_ap) r = r - alpha * (double)aa[Halo<T>::at(hy, hx)];
         return r;
       };
-      auto qval = [&](int hy, int hx) -> T {
-        return (T)rnew(hy, hx) * S.lut[(cc[Halo<uint8_t>::at(hy, hx)] & 63) * 4 + 1];
-      };
-#pragma unroll
-      for (int q = 0; q < PCG_RPT; ++q) {            // own residuals (float64) and codes
-        const int hy = ly0 + q * PCG_RSTEP + 1;
-        rown[q] = rnew(hy, lx + 1);
-        cown[q] = cc[Halo<uint8_t>::at(hy, lx + 1)];
-      }
-      {
-        T* qcur = &W.qb[qb][0][0];
-        const T* qprv = &W.qb[qbp][0][0];
-        T* ycur = &W.yb[yb][0][0];
-        const bool do_y = kk >= u.k0 && A.precond == 2;
-        for (int e = threadIdx.x; e < YH * YW; e += PCG_THREADS) {
-          const int yx = e % YW, yy = e / YW;
-          const int hy = yy + 1, hx = yx + 1;
+      // pass 1: q = r'/d once per element of the 34 x 34 halo tile
+      if (A.precond == 2) {
+        for (int e = threadIdx.x; e < HH * HW; e += PCG_THREADS) {
+          const int hy = e / HW, hx = e - hy * HW;
           const uint8_t cd = cc[Halo<uint8_t>::at(hy, hx)];
-          const T qp = (T)rnew(hy, hx) * S.lut[(cd & 63) * 4 + 1];
-          qcur[e] = qp;
-          if (do_y) {
-            // y = s (r + w sum_a w_a q_{-a}) with s r = (2-w) w q
-            const T sv = S.lut[(cd & 63) * 4 + 2];
-            ycur[e] = c0 * qp + sv * (om * (A.wx * qval(hy, hx - 1) + A.wy * qval(hy - 1, hx) + A.wz * qprv[e]));
-          }
+          qcur[e] = (T)rnew(hy, hx) * S.lut[(cd & 63) * 4 + 1];
         }
       }
       __syncthreads();
-      if (threadIdx.x == 0 && more) {     // the raw stage is free: refill it
+      if (threadIdx.x == 0 && more && j > 0) {     // stage j-1 is free: refill it
         issue_B<T>(A, ring, S.full, t0 + issued, prod, tr);
         ++issued;
         more = cursor_next<T>(A, prod);
       }
+      // pass 2: y(kk) = s (r' + w sum_a w_a q_{-a}) on the 33 x 33 y tile, with
+      // s r' = (2-w) w q; the own cells keep theirs for z(kk-1) below
+      const bool do_y = kk >= u.k0 && A.precond == 2;
+      auto yval = [&](int hy, int hx) -> T {
+        const int e = hy * HW + hx;
+        const T sv = S.lut[(cc[Halo<uint8_t>::at(hy, hx)] & 63) * 4 + 2];
+        return c0 * qcur[e] + sv * (om * (A.wx * qcur[e - 1] + A.wy * qcur[e - HW] + A.wz * qprv[e]));
+      };
+      T yown[PCG_RPT];
+#pragma unroll
+      for (int q = 0; q < PCG_RPT; ++q) {
+        const int ly = ly0 + q * PCG_RSTEP;
+        rown[q] = rnew(ly + 1, lx + 1);
+        cown[q] = cc[Halo<uint8_t>::at(ly + 1, lx + 1)];
+        if (do_y) {
+          yown[q] = yval(ly + 1, lx + 1);
+          ycur[ly * YW + lx] = yown[q];
+        }
+      }
+      if (do_y && threadIdx.x < YW + PCG_TY) {      // row 32 and column 32 of the y tile
+        const int t = threadIdx.x;
+        const int yy = t < YW ? PCG_TY : t - YW, yx = t < YW ? t : PCG_TX;
+        ycur[yy * YW + yx] = yval(yy + 1, yx + 1);
+      }
+      // z on plane kk-1 (own cells): y(kk-1) from the previous stage, y(kk) own
       if (kk >= u.k0 + 1) {
         const int k = kk - 1;
         const int i = u.i0 + lx;
-        const T* y0 = &W.yb[ybp][0][0];
-        const T* y1 = &W.yb[yb][0][0];
 #pragma unroll
         for (int q = 0; q < PCG_RPT; ++q) {
           const int ly = ly0 + q * PCG_RSTEP, jj = u.j0 + ly;
@@ -583,7 +618,7 @@ __device__ void phaseB(const PcgArgs<T>& A, double* part, PcgShared<T>& S, uint8
             const int o = ly * YW + lx;
             const T invd = S.lut[(cd & 63) * 4 + 1];
             if (A.precond == 2)
-              zv = y0[o] + om * invd * (A.wx * y0[o + 1] + A.wy * y0[o + YW] + A.wz * y1[o]);
+              zv = yprv[o] + om * invd * (A.wx * yprv[o + 1] + A.wy * yprv[o + YW] + A.wz * yown[q]);
             else if (A.precond == 1)
               zv = (T)rprev[q] * invd;
             else
@@ -635,7 +670,7 @@ __device__ void finish_x(const PcgArgs<T>& A, int unit, T alpha, const T* __rest
 }
 
 template <typename T>
-__global__ void __launch_bounds__(PCG_THREADS) k_pcg(const __grid_constant__ PcgArgs<T> A) {
+__global__ void __launch_bounds__(PCG_THREADS, CW_PCG_MINB) k_pcg(const __grid_constant__ PcgArgs<T> A) {
   // dynamic smem is the only shared allocation of this kernel, so it starts
   // at the (1 KB aligned) base of the block's window; keep every access on
   // this array so the compiler emits LDS/STS rather than generic loads
@@ -663,6 +698,7 @@ __global__ void __launch_bounds__(PCG_THREADS) k_pcg(const __grid_constant__ Pcg
   // phase 0 writes per unit, the ring phases per block (fixed unit->block map)
   double* P[2] = {A.part, A.part + 3 * U};
 
+  if (A.probe_mode == 8 && blockIdx.x == 0 && threadIdx.x == 0) rep->criterion = 0.0;
   for (int u = blockIdx.x; u < U; u += B) phase0<T>(A, P[0], u, S);
   grid_barrier(A.bar, A.gate, rep, A.timeout_ns);
   const double b2 = fold_partials(P[0], U, 0, S.bc);
@@ -694,13 +730,25 @@ __global__ void __launch_bounds__(PCG_THREADS) k_pcg(const __grid_constant__ Pcg
   int it = 0, converged = 0, status = 0;
   bool finished = false;
   if (A.probe_mode) {
+    unsigned long long wait_ns = 0;
     // timing probe: repeat one phase (1: A, 2: B, 3: barrier only) with its
     // grid barrier; the state's p is not meaningful afterwards
     for (int q = 0; q < A.probe_iters; ++q) {
-      if (A.probe_mode == 1) phaseA<T>(A, P[0], S, ring, ticket, false, (T)0.5, true, (T)0.0, q & 1);
-      if (A.probe_mode == 2) phaseB<T>(A, P[1], S, ring, ticket, true, 0.0, q & 1, true);
+      // 6, 7: phase A and phase B alternate as in the solve (7: stream only)
+      const bool pa = A.probe_mode == 1 || A.probe_mode == 4 || (A.probe_mode >= 6 && !(q & 1));
+      const bool pb = A.probe_mode == 2 || (A.probe_mode >= 6 && (q & 1));
+      if (pa) phaseA<T>(A, P[0], S, ring, ticket, false, (T)0.5, true, (T)0.0, (q >> 1) & 1);
+      if (pb) phaseB<T>(A, P[1], S, ring, ticket, true, 0.0, (q >> 1) & 1, true);
+      const unsigned long long ta = globaltimer();
       grid_barrier(A.bar, A.gate, rep, A.timeout_ns);
+      wait_ns += globaltimer() - ta;
+      if (A.probe_mode == 5) {   // barrier plus phase B's two folds
+        rz += fold_partials(P[1], B, 0, S.bc);
+        rmax = fold_partials(P[1] + U, B, 1, S.bc);
+      }
     }
+    // 8: report the mean grid-barrier wait per block and phase (us) as the criterion
+    if (A.probe_mode == 8 && threadIdx.x == 0) atomicAdd(&rep->criterion, (double)wait_ns * 1e-3 / (B * A.probe_iters));
     if (blockIdx.x == 0 && threadIdx.x == 0) { rep->iterations = A.probe_iters; rep->converged = 1; }
     return;
   }

@@ -7,15 +7,27 @@ from paper_2204_01117_b200.scenario import CompiledScenario, scenario_from_dict
 comp = CompiledScenario.compile(scenario_from_dict(scenes.block_city(256, 256, 64, 2.0, 0, 6, 0.2)))
 st = comp.make_state()
 comp.step_states(st, 2)
-n = 200
-for mode in (1, 2, 3):
+NAMES = {1: "phase A + barrier", 2: "phase B + barrier", 3: "barrier", 4: "phase A TMA stream only + barrier",
+         5: "barrier + 2 folds", 6: "A,B alternating (per phase)", 7: "A,B alternating, stream only (per phase)",
+         8: "A,B alternating, barrier wait reported (per phase)"}
+
+
+def timed(mode, n):
     os.environ["CW_PCG_PROBE"] = f"{mode},{n}"
     s = st.copy()
     solver.step_many(s, comp.scenario.solver, comp.psys, comp.preconditioner, comp.scenario.inlet, 1)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    solver.step_many(s, comp.scenario.solver, comp.psys, comp.preconditioner, comp.scenario.inlet, 1)
+    rep = solver.step_many(s, comp.scenario.solver, comp.psys, comp.preconditioner, comp.scenario.inlet, 1)
     e1.record(); torch.cuda.synchronize()
-    print(f"mode {mode}: {e0.elapsed_time(e1) * 1e3 / n:.2f} us per phase+barrier (incl. rest of step /{n})", flush=True)
+    if mode == 8:
+        print(f"  mean grid-barrier wait per block and phase: {rep[0].pcg.criterion:.2f} us", flush=True)
+    return e0.elapsed_time(e1) * 1e3
+
+
+modes = [int(m) for m in sys.argv[1].split(",")] if len(sys.argv) > 1 else [1, 2, 3, 4, 5, 6, 7]
+for mode in modes:
+    a, b = timed(mode, 100), timed(mode, 400)
+    print(f"mode {mode} ({NAMES.get(mode, '?')}): {(b - a) / 300:.2f} us per iteration", flush=True)
 os.environ.pop("CW_PCG_PROBE")
