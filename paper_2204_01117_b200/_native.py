@@ -16,7 +16,7 @@ from .errors import (ClassificationError, NativeError, ProjectionError,
                      SingularSystemError)
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libcitywind_b200.so")
+LIB_PATH = os.environ.get("CW_LIB") or os.path.join(HERE, "libcitywind_b200.so")   # CW_LIB: developer variant builds
 
 CW_OK, CW_ERR_INVALID, CW_ERR_CUDA, CW_ERR_SINGULAR, CW_ERR_PCG = 0, 1, 2, 3, 4
 CW_ERR_NONFINITE, CW_ERR_TIMEOUT, CW_ERR_RHS, CW_ERR_GEOMETRY = 5, 6, 7, 8

@@ -268,6 +268,15 @@ extern "C" void cw_ctx_destroy(cw_ctx* c) {
 }
 
 static inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+static inline dim3 g3(int ex, int ey, int ez) {   // 3-D stage-kernel grid (cw_step.cuh CW_IJK)
+  return dim3((unsigned)((ex + ST_BX - 1) / ST_BX), (unsigned)((ey + ST_BY - 1) / ST_BY), (unsigned)ez);
+}
+static const dim3 B3(ST_BX, ST_BY);
+static inline dim3 g3c(const Dims& d, int comp) {
+  int ex, ey, ez;
+  comp_extent(d, comp, ex, ey, ez);
+  return g3(ex, ey, ez);
+}
 static inline int nblk(long long n, int bs = 256) {
   long long b = (n + bs - 1) / bs;
   return (int)std::max<long long>(1, std::min<long long>(b, 148LL * 32));
@@ -397,7 +406,7 @@ static void launch_bc(cw_ctx* c, BcFields<T> F, const int8_t* lab, const cw_para
     (k_bc_outlet_side<T><<<nblk((long long)(e1 + 1) * (e2 + 1)), 256, 0, st>>>(d, axis, pos, F, lab, c->gate), ++c->launches);
   }
   const long long n = c->ncell + c->nu_ + c->nv_ + (d.is2d ? 0 : c->nw_);
-  (k_bc_inlet_wall<T><<<nblk(n), 256, 0, st>>>(d, F, lab, (const T*)c->uzx, (const T*)c->uzy, (T)prm->k_in,
+  (k_bc_inlet_wall<T><<<g3(d.nx + 1, d.ny + 1, d.nz + 1), B3, 0, st>>>(d, F, lab, (const T*)c->uzx, (const T*)c->uzy, (T)prm->k_in,
                                               (T)prm->omega_in, (T)(prm->k_in / prm->omega_in), c->gate), ++c->launches);
 }
 
@@ -489,11 +498,11 @@ static void st_advect(cw_ctx* c, const StepPtrs<T>& P, const cw_params* prm, T* 
   const long long nf[3] = {c->nu_, c->nv_, c->nw_};
   const int ncomp = d.is2d ? 2 : 3;
   if (prm->turbulence)
-    (k_upwind<T><<<nblk(c->ncell), 256, 0, st>>>(d, P.u, P.v, P.w, P.k, P.om, kout, wout, dt, c->gate), ++c->launches);
+    (k_upwind<T><<<g3(d.nx, d.ny, d.nz), B3, 0, st>>>(d, P.u, P.v, P.w, P.k, P.om, kout, wout, dt, c->gate), ++c->launches);
   for (int a = 0; a < ncomp; ++a)
-    (k_mac_predict<T><<<nblk(nf[a]), 256, 0, st>>>(d, a, P.u, P.v, P.w, (T*)c->ahead[a], dt, c->gate), ++c->launches);
+    (k_mac_predict<T><<<g3c(d, a), B3, 0, st>>>(d, a, P.u, P.v, P.w, (T*)c->ahead[a], dt, c->gate), ++c->launches);
   for (int a = 0; a < ncomp; ++a)
-    (k_mac_correct<T><<<nblk(nf[a]), 256, 0, st>>>(d, a, P.u, P.v, P.w, (const T*)c->ahead[a], (T*)c->adv[a], dt, c->gate), ++c->launches);
+    (k_mac_correct<T><<<g3c(d, a), B3, 0, st>>>(d, a, P.u, P.v, P.w, (const T*)c->ahead[a], (T*)c->adv[a], dt, c->gate), ++c->launches);
 }
 
 template <typename T>
@@ -504,7 +513,7 @@ static void st_diffuse(cw_ctx* c, const StepPtrs<T>& P, const cw_params* prm, cu
   double cap = nu_stable<T>(c, prm->dt) - prm->nu;
   if (cap <= 0) cap = 0.0;                               // solver.py:195-201
   for (int a = 0; a < (d.is2d ? 2 : 3); ++a)
-    (k_diffuse<T><<<nblk(nf[a]), 256, 0, st>>>(d, a, (const T*)c->adv[a], cu[a], P.nut, (T)prm->dt,
+    (k_diffuse<T><<<g3c(d, a), B3, 0, st>>>(d, a, (const T*)c->adv[a], cu[a], P.nut, (T)prm->dt,
                                                (T)prm->nu, (T)cap, c->gate), ++c->launches);
 }
 
@@ -514,9 +523,9 @@ static void st_drag(cw_ctx* c, const StepPtrs<T>& P, const cw_params* prm, int h
   const Dims& d = c->d;
   const long long nf[3] = {c->nu_, c->nv_, c->nw_};
   T* cu[3] = {P.u, P.v, P.w};
-  (k_cell_speed<T><<<nblk(c->ncell), 256, 0, st>>>(d, P.u, P.v, P.w, (T*)c->speed, c->gate), ++c->launches);
+  (k_cell_speed<T><<<g3(d.nx, d.ny, d.nz), B3, 0, st>>>(d, P.u, P.v, P.w, (T*)c->speed, c->gate), ++c->launches);
   for (int a = 0; a < (d.is2d ? 2 : 3); ++a)
-    (k_drag<T><<<nblk(nf[a]), 256, 0, st>>>(d, a, cu[a], P.g, (const T*)c->speed, (T)prm->dt, c->gate), ++c->launches);
+    (k_drag<T><<<g3c(d, a), B3, 0, st>>>(d, a, cu[a], P.g, (const T*)c->speed, (T)prm->dt, c->gate), ++c->launches);
 }
 
 template <typename T>
@@ -532,8 +541,8 @@ static int st_project(cw_ctx* c, const StepPtrs<T>& P, const cw_fields* f, const
   if (tpcg) cudaEventRecord(c->pev[2 * c->pcg_timed++ + 1], st);
   if (rc) return rc;
   for (int a = 0; a < (d.is2d ? 2 : 3); ++a)
-    (k_gradient<T><<<nblk(nf[a]), 256, 0, st>>>(d, a, cu[a], P.p, P.lab, (T)prm->dt, c->gate), ++c->launches);
-  (k_div_max<T><<<nblk(c->ncell), 256, 0, st>>>(d, P.u, P.v, P.w, P.lab, rep, SLOT_DIV_AFTER, c->gate), ++c->launches);
+    (k_gradient<T><<<g3c(d, a), B3, 0, st>>>(d, a, cu[a], P.p, P.lab, (T)prm->dt, c->gate), ++c->launches);
+  (k_div_max<T><<<g3(d.nx, d.ny, d.nz), B3, 0, st>>>(d, P.u, P.v, P.w, P.lab, rep, SLOT_DIV_AFTER, c->gate), ++c->launches);
   return CW_OK;
 }
 
@@ -547,7 +556,7 @@ static void st_turb(cw_ctx* c, const StepPtrs<T>& P, const cw_params* prm, const
   sc.c_mu = prm->c_mu; sc.alpha = prm->alpha; sc.beta = prm->beta;
   sc.sigma = prm->sigma; sc.sigma_star = prm->sigma_star; sc.c_lim = prm->c_lim;
   sc.k_in = prm->k_in; sc.om_in = prm->omega_in; sc.nut_in = prm->k_in / prm->omega_in;
-  (k_turbulence<T><<<nblk(c->ncell), 256, 0, st>>>(c->d, P.u, P.v, P.w, kin, win, P.k, P.om, P.nut, sc, rep, c->gate), ++c->launches);
+  (k_turbulence<T><<<g3(c->d.nx, c->d.ny, c->d.nz), B3, 0, st>>>(c->d, P.u, P.v, P.w, kin, win, P.k, P.om, P.nut, sc, rep, c->gate), ++c->launches);
   (k_turb_check<<<1, 1, 0, st>>>(rep, c->gate), ++c->launches);
 }
 

@@ -123,4 +123,21 @@ __device__ __forceinline__ T block_max(T v, T* scratch) {
   return t;  // valid in thread 0
 }
 
+// block_max for 2-D blocks (linear thread id x + y * blockDim.x); result in thread (0, 0)
+template <typename T>
+__device__ __forceinline__ T block_max_2d(T v, T* scratch) {
+  const int tid = threadIdx.x + threadIdx.y * blockDim.x;
+  const int lane = tid & 31, wid = tid >> 5, nw = (blockDim.x * blockDim.y + 31) >> 5;
+  v = warp_max(v);
+  __syncthreads();
+  if (lane == 0) scratch[wid] = v;
+  __syncthreads();
+  T t = (T)0;
+  if (wid == 0) {
+    t = lane < nw ? scratch[lane] : (T)0;
+    t = warp_max(t);
+  }
+  return t;
+}
+
 }  // namespace cw

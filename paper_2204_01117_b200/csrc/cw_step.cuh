@@ -38,6 +38,16 @@ template <> __device__ __forceinline__ void report_max<double>(DevReport* r, int
   for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < (n); \
        idx += (long long)gridDim.x * blockDim.x)
 
+// Stage kernels run on a 3-D grid: blockDim (32, 8), grid (ceil(ex/32),
+// ceil(ey/8), ez) -- the element's (i, j, k) come from the launch, no
+// per-element 64-bit division.
+constexpr int ST_BX = 32, ST_BY = 8;
+#define CW_IJK(ex, ey, ez, inb)                                  \
+  const int i = (int)(blockIdx.x * ST_BX + threadIdx.x);         \
+  const int j = (int)(blockIdx.y * ST_BY + threadIdx.y);         \
+  const int k = (int)blockIdx.z;                                 \
+  const bool inb = i < (ex) && j < (ey) && k < (ez)
+
 __device__ __forceinline__ int clampi(int a, int lo, int hi) { return a < lo ? lo : (a > hi ? hi : a); }
 
 // ---------------------------------------------------------------------------
@@ -48,9 +58,9 @@ __global__ void k_upwind(Dims d, const T* __restrict__ u, const T* __restrict__ 
                          const T* __restrict__ win, T* __restrict__ kout, T* __restrict__ wout,
                          T dt, const int* gate) {
   if (*gate) return;
-  const long long n = d.ncell();
-  CW_GRID_STRIDE(c, n) {
-    const int i = (int)(c % d.nx), j = (int)((c / d.nx) % d.ny), k = (int)(c / ((long long)d.nx * d.ny));
+  CW_IJK(d.nx, d.ny, d.nz, inb);
+  if (inb) {
+    const long long c = d.cidx(i, j, k);
     T a[3];
     a[0] = (T)0.5 * (u[((long long)k * d.ny + j) * (d.nx + 1) + i] + u[((long long)k * d.ny + j) * (d.nx + 1) + i + 1]);
     a[1] = (T)0.5 * (v[((long long)k * (d.ny + 1) + j) * d.nx + i] + v[((long long)k * (d.ny + 1) + j + 1) * d.nx + i]);
@@ -104,9 +114,9 @@ __global__ void k_mac_predict(Dims d, int comp, const T* __restrict__ u, const T
   comp_offset(comp, fox, foy, foz);
   const T ox = (T)fox, oy = (T)foy, oz = (T)foz;
   const T* arr = comp == 0 ? u : (comp == 1 ? v : w);
-  const long long n = (long long)ex * ey * ez;
-  CW_GRID_STRIDE(c, n) {
-    const int i = (int)(c % ex), j = (int)((c / ex) % ey), k = (int)(c / ((long long)ex * ey));
+  CW_IJK(ex, ey, ez, inb);
+  if (inb) {
+    const long long c = ((long long)k * ey + j) * ex + i;
     const T X = (T)i + ox, Y = (T)j + oy, Z = (T)k + oz;
     T us, vs, ws;
     velocity_at(d, u, v, w, X, Y, Z, us, vs, ws);
@@ -126,9 +136,9 @@ __global__ void k_mac_correct(Dims d, int comp, const T* __restrict__ u, const T
   comp_offset(comp, fox, foy, foz);
   const T ox = (T)fox, oy = (T)foy, oz = (T)foz;
   const T* arr = comp == 0 ? u : (comp == 1 ? v : w);
-  const long long n = (long long)ex * ey * ez;
-  CW_GRID_STRIDE(c, n) {
-    const int i = (int)(c % ex), j = (int)((c / ex) % ey), k = (int)(c / ((long long)ex * ey));
+  CW_IJK(ex, ey, ez, inb);
+  if (inb) {
+    const long long c = ((long long)k * ey + j) * ex + i;
     const T X = (T)i + ox, Y = (T)j + oy, Z = (T)k + oz;
     T us, vs, ws;
     velocity_at(d, u, v, w, X, Y, Z, us, vs, ws);
@@ -160,12 +170,13 @@ __global__ void k_diffuse(Dims d, int comp, const T* __restrict__ src, T* __rest
   if (*gate) return;
   int ex, ey, ez;
   comp_extent(d, comp, ex, ey, ez);
-  const long long n = (long long)ex * ey * ez;
   const int ext[3] = {ex, ey, ez};
   const long long str[3] = {1, ex, (long long)ex * ey};
   const T h[3] = {(T)d.dx, (T)d.dy, (T)d.dz};
-  CW_GRID_STRIDE(c, n) {
-    const int pos[3] = {(int)(c % ex), (int)((c / ex) % ey), (int)(c / ((long long)ex * ey))};
+  CW_IJK(ex, ey, ez, inb);
+  if (inb) {
+    const long long c = ((long long)k * ey + j) * ex + i;
+    const int pos[3] = {i, j, k};
     const T mid = src[c];
     T lap = (T)0;
 #pragma unroll
@@ -193,9 +204,9 @@ template <typename T>
 __global__ void k_cell_speed(Dims d, const T* __restrict__ u, const T* __restrict__ v,
                              const T* __restrict__ w, T* __restrict__ speed, const int* gate) {
   if (*gate) return;
-  const long long n = d.ncell();
-  CW_GRID_STRIDE(c, n) {
-    const int i = (int)(c % d.nx), j = (int)((c / d.nx) % d.ny), k = (int)(c / ((long long)d.nx * d.ny));
+  CW_IJK(d.nx, d.ny, d.nz, inb);
+  if (inb) {
+    const long long c = d.cidx(i, j, k);
     const long long ui = ((long long)k * d.ny + j) * (d.nx + 1) + i;
     const long long vi = ((long long)k * (d.ny + 1) + j) * d.nx + i;
     const T uc = (T)0.5 * (u[ui] + u[ui + 1]);
@@ -211,10 +222,11 @@ __global__ void k_drag(Dims d, int comp, T* __restrict__ arr, const T* __restric
   if (*gate) return;
   int ex, ey, ez;
   comp_extent(d, comp, ex, ey, ez);
-  const long long n = (long long)ex * ey * ez;
   const int nc = comp == 0 ? d.nx : (comp == 1 ? d.ny : d.nz);
-  CW_GRID_STRIDE(c, n) {
-    int p[3] = {(int)(c % ex), (int)((c / ex) % ey), (int)(c / ((long long)ex * ey))};
+  CW_IJK(ex, ey, ez, inb);
+  if (inb) {
+    const long long c = ((long long)k * ey + j) * ex + i;
+    int p[3] = {i, j, k};
     const int f = p[comp];
     p[comp] = clampi(f - 1, 0, nc - 1);
     const long long lo = d.cidx(p[0], p[1], p[2]);
@@ -244,9 +256,9 @@ __global__ void k_bc_outlet_side(Dims d, int axis, int pos, BcFields<T> F,
   const int a1 = axis == 0 ? 1 : 0, a2 = axis == 2 ? 1 : 2;   // in-plane axes
   const int n1 = ext[a1] + 1, n2 = ext[a2] + 1;
   const int inner = pos == 0 ? pos + 1 : pos - 1;
-  const long long n = (long long)n1 * n2;
-  CW_GRID_STRIDE(t, n) {
-    const int q1 = (int)(t % n1), q2 = (int)(t / n1);
+  const int n = n1 * n2;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
+    const int q1 = t % n1, q2 = t / n1;
     int c[3];
     // cells (scalars) and the normal velocity component
     if (q1 < ext[a1] && q2 < ext[a2]) {
@@ -298,42 +310,43 @@ __global__ void k_bc_outlet_side(Dims d, int axis, int pos, BcFields<T> F,
   }
 }
 
-// inlet scalars, inlet face velocities, then walls zero all touching faces
+// inlet scalars, inlet face velocities, then walls zero all touching faces.
+// One thread per (i, j, k) of the union of the cell and face extents.
+template <typename T>
+__device__ __forceinline__ void bc_face(const Dims& d, int comp, T* arr, const int8_t* lab, int i, int j, int k,
+                                        const T* uz_dirx, const T* uz_diry) {
+  int ex, ey, ez;
+  comp_extent(d, comp, ex, ey, ez);
+  if (i >= ex || j >= ey || k >= ez) return;
+  const int ext[3] = {d.nx, d.ny, d.nz};
+  int p[3] = {i, j, k};
+  const int f = p[comp];
+  p[comp] = clampi(f - 1, 0, ext[comp] - 1);
+  const int8_t la = lab[d.cidx(p[0], p[1], p[2])];
+  p[comp] = clampi(f, 0, ext[comp] - 1);
+  const int8_t lb = lab[d.cidx(p[0], p[1], p[2])];
+  const long long r = ((long long)k * ey + j) * ex + i;
+  if (la == SOLID_WALL || lb == SOLID_WALL) {
+    arr[r] = (T)0;
+  } else if (la == INLET || lb == INLET) {
+    arr[r] = comp == 0 ? uz_dirx[p[2]] : (comp == 1 ? uz_diry[p[2]] : (T)0);
+  }
+}
+
 template <typename T>
 __global__ void k_bc_inlet_wall(Dims d, BcFields<T> F, const int8_t* __restrict__ lab,
                                 const T* __restrict__ uz_dirx, const T* __restrict__ uz_diry,
                                 T k_in, T om_in, T nut_in, const int* gate) {
   if (*gate) return;
-  const long long nc = d.ncell();
-  const long long nu = (long long)(d.nx + 1) * d.ny * d.nz;
-  const long long nv = (long long)d.nx * (d.ny + 1) * d.nz;
-  const long long nw = d.is2d ? 0 : (long long)d.nx * d.ny * (d.nz + 1);
-  const long long n = nc + nu + nv + nw;
-  const int ext[3] = {d.nx, d.ny, d.nz};
-  CW_GRID_STRIDE(t, n) {
-    if (t < nc) {
-      if (lab[t] == INLET) { F.k[t] = k_in; F.om[t] = om_in; F.nut[t] = nut_in; }
-      continue;
-    }
-    long long r = t - nc;
-    int comp = 0;
-    if (r >= nu) { r -= nu; comp = 1; if (r >= nv) { r -= nv; comp = 2; } }
-    int ex, ey, ez;
-    comp_extent(d, comp, ex, ey, ez);
-    int p[3] = {(int)(r % ex), (int)((r / ex) % ey), (int)(r / ((long long)ex * ey))};
-    const int f = p[comp];
-    p[comp] = clampi(f - 1, 0, ext[comp] - 1);
-    const int8_t la = lab[d.cidx(p[0], p[1], p[2])];
-    p[comp] = clampi(f, 0, ext[comp] - 1);
-    const int8_t lb = lab[d.cidx(p[0], p[1], p[2])];
-    T* arr = comp == 0 ? F.u : (comp == 1 ? F.v : F.w);
-    if (la == SOLID_WALL || lb == SOLID_WALL) {
-      arr[r] = (T)0;
-    } else if (la == INLET || lb == INLET) {
-      const int kk = p[2];
-      arr[r] = comp == 0 ? uz_dirx[kk] : (comp == 1 ? uz_diry[kk] : (T)0);
-    }
+  CW_IJK(d.nx + 1, d.ny + 1, d.nz + 1, inb);
+  if (!inb) return;
+  if (i < d.nx && j < d.ny && k < d.nz) {
+    const long long t = d.cidx(i, j, k);
+    if (lab[t] == INLET) { F.k[t] = k_in; F.om[t] = om_in; F.nut[t] = nut_in; }
   }
+  bc_face<T>(d, 0, F.u, lab, i, j, k, uz_dirx, uz_diry);
+  bc_face<T>(d, 1, F.v, lab, i, j, k, uz_dirx, uz_diry);
+  if (!d.is2d) bc_face<T>(d, 2, F.w, lab, i, j, k, uz_dirx, uz_diry);
 }
 
 // ---------------------------------------------------------------------------
@@ -344,13 +357,14 @@ __global__ void k_gradient(Dims d, int comp, T* __restrict__ arr, const T* __res
   if (*gate) return;
   int ex, ey, ez;
   comp_extent(d, comp, ex, ey, ez);
-  const long long n = (long long)ex * ey * ez;
   const T h = comp == 0 ? (T)d.dx : (comp == 1 ? (T)d.dy : (T)d.dz);
   const int nc = comp == 0 ? d.nx : (comp == 1 ? d.ny : d.nz);
-  CW_GRID_STRIDE(c, n) {
-    int q[3] = {(int)(c % ex), (int)((c / ex) % ey), (int)(c / ((long long)ex * ey))};
+  CW_IJK(ex, ey, ez, inb);
+  if (inb) {
+    const long long c = ((long long)k * ey + j) * ex + i;
+    int q[3] = {i, j, k};
     const int f = q[comp];
-    if (f < 1 || f > nc - 1) continue;
+    if (f < 1 || f > nc - 1) return;
     q[comp] = f - 1;
     const long long lo = d.cidx(q[0], q[1], q[2]);
     q[comp] = f;
@@ -361,7 +375,7 @@ __global__ void k_gradient(Dims d, int comp, T* __restrict__ arr, const T* __res
     if (au && bu) grad = (p[hi] - p[lo]) / h;
     else if (au && lb == OUTLET) grad = -p[lo] / h;
     else if (bu && la == OUTLET) grad = p[hi] / h;
-    else continue;
+    else return;
     arr[c] -= dt * grad;
   }
 }
@@ -373,11 +387,10 @@ __global__ void k_div_max(Dims d, const T* __restrict__ u, const T* __restrict__
                           DevReport* rep, int slot, const int* gate) {
   if (*gate) return;
   __shared__ T scratch[32];
-  const long long n = d.ncell();
   T m = (T)0;
-  CW_GRID_STRIDE(c, n) {
-    if (!is_unknown(lab[c])) continue;
-    const int i = (int)(c % d.nx), j = (int)((c / d.nx) % d.ny), k = (int)(c / ((long long)d.nx * d.ny));
+  CW_IJK(d.nx, d.ny, d.nz, inb);
+  const long long c = d.cidx(i, j, k);
+  if (inb && is_unknown(lab[c])) {
     const long long ui = ((long long)k * d.ny + j) * (d.nx + 1) + i;
     const long long vi = ((long long)k * (d.ny + 1) + j) * d.nx + i;
     T div = (u[ui + 1] - u[ui]) / (T)d.dx + (v[vi + d.nx] - v[vi]) / (T)d.dy;
@@ -385,8 +398,8 @@ __global__ void k_div_max(Dims d, const T* __restrict__ u, const T* __restrict__
     const T a = fabs(div);
     m = (a > m || a != a) ? a : m;
   }
-  m = block_max(m, scratch);
-  if (threadIdx.x == 0) report_max<T>(rep, slot, m);
+  m = block_max_2d(m, scratch);
+  if (threadIdx.x == 0 && threadIdx.y == 0) report_max<T>(rep, slot, m);
 }
 
 // max |u|,|v|,|w| for the CFL number (solver.py:456-458)
@@ -466,10 +479,10 @@ __global__ void k_turbulence(Dims d, const T* __restrict__ u, const T* __restric
                              const T* __restrict__ win, T* __restrict__ kout, T* __restrict__ wout,
                              T* __restrict__ nut, StepConsts sc, DevReport* rep, const int* gate) {
   if (*gate) return;
-  const long long n = d.ncell();
   const T dt = (T)sc.dt, nu = (T)sc.nu, cap = (T)sc.cap_turb;
-  CW_GRID_STRIDE(c, n) {
-    const int i = (int)(c % d.nx), j = (int)((c / d.nx) % d.ny), k = (int)(c / ((long long)d.nx * d.ny));
+  CW_IJK(d.nx, d.ny, d.nz, inb);
+  if (inb) {
+    const long long c = d.cidx(i, j, k);
     const long long ui = ((long long)k * d.ny + j) * (d.nx + 1) + i;
     const long long vi = ((long long)k * (d.ny + 1) + j) * d.nx + i;
     const T dudx = (u[ui + 1] - u[ui]) / (T)d.dx;

@@ -9,7 +9,10 @@ st = comp.make_state()
 comp.step_states(st, 2)
 NAMES = {1: "phase A + barrier", 2: "phase B + barrier", 3: "barrier", 4: "phase A TMA stream only + barrier",
          5: "barrier + 2 folds", 6: "A,B alternating (per phase)", 7: "A,B alternating, stream only (per phase)",
-         8: "A,B alternating, barrier wait reported (per phase)"}
+         8: "A,B alternating, barrier wait reported (per phase)",
+         9: "A,B alternating, no global stores (per phase)",
+         10: "A,B alternating, no loads: compute on stale stages (per phase)",
+         12: "A,B alternating, TMA wait reported (per phase)"}
 
 
 def timed(mode, n):
@@ -21,8 +24,9 @@ def timed(mode, n):
     e0.record()
     rep = solver.step_many(s, comp.scenario.solver, comp.psys, comp.preconditioner, comp.scenario.inlet, 1)
     e1.record(); torch.cuda.synchronize()
-    if mode == 8:
-        print(f"  mean grid-barrier wait per block and phase: {rep[0].pcg.criterion:.2f} us", flush=True)
+    if mode in (8, 12):
+        what = "grid-barrier" if mode == 8 else "TMA stage (thread 0)"
+        print(f"  mean {what} wait per block and phase: {rep[0].pcg.criterion:.2f} us", flush=True)
     return e0.elapsed_time(e1) * 1e3
 
 
