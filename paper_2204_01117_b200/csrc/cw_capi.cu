@@ -167,6 +167,10 @@ extern "C" int cw_ctx_create(const cw_grid* g, int precision, int device, cw_ctx
   c->nu_ = (long long)(d.nx + 1) * d.ny * d.nz;
   c->nv_ = (long long)d.nx * (d.ny + 1) * d.nz;
   c->nw_ = (long long)d.nx * d.ny * (d.nz + 1);
+  if (std::max(std::max(c->nu_, c->nv_), c->nw_) >= (1LL << 31) || d.nz > 65535) {   // 32-bit gathers, 3-D grids
+    cw_ctx_destroy(c);
+    return fail(CW_ERR_INVALID, "grid too large for one device context (face arrays must hold < 2^31 cells, nz <= 65535)");
+  }
   const size_t cb = c->ncell * c->esz;
   size_t fb[3] = {c->nu_ * c->esz, c->nv_ * c->esz, c->nw_ * c->esz};
   int rc = CW_OK;
@@ -499,10 +503,12 @@ static void st_advect(cw_ctx* c, const StepPtrs<T>& P, const cw_params* prm, T* 
   const int ncomp = d.is2d ? 2 : 3;
   if (prm->turbulence)
     (k_upwind<T><<<g3(d.nx, d.ny, d.nz), B3, 0, st>>>(d, P.u, P.v, P.w, P.k, P.om, kout, wout, dt, c->gate), ++c->launches);
-  for (int a = 0; a < ncomp; ++a)
-    (k_mac_predict<T><<<g3c(d, a), B3, 0, st>>>(d, a, P.u, P.v, P.w, (T*)c->ahead[a], dt, c->gate), ++c->launches);
-  for (int a = 0; a < ncomp; ++a)
-    (k_mac_correct<T><<<g3c(d, a), B3, 0, st>>>(d, a, P.u, P.v, P.w, (const T*)c->ahead[a], (T*)c->adv[a], dt, c->gate), ++c->launches);
+  (void)ncomp;
+  (k_mac_predict<T><<<g3(d.nx + 1, d.ny + 1, d.nz + 1), B3, 0, st>>>(
+       d, P.u, P.v, P.w, (T*)c->ahead[0], (T*)c->ahead[1], (T*)c->ahead[2], dt, c->gate), ++c->launches);
+  (k_mac_correct<T><<<g3(d.nx + 1, d.ny + 1, d.nz + 1), B3, 0, st>>>(
+       d, P.u, P.v, P.w, (const T*)c->ahead[0], (const T*)c->ahead[1], (const T*)c->ahead[2], (T*)c->adv[0],
+       (T*)c->adv[1], (T*)c->adv[2], dt, c->gate), ++c->launches);
 }
 
 template <typename T>

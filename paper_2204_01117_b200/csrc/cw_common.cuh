@@ -34,20 +34,12 @@ __host__ __device__ inline void comp_extent(const Dims& d, int comp, int& ex, in
 
 // ---------------------------------------------------------------------------
 // Trilinear gather with clamped indices (advection.py:49-101, _kernels.py:25-58)
+// Arrays hold < 2^31 elements (checked at context creation): 32-bit indices.
 template <typename T>
-__device__ __forceinline__ T gather(const T* __restrict__ a, int ex, int ey, int ez,
-                                    T fx, T fy, T fz, T* mn, T* mx) {
-  int i0 = (int)floor(fx), j0 = (int)floor(fy), k0 = (int)floor(fz);
-  const int im = ex - 2 > 0 ? ex - 2 : 0, jm = ey - 2 > 0 ? ey - 2 : 0, km = ez - 2 > 0 ? ez - 2 : 0;
-  i0 = i0 < 0 ? 0 : (i0 > im ? im : i0);
-  j0 = j0 < 0 ? 0 : (j0 > jm ? jm : j0);
-  k0 = k0 < 0 ? 0 : (k0 > km ? km : k0);
-  T tx = fx - (T)i0, ty = fy - (T)j0, tz = fz - (T)k0;
-  tx = tx < (T)0 ? (T)0 : (tx > (T)1 ? (T)1 : tx);
-  ty = ty < (T)0 ? (T)0 : (ty > (T)1 ? (T)1 : ty);
-  tz = tz < (T)0 ? (T)0 : (tz > (T)1 ? (T)1 : tz);
-  const long long sx = ex > 1 ? 1 : 0, sy = ey > 1 ? ex : 0, sz = ez > 1 ? (long long)ex * ey : 0;
-  const long long b = ((long long)k0 * ey + j0) * ex + i0;
+__device__ __forceinline__ T gather_at(const T* __restrict__ a, int ex, int ey, int ez, int i0, int j0, int k0,
+                                       T tx, T ty, T tz, T* mn, T* mx) {
+  const int sx = ex > 1 ? 1 : 0, sy = ey > 1 ? ex : 0, sz = ez > 1 ? ex * ey : 0;
+  const int b = (k0 * ey + j0) * ex + i0;
   const T c000 = a[b], c100 = a[b + sx], c010 = a[b + sy], c110 = a[b + sx + sy];
   const T c001 = a[b + sz], c101 = a[b + sx + sz], c011 = a[b + sy + sz], c111 = a[b + sx + sy + sz];
   const T ox = (T)1 - tx, oy = (T)1 - ty, oz = (T)1 - tz;
@@ -63,6 +55,33 @@ __device__ __forceinline__ T gather(const T* __restrict__ a, int ex, int ey, int
     *mx = hi;
   }
   return c0 * oz + c1 * tz;
+}
+
+template <typename T>
+__device__ __forceinline__ T gather(const T* __restrict__ a, int ex, int ey, int ez,
+                                    T fx, T fy, T fz, T* mn, T* mx) {
+  int i0 = (int)floor(fx), j0 = (int)floor(fy), k0 = (int)floor(fz);
+  const int im = ex - 2 > 0 ? ex - 2 : 0, jm = ey - 2 > 0 ? ey - 2 : 0, km = ez - 2 > 0 ? ez - 2 : 0;
+  i0 = i0 < 0 ? 0 : (i0 > im ? im : i0);
+  j0 = j0 < 0 ? 0 : (j0 > jm ? jm : j0);
+  k0 = k0 < 0 ? 0 : (k0 > km ? km : k0);
+  T tx = fx - (T)i0, ty = fy - (T)j0, tz = fz - (T)k0;
+  tx = tx < (T)0 ? (T)0 : (tx > (T)1 ? (T)1 : tx);
+  ty = ty < (T)0 ? (T)0 : (ty > (T)1 ? (T)1 : ty);
+  tz = tz < (T)0 ? (T)0 : (tz > (T)1 ? (T)1 : tz);
+  return gather_at<T>(a, ex, ey, ez, i0, j0, k0, tx, ty, tz, mn, mx);
+}
+
+// The same gather at a point i + half/2 on one axis (half in {-1, 0, 1}):
+// floor, clamp and fraction in integer arithmetic.  Every value involved is
+// an exact small integer or half, so i0 and t equal gather()'s bit for bit.
+template <typename T>
+__device__ __forceinline__ void axis_at(int i, int half, int e, int& i0, T& t) {
+  const int fl = half < 0 ? i - 1 : i;
+  const int im = e - 2 > 0 ? e - 2 : 0;
+  i0 = fl < 0 ? 0 : (fl > im ? im : fl);
+  const int h2 = 2 * (i - i0) + half;      // 2 (x - i0)
+  t = h2 <= 0 ? (T)0 : (h2 >= 2 ? (T)1 : (T)0.5);
 }
 
 // ---------------------------------------------------------------------------

@@ -96,62 +96,95 @@ __device__ __forceinline__ void comp_offset(int comp, float& ox, float& oy, floa
   oz = comp == 2 ? 0.f : 0.5f;
 }
 
+// Velocity of the pre-advection field at the face point of component `comp`
+// with integer index (i, j, k): the point sits at fixed half-cell offsets from
+// every velocity grid, so the gathers take the integer path (axis_at).
 template <typename T>
-__device__ __forceinline__ void velocity_at(const Dims& d, const T* u, const T* v, const T* w,
-                                            T X, T Y, T Z, T& us, T& vs, T& ws) {
-  us = gather<T>(u, d.nx + 1, d.ny, d.nz, X, Y - (T)0.5, Z - (T)0.5, nullptr, nullptr);
-  vs = gather<T>(v, d.nx, d.ny + 1, d.nz, X - (T)0.5, Y, Z - (T)0.5, nullptr, nullptr);
-  ws = gather<T>(w, d.nx, d.ny, d.nz + 1, X - (T)0.5, Y - (T)0.5, Z, nullptr, nullptr);
+__device__ __forceinline__ void velocity_at(const Dims& d, int comp, const T* u, const T* v, const T* w,
+                                            int i, int j, int k, T& us, T& vs, T& ws) {
+  // half-offsets (in units of 0.5 cell) of the face point minus each grid's offset
+  const int hx = comp == 0 ? 0 : 1, hy = comp == 1 ? 0 : 1, hz = comp == 2 ? 0 : 1;
+  int i0, j0, k0;
+  T tx, ty, tz;
+  // u grid: offsets (0, .5, .5), extents (nx+1, ny, nz)
+  axis_at<T>(i, hx, d.nx + 1, i0, tx); axis_at<T>(j, hy - 1, d.ny, j0, ty); axis_at<T>(k, hz - 1, d.nz, k0, tz);
+  us = gather_at<T>(u, d.nx + 1, d.ny, d.nz, i0, j0, k0, tx, ty, tz, nullptr, nullptr);
+  // v grid: offsets (.5, 0, .5)
+  axis_at<T>(i, hx - 1, d.nx, i0, tx); axis_at<T>(j, hy, d.ny + 1, j0, ty); axis_at<T>(k, hz - 1, d.nz, k0, tz);
+  vs = gather_at<T>(v, d.nx, d.ny + 1, d.nz, i0, j0, k0, tx, ty, tz, nullptr, nullptr);
+  // w grid: offsets (.5, .5, 0)
+  axis_at<T>(i, hx - 1, d.nx, i0, tx); axis_at<T>(j, hy - 1, d.ny, j0, ty); axis_at<T>(k, hz, d.nz + 1, k0, tz);
+  ws = gather_at<T>(w, d.nx, d.ny, d.nz + 1, i0, j0, k0, tx, ty, tz, nullptr, nullptr);
 }
 
+// One thread per (i, j, k) of the union of the face extents handles the u, v
+// and w faces there (all three read the same pre-advection velocity).
 template <typename T>
-__global__ void k_mac_predict(Dims d, int comp, const T* __restrict__ u, const T* __restrict__ v,
-                              const T* __restrict__ w, T* __restrict__ ahead, T dt, const int* gate) {
-  if (*gate) return;
+__device__ __forceinline__ void mac_predict_face(const Dims& d, int comp, const T* u, const T* v, const T* w,
+                                                 T* ahead, T dt, int i, int j, int k) {
   int ex, ey, ez;
   comp_extent(d, comp, ex, ey, ez);
+  if (i >= ex || j >= ey || k >= ez) return;
   float fox, foy, foz;
   comp_offset(comp, fox, foy, foz);
   const T ox = (T)fox, oy = (T)foy, oz = (T)foz;
   const T* arr = comp == 0 ? u : (comp == 1 ? v : w);
-  CW_IJK(ex, ey, ez, inb);
-  if (inb) {
-    const long long c = ((long long)k * ey + j) * ex + i;
-    const T X = (T)i + ox, Y = (T)j + oy, Z = (T)k + oz;
-    T us, vs, ws;
-    velocity_at(d, u, v, w, X, Y, Z, us, vs, ws);
-    const T bx = X - dt * us / (T)d.dx, by = Y - dt * vs / (T)d.dy, bz = Z - dt * ws / (T)d.dz;
-    ahead[c] = gather<T>(arr, ex, ey, ez, bx - ox, by - oy, bz - oz, nullptr, nullptr);
-  }
+  const long long c = ((long long)k * ey + j) * ex + i;
+  const T X = (T)i + ox, Y = (T)j + oy, Z = (T)k + oz;
+  T us, vs, ws;
+  velocity_at<T>(d, comp, u, v, w, i, j, k, us, vs, ws);
+  const T bx = X - dt * us / (T)d.dx, by = Y - dt * vs / (T)d.dy, bz = Z - dt * ws / (T)d.dz;
+  ahead[c] = gather<T>(arr, ex, ey, ez, bx - ox, by - oy, bz - oz, nullptr, nullptr);
 }
 
 template <typename T>
-__global__ void k_mac_correct(Dims d, int comp, const T* __restrict__ u, const T* __restrict__ v,
-                              const T* __restrict__ w, const T* __restrict__ ahead,
-                              T* __restrict__ out, T dt, const int* gate) {
+__global__ void k_mac_predict(Dims d, const T* __restrict__ u, const T* __restrict__ v,
+                              const T* __restrict__ w, T* __restrict__ a0, T* __restrict__ a1,
+                              T* __restrict__ a2, T dt, const int* gate) {
   if (*gate) return;
+  CW_IJK(d.nx + 1, d.ny + 1, d.nz + 1, inb);
+  if (!inb) return;
+  mac_predict_face<T>(d, 0, u, v, w, a0, dt, i, j, k);
+  mac_predict_face<T>(d, 1, u, v, w, a1, dt, i, j, k);
+  if (!d.is2d) mac_predict_face<T>(d, 2, u, v, w, a2, dt, i, j, k);
+}
+
+template <typename T>
+__device__ __forceinline__ void mac_correct_face(const Dims& d, int comp, const T* u, const T* v, const T* w,
+                                                 const T* ahead, T* out, T dt, int i, int j, int k) {
   int ex, ey, ez;
   comp_extent(d, comp, ex, ey, ez);
+  if (i >= ex || j >= ey || k >= ez) return;
   float fox, foy, foz;
   comp_offset(comp, fox, foy, foz);
   const T ox = (T)fox, oy = (T)foy, oz = (T)foz;
   const T* arr = comp == 0 ? u : (comp == 1 ? v : w);
-  CW_IJK(ex, ey, ez, inb);
-  if (inb) {
-    const long long c = ((long long)k * ey + j) * ex + i;
-    const T X = (T)i + ox, Y = (T)j + oy, Z = (T)k + oz;
-    T us, vs, ws;
-    velocity_at(d, u, v, w, X, Y, Z, us, vs, ws);
-    T mn, mx;
-    const T bx = X - dt * us / (T)d.dx, by = Y - dt * vs / (T)d.dy, bz = Z - dt * ws / (T)d.dz;
-    (void)gather<T>(arr, ex, ey, ez, bx - ox, by - oy, bz - oz, &mn, &mx);
-    const T fx = X + dt * us / (T)d.dx, fy = Y + dt * vs / (T)d.dy, fz = Z + dt * ws / (T)d.dz;
-    const T back = gather<T>(ahead, ex, ey, ez, fx - ox, fy - oy, fz - oz, nullptr, nullptr);
-    T cor = ahead[c] + (T)0.5 * (arr[c] - back);
-    cor = cor < mn ? mn : cor;
-    cor = cor > mx ? mx : cor;
-    out[c] = cor;
-  }
+  const long long c = ((long long)k * ey + j) * ex + i;
+  const T X = (T)i + ox, Y = (T)j + oy, Z = (T)k + oz;
+  T us, vs, ws;
+  velocity_at<T>(d, comp, u, v, w, i, j, k, us, vs, ws);
+  T mn, mx;
+  const T bx = X - dt * us / (T)d.dx, by = Y - dt * vs / (T)d.dy, bz = Z - dt * ws / (T)d.dz;
+  (void)gather<T>(arr, ex, ey, ez, bx - ox, by - oy, bz - oz, &mn, &mx);
+  const T fx = X + dt * us / (T)d.dx, fy = Y + dt * vs / (T)d.dy, fz = Z + dt * ws / (T)d.dz;
+  const T back = gather<T>(ahead, ex, ey, ez, fx - ox, fy - oy, fz - oz, nullptr, nullptr);
+  T cor = ahead[c] + (T)0.5 * (arr[c] - back);
+  cor = cor < mn ? mn : cor;
+  cor = cor > mx ? mx : cor;
+  out[c] = cor;
+}
+
+template <typename T>
+__global__ void k_mac_correct(Dims d, const T* __restrict__ u, const T* __restrict__ v,
+                              const T* __restrict__ w, const T* __restrict__ a0, const T* __restrict__ a1,
+                              const T* __restrict__ a2, T* __restrict__ o0, T* __restrict__ o1,
+                              T* __restrict__ o2, T dt, const int* gate) {
+  if (*gate) return;
+  CW_IJK(d.nx + 1, d.ny + 1, d.nz + 1, inb);
+  if (!inb) return;
+  mac_correct_face<T>(d, 0, u, v, w, a0, o0, dt, i, j, k);
+  mac_correct_face<T>(d, 1, u, v, w, a1, o1, dt, i, j, k);
+  if (!d.is2d) mac_correct_face<T>(d, 2, u, v, w, a2, o2, dt, i, j, k);
 }
 
 // ---------------------------------------------------------------------------
