@@ -17,7 +17,6 @@
 #include "../../include/citywind_b200.h"
 #include "cw_common.cuh"
 #include "cw_pcg.cuh"
-#include "cw_pcg2.cuh"
 #include "cw_step.cuh"
 #include "cw_aux.cuh"
 
@@ -73,8 +72,6 @@ struct cw_ctx {
   int precond = 2;
   long long n_unknown = 0;
   int U = 0, ntx = 0, nty = 0, zc = 1, pcg_blocks = 0;
-  int impl = 0;                // 0: TMA ring phases (k_pcg), 1: L1 z-march phases (k_pcg2)
-  int U2 = 0, ntx2 = 0, nty2 = 0, zc2 = 1, blocks2 = 0;
   // pending reports
   int head = 0;
   std::vector<double> slot_dt;
@@ -229,23 +226,7 @@ extern "C" int cw_ctx_create(const cw_grid* g, int precision, int device, cw_ctx
     r2 |= make_tmap(&c->tm[8], CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, c->code, c, TX, TY);
     if (r2 != CW_OK) { cw_ctx_destroy(c); return CW_ERR_CUDA; }
   }
-  {
-    // second implementation: 32x8 column tiles, short z-chunks (its halo
-    // planes are L1/L2 hits), every resident block
-    int per2 = 0;
-    cudaError_t e2 = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-        &per2, precision == 4 ? (const void*)k_pcg2<float> : (const void*)k_pcg2<double>, P2_THREADS, 0);
-    if (e2 != cudaSuccess || per2 < 1) { cw_ctx_destroy(c); return fail(CW_ERR_CUDA, "k_pcg2 cannot be resident"); }
-    c->ntx2 = (d.nx + P2_TX - 1) / P2_TX;
-    c->nty2 = (d.ny + P2_TY - 1) / P2_TY;
-    c->zc2 = std::min(d.nz, 8);
-    if (const char* ev = std::getenv("CW_PCG2_ZC")) c->zc2 = std::max(1, std::min(d.nz, std::atoi(ev)));
-    c->U2 = c->ntx2 * c->nty2 * ((d.nz + c->zc2 - 1) / c->zc2);
-    c->blocks2 = std::min(c->U2, per2 * c->num_sms);
-    const char* im = std::getenv("CW_PCG_IMPL");
-    c->impl = (im && std::strcmp(im, "tma") == 0) ? 0 : ((im && std::strcmp(im, "l1") == 0) ? 1 : 0);
-  }
-  rc = alloc((void**)&c->part, 6 * (size_t)std::max(c->U, c->U2) * sizeof(double));
+  rc = alloc((void**)&c->part, 6 * (size_t)std::max(c->U, c->pcg_blocks) * sizeof(double));
   rc |= alloc((void**)&c->reg_part, (size_t)1024 * 64 * sizeof(double));
   rc |= alloc((void**)&c->reg_cnt, (size_t)1024 * 64 * sizeof(long long));
   rc |= alloc((void**)&c->reg_out, 64 * sizeof(double));
@@ -460,8 +441,7 @@ static int launch_pcg(cw_ctx* c, const cw_fields* f, DevReport* rep, double dt, 
   A.res_factor = std::pow(10.0, -4.5);   // DIV_REDUCTION_TARGET, solver.py:232
   A.max_iter = 10000;                    // project(max_iter=10_000), solver.py:249
   A.precond = c->precond;
-  if (c->impl == 1) { A.ntx = c->ntx2; A.nty = c->nty2; A.zc = c->zc2; A.U = c->U2; }
-  else { A.ntx = c->ntx; A.nty = c->nty; A.zc = c->zc; A.U = c->U; }
+  A.ntx = c->ntx; A.nty = c->nty; A.zc = c->zc; A.U = c->U;
   A.timeout_ns = 20LL * 1000 * 1000 * 1000;
   A.probe_mode = 0;
   A.probe_iters = 0;
@@ -472,10 +452,7 @@ static int launch_pcg(cw_ctx* c, const cw_fields* f, DevReport* rep, double dt, 
   }
   CW_CUDA(cudaMemsetAsync(c->bar, 0, 64 * sizeof(unsigned), st));
   void* args[] = {&A};
-  if (c->impl == 1)
-    CW_CUDA(cudaLaunchCooperativeKernel((const void*)k_pcg2<T>, dim3(c->blocks2), dim3(P2_THREADS), args, 0, st));
-  else
-    CW_CUDA(cudaLaunchCooperativeKernel((const void*)k_pcg<T>, dim3(c->pcg_blocks), dim3(PCG_THREADS), args, c->pcg_smem, st));
+  CW_CUDA(cudaLaunchCooperativeKernel((const void*)k_pcg<T>, dim3(c->pcg_blocks), dim3(PCG_THREADS), args, c->pcg_smem, st));
   return CW_OK;
 }
 
