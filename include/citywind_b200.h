@@ -28,7 +28,7 @@
 extern "C" {
 #endif
 
-#define CW_ABI_VERSION 1
+#define CW_ABI_VERSION 2
 
 #define CW_OK 0
 #define CW_ERR_INVALID 1       /* ValueError: bad argument / shape */
@@ -89,6 +89,56 @@ const char *cw_last_error(void);
 int cw_ctx_create(const cw_grid *grid, int precision, int device, cw_ctx **out);
 void cw_ctx_destroy(cw_ctx *ctx);
 
+/* z-slab decomposition (the reference is single-process, so these
+ * have no reference counterpart: they split the grid of one
+ * CompiledScenario, ref scenario.py:364-381, over devices).
+ * A slab context covers global planes [k_lo - halo, k_hi + halo) clipped to
+ * [0, nz) and owns [k_lo, k_hi).  Its fields are that window (x-fastest, the
+ * same shapes as a grid of nz_local planes).  Every stage runs on the whole
+ * window; reductions and reports cover the owned planes only.  The caller
+ * refreshes the halo planes from the neighbours (state at the start of a
+ * step, p after the projection).  halo >= 2. */
+#define CW_MAX_SLABS 64
+int cw_ctx_create_slab(const cw_grid *global_grid, int k_lo, int k_hi, int halo, int precision,
+                       int device, cw_ctx **out);
+int cw_slab_info(cw_ctx *ctx, int *kg0, int *nz_local, int *own0, int *own1);
+
+/* Owned-plane sums behind default_projection_tol (ref solver.py:235-243) for
+ * combining over slabs: sum of diag(W) (AI1), sum of 1/diag(A) (Jacobi),
+ * unknown count, and whether the window has an outlet cell. */
+int cw_operator_partials(cw_ctx *ctx, double *wdiag_sum, double *jacobi_sum, long long *n_unknown,
+                         int *has_outlet);
+
+/* Device buffers a neighbouring slab writes into (halo planes of the pitched
+ * PCG vectors) and the root slab's barrier / value table.  o0, o1: the
+ * owner's owned local planes. */
+typedef struct {
+  void *r0, *r1, *p0, *p1, *z, *Ap;
+  void *xbar, *xval;
+  int o0, o1;
+} cw_slab_buffers;
+int cw_slab_buffers_get(cw_ctx *ctx, cw_slab_buffers *out);
+
+/* One device per slab: attach this context as slab `slab` of `nslab` with
+ * the neighbours' buffers (NULL z pointer = no neighbour) and the root
+ * slab's (slab 0) barrier, as pointers valid on this device (same process,
+ * or opened with cw_ipc_open).  The projection then pushes its boundary
+ * planes into the neighbours while it computes them and meets the other
+ * slabs at the root's barrier (system-scope atomics over NVLink). */
+int cw_slab_attach(cw_ctx *ctx, int slab, int nslab, const cw_slab_buffers *lower,
+                   const cw_slab_buffers *upper, const cw_slab_buffers *root);
+
+/* All slabs on one device: the projection of every slab in one cooperative
+ * launch (the same kernel code as the attached multi-device solve, blocks
+ * partitioned by slab).  ctxs in z order, fields per slab. */
+int cw_slab_group_pcg(cw_ctx **ctxs, const cw_fields *fields, int n, const cw_params *prm,
+                      double pcg_tol, void *stream);
+
+/* CUDA IPC for cw_slab_buffers between processes (64-byte handles). */
+int cw_ipc_get(void *d_ptr, unsigned char handle[64]);
+int cw_ipc_open(const unsigned char handle[64], int device, void **d_ptr);
+int cw_ipc_close(void *d_ptr);
+
 /* build_pressure_matrix + build_ai_preconditioner(A, omega, 1, truncate=False)
  * (ref linalg.py:57-126, 201-232; called from scenario.py:377-379), matrix-free:
  * derives the per-cell operator code from labels (device int8).  Returns the
@@ -128,6 +178,13 @@ int cw_step(cw_ctx *ctx, const cw_fields *f, const cw_params *prm, const cw_inle
 #define CW_STAGE_BOUNDARY 4
 #define CW_STAGE_PROJECT 5
 #define CW_STAGE_TURBULENCE 6
+/* a step split around the projection (z-slab steps exchange halos between):
+ * PRE = advect, diffuse, drag, boundary; SOLVE = the PCG alone (p on the
+ * owned planes); POST = pressure gradient, div after, turbulence, boundary,
+ * CFL.  PRE, SOLVE, POST in order equal one step. */
+#define CW_STAGE_PRE 7
+#define CW_STAGE_POST 8
+#define CW_STAGE_SOLVE 9
 int cw_run_stage(cw_ctx *ctx, const cw_fields *f, const cw_params *prm, const cw_inlet *inl,
                  int stage, double pcg_tol, void *stream);
 

@@ -59,6 +59,17 @@ class cw_object(C.Structure):
                 ("n_verts", C.c_int), ("tri_offset", C.c_int), ("n_tris", C.c_int)]
 
 
+class cw_slab_buffers(C.Structure):
+    _fields_ = [("r0", C.c_void_p), ("r1", C.c_void_p), ("p0", C.c_void_p), ("p1", C.c_void_p),
+                ("z", C.c_void_p), ("Ap", C.c_void_p), ("xbar", C.c_void_p), ("xval", C.c_void_p),
+                ("o0", C.c_int), ("o1", C.c_int)]
+
+    BUFFERS = ("r0", "r1", "p0", "p1", "z", "Ap", "xbar", "xval")
+
+
+CW_STAGE_PRE, CW_STAGE_POST, CW_STAGE_SOLVE = 7, 8, 9
+CW_MAX_SLABS = 64
+
 # exported symbol -> (restype, argtypes); must match include/citywind_b200.h
 _P = C.c_void_p
 SIGNATURES = {
@@ -66,6 +77,20 @@ SIGNATURES = {
     "cw_last_error": (C.c_char_p, []),
     "cw_ctx_create": (C.c_int, [C.POINTER(cw_grid), C.c_int, C.c_int, C.POINTER(_P)]),
     "cw_ctx_destroy": (None, [_P]),
+    "cw_ctx_create_slab": (C.c_int, [C.POINTER(cw_grid), C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                                     C.POINTER(_P)]),
+    "cw_slab_info": (C.c_int, [_P, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int),
+                               C.POINTER(C.c_int)]),
+    "cw_operator_partials": (C.c_int, [_P, C.POINTER(C.c_double), C.POINTER(C.c_double),
+                                       C.POINTER(C.c_longlong), C.POINTER(C.c_int)]),
+    "cw_slab_buffers_get": (C.c_int, [_P, C.POINTER(cw_slab_buffers)]),
+    "cw_slab_attach": (C.c_int, [_P, C.c_int, C.c_int, C.POINTER(cw_slab_buffers),
+                                 C.POINTER(cw_slab_buffers), C.POINTER(cw_slab_buffers)]),
+    "cw_slab_group_pcg": (C.c_int, [C.POINTER(_P), C.POINTER(cw_fields), C.c_int, C.POINTER(cw_params),
+                                    C.c_double, _P]),
+    "cw_ipc_get": (C.c_int, [_P, C.POINTER(C.c_ubyte)]),
+    "cw_ipc_open": (C.c_int, [C.POINTER(C.c_ubyte), C.c_int, C.POINTER(_P)]),
+    "cw_ipc_close": (C.c_int, [_P]),
     "cw_set_operator": (C.c_int, [_P, _P, C.c_double, C.POINTER(C.c_longlong),
                                   C.POINTER(C.c_double), _P]),
     "cw_set_preconditioner": (C.c_int, [_P, C.c_int, C.POINTER(C.c_double)]),

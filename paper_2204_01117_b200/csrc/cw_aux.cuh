@@ -45,7 +45,7 @@ __global__ void k_build_code(Dims d, int nxp, const int8_t* __restrict__ lab, ui
     }
     code[pc] = cd;
     if (outl) atomicOr(&flag[0], 1);
-    if ((cd & 63) == 0) atomicOr(&flag[1], 1);
+    if ((cd & 63) == 0 && k >= d.o0 && k < d.o1) atomicOr(&flag[1], 1);   // owned planes (z-slab halos are partial)
   }
 }
 
@@ -63,11 +63,12 @@ __device__ __forceinline__ double code_d(uint8_t cd, double wx, double wy, doubl
 __global__ void k_wdiag_partials(Dims d, int nxp, const uint8_t* __restrict__ code, double wx, double wy, double wz,
                                  double om, double* part, long long* cnt, double* jpart) {
   __shared__ double red[32];
-  const long long n = d.ncell();
+  const long long plane = (long long)d.nx * d.ny;
   double acc = 0.0, jacc = 0.0;
   long long m = 0;
   const double w[3] = {wx, wy, wz};
-  CW_GRID_STRIDE(c0, n) {
+  for (long long c0 = d.o0 * plane + (long long)blockIdx.x * blockDim.x + threadIdx.x; c0 < d.o1 * plane;
+       c0 += (long long)gridDim.x * blockDim.x) {   // owned planes
     const int pos[3] = {(int)(c0 % d.nx), (int)((c0 / d.nx) % d.ny), (int)(c0 / ((long long)d.nx * d.ny))};
     const long long c = ((long long)pos[2] * d.ny + pos[1]) * nxp + pos[0];
     const uint8_t cd = code[c];
@@ -129,13 +130,14 @@ __global__ void k_region_partials(Dims d, double ox, double oy, double oz, const
   double s[16];
   long long m[16];
   for (int b = 0; b < 16; ++b) { s[b] = 0.0; m[b] = 0; }
-  const long long n = d.ncell();
-  CW_GRID_STRIDE(c, n) {
+  const long long plane = (long long)d.nx * d.ny;
+  for (long long c = d.o0 * plane + (long long)blockIdx.x * blockDim.x + threadIdx.x; c < d.o1 * plane;
+       c += (long long)gridDim.x * blockDim.x) {   // owned planes
     if (lab[c] != AIR) continue;
     const int i = (int)(c % d.nx), j = (int)((c / d.nx) % d.ny), k = (int)(c / ((long long)d.nx * d.ny));
     const double cx = ox + ((double)i + 0.5) * d.ddx;
     const double cy = oy + ((double)j + 0.5) * d.ddy;
-    const double cz = oz + ((double)k + 0.5) * d.ddz;
+    const double cz = oz + ((double)(k + d.kg0) + 0.5) * d.ddz;   // global plane index
     bool anyb = false;
     for (int b = 0; b < B.n; ++b)
       anyb |= cx >= B.lo[b][0] && cx <= B.hi[b][0] && cy >= B.lo[b][1] && cy <= B.hi[b][1] &&

@@ -71,7 +71,18 @@ struct cw_ctx {
   double tol_kind[3] = {1e-8, 0.0, 0.0};   // default_projection_tol per preconditioner kind
   int precond = 2;
   long long n_unknown = 0;
-  int U = 0, ntx = 0, nty = 0, zc = 1, pcg_blocks = 0;
+  double op_sum[2] = {0.0, 0.0};   // owned-plane sums of diag(W) (AI1) and 1/d (Jacobi)
+  long long op_n = 0;
+  bool op_outlet = false;
+  int U = 0, ntx = 0, nty = 0, zc = 1, pcg_blocks = 0, part_stride = 0;
+  int max_blocks = 0;          // co-resident PCG blocks on this device
+  // z-slab solve across devices (cw_slab_attach): this slab's place and the
+  // neighbours' / root's buffers (device pointers valid on this device)
+  int nslab = 1, slab = 0;
+  cw_slab_buffers lower{}, upper{}, root{};
+  unsigned* xbar = nullptr;    // this context's cross-slab barrier (used when it is the root)
+  double* xval = nullptr;
+  void* slab_args = nullptr;   // device array of per-slab kernel arguments (group launches)
   // pending reports
   int head = 0;
   std::vector<double> slot_dt;
@@ -94,6 +105,8 @@ extern "C" int cw_abi_version(void) { return CW_ABI_VERSION; }
 // shared with cw_voxel.cu
 int cw_internal_fail(int code, const char* msg) { return fail(code, msg); }
 int cw_internal_device(cw_ctx* c, int* nx, int* ny, int* nz, double* h, double* origin) {
+  if (c->d.kg0 != 0 || c->d.nz != c->d.nzg)
+    return fail(CW_ERR_INVALID, "voxelize on a whole-grid context and copy the slab's window");
   cudaError_t e = cudaSetDevice(c->device);
   if (e != cudaSuccess) return fail(CW_ERR_CUDA, cudaGetErrorString(e));
   *nx = c->d.nx; *ny = c->d.ny; *nz = c->d.nz;
@@ -114,9 +127,15 @@ static int alloc(void** p, size_t bytes) {
 template <typename T>
 static int pcg_occupancy(int* blocks_per_sm, size_t* smem) {
   *smem = pcg_smem_bytes<T>();
-  cudaError_t e = cudaFuncSetAttribute(k_pcg<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)*smem);
+  cudaError_t e = cudaFuncSetAttribute(k_pcg<T, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)*smem);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_pcg<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)*smem);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_pcg_slabs<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)*smem);
   if (e != cudaSuccess) return fail(CW_ERR_CUDA, std::string("smem attribute: ") + cudaGetErrorString(e));
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_pcg<T>, PCG_THREADS, *smem);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_pcg<T, false>, PCG_THREADS, *smem);
+  int b1 = 0, b2 = 0;
+  if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b1, k_pcg<T, true>, PCG_THREADS, *smem);
+  if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b2, k_pcg_slabs<T>, PCG_THREADS, *smem);
+  *blocks_per_sm = std::min(*blocks_per_sm, std::min(b1, b2));
   if (e != cudaSuccess) return fail(CW_ERR_CUDA, std::string("occupancy: ") + cudaGetErrorString(e));
   return CW_OK;
 }
@@ -143,7 +162,10 @@ static int make_tmap(CUtensorMap* m, CUtensorMapDataType dt, size_t esz, void* b
   return CW_OK;
 }
 
-extern "C" int cw_ctx_create(const cw_grid* g, int precision, int device, cw_ctx** out) {
+// A context over the local grid g (a whole grid, or a z-slab window: global
+// planes [kg0, kg0 + g->nz) of nzg, owning local planes [own0, own1)).
+static int ctx_create(const cw_grid* g, int kg0, int nzg, int own0, int own1, int precision, int device,
+                      cw_ctx** out) {
   if (!g || !out) return fail(CW_ERR_INVALID, "null argument");
   if (precision != 4 && precision != 8) return fail(CW_ERR_INVALID, "precision must be 4 or 8");
   if (g->nx < 1 || g->ny < 1 || g->nz < 1) return fail(CW_ERR_INVALID, "cell counts must be >= 1");
@@ -160,6 +182,7 @@ extern "C" int cw_ctx_create(const cw_grid* g, int precision, int device, cw_ctx
   d.dx = (float)g->dx; d.dy = (float)g->dy; d.dz = (float)g->dz;
   d.ddx = g->dx; d.ddy = g->dy; d.ddz = g->dz;
   d.is2d = g->nz == 1;
+  d.o0 = own0; d.o1 = own1; d.kg0 = kg0; d.nzg = nzg;
   c->ncell = d.ncell();
   c->nu_ = (long long)(d.nx + 1) * d.ny * d.nz;
   c->nv_ = (long long)d.nx * (d.ny + 1) * d.nz;
@@ -193,22 +216,24 @@ extern "C" int cw_ctx_create(const cw_grid* g, int precision, int device, cw_ctx
   rc = precision == 4 ? pcg_occupancy<float>(&per_sm, &c->pcg_smem) : pcg_occupancy<double>(&per_sm, &c->pcg_smem);
   if (rc != CW_OK || per_sm < 1) { cw_ctx_destroy(c); return rc != CW_OK ? rc : fail(CW_ERR_CUDA, "pcg kernel cannot be resident"); }
   const int maxb = per_sm * c->num_sms;
+  c->max_blocks = maxb;
   c->ntx = (d.nx + TX - 1) / TX;
   c->nty = (d.ny + TY - 1) / TY;
   const int tiles = c->ntx * c->nty;
   // choose the z-chunk: each block streams ceil(U/B) units of zc+2 planes;
   // minimise that critical path (halo planes included).  CW_PCG_ZC overrides.
-  int best_zc = d.nz, best_cost = 1 << 30;
-  for (int zc = 1; zc <= d.nz; ++zc) {
-    const int U = tiles * ((d.nz + zc - 1) / zc);
+  const int nown = d.o1 - d.o0;
+  int best_zc = nown, best_cost = 1 << 30;
+  for (int zc = 1; zc <= nown; ++zc) {
+    const int U = tiles * ((nown + zc - 1) / zc);
     const int B = std::min(U, maxb);
     const int m = (U + B - 1) / B;
     const int cost = m * (zc + 2);
     if (cost < best_cost) { best_cost = cost; best_zc = zc; }
   }
-  if (const char* ev = std::getenv("CW_PCG_ZC")) best_zc = std::max(1, std::min(d.nz, std::atoi(ev)));
+  if (const char* ev = std::getenv("CW_PCG_ZC")) best_zc = std::max(1, std::min(nown, std::atoi(ev)));
   c->zc = best_zc;
-  c->U = tiles * ((d.nz + best_zc - 1) / best_zc);
+  c->U = tiles * ((nown + best_zc - 1) / best_zc);
   c->pcg_blocks = std::min(c->U, maxb);
   if (const char* eb = std::getenv("CW_PCG_BLOCKS")) c->pcg_blocks = std::max(1, std::min(c->pcg_blocks, std::atoi(eb)));
   {
@@ -226,7 +251,11 @@ extern "C" int cw_ctx_create(const cw_grid* g, int precision, int device, cw_ctx
     r2 |= make_tmap(&c->tm[8], CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, c->code, c, TX, TY);
     if (r2 != CW_OK) { cw_ctx_destroy(c); return CW_ERR_CUDA; }
   }
-  rc = alloc((void**)&c->part, 6 * (size_t)std::max(c->U, c->pcg_blocks) * sizeof(double));
+  c->part_stride = std::max(c->U, maxb);
+  rc = alloc((void**)&c->part, 6 * (size_t)c->part_stride * sizeof(double));
+  rc |= alloc((void**)&c->xbar, 64 * sizeof(unsigned));
+  rc |= alloc((void**)&c->xval, 6 * (size_t)CW_MAX_SLABS * sizeof(double));
+  rc |= alloc(&c->slab_args, (size_t)CW_MAX_SLABS * sizeof(PcgArgs<double>));
   rc |= alloc((void**)&c->reg_part, (size_t)1024 * 64 * sizeof(double));
   rc |= alloc((void**)&c->reg_cnt, (size_t)1024 * 64 * sizeof(long long));
   rc |= alloc((void**)&c->reg_out, 64 * sizeof(double));
@@ -237,13 +266,38 @@ extern "C" int cw_ctx_create(const cw_grid* g, int precision, int device, cw_ctx
   return CW_OK;
 }
 
+extern "C" int cw_ctx_create(const cw_grid* g, int precision, int device, cw_ctx** out) {
+  if (!g) return fail(CW_ERR_INVALID, "null argument");
+  return ctx_create(g, 0, g->nz, 0, g->nz, precision, device, out);
+}
+
+extern "C" int cw_ctx_create_slab(const cw_grid* g, int k_lo, int k_hi, int halo, int precision, int device,
+                                  cw_ctx** out) {
+  if (!g || !out) return fail(CW_ERR_INVALID, "null argument");
+  if (!(0 <= k_lo && k_lo < k_hi && k_hi <= g->nz)) return fail(CW_ERR_INVALID, "slab planes must satisfy 0 <= k_lo < k_hi <= nz");
+  if (halo < 2) return fail(CW_ERR_INVALID, "slab halo must be >= 2 planes");
+  const int kb = std::max(k_lo - halo, 0), ke = std::min(k_hi + halo, g->nz);
+  cw_grid loc = *g;
+  loc.nz = ke - kb;   // origin stays the global one: heights use the global plane index
+  return ctx_create(&loc, kb, g->nz, k_lo - kb, k_hi - kb, precision, device, out);
+}
+
+extern "C" int cw_slab_info(cw_ctx* c, int* kg0, int* nz_local, int* own0, int* own1) {
+  if (!c) return fail(CW_ERR_INVALID, "null argument");
+  if (kg0) *kg0 = c->d.kg0;
+  if (nz_local) *nz_local = c->d.nz;
+  if (own0) *own0 = c->d.o0;
+  if (own1) *own1 = c->d.o1;
+  return CW_OK;
+}
+
 extern "C" void cw_ctx_destroy(cw_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
   void* ptrs[] = {c->tk, c->tw, c->speed, c->ahead[0], c->ahead[1], c->ahead[2], c->adv[0], c->adv[1],
                   c->adv[2], c->r0, c->r1, c->p0, c->p1, c->z, c->Ap, c->xw, c->lut, c->uzx, c->uzy, c->code,
                   c->part, c->bar, c->gate, c->rep, c->reg_part, c->reg_cnt, c->reg_out, c->reg_cout,
-                  c->flag};
+                  c->flag, c->xbar, c->xval, c->slab_args};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->ev_made)
@@ -313,19 +367,33 @@ extern "C" int cw_set_operator(cw_ctx* c, const signed char* lab, double ai_omeg
   double sum = 0.0, jsum = 0.0;
   long long n = 0;
   for (int b = 0; b < nb; ++b) { sum += parts[b]; jsum += jparts[b]; n += cnts[b]; }
-  if (n == 0) return fail(CW_ERR_INVALID, "no flow cells to solve for");
-  if (flags[0] == 0) return fail(CW_ERR_SINGULAR, "no outlet cells: pressure defined only up to a constant");
+  const bool slab = d.kg0 != 0 || d.nz != d.nzg;
+  c->op_sum[0] = sum; c->op_sum[1] = jsum; c->op_n = n; c->op_outlet = flags[0] != 0;
+  // a z-slab's operator checks are global: the caller combines cw_operator_partials
+  if (n == 0 && !slab) return fail(CW_ERR_INVALID, "no flow cells to solve for");
+  if (flags[0] == 0 && !slab) return fail(CW_ERR_SINGULAR, "no outlet cells: pressure defined only up to a constant");
   if (flags[1] != 0) return fail(CW_ERR_INVALID, "AI preconditioner requires a positive diagonal");
   c->omega = ai_omega;
   c->n_unknown = n;
-  const double mean = sum / (double)n;
+  const double mean = n > 0 ? sum / (double)n : 0.0;
   c->tol_kind[0] = 1e-8;                                           // no W: mscale 1
-  c->tol_kind[1] = 1e-8 * std::max(jsum / (double)n, 1e-300);      // Jacobi W = diag(1/d)
+  c->tol_kind[1] = 1e-8 * std::max(n > 0 ? jsum / (double)n : 0.0, 1e-300);   // Jacobi W = diag(1/d)
   c->tol_kind[2] = 1e-8 * std::max(mean, 1e-300);                  // AI1
   c->tol_default = c->tol_kind[c->precond];
   c->have_op = true;
   if (n_unknown) *n_unknown = n;
   if (tol_default) *tol_default = c->tol_default;
+  return CW_OK;
+}
+
+extern "C" int cw_operator_partials(cw_ctx* c, double* wdiag_sum, double* jacobi_sum, long long* n_unknown,
+                                    int* has_outlet) {
+  if (!c) return fail(CW_ERR_INVALID, "null argument");
+  if (!c->have_op) return fail(CW_ERR_INVALID, "cw_set_operator first");
+  if (wdiag_sum) *wdiag_sum = c->op_sum[0];
+  if (jacobi_sum) *jacobi_sum = c->op_sum[1];
+  if (n_unknown) *n_unknown = c->op_n;
+  if (has_outlet) *has_outlet = c->op_outlet ? 1 : 0;
   return CW_OK;
 }
 
@@ -357,7 +425,7 @@ static int upload_inlet(cw_ctx* c, const cw_inlet* inl, cudaStream_t st) {
   const int nz = c->d.nz;
   std::vector<double> ux(nz), uy(nz);
   for (int k = 0; k < nz; ++k) {
-    const double zc = c->grid.origin[2] + ((double)k + 0.5) * c->grid.dz;   // solver.py:384
+    const double zc = c->grid.origin[2] + ((double)(k + c->d.kg0) + 0.5) * c->grid.dz;   // solver.py:384
     double s;
     if (inl->kind == 0) s = inl->speed;
     else s = zc > inl->z0 ? inl->u_star / inl->kappa * std::log(zc / inl->z0) : 0.0;   // solver.py:75-82
@@ -416,8 +484,7 @@ extern "C" int cw_apply_boundary(cw_ctx* c, const cw_fields* f, const cw_params*
 // the step
 
 template <typename T>
-static int launch_pcg(cw_ctx* c, const cw_fields* f, DevReport* rep, double dt, double tol, cudaStream_t st) {
-  PcgArgs<T> A;
+static void fill_pcg_args(PcgArgs<T>& A, cw_ctx* c, const cw_fields* f, DevReport* rep, double dt, double tol) {
   A.tm_z = c->tm[0]; A.tm_p0 = c->tm[1]; A.tm_p1 = c->tm[2]; A.tm_x = c->tm[3]; A.tm_ap = c->tm[4];
   A.tm_r0 = c->tm[5]; A.tm_r1 = c->tm[6]; A.tm_code = c->tm[7]; A.tm_code_own = c->tm[8];
   A.d = c->d;
@@ -428,6 +495,7 @@ static int launch_pcg(cw_ctx* c, const cw_fields* f, DevReport* rep, double dt, 
   A.r0 = (double*)c->r0; A.r1 = (double*)c->r1; A.p0 = (T*)c->p0; A.p1 = (T*)c->p1; A.z = (T*)c->z; A.Ap = (T*)c->Ap;
   A.x = (T*)c->xw;
   A.part = c->part;
+  A.PS = c->part_stride;
   A.bar = c->bar;
   A.gate = c->gate;
   A.rep = rep;
@@ -442,6 +510,10 @@ static int launch_pcg(cw_ctx* c, const cw_fields* f, DevReport* rep, double dt, 
   A.max_iter = 10000;                    // project(max_iter=10_000), solver.py:249
   A.precond = c->precond;
   A.ntx = c->ntx; A.nty = c->nty; A.zc = c->zc; A.U = c->U;
+  A.o0 = c->d.o0; A.o1 = c->d.o1;
+  A.nslab = 1; A.slab = 0;
+  A.lo = PcgPeer<T>{}; A.hi = PcgPeer<T>{};
+  A.xbar = nullptr; A.xval = nullptr;
   A.timeout_ns = 20LL * 1000 * 1000 * 1000;
   A.probe_mode = 0;
   A.probe_iters = 0;
@@ -450,9 +522,39 @@ static int launch_pcg(cw_ctx* c, const cw_fields* f, DevReport* rep, double dt, 
     const char* comma = std::strchr(pe, 0x2c);
     A.probe_iters = comma ? std::atoi(comma + 1) : 100;
   }
+}
+
+template <typename T>
+static PcgPeer<T> peer_of(const cw_slab_buffers& b, int plane, long long pplane) {
+  PcgPeer<T> q{};
+  if (!b.z) return q;
+  q.r0 = (double*)b.r0; q.r1 = (double*)b.r1;
+  q.p0 = (T*)b.p0; q.p1 = (T*)b.p1; q.z = (T*)b.z; q.Ap = (T*)b.Ap;
+  q.plane_off = (long long)plane * pplane;
+  return q;
+}
+
+// this context's slab within an attached multi-device solve
+template <typename T>
+static void set_slab_peers(PcgArgs<T>& A, const cw_ctx* c) {
+  const long long pplane = (long long)c->nxp * c->d.ny;
+  A.nslab = c->nslab;
+  A.slab = c->slab;
+  A.lo = peer_of<T>(c->lower, c->lower.o1, pplane);       // their halo plane above their slab
+  A.hi = peer_of<T>(c->upper, c->upper.o0 - 1, pplane);   // their halo plane below their slab
+  A.xbar = (unsigned*)c->root.xbar;
+  A.xval = (double*)c->root.xval;
+}
+
+template <typename T>
+static int launch_pcg(cw_ctx* c, const cw_fields* f, DevReport* rep, double dt, double tol, cudaStream_t st) {
+  PcgArgs<T> A;
+  fill_pcg_args<T>(A, c, f, rep, dt, tol);
+  if (c->nslab > 1) set_slab_peers<T>(A, c);
   CW_CUDA(cudaMemsetAsync(c->bar, 0, 64 * sizeof(unsigned), st));
   void* args[] = {&A};
-  CW_CUDA(cudaLaunchCooperativeKernel((const void*)k_pcg<T>, dim3(c->pcg_blocks), dim3(PCG_THREADS), args, c->pcg_smem, st));
+  const void* kfn = c->nslab > 1 ? (const void*)k_pcg<T, true> : (const void*)k_pcg<T, false>;
+  CW_CUDA(cudaLaunchCooperativeKernel(kfn, dim3(c->pcg_blocks), dim3(PCG_THREADS), args, c->pcg_smem, st));
   return CW_OK;
 }
 
@@ -512,6 +614,9 @@ static void st_drag(cw_ctx* c, const StepPtrs<T>& P, const cw_params* prm, int h
 }
 
 template <typename T>
+static void st_project_tail(cw_ctx* c, const StepPtrs<T>& P, const cw_params* prm, DevReport* rep, cudaStream_t st);
+
+template <typename T>
 static int st_project(cw_ctx* c, const StepPtrs<T>& P, const cw_fields* f, const cw_params* prm, double tol,
                       DevReport* rep, cudaStream_t st) {
   const Dims& d = c->d;
@@ -523,10 +628,18 @@ static int st_project(cw_ctx* c, const StepPtrs<T>& P, const cw_fields* f, const
   ++c->launches;
   if (tpcg) cudaEventRecord(c->pev[2 * c->pcg_timed++ + 1], st);
   if (rc) return rc;
+  st_project_tail<T>(c, P, prm, rep, st);
+  return CW_OK;
+}
+
+// after the PCG: pressure-gradient update and max |div| (solver.py:282-304)
+template <typename T>
+static void st_project_tail(cw_ctx* c, const StepPtrs<T>& P, const cw_params* prm, DevReport* rep, cudaStream_t st) {
+  const Dims& d = c->d;
+  T* cu[3] = {P.u, P.v, P.w};
   for (int a = 0; a < (d.is2d ? 2 : 3); ++a)
     (k_gradient<T><<<g3c(d, a), B3, 0, st>>>(d, a, cu[a], P.p, P.lab, (T)prm->dt, c->gate), ++c->launches);
-  (k_div_max<T><<<g3(d.nx, d.ny, d.nz), B3, 0, st>>>(d, P.u, P.v, P.w, P.lab, rep, SLOT_DIV_AFTER, c->gate), ++c->launches);
-  return CW_OK;
+  (k_div_max<T><<<g3(d.nx, d.ny, d.o1 - d.o0), B3, 0, st>>>(d, P.u, P.v, P.w, P.lab, rep, SLOT_DIV_AFTER, c->gate), ++c->launches);
 }
 
 template <typename T>
@@ -579,7 +692,8 @@ static int enqueue_step(cw_ctx* c, const cw_fields* f, const cw_params* prm, dou
   mark(6);
   BcFields<T> F2{P.u, P.v, P.w, P.p, P.k, P.om, P.nut};
   launch_bc<T>(c, F2, P.lab, prm, st);                        // "boundary2"
-  (k_speed_max<T><<<nblk(c->nu_ + c->nv_ + c->nw_), 256, 0, st>>>(c->nu_, c->nv_, c->nw_, P.u, P.v, P.w, rep, c->gate), ++c->launches);
+  (k_speed_max<T><<<g3(c->d.nx + 1, c->d.ny + 1, c->d.o1 - c->d.o0 + 1), B3, 0, st>>>(c->d, P.u, P.v, P.w, rep, c->gate),
+   ++c->launches);
   mark(7);
   CW_CUDA(cudaGetLastError());
   return CW_OK;
@@ -624,6 +738,36 @@ static int enqueue_stage(cw_ctx* c, const cw_fields* f, const cw_params* prm, in
       if (rc) return rc;
       break;
     }
+    case CW_STAGE_PRE: {        // step() up to the projection; k, omega stay in tk, tw until POST
+      const bool turb = prm->turbulence != 0;
+      st_advect<T>(c, P, prm, (T*)c->tk, (T*)c->tw, st);
+      st_diffuse<T>(c, P, prm, st);
+      st_drag<T>(c, P, prm, f->has_drag, st);
+      StepPtrs<T> B = P;
+      if (turb) { B.k = (T*)c->tk; B.om = (T*)c->tw; }
+      BcFields<T> F1{B.u, B.v, B.w, B.p, B.k, B.om, B.nut};
+      launch_bc<T>(c, F1, P.lab, prm, st);
+      break;
+    }
+    case CW_STAGE_SOLVE: {
+      if (!c->have_op) return fail(CW_ERR_INVALID, "cw_set_operator has not been called");
+      const bool tpcg = c->pcg_timed < (int)c->pev.size() / 2;
+      if (tpcg) cudaEventRecord(c->pev[2 * c->pcg_timed], st);
+      int rc = launch_pcg<T>(c, f, rep, prm->dt, tol, st);
+      ++c->launches;
+      if (tpcg) cudaEventRecord(c->pev[2 * c->pcg_timed++ + 1], st);
+      if (rc) return rc;
+      break;
+    }
+    case CW_STAGE_POST: {       // step() after the projection
+      st_project_tail<T>(c, P, prm, rep, st);
+      if (prm->turbulence) st_turb<T>(c, P, prm, (const T*)c->tk, (const T*)c->tw, rep, st);
+      BcFields<T> F2{P.u, P.v, P.w, P.p, P.k, P.om, P.nut};
+      launch_bc<T>(c, F2, P.lab, prm, st);
+      (k_speed_max<T><<<g3(d.nx + 1, d.ny + 1, d.o1 - d.o0 + 1), B3, 0, st>>>(d, P.u, P.v, P.w, rep, c->gate),
+       ++c->launches);
+      break;
+    }
     case CW_STAGE_TURBULENCE:
       CW_CUDA(cudaMemcpyAsync(c->tk, P.k, cb, cudaMemcpyDeviceToDevice, st));
       CW_CUDA(cudaMemcpyAsync(c->tw, P.om, cb, cudaMemcpyDeviceToDevice, st));
@@ -633,6 +777,122 @@ static int enqueue_stage(cw_ctx* c, const cw_fields* f, const cw_params* prm, in
       return fail(CW_ERR_INVALID, "unknown stage");
   }
   CW_CUDA(cudaGetLastError());
+  return CW_OK;
+}
+
+// ---------------------------------------------------------------------------
+// z-slab solves
+
+extern "C" int cw_slab_buffers_get(cw_ctx* c, cw_slab_buffers* out) {
+  if (!c || !out) return fail(CW_ERR_INVALID, "null argument");
+  out->r0 = c->r0; out->r1 = c->r1; out->p0 = c->p0; out->p1 = c->p1; out->z = c->z; out->Ap = c->Ap;
+  out->xbar = c->xbar; out->xval = c->xval;
+  out->o0 = c->d.o0; out->o1 = c->d.o1;
+  return CW_OK;
+}
+
+extern "C" int cw_slab_attach(cw_ctx* c, int slab, int nslab, const cw_slab_buffers* lower,
+                              const cw_slab_buffers* upper, const cw_slab_buffers* root) {
+  if (!c || !root) return fail(CW_ERR_INVALID, "null argument");
+  if (nslab < 1 || nslab > CW_MAX_SLABS || slab < 0 || slab >= nslab) return fail(CW_ERR_INVALID, "bad slab index");
+  const bool has_lo = c->d.kg0 + c->d.o0 > 0, has_hi = c->d.kg0 + c->d.o1 < c->d.nzg;
+  if (has_lo != (lower && lower->z != nullptr) || has_hi != (upper && upper->z != nullptr))
+    return fail(CW_ERR_INVALID, "neighbour buffers must be given exactly for interior slab faces");
+  if ((lower && lower->z && lower->o1 < 1) || (upper && upper->z && upper->o0 < 1))
+    return fail(CW_ERR_INVALID, "neighbour slab has no halo plane");
+  c->slab = slab;
+  c->nslab = nslab;
+  c->lower = lower ? *lower : cw_slab_buffers{};
+  c->upper = upper ? *upper : cw_slab_buffers{};
+  c->root = *root;
+  return CW_OK;
+}
+
+template <typename T>
+static int group_pcg(cw_ctx** cs, const cw_fields* fs, int n, const cw_params* prm, double pcg_tol,
+                     cudaStream_t st) {
+  cw_ctx* c0 = cs[0];
+  // blocks per slab: every slab gets the same share of the co-resident blocks
+  int umax = 0;
+  for (int s = 0; s < n; ++s) umax = std::max(umax, cs[s]->U);
+  const int bps = std::max(1, std::min(c0->max_blocks / n, umax));
+  std::vector<PcgArgs<T>> args(n);
+  for (int s = 0; s < n; ++s) {
+    cw_ctx* c = cs[s];
+    const double tol = pcg_tol < 0 || std::isnan(pcg_tol) ? c->tol_default : pcg_tol;
+    const int slot = c->head++;
+    c->slot_dt[slot] = prm->dt;
+    DevReport* rep = c->rep + slot;
+    (k_report_init<<<1, 1, 0, st>>>(rep), ++c->launches);
+    fill_pcg_args<T>(args[s], c, &fs[s], rep, prm->dt, tol);
+    args[s].probe_mode = 0;   // timing probes assume one slab
+    cw_slab_buffers lo{}, hi{}, root{};
+    if (s > 0) cw_slab_buffers_get(cs[s - 1], &lo);
+    if (s + 1 < n) cw_slab_buffers_get(cs[s + 1], &hi);
+    cw_slab_buffers_get(c0, &root);
+    const long long pplane = (long long)c->nxp * c->d.ny;
+    args[s].nslab = n;
+    args[s].slab = s;
+    args[s].lo = peer_of<T>(lo, lo.o1, pplane);
+    args[s].hi = peer_of<T>(hi, hi.o0 - 1, pplane);
+    args[s].xbar = c0->xbar;
+    args[s].xval = c0->xval;
+    CW_CUDA(cudaMemsetAsync(c->bar, 0, 64 * sizeof(unsigned), st));
+  }
+  CW_CUDA(cudaMemsetAsync(c0->xbar, 0, 64 * sizeof(unsigned), st));
+  CW_CUDA(cudaMemcpyAsync(c0->slab_args, args.data(), n * sizeof(PcgArgs<T>), cudaMemcpyHostToDevice, st));
+  const PcgArgs<T>* dargs = (const PcgArgs<T>*)c0->slab_args;
+  int ibps = bps;
+  void* kargs[] = {(void*)&dargs, (void*)&ibps};
+  CW_CUDA(cudaLaunchCooperativeKernel((const void*)k_pcg_slabs<T>, dim3(n * bps), dim3(PCG_THREADS), kargs,
+                                      c0->pcg_smem, st));
+  ++c0->launches;
+  CW_CUDA(cudaStreamSynchronize(st));   // the host argument array goes out of scope
+  return CW_OK;
+}
+
+extern "C" int cw_slab_group_pcg(cw_ctx** cs, const cw_fields* fs, int n, const cw_params* prm, double pcg_tol,
+                                 void* stream) {
+  if (!cs || !fs || !prm || n < 1) return fail(CW_ERR_INVALID, "null argument");
+  if (n > CW_MAX_SLABS) return fail(CW_ERR_INVALID, "too many slabs");
+  for (int s = 0; s < n; ++s) {
+    cw_ctx* c = cs[s];
+    if (!c) return fail(CW_ERR_INVALID, "null context");
+    if (!c->have_op) return fail(CW_ERR_INVALID, "cw_set_operator has not been called");
+    if (c->device != cs[0]->device || c->prec != cs[0]->prec || c->d.nx != cs[0]->d.nx ||
+        c->d.ny != cs[0]->d.ny || c->d.nzg != cs[0]->d.nzg)
+      return fail(CW_ERR_INVALID, "slabs must share device, precision and global grid");
+    const int lo = c->d.kg0 + c->d.o0, hi = c->d.kg0 + c->d.o1;
+    if ((s == 0 && lo != 0) || (s + 1 == n && hi != c->d.nzg) ||
+        (s > 0 && cs[s - 1]->d.kg0 + cs[s - 1]->d.o1 != lo))
+      return fail(CW_ERR_INVALID, "slabs must tile the global grid in z order");
+    if (c->head + 1 > RING) return fail(CW_ERR_INVALID, "report ring full: call cw_read_reports");
+  }
+  CW_CUDA(cudaSetDevice(cs[0]->device));
+  return cs[0]->prec == 4 ? group_pcg<float>(cs, fs, n, prm, pcg_tol, S(stream))
+                          : group_pcg<double>(cs, fs, n, prm, pcg_tol, S(stream));
+}
+
+extern "C" int cw_ipc_get(void* p, unsigned char handle[64]) {
+  if (!p || !handle) return fail(CW_ERR_INVALID, "null argument");
+  cudaIpcMemHandle_t h;
+  CW_CUDA(cudaIpcGetMemHandle(&h, p));
+  std::memcpy(handle, &h, 64);
+  return CW_OK;
+}
+
+extern "C" int cw_ipc_open(const unsigned char handle[64], int device, void** p) {
+  if (!handle || !p) return fail(CW_ERR_INVALID, "null argument");
+  CW_CUDA(cudaSetDevice(device));
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, 64);
+  CW_CUDA(cudaIpcOpenMemHandle(p, h, cudaIpcMemLazyEnablePeerAccess));
+  return CW_OK;
+}
+
+extern "C" int cw_ipc_close(void* p) {
+  if (!p) return fail(CW_ERR_INVALID, "null argument");
+  CW_CUDA(cudaIpcCloseMemHandle(p));
   return CW_OK;
 }
 

@@ -19,6 +19,10 @@ struct Dims {
   float dx, dy, dz;        // spacings in the arithmetic type used by kernels
   double ddx, ddy, ddz;    // float64 spacings for host-side derived constants
   int is2d;
+  // z-slab window: the local grid holds global planes [kg0, kg0 + nz) of a
+  // grid with nzg planes and owns local planes [o0, o1) (reductions and
+  // reports cover the owned planes only).  A whole grid: 0, nz, 0, nz.
+  int o0, o1, kg0, nzg;
   __host__ __device__ inline long long ncell() const { return (long long)nx * ny * nz; }
   __host__ __device__ inline long long cidx(int i, int j, int k) const {
     return ((long long)k * ny + j) * nx + i;

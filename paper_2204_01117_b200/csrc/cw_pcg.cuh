@@ -67,6 +67,16 @@ struct Halo {
   __device__ __forceinline__ static int at(int hy, int hx) { return hy * BW + hx + OFF; }
 };
 
+// z-slab neighbour: the pitched PCG vectors of the slab below or above, and
+// the element offset of the plane of theirs that mirrors our boundary plane
+// (their halo plane).  Null pointers: no neighbour on that side.
+template <typename T>
+struct PcgPeer {
+  double* r0; double* r1;
+  T* p0; T* p1; T* z; T* Ap;
+  long long plane_off;
+};
+
 template <typename T>
 struct PcgArgs {
   CUtensorMap tm_z, tm_p0, tm_p1, tm_x, tm_ap, tm_r0, tm_r1, tm_code, tm_code_own;
@@ -87,6 +97,15 @@ struct PcgArgs {
   int max_iter;
   int precond;               // 0 identity, 1 jacobi (diag(1/d)), 2 AI1 (K^T K)
   int ntx, nty, zc, U;
+  int PS;                    // partial-slot stride, >= max(U, blocks serving the slab)
+  int o0, o1;                // owned planes [o0, o1) of the local grid (a z-slab window)
+  // z-slab decomposition (nslab > 1): boundary planes are pushed into the
+  // neighbours' halo planes as they are written; the slabs meet at the root
+  // slab's barrier, where each slab's folded partials are published
+  int nslab, slab;
+  PcgPeer<T> lo, hi;
+  unsigned int* xbar;        // root slab: [0] arrivals, [32] generation (system scope)
+  double* xval;              // root slab: [2 sets][3 values][nslab]
   long long timeout_ns;
   int probe_mode, probe_iters;   // developer timing probe (CW_PCG_PROBE), 0 = off
 };
@@ -136,7 +155,8 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 
 // Grid barrier for a cooperative launch (all blocks co-resident).  Times out
 // (status 3) instead of hanging if the co-residency assumption is ever broken.
-__device__ __forceinline__ void grid_barrier(unsigned* bar, int* gate, DevReport* rep, long long timeout_ns) {
+__device__ __forceinline__ void grid_barrier(unsigned* bar, int* gate, DevReport* rep, long long timeout_ns,
+                                             unsigned nblocks) {
   __syncthreads();
   if (threadIdx.x == 0) {
     unsigned* count = bar;
@@ -144,7 +164,7 @@ __device__ __forceinline__ void grid_barrier(unsigned* bar, int* gate, DevReport
     const unsigned g = ld_acquire(gen);
     __threadfence();
     const unsigned prev = atomicAdd(count, 1u);
-    if (prev == gridDim.x - 1) {
+    if (prev == nblocks - 1) {
       atomicExch(count, 0u);
       __threadfence();
       atomicAdd(gen, 1u);
@@ -230,6 +250,8 @@ struct PcgShared {
   };
   double red[32];
   double bc[4];
+  double vals[4];           // slab_reduce results
+  unsigned last, gen0;      // slab_reduce: this block arrived last; generation seen
   alignas(8) uint64_t full[8];
 };
 
@@ -242,6 +264,12 @@ struct Unit {
   int i0, j0, k0, k1;
 };
 
+// This block's place among the blocks serving its slab (the whole grid when
+// there is one slab per launch).
+struct Blk {
+  int id, n;
+};
+
 template <typename T>
 __device__ __forceinline__ Unit unit_of(const PcgArgs<T>& A, int u) {
   const int per = A.ntx * A.nty;
@@ -249,22 +277,23 @@ __device__ __forceinline__ Unit unit_of(const PcgArgs<T>& A, int u) {
   Unit t;
   t.i0 = (rem % A.ntx) * PCG_TX;
   t.j0 = (rem / A.ntx) * PCG_TY;
-  t.k0 = tz * A.zc;
-  t.k1 = min(t.k0 + A.zc, A.d.nz);
+  t.k0 = A.o0 + tz * A.zc;
+  t.k1 = min(t.k0 + A.zc, A.o1);
   return t;
 }
 
 // Jobs of one ring phase for this block: its units in order (unit
-// blockIdx.x + m*gridDim.x), each contributing planes k0-1 .. k1.
+// blk.id + m*blk.n), each contributing planes k0-1 .. k1.
 struct JobCursor {
-  int unit;
+  int unit, nb;
   Unit t;
   int kk;
 };
 
 template <typename T>
-__device__ __forceinline__ bool cursor_begin(const PcgArgs<T>& A, JobCursor& c) {
-  c.unit = blockIdx.x;
+__device__ __forceinline__ bool cursor_begin(const PcgArgs<T>& A, const Blk& blk, JobCursor& c) {
+  c.unit = blk.id;
+  c.nb = blk.n;
   if (c.unit >= A.U) return false;
   c.t = unit_of<T>(A, c.unit);
   c.kk = c.t.k0 - 1;
@@ -273,7 +302,7 @@ __device__ __forceinline__ bool cursor_begin(const PcgArgs<T>& A, JobCursor& c) 
 template <typename T>
 __device__ __forceinline__ bool cursor_next(const PcgArgs<T>& A, JobCursor& c) {
   if (c.kk < c.t.k1) { ++c.kk; return true; }
-  c.unit += gridDim.x;
+  c.unit += c.nb;
   if (c.unit >= A.U) return false;
   c.t = unit_of<T>(A, c.unit);
   c.kk = c.t.k0 - 1;
@@ -312,7 +341,7 @@ __device__ __forceinline__ void issue_B(const PcgArgs<T>& A, uint8_t* ring, uint
 
 // ---- phase 0: b = -div/dt, r0 = b - A x0 with x0 = p on the unknowns ------
 // (once per projection; plain loads)
-template <typename T>
+template <typename T, bool SLABS>
 __device__ void phase0(const PcgArgs<T>& A, double* part, int unit, PcgShared<T>& S) {
   const Dims& d = A.d;
   const Unit t = unit_of<T>(A, unit);
@@ -363,6 +392,8 @@ __device__ void phase0(const PcgArgs<T>& A, double* part, int unit, PcgShared<T>
                            (double)A.wz * ((double)pm[q] + (double)pn));
         A.r0[pc_] = b - ax;
         A.x[pc_] = pc;
+        if (SLABS && k == A.o0 && A.lo.r0) A.lo.r0[A.lo.plane_off + (pc_ - k * pplane)] = b - ax;       // z-slab halo push
+        if (SLABS && k == A.o1 - 1 && A.hi.r0) A.hi.r0[A.hi.plane_off + (pc_ - k * pplane)] = b - ax;
         b2 += b * b;
         const double ab = fabs(b), ad = fabs(div);
         bmax = (ab > bmax || ab != ab) ? ab : bmax;
@@ -382,16 +413,16 @@ __device__ void phase0(const PcgArgs<T>& A, double* part, int unit, PcgShared<T>
   const double m2 = block_max(dmax, S.red);
   if (threadIdx.x == 0) {
     part[unit] = s0;
-    part[A.U + unit] = m1;
-    part[2 * A.U + unit] = m2;
+    part[A.PS + unit] = m1;
+    part[2 * A.PS + unit] = m2;
   }
   __syncthreads();
 }
 
 // ---- phase A: p' = z + beta p, x += alpha_prev p, Ap = A p' ---------------
-template <typename T>
-__device__ void phaseA(const PcgArgs<T>& A, double* part, PcgShared<T>& S, uint8_t* ring, unsigned& ticket,
-                       bool first, T beta, bool upd_x, T alpha_prev, int pin_sel) {
+template <typename T, bool SLABS>
+__device__ void phaseA(const PcgArgs<T>& A, const Blk& blk, double* part, PcgShared<T>& S, uint8_t* ring,
+                       unsigned& ticket, bool first, T beta, bool upd_x, T alpha_prev, int pin_sel) {
   using L = StageLayout<T>;
   static_assert(L::DEPTH >= 3, "phase A holds two stages");
   const Dims& d = A.d;
@@ -401,7 +432,7 @@ __device__ void phaseA(const PcgArgs<T>& A, double* part, PcgShared<T>& S, uint8
   const long long pplane = (long long)A.nxp * d.ny;
   JobCursor prod, cons;
   double acc = 0.0;
-  if (cursor_begin<T>(A, cons)) {
+  if (cursor_begin<T>(A, blk, cons)) {
     prod = cons;
     const unsigned t0 = ticket;
     unsigned issued = 0;
@@ -466,6 +497,17 @@ __device__ void phaseA(const PcgArgs<T>& A, double* part, PcgShared<T>& S, uint8
           pout[pc_] = pcur[q];
           A.Ap[pc_] = (T)ap;
           if (upd_x) A.x[pc_] = xn[q];
+          if (SLABS && A.nslab > 1) {   // boundary planes go to the neighbours' halo planes
+            const long long e = (long long)jj * A.nxp + i;
+            if (kk - 1 == A.o0 && A.lo.Ap) {
+              (pin_sel == 0 ? A.lo.p1 : A.lo.p0)[A.lo.plane_off + e] = pcur[q];
+              A.lo.Ap[A.lo.plane_off + e] = (T)ap;
+            }
+            if (kk - 1 == A.o1 - 1 && A.hi.Ap) {
+              (pin_sel == 0 ? A.hi.p1 : A.hi.p0)[A.hi.plane_off + e] = pcur[q];
+              A.hi.Ap[A.hi.plane_off + e] = (T)ap;
+            }
+          }
           acc += (double)pcur[q] * ap;
           pend[q] = false;
         }
@@ -497,16 +539,16 @@ __device__ void phaseA(const PcgArgs<T>& A, double* part, PcgShared<T>& S, uint8
     ticket = t0 + j;
   }
   const double sum = block_sum(acc, S.red);
-  if (threadIdx.x == 0) part[blockIdx.x] = sum;
+  if (threadIdx.x == 0) part[blk.id] = sum;
 }
 
 // ---- phase B: r' = r - alpha Ap, z = W r' ----------------------------------
 // One pass per landed plane kk computes q = r'/d on the y-tile (recomputing
 // the two in-plane lower neighbours from the stage instead of staging q) and
 // y(kk); after one barrier the own cells finish z on plane kk-1.
-template <typename T>
-__device__ void phaseB(const PcgArgs<T>& A, double* part, PcgShared<T>& S, uint8_t* ring, unsigned& ticket,
-                       bool use_ap, double alpha, int rin_sel, bool write_r) {
+template <typename T, bool SLABS>
+__device__ void phaseB(const PcgArgs<T>& A, const Blk& blk, double* part, PcgShared<T>& S, uint8_t* ring,
+                       unsigned& ticket, bool use_ap, double alpha, int rin_sel, bool write_r) {
   using L = StageLayout<T>;
   const Dims& d = A.d;
   const CUtensorMap* tr = rin_sel == 0 ? &A.tm_r0 : &A.tm_r1;
@@ -518,7 +560,7 @@ __device__ void phaseB(const PcgArgs<T>& A, double* part, PcgShared<T>& S, uint8
   PcgWork<T>& W = S.wk;
   JobCursor prod, cons;
   double acc = 0.0, rmax = 0.0;
-  if (cursor_begin<T>(A, cons)) {
+  if (cursor_begin<T>(A, blk, cons)) {
     prod = cons;
     const unsigned t0 = ticket;
     unsigned issued = 0;
@@ -625,6 +667,17 @@ __device__ void phaseB(const PcgArgs<T>& A, double* part, PcgShared<T>& S, uint8
               zv = (T)rprev[q];
             A.z[pc_] = zv;
             if (write_r) rout[pc_] = rprev[q];
+            if (SLABS && A.nslab > 1) {   // boundary planes go to the neighbours' halo planes
+              const long long e = (long long)jj * A.nxp + i;
+              if (k == A.o0 && A.lo.z) {
+                A.lo.z[A.lo.plane_off + e] = zv;
+                if (write_r) (rin_sel == 0 ? A.lo.r1 : A.lo.r0)[A.lo.plane_off + e] = rprev[q];
+              }
+              if (k == A.o1 - 1 && A.hi.z) {
+                A.hi.z[A.hi.plane_off + e] = zv;
+                if (write_r) (rin_sel == 0 ? A.hi.r1 : A.hi.r0)[A.hi.plane_off + e] = rprev[q];
+              }
+            }
             acc += rprev[q] * (double)zv;
             const double ar = fabs(rprev[q]);
             rmax = (ar > rmax || ar != ar) ? ar : rmax;
@@ -642,8 +695,8 @@ __device__ void phaseB(const PcgArgs<T>& A, double* part, PcgShared<T>& S, uint8
   __syncthreads();
   const double mx = block_max(rmax, S.red);
   if (threadIdx.x == 0) {
-    part[blockIdx.x] = sm;
-    part[A.U + blockIdx.x] = mx;
+    part[blk.id] = sm;
+    part[A.PS + blk.id] = mx;
   }
   __syncthreads();
 }
@@ -669,12 +722,112 @@ __device__ void finish_x(const PcgArgs<T>& A, int unit, T alpha, const T* __rest
   }
 }
 
+// ---------------------------------------------------------------------------
+// Phase end for z-slab solves (nslab > 1).  The last block of this slab to
+// arrive folds the slab's partials (fixed order), publishes them in the root
+// slab's value table and meets the other slabs at the root's counter (system
+// scope: slabs may live on different GPUs, reached over NVLink); then it
+// releases its own slab.  Every block then combines the slab values in slab
+// order, so all blocks of all slabs hold the same bits.
+__device__ __forceinline__ unsigned ld_acquire_sys(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
 template <typename T>
-__global__ void __launch_bounds__(PCG_THREADS, CW_PCG_MINB) k_pcg(const __grid_constant__ PcgArgs<T> A) {
+__device__ void slab_reduce(const PcgArgs<T>& A, const Blk& blk, const double* part, int n, int stride, int nval,
+                            unsigned maxmask, int set, double* out, PcgShared<T>& S) {
+  __syncthreads();
+  unsigned* count = A.bar;
+  unsigned* gen = A.bar + 32;
+  if (threadIdx.x == 0) {
+    S.gen0 = ld_acquire(gen);
+    __threadfence_system();   // this block's writes (and its pushes into peer slabs) before the arrival
+    S.last = atomicAdd(count, 1u) == (unsigned)blk.n - 1;
+  }
+  __syncthreads();
+  if (S.last) {
+    for (int q = 0; q < nval; ++q) {
+      const double v = fold_partials(part + (size_t)q * stride, n, (maxmask >> q) & 1u, S.bc);
+      if (threadIdx.x == 0) A.xval[((size_t)set * 3 + q) * A.nslab + A.slab] = v;
+    }
+    if (threadIdx.x == 0) {
+      unsigned* xc = A.xbar;
+      unsigned* xg = A.xbar + 32;
+      const unsigned g = ld_acquire_sys(xg);
+      __threadfence_system();
+      if (atomicAdd_system(xc, 1u) == (unsigned)A.nslab - 1) {
+        atomicExch_system(xc, 0u);
+        __threadfence_system();
+        atomicAdd_system(xg, 1u);
+      } else {
+        const unsigned long long t0 = globaltimer();
+        unsigned spins = 0;
+        while (ld_acquire_sys(xg) == g) {
+          __nanosleep(64);
+          if ((++spins & 1023u) == 0 && (long long)(globaltimer() - t0) > A.timeout_ns) {
+            A.rep->status = 3;
+            *A.gate = 3;
+            break;
+          }
+        }
+      }
+      atomicExch(count, 0u);
+      __threadfence();
+      atomicAdd(gen, 1u);
+    }
+  } else if (threadIdx.x == 0) {
+    const unsigned long long t0 = globaltimer();
+    unsigned spins = 0;
+    while (ld_acquire(gen) == S.gen0) {
+      __nanosleep(32);
+      if ((++spins & 1023u) == 0 && (long long)(globaltimer() - t0) > A.timeout_ns) {
+        A.rep->status = 3;
+        *A.gate = 3;
+        break;
+      }
+    }
+  }
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    fence_proxy_async();   // the next phase's TMA reads see the pushed halo planes
+  }
+  __syncthreads();
+  if (threadIdx.x < nval) {
+    const int q = threadIdx.x;
+    const volatile double* xv = A.xval + ((size_t)set * 3 + q) * A.nslab;
+    double v = xv[0];
+    for (int s2 = 1; s2 < A.nslab; ++s2) {
+      const double w = xv[s2];
+      if ((maxmask >> q) & 1u) v = (w > v || w != w) ? w : v;
+      else v += w;
+    }
+    S.vals[q] = v;
+  }
+  __syncthreads();
+  for (int q = 0; q < nval; ++q) out[q] = S.vals[q];
+  __syncthreads();
+}
+
+// Phase end: barrier, then the reduced values out[0..nval) (thread-local; bit q
+// of maxmask: max instead of sum) over partials part[q*stride + 0..n).
+template <typename T, bool SLABS>
+__device__ __forceinline__ void phase_end(const PcgArgs<T>& A, const Blk& blk, const double* part, int n, int stride,
+                                          int nval, unsigned maxmask, int set, double* out, PcgShared<T>& S) {
+  if (SLABS && A.nslab > 1) {
+    slab_reduce<T>(A, blk, part, n, stride, nval, maxmask, set, out, S);
+    return;
+  }
+  grid_barrier(A.bar, A.gate, A.rep, A.timeout_ns, (unsigned)blk.n);
+  for (int q = 0; q < nval; ++q) out[q] = fold_partials(part + (size_t)q * stride, n, (maxmask >> q) & 1u, S.bc);
+}
+
+template <typename T, bool SLABS>
+__device__ __forceinline__ void pcg_body(const PcgArgs<T>& A, const Blk& blk, uint8_t* smem_raw) {
   // dynamic smem is the only shared allocation of this kernel, so it starts
   // at the (1 KB aligned) base of the block's window; keep every access on
   // this array so the compiler emits LDS/STS rather than generic loads
-  extern __shared__ __align__(128) uint8_t smem_raw[];
   uint8_t* ring = smem_raw;
   PcgShared<T>& S =
       *reinterpret_cast<PcgShared<T>*>(smem_raw + (size_t)StageLayout<T>::STAGE * StageLayout<T>::DEPTH);
@@ -692,40 +845,40 @@ __global__ void __launch_bounds__(PCG_THREADS, CW_PCG_MINB) k_pcg(const __grid_c
   __syncthreads();
   DevReport* rep = A.rep;
   const int U = A.U;
-  const int B = gridDim.x;
+  const int B = blk.n;
+  const bool lead = blk.id == 0 && threadIdx.x == 0;
   unsigned ticket = 0;
   // two partial sets, alternated by phase, so one barrier per phase suffices;
   // phase 0 writes per unit, the ring phases per block (fixed unit->block map)
-  double* P[2] = {A.part, A.part + 3 * U};
+  double* P[2] = {A.part, A.part + 3 * A.PS};
+  double red[3];
 
-  if (A.probe_mode == 8 && blockIdx.x == 0 && threadIdx.x == 0) rep->criterion = 0.0;
-  for (int u = blockIdx.x; u < U; u += B) phase0<T>(A, P[0], u, S);
-  grid_barrier(A.bar, A.gate, rep, A.timeout_ns);
-  const double b2 = fold_partials(P[0], U, 0, S.bc);
-  const double bmax = fold_partials(P[0] + U, U, 1, S.bc);
-  const double divmax = fold_partials(P[0] + 2 * U, U, 1, S.bc);
-  if (blockIdx.x == 0 && threadIdx.x == 0) report_max<T>(rep, SLOT_DIV_BEFORE, (T)divmax);
+  if (A.probe_mode == 8 && lead) rep->criterion = 0.0;
+  for (int u = blk.id; u < U; u += B) phase0<T, SLABS>(A, P[0], u, S);
+  phase_end<T, SLABS>(A, blk, P[0], U, A.PS, 3, 6u, 0, red, S);
+  const double b2 = red[0], bmax = red[1], divmax = red[2];
+  if (lead) report_max<T>(rep, SLOT_DIV_BEFORE, (T)divmax);
   if (*(volatile int*)A.gate == 3) {
-    if (blockIdx.x == 0 && threadIdx.x == 0) rep->status = 3;
+    if (lead) rep->status = 3;
     return;
   }
   if (!isfinite(bmax)) {                     // pcg_solve raises on a non-finite rhs
-    if (blockIdx.x == 0 && threadIdx.x == 0) { rep->status = 4; *A.gate = 4; }
+    if (lead) { rep->status = 4; *A.gate = 4; }
     return;
   }
   if (b2 == 0.0) {                           // linalg.py:329-330: x = 0, 0 iterations
-    for (int u = blockIdx.x; u < U; u += B) finish_x<T>(A, u, (T)0, A.p0, true);
-    if (blockIdx.x == 0 && threadIdx.x == 0) { rep->iterations = 0; rep->converged = 1; rep->criterion = 0.0; }
+    for (int u = blk.id; u < U; u += B) finish_x<T>(A, u, (T)0, A.p0, true);
+    if (lead) { rep->iterations = 0; rep->converged = 1; rep->criterion = 0.0; }
     return;
   }
   const double res_target = A.res_factor * bmax;   // solver.py:266 (b.any() holds: b2 > 0)
   const double tol = A.tol;
 
   // z = W r0, rz, max|r0|  (pcg_solve:342-345)
-  phaseB<T>(A, P[1], S, ring, ticket, false, 0.0, 0, false);
-  grid_barrier(A.bar, A.gate, rep, A.timeout_ns);
-  double rz = fold_partials(P[1], B, 0, S.bc);
-  double rmax = fold_partials(P[1] + U, B, 1, S.bc);
+  phaseB<T, SLABS>(A, blk, P[1], S, ring, ticket, false, 0.0, 0, false);
+  phase_end<T, SLABS>(A, blk, P[1], B, A.PS, 2, 2u, 1, red, S);
+  double rz = red[0];
+  double rmax = red[1];
   double crit = rz / b2;
   int it = 0, converged = 0, status = 0;
   bool finished = false;
@@ -737,19 +890,19 @@ __global__ void __launch_bounds__(PCG_THREADS, CW_PCG_MINB) k_pcg(const __grid_c
       // 6, 7: phase A and phase B alternate as in the solve (7: stream only)
       const bool pa = A.probe_mode == 1 || A.probe_mode == 4 || (A.probe_mode >= 6 && !(q & 1));
       const bool pb = A.probe_mode == 2 || (A.probe_mode >= 6 && (q & 1));
-      if (pa) phaseA<T>(A, P[0], S, ring, ticket, false, (T)0.5, true, (T)0.0, (q >> 1) & 1);
-      if (pb) phaseB<T>(A, P[1], S, ring, ticket, true, 0.0, (q >> 1) & 1, true);
+      if (pa) phaseA<T, SLABS>(A, blk, P[0], S, ring, ticket, false, (T)0.5, true, (T)0.0, (q >> 1) & 1);
+      if (pb) phaseB<T, SLABS>(A, blk, P[1], S, ring, ticket, true, 0.0, (q >> 1) & 1, true);
       const unsigned long long ta = globaltimer();
-      grid_barrier(A.bar, A.gate, rep, A.timeout_ns);
+      grid_barrier(A.bar, A.gate, rep, A.timeout_ns, (unsigned)B);
       wait_ns += globaltimer() - ta;
       if (A.probe_mode == 5) {   // barrier plus phase B's two folds
         rz += fold_partials(P[1], B, 0, S.bc);
-        rmax = fold_partials(P[1] + U, B, 1, S.bc);
+        rmax = fold_partials(P[1] + A.PS, B, 1, S.bc);
       }
     }
     // 8: report the mean grid-barrier wait per block and phase (us) as the criterion
     if (A.probe_mode == 8 && threadIdx.x == 0) atomicAdd(&rep->criterion, (double)wait_ns * 1e-3 / (B * A.probe_iters));
-    if (blockIdx.x == 0 && threadIdx.x == 0) { rep->iterations = A.probe_iters; rep->converged = 1; }
+    if (lead) { rep->iterations = A.probe_iters; rep->converged = 1; }
     return;
   }
   if (0.0 <= crit && crit < tol && rmax <= res_target) { converged = 1; finished = true; }
@@ -761,17 +914,17 @@ __global__ void __launch_bounds__(PCG_THREADS, CW_PCG_MINB) k_pcg(const __grid_c
     if (it >= A.max_iter) break;
     ++it;
     const bool first = it == 1;
-    phaseA<T>(A, P[0], S, ring, ticket, first, (T)beta, !first, (T)alpha, psel);
-    grid_barrier(A.bar, A.gate, rep, A.timeout_ns);
-    const double pAp = fold_partials(P[0], B, 0, S.bc);
+    phaseA<T, SLABS>(A, blk, P[0], S, ring, ticket, first, (T)beta, !first, (T)alpha, psel);
+    phase_end<T, SLABS>(A, blk, P[0], B, A.PS, 1, 0u, 0, red, S);
+    const double pAp = red[0];
     psel ^= 1;                                // the new p went to the other buffer
     if (*(volatile int*)A.gate == 3) { status = 3; alpha = 0.0; break; }
     if (pAp <= 0.0) { it -= 1; alpha = 0.0; break; }   // linalg.py:354-355
     alpha = rz / pAp;
-    phaseB<T>(A, P[1], S, ring, ticket, true, alpha, rsel, true);
-    grid_barrier(A.bar, A.gate, rep, A.timeout_ns);
-    const double rz_new = fold_partials(P[1], B, 0, S.bc);
-    rmax = fold_partials(P[1] + U, B, 1, S.bc);
+    phaseB<T, SLABS>(A, blk, P[1], S, ring, ticket, true, alpha, rsel, true);
+    phase_end<T, SLABS>(A, blk, P[1], B, A.PS, 2, 2u, 1, red, S);
+    const double rz_new = red[0];
+    rmax = red[1];
     rsel ^= 1;
     crit = rz_new / b2;
     if (*(volatile int*)A.gate == 3) { status = 3; break; }
@@ -782,14 +935,31 @@ __global__ void __launch_bounds__(PCG_THREADS, CW_PCG_MINB) k_pcg(const __grid_c
   }
   // state p = x, plus the alpha p of the last completed iteration if pending
   const T* plast = psel == 0 ? A.p0 : A.p1;
-  for (int u = blockIdx.x; u < U; u += B) finish_x<T>(A, u, (T)alpha, plast, false);
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
+  for (int u = blk.id; u < U; u += B) finish_x<T>(A, u, (T)alpha, plast, false);
+  if (lead) {
     rep->iterations = it;
     rep->converged = converged;
     rep->criterion = crit;
     if (status) rep->status = status;
     else if (!converged) { rep->status = 1; *A.gate = 1; }
   }
+}
+
+// One slab per launch (the whole grid, or this GPU's slab of a multi-GPU solve).
+// SLABS = false: a whole grid; the z-slab code paths are compiled out.
+template <typename T, bool SLABS>
+__global__ void __launch_bounds__(PCG_THREADS, CW_PCG_MINB) k_pcg(const __grid_constant__ PcgArgs<T> A) {
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  pcg_body<T, SLABS>(A, Blk{(int)blockIdx.x, (int)gridDim.x}, smem_raw);
+}
+
+// All slabs of a z-slab solve on one device in one cooperative launch: blocks
+// [s*bps, (s+1)*bps) serve slab s, whose arguments sit in global memory.
+template <typename T>
+__global__ void __launch_bounds__(PCG_THREADS, CW_PCG_MINB) k_pcg_slabs(const PcgArgs<T>* __restrict__ all, int bps) {
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  const int s = blockIdx.x / bps;
+  pcg_body<T, true>(all[s], Blk{(int)(blockIdx.x - s * bps), bps}, smem_raw);
 }
 
 }  // namespace cw

@@ -47,6 +47,12 @@ constexpr int ST_BX = 32, ST_BY = 8;
   const int j = (int)(blockIdx.y * ST_BY + threadIdx.y);         \
   const int k = (int)blockIdx.z;                                 \
   const bool inb = i < (ex) && j < (ey) && k < (ez)
+// the same over the owned planes of a z-slab window only (grid z = o1 - o0 [+1])
+#define CW_IJK_OWN(ex, ey, kend, inb)                            \
+  const int i = (int)(blockIdx.x * ST_BX + threadIdx.x);         \
+  const int j = (int)(blockIdx.y * ST_BY + threadIdx.y);         \
+  const int k = d.o0 + (int)blockIdx.z;                          \
+  const bool inb = i < (ex) && j < (ey) && k < (kend)
 
 __device__ __forceinline__ int clampi(int a, int lo, int hi) { return a < lo ? lo : (a > hi ? hi : a); }
 
@@ -421,7 +427,7 @@ __global__ void k_div_max(Dims d, const T* __restrict__ u, const T* __restrict__
   if (*gate) return;
   __shared__ T scratch[32];
   T m = (T)0;
-  CW_IJK(d.nx, d.ny, d.nz, inb);
+  CW_IJK_OWN(d.nx, d.ny, d.o1, inb);
   const long long c = d.cidx(i, j, k);
   if (inb && is_unknown(lab[c])) {
     const long long ui = ((long long)k * d.ny + j) * (d.nx + 1) + i;
@@ -435,21 +441,28 @@ __global__ void k_div_max(Dims d, const T* __restrict__ u, const T* __restrict__
   if (threadIdx.x == 0 && threadIdx.y == 0) report_max<T>(rep, slot, m);
 }
 
-// max |u|,|v|,|w| for the CFL number (solver.py:456-458)
+// max |u|,|v|,|w| for the CFL number (solver.py:456-458), over the owned
+// planes (w: faces o0..o1; a face shared with the slab above is counted by
+// both, which a max does not notice)
 template <typename T>
-__global__ void k_speed_max(long long nu, long long nv, long long nw, const T* __restrict__ u,
-                            const T* __restrict__ v, const T* __restrict__ w, DevReport* rep,
-                            const int* gate) {
+__global__ void k_speed_max(Dims d, const T* __restrict__ u, const T* __restrict__ v, const T* __restrict__ w,
+                            DevReport* rep, const int* gate) {
   if (*gate) return;
   __shared__ T scratch[32];
   T m = (T)0;
-  const long long n = nu + nv + nw;
-  CW_GRID_STRIDE(t, n) {
-    const T a = t < nu ? fabs(u[t]) : (t < nu + nv ? fabs(v[t - nu]) : fabs(w[t - nu - nv]));
-    m = (a > m || a != a) ? a : m;
+  CW_IJK_OWN(d.nx + 1, d.ny + 1, d.o1 + 1, inb);
+  if (inb) {
+    if (k < d.o1) {
+      if (j < d.ny) { const T a = fabs(u[((long long)k * d.ny + j) * (d.nx + 1) + i]); m = (a > m || a != a) ? a : m; }
+      if (i < d.nx) { const T a = fabs(v[((long long)k * (d.ny + 1) + j) * d.nx + i]); m = (a > m || a != a) ? a : m; }
+    }
+    if (i < d.nx && j < d.ny) {
+      const T a = fabs(w[((long long)k * d.ny + j) * d.nx + i]);
+      m = (a > m || a != a) ? a : m;
+    }
   }
-  m = block_max(m, scratch);
-  if (threadIdx.x == 0) report_max<T>(rep, SLOT_SPEED, m);
+  m = block_max_2d(m, scratch);
+  if (threadIdx.x == 0 && threadIdx.y == 0) report_max<T>(rep, SLOT_SPEED, m);
 }
 
 // ---------------------------------------------------------------------------
@@ -535,9 +548,11 @@ __global__ void k_turbulence(Dims d, const T* __restrict__ u, const T* __restric
     const T kn = (kc + dt * (pk + dk * pad_lap(d, kin, c, i, j, k))) / ((T)1 + dt * (T)sc.c_mu * wc);
     const T wn = (wc + dt * ((T)2 * (T)sc.alpha * s2 + dw * pad_lap(d, win, c, i, j, k)))
                  / ((T)1 + dt * (T)sc.beta * wc);
-    const long long ref = ((long long)i * d.ny + j) * d.nz + k;
-    if (!isfinite(kn)) atomicMin(&rep->bad_index[0], ref);
-    if (!isfinite(wn)) atomicMin(&rep->bad_index[1], ref);
+    if (k >= d.o0 && k < d.o1) {   // reference C order over the global grid
+      const long long ref = ((long long)i * d.ny + j) * d.nzg + (k + d.kg0);
+      if (!isfinite(kn)) atomicMin(&rep->bad_index[0], ref);
+      if (!isfinite(wn)) atomicMin(&rep->bad_index[1], ref);
+    }
     const T kf = kn > (T)1e-12 ? kn : (T)1e-12;
     const T wf = wn > (T)1e-8 ? wn : (T)1e-8;
     T omt = (T)sc.c_lim * sqrt(s2) / ((T)sc.c_mu / (T)2);

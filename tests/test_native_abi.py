@@ -42,7 +42,7 @@ def test_ctypes_table_matches_header():
 
 
 def test_abi_version(lib):
-    assert lib.cw_abi_version() == 1
+    assert lib.cw_abi_version() == 2
 
 
 def test_context_creation_fails_loudly_without_gpu(lib):
