@@ -326,3 +326,107 @@ class SlabDomain:
         for name in FIELDS:
             out[name] = torch.cat([p.owned_view(name) for p in self.parts], dim=0)
         return out
+
+
+# ---------------------------------------------------------------------------
+# one slab per device (one process per GPU)
+
+class DistSlabSolver:
+    """This rank's slab of a grid split over the ranks of a torch.distributed
+    group (one GPU each).  Halos move with NCCL point-to-point over NVLink;
+    the projection is one cooperative launch per GPU whose blocks store their
+    boundary planes straight into the neighbours' halo planes (CUDA IPC
+    mappings) and meet the other GPUs at rank 0's barrier."""
+
+    def __init__(self, state: FlowState, params: SolverParams, profile: InletProfile, group=None,
+                 omega: float = 1.65, precond: int = 2, halo: int = DEFAULT_HALO, pcg_tol=None):
+        import torch.distributed as dist
+        self.dist = dist
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.n = dist.get_world_size(group)
+        grid = state.grid
+        self.grid = grid
+        self.params = params
+        self.profile = profile
+        ranges = plan_slabs(grid.nz, self.n)
+        if min(b - a for a, b in ranges) < halo:
+            raise ValueError(f"slabs of {min(b - a for a, b in ranges)} planes cannot feed a {halo}-plane halo")
+        self.windows = [SlabWindow.of(a, b, halo, grid.nz) for a, b in ranges]
+        self.part = SlabPart(grid, self.windows[self.rank], halo, state.dtype, state.device)
+        self.part.load(state, params)
+        s, js, m, outl = self.part.set_operator(omega, precond)
+        t = torch.tensor([s, js, float(m), float(outl)], dtype=torch.float64, device=state.device)
+        dist.all_reduce(t, group=group)
+        if t[2].item() == 0:
+            raise ValueError("no flow cells to solve for")
+        if t[3].item() == 0:
+            from .errors import SingularSystemError
+            raise SingularSystemError("no outlet cells: pressure defined only up to a constant")
+        mean = (t[0] if precond == 2 else t[1]).item() / t[2].item()
+        self.tol = float(pcg_tol) if pcg_tol is not None else (1e-8 if precond == 0 else 1e-8 * max(mean, 1e-300))
+        self.exchange = DistExchange(self.windows, self.rank, group)
+        self._attach()
+        self.time = state.time
+        self.step_count = state.step_count
+
+    def _attach(self):
+        """Open the neighbours' (and rank 0's) PCG buffers through CUDA IPC."""
+        if self.n == 1:
+            return
+        lib = N.lib()
+        mine = self.part.buffers()
+        handles = {}
+        for name in N.cw_slab_buffers.BUFFERS:
+            h = (C.c_ubyte * 64)()
+            N.check(lib.cw_ipc_get(C.c_void_p(getattr(mine, name)), h))
+            handles[name] = bytes(h)
+        allh = [None] * self.n
+        self.dist.all_gather_object(allh, (handles, mine.o0, mine.o1), group=self.group)
+        dev = self.part.device.index or 0
+        self._opened = []
+
+        def open_peer(r):
+            if r == self.rank:
+                return mine
+            hs, o0, o1 = allh[r]
+            b = N.cw_slab_buffers()
+            for name in N.cw_slab_buffers.BUFFERS:
+                p = C.c_void_p()
+                N.check(lib.cw_ipc_open((C.c_ubyte * 64)(*hs[name]), dev, C.byref(p)))
+                self._opened.append(p)
+                setattr(b, name, p.value)
+            b.o0, b.o1 = o0, o1
+            return b
+
+        lower = open_peer(self.rank - 1) if self.rank > 0 else None
+        upper = open_peer(self.rank + 1) if self.rank + 1 < self.n else None
+        root = open_peer(0) if self.rank not in (0, 1) else (mine if self.rank == 0 else lower)
+        N.check(lib.cw_slab_attach(self.part.h, self.rank, self.n, C.byref(lower) if lower else None,
+                                   C.byref(upper) if upper else None, C.byref(root)))
+        self.dist.barrier(group=self.group)
+
+    def step(self) -> StepReport:
+        prm = self.params.native()
+        inl = self.profile.native()
+        p = self.part
+        self.exchange.exchange(p.fields)
+        p.run(N.CW_STAGE_PRE, prm, inl)
+        p.run(N.CW_STAGE_SOLVE, prm, inl, self.tol)
+        self.exchange.exchange(p.fields, names=("p",))
+        p.run(N.CW_STAGE_POST, prm, inl)
+        rc, r = p.reports(3)
+        if rc != N.CW_OK:
+            from .solver import _raise_for
+            bad = next((x for x in r if x.status != N.CW_OK), r[-1] if r else None)
+            _raise_for(rc, bad, self.grid)
+        t = torch.tensor([r[1].div_before, r[2].div_after, r[2].cfl], dtype=torch.float64, device=p.device)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX, group=self.group)
+        self.time += self.params.dt
+        self.step_count += 1
+        return StepReport(timings={}, pcg=PcgReport(int(r[1].iterations), bool(r[1].converged),
+                                                    float(r[1].criterion)),
+                          cfl=float(t[2]), div_before=float(t[0]), div_after=float(t[1]))
+
+    def step_many(self, n: int):
+        return [self.step() for _ in range(n)]

@@ -72,3 +72,30 @@ def test_halo_too_deep_is_rejected():
     st = comp.make_state()
     with pytest.raises(ValueError):
         SlabDomain(st, comp.scenario.solver, comp.scenario.inlet, 4, halo=4)
+
+
+def test_dist_slab_solver_single_rank():
+    """The one-slab-per-GPU driver with a one-rank NCCL group equals the
+    whole-grid step bit for bit (the multi-GPU attach path needs >1 GPU)."""
+    import os
+    import socket
+    import torch.distributed as dist
+    from paper_2204_01117_b200.slabs import DistSlabSolver
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        comp = _compiled(scenes.cuboid(24, 24, 12, 2.0, 0.3, steps=5))
+        sc = comp.scenario
+        ref = comp.make_state()
+        sol = DistSlabSolver(ref.copy(), sc.solver, sc.inlet, omega=sc.ai_omega, pcg_tol=sc.pcg_tol)
+        got = [r.pcg.iterations for r in sol.step_many(5)]
+        want = [r.pcg.iterations for r in comp.step_states(ref, 5)]
+        assert got == want
+        for n in FIELDS:
+            assert torch.equal(sol.part.owned_view(n), ref.fields[n]), n
+    finally:
+        dist.destroy_process_group()
