@@ -153,25 +153,24 @@ __device__ __forceinline__ unsigned long long globaltimer() {
   return t;
 }
 
-// Grid barrier for a cooperative launch (all blocks co-resident).  Times out
+// Grid barrier for a cooperative launch (all blocks co-resident).  The
+// arrival counter only grows during a launch (zeroed before it): barrier e
+// (0-based, counted per block in `epoch`) completes when it reaches
+// (e+1)*nblocks.  Arrival is one release reduction, waiting is acquire loads:
+// no counter reset and no generation word on the critical path.  Times out
 // (status 3) instead of hanging if the co-residency assumption is ever broken.
 __device__ __forceinline__ void grid_barrier(unsigned* bar, int* gate, DevReport* rep, long long timeout_ns,
-                                             unsigned nblocks) {
+                                             unsigned nblocks, unsigned& epoch) {
   __syncthreads();
+  ++epoch;
   if (threadIdx.x == 0) {
     unsigned* count = bar;
-    unsigned* gen = bar + 32;
-    const unsigned g = ld_acquire(gen);
-    __threadfence();
-    const unsigned prev = atomicAdd(count, 1u);
-    if (prev == nblocks - 1) {
-      atomicExch(count, 0u);
-      __threadfence();
-      atomicAdd(gen, 1u);
-    } else {
+    const unsigned target = epoch * nblocks;
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(count) : "memory");
+    if (ld_acquire(count) < target) {
       const unsigned long long t0 = globaltimer();
       unsigned spins = 0;
-      while (ld_acquire(gen) == g) {
+      while (ld_acquire(count) < target) {
         __nanosleep(32);
         if ((++spins & 1023u) == 0 && (long long)(globaltimer() - t0) > timeout_ns) {
           rep->status = 3;
@@ -180,7 +179,6 @@ __device__ __forceinline__ void grid_barrier(unsigned* bar, int* gate, DevReport
         }
       }
     }
-    __threadfence();
     fence_proxy_async();   // the next phase's TMA (async proxy) reads see this phase's writes
   }
   __syncthreads();
@@ -814,12 +812,13 @@ __device__ void slab_reduce(const PcgArgs<T>& A, const Blk& blk, const double* p
 // of maxmask: max instead of sum) over partials part[q*stride + 0..n).
 template <typename T, bool SLABS>
 __device__ __forceinline__ void phase_end(const PcgArgs<T>& A, const Blk& blk, const double* part, int n, int stride,
-                                          int nval, unsigned maxmask, int set, double* out, PcgShared<T>& S) {
+                                          int nval, unsigned maxmask, int set, double* out, PcgShared<T>& S,
+                                          unsigned& epoch) {
   if (SLABS && A.nslab > 1) {
     slab_reduce<T>(A, blk, part, n, stride, nval, maxmask, set, out, S);
     return;
   }
-  grid_barrier(A.bar, A.gate, A.rep, A.timeout_ns, (unsigned)blk.n);
+  grid_barrier(A.bar, A.gate, A.rep, A.timeout_ns, (unsigned)blk.n, epoch);
   for (int q = 0; q < nval; ++q) out[q] = fold_partials(part + (size_t)q * stride, n, (maxmask >> q) & 1u, S.bc);
 }
 
@@ -848,6 +847,7 @@ __device__ __forceinline__ void pcg_body(const PcgArgs<T>& A, const Blk& blk, ui
   const int B = blk.n;
   const bool lead = blk.id == 0 && threadIdx.x == 0;
   unsigned ticket = 0;
+  unsigned epoch = 0;    // grid barriers passed (every thread keeps the count)
   // two partial sets, alternated by phase, so one barrier per phase suffices;
   // phase 0 writes per unit, the ring phases per block (fixed unit->block map)
   double* P[2] = {A.part, A.part + 3 * A.PS};
@@ -855,7 +855,7 @@ __device__ __forceinline__ void pcg_body(const PcgArgs<T>& A, const Blk& blk, ui
 
   if (A.probe_mode == 8 && lead) rep->criterion = 0.0;
   for (int u = blk.id; u < U; u += B) phase0<T, SLABS>(A, P[0], u, S);
-  phase_end<T, SLABS>(A, blk, P[0], U, A.PS, 3, 6u, 0, red, S);
+  phase_end<T, SLABS>(A, blk, P[0], U, A.PS, 3, 6u, 0, red, S, epoch);
   const double b2 = red[0], bmax = red[1], divmax = red[2];
   if (lead) report_max<T>(rep, SLOT_DIV_BEFORE, (T)divmax);
   if (*(volatile int*)A.gate == 3) {
@@ -876,7 +876,7 @@ __device__ __forceinline__ void pcg_body(const PcgArgs<T>& A, const Blk& blk, ui
 
   // z = W r0, rz, max|r0|  (pcg_solve:342-345)
   phaseB<T, SLABS>(A, blk, P[1], S, ring, ticket, false, 0.0, 0, false);
-  phase_end<T, SLABS>(A, blk, P[1], B, A.PS, 2, 2u, 1, red, S);
+  phase_end<T, SLABS>(A, blk, P[1], B, A.PS, 2, 2u, 1, red, S, epoch);
   double rz = red[0];
   double rmax = red[1];
   double crit = rz / b2;
@@ -893,7 +893,7 @@ __device__ __forceinline__ void pcg_body(const PcgArgs<T>& A, const Blk& blk, ui
       if (pa) phaseA<T, SLABS>(A, blk, P[0], S, ring, ticket, false, (T)0.5, true, (T)0.0, (q >> 1) & 1);
       if (pb) phaseB<T, SLABS>(A, blk, P[1], S, ring, ticket, true, 0.0, (q >> 1) & 1, true);
       const unsigned long long ta = globaltimer();
-      grid_barrier(A.bar, A.gate, rep, A.timeout_ns, (unsigned)B);
+      grid_barrier(A.bar, A.gate, rep, A.timeout_ns, (unsigned)B, epoch);
       wait_ns += globaltimer() - ta;
       if (A.probe_mode == 5) {   // barrier plus phase B's two folds
         rz += fold_partials(P[1], B, 0, S.bc);
@@ -915,14 +915,14 @@ __device__ __forceinline__ void pcg_body(const PcgArgs<T>& A, const Blk& blk, ui
     ++it;
     const bool first = it == 1;
     phaseA<T, SLABS>(A, blk, P[0], S, ring, ticket, first, (T)beta, !first, (T)alpha, psel);
-    phase_end<T, SLABS>(A, blk, P[0], B, A.PS, 1, 0u, 0, red, S);
+    phase_end<T, SLABS>(A, blk, P[0], B, A.PS, 1, 0u, 0, red, S, epoch);
     const double pAp = red[0];
     psel ^= 1;                                // the new p went to the other buffer
     if (*(volatile int*)A.gate == 3) { status = 3; alpha = 0.0; break; }
     if (pAp <= 0.0) { it -= 1; alpha = 0.0; break; }   // linalg.py:354-355
     alpha = rz / pAp;
     phaseB<T, SLABS>(A, blk, P[1], S, ring, ticket, true, alpha, rsel, true);
-    phase_end<T, SLABS>(A, blk, P[1], B, A.PS, 2, 2u, 1, red, S);
+    phase_end<T, SLABS>(A, blk, P[1], B, A.PS, 2, 2u, 1, red, S, epoch);
     const double rz_new = red[0];
     rmax = red[1];
     rsel ^= 1;
