@@ -208,6 +208,47 @@ __device__ __forceinline__ double fold_partials(const double* part, int n, int m
   return r;
 }
 
+// Fold up to three partial arrays part[q*stride + 0..n) at once with the
+// whole block (one L2 round trip): per-thread strided sums, warp trees, then
+// the warp results in warp order.  A fixed order: every block gets the same
+// bits.  Bit q of maxmask: max (non-negative values, NaN wins) instead of sum.
+__device__ __forceinline__ void fold_multi(const double* part, int n, int stride, int nval, unsigned maxmask,
+                                           double* out, double* sh) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int q = 0; q < 3; ++q) {
+    if (q < nval) {
+      const bool mx = (maxmask >> q) & 1u;
+      double a = 0.0;
+      for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const double v = __ldcg(part + (size_t)q * stride + i);
+        a = mx ? ((v > a || v != v) ? v : a) : a + v;
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double b = __shfl_down_sync(0xffffffffu, a, o);
+        a = mx ? ((b > a || b != b) ? b : a) : a + b;
+      }
+      if (lane == 0) sh[q * 32 + wid] = a;
+    }
+  }
+  __syncthreads();
+  const int nw = (blockDim.x + 31) >> 5;
+#pragma unroll
+  for (int q = 0; q < 3; ++q) {
+    if (q < nval) {
+      const bool mx = (maxmask >> q) & 1u;
+      double a = sh[q * 32];
+      for (int w = 1; w < nw; ++w) {
+        const double b = sh[q * 32 + w];
+        a = mx ? ((b > a || b != b) ? b : a) : a + b;
+      }
+      out[q] = a;
+    }
+  }
+  __syncthreads();
+}
+
 // ---------------------------------------------------------------------------
 // shared memory layout
 
@@ -249,6 +290,7 @@ struct PcgShared {
   double red[32];
   double bc[4];
   double vals[4];           // slab_reduce results
+  double fold[3 * 32];      // fold_multi warp results
   unsigned last, gen0;      // slab_reduce: this block arrived last; generation seen
   alignas(8) uint64_t full[8];
 };
@@ -819,7 +861,7 @@ __device__ __forceinline__ void phase_end(const PcgArgs<T>& A, const Blk& blk, c
     return;
   }
   grid_barrier(A.bar, A.gate, A.rep, A.timeout_ns, (unsigned)blk.n, epoch);
-  for (int q = 0; q < nval; ++q) out[q] = fold_partials(part + (size_t)q * stride, n, (maxmask >> q) & 1u, S.bc);
+  fold_multi(part, n, stride, nval, maxmask, out, S.fold);
 }
 
 template <typename T, bool SLABS>
