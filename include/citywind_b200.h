@@ -223,6 +223,15 @@ typedef struct {
   int vert_offset, n_verts, tri_offset, n_tris;
 } cw_object;
 
+/* Painted-porosity base layer for the following cw_voxelize calls
+ * (decode_painted_porosity, ref grid.py:337-377, combined with the objects by
+ * combine_porosity, ref scenario.py:351-360, as in voxelize_design,
+ * ref scenario.py:402-412): an 8-bit (ny, nx) raster on the device (row 0 =
+ * min-y row), phi = pixel / 255 on planes [0, kmax); an optional tree mask of
+ * the same shape (non-zero = TREE with LAD tree_lad).  d_image NULL: open air. */
+int cw_set_paint(cw_ctx *ctx, const unsigned char *d_image, const unsigned char *d_tree_mask, int kmax,
+                 double tree_lad);
+
 int cw_voxelize(cw_ctx *ctx, const cw_object *objs, int n_obj, const double *verts,
                 const int *tris, int subdiv, const signed char *d_boundary_labels,
                 signed char *d_labels, double *d_phi, double *d_lad, int *n_overlap_warnings,

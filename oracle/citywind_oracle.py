@@ -793,9 +793,11 @@ class Scene:
     ai_omega: float = 1.65
     pcg_tol: float | None = None
     init_mode: str = "inflow"
+    paint: dict | None = None
+    base_dir: str = "."
 
 
-def scene_from_dict(doc):
+def scene_from_dict(doc, base_dir="."):
     gd = doc["grid"]
     grid = Grid(int(gd["nx"]), int(gd["ny"]), int(gd.get("nz", 1)), float(gd["dx"]),
                 float(gd["dy"]), float(gd.get("dz", gd["dx"])),
@@ -810,7 +812,7 @@ def scene_from_dict(doc):
     return Scene(grid, faces, inlet, params, list(doc.get("objects", [])),
                  list(doc.get("design", [])), doc.get("objective"),
                  int(num.get("subdiv", 4)), float(num.get("ai_omega", 1.65)),
-                 num.get("pcg_tol"), num.get("init", "inflow"))
+                 num.get("pcg_tol"), num.get("init", "inflow"), doc.get("paint"), base_dir)
 
 
 class Compiled:

@@ -2,6 +2,7 @@
 
 numpy restatement of the reference voxelizer path:
   scenario.py:327-360,383-417 (design bindings, object instantiation, layer merge)
+  grid.py:337-377,385-429 (painted-porosity base layer, PGM/PNG rasters)
   grid.py:133-141,144-211,214-230,233-325,473-478 (candidates, column casts,
       exact box coverage, sample merge, labels)
   geometry.py:145-241,301-316 (batch ray casts, point queries, cylinder mesh)
@@ -10,8 +11,8 @@ Every floating-point expression keeps the reference's operation order, and
 the per-cell sample mean uses np.mean exactly as the reference does
 (grid.py:316,319), so the result is bit-identical to the reference (pinned by
 tests/test_oracle_golden.py against fixtures made from the reference).
-The painted-porosity layer (grid.py:337-377) is not restated: no parity
-scene uses ``paint``.
+The painted-porosity layer is pinned by the paint_city golden
+(scripts/make_golden.py writes its raster into the fixture).
 """
 from __future__ import annotations
 
@@ -327,6 +328,64 @@ def scene_objects(scene, theta=None):
     return out
 
 
+def read_raster(path):
+    """grid.py:385-429: binary PGM (P5, maxval 255) or 8-bit PNG, (rows, cols)."""
+    if not str(path).lower().endswith(".pgm"):
+        from PIL import Image
+        img = Image.open(path)
+        return np.asarray(img if img.mode == "L" else img.convert("L"), dtype=np.uint8)
+    data = open(path, "rb").read()
+    toks, pos = [], 0
+    while len(toks) < 4:
+        while data[pos:pos + 1].isspace():
+            pos += 1
+        if data[pos:pos + 1] == b"#":
+            while pos < len(data) and data[pos] != 0x0A:
+                pos += 1
+            continue
+        st = pos
+        while pos < len(data) and not data[pos:pos + 1].isspace():
+            pos += 1
+        toks.append(data[st:pos])
+    w, h = int(toks[1]), int(toks[2])
+    return np.frombuffer(data, np.uint8, count=w * h, offset=pos + 1).reshape(h, w)
+
+
+def painted_layer(grid, image, tree_mask, extrude_height, tree_lad):
+    """decode_painted_porosity (grid.py:337-377) in the x-fastest layout:
+    planes k < kmax take phi = pixel / 255, TREE where the mask is set (LAD
+    tree_lad), BUILDING where phi < 1, else AIR."""
+    labels = np.zeros(grid.cshape, np.int8)
+    phi = np.ones(grid.cshape)
+    lad = np.zeros(grid.cshape)
+    img = np.asarray(image, np.uint8)
+    tree = np.zeros(img.shape, bool) if tree_mask is None else np.asarray(tree_mask) != 0
+    if grid.nz == 1 or extrude_height is None:
+        kmax = grid.nz
+    else:
+        zc = grid.origin[2] + (np.arange(grid.nz) + 0.5) * grid.dz - grid.origin[2]
+        kmax = int(np.sum(zc <= extrude_height))
+    p2 = img.astype(float) / 255.0                      # (ny, nx): x fastest already
+    l2 = np.where(tree, TREE, np.where((p2 < 1.0) | tree, BUILDING, AIR)).astype(np.int8)
+    for k in range(kmax):
+        phi[k] = p2
+        labels[k] = l2
+        lad[k] = np.where(tree, tree_lad, 0.0)
+    return labels, phi, lad
+
+
+def combine_layers(bl, bp, ba, al, ap, aa):
+    """combine_porosity (scenario.py:351-360): lower phi wins, LAD by max,
+    object TREE labels over AIR."""
+    phi = np.minimum(bp, ap)
+    lad = np.maximum(ba, aa)
+    labels = bl.copy()
+    take = ap < bp
+    labels[take] = al[take]
+    labels[(al == TREE) & (labels == AIR)] = TREE
+    return labels, phi, lad
+
+
 def combine_with_open_air(labels, phi, lad):
     """combine_porosity (scenario.py:351-360) against an open-air base layer."""
     phi_c = np.minimum(np.ones_like(phi), phi)
@@ -339,9 +398,21 @@ def combine_with_open_air(labels, phi, lad):
 
 
 def voxelize_scene(scene, boundary_labels, theta=None, stats=None):
+    """CompiledScenario.voxelize_design (scenario.py:383-417)."""
+    import os
     labels, phi, lad = (np.zeros(scene.grid.cshape, np.int8), np.ones(scene.grid.cshape),
                         np.zeros(scene.grid.cshape))
+    paint = getattr(scene, "paint", None)
+    if paint is not None:
+        base = getattr(scene, "base_dir", ".")
+        img = read_raster(os.path.join(base, paint["path"]))
+        mask = read_raster(os.path.join(base, paint["tree_mask"])) if paint.get("tree_mask") else None
+        labels, phi, lad = painted_layer(scene.grid, img, mask, paint.get("extrude_height"),
+                                         float(paint.get("tree_lad", 1.0)))
     if scene.objects:
         ol, op, oa = voxelize(scene_objects(scene, theta), scene.grid, scene.subdiv, stats)
-        labels, phi, lad = combine_with_open_air(ol, op, oa)
+        if paint is not None:
+            labels, phi, lad = combine_layers(labels, phi, lad, ol, op, oa)
+        else:
+            labels, phi, lad = combine_with_open_air(ol, op, oa)
     return merge_labels(boundary_labels, labels), phi, lad

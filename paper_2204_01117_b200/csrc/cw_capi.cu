@@ -83,6 +83,11 @@ struct cw_ctx {
   unsigned* xbar = nullptr;    // this context's cross-slab barrier (used when it is the root)
   double* xval = nullptr;
   void* slab_args = nullptr;   // device array of per-slab kernel arguments (group launches)
+  // painted-porosity layer for cw_voxelize (device buffers owned by the caller)
+  const uint8_t* paint = nullptr;
+  const uint8_t* paint_mask = nullptr;
+  int paint_kmax = 0;
+  double paint_lad = 1.0;
   // pending reports
   int head = 0;
   std::vector<double> slot_dt;
@@ -114,7 +119,24 @@ int cw_internal_device(cw_ctx* c, int* nx, int* ny, int* nz, double* h, double* 
   for (int a = 0; a < 3; ++a) origin[a] = c->grid.origin[a];
   return CW_OK;
 }
+void cw_internal_paint(cw_ctx* c, const uint8_t** image, const uint8_t** mask, int* kmax, double* tree_lad) {
+  *image = c->paint;
+  *mask = c->paint_mask;
+  *kmax = c->paint_kmax;
+  *tree_lad = c->paint_lad;
+}
 extern "C" const char* cw_last_error(void) { return g_err.c_str(); }
+
+extern "C" int cw_set_paint(cw_ctx* c, const unsigned char* d_image, const unsigned char* d_tree_mask, int kmax,
+                            double tree_lad) {
+  if (!c) return fail(CW_ERR_INVALID, "null argument");
+  if (d_image && (kmax < 0 || kmax > c->d.nz)) return fail(CW_ERR_INVALID, "kmax must lie in [0, nz]");
+  c->paint = d_image;
+  c->paint_mask = d_image ? d_tree_mask : nullptr;
+  c->paint_kmax = d_image ? kmax : 0;
+  c->paint_lad = tree_lad;
+  return CW_OK;
+}
 
 static int alloc(void** p, size_t bytes) {
   cudaError_t e = cudaMalloc(p, bytes);

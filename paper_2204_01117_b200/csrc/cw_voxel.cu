@@ -66,6 +66,11 @@ struct VoxObj {
 struct VoxGrid {
   int nx, ny, nz, sd, nsamp;
   double ox, oy, oz, hx, hy, hz;
+  // painted-porosity base layer (grid.py:337-377), or paint == nullptr
+  const uint8_t* paint;      // (ny, nx) raster, row 0 = min-y row: pixel (j, i) at j*nx + i
+  const uint8_t* tmask;      // tree mask of the same shape, or nullptr
+  int kmax;                  // planes [0, kmax) carry the paint
+  double tree_lad;
 };
 
 // numpy pairwise summation (loops_utils.h.src pairwise_sum), n <= 512
@@ -274,16 +279,36 @@ __device__ __forceinline__ bool in_range(const MeshObj& m, int i, int j, int k) 
          k < m.a0[2] + m.n[2];
 }
 
-// final label/phi/lad of one cell: combine with the open-air layer
+// the base layer under the objects at cell c: open air, or the painted
+// raster extruded over planes [0, kmax) (decode_painted_porosity, grid.py:337-377)
+__device__ __forceinline__ void base_layer(const VoxGrid& g, long long c, int8_t& blab, double& bphi, double& blad) {
+  blab = AIR;
+  bphi = 1.0;
+  blad = 0.0;
+  if (!g.paint) return;
+  const long long plane = (long long)g.nx * g.ny;
+  const long long k = c / plane;
+  if (k >= g.kmax) return;
+  const long long p = c - k * plane;
+  const bool tree = g.tmask != nullptr && g.tmask[p] != 0;
+  bphi = DDIV((double)g.paint[p], 255.0);                 // image / 255.0 (float64)
+  blab = tree ? (int8_t)TREE : ((bphi < 1.0) ? (int8_t)BUILDING : (int8_t)AIR);
+  blad = tree ? g.tree_lad : 0.0;
+}
+
+// final label/phi/lad of one cell: combine_porosity(base, objects)
 // (scenario.py:351-360) and overlay under the boundary frame (grid.py:473-478)
-__device__ __forceinline__ void write_cell(long long c, int8_t bnd, double phi, double lad, const CellAcc& a,
-                                           int8_t* labels, double* ophi, double* olad) {
+__device__ __forceinline__ void write_cell(const VoxGrid& g, long long c, int8_t bnd, double phi, double lad,
+                                           const CellAcc& a, int8_t* labels, double* ophi, double* olad) {
   int8_t lab = AIR;
   if (a.kind != 0 && (phi < DSUB(1.0, 1e-12) || lad > 0.0)) lab = (int8_t)a.kind;   // grid.py:320-324
-  int8_t comb = phi < 1.0 ? lab : (int8_t)AIR;
+  int8_t blab;
+  double bphi, blad;
+  base_layer(g, c, blab, bphi, blad);
+  int8_t comb = phi < bphi ? lab : blab;                  // take = add.phi < base.phi
   if (lab == TREE && comb == AIR) comb = TREE;
-  ophi[c] = phi;
-  olad[c] = lad;
+  ophi[c] = phi < bphi ? phi : bphi;                      // np.minimum
+  olad[c] = lad > blad ? lad : blad;                      // np.maximum
   labels[c] = (bnd == AIR && comb != AIR) ? comb : bnd;
 }
 
@@ -329,7 +354,7 @@ __global__ void k_vox_merge(VoxGrid g, const VoxObj* __restrict__ objs, int nobj
     }
     const double phi = phi_e ? DDIV(pw_const(sp, g.nsamp), (double)g.nsamp) : 1.0;
     const double lad = lad_e ? DDIV(pw_const(sl, g.nsamp), (double)g.nsamp) : 0.0;
-    write_cell(c, bnd[c], phi, lad, a, labels, ophi, olad);
+    write_cell(g, c, bnd[c], phi, lad, a, labels, ophi, olad);
   }
 }
 
@@ -403,7 +428,7 @@ __global__ void k_vox_complex(VoxGrid g, const VoxObj* __restrict__ objs, int no
     if (lane == 0) {
       const double phi = phi_e ? DDIV(pw_sum(sbuf, g.nsamp), (double)g.nsamp) : 1.0;
       const double lad = lad_e ? DDIV(pw_sum(sbuf + 512, g.nsamp), (double)g.nsamp) : 0.0;
-      write_cell(c, bnd[c], phi, lad, a, labels, ophi, olad);
+      write_cell(g, c, bnd[c], phi, lad, a, labels, ophi, olad);
     }
     __syncwarp();
   }
@@ -438,6 +463,7 @@ static const double PRIMARY[3] = {0x1.2470b1aa2db79p-2, 0x1.24c01e97c27f3p-1, 0x
 struct cw_ctx;
 extern int cw_internal_fail(int code, const char* msg);
 extern int cw_internal_device(cw_ctx* c, int* nx, int* ny, int* nz, double* h, double* origin);
+extern void cw_internal_paint(cw_ctx* c, const uint8_t** image, const uint8_t** mask, int* kmax, double* tree_lad);
 
 #define VCUDA(call)                                                                        \
   do {                                                                                     \
@@ -624,7 +650,8 @@ extern "C" int cw_voxelize(cw_ctx* ctx, const cw_object* objs, int n_obj, const 
     }
   }
   // 3) merge
-  VoxGrid g{nx, ny, nz, sd, sd * sd * sd, org[0], org[1], org[2], h[0], h[1], h[2]};
+  VoxGrid g{nx, ny, nz, sd, sd * sd * sd, org[0], org[1], org[2], h[0], h[1], h[2], nullptr, nullptr, 0, 0.0};
+  cw_internal_paint(ctx, &g.paint, &g.tmask, &g.kmax, &g.tree_lad);
   k_vox_merge<<<(int)std::min<long long>((ncell + 255) / 256, 148LL * 16), 256, 0, st>>>(
       g, d_obj, (int)live.size(), d_mesh, d_bits, (const int8_t*)d_bnd, (int8_t*)d_labels, d_phi, d_lad, d_list,
       d_err + 1, d_err + 2);

@@ -160,6 +160,89 @@ def interior_mask(labels: np.ndarray) -> np.ndarray:
     return (labels == 0) | (labels == 1) | (labels == 2)
 
 
+# ---------------------------------------------------------------------------
+# painted porosity (grid.py:337-429): host raster I/O and the host decode; the
+# device path feeds the raster to cw_set_paint + cw_voxelize instead
+
+def read_pgm(path) -> np.ndarray:
+    """Binary 8-bit PGM (P5) as a (rows, cols) uint8 array; row 0 = min-y row."""
+    data = open(path, "rb").read()
+    fields, pos = [], 0
+    while len(fields) < 4:
+        while pos < len(data) and data[pos:pos + 1].isspace():
+            pos += 1
+        if data[pos:pos + 1] == b"#":              # comment to end of line
+            pos = data.find(b"\n", pos)
+            pos = len(data) if pos < 0 else pos
+            continue
+        end = pos
+        while end < len(data) and not data[end:end + 1].isspace():
+            end += 1
+        fields.append(data[pos:end])
+        pos = end
+    if fields[0] != b"P5":
+        raise ValueError(f"not a binary PGM: magic {fields[0]!r}")
+    w, h, maxval = (int(f) for f in fields[1:])
+    if maxval != 255:
+        raise ValueError(f"PGM depth must be 8-bit (maxval 255), got {maxval}")
+    return np.frombuffer(data, dtype=np.uint8, count=w * h, offset=pos + 1).reshape(h, w)
+
+
+def write_pgm(path, image: np.ndarray) -> None:
+    image = np.asarray(image, dtype=np.uint8)
+    with open(path, "wb") as fh:
+        fh.write(b"P5\n%d %d\n255\n" % (image.shape[1], image.shape[0]))
+        fh.write(np.ascontiguousarray(image).tobytes())
+
+
+def load_raster(path) -> np.ndarray:
+    """PGM or 8-bit grayscale PNG (grid.py:419-429)."""
+    if str(path).lower().endswith(".pgm"):
+        return read_pgm(path)
+    from PIL import Image
+    img = Image.open(path)
+    return np.asarray(img if img.mode == "L" else img.convert("L"), dtype=np.uint8)
+
+
+def paint_planes(grid: "GridSpec", extrude_height) -> int:
+    """Planes [0, kmax) that carry the paint (grid.py:365-369)."""
+    if grid.is_2d or extrude_height is None:
+        return grid.nz
+    zc = grid.axis_centers(2) - grid.origin[2]
+    return int(np.sum(zc <= extrude_height))
+
+
+def decode_painted_porosity(image: np.ndarray, grid: "GridSpec", tree_mask=None, extrude_height=None,
+                            tree_lad: float = 1.0):
+    """Raster -> (labels, PorosityField) in the reference layout (grid.py:337-377):
+    phi = pixel / 255 extruded over the painted planes; dark pixels BUILDING,
+    tree-mask pixels TREE with LAD tree_lad."""
+    image = np.asarray(image)
+    if image.dtype != np.uint8:
+        raise ValueError(f"painted porosity must be 8-bit, got {image.dtype}")
+    if image.shape != (grid.ny, grid.nx):
+        raise ValueError(f"raster shape {image.shape} != (ny, nx) = {(grid.ny, grid.nx)}")
+    tree = np.zeros(image.shape, bool) if tree_mask is None else np.asarray(tree_mask) != 0
+    if tree.shape != image.shape:
+        raise ValueError("tree mask shape differs from image")
+    phi2 = image.astype(np.float64).T / 255.0
+    t2 = tree.T
+    lab2 = np.where(t2, int(CellLabel.TREE), np.where((phi2 < 1.0) | t2, int(CellLabel.BUILDING),
+                                                       int(CellLabel.AIR))).astype(np.int8)
+    labels = np.full(grid.shape, int(CellLabel.AIR), np.int8)
+    poros = PorosityField.open_air(grid)
+    km = paint_planes(grid, extrude_height)
+    labels[:, :, :km] = lab2[:, :, None]
+    poros.phi[:, :, :km] = phi2[:, :, None]
+    poros.lad[:, :, :km] = np.where(t2, float(tree_lad), 0.0)[:, :, None]
+    return labels, poros
+
+
+def encode_porosity_raster(poros: PorosityField, k: int = 0) -> np.ndarray:
+    """One z-slice of phi as a (ny, nx) uint8 raster (grid.py:380-382)."""
+    return np.round(poros.phi[:, :, k].T * 255.0).astype(np.uint8)
+
+
 def default_device():
     if not torch.cuda.is_available():
         raise RuntimeError("paper_2204_01117_b200 needs a CUDA device (B200); there is no CPU path")

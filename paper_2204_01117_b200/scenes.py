@@ -161,6 +161,46 @@ def channel_2d(nx: int = 24, ny: int = 16, dt: float = 0.1, speed: float = 2.0) 
     }
 
 
+def paint_rasters():
+    """Raster and tree mask (ny=40, nx=48) of ``painted_city``: opaque, porous
+    and noisy patches, a tree patch over a porous one (non-zero mask = tree)."""
+    rng = np.random.default_rng(11)
+    img = np.full((40, 48), 255, np.uint8)
+    img[5:15, 6:20] = 0
+    img[20:32, 10:18] = 76
+    img[8:30, 28:40] = 180
+    img[33:38, 2:46] = rng.integers(0, 256, (5, 44))
+    mask = np.zeros_like(img)
+    mask[22:30, 30:38] = 255
+    mask[2:6, 40:46] = 1
+    return img, mask
+
+
+def write_paint_files(directory: str) -> None:
+    """Write paint.pgm / trees.pgm (binary PGM, grid.py:412-416) for ``painted_city``."""
+    import os
+    from .grid import write_pgm
+    img, mask = paint_rasters()
+    write_pgm(os.path.join(directory, "paint.pgm"), img)
+    write_pgm(os.path.join(directory, "trees.pgm"), mask)
+
+
+def painted_city(dt: float = 0.3) -> dict:
+    """48x40x16 scene on a painted base layer extruded to 9 m (grid.py:337-377)
+    plus a box building crossing the paint and a tree cylinder; the rasters
+    come from ``write_paint_files`` in the scenario's base directory."""
+    doc = cuboid(48, 40, 16, 2.0, dt)
+    doc["name"] = "paint-city-48x40x16"
+    doc["paint"] = {"path": "paint.pgm", "extrude_height": 9.0, "tree_mask": "trees.pgm", "tree_lad": 0.8}
+    doc["objects"] = [
+        {"name": "b0", "kind": "building", "shape": "box", "lo": [30.0, 14.0, 0.0], "hi": [50.0, 30.0, 14.0],
+         "phi": 0.2},
+        {"name": "t0", "kind": "tree", "shape": "cylinder", "center": [70.0, 60.0], "radius": 5.0,
+         "z0": 2.0, "z1": 12.0, "lad": 1.5},
+    ]
+    return doc
+
+
 def scaled(doc: dict, **grid) -> dict:
     """Copy of ``doc`` with grid entries replaced (used to shrink scenes)."""
     out = copy.deepcopy(doc)

@@ -9,6 +9,7 @@ boundary frame (grid.py:473-478).
 from __future__ import annotations
 
 import ctypes as C
+import threading
 import warnings
 from dataclasses import dataclass
 
@@ -42,9 +43,23 @@ class GridObject:
             raise ValueError("object LAD must be >= 0")
 
 
-def voxelize_device(ctx, objects, grid: GridSpec, subdiv: int, boundary_dev: torch.Tensor):
+_paint_lock = threading.Lock()
+
+
+def voxelize_device(ctx, objects, grid: GridSpec, subdiv: int, boundary_dev: torch.Tensor, paint=None):
     """Returns (labels_dev int8, phi_dev float64, lad_dev float64) in the
-    x-fastest layout; labels already merged with the boundary labels."""
+    x-fastest layout; labels already merged with the boundary labels.
+    ``paint``: optional base layer (image uint8 (ny, nx) device tensor, tree
+    mask or None, kmax, tree_lad) under the objects (scenario.py:402-412)."""
+    if paint is not None:
+        img, mask, kmax, tree_lad = paint
+        with _paint_lock:   # the paint lives in the shared voxelizer context for this call only
+            N.check(N.lib().cw_set_paint(ctx.h, N.ptr(img), N.ptr(mask), int(kmax), float(tree_lad)))
+            try:
+                return voxelize_device(ctx, objects, grid, subdiv, boundary_dev)
+            finally:
+                torch.cuda.current_stream(boundary_dev.device).synchronize()
+                N.check(N.lib().cw_set_paint(ctx.h, None, None, 0, 1.0))
     if not 1 <= subdiv <= 8:
         raise ValueError("subdiv must be in [1, 8]")
     device = boundary_dev.device

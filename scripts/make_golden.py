@@ -46,6 +46,7 @@ SCENES = {
     "canyon_48": (scenes.canyon(48, 48, 24, 1.0, 0.2, n_trees=4), 25),
     "city_64": (scenes.block_city(64, 64, 24, 2.0, seed=3, nb=3, dt=0.25), 30),
     "channel2d": (scenes.channel_2d(24, 16, 0.1, 2.0), 60),
+    "paint_city_48": (scenes.painted_city(), 15),
 }
 VOXEL_ONLY = {
     "vox_canyon_128": scenes.canyon(128, 128, 64, 1.0, 0.2),
@@ -81,6 +82,9 @@ def run_scene(name, doc, steps):
                w_diag_mean=np.array(float(np.mean(W.diagonal()))),
                a_nnz=np.array(comp.psys.A.nnz), w_nnz=np.array(W.nnz),
                steps=np.array(steps))
+    if doc.get("paint"):
+        img, mask = scenes.paint_rasters()
+        out.update(paint_image=img, paint_mask=mask)
     np.savez_compressed(os.path.join(OUT, f"{name}.npz"), **out)
     print(f"{name}: {steps} steps in {time.perf_counter() - t0:.1f}s, iters={iters}")
 
@@ -124,6 +128,7 @@ def main():
     os.makedirs(OUT, exist_ok=True)
     cwd = tempfile.mkdtemp()
     os.chdir(cwd)
+    scenes.write_paint_files(cwd)
     for name, (doc, steps) in SCENES.items():
         if a.only in (None, name):
             run_scene(name, doc, steps)

@@ -18,7 +18,24 @@ STEP_SCENES = {
     "canyon_48": lambda: scenes.canyon(48, 48, 24, 1.0, 0.2, n_trees=4),
     "city_64": lambda: scenes.block_city(64, 64, 24, 2.0, seed=3, nb=3, dt=0.25),
     "channel2d": lambda: scenes.channel_2d(24, 16, 0.1, 2.0),
+    "paint_city_48": scenes.painted_city,
 }
+
+
+@pytest.fixture(scope="module")
+def base_dir(tmp_path_factory):
+    """Rasters of the painted scene, as the golden script wrote them."""
+    d = tmp_path_factory.mktemp("paint")
+    scenes.write_paint_files(str(d))
+    return str(d)
+
+
+def test_paint_rasters_match_fixture(base_dir):
+    g = load("paint_city_48")
+    img = vo.read_raster(os.path.join(base_dir, "paint.pgm"))
+    mask = vo.read_raster(os.path.join(base_dir, "trees.pgm"))
+    assert np.array_equal(img, g["paint_image"]) and np.array_equal(mask, g["paint_mask"])
+    assert (g["labels"] == 1).sum() > 0 and ((g["phi"] > 0) & (g["phi"] < 1)).sum() > 0
 
 
 def load(name):
@@ -36,9 +53,9 @@ def sha(a):
 
 
 @pytest.mark.parametrize("name", sorted(STEP_SCENES))
-def test_oracle_voxelizer_and_index_bitexact(name):
+def test_oracle_voxelizer_and_index_bitexact(name, base_dir):
     g = load(name)
-    comp = co.Compiled(co.scene_from_dict(STEP_SCENES[name]()))
+    comp = co.Compiled(co.scene_from_dict(STEP_SCENES[name](), base_dir))
     labels, phi, lad = comp.voxelize_design()
     assert np.array_equal(labels, g["labels"])
     assert np.array_equal(phi, g["phi"])
@@ -49,9 +66,9 @@ def test_oracle_voxelizer_and_index_bitexact(name):
 
 
 @pytest.mark.parametrize("name", sorted(STEP_SCENES))
-def test_oracle_steps_match_reference(name):
+def test_oracle_steps_match_reference(name, base_dir):
     g = load(name)
-    comp = co.Compiled(co.scene_from_dict(STEP_SCENES[name]()))
+    comp = co.Compiled(co.scene_from_dict(STEP_SCENES[name](), base_dir))
     st = comp.make_state()
     for f in ("u", "v", "w", "p", "k", "omega", "nu_t"):
         assert np.array_equal(getattr(st, f), g[f"init_{f}"]), f
