@@ -211,6 +211,20 @@ long long cw_launch_count(cw_ctx *ctx, int reset);
 int cw_region_speed(cw_ctx *ctx, const cw_fields *f, int n, const double *lo3n,
                     const double *hi3n, double *mean_out, long long *count_out, void *stream);
 
+/* Velocity at physical points, float64 trilinear samples of the staggered
+ * grids (the probes of run_simulation, ref scenario.py:473-478, via
+ * Advector.velocity_at, ref advection.py:107-111).  Device arrays: pts 3n,
+ * out 3n = (u, v, w) per point.  No host synchronisation. */
+int cw_probe(cw_ctx *ctx, const cw_fields *f, int n, const double *d_points, double *d_out, void *stream);
+
+/* trace_streamlines (ref solver.py:488-532): one device thread per seed, RK2
+ * midpoint steps of step_len along the normalised velocity, ending on domain
+ * exit, after max_steps, or below min_speed.  Device outputs: paths
+ * [nseeds][max_steps + 1][3], len[nseeds] points per polyline (0 for a seed
+ * outside the domain). */
+int cw_streamlines(cw_ctx *ctx, const cw_fields *f, int nseeds, const double *d_seeds, double step_len,
+                   int max_steps, double min_speed, double *d_paths, int *d_len, void *stream);
+
 /* Voxelizer, ref grid.py:233-325 + scenario.py:327-360 (bit-exact float64).
  * Objects in order; kind 1 building / 2 tree; shape 0 box (lo, hi), shape 1
  * closed triangle mesh given by (verts, tris) slices of the packed arrays.

@@ -875,3 +875,42 @@ def from_ref_layout(a):
 
 def field_digest(a):
     return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def trace_streamlines(state, seeds, step_len, max_steps=2000, min_speed=1e-6):
+    """solver.py:488-532: RK2 midpoint streamlines of the staggered velocity."""
+    g = state.grid
+    origin = np.asarray(g.origin, float)
+    spacing = np.array([g.dx, g.dy, g.dz])
+    lo = origin
+    hi = origin + spacing * np.array([g.nx, g.ny, g.nz])
+
+    def vel(p):
+        c = (p - origin) / spacing
+        us, vs, ws = velocity_at(state, np.array([c[0]]), np.array([c[1]]), np.array([c[2]]))
+        return np.array([us[0], vs[0], ws[0]])
+
+    out = []
+    for seed in np.atleast_2d(np.asarray(seeds, float)):
+        if np.any(seed < lo) or np.any(seed > hi):
+            out.append(np.empty((0, 3)))
+            continue
+        pts, p = [seed.copy()], seed.copy()
+        for _ in range(max_steps):
+            v1 = vel(p)
+            s1 = np.linalg.norm(v1)
+            if s1 < min_speed:
+                break
+            mid = p + 0.5 * step_len * v1 / s1
+            if np.any(mid < lo) or np.any(mid > hi):
+                break
+            v2 = vel(mid)
+            s2 = np.linalg.norm(v2)
+            if s2 < min_speed:
+                break
+            p = p + step_len * v2 / s2
+            if np.any(p < lo) or np.any(p > hi):
+                break
+            pts.append(p.copy())
+        out.append(np.array(pts))
+    return out

@@ -92,6 +92,9 @@ SIGNATURES = {
     "cw_ipc_open": (C.c_int, [C.POINTER(C.c_ubyte), C.c_int, C.POINTER(_P)]),
     "cw_ipc_close": (C.c_int, [_P]),
     "cw_set_paint": (C.c_int, [_P, _P, _P, C.c_int, C.c_double]),
+    "cw_probe": (C.c_int, [_P, C.POINTER(cw_fields), C.c_int, _P, _P, _P]),
+    "cw_streamlines": (C.c_int, [_P, C.POINTER(cw_fields), C.c_int, _P, C.c_double, C.c_int, C.c_double,
+                                 _P, _P, _P]),
     "cw_set_operator": (C.c_int, [_P, _P, C.c_double, C.POINTER(C.c_longlong),
                                   C.POINTER(C.c_double), _P]),
     "cw_set_preconditioner": (C.c_int, [_P, C.c_int, C.POINTER(C.c_double)]),

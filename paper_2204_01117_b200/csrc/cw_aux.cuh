@@ -174,3 +174,100 @@ __global__ void k_region_fold(int nblocks, int n, const double* part, const long
 }
 
 }  // namespace cw
+
+namespace cw {
+
+// ---------------------------------------------------------------------------
+// Velocity samples at arbitrary points, float64 (Advector.sample/velocity_at,
+// advection.py:49-111: trilinear with clamped indices on the staggered grids)
+template <typename T>
+__device__ __forceinline__ double sample64(const T* __restrict__ a, int ex, int ey, int ez, double fx, double fy,
+                                           double fz) {
+  int i0 = (int)floor(fx), j0 = (int)floor(fy), k0 = (int)floor(fz);
+  const int im = ex - 2 > 0 ? ex - 2 : 0, jm = ey - 2 > 0 ? ey - 2 : 0, km = ez - 2 > 0 ? ez - 2 : 0;
+  i0 = i0 < 0 ? 0 : (i0 > im ? im : i0);
+  j0 = j0 < 0 ? 0 : (j0 > jm ? jm : j0);
+  k0 = k0 < 0 ? 0 : (k0 > km ? km : k0);
+  double tx = fx - i0, ty = fy - j0, tz = fz - k0;
+  tx = tx < 0.0 ? 0.0 : (tx > 1.0 ? 1.0 : tx);
+  ty = ty < 0.0 ? 0.0 : (ty > 1.0 ? 1.0 : ty);
+  tz = tz < 0.0 ? 0.0 : (tz > 1.0 ? 1.0 : tz);
+  const long long sx = ex > 1 ? 1 : 0, sy = ey > 1 ? ex : 0, sz = ez > 1 ? (long long)ex * ey : 0;
+  const long long b = ((long long)k0 * ey + j0) * ex + i0;
+  const double c000 = a[b], c100 = a[b + sx], c010 = a[b + sy], c110 = a[b + sx + sy];
+  const double c001 = a[b + sz], c101 = a[b + sx + sz], c011 = a[b + sy + sz], c111 = a[b + sx + sy + sz];
+  const double ox = 1.0 - tx, oy = 1.0 - ty, oz = 1.0 - tz;
+  const double c00 = c000 * ox + c100 * tx, c10 = c010 * ox + c110 * tx;
+  const double c01 = c001 * ox + c101 * tx, c11 = c011 * ox + c111 * tx;
+  const double c0 = c00 * oy + c10 * ty, c1 = c01 * oy + c11 * ty;
+  return c0 * oz + c1 * tz;
+}
+
+// velocity at grid coordinates (X, Y, Z) = (p - origin) / h
+template <typename T>
+__device__ __forceinline__ void velocity64(const Dims& d, const T* u, const T* v, const T* w, double X, double Y,
+                                           double Z, double& us, double& vs, double& ws) {
+  us = sample64<T>(u, d.nx + 1, d.ny, d.nz, X, Y - 0.5, Z - 0.5);
+  vs = sample64<T>(v, d.nx, d.ny + 1, d.nz, X - 0.5, Y, Z - 0.5);
+  ws = sample64<T>(w, d.nx, d.ny, d.nz + 1, X - 0.5, Y - 0.5, Z);
+}
+
+struct Frame {
+  double o[3], h[3], lo[3], hi[3];
+};
+
+template <typename T>
+__global__ void k_probe(Dims d, Frame fr, const T* __restrict__ u, const T* __restrict__ v,
+                        const T* __restrict__ w, const double* __restrict__ pts, int n, double* __restrict__ out) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= n) return;
+  double us, vs, ws;
+  velocity64<T>(d, u, v, w, (pts[3 * q] - fr.o[0]) / fr.h[0], (pts[3 * q + 1] - fr.o[1]) / fr.h[1],
+                (pts[3 * q + 2] - fr.o[2]) / fr.h[2], us, vs, ws);
+  out[3 * q] = us;
+  out[3 * q + 1] = vs;
+  out[3 * q + 2] = ws;
+}
+
+__device__ __forceinline__ bool outside(const Frame& fr, const double* p) {
+  return p[0] < fr.lo[0] || p[1] < fr.lo[1] || p[2] < fr.lo[2] || p[0] > fr.hi[0] || p[1] > fr.hi[1] ||
+         p[2] > fr.hi[2];
+}
+
+// trace_streamlines (solver.py:488-532): one thread per seed, RK2 midpoint steps
+template <typename T>
+__global__ void k_streamlines(Dims d, Frame fr, const T* __restrict__ u, const T* __restrict__ v,
+                              const T* __restrict__ w, const double* __restrict__ seeds, int nseeds,
+                              double step_len, int max_steps, double min_speed, double* __restrict__ paths,
+                              int* __restrict__ len) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= nseeds) return;
+  double* out = paths + (size_t)s * (max_steps + 1) * 3;
+  double p[3] = {seeds[3 * s], seeds[3 * s + 1], seeds[3 * s + 2]};
+  if (outside(fr, p)) { len[s] = 0; return; }
+  int m = 0;
+  for (int a = 0; a < 3; ++a) out[a] = p[a];
+  ++m;
+  auto vel = [&](const double* x, double* vv) {
+    velocity64<T>(d, u, v, w, (x[0] - fr.o[0]) / fr.h[0], (x[1] - fr.o[1]) / fr.h[1], (x[2] - fr.o[2]) / fr.h[2],
+                  vv[0], vv[1], vv[2]);
+  };
+  for (int it = 0; it < max_steps; ++it) {
+    double v1[3], v2[3], mid[3];
+    vel(p, v1);
+    const double s1 = sqrt((v1[0] * v1[0] + v1[1] * v1[1]) + v1[2] * v1[2]);
+    if (s1 < min_speed) break;
+    for (int a = 0; a < 3; ++a) mid[a] = p[a] + 0.5 * step_len * v1[a] / s1;
+    if (outside(fr, mid)) break;
+    vel(mid, v2);
+    const double s2 = sqrt((v2[0] * v2[0] + v2[1] * v2[1]) + v2[2] * v2[2]);
+    if (s2 < min_speed) break;
+    for (int a = 0; a < 3; ++a) p[a] = p[a] + step_len * v2[a] / s2;
+    if (outside(fr, p)) break;
+    for (int a = 0; a < 3; ++a) out[3 * m + a] = p[a];
+    ++m;
+  }
+  len[s] = m;
+}
+
+}  // namespace cw

@@ -803,6 +803,60 @@ static int enqueue_stage(cw_ctx* c, const cw_fields* f, const cw_params* prm, in
 }
 
 // ---------------------------------------------------------------------------
+// probes and streamlines (run_simulation probes, scenario.py:473-478;
+// trace_streamlines, solver.py:488-532)
+
+static Frame frame_of(const cw_ctx* c) {
+  Frame fr;
+  const double h[3] = {c->grid.dx, c->grid.dy, c->grid.dz};
+  const int n[3] = {c->d.nx, c->d.ny, c->d.nz};
+  for (int a = 0; a < 3; ++a) {
+    fr.o[a] = c->grid.origin[a];
+    fr.h[a] = h[a];
+    fr.lo[a] = c->grid.origin[a];
+    fr.hi[a] = c->grid.origin[a] + h[a] * n[a];   // GridSpec.extent(): lo + spacing * shape
+  }
+  return fr;
+}
+
+extern "C" int cw_probe(cw_ctx* c, const cw_fields* f, int n, const double* pts, double* out, void* stream) {
+  if (!c || !f || (n > 0 && (!pts || !out))) return fail(CW_ERR_INVALID, "null argument");
+  if (c->d.kg0 != 0 || c->d.nz != c->d.nzg) return fail(CW_ERR_INVALID, "probes need a whole-grid context");
+  if (n == 0) return CW_OK;
+  CW_CUDA(cudaSetDevice(c->device));
+  const Frame fr = frame_of(c);
+  if (c->prec == 4)
+    (k_probe<float><<<(n + 127) / 128, 128, 0, S(stream)>>>(c->d, fr, (const float*)f->u, (const float*)f->v,
+                                                            (const float*)f->w, pts, n, out), ++c->launches);
+  else
+    (k_probe<double><<<(n + 127) / 128, 128, 0, S(stream)>>>(c->d, fr, (const double*)f->u, (const double*)f->v,
+                                                             (const double*)f->w, pts, n, out), ++c->launches);
+  CW_CUDA(cudaGetLastError());
+  return CW_OK;
+}
+
+extern "C" int cw_streamlines(cw_ctx* c, const cw_fields* f, int nseeds, const double* seeds, double step_len,
+                              int max_steps, double min_speed, double* paths, int* len, void* stream) {
+  if (!c || !f || (nseeds > 0 && (!seeds || !paths || !len))) return fail(CW_ERR_INVALID, "null argument");
+  if (max_steps < 0) return fail(CW_ERR_INVALID, "max_steps < 0");
+  if (c->d.kg0 != 0 || c->d.nz != c->d.nzg) return fail(CW_ERR_INVALID, "streamlines need a whole-grid context");
+  if (nseeds == 0) return CW_OK;
+  CW_CUDA(cudaSetDevice(c->device));
+  const Frame fr = frame_of(c);
+  const int nb = (nseeds + 63) / 64;
+  if (c->prec == 4)
+    (k_streamlines<float><<<nb, 64, 0, S(stream)>>>(c->d, fr, (const float*)f->u, (const float*)f->v,
+                                                    (const float*)f->w, seeds, nseeds, step_len, max_steps,
+                                                    min_speed, paths, len), ++c->launches);
+  else
+    (k_streamlines<double><<<nb, 64, 0, S(stream)>>>(c->d, fr, (const double*)f->u, (const double*)f->v,
+                                                     (const double*)f->w, seeds, nseeds, step_len, max_steps,
+                                                     min_speed, paths, len), ++c->launches);
+  CW_CUDA(cudaGetLastError());
+  return CW_OK;
+}
+
+// ---------------------------------------------------------------------------
 // z-slab solves
 
 extern "C" int cw_slab_buffers_get(cw_ctx* c, cw_slab_buffers* out) {

@@ -452,35 +452,44 @@ def region_average_speed(state: FlowState, box_lo, box_hi,
     return float(means[0])
 
 
-def _gather_point(t: torch.Tensor, fx: float, fy: float, fz: float) -> float:
-    """Trilinear sample of an x-fastest device array at fractional (x, y, z),
-    indices clamped like advection.py:49-101 (8 device reads)."""
-    nz, ny, nx = t.shape
-
-    def split(f, n):
-        i0 = int(min(max(np.floor(f), 0), max(n - 2, 0)))
-        return i0, float(np.clip(f - i0, 0.0, 1.0)), (1 if n > 1 else 0)
-
-    i0, tx, sx = split(fx, nx)
-    j0, ty, sy = split(fy, ny)
-    k0, tz, sz = split(fz, nz)
-    c = t[k0:k0 + 1 + sz, j0:j0 + 1 + sy, i0:i0 + 1 + sx].double().cpu().numpy()
-    c = np.broadcast_to(c if c.shape == (2, 2, 2) else np.pad(c, [(0, 2 - c.shape[0]), (0, 2 - c.shape[1]),
-                                                              (0, 2 - c.shape[2])], mode="edge"), (2, 2, 2))
-    c00 = c[0, 0, 0] * (1 - tx) + c[0, 0, 1] * tx
-    c10 = c[0, 1, 0] * (1 - tx) + c[0, 1, 1] * tx
-    c01 = c[1, 0, 0] * (1 - tx) + c[1, 0, 1] * tx
-    c11 = c[1, 1, 0] * (1 - tx) + c[1, 1, 1] * tx
-    c0 = c00 * (1 - ty) + c10 * ty
-    c1 = c01 * (1 - ty) + c11 * ty
-    return float(c0 * (1 - tz) + c1 * tz)
+def probe_velocities(state: FlowState, points, out: torch.Tensor | None = None) -> torch.Tensor:
+    """Velocities at physical points on the device (``cw_probe``): float64
+    staggered trilinear samples of u, v, w (run_simulation's probes,
+    scenario.py:473-478, through Advector.velocity_at, advection.py:107-111).
+    Returns (or fills) a (n, 3) float64 device tensor; no host synchronisation."""
+    pts = torch.as_tensor(np.asarray(points, dtype=np.float64).reshape(-1, 3), device=state.device)
+    if out is None:
+        out = torch.empty((pts.shape[0], 3), dtype=torch.float64, device=state.device)
+    ctx = _scratch_ctx(state)
+    f = ctx.fields(state)
+    N.check(N.lib().cw_probe(ctx.h, C.byref(f), int(pts.shape[0]), N.ptr(pts), N.ptr(out), ctx.stream))
+    # pts is freed only after the kernel ran: torch's caching allocator reuses
+    # the block on this same stream, after the kernel in stream order
+    return out
 
 
 def probe_velocity(state: FlowState, pos) -> tuple:
     """Velocity at a physical point (the probes of run_simulation,
     scenario.py:473-478): staggered trilinear samples of u, v, w."""
-    g = state.grid
-    X, Y, Z = ((np.asarray(pos, float) - np.asarray(g.origin)) / g.spacing)
-    f = state.fields
-    return (_gather_point(f["u"], X, Y - 0.5, Z - 0.5), _gather_point(f["v"], X - 0.5, Y, Z - 0.5),
-            _gather_point(f["w"], X - 0.5, Y - 0.5, Z))
+    v = probe_velocities(state, [pos])[0].cpu().numpy()
+    return float(v[0]), float(v[1]), float(v[2])
+
+
+def trace_streamlines(state: FlowState, seeds, step_len: float, max_steps: int = 2000,
+                      min_speed: float = 1e-6) -> list:
+    """Midpoint (RK2) streamlines of the instantaneous velocity (solver.py:488-532),
+    one device thread per seed (``cw_streamlines``).  A polyline ends on domain
+    exit, after max_steps, or where the speed drops below min_speed; seeds
+    outside the domain give empty polylines."""
+    sd = np.atleast_2d(np.asarray(seeds, dtype=np.float64))
+    n = sd.shape[0]
+    dev = state.device
+    seeds_d = torch.as_tensor(np.ascontiguousarray(sd), device=dev)
+    paths = torch.empty((n, int(max_steps) + 1, 3), dtype=torch.float64, device=dev)
+    lens = torch.empty(n, dtype=torch.int32, device=dev)
+    ctx = _scratch_ctx(state)
+    f = ctx.fields(state)
+    N.check(N.lib().cw_streamlines(ctx.h, C.byref(f), n, N.ptr(seeds_d), float(step_len), int(max_steps),
+                                   float(min_speed), N.ptr(paths), N.ptr(lens), ctx.stream))
+    p, m = paths.cpu().numpy(), lens.cpu().numpy()
+    return [p[i, :m[i]].copy() if m[i] > 0 else np.empty((0, 3)) for i in range(n)]
