@@ -1,0 +1,50 @@
+"""GPU: non-box unknown sets -- interior SOLID_WALL cells
+inside the flow, as validate_porosity's no-slip "truth" runs build them
+(ref validate.py:210-217), started from rest (solver.py:464-481 mode "rest").
+Per-step PCG iteration counts must equal the oracle's; fields within 1e-4."""
+import numpy as np
+import pytest
+
+from helpers import FIELDS, device_params, device_state, fields_of, ref_grid, rel_l2
+from paper_2204_01117_b200 import scenes
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+
+@pytest.mark.parametrize("prec", ["fp32", "fp64"])
+def test_interior_walls_match_oracle(prec):
+    from oracle import citywind_oracle as co
+    from paper_2204_01117_b200 import solver
+    from paper_2204_01117_b200.grid import to_ref_layout
+    from paper_2204_01117_b200.linalg import build_ai_preconditioner, build_pressure_matrix
+    doc = scenes.cuboid(32, 20, 8, 1.0, 0.1)
+    doc["objects"] = []
+    doc["solver"]["u_ref"] = 2.0
+    doc["inlet"]["speed"] = 2.0
+    sc = co.scene_from_dict(doc)
+    g = sc.grid
+    labels = co.classify_boundary(g, sc.faces)          # x-fastest (nz, ny, nx)
+    labels[1:6, 7:13, 10:14] = 5                          # an interior no-slip block
+    labels[1:3, 2:4, 20:26] = 5                           # and a low wall near the side
+    phi, lad = np.ones(g.cshape), np.zeros(g.cshape)
+    psys = co.build_pressure_matrix(g, labels)
+    W = co.build_ai_preconditioner(psys.A, sc.ai_omega)
+    ost = co.make_initial_state(g, labels, phi, lad, sc.params, sc.inlet, mode="rest")
+    dtype = torch.float32 if prec == "fp32" else torch.float64
+    dst = device_state(ost, dtype)
+    dpsys = build_pressure_matrix(ref_grid(g), to_ref_layout(labels))
+    dpre = build_ai_preconditioner(dpsys, sc.ai_omega, 1, truncate=False)
+    p, prof = device_params(sc)
+    want = []
+    for _ in range(20):
+        want.append(co.step(ost, sc.params, psys, W, sc.inlet).pcg.iterations)
+    reps = solver.step_many(dst, p, dpsys, dpre, prof, 20)
+    assert [r.pcg.iterations for r in reps] == want
+    got = fields_of(dst)
+    tol = 1e-4 if prec == "fp32" else 1e-9
+    for n in FIELDS:
+        assert rel_l2(got[n], getattr(ost, n)) <= tol, n
+    # no-slip: every face touching a wall cell is zero
+    u = got["u"]
+    assert np.all(u[1:6, 7:13, 10:15] == 0.0)
