@@ -27,6 +27,8 @@ struct Dims {
   __host__ __device__ inline long long cidx(int i, int j, int k) const {
     return ((long long)k * ny + j) * nx + i;
   }
+  // 32-bit cell index (contexts hold < 2^31 cells per field, cw_capi.cu)
+  __host__ __device__ inline int cidx32(int i, int j, int k) const { return (k * ny + j) * nx + i; }
 };
 
 // Extents of component arrays: comp 0 = u, 1 = v, 2 = w, 3 = cell.

@@ -66,14 +66,14 @@ __global__ void k_upwind(Dims d, const T* __restrict__ u, const T* __restrict__ 
   if (*gate) return;
   CW_IJK(d.nx, d.ny, d.nz, inb);
   if (inb) {
-    const long long c = d.cidx(i, j, k);
+    const int c = d.cidx32(i, j, k);
     T a[3];
-    a[0] = (T)0.5 * (u[((long long)k * d.ny + j) * (d.nx + 1) + i] + u[((long long)k * d.ny + j) * (d.nx + 1) + i + 1]);
-    a[1] = (T)0.5 * (v[((long long)k * (d.ny + 1) + j) * d.nx + i] + v[((long long)k * (d.ny + 1) + j + 1) * d.nx + i]);
-    a[2] = (T)0.5 * (w[c] + w[c + (long long)d.nx * d.ny]);
+    a[0] = (T)0.5 * (u[((int)k * d.ny + j) * (d.nx + 1) + i] + u[((int)k * d.ny + j) * (d.nx + 1) + i + 1]);
+    a[1] = (T)0.5 * (v[((int)k * (d.ny + 1) + j) * d.nx + i] + v[((int)k * (d.ny + 1) + j + 1) * d.nx + i]);
+    a[2] = (T)0.5 * (w[c] + w[c + (int)d.nx * d.ny]);
     const int pos[3] = {i, j, k};
     const int ext[3] = {d.nx, d.ny, d.nz};
-    const long long str[3] = {1, d.nx, (long long)d.nx * d.ny};
+    const int str[3] = {1, d.nx, (int)d.nx * d.ny};
     const T h[3] = {(T)d.dx, (T)d.dy, (T)d.dz};
 #pragma unroll
     for (int f = 0; f < 2; ++f) {
@@ -135,7 +135,7 @@ __device__ __forceinline__ void mac_predict_face(const Dims& d, int comp, const 
   comp_offset(comp, fox, foy, foz);
   const T ox = (T)fox, oy = (T)foy, oz = (T)foz;
   const T* arr = comp == 0 ? u : (comp == 1 ? v : w);
-  const long long c = ((long long)k * ey + j) * ex + i;
+  const int c = ((int)k * ey + j) * ex + i;
   const T X = (T)i + ox, Y = (T)j + oy, Z = (T)k + oz;
   T us, vs, ws;
   velocity_at<T>(d, comp, u, v, w, i, j, k, us, vs, ws);
@@ -165,7 +165,7 @@ __device__ __forceinline__ void mac_correct_face(const Dims& d, int comp, const 
   comp_offset(comp, fox, foy, foz);
   const T ox = (T)fox, oy = (T)foy, oz = (T)foz;
   const T* arr = comp == 0 ? u : (comp == 1 ? v : w);
-  const long long c = ((long long)k * ey + j) * ex + i;
+  const int c = ((int)k * ey + j) * ex + i;
   const T X = (T)i + ox, Y = (T)j + oy, Z = (T)k + oz;
   T us, vs, ws;
   velocity_at<T>(d, comp, u, v, w, i, j, k, us, vs, ws);
@@ -196,7 +196,7 @@ __global__ void k_mac_correct(Dims d, const T* __restrict__ u, const T* __restri
 // ---------------------------------------------------------------------------
 // explicit diffusion with the capped eddy viscosity (solver.py:175-208)
 template <typename T>
-__device__ __forceinline__ T nu_eff(const T* nut, long long c, T nu, T cap) {
+__device__ __forceinline__ T nu_eff(const T* nut, int c, T nu, T cap) {
   T t = nut[c];
   t = t < (T)0 ? (T)0 : t;
   t = t > cap ? cap : t;
@@ -210,11 +210,11 @@ __global__ void k_diffuse(Dims d, int comp, const T* __restrict__ src, T* __rest
   int ex, ey, ez;
   comp_extent(d, comp, ex, ey, ez);
   const int ext[3] = {ex, ey, ez};
-  const long long str[3] = {1, ex, (long long)ex * ey};
+  const int str[3] = {1, ex, (int)ex * ey};
   const T h[3] = {(T)d.dx, (T)d.dy, (T)d.dz};
   CW_IJK(ex, ey, ez, inb);
   if (inb) {
-    const long long c = ((long long)k * ey + j) * ex + i;
+    const int c = ((int)k * ey + j) * ex + i;
     const int pos[3] = {i, j, k};
     const T mid = src[c];
     T lap = (T)0;
@@ -230,9 +230,9 @@ __global__ void k_diffuse(Dims d, int comp, const T* __restrict__ src, T* __rest
     const int nc = comp == 0 ? d.nx : (comp == 1 ? d.ny : d.nz);
     const int f = pos[comp];
     ci[comp] = clampi(f - 1, 0, nc - 1);
-    const T a = nu_eff(nut, d.cidx(ci[0], ci[1], ci[2]), nu, cap);
+    const T a = nu_eff(nut, d.cidx32(ci[0], ci[1], ci[2]), nu, cap);
     ci[comp] = clampi(f, 0, nc - 1);
-    const T b = nu_eff(nut, d.cidx(ci[0], ci[1], ci[2]), nu, cap);
+    const T b = nu_eff(nut, d.cidx32(ci[0], ci[1], ci[2]), nu, cap);
     dst[c] = mid + dt * ((T)0.5 * (a + b)) * lap;
   }
 }
@@ -245,12 +245,12 @@ __global__ void k_cell_speed(Dims d, const T* __restrict__ u, const T* __restric
   if (*gate) return;
   CW_IJK(d.nx, d.ny, d.nz, inb);
   if (inb) {
-    const long long c = d.cidx(i, j, k);
-    const long long ui = ((long long)k * d.ny + j) * (d.nx + 1) + i;
-    const long long vi = ((long long)k * (d.ny + 1) + j) * d.nx + i;
+    const int c = d.cidx32(i, j, k);
+    const int ui = ((int)k * d.ny + j) * (d.nx + 1) + i;
+    const int vi = ((int)k * (d.ny + 1) + j) * d.nx + i;
     const T uc = (T)0.5 * (u[ui] + u[ui + 1]);
     const T vc = (T)0.5 * (v[vi] + v[vi + d.nx]);
-    const T wc = (T)0.5 * (w[c] + w[c + (long long)d.nx * d.ny]);
+    const T wc = (T)0.5 * (w[c] + w[c + (int)d.nx * d.ny]);
     speed[c] = sqrt(uc * uc + vc * vc + wc * wc);
   }
 }
@@ -264,13 +264,13 @@ __global__ void k_drag(Dims d, int comp, T* __restrict__ arr, const T* __restric
   const int nc = comp == 0 ? d.nx : (comp == 1 ? d.ny : d.nz);
   CW_IJK(ex, ey, ez, inb);
   if (inb) {
-    const long long c = ((long long)k * ey + j) * ex + i;
+    const int c = ((int)k * ey + j) * ex + i;
     int p[3] = {i, j, k};
     const int f = p[comp];
     p[comp] = clampi(f - 1, 0, nc - 1);
-    const long long lo = d.cidx(p[0], p[1], p[2]);
+    const int lo = d.cidx32(p[0], p[1], p[2]);
     p[comp] = clampi(f, 0, nc - 1);
-    const long long hi = d.cidx(p[0], p[1], p[2]);
+    const int hi = d.cidx32(p[0], p[1], p[2]);
     const T gf = (T)0.5 * (g[lo] + g[hi]);
     const T sf = (T)0.5 * (speed[lo] + speed[hi]);
     T fac = (T)1 - dt * gf * sf;
@@ -302,10 +302,10 @@ __global__ void k_bc_outlet_side(Dims d, int axis, int pos, BcFields<T> F,
     // cells (scalars) and the normal velocity component
     if (q1 < ext[a1] && q2 < ext[a2]) {
       c[axis] = pos; c[a1] = q1; c[a2] = q2;
-      const long long cc = d.cidx(c[0], c[1], c[2]);
+      const int cc = d.cidx32(c[0], c[1], c[2]);
       if (lab[cc] == OUTLET) {
         c[axis] = inner;
-        const long long ci = d.cidx(c[0], c[1], c[2]);
+        const int ci = d.cidx32(c[0], c[1], c[2]);
         F.k[cc] = F.k[ci]; F.om[cc] = F.om[ci]; F.nut[cc] = F.nut[ci]; F.p[cc] = F.p[ci];
         if (!(d.is2d && axis == 2)) {
           int ex, ey, ez;
@@ -313,9 +313,9 @@ __global__ void k_bc_outlet_side(Dims d, int axis, int pos, BcFields<T> F,
           int f[3];
           f[a1] = q1; f[a2] = q2;
           f[axis] = pos > 0 ? pos + 1 : 0;
-          const long long fo = ((long long)f[2] * ey + f[1]) * ex + f[0];
+          const int fo = ((int)f[2] * ey + f[1]) * ex + f[0];
           f[axis] = pos > 0 ? pos : 1;
-          const long long fs = ((long long)f[2] * ey + f[1]) * ex + f[0];
+          const int fs = ((int)f[2] * ey + f[1]) * ex + f[0];
           T* arr = axis == 0 ? F.u : (axis == 1 ? F.v : F.w);
           arr[fo] = arr[fs];
         }
@@ -332,17 +332,17 @@ __global__ void k_bc_outlet_side(Dims d, int axis, int pos, BcFields<T> F,
       if (qa > ext[caxis] || qb >= ext[oth]) continue;
       c[axis] = pos; c[oth] = qb;
       c[caxis] = clampi(qa - 1, 0, ext[caxis] - 1);
-      bool m = lab[d.cidx(c[0], c[1], c[2])] == OUTLET;
+      bool m = lab[d.cidx32(c[0], c[1], c[2])] == OUTLET;
       c[caxis] = clampi(qa, 0, ext[caxis] - 1);
-      m = m || lab[d.cidx(c[0], c[1], c[2])] == OUTLET;
+      m = m || lab[d.cidx32(c[0], c[1], c[2])] == OUTLET;
       if (!m) continue;
       int ex, ey, ez;
       comp_extent(d, caxis, ex, ey, ez);
       int f[3];
       f[axis] = pos; f[caxis] = qa; f[oth] = qb;
-      const long long fo = ((long long)f[2] * ey + f[1]) * ex + f[0];
+      const int fo = ((int)f[2] * ey + f[1]) * ex + f[0];
       f[axis] = inner;
-      const long long fs = ((long long)f[2] * ey + f[1]) * ex + f[0];
+      const int fs = ((int)f[2] * ey + f[1]) * ex + f[0];
       T* arr = caxis == 0 ? F.u : (caxis == 1 ? F.v : F.w);
       arr[fo] = arr[fs];
     }
@@ -361,10 +361,10 @@ __device__ __forceinline__ void bc_face(const Dims& d, int comp, T* arr, const i
   int p[3] = {i, j, k};
   const int f = p[comp];
   p[comp] = clampi(f - 1, 0, ext[comp] - 1);
-  const int8_t la = lab[d.cidx(p[0], p[1], p[2])];
+  const int8_t la = lab[d.cidx32(p[0], p[1], p[2])];
   p[comp] = clampi(f, 0, ext[comp] - 1);
-  const int8_t lb = lab[d.cidx(p[0], p[1], p[2])];
-  const long long r = ((long long)k * ey + j) * ex + i;
+  const int8_t lb = lab[d.cidx32(p[0], p[1], p[2])];
+  const int r = ((int)k * ey + j) * ex + i;
   if (la == SOLID_WALL || lb == SOLID_WALL) {
     arr[r] = (T)0;
   } else if (la == INLET || lb == INLET) {
@@ -380,7 +380,7 @@ __global__ void k_bc_inlet_wall(Dims d, BcFields<T> F, const int8_t* __restrict_
   CW_IJK(d.nx + 1, d.ny + 1, d.nz + 1, inb);
   if (!inb) return;
   if (i < d.nx && j < d.ny && k < d.nz) {
-    const long long t = d.cidx(i, j, k);
+    const int t = d.cidx32(i, j, k);
     if (lab[t] == INLET) { F.k[t] = k_in; F.om[t] = om_in; F.nut[t] = nut_in; }
   }
   bc_face<T>(d, 0, F.u, lab, i, j, k, uz_dirx, uz_diry);
@@ -400,14 +400,14 @@ __global__ void k_gradient(Dims d, int comp, T* __restrict__ arr, const T* __res
   const int nc = comp == 0 ? d.nx : (comp == 1 ? d.ny : d.nz);
   CW_IJK(ex, ey, ez, inb);
   if (inb) {
-    const long long c = ((long long)k * ey + j) * ex + i;
+    const int c = ((int)k * ey + j) * ex + i;
     int q[3] = {i, j, k};
     const int f = q[comp];
     if (f < 1 || f > nc - 1) return;
     q[comp] = f - 1;
-    const long long lo = d.cidx(q[0], q[1], q[2]);
+    const int lo = d.cidx32(q[0], q[1], q[2]);
     q[comp] = f;
-    const long long hi = d.cidx(q[0], q[1], q[2]);
+    const int hi = d.cidx32(q[0], q[1], q[2]);
     const int8_t la = lab[lo], lb = lab[hi];
     const bool au = is_unknown(la), bu = is_unknown(lb);
     T grad = (T)0;
@@ -428,12 +428,12 @@ __global__ void k_div_max(Dims d, const T* __restrict__ u, const T* __restrict__
   __shared__ T scratch[32];
   T m = (T)0;
   CW_IJK_OWN(d.nx, d.ny, d.o1, inb);
-  const long long c = d.cidx(i, j, k);
+  const int c = d.cidx32(i, j, k);
   if (inb && is_unknown(lab[c])) {
-    const long long ui = ((long long)k * d.ny + j) * (d.nx + 1) + i;
-    const long long vi = ((long long)k * (d.ny + 1) + j) * d.nx + i;
+    const int ui = ((int)k * d.ny + j) * (d.nx + 1) + i;
+    const int vi = ((int)k * (d.ny + 1) + j) * d.nx + i;
     T div = (u[ui + 1] - u[ui]) / (T)d.dx + (v[vi + d.nx] - v[vi]) / (T)d.dy;
-    if (!d.is2d) div = div + (w[c + (long long)d.nx * d.ny] - w[c]) / (T)d.dz;
+    if (!d.is2d) div = div + (w[c + (int)d.nx * d.ny] - w[c]) / (T)d.dz;
     const T a = fabs(div);
     m = (a > m || a != a) ? a : m;
   }
@@ -453,11 +453,11 @@ __global__ void k_speed_max(Dims d, const T* __restrict__ u, const T* __restrict
   CW_IJK_OWN(d.nx + 1, d.ny + 1, d.o1 + 1, inb);
   if (inb) {
     if (k < d.o1) {
-      if (j < d.ny) { const T a = fabs(u[((long long)k * d.ny + j) * (d.nx + 1) + i]); m = (a > m || a != a) ? a : m; }
-      if (i < d.nx) { const T a = fabs(v[((long long)k * (d.ny + 1) + j) * d.nx + i]); m = (a > m || a != a) ? a : m; }
+      if (j < d.ny) { const T a = fabs(u[((int)k * d.ny + j) * (d.nx + 1) + i]); m = (a > m || a != a) ? a : m; }
+      if (i < d.nx) { const T a = fabs(v[((int)k * (d.ny + 1) + j) * d.nx + i]); m = (a > m || a != a) ? a : m; }
     }
     if (i < d.nx && j < d.ny) {
-      const T a = fabs(w[((long long)k * d.ny + j) * d.nx + i]);
+      const T a = fabs(w[((int)k * d.ny + j) * d.nx + i]);
       m = (a > m || a != a) ? a : m;
     }
   }
@@ -471,15 +471,15 @@ template <typename T>
 __device__ __forceinline__ T cell_vel(const Dims& d, int comp, const T* u, const T* v, const T* w,
                                       int i, int j, int k) {
   if (comp == 0) {
-    const long long ui = ((long long)k * d.ny + j) * (d.nx + 1) + i;
+    const int ui = ((int)k * d.ny + j) * (d.nx + 1) + i;
     return (T)0.5 * (u[ui] + u[ui + 1]);
   }
   if (comp == 1) {
-    const long long vi = ((long long)k * (d.ny + 1) + j) * d.nx + i;
+    const int vi = ((int)k * (d.ny + 1) + j) * d.nx + i;
     return (T)0.5 * (v[vi] + v[vi + d.nx]);
   }
-  const long long c = d.cidx(i, j, k);
-  return (T)0.5 * (w[c] + w[c + (long long)d.nx * d.ny]);
+  const int c = d.cidx32(i, j, k);
+  return (T)0.5 * (w[c] + w[c + (int)d.nx * d.ny]);
 }
 
 // np.gradient of the cell-centred component `comp` along `ax` (edge_order 1)
@@ -501,9 +501,9 @@ __device__ __forceinline__ T cgrad(const Dims& d, int comp, int ax, const T* u, 
 }
 
 template <typename T>
-__device__ __forceinline__ T pad_lap(const Dims& d, const T* f, long long c, int i, int j, int k) {
+__device__ __forceinline__ T pad_lap(const Dims& d, const T* f, int c, int i, int j, int k) {
   const int pos[3] = {i, j, k}, ext[3] = {d.nx, d.ny, d.nz};
-  const long long str[3] = {1, d.nx, (long long)d.nx * d.ny};
+  const int str[3] = {1, d.nx, (int)d.nx * d.ny};
   const T h[3] = {(T)d.dx, (T)d.dy, (T)d.dz};
   const T fc = f[c];
   T out = (T)0;
@@ -528,12 +528,12 @@ __global__ void k_turbulence(Dims d, const T* __restrict__ u, const T* __restric
   const T dt = (T)sc.dt, nu = (T)sc.nu, cap = (T)sc.cap_turb;
   CW_IJK(d.nx, d.ny, d.nz, inb);
   if (inb) {
-    const long long c = d.cidx(i, j, k);
-    const long long ui = ((long long)k * d.ny + j) * (d.nx + 1) + i;
-    const long long vi = ((long long)k * (d.ny + 1) + j) * d.nx + i;
+    const int c = d.cidx32(i, j, k);
+    const int ui = ((int)k * d.ny + j) * (d.nx + 1) + i;
+    const int vi = ((int)k * (d.ny + 1) + j) * d.nx + i;
     const T dudx = (u[ui + 1] - u[ui]) / (T)d.dx;
     const T dvdy = (v[vi + d.nx] - v[vi]) / (T)d.dy;
-    const T dwdz = (w[c + (long long)d.nx * d.ny] - w[c]) / (T)d.dz;
+    const T dwdz = (w[c + (int)d.nx * d.ny] - w[c]) / (T)d.dz;
     const T dudy = cgrad(d, 0, 1, u, v, w, i, j, k), dudz = cgrad(d, 0, 2, u, v, w, i, j, k);
     const T dvdx = cgrad(d, 1, 0, u, v, w, i, j, k), dvdz = cgrad(d, 1, 2, u, v, w, i, j, k);
     const T dwdx = cgrad(d, 2, 0, u, v, w, i, j, k), dwdy = cgrad(d, 2, 1, u, v, w, i, j, k);
