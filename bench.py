@@ -249,33 +249,67 @@ def doc_cells(doc):
 # ---------------------------------------------------------------------------
 # the B200 arm
 
-def zslab_leg(args, comp, sc, dist, world, ncell):
-    """One C3 simulation split into `world` z-slabs, one per GPU:
-    device-timed steps, max over ranks.  Returns (ok, result dict)."""
+def zslab_child(args):
+    """Child-process body of the z-slab leg (one per rank, its own process
+    group): prints one JSON line on rank 0.  Kept out of the parent so that a
+    failure on the multi-GPU path cannot take the bench line down with it."""
     import torch
+    import torch.distributed as dist
+    from paper_2204_01117_b200.scenario import CompiledScenario, scenario_from_dict
     from paper_2204_01117_b200.slabs import DEFAULT_HALO, DistSlabSolver
+    world = int(os.environ["WORLD_SIZE"])
+    rank = int(os.environ["RANK"])
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    doc = c3_doc(args.dt)
+    ncell = doc_cells(doc)
+    sc = scenario_from_dict(doc)
+    comp = CompiledScenario.compile(sc, dtype=torch.float32)
+    state = comp.make_state()
+    sol = DistSlabSolver(state, sc.solver, sc.inlet, omega=sc.ai_omega, pcg_tol=sc.pcg_tol)
+    del state
+    sol.step_many(args.warmup)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    dist.barrier()
+    torch.cuda.synchronize()
+    e0.record()
+    reps = sol.step_many(args.steps)
+    e1.record()
+    torch.cuda.synchronize()
+    t = torch.tensor([e0.elapsed_time(e1)], device="cuda", dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    if rank == 0:
+        print("ZSLAB " + json.dumps({
+            "value": ncell * args.steps / (ms * 1e-3), "ms_per_step": ms / args.steps,
+            "pcg_iterations": [r.pcg.iterations for r in reps], "slabs": world,
+            "planes_per_slab": [w.k_hi - w.k_lo for w in sol.windows], "halo": DEFAULT_HALO,
+            "path": "slabs.DistSlabSolver: NCCL halo exchange, one cooperative PCG launch per GPU with "
+                    "boundary planes stored into the neighbours over NVLink (CUDA IPC) and a cross-GPU barrier"}),
+              flush=True)
+    dist.destroy_process_group()
+
+
+def zslab_leg(args, dist, rank):
+    """One C3 simulation split into z-slabs, one per GPU, timed in
+    a child process per rank (device events, max over ranks).  Returns
+    (ok on every rank, result dict)."""
+    import subprocess
+    import torch
+    env = dict(os.environ)
+    env["MASTER_PORT"] = str(int(os.environ.get("MASTER_PORT", "29500")) + 11)
+    cmd = [sys.executable, os.path.abspath(__file__), "--zslab-child", "--steps", str(args.steps),
+           "--warmup", str(args.warmup), "--dt", str(args.dt)]
     res, ok = {}, 1.0
     try:
-        state = comp.make_state()
-        sol = DistSlabSolver(state, sc.solver, sc.inlet, omega=sc.ai_omega, pcg_tol=sc.pcg_tol)
-        del state
-        sol.step_many(args.warmup)
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        dist.barrier()
-        torch.cuda.synchronize()
-        e0.record()
-        reps = sol.step_many(args.steps)
-        e1.record()
-        torch.cuda.synchronize()
-        ms = e0.elapsed_time(e1)
-        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
-        res = {"value": ncell * args.steps / (ms * 1e-3), "ms_per_step": ms / args.steps,
-               "pcg_iterations": [r.pcg.iterations for r in reps], "slabs": world,
-               "planes_per_slab": [b.k_hi - b.k_lo for b in sol.windows], "halo": DEFAULT_HALO,
-               "path": "slabs.DistSlabSolver: NCCL halo exchange, one cooperative PCG launch per GPU with "
-                       "boundary planes stored into the neighbours over NVLink (CUDA IPC) and a cross-GPU barrier"}
+        out = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=900)
+        line = next((ln[6:] for ln in out.stdout.splitlines() if ln.startswith("ZSLAB ")), None)
+        if out.returncode != 0:
+            ok = 0.0
+            res = {"error": f"child exit {out.returncode}: {out.stderr.strip().splitlines()[-1] if out.stderr.strip() else ''}"[:300]}
+        elif rank == 0:
+            res = json.loads(line)
     except Exception as e:   # reported, and the design-per-GPU number stands
         ok = 0.0
         res = {"error": f"{type(e).__name__}: {e}"[:300]}
@@ -401,7 +435,7 @@ def run_b200(args):
     # N > 1: the same C3 simulation split into z-slabs over the GPUs
     zslab = None
     if dist is not None and not args.no_zslab:
-        zok, zslab = zslab_leg(args, comp, sc, dist, world, ncell)
+        zok, zslab = zslab_leg(args, dist, rank)
         zslab["ok"] = zok
 
     # seconds per design evaluation (C4 recipe on the C3 city: 16 extent
@@ -479,11 +513,14 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-design", action="store_true")
     ap.add_argument("--no-zslab", action="store_true", help="N > 1: skip the z-slab leg (design-per-GPU only)")
+    ap.add_argument("--zslab-child", action="store_true", help=argparse.SUPPRESS)
     ap.add_argument("--settle", type=int, default=120)
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
-    if args.impl == "reference":
+    if args.zslab_child:
+        zslab_child(args)
+    elif args.impl == "reference":
         run_reference(args)
     else:
         run_b200(args)
