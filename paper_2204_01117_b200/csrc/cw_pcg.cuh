@@ -389,15 +389,29 @@ __device__ void phase0(const PcgArgs<T>& A, double* part, int unit, PcgShared<T>
   const int i = t.i0 + lx;
   const long long plane = (long long)d.nx * d.ny;
   const long long pplane = (long long)A.nxp * d.ny;
+  // x0 = state p on the unknowns, 0 elsewhere and outside the grid: the code
+  // byte and p are loaded independently (clamped address), then selected
   auto xval = [&](int kk, int gi, int gj) -> T {
-    if (kk < 0 || kk >= d.nz || gi < 0 || gi >= d.nx || gj < 0 || gj >= d.ny) return (T)0;
-    if (!(A.code[kk * pplane + (long long)gj * A.nxp + gi] & 64)) return (T)0;
-    return A.state_p[kk * plane + (long long)gj * d.nx + gi];
+    const bool in = kk >= 0 && kk < d.nz && gi >= 0 && gi < d.nx && gj >= 0 && gj < d.ny;
+    const int ck = in ? kk : 0, ci = in ? gi : 0, cj = in ? gj : 0;
+    const uint8_t cd = __ldg(A.code + (ck * pplane + (long long)cj * A.nxp + ci));
+    const T pv = __ldg(A.state_p + (ck * plane + (long long)cj * d.nx + ci));
+    return (in && (cd & 64)) ? pv : (T)0;
   };
-  auto load = [&](int kk, int b) {
-    for (int e = threadIdx.x; e < HH * HW; e += PCG_THREADS) {
-      const int hx = e % HW, hy = e / HW;
-      S.pa[b][hy][hx] = xval(kk, t.i0 + hx - 1, t.j0 + hy - 1);
+  constexpr int NL = (HH * HW + PCG_THREADS - 1) / PCG_THREADS;   // halo elements per thread
+  T nxt[NL];
+  auto fetch = [&](int kk) {   // plane kk's halo tile into registers
+#pragma unroll
+    for (int m = 0; m < NL; ++m) {
+      const int e = threadIdx.x + m * PCG_THREADS;
+      nxt[m] = e < HH * HW ? xval(kk, t.i0 + e % HW - 1, t.j0 + e / HW - 1) : (T)0;
+    }
+  };
+  auto store = [&](int b) {
+#pragma unroll
+    for (int m = 0; m < NL; ++m) {
+      const int e = threadIdx.x + m * PCG_THREADS;
+      if (e < HH * HW) S.pa[b][e / HW][e % HW] = nxt[m];
     }
   };
   double b2 = 0.0, bmax = 0.0, dmax = 0.0;
@@ -405,17 +419,20 @@ __device__ void phase0(const PcgArgs<T>& A, double* part, int unit, PcgShared<T>
 #pragma unroll
   for (int q = 0; q < PCG_RPT; ++q) pm[q] = xval(t.k0 - 1, i, t.j0 + ly0 + q * PCG_RSTEP);
   int bc = 0, bn = 1;
-  load(t.k0, bc);
+  fetch(t.k0);
+  store(bc);
+  fetch(t.k0 + 1);
+  store(bn);
+  __syncthreads();
   for (int k = t.k0; k < t.k1; ++k) {
-    load(k + 1, bn);
-    __syncthreads();
+    if (k + 2 <= t.k1) fetch(k + 2);   // in flight while plane k is computed
 #pragma unroll
     for (int q = 0; q < PCG_RPT; ++q) {
       const int ly = ly0 + q * PCG_RSTEP, j = t.j0 + ly;
       if (i >= d.nx || j >= d.ny) continue;
       const long long c = k * plane + (long long)j * d.nx + i;
       const long long pc_ = k * pplane + (long long)j * A.nxp + i;
-      const uint8_t cd = A.code[pc_];
+      const uint8_t cd = __ldg(A.code + pc_);
       const T pc = S.pa[bc][ly + 1][lx + 1];
       const T pn = S.pa[bn][ly + 1][lx + 1];
       if (cd & 64) {
@@ -443,6 +460,8 @@ __device__ void phase0(const PcgArgs<T>& A, double* part, int unit, PcgShared<T>
       }
       pm[q] = pc;
     }
+    __syncthreads();             // plane k's tile is consumed: plane k+2 takes its buffer
+    if (k + 2 <= t.k1) store(bc);
     __syncthreads();
     const int tmp = bc; bc = bn; bn = tmp;
   }
