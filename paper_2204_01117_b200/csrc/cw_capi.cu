@@ -330,9 +330,15 @@ extern "C" void cw_ctx_destroy(cw_ctx* c) {
 
 static inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 static inline dim3 g3(int ex, int ey, int ez) {   // 3-D stage-kernel grid (cw_step.cuh CW_IJK)
-  return dim3((unsigned)((ex + ST_BX - 1) / ST_BX), (unsigned)((ey + ST_BY - 1) / ST_BY), (unsigned)ez);
+  return dim3((unsigned)((ex + ST_BX - 1) / ST_BX), (unsigned)((ey + ST_BY - 1) / ST_BY),
+              (unsigned)((ez + ST_BZ - 1) / ST_BZ));
 }
-static const dim3 B3(ST_BX, ST_BY);
+static const dim3 B3(ST_BX, ST_BY, ST_BZ);
+// owned-plane reductions (CW_IJK_OWN): one plane per block
+static inline dim3 g3r(int ex, int ey, int nz) {
+  return dim3((unsigned)((ex + ST_BX - 1) / ST_BX), (unsigned)((ey + 7) / 8), (unsigned)nz);
+}
+static const dim3 B3R(ST_BX, 8, 1);
 static inline dim3 g3c(const Dims& d, int comp) {
   int ex, ey, ez;
   comp_extent(d, comp, ex, ey, ez);
@@ -661,7 +667,7 @@ static void st_project_tail(cw_ctx* c, const StepPtrs<T>& P, const cw_params* pr
   T* cu[3] = {P.u, P.v, P.w};
   for (int a = 0; a < (d.is2d ? 2 : 3); ++a)
     (k_gradient<T><<<g3c(d, a), B3, 0, st>>>(d, a, cu[a], P.p, P.lab, (T)prm->dt, c->gate), ++c->launches);
-  (k_div_max<T><<<g3(d.nx, d.ny, d.o1 - d.o0), B3, 0, st>>>(d, P.u, P.v, P.w, P.lab, rep, SLOT_DIV_AFTER, c->gate), ++c->launches);
+  (k_div_max<T><<<g3r(d.nx, d.ny, d.o1 - d.o0), B3R, 0, st>>>(d, P.u, P.v, P.w, P.lab, rep, SLOT_DIV_AFTER, c->gate), ++c->launches);
 }
 
 template <typename T>
@@ -714,7 +720,7 @@ static int enqueue_step(cw_ctx* c, const cw_fields* f, const cw_params* prm, dou
   mark(6);
   BcFields<T> F2{P.u, P.v, P.w, P.p, P.k, P.om, P.nut};
   launch_bc<T>(c, F2, P.lab, prm, st);                        // "boundary2"
-  (k_speed_max<T><<<g3(c->d.nx + 1, c->d.ny + 1, c->d.o1 - c->d.o0 + 1), B3, 0, st>>>(c->d, P.u, P.v, P.w, rep, c->gate),
+  (k_speed_max<T><<<g3r(c->d.nx + 1, c->d.ny + 1, c->d.o1 - c->d.o0 + 1), B3R, 0, st>>>(c->d, P.u, P.v, P.w, rep, c->gate),
    ++c->launches);
   mark(7);
   CW_CUDA(cudaGetLastError());
@@ -786,7 +792,7 @@ static int enqueue_stage(cw_ctx* c, const cw_fields* f, const cw_params* prm, in
       if (prm->turbulence) st_turb<T>(c, P, prm, (const T*)c->tk, (const T*)c->tw, rep, st);
       BcFields<T> F2{P.u, P.v, P.w, P.p, P.k, P.om, P.nut};
       launch_bc<T>(c, F2, P.lab, prm, st);
-      (k_speed_max<T><<<g3(d.nx + 1, d.ny + 1, d.o1 - d.o0 + 1), B3, 0, st>>>(d, P.u, P.v, P.w, rep, c->gate),
+      (k_speed_max<T><<<g3r(d.nx + 1, d.ny + 1, d.o1 - d.o0 + 1), B3R, 0, st>>>(d, P.u, P.v, P.w, rep, c->gate),
        ++c->launches);
       break;
     }

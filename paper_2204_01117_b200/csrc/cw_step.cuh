@@ -41,16 +41,23 @@ template <> __device__ __forceinline__ void report_max<double>(DevReport* r, int
 // Stage kernels run on a 3-D grid: blockDim (32, 8), grid (ceil(ex/32),
 // ceil(ey/8), ez) -- the element's (i, j, k) come from the launch, no
 // per-element 64-bit division.
-constexpr int ST_BX = 32, ST_BY = 8;
+#ifndef CW_ST_BY
+#define CW_ST_BY 8
+#endif
+#ifndef CW_ST_BZ
+#define CW_ST_BZ 1
+#endif
+// blocks span ST_BZ planes so that z-neighbour reads hit the block's own L1
+constexpr int ST_BX = 32, ST_BY = CW_ST_BY, ST_BZ = CW_ST_BZ;
 #define CW_IJK(ex, ey, ez, inb)                                  \
   const int i = (int)(blockIdx.x * ST_BX + threadIdx.x);         \
   const int j = (int)(blockIdx.y * ST_BY + threadIdx.y);         \
-  const int k = (int)blockIdx.z;                                 \
+  const int k = (int)(blockIdx.z * ST_BZ + threadIdx.z);         \
   const bool inb = i < (ex) && j < (ey) && k < (ez)
 // the same over the owned planes of a z-slab window only (grid z = o1 - o0 [+1])
 #define CW_IJK_OWN(ex, ey, kend, inb)                            \
   const int i = (int)(blockIdx.x * ST_BX + threadIdx.x);         \
-  const int j = (int)(blockIdx.y * ST_BY + threadIdx.y);         \
+  const int j = (int)(blockIdx.y * 8 + threadIdx.y);             \
   const int k = d.o0 + (int)blockIdx.z;                          \
   const bool inb = i < (ex) && j < (ey) && k < (kend)
 
