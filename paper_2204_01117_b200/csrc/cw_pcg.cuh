@@ -478,6 +478,45 @@ __device__ void phase0(const PcgArgs<T>& A, double* part, int unit, PcgShared<T>
   __syncthreads();
 }
 
+// A p' per cell.  float32 state: the difference form sum_a w_a (p_i - p_a)
+// over the neighbours a that are unknowns or outlets (p_a = 0 at an outlet).
+// The 7-point combination of a smooth p cancels d*p almost entirely, so the
+// direct form d*p - sum w p_a needs float64; in the difference form the
+// cancellation happens inside the differences, which are exact in float32
+// when neighbours are within a factor of two (Sterbenz) and otherwise carry
+// no cancellation, so float32 arithmetic keeps ~eps*|A p| accuracy.  float64
+// state: the direct form in float64.  The +z term is added once the next
+// plane lands (ap_finish).
+template <typename T> struct ApAccT { typedef double type; };
+template <> struct ApAccT<float> { typedef float type; };
+template <typename T> using ApAcc = typename ApAccT<T>::type;
+
+template <typename T>
+__device__ __forceinline__ ApAcc<T> ap_partial(uint8_t cd, T d, T pc, T pxp, T pxm, T pyp, T pym, T pzm, T wx, T wy,
+                                               T wz) {
+  if constexpr (sizeof(T) == 4) {
+    float a = 0.f;
+    if (cd & 1) a += wx * (pc - pxp);
+    if (cd & 2) a += wx * (pc - pxm);
+    if (cd & 4) a += wy * (pc - pyp);
+    if (cd & 8) a += wy * (pc - pym);
+    if (cd & 32) a += wz * (pc - pzm);
+    return a;
+  } else {
+    return (double)d * (double)pc - ((double)wx * ((double)pxm + (double)pxp) +
+                                     (double)wy * ((double)pym + (double)pyp) + (double)wz * (double)pzm);
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ double ap_finish(ApAcc<T> part, T wz, T pc, T pzp, bool zp) {
+  if constexpr (sizeof(T) == 4) {
+    return (double)(zp ? part + wz * (pc - pzp) : part);
+  } else {
+    return part - (double)wz * (double)pzp;
+  }
+}
+
 // ---- phase A: p' = z + beta p, x += alpha_prev p, Ap = A p' ---------------
 template <typename T, bool SLABS>
 __device__ void phaseA(const PcgArgs<T>& A, const Blk& blk, double* part, PcgShared<T>& S, uint8_t* ring,
@@ -514,7 +553,8 @@ __device__ void phaseA(const PcgArgs<T>& A, const Blk& blk, double* part, PcgSha
     // per own row: the previous plane's p', and plane kk-1's pending result
     // (A p without its +z term, new x, own flag) finished once plane kk lands
     T pm[PCG_RPT], pcur[PCG_RPT], xn[PCG_RPT];
-    double part_ap[PCG_RPT];
+    bool pzb[PCG_RPT];       // the +z neighbour is an unknown or an outlet
+    ApAcc<T> part_ap[PCG_RPT];
     bool pend[PCG_RPT];
 #pragma unroll
     for (int q = 0; q < PCG_RPT; ++q) { pm[q] = (T)0; pend[q] = false; }
@@ -547,12 +587,9 @@ __device__ void phaseA(const PcgArgs<T>& A, const Blk& blk, double* part, PcgSha
         const int ly = ly0 + q * PCG_RSTEP, jj = u.j0 + ly;
         const T pn = pnew(st, ly + 1, lx + 1);     // own p' on plane kk
         if (pend[q]) {
-          // finish plane kk-1: add the +z neighbour (this plane) and store.
-          // A p is accumulated in float64 from the stored p: the 7-point
-          // difference of a smooth p cancels d*p almost entirely, so float32
-          // arithmetic would leave a relative error ~eps*d|p|/|Ap|
+          // finish plane kk-1: add the +z neighbour (this plane) and store
           const long long pc_ = (long long)(kk - 1) * pplane + (long long)jj * A.nxp + i;
-          const double ap = part_ap[q] - (double)A.wz * (double)pn;
+          const double ap = ap_finish<T>(part_ap[q], A.wz, pcur[q], pn, pzb[q]);
           pout[pc_] = pcur[q];
           A.Ap[pc_] = (T)ap;
           if (upd_x) A.x[pc_] = xn[q];
@@ -573,10 +610,10 @@ __device__ void phaseA(const PcgArgs<T>& A, const Blk& blk, double* part, PcgSha
         if (kk >= u.k0 && kk < u.k1) {
           const uint8_t cd = cc[ly * PCG_TX + lx];
           if ((cd & 64) && i < d.nx && jj < d.ny) {
-            part_ap[q] = (double)S.lut[(cd & 63) * 4] * (double)pn -
-                         ((double)A.wx * ((double)pnew(st, ly + 1, lx) + (double)pnew(st, ly + 1, lx + 2)) +
-                          (double)A.wy * ((double)pnew(st, ly, lx + 1) + (double)pnew(st, ly + 2, lx + 1)) +
-                          (double)A.wz * (double)pm[q]);
+            part_ap[q] = ap_partial<T>(cd, S.lut[(cd & 63) * 4], pn, pnew(st, ly + 1, lx + 2),
+                                       pnew(st, ly + 1, lx), pnew(st, ly + 2, lx + 1), pnew(st, ly, lx + 1),
+                                       pm[q], A.wx, A.wy, A.wz);
+            pzb[q] = (cd >> 4) & 1;
             pcur[q] = pn;
             if (upd_x) xn[q] = xx[ly * PCG_TX + lx] + alpha_prev * pp[Halo<T>::at(ly + 1, lx + 1)];
             pend[q] = true;
