@@ -914,3 +914,35 @@ def trace_streamlines(state, seeds, step_len, max_steps=2000, min_speed=1e-6):
             pts.append(p.copy())
         out.append(np.array(pts))
     return out
+
+
+def gradient_descent(compiled, theta0, lo, hi, lam=1.0, eps=0.1, max_iter=30, rel_tol=1e-3):
+    """optimize.py:112-192: forward differences (+eps, or -eps past the upper
+    bound), theta <- clamp(theta - lam * grad), stop after 3 consecutive
+    relative loss changes below rel_tol.  Returns (thetas, losses)."""
+    lo, hi = np.asarray(lo, float), np.asarray(hi, float)
+    theta = np.clip(np.asarray(theta0, float), lo, hi)
+    base = evaluate_objective(compiled, theta)[0]
+    history, thetas = [base], [theta.copy()]
+    stable = 0
+    for _ in range(max_iter):
+        grad = np.zeros_like(theta)
+        for i in range(len(theta)):
+            h = eps if theta[i] + eps <= hi[i] else -eps
+            t = theta.copy()
+            t[i] += h
+            grad[i] = (evaluate_objective(compiled, t)[0] - base) / h
+        theta = np.clip(theta - lam * grad, lo, hi)
+        base = evaluate_objective(compiled, theta)[0]
+        if not math.isfinite(base):
+            break
+        rel = abs(history[-1] - base) / max(history[-1], 1e-12)
+        history.append(base)
+        thetas.append(theta.copy())
+        if rel < rel_tol:
+            stable += 1
+            if stable >= 3:
+                break
+        else:
+            stable = 0
+    return thetas, history

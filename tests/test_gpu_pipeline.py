@@ -108,3 +108,24 @@ def test_snapshot_format_matches_oracle_layout(tmp_path):
     snap = read_snapshot(path)
     for n in ("u", "v", "w", "k"):
         np.testing.assert_array_equal(snap.arrays[n], getattr(ost, n).astype(np.float32).transpose(2, 1, 0))
+
+
+def test_gradient_descent_trajectory_matches_oracle():
+    """optimize.gradient_descent on the device against the oracle's
+    restatement (optimize.py:112-192): the same theta after two iterations
+    (north_star: optimized design parameters within 1e-4)."""
+    from oracle import citywind_oracle as co
+    from paper_2204_01117_b200.optimize import DesignVector, gradient_descent
+    from paper_2204_01117_b200.scenario import CompiledScenario, scenario_from_dict
+    doc = _design_doc()
+    sc = scenario_from_dict(doc)
+    comp = CompiledScenario.compile(sc)
+    res = gradient_descent(comp, eps=0.5, max_iter=2, lam=2.0)
+    design = DesignVector.from_scenario(sc)
+    thetas, losses = co.gradient_descent(oracle_compiled(doc), design.values, design.lo, design.hi,
+                                         lam=2.0, eps=0.5, max_iter=2)
+    assert len(res.theta_history) == len(thetas) == 3
+    for a, b in zip(res.theta_history, thetas):
+        np.testing.assert_allclose(a, b, rtol=1e-4, atol=1e-4 * max(1.0, float(np.abs(b).max())))
+    np.testing.assert_allclose(res.history, losses, rtol=1e-4)
+    assert not np.allclose(thetas[0], thetas[-1])      # the design moved
