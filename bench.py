@@ -33,10 +33,18 @@ PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
 # algorithmic bytes: per step 164*N + 44*I*Nu (+8*Nu); the PCG
 # launch moves 20*N (divergence -> r0) + 8*Nu (z0 = W r0) + 44*I*Nu
 PCG_B_PER_UNKNOWN_ITER = 44
-# mean PCG iterations per step of the C3 scene over steps 3..12 (device run,
-# equal to the reference's counts by the parity gates) -- used only to
-# extrapolate the CPU reference's bounded samples to a full step
-REF_ITERS_PER_STEP = 143.0
+# PCG iterations of C3 steps 1..60 at dt 0.2 (device run; the parity gates
+# hold the device's per-step counts equal to the reference's) -- used only to
+# extrapolate the CPU reference's bounded samples to the same steps the B200
+# arm times (steps warmup+1 .. warmup+steps)
+C3_ITERS = [264, 265, 249, 231, 202, 183, 170, 147, 132, 115, 106, 100, 96, 91, 87, 85, 83, 84, 83, 84,
+            83, 84, 84, 85, 84, 85, 84, 85, 84, 85, 84, 85, 84, 85, 84, 85, 84, 85, 85, 85,
+            85, 86, 85, 85, 85, 86, 85, 86, 85, 86, 86, 85, 86, 85, 86, 85, 86, 86, 85, 85]
+
+
+def ref_iters_per_step(warmup, steps):
+    seq = C3_ITERS + [C3_ITERS[-1]] * max(0, warmup + steps - len(C3_ITERS))
+    return float(np.mean(seq[warmup:warmup + steps]))
 
 
 def c3_doc(dt):
@@ -197,10 +205,10 @@ class OracleSampler:
             rz = rz_new
         return (time.perf_counter() - t0) / m
 
-    def sample(self, m=8):
+    def sample(self, m=8, iters_per_step=None):
         ts = self.stages()
         ti = self.pcg_iters(m)
-        step_s = ts + ti * REF_ITERS_PER_STEP
+        step_s = ts + ti * (iters_per_step if iters_per_step is not None else float(np.mean(C3_ITERS[3:23])))
         return self.n / step_s, ts, ti
 
 
@@ -214,12 +222,13 @@ def run_reference(args):
         return
     doc = c3_doc(args.dt)
     smp = OracleSampler(doc)
+    ips = ref_iters_per_step(args.warmup, args.steps)
     for _ in range(args.warmup):
-        smp.sample(4)
+        smp.sample(4, ips)
     vals, tstage, titer = [], [], []
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        v, ts, ti = smp.sample(4)
+        v, ts, ti = smp.sample(4, ips)
         vals.append(v)
         tstage.append(ts)
         titer.append(ti)
@@ -228,7 +237,8 @@ def run_reference(args):
     cores = cpu_threads()
     sample = (f"per step: the C3 step's non-projection stages on the full 256x256x64 grid "
               f"(mean {np.mean(tstage):.2f} s) + 4 PCG iterations (mean {np.mean(titer):.3f} s/iteration), "
-              f"extrapolated to {REF_ITERS_PER_STEP} iterations/step; oracle/ numpy+scipy port, "
+              f"extrapolated to {ips:.1f} iterations/step (the mean of C3 steps {args.warmup + 1}-"
+              f"{args.warmup + args.steps}, the steps the B200 arm times); oracle/ numpy+scipy port, "
               f"OpenBLAS ddot on {cores} threads, CSR matvec single-threaded")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * doc_cells(doc) / value,
