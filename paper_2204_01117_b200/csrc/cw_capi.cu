@@ -625,9 +625,9 @@ static void st_diffuse(cw_ctx* c, const StepPtrs<T>& P, const cw_params* prm, cu
   T* cu[3] = {P.u, P.v, P.w};
   double cap = nu_stable<T>(c, prm->dt) - prm->nu;
   if (cap <= 0) cap = 0.0;                               // solver.py:195-201
-  for (int a = 0; a < (d.is2d ? 2 : 3); ++a)
-    (k_diffuse<T><<<g3c(d, a), B3, 0, st>>>(d, a, (const T*)c->adv[a], cu[a], P.nut, (T)prm->dt,
-                                               (T)prm->nu, (T)cap, c->gate), ++c->launches);
+  (k_diffuse<T><<<g3(d.nx + 1, d.ny + 1, d.nz + 1), B3, 0, st>>>(
+       d, (const T*)c->adv[0], (const T*)c->adv[1], (const T*)c->adv[2], cu[0], cu[1], cu[2], P.nut, (T)prm->dt,
+       (T)prm->nu, (T)cap, c->gate), ++c->launches);
 }
 
 template <typename T>
@@ -637,8 +637,8 @@ static void st_drag(cw_ctx* c, const StepPtrs<T>& P, const cw_params* prm, int h
   const long long nf[3] = {c->nu_, c->nv_, c->nw_};
   T* cu[3] = {P.u, P.v, P.w};
   (k_cell_speed<T><<<g3(d.nx, d.ny, d.nz), B3, 0, st>>>(d, P.u, P.v, P.w, (T*)c->speed, c->gate), ++c->launches);
-  for (int a = 0; a < (d.is2d ? 2 : 3); ++a)
-    (k_drag<T><<<g3c(d, a), B3, 0, st>>>(d, a, cu[a], P.g, (const T*)c->speed, (T)prm->dt, c->gate), ++c->launches);
+  (k_drag<T><<<g3(d.nx + 1, d.ny + 1, d.nz + 1), B3, 0, st>>>(d, cu[0], cu[1], cu[2], P.g, (const T*)c->speed,
+                                                                (T)prm->dt, c->gate), ++c->launches);
 }
 
 template <typename T>
@@ -665,8 +665,8 @@ template <typename T>
 static void st_project_tail(cw_ctx* c, const StepPtrs<T>& P, const cw_params* prm, DevReport* rep, cudaStream_t st) {
   const Dims& d = c->d;
   T* cu[3] = {P.u, P.v, P.w};
-  for (int a = 0; a < (d.is2d ? 2 : 3); ++a)
-    (k_gradient<T><<<g3c(d, a), B3, 0, st>>>(d, a, cu[a], P.p, P.lab, (T)prm->dt, c->gate), ++c->launches);
+  (k_gradient<T><<<g3(d.nx + 1, d.ny + 1, d.nz + 1), B3, 0, st>>>(d, cu[0], cu[1], cu[2], P.p, P.lab, (T)prm->dt,
+                                                                    c->gate), ++c->launches);
   (k_div_max<T><<<g3r(d.nx, d.ny, d.o1 - d.o0), B3R, 0, st>>>(d, P.u, P.v, P.w, P.lab, rep, SLOT_DIV_AFTER, c->gate), ++c->launches);
 }
 

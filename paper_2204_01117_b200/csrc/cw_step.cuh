@@ -211,16 +211,15 @@ __device__ __forceinline__ T nu_eff(const T* nut, int c, T nu, T cap) {
 }
 
 template <typename T>
-__global__ void k_diffuse(Dims d, int comp, const T* __restrict__ src, T* __restrict__ dst,
-                          const T* __restrict__ nut, T dt, T nu, T cap, const int* gate) {
-  if (*gate) return;
+__device__ __forceinline__ void diffuse_face(const Dims& d, int comp, const T* __restrict__ src,
+                                             T* __restrict__ dst, const T* __restrict__ nut, T dt, T nu, T cap,
+                                             int i, int j, int k) {
   int ex, ey, ez;
   comp_extent(d, comp, ex, ey, ez);
   const int ext[3] = {ex, ey, ez};
   const int str[3] = {1, ex, (int)ex * ey};
   const T h[3] = {(T)d.dx, (T)d.dy, (T)d.dz};
-  CW_IJK(ex, ey, ez, inb);
-  if (inb) {
+  if (i < ex && j < ey && k < ez) {
     const int c = ((int)k * ey + j) * ex + i;
     const int pos[3] = {i, j, k};
     const T mid = src[c];
@@ -244,6 +243,19 @@ __global__ void k_diffuse(Dims d, int comp, const T* __restrict__ src, T* __rest
   }
 }
 
+// all components in one launch over the union of the face extents
+template <typename T>
+__global__ void k_diffuse(Dims d, const T* __restrict__ s0, const T* __restrict__ s1, const T* __restrict__ s2,
+                          T* __restrict__ d0, T* __restrict__ d1, T* __restrict__ d2, const T* __restrict__ nut,
+                          T dt, T nu, T cap, const int* gate) {
+  if (*gate) return;
+  CW_IJK(d.nx + 1, d.ny + 1, d.nz + 1, inb);
+  if (!inb) return;
+  diffuse_face<T>(d, 0, s0, d0, nut, dt, nu, cap, i, j, k);
+  diffuse_face<T>(d, 1, s1, d1, nut, dt, nu, cap, i, j, k);
+  if (!d.is2d) diffuse_face<T>(d, 2, s2, d2, nut, dt, nu, cap, i, j, k);
+}
+
 // ---------------------------------------------------------------------------
 // porosity drag (solver.py:123-168)
 template <typename T>
@@ -263,14 +275,12 @@ __global__ void k_cell_speed(Dims d, const T* __restrict__ u, const T* __restric
 }
 
 template <typename T>
-__global__ void k_drag(Dims d, int comp, T* __restrict__ arr, const T* __restrict__ g,
-                       const T* __restrict__ speed, T dt, const int* gate) {
-  if (*gate) return;
+__device__ __forceinline__ void drag_face(const Dims& d, int comp, T* __restrict__ arr, const T* __restrict__ g,
+                                          const T* __restrict__ speed, T dt, int i, int j, int k) {
   int ex, ey, ez;
   comp_extent(d, comp, ex, ey, ez);
   const int nc = comp == 0 ? d.nx : (comp == 1 ? d.ny : d.nz);
-  CW_IJK(ex, ey, ez, inb);
-  if (inb) {
+  if (i < ex && j < ey && k < ez) {
     const int c = ((int)k * ey + j) * ex + i;
     int p[3] = {i, j, k};
     const int f = p[comp];
@@ -284,6 +294,17 @@ __global__ void k_drag(Dims d, int comp, T* __restrict__ arr, const T* __restric
     fac = fac > (T)0 ? fac : (T)0;
     arr[c] *= fac;
   }
+}
+
+template <typename T>
+__global__ void k_drag(Dims d, T* __restrict__ u, T* __restrict__ v, T* __restrict__ w, const T* __restrict__ g,
+                       const T* __restrict__ speed, T dt, const int* gate) {
+  if (*gate) return;
+  CW_IJK(d.nx + 1, d.ny + 1, d.nz + 1, inb);
+  if (!inb) return;
+  drag_face<T>(d, 0, u, g, speed, dt, i, j, k);
+  drag_face<T>(d, 1, v, g, speed, dt, i, j, k);
+  if (!d.is2d) drag_face<T>(d, 2, w, g, speed, dt, i, j, k);
 }
 
 // ---------------------------------------------------------------------------
@@ -398,15 +419,13 @@ __global__ void k_bc_inlet_wall(Dims d, BcFields<T> F, const int8_t* __restrict_
 // ---------------------------------------------------------------------------
 // pressure-gradient update (solver.py:282-303)
 template <typename T>
-__global__ void k_gradient(Dims d, int comp, T* __restrict__ arr, const T* __restrict__ p,
-                           const int8_t* __restrict__ lab, T dt, const int* gate) {
-  if (*gate) return;
+__device__ __forceinline__ void gradient_face(const Dims& d, int comp, T* __restrict__ arr, const T* __restrict__ p,
+                                              const int8_t* __restrict__ lab, T dt, int i, int j, int k) {
   int ex, ey, ez;
   comp_extent(d, comp, ex, ey, ez);
   const T h = comp == 0 ? (T)d.dx : (comp == 1 ? (T)d.dy : (T)d.dz);
   const int nc = comp == 0 ? d.nx : (comp == 1 ? d.ny : d.nz);
-  CW_IJK(ex, ey, ez, inb);
-  if (inb) {
+  if (i < ex && j < ey && k < ez) {
     const int c = ((int)k * ey + j) * ex + i;
     int q[3] = {i, j, k};
     const int f = q[comp];
@@ -424,6 +443,17 @@ __global__ void k_gradient(Dims d, int comp, T* __restrict__ arr, const T* __res
     else return;
     arr[c] -= dt * grad;
   }
+}
+
+template <typename T>
+__global__ void k_gradient(Dims d, T* __restrict__ u, T* __restrict__ v, T* __restrict__ w, const T* __restrict__ p,
+                           const int8_t* __restrict__ lab, T dt, const int* gate) {
+  if (*gate) return;
+  CW_IJK(d.nx + 1, d.ny + 1, d.nz + 1, inb);
+  if (!inb) return;
+  gradient_face<T>(d, 0, u, p, lab, dt, i, j, k);
+  gradient_face<T>(d, 1, v, p, lab, dt, i, j, k);
+  if (!d.is2d) gradient_face<T>(d, 2, w, p, lab, dt, i, j, k);
 }
 
 // max |div| over unknown cells (solver.py:215-229)
