@@ -606,13 +606,10 @@ template <typename T>
 static void st_advect(cw_ctx* c, const StepPtrs<T>& P, const cw_params* prm, T* kout, T* wout, cudaStream_t st) {
   const Dims& d = c->d;
   const T dt = (T)prm->dt;
-  const long long nf[3] = {c->nu_, c->nv_, c->nw_};
-  const int ncomp = d.is2d ? 2 : 3;
-  if (prm->turbulence)
-    (k_upwind<T><<<g3(d.nx, d.ny, d.nz), B3, 0, st>>>(d, P.u, P.v, P.w, P.k, P.om, kout, wout, dt, c->gate), ++c->launches);
-  (void)ncomp;
+  const bool turb = prm->turbulence != 0;    // upwind k, omega ride along in the predictor launch
   (k_mac_predict<T><<<g3(d.nx + 1, d.ny + 1, d.nz + 1), B3, 0, st>>>(
-       d, P.u, P.v, P.w, (T*)c->ahead[0], (T*)c->ahead[1], (T*)c->ahead[2], dt, c->gate), ++c->launches);
+       d, P.u, P.v, P.w, (T*)c->ahead[0], (T*)c->ahead[1], (T*)c->ahead[2], dt, (const T*)P.k, (const T*)P.om,
+       turb ? kout : (T*)nullptr, turb ? wout : (T*)nullptr, c->gate), ++c->launches);
   (k_mac_correct<T><<<g3(d.nx + 1, d.ny + 1, d.nz + 1), B3, 0, st>>>(
        d, P.u, P.v, P.w, (const T*)c->ahead[0], (const T*)c->ahead[1], (const T*)c->ahead[2], (T*)c->adv[0],
        (T*)c->adv[1], (T*)c->adv[2], dt, c->gate), ++c->launches);

@@ -66,13 +66,11 @@ __device__ __forceinline__ int clampi(int a, int lo, int hi) { return a < lo ? l
 // ---------------------------------------------------------------------------
 // upwind k and omega (advection.py:154-173), old velocity, axes x,y,z in turn
 template <typename T>
-__global__ void k_upwind(Dims d, const T* __restrict__ u, const T* __restrict__ v,
-                         const T* __restrict__ w, const T* __restrict__ kin,
-                         const T* __restrict__ win, T* __restrict__ kout, T* __restrict__ wout,
-                         T dt, const int* gate) {
-  if (*gate) return;
-  CW_IJK(d.nx, d.ny, d.nz, inb);
-  if (inb) {
+__device__ __forceinline__ void upwind_cell(const Dims& d, const T* __restrict__ u, const T* __restrict__ v,
+                                            const T* __restrict__ w, const T* __restrict__ kin,
+                                            const T* __restrict__ win, T* __restrict__ kout, T* __restrict__ wout,
+                                            T dt, int i, int j, int k) {
+  if (i < d.nx && j < d.ny && k < d.nz) {
     const int c = d.cidx32(i, j, k);
     T a[3];
     a[0] = (T)0.5 * (u[((int)k * d.ny + j) * (d.nx + 1) + i] + u[((int)k * d.ny + j) * (d.nx + 1) + i + 1]);
@@ -150,13 +148,17 @@ __device__ __forceinline__ void mac_predict_face(const Dims& d, int comp, const 
   ahead[c] = gather<T>(arr, ex, ey, ez, bx - ox, by - oy, bz - oz, nullptr, nullptr);
 }
 
+// the predictor launch also runs the upwind step of k and omega (cells,
+// advection.py:154-173) when kout != nullptr: both read the old velocity
 template <typename T>
 __global__ void k_mac_predict(Dims d, const T* __restrict__ u, const T* __restrict__ v,
                               const T* __restrict__ w, T* __restrict__ a0, T* __restrict__ a1,
-                              T* __restrict__ a2, T dt, const int* gate) {
+                              T* __restrict__ a2, T dt, const T* __restrict__ kin, const T* __restrict__ win,
+                              T* __restrict__ kout, T* __restrict__ wout, const int* gate) {
   if (*gate) return;
   CW_IJK(d.nx + 1, d.ny + 1, d.nz + 1, inb);
   if (!inb) return;
+  if (kout) upwind_cell<T>(d, u, v, w, kin, win, kout, wout, dt, i, j, k);
   mac_predict_face<T>(d, 0, u, v, w, a0, dt, i, j, k);
   mac_predict_face<T>(d, 1, u, v, w, a1, dt, i, j, k);
   if (!d.is2d) mac_predict_face<T>(d, 2, u, v, w, a2, dt, i, j, k);
