@@ -274,10 +274,13 @@ struct StageLayout {
   static constexpr unsigned BYTES_B = Halo<double>::BYTES + Halo<T>::BYTES + Halo<uint8_t>::BYTES;
 };
 
+// phase-B work planes.  q tile: halo column hx at PCG_QOFF + hx, so the own
+// quads (hx = 1 + 4 tx) start on 16-byte boundaries; y tile: column x at x.
+constexpr int PCG_QOFF = 3, PCG_QW = 40, PCG_YP = 36;
 template <typename T>
-struct PcgWork {          // phase-B work planes
-  T qb[3][HH][HW];        // q = r'/d on the halo tile, planes kk, kk-1 (+1 hazard-free)
-  T yb[2][YH][YW];        // y on the y tile, planes kk and kk-1
+struct PcgWork {
+  alignas(16) T qb[3][HH][PCG_QW];   // q = r'/d on the halo tile, planes kk, kk-1 (+1 hazard-free)
+  alignas(16) T yb[2][YH][PCG_YP];   // y on the y tile, planes kk and kk-1
 };
 
 template <typename T>
@@ -517,16 +520,65 @@ __device__ __forceinline__ double ap_finish(ApAcc<T> part, T wz, T pc, T pzp, bo
   }
 }
 
+// ---------------------------------------------------------------------------
+// Ring phases.  Thread layout: QX = 8 threads across x, each owning an x quad
+// (4 consecutive cells of one row), times 32 rows: one 32 x 32 plane per
+// block sweep.  Own quads move as 128-bit shared and global accesses; the x
+// neighbours come from the adjacent lanes of the row (shuffles), the tile
+// edges from the halo columns, the y neighbours from the rows above and below
+// (128-bit loads), the z neighbours from registers carried through the z march.
+constexpr int QX = PCG_TX / 4;
+static_assert(PCG_THREADS == QX * PCG_TY, "one thread per x quad of a 32 x 32 plane");
+
+__device__ __forceinline__ float fmat(float a, float b, float c) { return __fmaf_rn(a, b, c); }
+__device__ __forceinline__ double fmat(double a, double b, double c) { return __fma_rn(a, b, c); }
+
+template <typename E>
+__device__ __forceinline__ void ld4(const E* p, E (&v)[4]) {   // p: 16-byte aligned
+  if constexpr (sizeof(E) == 4) {
+    const float4 t = *reinterpret_cast<const float4*>(p);
+    v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
+  } else {
+    const double2 a = *reinterpret_cast<const double2*>(p), b = *reinterpret_cast<const double2*>(p + 2);
+    v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
+  }
+}
+template <typename E>
+__device__ __forceinline__ void st4(E* p, const E (&v)[4]) {
+  if constexpr (sizeof(E) == 4) {
+    *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
+  } else {
+    *reinterpret_cast<double2*>(p) = make_double2(v[0], v[1]);
+    *reinterpret_cast<double2*>(p + 2) = make_double2(v[2], v[3]);
+  }
+}
+// the neighbouring lane of the same 8-lane row (a lane at the row's end gets its own value)
+template <typename E>
+__device__ __forceinline__ E from_left(E v) { return __shfl_up_sync(0xffffffffu, v, 1, QX); }
+template <typename E>
+__device__ __forceinline__ E from_right(E v) { return __shfl_down_sync(0xffffffffu, v, 1, QX); }
+
+template <typename T>
+__device__ __forceinline__ T lut_at(const T* lut, unsigned cd, int which) { return lut[(cd & 63u) * 4 + which]; }
+
+// y = s (r' + w sum_a w_a q_{i-e_a}) with s r' = (2-w) w q
+template <typename T>
+__device__ __forceinline__ T y_of(T c0, T q, T s, T om, T wx, T qxm, T wy, T qym, T wz, T qzm) {
+  return c0 * q + s * (om * (wx * qxm + wy * qym + wz * qzm));
+}
+
 // ---- phase A: p' = z + beta p, x += alpha_prev p, Ap = A p' ---------------
 template <typename T, bool SLABS>
 __device__ void phaseA(const PcgArgs<T>& A, const Blk& blk, double* part, PcgShared<T>& S, uint8_t* ring,
                        unsigned& ticket, bool first, T beta, bool upd_x, T alpha_prev, int pin_sel) {
   using L = StageLayout<T>;
+  using H = Halo<T>;
   static_assert(L::DEPTH >= 3, "phase A holds two stages");
   const Dims& d = A.d;
   const CUtensorMap* tp = pin_sel == 0 ? &A.tm_p0 : &A.tm_p1;
   T* __restrict__ pout = pin_sel == 0 ? A.p1 : A.p0;
-  const int lx = threadIdx.x % PCG_TX, ly0 = threadIdx.x / PCG_TX;
+  const int tx = threadIdx.x % QX, ty = threadIdx.x / QX;
+  const int hy = ty + 1, hx0 = 1 + 4 * tx;     // halo coordinates of this thread's first cell
   const long long pplane = (long long)A.nxp * d.ny;
   JobCursor prod, cons;
   double acc = 0.0;
@@ -542,22 +594,15 @@ __device__ void phaseA(const PcgArgs<T>& A, const Blk& blk, double* part, PcgSha
         more = cursor_next<T>(A, prod);
       }
     }
-    auto pnew = [&](const uint8_t* st, int hy, int hx) -> T {
-      const T* zz = reinterpret_cast<const T*>(st + L::A_Z);
-      const T* pp = reinterpret_cast<const T*>(st + L::A_P);
-      const int o = Halo<T>::at(hy, hx);
-      const T zv = zz[o];
-      return first ? zv : zv + beta * pp[o];
-    };
     unsigned j = 0;     // consumer job number in this phase
-    // per own row: the previous plane's p', and plane kk-1's pending result
-    // (A p without its +z term, new x, own flag) finished once plane kk lands
-    T pm[PCG_RPT], pcur[PCG_RPT], xn[PCG_RPT];
-    bool pzb[PCG_RPT];       // the +z neighbour is an unknown or an outlet
-    ApAcc<T> part_ap[PCG_RPT];
-    bool pend[PCG_RPT];
+    // per own cell: the previous plane's p', and plane kk-1's pending result
+    // (A p' without its +z term, p', new x) finished once plane kk lands
+    T pm[4], pcur[4], xn[4];
+    ApAcc<T> pap[4];
+    unsigned pzb = 0;   // bit c: cell c's +z neighbour is an unknown or an outlet
+    bool pend = false;
 #pragma unroll
-    for (int q = 0; q < PCG_RPT; ++q) { pm[q] = (T)0; pend[q] = false; }
+    for (int c = 0; c < 4; ++c) pm[c] = (T)0;
     bool live = true;
     while (live) {
       const unsigned tk = t0 + j;
@@ -577,50 +622,80 @@ __device__ void phaseA(const PcgArgs<T>& A, const Blk& blk, double* part, PcgSha
         continue;
       }
       const Unit u = cons.t;
-      const int i = u.i0 + lx;
       const int kk = cons.kk;
-      const T* xx = reinterpret_cast<const T*>(st + L::A_X);
+      const int i = u.i0 + 4 * tx, jj = u.j0 + ty;
+      const bool in_rows = jj < d.ny && i < A.nxp;
+      const T* zz = reinterpret_cast<const T*>(st + L::A_Z);
       const T* pp = reinterpret_cast<const T*>(st + L::A_P);
-      const uint8_t* cc = st + L::A_C;
+      auto pnew1 = [&](int y, int x) -> T {
+        const int o = H::at(y, x);
+        return first ? zz[o] : fmat(beta, pp[o], zz[o]);
+      };
+      auto pnew4 = [&](int y, T (&pn)[4], T (&po)[4]) {
+        T zo[4];
+        ld4<T>(zz + H::at(y, hx0), zo);
+        ld4<T>(pp + H::at(y, hx0), po);
 #pragma unroll
-      for (int q = 0; q < PCG_RPT; ++q) {
-        const int ly = ly0 + q * PCG_RSTEP, jj = u.j0 + ly;
-        const T pn = pnew(st, ly + 1, lx + 1);     // own p' on plane kk
-        if (pend[q]) {
-          // finish plane kk-1: add the +z neighbour (this plane) and store
-          const long long pc_ = (long long)(kk - 1) * pplane + (long long)jj * A.nxp + i;
-          const double ap = ap_finish<T>(part_ap[q], A.wz, pcur[q], pn, pzb[q]);
-          pout[pc_] = pcur[q];
-          A.Ap[pc_] = (T)ap;
-          if (upd_x) A.x[pc_] = xn[q];
+        for (int c = 0; c < 4; ++c) pn[c] = first ? zo[c] : fmat(beta, po[c], zo[c]);
+      };
+      T pn[4], po[4];
+      pnew4(hy, pn, po);                       // own p' on plane kk
+      if (pend) {
+        // finish plane kk-1: add the +z neighbour (this plane) and store
+        T apv[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const double ap = ap_finish<T>(pap[c], A.wz, pcur[c], pn[c], (pzb >> c) & 1u);
+          apv[c] = (T)ap;
+          acc += (double)pcur[c] * ap;
+        }
+        if (in_rows) {
+          const long long e = (long long)jj * A.nxp + i;
+          const long long pc_ = (long long)(kk - 1) * pplane + e;
+          st4<T>(pout + pc_, pcur);
+          st4<T>(A.Ap + pc_, apv);
+          if (upd_x) st4<T>(A.x + pc_, xn);
           if (SLABS && A.nslab > 1) {   // boundary planes go to the neighbours' halo planes
-            const long long e = (long long)jj * A.nxp + i;
             if (kk - 1 == A.o0 && A.lo.Ap) {
-              (pin_sel == 0 ? A.lo.p1 : A.lo.p0)[A.lo.plane_off + e] = pcur[q];
-              A.lo.Ap[A.lo.plane_off + e] = (T)ap;
+              st4<T>((pin_sel == 0 ? A.lo.p1 : A.lo.p0) + A.lo.plane_off + e, pcur);
+              st4<T>(A.lo.Ap + A.lo.plane_off + e, apv);
             }
             if (kk - 1 == A.o1 - 1 && A.hi.Ap) {
-              (pin_sel == 0 ? A.hi.p1 : A.hi.p0)[A.hi.plane_off + e] = pcur[q];
-              A.hi.Ap[A.hi.plane_off + e] = (T)ap;
+              st4<T>((pin_sel == 0 ? A.hi.p1 : A.hi.p0) + A.hi.plane_off + e, pcur);
+              st4<T>(A.hi.Ap + A.hi.plane_off + e, apv);
             }
           }
-          acc += (double)pcur[q] * ap;
-          pend[q] = false;
         }
-        if (kk >= u.k0 && kk < u.k1) {
-          const uint8_t cd = cc[ly * PCG_TX + lx];
-          if ((cd & 64) && i < d.nx && jj < d.ny) {
-            part_ap[q] = ap_partial<T>(cd, S.lut[(cd & 63) * 4], pn, pnew(st, ly + 1, lx + 2),
-                                       pnew(st, ly + 1, lx), pnew(st, ly + 2, lx + 1), pnew(st, ly, lx + 1),
-                                       pm[q], A.wx, A.wy, A.wz);
-            pzb[q] = (cd >> 4) & 1;
-            pcur[q] = pn;
-            if (upd_x) xn[q] = xx[ly * PCG_TX + lx] + alpha_prev * pp[Halo<T>::at(ly + 1, lx + 1)];
-            pend[q] = true;
-          }
-        }
-        pm[q] = pn;
+        pend = false;
       }
+      if (kk >= u.k0 && kk < u.k1) {
+        const uint32_t cw4 = *reinterpret_cast<const uint32_t*>(st + L::A_C + ty * PCG_TX + 4 * tx);
+        T pym[4], pyp[4], tmp[4];
+        pnew4(hy - 1, pym, tmp);
+        pnew4(hy + 1, pyp, tmp);
+        T left = from_left(pn[3]), right = from_right(pn[0]);
+        if (tx == 0) left = pnew1(hy, 0);
+        if (tx == QX - 1) right = pnew1(hy, PCG_TX + 1);
+        T xo[4];
+        if (upd_x) ld4<T>(reinterpret_cast<const T*>(st + L::A_X) + ty * PCG_TX + 4 * tx, xo);
+        pzb = 0;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const unsigned cd = (cw4 >> (8 * c)) & 0xffu;
+          const bool unk = (cd & 64u) != 0;
+          const T pxm = c == 0 ? left : pn[c - 1];
+          const T pxp = c == 3 ? right : pn[c + 1];
+          pap[c] = unk ? ap_partial<T>((uint8_t)cd, lut_at(S.lut, cd, 0), pn[c], pxp, pxm, pyp[c], pym[c], pm[c],
+                                       A.wx, A.wy, A.wz)
+                       : (ApAcc<T>)0;
+          pzb |= (unk && (cd & 16u)) ? (1u << c) : 0u;
+          pcur[c] = unk ? pn[c] : (T)0;
+          if (upd_x) xn[c] = unk ? fmat(alpha_prev, po[c], xo[c]) : (T)0;
+        }
+        pend = true;
+      }
+#pragma unroll
+      for (int c = 0; c < 4; ++c) pm[c] = pn[c];
       live = cursor_next<T>(A, cons);
       ++j;
       __syncthreads();   // every thread is done with this job's stage: refill it
@@ -639,19 +714,24 @@ __device__ void phaseA(const PcgArgs<T>& A, const Blk& blk, double* part, PcgSha
 }
 
 // ---- phase B: r' = r - alpha Ap, z = W r' ----------------------------------
-// One pass per landed plane kk computes q = r'/d on the y-tile (recomputing
-// the two in-plane lower neighbours from the stage instead of staging q) and
-// y(kk); after one barrier the own cells finish z on plane kk-1.
+// Per landed plane kk: pass 1 computes q = r'/d on the 34 x 34 halo tile
+// (own quads plus the 132-cell ring) into a 3-plane shared ring; after one
+// barrier pass 2 computes y(kk) on the 33 x 33 y tile and the own cells
+// finish z on plane kk-1 from y(kk-1) (shared) and y(kk) (registers).
 template <typename T, bool SLABS>
 __device__ void phaseB(const PcgArgs<T>& A, const Blk& blk, double* part, PcgShared<T>& S, uint8_t* ring,
                        unsigned& ticket, bool use_ap, double alpha, int rin_sel, bool write_r) {
   using L = StageLayout<T>;
+  using H = Halo<T>;
+  using HD = Halo<double>;
+  using HC = Halo<uint8_t>;
   const Dims& d = A.d;
   const CUtensorMap* tr = rin_sel == 0 ? &A.tm_r0 : &A.tm_r1;
   double* __restrict__ rout = rin_sel == 0 ? A.r1 : A.r0;
   const T om = A.om;
   const T c0 = ((T)2 - om) * om;          // s * d
-  const int lx = threadIdx.x % PCG_TX, ly0 = threadIdx.x / PCG_TX;
+  const int tx = threadIdx.x % QX, ty = threadIdx.x / QX;
+  const int hy = ty + 1, hx0 = 1 + 4 * tx;
   const long long pplane = (long long)A.nxp * d.ny;
   PcgWork<T>& W = S.wk;
   JobCursor prod, cons;
@@ -669,10 +749,12 @@ __device__ void phaseB(const PcgArgs<T>& A, const Blk& blk, double* part, PcgSha
       }
     }
     unsigned j = 0;
-    double rprev[PCG_RPT], rown[PCG_RPT];
-    uint8_t cprev[PCG_RPT], cown[PCG_RPT];
+    // the previous plane's own r', q, y, 1/d and codes
+    double rprev[4];
+    T qprev[4], yprev[4], ivprev[4];
+    uint32_t cprev = 0;
 #pragma unroll
-    for (int q = 0; q < PCG_RPT; ++q) { rprev[q] = 0.0; cprev[q] = 0; }
+    for (int c = 0; c < 4; ++c) { rprev[c] = 0.0; qprev[c] = (T)0; yprev[c] = (T)0; ivprev[c] = (T)0; }
     bool live = true;
     while (live) {
       const unsigned tk = t0 + j;
@@ -692,24 +774,44 @@ __device__ void phaseB(const PcgArgs<T>& A, const Blk& blk, double* part, PcgSha
       }
       const Unit u = cons.t;
       const int kk = cons.kk;
-      T* qcur = &W.qb[j % 3][0][0];                  // q planes kk, kk-1 (ring of 3)
-      const T* qprv = &W.qb[(j + 2) % 3][0][0];
-      T* ycur = &W.yb[j & 1][0][0];                  // y planes kk, kk-1 (ring of 2)
-      const T* yprv = &W.yb[(j + 1) & 1][0][0];
+      T(*qcur)[PCG_QW] = W.qb[j % 3];                  // q planes kk, kk-1 (ring of 3)
+      const T(*qprv)[PCG_QW] = W.qb[(j + 2) % 3];
+      T(*ycur)[PCG_YP] = W.yb[j & 1];                  // y planes kk, kk-1 (ring of 2)
+      const T(*yprv)[PCG_YP] = W.yb[(j + 1) & 1];
       const double* rr = reinterpret_cast<const double*>(st + L::B_R);
       const T* aa = reinterpret_cast<const T*>(st + L::B_AP);
       const uint8_t* cc = st + L::B_C;
-      auto rnew = [&](int hy, int hx) -> double {
-        double r = rr[Halo<double>::at(hy, hx)];
-        if (use_ap) r = r - alpha * (double)aa[Halo<T>::at(hy, hx)];
-        return r;
-      };
-      // pass 1: q = r'/d once per element of the 34 x 34 halo tile
+      // pass 1: own quad r', 1/d, s, q; the halo ring of q
+      double rown[4];
+      T qown[4], ivown[4], sown[4];
+      const uint32_t cown = *reinterpret_cast<const uint32_t*>(cc + HC::at(hy, hx0));
+      {
+        double r4[4];
+        ld4<double>(rr + HD::at(hy, hx0), r4);
+        T a4[4];
+        if (use_ap) ld4<T>(aa + H::at(hy, hx0), a4);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const unsigned cd = (cown >> (8 * c)) & 0xffu;
+          rown[c] = use_ap ? fmat(-alpha, (double)a4[c], r4[c]) : r4[c];
+          ivown[c] = lut_at(S.lut, cd, 1);
+          sown[c] = lut_at(S.lut, cd, 2);
+          qown[c] = (T)rown[c] * ivown[c];
+        }
+      }
       if (A.precond == 2) {
-        for (int e = threadIdx.x; e < HH * HW; e += PCG_THREADS) {
-          const int hy = e / HW, hx = e - hy * HW;
-          const uint8_t cd = cc[Halo<uint8_t>::at(hy, hx)];
-          qcur[e] = (T)rnew(hy, hx) * S.lut[(cd & 63) * 4 + 1];
+        st4<T>(&qcur[hy][hx0 + PCG_QOFF], qown);
+        if (threadIdx.x < 2 * HW + 2 * PCG_TY) {       // ring: rows 0 and 33, columns 0 and 33
+          const int t = threadIdx.x;
+          int ry, rx;
+          if (t < HW) { ry = 0; rx = t; }
+          else if (t < 2 * HW) { ry = HH - 1; rx = t - HW; }
+          else if (t < 2 * HW + PCG_TY) { ry = t - 2 * HW + 1; rx = 0; }
+          else { ry = t - 2 * HW - PCG_TY + 1; rx = HW - 1; }
+          const unsigned cd = cc[HC::at(ry, rx)];
+          double r = rr[HD::at(ry, rx)];
+          if (use_ap) r = fmat(-alpha, (double)aa[H::at(ry, rx)], r);
+          qcur[ry][rx + PCG_QOFF] = (T)r * lut_at(S.lut, cd, 1);
         }
       }
       __syncthreads();
@@ -718,70 +820,79 @@ __device__ void phaseB(const PcgArgs<T>& A, const Blk& blk, double* part, PcgSha
         ++issued;
         more = cursor_next<T>(A, prod);
       }
-      // pass 2: y(kk) = s (r' + w sum_a w_a q_{-a}) on the 33 x 33 y tile, with
-      // s r' = (2-w) w q; the own cells keep theirs for z(kk-1) below
+      // pass 2: y(kk) on the y tile (own quads in registers and shared, plus
+      // row 32 and column 32)
       const bool do_y = kk >= u.k0 && A.precond == 2;
-      auto yval = [&](int hy, int hx) -> T {
-        const int e = hy * HW + hx;
-        const T sv = S.lut[(cc[Halo<uint8_t>::at(hy, hx)] & 63) * 4 + 2];
-        return c0 * qcur[e] + sv * (om * (A.wx * qcur[e - 1] + A.wy * qcur[e - HW] + A.wz * qprv[e]));
-      };
-      T yown[PCG_RPT];
+      T yown[4];
+      if (do_y) {
+        T qym[4];
+        ld4<T>(&qcur[hy - 1][hx0 + PCG_QOFF], qym);
+        T left = from_left(qown[3]);
+        if (tx == 0) left = qcur[hy][PCG_QOFF];
 #pragma unroll
-      for (int q = 0; q < PCG_RPT; ++q) {
-        const int ly = ly0 + q * PCG_RSTEP;
-        rown[q] = rnew(ly + 1, lx + 1);
-        cown[q] = cc[Halo<uint8_t>::at(ly + 1, lx + 1)];
-        if (do_y) {
-          yown[q] = yval(ly + 1, lx + 1);
-          ycur[ly * YW + lx] = yown[q];
+        for (int c = 0; c < 4; ++c)
+          yown[c] = y_of<T>(c0, qown[c], sown[c], om, A.wx, c == 0 ? left : qown[c - 1], A.wy, qym[c], A.wz, qprev[c]);
+        st4<T>(&ycur[ty][4 * tx], yown);
+        if (threadIdx.x < YW + PCG_TY) {
+          const int t = threadIdx.x;
+          const int yy = t < YW ? PCG_TY : t - YW, yx = t < YW ? t : PCG_TX;
+          const int qy = yy + 1, qx = yx + 1 + PCG_QOFF;
+          ycur[yy][yx] = y_of<T>(c0, qcur[qy][qx], lut_at(S.lut, cc[HC::at(yy + 1, yx + 1)], 2), om, A.wx,
+                                 qcur[qy][qx - 1], A.wy, qcur[qy - 1][qx], A.wz, qprv[qy][qx]);
         }
       }
-      if (do_y && threadIdx.x < YW + PCG_TY) {      // row 32 and column 32 of the y tile
-        const int t = threadIdx.x;
-        const int yy = t < YW ? PCG_TY : t - YW, yx = t < YW ? t : PCG_TX;
-        ycur[yy * YW + yx] = yval(yy + 1, yx + 1);
-      }
-      // z on plane kk-1 (own cells): y(kk-1) from the previous stage, y(kk) own
+      // z on plane kk-1 (own cells): y(kk-1) from the previous plane, y(kk) own
       if (kk >= u.k0 + 1) {
         const int k = kk - 1;
-        const int i = u.i0 + lx;
+        const int i = u.i0 + 4 * tx, jj = u.j0 + ty;
+        T zv[4];
+        if (A.precond == 2) {
+          T yyp[4];
+          ld4<T>(&yprv[ty + 1][4 * tx], yyp);
+          T right = from_right(yprev[0]);
+          if (tx == QX - 1) right = yprv[ty][PCG_TX];
 #pragma unroll
-        for (int q = 0; q < PCG_RPT; ++q) {
-          const int ly = ly0 + q * PCG_RSTEP, jj = u.j0 + ly;
-          const uint8_t cd = cprev[q];
-          if ((cd & 64) && i < d.nx && jj < d.ny) {
-            const long long pc_ = k * pplane + (long long)jj * A.nxp + i;
-            T zv;
-            const int o = ly * YW + lx;
-            const T invd = S.lut[(cd & 63) * 4 + 1];
-            if (A.precond == 2)
-              zv = yprv[o] + om * invd * (A.wx * yprv[o + 1] + A.wy * yprv[o + YW] + A.wz * yown[q]);
-            else if (A.precond == 1)
-              zv = (T)rprev[q] * invd;
-            else
-              zv = (T)rprev[q];
-            A.z[pc_] = zv;
-            if (write_r) rout[pc_] = rprev[q];
-            if (SLABS && A.nslab > 1) {   // boundary planes go to the neighbours' halo planes
-              const long long e = (long long)jj * A.nxp + i;
-              if (k == A.o0 && A.lo.z) {
-                A.lo.z[A.lo.plane_off + e] = zv;
-                if (write_r) (rin_sel == 0 ? A.lo.r1 : A.lo.r0)[A.lo.plane_off + e] = rprev[q];
-              }
-              if (k == A.o1 - 1 && A.hi.z) {
-                A.hi.z[A.hi.plane_off + e] = zv;
-                if (write_r) (rin_sel == 0 ? A.hi.r1 : A.hi.r0)[A.hi.plane_off + e] = rprev[q];
-              }
+          for (int c = 0; c < 4; ++c)
+            zv[c] = yprev[c] + om * ivprev[c] * (A.wx * (c == 3 ? right : yprev[c + 1]) + A.wy * yyp[c] + A.wz * yown[c]);
+        } else {
+#pragma unroll
+          for (int c = 0; c < 4; ++c) zv[c] = A.precond == 1 ? (T)rprev[c] * ivprev[c] : (T)rprev[c];
+        }
+        double rv[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const bool unk = (cprev >> (8 * c + 6)) & 1u;
+          zv[c] = unk ? zv[c] : (T)0;
+          rv[c] = unk ? rprev[c] : 0.0;
+          acc += rv[c] * (double)zv[c];
+          const double ar = fabs(rv[c]);
+          rmax = (ar > rmax || ar != ar) ? ar : rmax;
+        }
+        if (jj < d.ny && i < A.nxp) {
+          const long long e = (long long)jj * A.nxp + i;
+          const long long pc_ = (long long)k * pplane + e;
+          st4<T>(A.z + pc_, zv);
+          if (write_r) st4<double>(rout + pc_, rv);
+          if (SLABS && A.nslab > 1) {   // boundary planes go to the neighbours' halo planes
+            if (k == A.o0 && A.lo.z) {
+              st4<T>(A.lo.z + A.lo.plane_off + e, zv);
+              if (write_r) st4<double>((rin_sel == 0 ? A.lo.r1 : A.lo.r0) + A.lo.plane_off + e, rv);
             }
-            acc += rprev[q] * (double)zv;
-            const double ar = fabs(rprev[q]);
-            rmax = (ar > rmax || ar != ar) ? ar : rmax;
+            if (k == A.o1 - 1 && A.hi.z) {
+              st4<T>(A.hi.z + A.hi.plane_off + e, zv);
+              if (write_r) st4<double>((rin_sel == 0 ? A.hi.r1 : A.hi.r0) + A.hi.plane_off + e, rv);
+            }
           }
         }
       }
 #pragma unroll
-      for (int q = 0; q < PCG_RPT; ++q) { rprev[q] = rown[q]; cprev[q] = cown[q]; }
+      for (int c = 0; c < 4; ++c) {
+        rprev[c] = rown[c];
+        qprev[c] = qown[c];
+        yprev[c] = yown[c];
+        ivprev[c] = ivown[c];
+      }
+      cprev = cown;
       live = cursor_next<T>(A, cons);
       ++j;
     }
