@@ -360,7 +360,9 @@ extern "C" int cw_set_operator(cw_ctx* c, const signed char* lab, double ai_omeg
   const Dims& d = c->d;
   const double w[3] = {1.0 / (c->grid.dx * c->grid.dx), 1.0 / (c->grid.dy * c->grid.dy),
                        1.0 / (c->grid.dz * c->grid.dz)};
-  // LUT: d, 1/d, s=(2-omega)*omega/d for each neighbour-bit pattern.
+  // LUT: d, 1/d, s*omega with s = (2-omega)*omega/d, and omega/d for each
+  // neighbour-bit pattern (the PCG's W r: y = (2-omega) omega q + s omega sum w q_-,
+  // z = y + (omega/d) sum w y_+, cw_pcg.cuh).
   // Neighbour order +x,-x,+y,-y,+z,-z (ref linalg.py:20 offsets order).
   std::vector<double> lut(64 * 4, 0.0);
   for (int b = 1; b < 64; ++b) {
@@ -369,7 +371,8 @@ extern "C" int cw_set_operator(cw_ctx* c, const signed char* lab, double ai_omeg
       if (b & (1 << q)) dd += w[q / 2];
     lut[b * 4 + 0] = dd;
     lut[b * 4 + 1] = 1.0 / dd;
-    lut[b * 4 + 2] = (2.0 - ai_omega) * ai_omega / dd;
+    lut[b * 4 + 2] = (2.0 - ai_omega) * ai_omega / dd * ai_omega;
+    lut[b * 4 + 3] = ai_omega / dd;
   }
   if (c->prec == 4) {
     std::vector<float> lf(lut.begin(), lut.end());

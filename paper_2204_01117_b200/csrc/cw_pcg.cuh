@@ -10,7 +10,7 @@
 //          z = y + (w/d) sum_a w_a y_{i+e_a}  with q = r/d, s = (2-w) w / d.
 // Both read a 1-byte per-cell code (bit 6: unknown; bits 0..5: neighbour
 // +x,-x,+y,-y,+z,-z is an unknown or an outlet) and a 64-entry table of
-// (d, 1/d, s) -- no CSR, no stored coefficients.
+// (d, 1/d, s w, w/d) -- no CSR, no stored coefficients.
 //
 // Data movement (B200): the PCG vectors live on a pitched copy of the grid
 // (row pitch nxp = nx rounded up to 16 elements, exact zeros off the
@@ -295,6 +295,7 @@ struct PcgShared {
   double vals[4];           // slab_reduce results
   double fold[3 * 32];      // fold_multi warp results
   unsigned last, gen0;      // slab_reduce: this block arrived last; generation seen
+  unsigned long long pt[3]; // timing probe (modes 13-16): phase start, first stage landed, jobs done
   alignas(8) uint64_t full[8];
 };
 
@@ -505,7 +506,8 @@ __device__ __forceinline__ ApAcc<T> ap_partial(uint8_t cd, T d, T pc, T pxp, T p
     if (cd & 8) a += wy * (pc - pym);
     if (cd & 32) a += wz * (pc - pzm);
     return a;
-  } else {
+  } else {   // 0 off the unknowns (code 0), like the difference form
+    if (!(cd & 64)) return 0.0;
     return (double)d * (double)pc - ((double)wx * ((double)pxm + (double)pxp) +
                                      (double)wy * ((double)pym + (double)pyp) + (double)wz * (double)pzm);
   }
@@ -516,7 +518,7 @@ __device__ __forceinline__ double ap_finish(ApAcc<T> part, T wz, T pc, T pzp, bo
   if constexpr (sizeof(T) == 4) {
     return (double)(zp ? part + wz * (pc - pzp) : part);
   } else {
-    return part - (double)wz * (double)pzp;
+    return zp ? part - (double)wz * (double)pzp : part;   // p = 0 on a +z neighbour that is not an unknown
   }
 }
 
@@ -525,8 +527,12 @@ __device__ __forceinline__ double ap_finish(ApAcc<T> part, T wz, T pc, T pzp, bo
 // (4 consecutive cells of one row), times 32 rows: one 32 x 32 plane per
 // block sweep.  Own quads move as 128-bit shared and global accesses; the x
 // neighbours come from the adjacent lanes of the row (shuffles), the tile
-// edges from the halo columns, the y neighbours from the rows above and below
-// (128-bit loads), the z neighbours from registers carried through the z march.
+// edges from the halo columns (every lane loads its edge cell, no divergent
+// path), the y neighbours from the rows above and below (128-bit loads), the
+// z neighbours from registers carried through the z march.  The march is
+// unrolled by two so the carried planes alternate between two register sets.
+// Shared offsets are fixed per thread; global offsets are 32-bit (pitched
+// fields hold < 2^31 elements, cw_capi.cu).
 constexpr int QX = PCG_TX / 4;
 static_assert(PCG_THREADS == QX * PCG_TY, "one thread per x quad of a 32 x 32 plane");
 
@@ -558,28 +564,53 @@ __device__ __forceinline__ E from_left(E v) { return __shfl_up_sync(0xffffffffu,
 template <typename E>
 __device__ __forceinline__ E from_right(E v) { return __shfl_down_sync(0xffffffffu, v, 1, QX); }
 
+// operator table row of a code byte: d, 1/d, s*w, w/d (cw_set_operator)
 template <typename T>
 __device__ __forceinline__ T lut_at(const T* lut, unsigned cd, int which) { return lut[(cd & 63u) * 4 + which]; }
 
-// y = s (r' + w sum_a w_a q_{i-e_a}) with s r' = (2-w) w q
+// y = s (r' + w sum_a w_a q_{i-e_a}) with s r' = (2-w) w q:  c0 q + (s w) (sum_a w_a q_{i-e_a})
 template <typename T>
-__device__ __forceinline__ T y_of(T c0, T q, T s, T om, T wx, T qxm, T wy, T qym, T wz, T qzm) {
-  return c0 * q + s * (om * (wx * qxm + wy * qym + wz * qzm));
+__device__ __forceinline__ T y_of(T c0, T q, T sw, T wx, T qxm, T wy, T qym, T wz, T qzm) {
+  return fmat(c0, q, sw * fmat(wx, qxm, fmat(wy, qym, wz * qzm)));
+}
+// z = y + (w/d) sum_a w_a y_{i+e_a}
+template <typename T>
+__device__ __forceinline__ T z_of(T y, T wd, T wx, T yxp, T wy, T yyp, T wz, T yzp) {
+  return fmat(wd, fmat(wx, yxp, fmat(wy, yyp, wz * yzp)), y);
+}
+
+// Producer side of a ring phase: thread 0 keeps DEPTH stages in flight.
+template <typename T, typename Issue>
+__device__ __forceinline__ void ring_fill(const PcgArgs<T>& A, JobCursor& prod, bool& more, unsigned& issued,
+                                          unsigned upto, Issue issue) {
+  while (more && issued < upto) {
+    issue(issued, prod);
+    ++issued;
+    more = cursor_next<T>(A, prod);
+  }
 }
 
 // ---- phase A: p' = z + beta p, x += alpha_prev p, Ap = A p' ---------------
+// (first iteration: the p box is read from z and beta = 0, so p' = z)
 template <typename T, bool SLABS>
 __device__ void phaseA(const PcgArgs<T>& A, const Blk& blk, double* part, PcgShared<T>& S, uint8_t* ring,
                        unsigned& ticket, bool first, T beta, bool upd_x, T alpha_prev, int pin_sel) {
   using L = StageLayout<T>;
   using H = Halo<T>;
-  static_assert(L::DEPTH >= 3, "phase A holds two stages");
   const Dims& d = A.d;
-  const CUtensorMap* tp = pin_sel == 0 ? &A.tm_p0 : &A.tm_p1;
+  const CUtensorMap* tp = first ? &A.tm_z : (pin_sel == 0 ? &A.tm_p0 : &A.tm_p1);
+  const T b = first ? (T)0 : beta;
   T* __restrict__ pout = pin_sel == 0 ? A.p1 : A.p0;
+  T* __restrict__ apout = A.Ap;
+  T* __restrict__ xout = A.x;
+  const T wx = A.wx, wy = A.wy, wz = A.wz;
   const int tx = threadIdx.x % QX, ty = threadIdx.x / QX;
-  const int hy = ty + 1, hx0 = 1 + 4 * tx;     // halo coordinates of this thread's first cell
-  const long long pplane = (long long)A.nxp * d.ny;
+  const bool lft = tx == 0, rgt = tx == QX - 1;
+  const int o_c = H::at(ty + 1, 1 + 4 * tx), o_dn = o_c - H::BW, o_up = o_c + H::BW;
+  const int o_e = H::at(ty + 1, lft ? 0 : (rgt ? PCG_TX + 1 : 1 + 4 * tx));
+  const int o_own = ty * PCG_TX + 4 * tx;      // own boxes: x (elements), code (bytes)
+  const int pplane = A.nxp * d.ny;
+  if (A.probe_mode >= 13 && threadIdx.x == 0) S.pt[0] = S.pt[1] = S.pt[2] = globaltimer();
   JobCursor prod, cons;
   double acc = 0.0;
   if (cursor_begin<T>(A, blk, cons)) {
@@ -587,126 +618,101 @@ __device__ void phaseA(const PcgArgs<T>& A, const Blk& blk, double* part, PcgSha
     const unsigned t0 = ticket;
     unsigned issued = 0;
     bool more = true;   // producer state, meaningful in thread 0 only
-    if (threadIdx.x == 0) {
-      while (more && issued < (unsigned)L::DEPTH) {
-        issue_A<T>(A, ring, S.full, t0 + issued, prod, tp);
-        ++issued;
-        more = cursor_next<T>(A, prod);
-      }
-    }
+    auto issue = [&](unsigned n, const JobCursor& c) { issue_A<T>(A, ring, S.full, t0 + n, c, tp); };
+    if (threadIdx.x == 0) ring_fill<T>(A, prod, more, issued, (unsigned)L::DEPTH, issue);
     unsigned j = 0;     // consumer job number in this phase
-    // per own cell: the previous plane's p', and plane kk-1's pending result
-    // (A p' without its +z term, p', new x) finished once plane kk lands
-    T pm[4], pcur[4], xn[4];
+    // plane kk-1's pending result (A p' without its +z term, p', new x),
+    // finished once plane kk lands
+    T pcur[4], xn[4];
     ApAcc<T> pap[4];
     unsigned pzb = 0;   // bit c: cell c's +z neighbour is an unknown or an outlet
     bool pend = false;
-#pragma unroll
-    for (int c = 0; c < 4; ++c) pm[c] = (T)0;
-    bool live = true;
-    while (live) {
+    T pa[4] = {(T)0, (T)0, (T)0, (T)0}, pb[4];   // p' of the previous / this plane (alternating)
+    auto plane = [&](const T (&pm)[4], T (&pn)[4]) -> bool {
       const unsigned tk = t0 + j;
       const int s = tk % L::DEPTH;
-      const uint8_t* st = ring + (size_t)s * L::STAGE;
+      const uint8_t* st = ring + s * L::STAGE;
       mbar_wait(&S.full[s], (tk / L::DEPTH) & 1u);
-      if (A.probe_mode == 4 || A.probe_mode == 7) {   // timing probe: stream the stages only
-        live = cursor_next<T>(A, cons);
-        ++j;
-        __syncthreads();
-        if (threadIdx.x == 0)
-          while (more && issued < j + L::DEPTH) {
-            issue_A<T>(A, ring, S.full, t0 + issued, prod, tp);
-            ++issued;
-            more = cursor_next<T>(A, prod);
-          }
-        continue;
-      }
-      const Unit u = cons.t;
+      if (A.probe_mode >= 13 && j == 0 && threadIdx.x == 0) S.pt[1] = globaltimer();
       const int kk = cons.kk;
-      const int i = u.i0 + 4 * tx, jj = u.j0 + ty;
-      const bool in_rows = jj < d.ny && i < A.nxp;
-      const T* zz = reinterpret_cast<const T*>(st + L::A_Z);
-      const T* pp = reinterpret_cast<const T*>(st + L::A_P);
-      auto pnew1 = [&](int y, int x) -> T {
-        const int o = H::at(y, x);
-        return first ? zz[o] : fmat(beta, pp[o], zz[o]);
-      };
-      auto pnew4 = [&](int y, T (&pn)[4], T (&po)[4]) {
-        T zo[4];
-        ld4<T>(zz + H::at(y, hx0), zo);
-        ld4<T>(pp + H::at(y, hx0), po);
+      const Unit u = cons.t;
+      if (A.probe_mode != 4 && A.probe_mode != 7) {
+        const T* zz = reinterpret_cast<const T*>(st + L::A_Z);
+        const T* pp = reinterpret_cast<const T*>(st + L::A_P);
+        const int jj = u.j0 + ty, i = u.i0 + 4 * tx;
+        const bool rows = jj < d.ny && i < A.nxp;
+        const int e = jj * A.nxp + i;
+        T zc[4], pc[4];
+        ld4<T>(zz + o_c, zc);
+        ld4<T>(pp + o_c, pc);
 #pragma unroll
-        for (int c = 0; c < 4; ++c) pn[c] = first ? zo[c] : fmat(beta, po[c], zo[c]);
-      };
-      T pn[4], po[4];
-      pnew4(hy, pn, po);                       // own p' on plane kk
-      if (pend) {
-        // finish plane kk-1: add the +z neighbour (this plane) and store
-        T apv[4];
+        for (int c = 0; c < 4; ++c) pn[c] = fmat(b, pc[c], zc[c]);
+        if (pend) {   // finish plane kk-1: add the +z neighbour (this plane) and store
+          T apv[4];
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          const double ap = ap_finish<T>(pap[c], A.wz, pcur[c], pn[c], (pzb >> c) & 1u);
-          apv[c] = (T)ap;
-          acc += (double)pcur[c] * ap;
-        }
-        if (in_rows) {
-          const long long e = (long long)jj * A.nxp + i;
-          const long long pc_ = (long long)(kk - 1) * pplane + e;
-          st4<T>(pout + pc_, pcur);
-          st4<T>(A.Ap + pc_, apv);
-          if (upd_x) st4<T>(A.x + pc_, xn);
-          if (SLABS && A.nslab > 1) {   // boundary planes go to the neighbours' halo planes
-            if (kk - 1 == A.o0 && A.lo.Ap) {
-              st4<T>((pin_sel == 0 ? A.lo.p1 : A.lo.p0) + A.lo.plane_off + e, pcur);
-              st4<T>(A.lo.Ap + A.lo.plane_off + e, apv);
-            }
-            if (kk - 1 == A.o1 - 1 && A.hi.Ap) {
-              st4<T>((pin_sel == 0 ? A.hi.p1 : A.hi.p0) + A.hi.plane_off + e, pcur);
-              st4<T>(A.hi.Ap + A.hi.plane_off + e, apv);
+          for (int c = 0; c < 4; ++c) {
+            const double ap = ap_finish<T>(pap[c], wz, pcur[c], pn[c], (pzb >> c) & 1u);
+            apv[c] = (T)ap;
+            acc += (double)pcur[c] * ap;
+          }
+          if (rows) {
+            const int g = (kk - 1) * pplane + e;
+            st4<T>(pout + g, pcur);
+            st4<T>(apout + g, apv);
+            if (upd_x) st4<T>(xout + g, xn);
+            if (SLABS && A.nslab > 1) {   // boundary planes go to the neighbours' halo planes
+              if (kk - 1 == A.o0 && A.lo.Ap) {
+                st4<T>((pin_sel == 0 ? A.lo.p1 : A.lo.p0) + A.lo.plane_off + e, pcur);
+                st4<T>(A.lo.Ap + A.lo.plane_off + e, apv);
+              }
+              if (kk - 1 == A.o1 - 1 && A.hi.Ap) {
+                st4<T>((pin_sel == 0 ? A.hi.p1 : A.hi.p0) + A.hi.plane_off + e, pcur);
+                st4<T>(A.hi.Ap + A.hi.plane_off + e, apv);
+              }
             }
           }
+          pend = false;
         }
-        pend = false;
-      }
-      if (kk >= u.k0 && kk < u.k1) {
-        const uint32_t cw4 = *reinterpret_cast<const uint32_t*>(st + L::A_C + ty * PCG_TX + 4 * tx);
-        T pym[4], pyp[4], tmp[4];
-        pnew4(hy - 1, pym, tmp);
-        pnew4(hy + 1, pyp, tmp);
-        T left = from_left(pn[3]), right = from_right(pn[0]);
-        if (tx == 0) left = pnew1(hy, 0);
-        if (tx == QX - 1) right = pnew1(hy, PCG_TX + 1);
-        T xo[4];
-        if (upd_x) ld4<T>(reinterpret_cast<const T*>(st + L::A_X) + ty * PCG_TX + 4 * tx, xo);
-        pzb = 0;
+        if (kk >= u.k0 && kk < u.k1) {
+          T zd[4], pd[4], zu[4], pu[4], pym[4], pyp[4];
+          ld4<T>(zz + o_dn, zd);
+          ld4<T>(pp + o_dn, pd);
+          ld4<T>(zz + o_up, zu);
+          ld4<T>(pp + o_up, pu);
+          const T pe = fmat(b, pp[o_e], zz[o_e]);
+          const uint32_t cw4 = *reinterpret_cast<const uint32_t*>(st + L::A_C + o_own);
+          T xv[4];
+          if (upd_x) ld4<T>(reinterpret_cast<const T*>(st + L::A_X) + o_own, xv);
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          const unsigned cd = (cw4 >> (8 * c)) & 0xffu;
-          const bool unk = (cd & 64u) != 0;
-          const T pxm = c == 0 ? left : pn[c - 1];
-          const T pxp = c == 3 ? right : pn[c + 1];
-          pap[c] = unk ? ap_partial<T>((uint8_t)cd, lut_at(S.lut, cd, 0), pn[c], pxp, pxm, pyp[c], pym[c], pm[c],
-                                       A.wx, A.wy, A.wz)
-                       : (ApAcc<T>)0;
-          pzb |= (unk && (cd & 16u)) ? (1u << c) : 0u;
-          pcur[c] = unk ? pn[c] : (T)0;
-          if (upd_x) xn[c] = unk ? fmat(alpha_prev, po[c], xo[c]) : (T)0;
+          for (int c = 0; c < 4; ++c) {
+            pym[c] = fmat(b, pd[c], zd[c]);
+            pyp[c] = fmat(b, pu[c], zu[c]);
+          }
+          T left = from_left(pn[3]), right = from_right(pn[0]);
+          left = lft ? pe : left;
+          right = rgt ? pe : right;
+          pzb = 0;
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const unsigned cd = (cw4 >> (8 * c)) & 0xffu;   // 0 off the unknowns: A p' = 0 there
+            pap[c] = ap_partial<T>((uint8_t)cd, lut_at(S.lut, cd, 0), pn[c], c == 3 ? right : pn[c + 1],
+                                   c == 0 ? left : pn[c - 1], pyp[c], pym[c], pm[c], wx, wy, wz);
+            pzb |= ((cd >> 4) & 1u) << c;
+            pcur[c] = pn[c];
+            if (upd_x) xn[c] = fmat(alpha_prev, pc[c], xv[c]);
+          }
+          pend = true;
         }
-        pend = true;
       }
-#pragma unroll
-      for (int c = 0; c < 4; ++c) pm[c] = pn[c];
-      live = cursor_next<T>(A, cons);
+      const bool live = cursor_next<T>(A, cons);
       ++j;
       __syncthreads();   // every thread is done with this job's stage: refill it
-      if (threadIdx.x == 0) {
-        while (more && issued < j + L::DEPTH) {
-          issue_A<T>(A, ring, S.full, t0 + issued, prod, tp);
-          ++issued;
-          more = cursor_next<T>(A, prod);
-        }
-      }
+      if (threadIdx.x == 0) ring_fill<T>(A, prod, more, issued, j + L::DEPTH, issue);
+      return live;
+    };
+    while (plane(pa, pb) && plane(pb, pa)) {
     }
+    if (A.probe_mode >= 13 && threadIdx.x == 0) S.pt[2] = globaltimer();
     ticket = t0 + j;
   }
   const double sum = block_sum(acc, S.red);
@@ -718,6 +724,12 @@ __device__ void phaseA(const PcgArgs<T>& A, const Blk& blk, double* part, PcgSha
 // (own quads plus the 132-cell ring) into a 3-plane shared ring; after one
 // barrier pass 2 computes y(kk) on the 33 x 33 y tile and the own cells
 // finish z on plane kk-1 from y(kk-1) (shared) and y(kk) (registers).
+template <typename T>
+struct PlaneB {           // one plane's own-quad values carried to the next plane
+  double r[4];            // r'
+  T q[4], y[4], wd[4];    // q = r'/d, y, w/d
+};
+
 template <typename T, bool SLABS>
 __device__ void phaseB(const PcgArgs<T>& A, const Blk& blk, double* part, PcgShared<T>& S, uint8_t* ring,
                        unsigned& ticket, bool use_ap, double alpha, int rin_sel, bool write_r) {
@@ -728,12 +740,34 @@ __device__ void phaseB(const PcgArgs<T>& A, const Blk& blk, double* part, PcgSha
   const Dims& d = A.d;
   const CUtensorMap* tr = rin_sel == 0 ? &A.tm_r0 : &A.tm_r1;
   double* __restrict__ rout = rin_sel == 0 ? A.r1 : A.r0;
+  T* __restrict__ zout = A.z;
   const T om = A.om;
   const T c0 = ((T)2 - om) * om;          // s * d
+  const T wx = A.wx, wy = A.wy, wz = A.wz;
+  const int precond = A.precond;
+  const double na = -alpha;
   const int tx = threadIdx.x % QX, ty = threadIdx.x / QX;
+  const bool lft = tx == 0, rgt = tx == QX - 1;
   const int hy = ty + 1, hx0 = 1 + 4 * tx;
-  const long long pplane = (long long)A.nxp * d.ny;
+  const int o_r = HD::at(hy, hx0), o_a = H::at(hy, hx0), o_c = HC::at(hy, hx0);
+  const int q_own = hy * PCG_QW + hx0 + PCG_QOFF, q_dn = q_own - PCG_QW, q_e = hy * PCG_QW + PCG_QOFF;
+  const int y_own = ty * PCG_YP + 4 * tx, y_up = y_own + PCG_YP, y_e = ty * PCG_YP + PCG_TX;
+  // ring cell of q (threads < 132): rows 0 and 33, columns 0 and 33
+  const int t = threadIdx.x;
+  const bool ring_t = t < 2 * HW + 2 * PCG_TY;
+  const int ry = t < HW ? 0 : (t < 2 * HW ? HH - 1 : (t < 2 * HW + PCG_TY ? t - 2 * HW + 1 : t - 2 * HW - PCG_TY + 1));
+  const int rx = t < HW ? t : (t < 2 * HW ? t - HW : (t < 2 * HW + PCG_TY ? 0 : HW - 1));
+  const int ro_r = HD::at(ry, rx), ro_a = H::at(ry, rx), ro_c = HC::at(ry, rx), ro_q = ry * PCG_QW + rx + PCG_QOFF;
+  // y-tile row 32 and column 32 (threads < 65)
+  const bool yh_t = t < YW + PCG_TY;
+  const int yy = t < YW ? PCG_TY : t - YW, yx = t < YW ? t : PCG_TX;
+  const int yo = yy * PCG_YP + yx, yq = (yy + 1) * PCG_QW + yx + 1 + PCG_QOFF, yc = HC::at(yy + 1, yx + 1);
+  const int pplane = A.nxp * d.ny;
   PcgWork<T>& W = S.wk;
+  T* qb = &W.qb[0][0][0];
+  T* yb = &W.yb[0][0][0];
+  constexpr int QPL = HH * PCG_QW, YPL = YH * PCG_YP;   // plane strides of the q and y rings
+  if (A.probe_mode >= 13 && threadIdx.x == 0) S.pt[0] = S.pt[1] = S.pt[2] = globaltimer();
   JobCursor prod, cons;
   double acc = 0.0, rmax = 0.0;
   if (cursor_begin<T>(A, blk, cons)) {
@@ -741,161 +775,140 @@ __device__ void phaseB(const PcgArgs<T>& A, const Blk& blk, double* part, PcgSha
     const unsigned t0 = ticket;
     unsigned issued = 0;
     bool more = true;
-    if (threadIdx.x == 0) {
-      while (more && issued < (unsigned)L::DEPTH) {
-        issue_B<T>(A, ring, S.full, t0 + issued, prod, tr);
-        ++issued;
-        more = cursor_next<T>(A, prod);
-      }
-    }
+    auto issue = [&](unsigned n, const JobCursor& c) { issue_B<T>(A, ring, S.full, t0 + n, c, tr); };
+    if (threadIdx.x == 0) ring_fill<T>(A, prod, more, issued, (unsigned)L::DEPTH, issue);
     unsigned j = 0;
-    // the previous plane's own r', q, y, 1/d and codes
-    double rprev[4];
-    T qprev[4], yprev[4], ivprev[4];
-    uint32_t cprev = 0;
+    PlaneB<T> pa, pb;
 #pragma unroll
-    for (int c = 0; c < 4; ++c) { rprev[c] = 0.0; qprev[c] = (T)0; yprev[c] = (T)0; ivprev[c] = (T)0; }
-    bool live = true;
-    while (live) {
+    for (int c = 0; c < 4; ++c) { pa.r[c] = 0.0; pa.q[c] = pa.y[c] = pa.wd[c] = (T)0; }
+    auto plane = [&](const PlaneB<T>& pv, PlaneB<T>& cu) -> bool {
       const unsigned tk = t0 + j;
       const int s = tk % L::DEPTH;
-      const uint8_t* st = ring + (size_t)s * L::STAGE;
+      const uint8_t* st = ring + s * L::STAGE;
       mbar_wait(&S.full[s], (tk / L::DEPTH) & 1u);
-      if (A.probe_mode == 7) {   // timing probe: stream the stages only
-        __syncthreads();
-        if (threadIdx.x == 0 && more) {
-          issue_B<T>(A, ring, S.full, t0 + issued, prod, tr);
-          ++issued;
-          more = cursor_next<T>(A, prod);
-        }
-        live = cursor_next<T>(A, cons);
-        ++j;
-        continue;
-      }
-      const Unit u = cons.t;
+      if (A.probe_mode >= 13 && j == 0 && threadIdx.x == 0) S.pt[1] = globaltimer();
       const int kk = cons.kk;
-      T(*qcur)[PCG_QW] = W.qb[j % 3];                  // q planes kk, kk-1 (ring of 3)
-      const T(*qprv)[PCG_QW] = W.qb[(j + 2) % 3];
-      T(*ycur)[PCG_YP] = W.yb[j & 1];                  // y planes kk, kk-1 (ring of 2)
-      const T(*yprv)[PCG_YP] = W.yb[(j + 1) & 1];
+      const Unit u = cons.t;
+      const bool probe_stream = A.probe_mode == 7;
+      T* qcur = qb + (j % 3) * QPL;               // q planes kk, kk-1 (ring of 3)
+      const T* qprv = qb + ((j + 2) % 3) * QPL;
+      T* ycur = yb + (j & 1) * YPL;               // y planes kk, kk-1 (ring of 2)
+      const T* yprv = yb + ((j + 1) & 1) * YPL;
       const double* rr = reinterpret_cast<const double*>(st + L::B_R);
       const T* aa = reinterpret_cast<const T*>(st + L::B_AP);
       const uint8_t* cc = st + L::B_C;
-      // pass 1: own quad r', 1/d, s, q; the halo ring of q
-      double rown[4];
-      T qown[4], ivown[4], sown[4];
-      const uint32_t cown = *reinterpret_cast<const uint32_t*>(cc + HC::at(hy, hx0));
-      {
+      const int jj = u.j0 + ty, i = u.i0 + 4 * tx;
+      const bool rows = jj < d.ny && i < A.nxp;
+      const int e = jj * A.nxp + i;
+      T sw[4], iv[4];
+      if (!probe_stream) {
+        // pass 1: own quad r', 1/d, s w, w/d, q; the halo ring of q
+        const uint32_t cw4 = *reinterpret_cast<const uint32_t*>(cc + o_c);
         double r4[4];
-        ld4<double>(rr + HD::at(hy, hx0), r4);
+        ld4<double>(rr + o_r, r4);
         T a4[4];
-        if (use_ap) ld4<T>(aa + H::at(hy, hx0), a4);
+        if (use_ap) ld4<T>(aa + o_a, a4);
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
-          const unsigned cd = (cown >> (8 * c)) & 0xffu;
-          rown[c] = use_ap ? fmat(-alpha, (double)a4[c], r4[c]) : r4[c];
-          ivown[c] = lut_at(S.lut, cd, 1);
-          sown[c] = lut_at(S.lut, cd, 2);
-          qown[c] = (T)rown[c] * ivown[c];
+          const unsigned cd = (cw4 >> (8 * c)) & 0xffu;   // 0 off the unknowns: q = y = z = 0 there
+          cu.r[c] = use_ap ? fmat(na, (double)a4[c], r4[c]) : r4[c];
+          iv[c] = lut_at(S.lut, cd, 1);
+          sw[c] = lut_at(S.lut, cd, 2);
+          cu.wd[c] = lut_at(S.lut, cd, 3);
+          cu.q[c] = (T)cu.r[c] * iv[c];
         }
-      }
-      if (A.precond == 2) {
-        st4<T>(&qcur[hy][hx0 + PCG_QOFF], qown);
-        if (threadIdx.x < 2 * HW + 2 * PCG_TY) {       // ring: rows 0 and 33, columns 0 and 33
-          const int t = threadIdx.x;
-          int ry, rx;
-          if (t < HW) { ry = 0; rx = t; }
-          else if (t < 2 * HW) { ry = HH - 1; rx = t - HW; }
-          else if (t < 2 * HW + PCG_TY) { ry = t - 2 * HW + 1; rx = 0; }
-          else { ry = t - 2 * HW - PCG_TY + 1; rx = HW - 1; }
-          const unsigned cd = cc[HC::at(ry, rx)];
-          double r = rr[HD::at(ry, rx)];
-          if (use_ap) r = fmat(-alpha, (double)aa[H::at(ry, rx)], r);
-          qcur[ry][rx + PCG_QOFF] = (T)r * lut_at(S.lut, cd, 1);
+        if (precond == 2) {
+          st4<T>(qcur + q_own, cu.q);
+          if (ring_t) {
+            double r = rr[ro_r];
+            if (use_ap) r = fmat(na, (double)aa[ro_a], r);
+            qcur[ro_q] = (T)r * lut_at(S.lut, cc[ro_c], 1);
+          }
         }
       }
       __syncthreads();
-      if (threadIdx.x == 0 && more && j > 0) {     // stage j-1 is free: refill it
-        issue_B<T>(A, ring, S.full, t0 + issued, prod, tr);
-        ++issued;
-        more = cursor_next<T>(A, prod);
-      }
-      // pass 2: y(kk) on the y tile (own quads in registers and shared, plus
-      // row 32 and column 32)
-      const bool do_y = kk >= u.k0 && A.precond == 2;
-      T yown[4];
-      if (do_y) {
-        T qym[4];
-        ld4<T>(&qcur[hy - 1][hx0 + PCG_QOFF], qym);
-        T left = from_left(qown[3]);
-        if (tx == 0) left = qcur[hy][PCG_QOFF];
+      if (threadIdx.x == 0 && j > 0) ring_fill<T>(A, prod, more, issued, j + L::DEPTH, issue);   // stage j-1 is free
+      if (!probe_stream) {
+        if (precond == 2) {
+          // pass 2: y(kk) on the y tile (own quads in registers and shared, plus row 32 and column 32)
+          if (kk >= u.k0) {
+            T qym[4];
+            ld4<T>(qcur + q_dn, qym);
+            const T qe = qcur[q_e];
+            T left = from_left(cu.q[3]);
+            left = lft ? qe : left;
 #pragma unroll
-        for (int c = 0; c < 4; ++c)
-          yown[c] = y_of<T>(c0, qown[c], sown[c], om, A.wx, c == 0 ? left : qown[c - 1], A.wy, qym[c], A.wz, qprev[c]);
-        st4<T>(&ycur[ty][4 * tx], yown);
-        if (threadIdx.x < YW + PCG_TY) {
-          const int t = threadIdx.x;
-          const int yy = t < YW ? PCG_TY : t - YW, yx = t < YW ? t : PCG_TX;
-          const int qy = yy + 1, qx = yx + 1 + PCG_QOFF;
-          ycur[yy][yx] = y_of<T>(c0, qcur[qy][qx], lut_at(S.lut, cc[HC::at(yy + 1, yx + 1)], 2), om, A.wx,
-                                 qcur[qy][qx - 1], A.wy, qcur[qy - 1][qx], A.wz, qprv[qy][qx]);
-        }
-      }
-      // z on plane kk-1 (own cells): y(kk-1) from the previous plane, y(kk) own
-      if (kk >= u.k0 + 1) {
-        const int k = kk - 1;
-        const int i = u.i0 + 4 * tx, jj = u.j0 + ty;
-        T zv[4];
-        if (A.precond == 2) {
-          T yyp[4];
-          ld4<T>(&yprv[ty + 1][4 * tx], yyp);
-          T right = from_right(yprev[0]);
-          if (tx == QX - 1) right = yprv[ty][PCG_TX];
+            for (int c = 0; c < 4; ++c)
+              cu.y[c] = y_of<T>(c0, cu.q[c], sw[c], wx, c == 0 ? left : cu.q[c - 1], wy, qym[c], wz, pv.q[c]);
+            st4<T>(ycur + y_own, cu.y);
+            if (yh_t)
+              ycur[yo] = y_of<T>(c0, qcur[yq], lut_at(S.lut, cc[yc], 2), wx, qcur[yq - 1], wy, qcur[yq - PCG_QW], wz,
+                                 qprv[yq]);
+          }
+          // z on plane kk-1 (own cells): y(kk-1) from the previous plane, y(kk) own
+          if (kk >= u.k0 + 1) {
+            T yyp[4], zv[4];
+            ld4<T>(yprv + y_up, yyp);
+            const T ye = yprv[y_e];
+            T right = from_right(pv.y[0]);
+            right = rgt ? ye : right;
 #pragma unroll
-          for (int c = 0; c < 4; ++c)
-            zv[c] = yprev[c] + om * ivprev[c] * (A.wx * (c == 3 ? right : yprev[c + 1]) + A.wy * yyp[c] + A.wz * yown[c]);
-        } else {
-#pragma unroll
-          for (int c = 0; c < 4; ++c) zv[c] = A.precond == 1 ? (T)rprev[c] * ivprev[c] : (T)rprev[c];
-        }
-        double rv[4];
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          const bool unk = (cprev >> (8 * c + 6)) & 1u;
-          zv[c] = unk ? zv[c] : (T)0;
-          rv[c] = unk ? rprev[c] : 0.0;
-          acc += rv[c] * (double)zv[c];
-          const double ar = fabs(rv[c]);
-          rmax = (ar > rmax || ar != ar) ? ar : rmax;
-        }
-        if (jj < d.ny && i < A.nxp) {
-          const long long e = (long long)jj * A.nxp + i;
-          const long long pc_ = (long long)k * pplane + e;
-          st4<T>(A.z + pc_, zv);
-          if (write_r) st4<double>(rout + pc_, rv);
-          if (SLABS && A.nslab > 1) {   // boundary planes go to the neighbours' halo planes
-            if (k == A.o0 && A.lo.z) {
-              st4<T>(A.lo.z + A.lo.plane_off + e, zv);
-              if (write_r) st4<double>((rin_sel == 0 ? A.lo.r1 : A.lo.r0) + A.lo.plane_off + e, rv);
+            for (int c = 0; c < 4; ++c) {
+              zv[c] = z_of<T>(pv.y[c], pv.wd[c], wx, c == 3 ? right : pv.y[c + 1], wy, yyp[c], wz, cu.y[c]);
+              acc = fmat(pv.r[c], (double)zv[c], acc);
+              const double ar = fabs(pv.r[c]);
+              rmax = (ar > rmax || ar != ar) ? ar : rmax;
             }
-            if (k == A.o1 - 1 && A.hi.z) {
-              st4<T>(A.hi.z + A.hi.plane_off + e, zv);
-              if (write_r) st4<double>((rin_sel == 0 ? A.hi.r1 : A.hi.r0) + A.hi.plane_off + e, rv);
+            if (rows) {
+              const int g = (kk - 1) * pplane + e;
+              st4<T>(zout + g, zv);
+              if (write_r) st4<double>(rout + g, pv.r);
+              if (SLABS && A.nslab > 1) {   // boundary planes go to the neighbours' halo planes
+                if (kk - 1 == A.o0 && A.lo.z) {
+                  st4<T>(A.lo.z + A.lo.plane_off + e, zv);
+                  if (write_r) st4<double>((rin_sel == 0 ? A.lo.r1 : A.lo.r0) + A.lo.plane_off + e, pv.r);
+                }
+                if (kk - 1 == A.o1 - 1 && A.hi.z) {
+                  st4<T>(A.hi.z + A.hi.plane_off + e, zv);
+                  if (write_r) st4<double>((rin_sel == 0 ? A.hi.r1 : A.hi.r0) + A.hi.plane_off + e, pv.r);
+                }
+              }
+            }
+          }
+        } else if (kk >= u.k0 && kk < u.k1) {
+          // identity / Jacobi: z = r' or r'/d on this plane
+          T zv[4];
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            zv[c] = precond == 1 ? (T)cu.r[c] * iv[c] : (T)cu.r[c];
+            acc = fmat(cu.r[c], (double)zv[c], acc);
+            const double ar = fabs(cu.r[c]);
+            rmax = (ar > rmax || ar != ar) ? ar : rmax;
+          }
+          if (rows) {
+            const int g = kk * pplane + e;
+            st4<T>(zout + g, zv);
+            if (write_r) st4<double>(rout + g, cu.r);
+            if (SLABS && A.nslab > 1) {
+              if (kk == A.o0 && A.lo.z) {
+                st4<T>(A.lo.z + A.lo.plane_off + e, zv);
+                if (write_r) st4<double>((rin_sel == 0 ? A.lo.r1 : A.lo.r0) + A.lo.plane_off + e, cu.r);
+              }
+              if (kk == A.o1 - 1 && A.hi.z) {
+                st4<T>(A.hi.z + A.hi.plane_off + e, zv);
+                if (write_r) st4<double>((rin_sel == 0 ? A.hi.r1 : A.hi.r0) + A.hi.plane_off + e, cu.r);
+              }
             }
           }
         }
       }
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        rprev[c] = rown[c];
-        qprev[c] = qown[c];
-        yprev[c] = yown[c];
-        ivprev[c] = ivown[c];
-      }
-      cprev = cown;
-      live = cursor_next<T>(A, cons);
+      const bool live = cursor_next<T>(A, cons);
       ++j;
+      return live;
+    };
+    while (plane(pa, pb) && plane(pb, pa)) {
     }
+    if (A.probe_mode >= 13 && threadIdx.x == 0) S.pt[2] = globaltimer();
     ticket = t0 + j;
   }
   const double sm = block_sum(acc, S.red);
@@ -1062,7 +1075,8 @@ __device__ __forceinline__ void pcg_body(const PcgArgs<T>& A, const Blk& blk, ui
   double* P[2] = {A.part, A.part + 3 * A.PS};
   double red[3];
 
-  if (A.probe_mode == 8 && lead) rep->criterion = 0.0;
+  if ((A.probe_mode == 8 || (A.probe_mode >= 13 && A.probe_mode <= 15)) && lead) rep->criterion = 0.0;
+  if (A.probe_mode == 16 && lead) rep->criterion = 1e30;
   for (int u = blk.id; u < U; u += B) phase0<T, SLABS>(A, P[0], u, S);
   phase_end<T, SLABS>(A, blk, P[0], U, A.PS, 3, 6u, 0, red, S, epoch);
   const double b2 = red[0], bmax = red[1], divmax = red[2];
@@ -1101,9 +1115,11 @@ __device__ __forceinline__ void pcg_body(const PcgArgs<T>& A, const Blk& blk, ui
       const bool pb = A.probe_mode == 2 || (A.probe_mode >= 6 && (q & 1));
       if (pa) phaseA<T, SLABS>(A, blk, P[0], S, ring, ticket, false, (T)0.5, true, (T)0.0, (q >> 1) & 1);
       if (pb) phaseB<T, SLABS>(A, blk, P[1], S, ring, ticket, true, 0.0, (q >> 1) & 1, true);
+      if (A.probe_mode >= 13 && threadIdx.x == 0)
+        wait_ns += A.probe_mode == 13 ? S.pt[1] - S.pt[0] : S.pt[2] - S.pt[0];
       const unsigned long long ta = globaltimer();
       grid_barrier(A.bar, A.gate, rep, A.timeout_ns, (unsigned)B, epoch);
-      wait_ns += globaltimer() - ta;
+      if (A.probe_mode < 13) wait_ns += globaltimer() - ta;
       if (A.probe_mode == 5) {   // barrier plus phase B's two folds
         rz += fold_partials(P[1], B, 0, S.bc);
         rmax = fold_partials(P[1] + A.PS, B, 1, S.bc);
@@ -1111,6 +1127,14 @@ __device__ __forceinline__ void pcg_body(const PcgArgs<T>& A, const Blk& blk, ui
     }
     // 8: report the mean grid-barrier wait per block and phase (us) as the criterion
     if (A.probe_mode == 8 && threadIdx.x == 0) atomicAdd(&rep->criterion, (double)wait_ns * 1e-3 / (B * A.probe_iters));
+    // 13: mean time to the first landed stage, 14: mean time to the end of the
+    // jobs (per block and phase, us); 15 / 16: max / min over blocks of the latter
+    if (A.probe_mode >= 13 && threadIdx.x == 0) {
+      const double us = (double)wait_ns * 1e-3 / A.probe_iters;
+      if (A.probe_mode <= 14) atomicAdd(&rep->criterion, us / B);
+      else if (A.probe_mode == 15) atomic_max_nonneg(&rep->criterion, us);
+      else atomicMin(reinterpret_cast<unsigned long long*>(&rep->criterion), (unsigned long long)__double_as_longlong(us));
+    }
     if (lead) { rep->iterations = A.probe_iters; rep->converged = 1; }
     return;
   }

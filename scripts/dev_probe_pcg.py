@@ -12,7 +12,9 @@ NAMES = {1: "phase A + barrier", 2: "phase B + barrier", 3: "barrier", 4: "phase
          8: "A,B alternating, barrier wait reported (per phase)",
          9: "A,B alternating, no global stores (per phase)",
          10: "A,B alternating, no loads: compute on stale stages (per phase)",
-         12: "A,B alternating, TMA wait reported (per phase)"}
+         12: "A,B alternating, TMA wait reported (per phase)",
+         13: "A,B alternating, mean first-stage latency reported", 14: "A,B alternating, mean job time reported",
+         15: "A,B alternating, max over blocks of job time", 16: "A,B alternating, min over blocks of job time"}
 
 
 def timed(mode, n):
@@ -24,6 +26,8 @@ def timed(mode, n):
     e0.record()
     rep = solver.step_many(s, comp.scenario.solver, comp.psys, comp.preconditioner, comp.scenario.inlet, 1)
     e1.record(); torch.cuda.synchronize()
+    if mode >= 13:
+        print(f"  {NAMES[mode]}: {rep[0].pcg.criterion:.2f} us", flush=True)
     if mode in (8, 12):
         what = "grid-barrier" if mode == 8 else "TMA stage (thread 0)"
         print(f"  mean {what} wait per block and phase: {rep[0].pcg.criterion:.2f} us", flush=True)
