@@ -279,7 +279,7 @@ struct StageLayout {
 constexpr int PCG_QOFF = 3, PCG_QW = 40, PCG_YP = 36;
 template <typename T>
 struct PcgWork {
-  alignas(16) T qb[3][HH][PCG_QW];   // q = r'/d on the halo tile, planes kk, kk-1 (+1 hazard-free)
+  alignas(16) T qb[4][HH][PCG_QW];   // q = r'/d on the halo tile, planes kk, kk-1 (+2 hazard-free)
   alignas(16) T yb[2][YH][PCG_YP];   // y on the y tile, planes kk and kk-1
 };
 
@@ -592,9 +592,12 @@ __device__ __forceinline__ void ring_fill(const PcgArgs<T>& A, JobCursor& prod, 
 
 // ---- phase A: p' = z + beta p, x += alpha_prev p, Ap = A p' ---------------
 // (first iteration: the p box is read from z and beta = 0, so p' = z)
-template <typename T, bool SLABS>
+// UPDX: x += alpha_prev p (every iteration but the first); STREAM: timing
+// probe that only streams the stages (CW_PCG_PROBE modes 4, 7)
+template <typename T, bool SLABS, bool UPDX, bool STREAM>
 __device__ void phaseA(const PcgArgs<T>& A, const Blk& blk, double* part, PcgShared<T>& S, uint8_t* ring,
-                       unsigned& ticket, bool first, T beta, bool upd_x, T alpha_prev, int pin_sel) {
+                       unsigned& ticket, bool first, T beta, T alpha_prev, int pin_sel) {
+  constexpr bool upd_x = UPDX;
   using L = StageLayout<T>;
   using H = Halo<T>;
   const Dims& d = A.d;
@@ -609,8 +612,9 @@ __device__ void phaseA(const PcgArgs<T>& A, const Blk& blk, double* part, PcgSha
   const int o_c = H::at(ty + 1, 1 + 4 * tx), o_dn = o_c - H::BW, o_up = o_c + H::BW;
   const int o_e = H::at(ty + 1, lft ? 0 : (rgt ? PCG_TX + 1 : 1 + 4 * tx));
   const int o_own = ty * PCG_TX + 4 * tx;      // own boxes: x (elements), code (bytes)
-  const int pplane = A.nxp * d.ny;
-  if (A.probe_mode >= 13 && threadIdx.x == 0) S.pt[0] = S.pt[1] = S.pt[2] = globaltimer();
+  const int nxp = A.nxp, ny = d.ny, pplane = nxp * ny;
+  const bool timing = A.probe_mode >= 13;
+  if (timing && threadIdx.x == 0) S.pt[0] = S.pt[1] = S.pt[2] = globaltimer();
   JobCursor prod, cons;
   double acc = 0.0;
   if (cursor_begin<T>(A, blk, cons)) {
@@ -633,15 +637,15 @@ __device__ void phaseA(const PcgArgs<T>& A, const Blk& blk, double* part, PcgSha
       const int s = tk % L::DEPTH;
       const uint8_t* st = ring + s * L::STAGE;
       mbar_wait(&S.full[s], (tk / L::DEPTH) & 1u);
-      if (A.probe_mode >= 13 && j == 0 && threadIdx.x == 0) S.pt[1] = globaltimer();
+      if (timing && j == 0 && threadIdx.x == 0) S.pt[1] = globaltimer();
       const int kk = cons.kk;
       const Unit u = cons.t;
-      if (A.probe_mode != 4 && A.probe_mode != 7) {
+      if (!STREAM) {
         const T* zz = reinterpret_cast<const T*>(st + L::A_Z);
         const T* pp = reinterpret_cast<const T*>(st + L::A_P);
         const int jj = u.j0 + ty, i = u.i0 + 4 * tx;
-        const bool rows = jj < d.ny && i < A.nxp;
-        const int e = jj * A.nxp + i;
+        const bool rows = jj < ny && i < nxp;
+        const int e = jj * nxp + i;
         T zc[4], pc[4];
         ld4<T>(zz + o_c, zc);
         ld4<T>(pp + o_c, pc);
@@ -712,7 +716,7 @@ __device__ void phaseA(const PcgArgs<T>& A, const Blk& blk, double* part, PcgSha
     };
     while (plane(pa, pb) && plane(pb, pa)) {
     }
-    if (A.probe_mode >= 13 && threadIdx.x == 0) S.pt[2] = globaltimer();
+    if (timing && threadIdx.x == 0) S.pt[2] = globaltimer();
     ticket = t0 + j;
   }
   const double sum = block_sum(acc, S.red);
@@ -730,9 +734,14 @@ struct PlaneB {           // one plane's own-quad values carried to the next pla
   T q[4], y[4], wd[4];    // q = r'/d, y, w/d
 };
 
-template <typename T, bool SLABS>
+// USE_AP: r' = r - alpha Ap, written back (false: z0 = W r0 from phase 0's
+// r0, nothing but z written); STREAM: timing probe, stages only (mode 7).
+// Partials: r'.z and a flag for |r'| > res_target anywhere (NaN included),
+// the max-norm half of pcg_solve's stopping rule (linalg.py:332-337).
+template <typename T, bool SLABS, bool USE_AP, bool STREAM>
 __device__ void phaseB(const PcgArgs<T>& A, const Blk& blk, double* part, PcgShared<T>& S, uint8_t* ring,
-                       unsigned& ticket, bool use_ap, double alpha, int rin_sel, bool write_r) {
+                       unsigned& ticket, double alpha, double res_target, int rin_sel) {
+  constexpr bool use_ap = USE_AP, write_r = USE_AP;
   using L = StageLayout<T>;
   using H = Halo<T>;
   using HD = Halo<double>;
@@ -762,14 +771,16 @@ __device__ void phaseB(const PcgArgs<T>& A, const Blk& blk, double* part, PcgSha
   const bool yh_t = t < YW + PCG_TY;
   const int yy = t < YW ? PCG_TY : t - YW, yx = t < YW ? t : PCG_TX;
   const int yo = yy * PCG_YP + yx, yq = (yy + 1) * PCG_QW + yx + 1 + PCG_QOFF, yc = HC::at(yy + 1, yx + 1);
-  const int pplane = A.nxp * d.ny;
+  const int nxp = A.nxp, ny = d.ny, pplane = nxp * ny;
+  const bool timing = A.probe_mode >= 13;
   PcgWork<T>& W = S.wk;
   T* qb = &W.qb[0][0][0];
   T* yb = &W.yb[0][0][0];
   constexpr int QPL = HH * PCG_QW, YPL = YH * PCG_YP;   // plane strides of the q and y rings
-  if (A.probe_mode >= 13 && threadIdx.x == 0) S.pt[0] = S.pt[1] = S.pt[2] = globaltimer();
+  if (timing && threadIdx.x == 0) S.pt[0] = S.pt[1] = S.pt[2] = globaltimer();
   JobCursor prod, cons;
-  double acc = 0.0, rmax = 0.0;
+  double acc = 0.0;
+  bool exceed = false;
   if (cursor_begin<T>(A, blk, cons)) {
     prod = cons;
     const unsigned t0 = ticket;
@@ -786,20 +797,20 @@ __device__ void phaseB(const PcgArgs<T>& A, const Blk& blk, double* part, PcgSha
       const int s = tk % L::DEPTH;
       const uint8_t* st = ring + s * L::STAGE;
       mbar_wait(&S.full[s], (tk / L::DEPTH) & 1u);
-      if (A.probe_mode >= 13 && j == 0 && threadIdx.x == 0) S.pt[1] = globaltimer();
+      if (timing && j == 0 && threadIdx.x == 0) S.pt[1] = globaltimer();
       const int kk = cons.kk;
       const Unit u = cons.t;
-      const bool probe_stream = A.probe_mode == 7;
-      T* qcur = qb + (j % 3) * QPL;               // q planes kk, kk-1 (ring of 3)
-      const T* qprv = qb + ((j + 2) % 3) * QPL;
+      constexpr bool probe_stream = STREAM;
+      T* qcur = qb + (j & 3) * QPL;               // q planes kk, kk-1 (ring of 4)
+      const T* qprv = qb + ((j + 3) & 3) * QPL;
       T* ycur = yb + (j & 1) * YPL;               // y planes kk, kk-1 (ring of 2)
       const T* yprv = yb + ((j + 1) & 1) * YPL;
       const double* rr = reinterpret_cast<const double*>(st + L::B_R);
       const T* aa = reinterpret_cast<const T*>(st + L::B_AP);
       const uint8_t* cc = st + L::B_C;
       const int jj = u.j0 + ty, i = u.i0 + 4 * tx;
-      const bool rows = jj < d.ny && i < A.nxp;
-      const int e = jj * A.nxp + i;
+      const bool rows = jj < ny && i < nxp;
+      const int e = jj * nxp + i;
       T sw[4], iv[4];
       if (!probe_stream) {
         // pass 1: own quad r', 1/d, s w, w/d, q; the halo ring of q
@@ -856,8 +867,7 @@ __device__ void phaseB(const PcgArgs<T>& A, const Blk& blk, double* part, PcgSha
             for (int c = 0; c < 4; ++c) {
               zv[c] = z_of<T>(pv.y[c], pv.wd[c], wx, c == 3 ? right : pv.y[c + 1], wy, yyp[c], wz, cu.y[c]);
               acc = fmat(pv.r[c], (double)zv[c], acc);
-              const double ar = fabs(pv.r[c]);
-              rmax = (ar > rmax || ar != ar) ? ar : rmax;
+              exceed |= !(fabs(pv.r[c]) <= res_target);
             }
             if (rows) {
               const int g = (kk - 1) * pplane + e;
@@ -882,8 +892,7 @@ __device__ void phaseB(const PcgArgs<T>& A, const Blk& blk, double* part, PcgSha
           for (int c = 0; c < 4; ++c) {
             zv[c] = precond == 1 ? (T)cu.r[c] * iv[c] : (T)cu.r[c];
             acc = fmat(cu.r[c], (double)zv[c], acc);
-            const double ar = fabs(cu.r[c]);
-            rmax = (ar > rmax || ar != ar) ? ar : rmax;
+            exceed |= !(fabs(cu.r[c]) <= res_target);
           }
           if (rows) {
             const int g = kk * pplane + e;
@@ -908,12 +917,12 @@ __device__ void phaseB(const PcgArgs<T>& A, const Blk& blk, double* part, PcgSha
     };
     while (plane(pa, pb) && plane(pb, pa)) {
     }
-    if (A.probe_mode >= 13 && threadIdx.x == 0) S.pt[2] = globaltimer();
+    if (timing && threadIdx.x == 0) S.pt[2] = globaltimer();
     ticket = t0 + j;
   }
   const double sm = block_sum(acc, S.red);
   __syncthreads();
-  const double mx = block_max(rmax, S.red);
+  const double mx = __syncthreads_or(exceed) ? 1.0 : 0.0;
   if (threadIdx.x == 0) {
     part[blk.id] = sm;
     part[A.PS + blk.id] = mx;
@@ -1098,7 +1107,7 @@ __device__ __forceinline__ void pcg_body(const PcgArgs<T>& A, const Blk& blk, ui
   const double tol = A.tol;
 
   // z = W r0, rz, max|r0|  (pcg_solve:342-345)
-  phaseB<T, SLABS>(A, blk, P[1], S, ring, ticket, false, 0.0, 0, false);
+  phaseB<T, SLABS, false, false>(A, blk, P[1], S, ring, ticket, 0.0, res_target, 0);
   phase_end<T, SLABS>(A, blk, P[1], B, A.PS, 2, 2u, 1, red, S, epoch);
   double rz = red[0];
   double rmax = red[1];
@@ -1113,8 +1122,11 @@ __device__ __forceinline__ void pcg_body(const PcgArgs<T>& A, const Blk& blk, ui
       // 6, 7: phase A and phase B alternate as in the solve (7: stream only)
       const bool pa = A.probe_mode == 1 || A.probe_mode == 4 || (A.probe_mode >= 6 && !(q & 1));
       const bool pb = A.probe_mode == 2 || (A.probe_mode >= 6 && (q & 1));
-      if (pa) phaseA<T, SLABS>(A, blk, P[0], S, ring, ticket, false, (T)0.5, true, (T)0.0, (q >> 1) & 1);
-      if (pb) phaseB<T, SLABS>(A, blk, P[1], S, ring, ticket, true, 0.0, (q >> 1) & 1, true);
+      const bool stream = A.probe_mode == 4 || A.probe_mode == 7;
+      if (pa && stream) phaseA<T, SLABS, true, true>(A, blk, P[0], S, ring, ticket, false, (T)0.5, (T)0.0, (q >> 1) & 1);
+      if (pa && !stream) phaseA<T, SLABS, true, false>(A, blk, P[0], S, ring, ticket, false, (T)0.5, (T)0.0, (q >> 1) & 1);
+      if (pb && A.probe_mode == 7) phaseB<T, SLABS, true, true>(A, blk, P[1], S, ring, ticket, 0.0, res_target, (q >> 1) & 1);
+      if (pb && A.probe_mode != 7) phaseB<T, SLABS, true, false>(A, blk, P[1], S, ring, ticket, 0.0, res_target, (q >> 1) & 1);
       if (A.probe_mode >= 13 && threadIdx.x == 0)
         wait_ns += A.probe_mode == 13 ? S.pt[1] - S.pt[0] : S.pt[2] - S.pt[0];
       const unsigned long long ta = globaltimer();
@@ -1138,7 +1150,7 @@ __device__ __forceinline__ void pcg_body(const PcgArgs<T>& A, const Blk& blk, ui
     if (lead) { rep->iterations = A.probe_iters; rep->converged = 1; }
     return;
   }
-  if (0.0 <= crit && crit < tol && rmax <= res_target) { converged = 1; finished = true; }
+  if (0.0 <= crit && crit < tol && rmax == 0.0) { converged = 1; finished = true; }   // rmax: the |r| > res_target flag
   else if (rz < 0.0) { finished = true; }
   int rsel = 0;       // r lives in r0 (0) or r1 (1)
   int psel = 1;       // previous p lives in p0 (0) or p1 (1); the first pass ignores it
@@ -1147,21 +1159,22 @@ __device__ __forceinline__ void pcg_body(const PcgArgs<T>& A, const Blk& blk, ui
     if (it >= A.max_iter) break;
     ++it;
     const bool first = it == 1;
-    phaseA<T, SLABS>(A, blk, P[0], S, ring, ticket, first, (T)beta, !first, (T)alpha, psel);
+    if (first) phaseA<T, SLABS, false, false>(A, blk, P[0], S, ring, ticket, true, (T)0, (T)0, psel);
+    else phaseA<T, SLABS, true, false>(A, blk, P[0], S, ring, ticket, false, (T)beta, (T)alpha, psel);
     phase_end<T, SLABS>(A, blk, P[0], B, A.PS, 1, 0u, 0, red, S, epoch);
     const double pAp = red[0];
     psel ^= 1;                                // the new p went to the other buffer
     if (*(volatile int*)A.gate == 3) { status = 3; alpha = 0.0; break; }
     if (pAp <= 0.0) { it -= 1; alpha = 0.0; break; }   // linalg.py:354-355
     alpha = rz / pAp;
-    phaseB<T, SLABS>(A, blk, P[1], S, ring, ticket, true, alpha, rsel, true);
+    phaseB<T, SLABS, true, false>(A, blk, P[1], S, ring, ticket, alpha, res_target, rsel);
     phase_end<T, SLABS>(A, blk, P[1], B, A.PS, 2, 2u, 1, red, S, epoch);
     const double rz_new = red[0];
     rmax = red[1];
     rsel ^= 1;
     crit = rz_new / b2;
     if (*(volatile int*)A.gate == 3) { status = 3; break; }
-    if (0.0 <= crit && crit < tol && rmax <= res_target) { converged = 1; break; }
+    if (0.0 <= crit && crit < tol && rmax == 0.0) { converged = 1; break; }
     if (rz_new < 0.0) break;                  // linalg.py:364-365
     beta = rz_new / rz;
     rz = rz_new;
