@@ -534,6 +534,9 @@ __device__ __forceinline__ double ap_finish(ApAcc<T> part, T wz, T pc, T pzp, bo
 // Shared offsets are fixed per thread; global offsets are 32-bit (pitched
 // fields hold < 2^31 elements, cw_capi.cu).
 constexpr int QX = PCG_TX / 4;
+#ifndef CW_ABL
+#define CW_ABL 0   // developer ablations of phase B (timing only; results are wrong when set)
+#endif
 static_assert(PCG_THREADS == QX * PCG_TY, "one thread per x quad of a 32 x 32 plane");
 
 __device__ __forceinline__ float fmat(float a, float b, float c) { return __fmaf_rn(a, b, c); }
@@ -556,6 +559,18 @@ __device__ __forceinline__ void st4(E* p, const E (&v)[4]) {
   } else {
     *reinterpret_cast<double2*>(p) = make_double2(v[0], v[1]);
     *reinterpret_cast<double2*>(p + 2) = make_double2(v[2], v[3]);
+  }
+}
+// global quad store: float64 quads go out as one 256-bit store (STG.E.ENL2.256),
+// so a warp instruction covers whole 32-byte sectors (two 128-bit halves would
+// each write half of every sector); p: 32-byte aligned for float64
+template <typename E>
+__device__ __forceinline__ void stg4(E* p, const E (&v)[4]) {
+  if constexpr (sizeof(E) == 8) {
+    asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(v[0]), "d"(v[1]), "d"(v[2]), "d"(v[3])
+                 : "memory");
+  } else {
+    st4<E>(p, v);
   }
 }
 // the neighbouring lane of the same 8-lane row (a lane at the row's end gets its own value)
@@ -661,17 +676,17 @@ __device__ void phaseA(const PcgArgs<T>& A, const Blk& blk, double* part, PcgSha
           }
           if (rows) {
             const int g = (kk - 1) * pplane + e;
-            st4<T>(pout + g, pcur);
-            st4<T>(apout + g, apv);
-            if (upd_x) st4<T>(xout + g, xn);
+            stg4<T>(pout + g, pcur);
+            stg4<T>(apout + g, apv);
+            if (upd_x) stg4<T>(xout + g, xn);
             if (SLABS && A.nslab > 1) {   // boundary planes go to the neighbours' halo planes
               if (kk - 1 == A.o0 && A.lo.Ap) {
-                st4<T>((pin_sel == 0 ? A.lo.p1 : A.lo.p0) + A.lo.plane_off + e, pcur);
-                st4<T>(A.lo.Ap + A.lo.plane_off + e, apv);
+                stg4<T>((pin_sel == 0 ? A.lo.p1 : A.lo.p0) + A.lo.plane_off + e, pcur);
+                stg4<T>(A.lo.Ap + A.lo.plane_off + e, apv);
               }
               if (kk - 1 == A.o1 - 1 && A.hi.Ap) {
-                st4<T>((pin_sel == 0 ? A.hi.p1 : A.hi.p0) + A.hi.plane_off + e, pcur);
-                st4<T>(A.hi.Ap + A.hi.plane_off + e, apv);
+                stg4<T>((pin_sel == 0 ? A.hi.p1 : A.hi.p0) + A.hi.plane_off + e, pcur);
+                stg4<T>(A.hi.Ap + A.hi.plane_off + e, apv);
               }
             }
           }
@@ -830,7 +845,7 @@ __device__ void phaseB(const PcgArgs<T>& A, const Blk& blk, double* part, PcgSha
         }
         if (precond == 2) {
           st4<T>(qcur + q_own, cu.q);
-          if (ring_t) {
+          if (ring_t && !(CW_ABL & 1)) {
             double r = rr[ro_r];
             if (use_ap) r = fmat(na, (double)aa[ro_a], r);
             qcur[ro_q] = (T)r * lut_at(S.lut, cc[ro_c], 1);
@@ -842,7 +857,7 @@ __device__ void phaseB(const PcgArgs<T>& A, const Blk& blk, double* part, PcgSha
       if (!probe_stream) {
         if (precond == 2) {
           // pass 2: y(kk) on the y tile (own quads in registers and shared, plus row 32 and column 32)
-          if (kk >= u.k0) {
+          if (kk >= u.k0 && !(CW_ABL & 8)) {
             T qym[4];
             ld4<T>(qcur + q_dn, qym);
             const T qe = qcur[q_e];
@@ -852,12 +867,12 @@ __device__ void phaseB(const PcgArgs<T>& A, const Blk& blk, double* part, PcgSha
             for (int c = 0; c < 4; ++c)
               cu.y[c] = y_of<T>(c0, cu.q[c], sw[c], wx, c == 0 ? left : cu.q[c - 1], wy, qym[c], wz, pv.q[c]);
             st4<T>(ycur + y_own, cu.y);
-            if (yh_t)
+            if (yh_t && !(CW_ABL & 2))
               ycur[yo] = y_of<T>(c0, qcur[yq], lut_at(S.lut, cc[yc], 2), wx, qcur[yq - 1], wy, qcur[yq - PCG_QW], wz,
                                  qprv[yq]);
           }
           // z on plane kk-1 (own cells): y(kk-1) from the previous plane, y(kk) own
-          if (kk >= u.k0 + 1) {
+          if (kk >= u.k0 + 1 && !(CW_ABL & 8)) {
             T yyp[4], zv[4];
             ld4<T>(yprv + y_up, yyp);
             const T ye = yprv[y_e];
@@ -869,18 +884,18 @@ __device__ void phaseB(const PcgArgs<T>& A, const Blk& blk, double* part, PcgSha
               acc = fmat(pv.r[c], (double)zv[c], acc);
               exceed |= !(fabs(pv.r[c]) <= res_target);
             }
-            if (rows) {
+            if (rows && !(CW_ABL & 4)) {
               const int g = (kk - 1) * pplane + e;
-              st4<T>(zout + g, zv);
-              if (write_r) st4<double>(rout + g, pv.r);
+              stg4<T>(zout + g, zv);
+              if (write_r) stg4<double>(rout + g, pv.r);
               if (SLABS && A.nslab > 1) {   // boundary planes go to the neighbours' halo planes
                 if (kk - 1 == A.o0 && A.lo.z) {
-                  st4<T>(A.lo.z + A.lo.plane_off + e, zv);
-                  if (write_r) st4<double>((rin_sel == 0 ? A.lo.r1 : A.lo.r0) + A.lo.plane_off + e, pv.r);
+                  stg4<T>(A.lo.z + A.lo.plane_off + e, zv);
+                  if (write_r) stg4<double>((rin_sel == 0 ? A.lo.r1 : A.lo.r0) + A.lo.plane_off + e, pv.r);
                 }
                 if (kk - 1 == A.o1 - 1 && A.hi.z) {
-                  st4<T>(A.hi.z + A.hi.plane_off + e, zv);
-                  if (write_r) st4<double>((rin_sel == 0 ? A.hi.r1 : A.hi.r0) + A.hi.plane_off + e, pv.r);
+                  stg4<T>(A.hi.z + A.hi.plane_off + e, zv);
+                  if (write_r) stg4<double>((rin_sel == 0 ? A.hi.r1 : A.hi.r0) + A.hi.plane_off + e, pv.r);
                 }
               }
             }
@@ -896,16 +911,16 @@ __device__ void phaseB(const PcgArgs<T>& A, const Blk& blk, double* part, PcgSha
           }
           if (rows) {
             const int g = kk * pplane + e;
-            st4<T>(zout + g, zv);
-            if (write_r) st4<double>(rout + g, cu.r);
+            stg4<T>(zout + g, zv);
+            if (write_r) stg4<double>(rout + g, cu.r);
             if (SLABS && A.nslab > 1) {
               if (kk == A.o0 && A.lo.z) {
-                st4<T>(A.lo.z + A.lo.plane_off + e, zv);
-                if (write_r) st4<double>((rin_sel == 0 ? A.lo.r1 : A.lo.r0) + A.lo.plane_off + e, cu.r);
+                stg4<T>(A.lo.z + A.lo.plane_off + e, zv);
+                if (write_r) stg4<double>((rin_sel == 0 ? A.lo.r1 : A.lo.r0) + A.lo.plane_off + e, cu.r);
               }
               if (kk == A.o1 - 1 && A.hi.z) {
-                st4<T>(A.hi.z + A.hi.plane_off + e, zv);
-                if (write_r) st4<double>((rin_sel == 0 ? A.hi.r1 : A.hi.r0) + A.hi.plane_off + e, cu.r);
+                stg4<T>(A.hi.z + A.hi.plane_off + e, zv);
+                if (write_r) stg4<double>((rin_sel == 0 ? A.hi.r1 : A.hi.r0) + A.hi.plane_off + e, cu.r);
               }
             }
           }
