@@ -140,6 +140,35 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, u
       "l"((unsigned long long)map), "r"(x), "r"(y), "r"(z), "r"(smem_u32(b))
       : "memory");
 }
+// L2 residency: the vectors re-read in the very next phase (z: B -> A, Ap:
+// A -> B) and the operator codes are stored / loaded evict_last so they stay in
+// the 126 MB L2 (36 MB at C3); the streams re-read only an iteration later (p,
+// x, r) are evict_first.  CW_L2HINT=0 drops the hints (developer comparison).
+#ifndef CW_L2HINT
+#define CW_L2HINT 1
+#endif
+__device__ __forceinline__ uint64_t l2_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t l2_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void tma_load_3d_hint(void* dst, const CUtensorMap* map, uint64_t* b, int x, int y, int z,
+                                                 uint64_t pol) {
+#if CW_L2HINT
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3, %4}], [%5], %6;" ::"r"(smem_u32(dst)),
+      "l"((unsigned long long)map), "r"(x), "r"(y), "r"(z), "r"(smem_u32(b)), "l"(pol)
+      : "memory");
+#else
+  tma_load_3d(dst, map, b, x, y, z);
+#endif
+}
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async;" ::: "memory"); }
 
 __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
@@ -363,11 +392,12 @@ __device__ __forceinline__ void issue_A(const PcgArgs<T>& A, uint8_t* ring, uint
   uint8_t* st = ring + (size_t)s * L::STAGE;
   const bool own = c.kk >= c.t.k0 && c.kk < c.t.k1;
   mbar_expect_tx(&full[s], L::BYTES_A_HALO + (own ? L::BYTES_A_X : 0u));
-  tma_load_3d(st + L::A_Z, &A.tm_z, &full[s], c.t.i0 - Halo<T>::SH, c.t.j0 - 1, c.kk);
-  tma_load_3d(st + L::A_P, tp, &full[s], c.t.i0 - Halo<T>::SH, c.t.j0 - 1, c.kk);
+  const uint64_t keep = l2_evict_last(), drop = l2_evict_first();
+  tma_load_3d_hint(st + L::A_Z, &A.tm_z, &full[s], c.t.i0 - Halo<T>::SH, c.t.j0 - 1, c.kk, keep);
+  tma_load_3d_hint(st + L::A_P, tp, &full[s], c.t.i0 - Halo<T>::SH, c.t.j0 - 1, c.kk, drop);
   if (own) {
-    tma_load_3d(st + L::A_X, &A.tm_x, &full[s], c.t.i0, c.t.j0, c.kk);
-    tma_load_3d(st + L::A_C, &A.tm_code_own, &full[s], c.t.i0, c.t.j0, c.kk);
+    tma_load_3d_hint(st + L::A_X, &A.tm_x, &full[s], c.t.i0, c.t.j0, c.kk, drop);
+    tma_load_3d_hint(st + L::A_C, &A.tm_code_own, &full[s], c.t.i0, c.t.j0, c.kk, keep);
   }
 }
 
@@ -378,9 +408,10 @@ __device__ __forceinline__ void issue_B(const PcgArgs<T>& A, uint8_t* ring, uint
   const int s = ticket % L::DEPTH;
   uint8_t* st = ring + (size_t)s * L::STAGE;
   mbar_expect_tx(&full[s], L::BYTES_B);
-  tma_load_3d(st + L::B_R, tr, &full[s], c.t.i0 - Halo<double>::SH, c.t.j0 - 1, c.kk);
-  tma_load_3d(st + L::B_AP, &A.tm_ap, &full[s], c.t.i0 - Halo<T>::SH, c.t.j0 - 1, c.kk);
-  tma_load_3d(st + L::B_C, &A.tm_code, &full[s], c.t.i0 - Halo<uint8_t>::SH, c.t.j0 - 1, c.kk);
+  const uint64_t keep = l2_evict_last(), drop = l2_evict_first();
+  tma_load_3d_hint(st + L::B_R, tr, &full[s], c.t.i0 - Halo<double>::SH, c.t.j0 - 1, c.kk, drop);
+  tma_load_3d_hint(st + L::B_AP, &A.tm_ap, &full[s], c.t.i0 - Halo<T>::SH, c.t.j0 - 1, c.kk, keep);
+  tma_load_3d_hint(st + L::B_C, &A.tm_code, &full[s], c.t.i0 - Halo<uint8_t>::SH, c.t.j0 - 1, c.kk, keep);
 }
 
 // ---- phase 0: b = -div/dt, r0 = b - A x0 with x0 = p on the unknowns ------
@@ -573,6 +604,23 @@ __device__ __forceinline__ void stg4(E* p, const E (&v)[4]) {
     st4<E>(p, v);
   }
 }
+// the same with an L2 eviction policy (l2_evict_first / l2_evict_last)
+template <typename E>
+__device__ __forceinline__ void stg4h(E* p, const E (&v)[4], uint64_t pol) {
+#if CW_L2HINT
+  if constexpr (sizeof(E) == 8) {
+    asm volatile("st.global.L2::cache_hint.v4.f64 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p), "d"(v[0]), "d"(v[1]),
+                 "d"(v[2]), "d"(v[3]), "l"(pol)
+                 : "memory");
+  } else {
+    asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p), "f"(v[0]), "f"(v[1]),
+                 "f"(v[2]), "f"(v[3]), "l"(pol)
+                 : "memory");
+  }
+#else
+  stg4<E>(p, v);
+#endif
+}
 // the neighbouring lane of the same 8-lane row (a lane at the row's end gets its own value)
 template <typename E>
 __device__ __forceinline__ E from_left(E v) { return __shfl_up_sync(0xffffffffu, v, 1, QX); }
@@ -622,6 +670,7 @@ __device__ void phaseA(const PcgArgs<T>& A, const Blk& blk, double* part, PcgSha
   T* __restrict__ apout = A.Ap;
   T* __restrict__ xout = A.x;
   const T wx = A.wx, wy = A.wy, wz = A.wz;
+  const uint64_t keep = l2_evict_last(), drop = l2_evict_first();
   const int tx = threadIdx.x % QX, ty = threadIdx.x / QX;
   const bool lft = tx == 0, rgt = tx == QX - 1;
   const int o_c = H::at(ty + 1, 1 + 4 * tx), o_dn = o_c - H::BW, o_up = o_c + H::BW;
@@ -676,9 +725,9 @@ __device__ void phaseA(const PcgArgs<T>& A, const Blk& blk, double* part, PcgSha
           }
           if (rows) {
             const int g = (kk - 1) * pplane + e;
-            stg4<T>(pout + g, pcur);
-            stg4<T>(apout + g, apv);
-            if (upd_x) stg4<T>(xout + g, xn);
+            stg4h<T>(pout + g, pcur, drop);
+            stg4h<T>(apout + g, apv, keep);
+            if (upd_x) stg4h<T>(xout + g, xn, drop);
             if (SLABS && A.nslab > 1) {   // boundary planes go to the neighbours' halo planes
               if (kk - 1 == A.o0 && A.lo.Ap) {
                 stg4<T>((pin_sel == 0 ? A.lo.p1 : A.lo.p0) + A.lo.plane_off + e, pcur);
@@ -770,6 +819,7 @@ __device__ void phaseB(const PcgArgs<T>& A, const Blk& blk, double* part, PcgSha
   const T wx = A.wx, wy = A.wy, wz = A.wz;
   const int precond = A.precond;
   const double na = -alpha;
+  const uint64_t keep = l2_evict_last(), drop = l2_evict_first();
   const int tx = threadIdx.x % QX, ty = threadIdx.x / QX;
   const bool lft = tx == 0, rgt = tx == QX - 1;
   const int hy = ty + 1, hx0 = 1 + 4 * tx;
@@ -886,8 +936,8 @@ __device__ void phaseB(const PcgArgs<T>& A, const Blk& blk, double* part, PcgSha
             }
             if (rows && !(CW_ABL & 4)) {
               const int g = (kk - 1) * pplane + e;
-              stg4<T>(zout + g, zv);
-              if (write_r) stg4<double>(rout + g, pv.r);
+              stg4h<T>(zout + g, zv, keep);
+              if (write_r) stg4h<double>(rout + g, pv.r, drop);
               if (SLABS && A.nslab > 1) {   // boundary planes go to the neighbours' halo planes
                 if (kk - 1 == A.o0 && A.lo.z) {
                   stg4<T>(A.lo.z + A.lo.plane_off + e, zv);
