@@ -203,6 +203,15 @@ static int ctx_create(const cw_grid* g, int kg0, int nzg, int own0, int own1, in
   d.nx = g->nx; d.ny = g->ny; d.nz = g->nz;
   d.dx = (float)g->dx; d.dy = (float)g->dy; d.dz = (float)g->dz;
   d.ddx = g->dx; d.ddy = g->dy; d.ddz = g->dz;
+  {
+    const double hh[3] = {g->dx, g->dy, g->dz};
+    for (int a = 0; a < 3; ++a) {
+      d.drh[a] = 1.0 / hh[a];
+      d.drh2[a] = 1.0 / (hh[a] * hh[a]);
+      d.rh[a] = (float)d.drh[a];
+      d.rh2[a] = (float)d.drh2[a];
+    }
+  }
   d.is2d = g->nz == 1;
   d.o0 = own0; d.o1 = own1; d.kg0 = kg0; d.nzg = nzg;
   c->ncell = d.ncell();

@@ -19,6 +19,10 @@ struct Dims {
   float dx, dy, dz;        // spacings in the arithmetic type used by kernels
   double ddx, ddy, ddz;    // float64 spacings for host-side derived constants
   int is2d;
+  // reciprocal spacings 1/h and 1/h^2 per axis (host-computed in float64):
+  // kernels multiply instead of dividing by the constant spacings
+  float rh[3], rh2[3];
+  double drh[3], drh2[3];
   // z-slab window: the local grid holds global planes [kg0, kg0 + nz) of a
   // grid with nzg planes and owns local planes [o0, o1) (reductions and
   // reports cover the owned planes only).  A whole grid: 0, nz, 0, nz.
@@ -30,6 +34,13 @@ struct Dims {
   // 32-bit cell index (contexts hold < 2^31 cells per field, cw_capi.cu)
   __host__ __device__ inline int cidx32(int i, int j, int k) const { return (k * ny + j) * nx + i; }
 };
+
+template <typename T> __host__ __device__ inline T inv_h(const Dims& d, int ax);
+template <> __host__ __device__ inline float inv_h<float>(const Dims& d, int ax) { return d.rh[ax]; }
+template <> __host__ __device__ inline double inv_h<double>(const Dims& d, int ax) { return d.drh[ax]; }
+template <typename T> __host__ __device__ inline T inv_h2(const Dims& d, int ax);
+template <> __host__ __device__ inline float inv_h2<float>(const Dims& d, int ax) { return d.rh2[ax]; }
+template <> __host__ __device__ inline double inv_h2<double>(const Dims& d, int ax) { return d.drh2[ax]; }
 
 // Extents of component arrays: comp 0 = u, 1 = v, 2 = w, 3 = cell.
 __host__ __device__ inline void comp_extent(const Dims& d, int comp, int& ex, int& ey, int& ez) {
@@ -76,6 +87,31 @@ __device__ __forceinline__ T gather(const T* __restrict__ a, int ex, int ey, int
   ty = ty < (T)0 ? (T)0 : (ty > (T)1 ? (T)1 : ty);
   tz = tz < (T)0 ? (T)0 : (tz > (T)1 ? (T)1 : tz);
   return gather_at<T>(a, ex, ey, ez, i0, j0, k0, tx, ty, tz, mn, mx);
+}
+
+// gather_at for weights t in {0, 1/2, 1} on every axis (the face-point
+// velocities): corners with weight 0 are not loaded.  Bit-identical to
+// gather_at for finite values: a weight of 1/2 scales exactly, and x, y, z
+// are combined in the same order.
+template <typename T>
+__device__ __forceinline__ T lin_half(const T* __restrict__ p, int s, T t) {
+  if (t == (T)0) return p[0];
+  if (t == (T)1) return p[s];
+  return p[0] * (T)0.5 + p[s] * (T)0.5;
+}
+template <typename T>
+__device__ __forceinline__ T gather_half(const T* __restrict__ a, int ex, int ey, int ez, int i0, int j0, int k0,
+                                         T tx, T ty, T tz) {
+  const int sx = ex > 1 ? 1 : 0, sy = ey > 1 ? ex : 0, sz = ez > 1 ? ex * ey : 0;
+  const T* b = a + (k0 * ey + j0) * ex + i0;
+  auto plane = [&](const T* q) -> T {
+    if (ty == (T)0) return lin_half(q, sx, tx);
+    if (ty == (T)1) return lin_half(q + sy, sx, tx);
+    return lin_half(q, sx, tx) * (T)0.5 + lin_half(q + sy, sx, tx) * (T)0.5;
+  };
+  if (tz == (T)0) return plane(b);
+  if (tz == (T)1) return plane(b + sz);
+  return plane(b) * (T)0.5 + plane(b + sz) * (T)0.5;
 }
 
 // The same gather at a point i + half/2 on one axis (half in {-1, 0, 1}):

@@ -450,6 +450,7 @@ __device__ void phase0(const PcgArgs<T>& A, double* part, int unit, PcgShared<T>
     }
   };
   double b2 = 0.0, bmax = 0.0, dmax = 0.0;
+  const double rdt = 1.0 / A.dt;
   T pm[PCG_RPT];
 #pragma unroll
   for (int q = 0; q < PCG_RPT; ++q) pm[q] = xval(t.k0 - 1, i, t.j0 + ly0 + q * PCG_RSTEP);
@@ -474,10 +475,10 @@ __device__ void phase0(const PcgArgs<T>& A, double* part, int unit, PcgShared<T>
         const long long ui = ((long long)k * d.ny + j) * (d.nx + 1) + i;
         const long long vi = ((long long)k * (d.ny + 1) + j) * d.nx + i;
         // divergence and A x0 in float64 from the stored fields
-        double div = ((double)A.u[ui + 1] - (double)A.u[ui]) / d.ddx +
-                     ((double)A.v[vi + d.nx] - (double)A.v[vi]) / d.ddy;
-        if (!d.is2d) div = div + ((double)A.w[c + plane] - (double)A.w[c]) / d.ddz;
-        const double b = -div / A.dt;
+        double div = ((double)A.u[ui + 1] - (double)A.u[ui]) * d.drh[0] +
+                     ((double)A.v[vi + d.nx] - (double)A.v[vi]) * d.drh[1];
+        if (!d.is2d) div = div + ((double)A.w[c + plane] - (double)A.w[c]) * d.drh[2];
+        const double b = -div * rdt;
         const double ax = (double)S.lut[(cd & 63) * 4] * (double)pc -
                           ((double)A.wx * ((double)S.pa[bc][ly + 1][lx] + (double)S.pa[bc][ly + 1][lx + 2]) +
                            (double)A.wy * ((double)S.pa[bc][ly][lx + 1] + (double)S.pa[bc][ly + 2][lx + 1]) +

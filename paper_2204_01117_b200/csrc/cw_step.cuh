@@ -79,7 +79,7 @@ __device__ __forceinline__ void upwind_cell(const Dims& d, const T* __restrict__
     const int pos[3] = {i, j, k};
     const int ext[3] = {d.nx, d.ny, d.nz};
     const int str[3] = {1, d.nx, (int)d.nx * d.ny};
-    const T h[3] = {(T)d.dx, (T)d.dy, (T)d.dz};
+    const T rh[3] = {inv_h<T>(d, 0), inv_h<T>(d, 1), inv_h<T>(d, 2)};
 #pragma unroll
     for (int f = 0; f < 2; ++f) {
       const T* fld = f ? win : kin;
@@ -88,8 +88,8 @@ __device__ __forceinline__ void upwind_cell(const Dims& d, const T* __restrict__
 #pragma unroll
       for (int ax = 0; ax < 3; ++ax) {
         if (ext[ax] == 1) continue;
-        const T bwd = pos[ax] > 0 ? (fc - fld[c - str[ax]]) / h[ax] : (T)0;
-        const T fwd = pos[ax] < ext[ax] - 1 ? (fld[c + str[ax]] - fc) / h[ax] : (T)0;
+        const T bwd = pos[ax] > 0 ? (fc - fld[c - str[ax]]) * rh[ax] : (T)0;
+        const T fwd = pos[ax] < ext[ax] - 1 ? (fld[c + str[ax]] - fc) * rh[ax] : (T)0;
         const T ap = a[ax] > (T)0 ? a[ax] : (T)0;
         const T am = a[ax] < (T)0 ? a[ax] : (T)0;
         out -= dt * (ap * bwd + am * fwd);
@@ -119,13 +119,13 @@ __device__ __forceinline__ void velocity_at(const Dims& d, int comp, const T* u,
   T tx, ty, tz;
   // u grid: offsets (0, .5, .5), extents (nx+1, ny, nz)
   axis_at<T>(i, hx, d.nx + 1, i0, tx); axis_at<T>(j, hy - 1, d.ny, j0, ty); axis_at<T>(k, hz - 1, d.nz, k0, tz);
-  us = gather_at<T>(u, d.nx + 1, d.ny, d.nz, i0, j0, k0, tx, ty, tz, nullptr, nullptr);
+  us = gather_half<T>(u, d.nx + 1, d.ny, d.nz, i0, j0, k0, tx, ty, tz);
   // v grid: offsets (.5, 0, .5)
   axis_at<T>(i, hx - 1, d.nx, i0, tx); axis_at<T>(j, hy, d.ny + 1, j0, ty); axis_at<T>(k, hz - 1, d.nz, k0, tz);
-  vs = gather_at<T>(v, d.nx, d.ny + 1, d.nz, i0, j0, k0, tx, ty, tz, nullptr, nullptr);
+  vs = gather_half<T>(v, d.nx, d.ny + 1, d.nz, i0, j0, k0, tx, ty, tz);
   // w grid: offsets (.5, .5, 0)
   axis_at<T>(i, hx - 1, d.nx, i0, tx); axis_at<T>(j, hy - 1, d.ny, j0, ty); axis_at<T>(k, hz, d.nz + 1, k0, tz);
-  ws = gather_at<T>(w, d.nx, d.ny, d.nz + 1, i0, j0, k0, tx, ty, tz, nullptr, nullptr);
+  ws = gather_half<T>(w, d.nx, d.ny, d.nz + 1, i0, j0, k0, tx, ty, tz);
 }
 
 // One thread per (i, j, k) of the union of the face extents handles the u, v
@@ -144,7 +144,7 @@ __device__ __forceinline__ void mac_predict_face(const Dims& d, int comp, const 
   const T X = (T)i + ox, Y = (T)j + oy, Z = (T)k + oz;
   T us, vs, ws;
   velocity_at<T>(d, comp, u, v, w, i, j, k, us, vs, ws);
-  const T bx = X - dt * us / (T)d.dx, by = Y - dt * vs / (T)d.dy, bz = Z - dt * ws / (T)d.dz;
+  const T bx = X - dt * us * inv_h<T>(d, 0), by = Y - dt * vs * inv_h<T>(d, 1), bz = Z - dt * ws * inv_h<T>(d, 2);
   ahead[c] = gather<T>(arr, ex, ey, ez, bx - ox, by - oy, bz - oz, nullptr, nullptr);
 }
 
@@ -179,9 +179,10 @@ __device__ __forceinline__ void mac_correct_face(const Dims& d, int comp, const 
   T us, vs, ws;
   velocity_at<T>(d, comp, u, v, w, i, j, k, us, vs, ws);
   T mn, mx;
-  const T bx = X - dt * us / (T)d.dx, by = Y - dt * vs / (T)d.dy, bz = Z - dt * ws / (T)d.dz;
+  const T sx = dt * us * inv_h<T>(d, 0), sy = dt * vs * inv_h<T>(d, 1), sz = dt * ws * inv_h<T>(d, 2);
+  const T bx = X - sx, by = Y - sy, bz = Z - sz;
   (void)gather<T>(arr, ex, ey, ez, bx - ox, by - oy, bz - oz, &mn, &mx);
-  const T fx = X + dt * us / (T)d.dx, fy = Y + dt * vs / (T)d.dy, fz = Z + dt * ws / (T)d.dz;
+  const T fx = X + sx, fy = Y + sy, fz = Z + sz;
   const T back = gather<T>(ahead, ex, ey, ez, fx - ox, fy - oy, fz - oz, nullptr, nullptr);
   T cor = ahead[c] + (T)0.5 * (arr[c] - back);
   cor = cor < mn ? mn : cor;
@@ -220,7 +221,7 @@ __device__ __forceinline__ void diffuse_face(const Dims& d, int comp, const T* _
   comp_extent(d, comp, ex, ey, ez);
   const int ext[3] = {ex, ey, ez};
   const int str[3] = {1, ex, (int)ex * ey};
-  const T h[3] = {(T)d.dx, (T)d.dy, (T)d.dz};
+  const T rh2[3] = {inv_h2<T>(d, 0), inv_h2<T>(d, 1), inv_h2<T>(d, 2)};
   if (i < ex && j < ey && k < ez) {
     const int c = ((int)k * ey + j) * ex + i;
     const int pos[3] = {i, j, k};
@@ -231,7 +232,7 @@ __device__ __forceinline__ void diffuse_face(const Dims& d, int comp, const T* _
       if (ext[ax] == 1 || (d.is2d && ax == 2)) continue;
       const T lo = pos[ax] > 0 ? src[c - str[ax]] : mid;
       const T hi = pos[ax] < ext[ax] - 1 ? src[c + str[ax]] : mid;
-      lap += (lo - (T)2 * mid + hi) / (h[ax] * h[ax]);
+      lap += (lo - (T)2 * mid + hi) * rh2[ax];
     }
     // face viscosity along the component's own axis, edge faces copy the cell
     int ci[3] = {pos[0], pos[1], pos[2]};
@@ -425,7 +426,7 @@ __device__ __forceinline__ void gradient_face(const Dims& d, int comp, T* __rest
                                               const int8_t* __restrict__ lab, T dt, int i, int j, int k) {
   int ex, ey, ez;
   comp_extent(d, comp, ex, ey, ez);
-  const T h = comp == 0 ? (T)d.dx : (comp == 1 ? (T)d.dy : (T)d.dz);
+  const T rh = inv_h<T>(d, comp);
   const int nc = comp == 0 ? d.nx : (comp == 1 ? d.ny : d.nz);
   if (i < ex && j < ey && k < ez) {
     const int c = ((int)k * ey + j) * ex + i;
@@ -439,9 +440,9 @@ __device__ __forceinline__ void gradient_face(const Dims& d, int comp, T* __rest
     const int8_t la = lab[lo], lb = lab[hi];
     const bool au = is_unknown(la), bu = is_unknown(lb);
     T grad = (T)0;
-    if (au && bu) grad = (p[hi] - p[lo]) / h;
-    else if (au && lb == OUTLET) grad = -p[lo] / h;
-    else if (bu && la == OUTLET) grad = p[hi] / h;
+    if (au && bu) grad = (p[hi] - p[lo]) * rh;
+    else if (au && lb == OUTLET) grad = -p[lo] * rh;
+    else if (bu && la == OUTLET) grad = p[hi] * rh;
     else return;
     arr[c] -= dt * grad;
   }
@@ -471,8 +472,8 @@ __global__ void k_div_max(Dims d, const T* __restrict__ u, const T* __restrict__
   if (inb && is_unknown(lab[c])) {
     const int ui = ((int)k * d.ny + j) * (d.nx + 1) + i;
     const int vi = ((int)k * (d.ny + 1) + j) * d.nx + i;
-    T div = (u[ui + 1] - u[ui]) / (T)d.dx + (v[vi + d.nx] - v[vi]) / (T)d.dy;
-    if (!d.is2d) div = div + (w[c + (int)d.nx * d.ny] - w[c]) / (T)d.dz;
+    T div = (u[ui + 1] - u[ui]) * inv_h<T>(d, 0) + (v[vi + d.nx] - v[vi]) * inv_h<T>(d, 1);
+    if (!d.is2d) div = div + (w[c + (int)d.nx * d.ny] - w[c]) * inv_h<T>(d, 2);
     const T a = fabs(div);
     m = (a > m || a != a) ? a : m;
   }
@@ -528,32 +529,31 @@ __device__ __forceinline__ T cgrad(const Dims& d, int comp, int ax, const T* u, 
   const int n = ax == 0 ? d.nx : (ax == 1 ? d.ny : d.nz);
   if (n == 1) return (T)0;
   const int q = ax == 0 ? i : (ax == 1 ? j : k);
-  const T h = ax == 0 ? (T)d.dx : (ax == 1 ? (T)d.dy : (T)d.dz);
+  const T rh = inv_h<T>(d, ax);
   int p0[3] = {i, j, k}, p1[3] = {i, j, k};
   if (q == 0) { p1[ax] = 1; p0[ax] = 0; }
   else if (q == n - 1) { p1[ax] = n - 1; p0[ax] = n - 2; }
   else { p1[ax] = q + 1; p0[ax] = q - 1; }
   const T f1 = cell_vel(d, comp, u, v, w, p1[0], p1[1], p1[2]);
   const T f0 = cell_vel(d, comp, u, v, w, p0[0], p0[1], p0[2]);
-  if (q == 0 || q == n - 1) return (f1 - f0) / h;
-  return (f1 - f0) / ((T)2 * h);
+  if (q == 0 || q == n - 1) return (f1 - f0) * rh;
+  return (f1 - f0) * ((T)0.5 * rh);
 }
 
 template <typename T>
 __device__ __forceinline__ T pad_lap(const Dims& d, const T* f, int c, int i, int j, int k) {
   const int pos[3] = {i, j, k}, ext[3] = {d.nx, d.ny, d.nz};
   const int str[3] = {1, d.nx, (int)d.nx * d.ny};
-  const T h[3] = {(T)d.dx, (T)d.dy, (T)d.dz};
   const T fc = f[c];
   T out = (T)0;
 #pragma unroll
   for (int ax = 0; ax < 3; ++ax) {
     const int n = ext[ax];
     if (n == 1) continue;
-    const T h2 = h[ax] * h[ax];
-    if (pos[ax] == 0) out += (f[c + str[ax]] - fc) / h2;
-    else if (pos[ax] == n - 1) out += (f[c - str[ax]] - fc) / h2;
-    else out += (f[c - str[ax]] - (T)2 * fc + f[c + str[ax]]) / h2;
+    const T r2 = inv_h2<T>(d, ax);
+    if (pos[ax] == 0) out += (f[c + str[ax]] - fc) * r2;
+    else if (pos[ax] == n - 1) out += (f[c - str[ax]] - fc) * r2;
+    else out += (f[c - str[ax]] - (T)2 * fc + f[c + str[ax]]) * r2;
   }
   return out;
 }
@@ -570,9 +570,9 @@ __global__ void k_turbulence(Dims d, const T* __restrict__ u, const T* __restric
     const int c = d.cidx32(i, j, k);
     const int ui = ((int)k * d.ny + j) * (d.nx + 1) + i;
     const int vi = ((int)k * (d.ny + 1) + j) * d.nx + i;
-    const T dudx = (u[ui + 1] - u[ui]) / (T)d.dx;
-    const T dvdy = (v[vi + d.nx] - v[vi]) / (T)d.dy;
-    const T dwdz = (w[c + (int)d.nx * d.ny] - w[c]) / (T)d.dz;
+    const T dudx = (u[ui + 1] - u[ui]) * inv_h<T>(d, 0);
+    const T dvdy = (v[vi + d.nx] - v[vi]) * inv_h<T>(d, 1);
+    const T dwdz = (w[c + (int)d.nx * d.ny] - w[c]) * inv_h<T>(d, 2);
     const T dudy = cgrad(d, 0, 1, u, v, w, i, j, k), dudz = cgrad(d, 0, 2, u, v, w, i, j, k);
     const T dvdx = cgrad(d, 1, 0, u, v, w, i, j, k), dvdz = cgrad(d, 1, 2, u, v, w, i, j, k);
     const T dwdx = cgrad(d, 2, 0, u, v, w, i, j, k), dwdy = cgrad(d, 2, 1, u, v, w, i, j, k);
@@ -594,7 +594,7 @@ __global__ void k_turbulence(Dims d, const T* __restrict__ u, const T* __restric
     }
     const T kf = kn > (T)1e-12 ? kn : (T)1e-12;
     const T wf = wn > (T)1e-8 ? wn : (T)1e-8;
-    T omt = (T)sc.c_lim * sqrt(s2) / ((T)sc.c_mu / (T)2);
+    T omt = (T)sc.c_lim * sqrt(s2) * ((T)2 / (T)sc.c_mu);
     omt = wf > omt ? wf : omt;
     omt = omt > (T)1e-8 ? omt : (T)1e-8;
     kout[c] = kf;
