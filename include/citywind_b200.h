@@ -70,6 +70,9 @@ typedef struct {
   const signed char *labels;                /* int8 CellLabel, ref grid.py:19-29 */
   const void *g;                            /* real per-cell drag coefficient C_d*G */
   int has_drag;                             /* any(g != 0), ref solver.py:157-158 */
+  long long labels_version;                 /* != 0: changes whenever the labels content may have
+                                               changed; lets the context reuse its boundary-write
+                                               lists (0: no reuse, full-volume boundary kernels) */
 } cw_fields;
 
 /* StepReport + PcgReport, ref solver.py:101-110, linalg.py:27-31 */

@@ -7,6 +7,7 @@ every compute entry point raises.
 from __future__ import annotations
 
 import ctypes as C
+import itertools
 import os
 import threading
 
@@ -43,7 +44,24 @@ class cw_inlet(C.Structure):
 
 class cw_fields(C.Structure):
     _fields_ = [(n, C.c_void_p) for n in ("u", "v", "w", "p", "k", "omega", "nu_t", "labels", "g")] + \
-               [("has_drag", C.c_int)]
+               [("has_drag", C.c_int), ("labels_version", C.c_longlong)]
+
+
+_LABEL_UIDS = itertools.count(1)
+
+
+def labels_version(t) -> int:
+    """A key that changes whenever the content of the labels tensor ``t`` may
+    have changed: a process-unique id stamped on the tensor object (a new
+    tensor at a recycled address gets a new id) and torch's in-place version
+    counter.  The context keys its boundary-write lists on it."""
+    if t is None:
+        return 0
+    uid = getattr(t, "_cw_uid", None)
+    if uid is None:
+        uid = next(_LABEL_UIDS)
+        t._cw_uid = uid
+    return (uid << 24) | (int(t._version) & 0xFFFFFF)
 
 
 class cw_report(C.Structure):

@@ -94,6 +94,12 @@ struct cw_ctx {
   // inlet cache
   cw_inlet inl_cache{};
   bool inl_valid = false;
+  // boundary-write lists (k_bc_*_list), built for the labels array at bc_lab
+  const void* bc_lab = nullptr;
+  long long bc_ver = 0;
+  BcEntry* bc_list[7] = {};   // 6 outlet sides in the reference's order, then inlet/wall
+  int bc_n[7] = {};
+  int* bc_count = nullptr;
   // stage timing
   bool timing = false;
   cudaEvent_t ev[8] = {};
@@ -331,6 +337,9 @@ extern "C" void cw_ctx_destroy(cw_ctx* c) {
                   c->flag, c->xbar, c->xval, c->slab_args};
   for (void* p : ptrs)
     if (p) cudaFree(p);
+  for (int q = 0; q < 7; ++q)
+    if (c->bc_list[q]) cudaFree(c->bc_list[q]);
+  if (c->bc_count) cudaFree(c->bc_count);
   if (c->ev_made)
     for (auto& e : c->ev) cudaEventDestroy(e);
   for (auto& e : c->pev) cudaEventDestroy(e);
@@ -487,9 +496,63 @@ static int upload_inlet(cw_ctx* c, const cw_inlet* inl, cudaStream_t st) {
   return CW_OK;
 }
 
-template <typename T>
-static void launch_bc(cw_ctx* c, BcFields<T> F, const int8_t* lab, const cw_params* prm, cudaStream_t st) {
+// Enumerate the boundary writes of this labels array (once per labels
+// pointer; labels are fixed while a context steps them).  0 on success.
+static int build_bc_lists(cw_ctx* c, const int8_t* lab, long long ver, cudaStream_t st) {
   const Dims& d = c->d;
+  for (int q = 0; q < 7; ++q) {
+    if (c->bc_list[q]) cudaFree(c->bc_list[q]);
+    c->bc_list[q] = nullptr;
+    c->bc_n[q] = 0;
+  }
+  c->bc_lab = nullptr;
+  if (!c->bc_count && alloc((void**)&c->bc_count, 8 * sizeof(int)) != CW_OK) return 1;
+  const int sides = d.is2d ? 4 : 6;
+  auto side_launch = [&](int s, BcEntry* out, int cap) {
+    const int axis = s / 2;
+    const int ext = axis == 0 ? d.nx : (axis == 1 ? d.ny : d.nz);
+    const int pos = (s & 1) ? ext - 1 : 0;
+    const int e1 = axis == 0 ? d.ny : d.nx, e2 = axis == 2 ? d.ny : d.nz;
+    k_bc_outlet_list<<<nblk((long long)(e1 + 1) * (e2 + 1)), 256, 0, st>>>(d, axis, pos, lab, out, c->bc_count + s, cap);
+  };
+  // pass 1: counts
+  if (cudaMemsetAsync(c->bc_count, 0, 8 * sizeof(int), st) != cudaSuccess) return 1;
+  for (int s = 0; s < sides; ++s) side_launch(s, nullptr, 0);
+  k_bc_inlet_wall_list<<<g3(d.nx + 1, d.ny + 1, d.nz + 1), B3, 0, st>>>(d, lab, nullptr, c->bc_count + 6, 0);
+  int cnt[8];
+  if (cudaMemcpyAsync(cnt, c->bc_count, sizeof(cnt), cudaMemcpyDeviceToHost, st) != cudaSuccess) return 1;
+  if (cudaStreamSynchronize(st) != cudaSuccess) return 1;
+  // pass 2: the entries
+  for (int q = 0; q < 7; ++q)
+    if (cnt[q] > 0 && alloc((void**)&c->bc_list[q], (size_t)cnt[q] * sizeof(BcEntry)) != CW_OK) return 1;
+  if (cudaMemsetAsync(c->bc_count, 0, 8 * sizeof(int), st) != cudaSuccess) return 1;
+  for (int s = 0; s < sides; ++s)
+    if (cnt[s] > 0) side_launch(s, c->bc_list[s], cnt[s]);
+  if (cnt[6] > 0)
+    k_bc_inlet_wall_list<<<g3(d.nx + 1, d.ny + 1, d.nz + 1), B3, 0, st>>>(d, lab, c->bc_list[6], c->bc_count + 6, cnt[6]);
+  if (cudaGetLastError() != cudaSuccess) return 1;
+  for (int q = 0; q < 7; ++q) c->bc_n[q] = cnt[q];
+  c->bc_lab = lab;
+  c->bc_ver = ver;
+  return 0;
+}
+
+template <typename T>
+static void launch_bc(cw_ctx* c, BcFields<T> F, const int8_t* lab, long long ver, const cw_params* prm,
+                      cudaStream_t st) {
+  const Dims& d = c->d;
+  if (ver != 0 && ((c->bc_lab == lab && c->bc_ver == ver) || build_bc_lists(c, lab, ver, st) == 0)) {
+    for (int q = 0; q < 6; ++q)
+      if (c->bc_n[q] > 0)
+        (k_bc_copy_list<T><<<nblk(c->bc_n[q]), 256, 0, st>>>(F, c->bc_list[q], c->bc_n[q], c->gate), ++c->launches);
+    if (c->bc_n[6] > 0)
+      (k_bc_set_list<T><<<nblk(c->bc_n[6]), 256, 0, st>>>(F, c->bc_list[6], c->bc_n[6], (const T*)c->uzx,
+                                                         (const T*)c->uzy, (T)prm->k_in, (T)prm->omega_in,
+                                                         (T)(prm->k_in / prm->omega_in), c->gate),
+       ++c->launches);
+    return;
+  }
+  cudaGetLastError();   // list build failed: the full-volume kernels below
   const int sides = d.is2d ? 4 : 6;
   for (int s = 0; s < sides; ++s) {
     const int axis = s / 2;
@@ -511,10 +574,10 @@ extern "C" int cw_apply_boundary(cw_ctx* c, const cw_fields* f, const cw_params*
   if (rc) return rc;
   if (c->prec == 4) {
     BcFields<float> F{(float*)f->u, (float*)f->v, (float*)f->w, (float*)f->p, (float*)f->k, (float*)f->omega, (float*)f->nu_t};
-    launch_bc<float>(c, F, (const int8_t*)f->labels, prm, S(stream));
+    launch_bc<float>(c, F, (const int8_t*)f->labels, f->labels_version, prm, S(stream));
   } else {
     BcFields<double> F{(double*)f->u, (double*)f->v, (double*)f->w, (double*)f->p, (double*)f->k, (double*)f->omega, (double*)f->nu_t};
-    launch_bc<double>(c, F, (const int8_t*)f->labels, prm, S(stream));
+    launch_bc<double>(c, F, (const int8_t*)f->labels, f->labels_version, prm, S(stream));
   }
   CW_CUDA(cudaGetLastError());
   return CW_OK;
@@ -603,6 +666,7 @@ template <typename T>
 struct StepPtrs {
   T *u, *v, *w, *p, *k, *om, *nut;
   const int8_t* lab;
+  long long lab_ver;
   const T* g;
 };
 
@@ -698,7 +762,7 @@ static StepPtrs<T> ptrs_of(const cw_fields* f) {
   StepPtrs<T> P;
   P.u = (T*)f->u; P.v = (T*)f->v; P.w = (T*)f->w; P.p = (T*)f->p;
   P.k = (T*)f->k; P.om = (T*)f->omega; P.nut = (T*)f->nu_t;
-  P.lab = (const int8_t*)f->labels; P.g = (const T*)f->g;
+  P.lab = (const int8_t*)f->labels; P.lab_ver = f->labels_version; P.g = (const T*)f->g;
   return P;
 }
 
@@ -720,7 +784,7 @@ static int enqueue_step(cw_ctx* c, const cw_fields* f, const cw_params* prm, dou
   StepPtrs<T> B = P;                                          // k, omega after upwind live in tk, tw
   if (turb) { B.k = (T*)c->tk; B.om = (T*)c->tw; }
   BcFields<T> F1{B.u, B.v, B.w, B.p, B.k, B.om, B.nut};
-  launch_bc<T>(c, F1, P.lab, prm, st);                        // "boundary"
+  launch_bc<T>(c, F1, P.lab, P.lab_ver, prm, st);                        // "boundary"
   mark(4);
   int rc = st_project<T>(c, P, f, prm, tol, rep, st);         // "project"
   if (rc) return rc;
@@ -728,7 +792,7 @@ static int enqueue_step(cw_ctx* c, const cw_fields* f, const cw_params* prm, dou
   if (turb) st_turb<T>(c, P, prm, B.k, B.om, rep, st);        // "turbulence"
   mark(6);
   BcFields<T> F2{P.u, P.v, P.w, P.p, P.k, P.om, P.nut};
-  launch_bc<T>(c, F2, P.lab, prm, st);                        // "boundary2"
+  launch_bc<T>(c, F2, P.lab, P.lab_ver, prm, st);                        // "boundary2"
   (k_speed_max<T><<<g3r(c->d.nx + 1, c->d.ny + 1, c->d.o1 - c->d.o0 + 1), B3R, 0, st>>>(c->d, P.u, P.v, P.w, rep, c->gate),
    ++c->launches);
   mark(7);
@@ -766,7 +830,7 @@ static int enqueue_stage(cw_ctx* c, const cw_fields* f, const cw_params* prm, in
       break;
     case CW_STAGE_BOUNDARY: {
       BcFields<T> F{P.u, P.v, P.w, P.p, P.k, P.om, P.nut};
-      launch_bc<T>(c, F, P.lab, prm, st);
+      launch_bc<T>(c, F, P.lab, P.lab_ver, prm, st);
       break;
     }
     case CW_STAGE_PROJECT: {
@@ -783,7 +847,7 @@ static int enqueue_stage(cw_ctx* c, const cw_fields* f, const cw_params* prm, in
       StepPtrs<T> B = P;
       if (turb) { B.k = (T*)c->tk; B.om = (T*)c->tw; }
       BcFields<T> F1{B.u, B.v, B.w, B.p, B.k, B.om, B.nut};
-      launch_bc<T>(c, F1, P.lab, prm, st);
+      launch_bc<T>(c, F1, P.lab, P.lab_ver, prm, st);
       break;
     }
     case CW_STAGE_SOLVE: {
@@ -800,7 +864,7 @@ static int enqueue_stage(cw_ctx* c, const cw_fields* f, const cw_params* prm, in
       st_project_tail<T>(c, P, prm, rep, st);
       if (prm->turbulence) st_turb<T>(c, P, prm, (const T*)c->tk, (const T*)c->tw, rep, st);
       BcFields<T> F2{P.u, P.v, P.w, P.p, P.k, P.om, P.nut};
-      launch_bc<T>(c, F2, P.lab, prm, st);
+      launch_bc<T>(c, F2, P.lab, P.lab_ver, prm, st);
       (k_speed_max<T><<<g3r(d.nx + 1, d.ny + 1, d.o1 - d.o0 + 1), B3R, 0, st>>>(d, P.u, P.v, P.w, rep, c->gate),
        ++c->launches);
       break;

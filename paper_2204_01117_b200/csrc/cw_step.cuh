@@ -420,6 +420,135 @@ __global__ void k_bc_inlet_wall(Dims d, BcFields<T> F, const int8_t* __restrict_
 }
 
 // ---------------------------------------------------------------------------
+// The same boundary writes from precomputed lists.  The labels fix which
+// locations each write touches, so they are enumerated once per labels array
+// (k_bc_outlet_list / k_bc_inlet_wall_list, the predicates of the kernels
+// above) and every step replays them with O(boundary) threads.  Within one
+// side's list, and within the inlet/wall list, every (array, dst) is written
+// by one entry and no entry reads another's dst, so entries run in any order;
+// the sides still run in the reference's order (one launch each).
+struct BcEntry {
+  int arr;   // 0 u, 1 v, 2 w; 3: the four scalars k, omega, nu_t, p (copy) / k, omega, nu_t (inlet)
+  int dst;
+  int src;   // copy: source index; set: inlet profile row (>= 0) or -1 for a zero (wall)
+};
+
+__device__ __forceinline__ void bc_emit(BcEntry* out, int* count, int cap, int arr, int dst, int src) {
+  const int q = atomicAdd(count, 1);
+  if (out && q < cap) out[q] = BcEntry{arr, dst, src};
+}
+
+__global__ void k_bc_outlet_list(Dims d, int axis, int pos, const int8_t* __restrict__ lab, BcEntry* out, int* count,
+                                 int cap) {
+  const int ext[3] = {d.nx, d.ny, d.nz};
+  const int a1 = axis == 0 ? 1 : 0, a2 = axis == 2 ? 1 : 2;
+  const int n1 = ext[a1] + 1, n2 = ext[a2] + 1;
+  const int inner = pos == 0 ? pos + 1 : pos - 1;
+  const int n = n1 * n2;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
+    const int q1 = t % n1, q2 = t / n1;
+    int c[3];
+    if (q1 < ext[a1] && q2 < ext[a2]) {
+      c[axis] = pos; c[a1] = q1; c[a2] = q2;
+      const int cc = d.cidx32(c[0], c[1], c[2]);
+      if (lab[cc] == OUTLET) {
+        c[axis] = inner;
+        bc_emit(out, count, cap, 3, cc, d.cidx32(c[0], c[1], c[2]));
+        if (!(d.is2d && axis == 2)) {
+          int ex, ey, ez;
+          comp_extent(d, axis, ex, ey, ez);
+          int f[3];
+          f[a1] = q1; f[a2] = q2;
+          f[axis] = pos > 0 ? pos + 1 : 0;
+          const int fo = ((int)f[2] * ey + f[1]) * ex + f[0];
+          f[axis] = pos > 0 ? pos : 1;
+          bc_emit(out, count, cap, axis, fo, ((int)f[2] * ey + f[1]) * ex + f[0]);
+        }
+      }
+    }
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+      const int caxis = s == 0 ? a1 : a2;
+      if (d.is2d && caxis == 2) continue;
+      const int qa = s == 0 ? q1 : q2, qb = s == 0 ? q2 : q1;
+      const int oth = s == 0 ? a2 : a1;
+      if (qa > ext[caxis] || qb >= ext[oth]) continue;
+      c[axis] = pos; c[oth] = qb;
+      c[caxis] = clampi(qa - 1, 0, ext[caxis] - 1);
+      bool m = lab[d.cidx32(c[0], c[1], c[2])] == OUTLET;
+      c[caxis] = clampi(qa, 0, ext[caxis] - 1);
+      m = m || lab[d.cidx32(c[0], c[1], c[2])] == OUTLET;
+      if (!m) continue;
+      int ex, ey, ez;
+      comp_extent(d, caxis, ex, ey, ez);
+      int f[3];
+      f[axis] = pos; f[caxis] = qa; f[oth] = qb;
+      const int fo = ((int)f[2] * ey + f[1]) * ex + f[0];
+      f[axis] = inner;
+      bc_emit(out, count, cap, caxis, fo, ((int)f[2] * ey + f[1]) * ex + f[0]);
+    }
+  }
+}
+
+__device__ __forceinline__ void bc_face_list(const Dims& d, int comp, const int8_t* lab, int i, int j, int k,
+                                             BcEntry* out, int* count, int cap) {
+  int ex, ey, ez;
+  comp_extent(d, comp, ex, ey, ez);
+  if (i >= ex || j >= ey || k >= ez) return;
+  const int ext[3] = {d.nx, d.ny, d.nz};
+  int p[3] = {i, j, k};
+  const int f = p[comp];
+  p[comp] = clampi(f - 1, 0, ext[comp] - 1);
+  const int8_t la = lab[d.cidx32(p[0], p[1], p[2])];
+  p[comp] = clampi(f, 0, ext[comp] - 1);
+  const int8_t lb = lab[d.cidx32(p[0], p[1], p[2])];
+  const int r = ((int)k * ey + j) * ex + i;
+  if (la == SOLID_WALL || lb == SOLID_WALL) bc_emit(out, count, cap, comp, r, -1);
+  else if (la == INLET || lb == INLET) bc_emit(out, count, cap, comp, r, p[2]);
+}
+
+__global__ void k_bc_inlet_wall_list(Dims d, const int8_t* __restrict__ lab, BcEntry* out, int* count, int cap) {
+  CW_IJK(d.nx + 1, d.ny + 1, d.nz + 1, inb);
+  if (!inb) return;
+  if (i < d.nx && j < d.ny && k < d.nz) {
+    const int t = d.cidx32(i, j, k);
+    if (lab[t] == INLET) bc_emit(out, count, cap, 3, t, 0);
+  }
+  bc_face_list(d, 0, lab, i, j, k, out, count, cap);
+  bc_face_list(d, 1, lab, i, j, k, out, count, cap);
+  if (!d.is2d) bc_face_list(d, 2, lab, i, j, k, out, count, cap);
+}
+
+template <typename T>
+__global__ void k_bc_copy_list(BcFields<T> F, const BcEntry* __restrict__ e, int n, const int* gate) {
+  if (*gate) return;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
+    const BcEntry x = e[t];
+    if (x.arr == 3) {
+      F.k[x.dst] = F.k[x.src]; F.om[x.dst] = F.om[x.src]; F.nut[x.dst] = F.nut[x.src]; F.p[x.dst] = F.p[x.src];
+    } else {
+      T* a = x.arr == 0 ? F.u : (x.arr == 1 ? F.v : F.w);
+      a[x.dst] = a[x.src];
+    }
+  }
+}
+
+template <typename T>
+__global__ void k_bc_set_list(BcFields<T> F, const BcEntry* __restrict__ e, int n, const T* __restrict__ uz_dirx,
+                              const T* __restrict__ uz_diry, T k_in, T om_in, T nut_in, const int* gate) {
+  if (*gate) return;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
+    const BcEntry x = e[t];
+    if (x.arr == 3) {
+      F.k[x.dst] = k_in; F.om[x.dst] = om_in; F.nut[x.dst] = nut_in;
+    } else {
+      T* a = x.arr == 0 ? F.u : (x.arr == 1 ? F.v : F.w);
+      a[x.dst] = x.src < 0 ? (T)0 : (x.arr == 0 ? uz_dirx[x.src] : (x.arr == 1 ? uz_diry[x.src] : (T)0));
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // pressure-gradient update (solver.py:282-303)
 template <typename T>
 __device__ __forceinline__ void gradient_face(const Dims& d, int comp, T* __restrict__ arr, const T* __restrict__ p,

@@ -62,7 +62,7 @@ class Context:
         f = state.fields
         return N.cw_fields(N.ptr(f["u"]), N.ptr(f["v"]), N.ptr(f["w"]), N.ptr(f["p"]), N.ptr(f["k"]),
                            N.ptr(f["omega"]), N.ptr(f["nu_t"]), N.ptr(state.labels_dev),
-                           N.ptr(g), int(bool(has_drag)))
+                           N.ptr(g), int(bool(has_drag)), N.labels_version(state.labels_dev))
 
     def read_reports(self, n):
         out = (N.cw_report * max(n, 1))()

@@ -229,7 +229,7 @@ class SlabPart:
         f = self.fields
         return N.cw_fields(N.ptr(f["u"]), N.ptr(f["v"]), N.ptr(f["w"]), N.ptr(f["p"]), N.ptr(f["k"]),
                            N.ptr(f["omega"]), N.ptr(f["nu_t"]), N.ptr(self.labels), N.ptr(self.g),
-                           int(bool(self.has_drag)))
+                           int(bool(self.has_drag)), N.labels_version(self.labels))
 
     def run(self, stage: int, prm, inl, tol=-1.0):
         f = self.native_fields()
