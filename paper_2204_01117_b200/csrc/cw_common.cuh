@@ -89,31 +89,6 @@ __device__ __forceinline__ T gather(const T* __restrict__ a, int ex, int ey, int
   return gather_at<T>(a, ex, ey, ez, i0, j0, k0, tx, ty, tz, mn, mx);
 }
 
-// gather_at for weights t in {0, 1/2, 1} on every axis (the face-point
-// velocities): corners with weight 0 are not loaded.  Bit-identical to
-// gather_at for finite values: a weight of 1/2 scales exactly, and x, y, z
-// are combined in the same order.
-template <typename T>
-__device__ __forceinline__ T lin_half(const T* __restrict__ p, int s, T t) {
-  if (t == (T)0) return p[0];
-  if (t == (T)1) return p[s];
-  return p[0] * (T)0.5 + p[s] * (T)0.5;
-}
-template <typename T>
-__device__ __forceinline__ T gather_half(const T* __restrict__ a, int ex, int ey, int ez, int i0, int j0, int k0,
-                                         T tx, T ty, T tz) {
-  const int sx = ex > 1 ? 1 : 0, sy = ey > 1 ? ex : 0, sz = ez > 1 ? ex * ey : 0;
-  const T* b = a + (k0 * ey + j0) * ex + i0;
-  auto plane = [&](const T* q) -> T {
-    if (ty == (T)0) return lin_half(q, sx, tx);
-    if (ty == (T)1) return lin_half(q + sy, sx, tx);
-    return lin_half(q, sx, tx) * (T)0.5 + lin_half(q + sy, sx, tx) * (T)0.5;
-  };
-  if (tz == (T)0) return plane(b);
-  if (tz == (T)1) return plane(b + sz);
-  return plane(b) * (T)0.5 + plane(b + sz) * (T)0.5;
-}
-
 // The same gather at a point i + half/2 on one axis (half in {-1, 0, 1}):
 // floor, clamp and fraction in integer arithmetic.  Every value involved is
 // an exact small integer or half, so i0 and t equal gather()'s bit for bit.

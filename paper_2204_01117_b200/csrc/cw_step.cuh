@@ -108,24 +108,45 @@ __device__ __forceinline__ void comp_offset(int comp, float& ox, float& oy, floa
 }
 
 // Velocity of the pre-advection field at the face point of component `comp`
-// with integer index (i, j, k): the point sits at fixed half-cell offsets from
-// every velocity grid, so the gathers take the integer path (axis_at).
+// with integer index (i, j, k) (advection.py:16-21, 49-101).  The point sits at
+// fixed half-cell offsets from every velocity grid, so the trilinear weights are
+// 0, 1/2 or 1: a weight-1/2 pair is an exact average, and at the domain edge the
+// clamped pair averages a value with itself (exact).  This equals the general
+// trilinear gather bit for bit (x, then y, then z, as gather_at) with 9 loads
+// and straight-line index arithmetic.
 template <typename T>
-__device__ __forceinline__ void velocity_at(const Dims& d, int comp, const T* u, const T* v, const T* w,
-                                            int i, int j, int k, T& us, T& vs, T& ws) {
-  // half-offsets (in units of 0.5 cell) of the face point minus each grid's offset
-  const int hx = comp == 0 ? 0 : 1, hy = comp == 1 ? 0 : 1, hz = comp == 2 ? 0 : 1;
-  int i0, j0, k0;
-  T tx, ty, tz;
-  // u grid: offsets (0, .5, .5), extents (nx+1, ny, nz)
-  axis_at<T>(i, hx, d.nx + 1, i0, tx); axis_at<T>(j, hy - 1, d.ny, j0, ty); axis_at<T>(k, hz - 1, d.nz, k0, tz);
-  us = gather_half<T>(u, d.nx + 1, d.ny, d.nz, i0, j0, k0, tx, ty, tz);
-  // v grid: offsets (.5, 0, .5)
-  axis_at<T>(i, hx - 1, d.nx, i0, tx); axis_at<T>(j, hy, d.ny + 1, j0, ty); axis_at<T>(k, hz - 1, d.nz, k0, tz);
-  vs = gather_half<T>(v, d.nx, d.ny + 1, d.nz, i0, j0, k0, tx, ty, tz);
-  // w grid: offsets (.5, .5, 0)
-  axis_at<T>(i, hx - 1, d.nx, i0, tx); axis_at<T>(j, hy - 1, d.ny, j0, ty); axis_at<T>(k, hz, d.nz + 1, k0, tz);
-  ws = gather_half<T>(w, d.nx, d.ny, d.nz + 1, i0, j0, k0, tx, ty, tz);
+__device__ __forceinline__ T avg2(T a, T b) { return a * (T)0.5 + b * (T)0.5; }
+
+template <typename T>
+__device__ __forceinline__ void face_velocity(const Dims& d, int comp, const T* __restrict__ u,
+                                              const T* __restrict__ v, const T* __restrict__ w, int i, int j, int k,
+                                              T& us, T& vs, T& ws) {
+  const int nx = d.nx, ny = d.ny, nz = d.nz;
+  const int uy = nx + 1, uz = (nx + 1) * ny;     // u strides
+  const int vy = nx, vz = nx * (ny + 1);         // v strides
+  const int wy = nx, wz = nx * ny;               // w strides
+  if (comp == 0) {           // u face: i in 0..nx, j < ny, k < nz
+    const int im = max(i - 1, 0), ip = min(i, nx - 1);
+    us = u[k * uz + j * uy + i];
+    const T* vr = v + k * vz + j * vy;           // rows j, j+1 of v on plane k
+    vs = avg2(avg2(vr[im], vr[ip]), avg2(vr[vy + im], vr[vy + ip]));
+    const T* wr = w + k * wz + j * wy;           // planes k, k+1 of w on row j
+    ws = avg2(avg2(wr[im], wr[ip]), avg2(wr[wz + im], wr[wz + ip]));
+  } else if (comp == 1) {    // v face: i < nx, j in 0..ny, k < nz
+    const int jm = max(j - 1, 0), jp = min(j, ny - 1);
+    vs = v[k * vz + j * vy + i];
+    const T* ur = u + k * uz + i;
+    us = avg2(avg2(ur[jm * uy], ur[jm * uy + 1]), avg2(ur[jp * uy], ur[jp * uy + 1]));
+    const T* wr = w + k * wz + i;
+    ws = avg2(avg2(wr[jm * wy], wr[jp * wy]), avg2(wr[wz + jm * wy], wr[wz + jp * wy]));
+  } else {                   // w face: i < nx, j < ny, k in 0..nz
+    const int km = max(k - 1, 0), kp = min(k, nz - 1);
+    ws = w[k * wz + j * wy + i];
+    const T* ur = u + j * uy + i;
+    us = avg2(avg2(ur[km * uz], ur[km * uz + 1]), avg2(ur[kp * uz], ur[kp * uz + 1]));
+    const T* vr = v + j * vy + i;
+    vs = avg2(avg2(vr[km * vz], vr[km * vz + vy]), avg2(vr[kp * vz], vr[kp * vz + vy]));
+  }
 }
 
 // One thread per (i, j, k) of the union of the face extents handles the u, v
@@ -143,7 +164,7 @@ __device__ __forceinline__ void mac_predict_face(const Dims& d, int comp, const 
   const int c = ((int)k * ey + j) * ex + i;
   const T X = (T)i + ox, Y = (T)j + oy, Z = (T)k + oz;
   T us, vs, ws;
-  velocity_at<T>(d, comp, u, v, w, i, j, k, us, vs, ws);
+  face_velocity<T>(d, comp, u, v, w, i, j, k, us, vs, ws);
   const T bx = X - dt * us * inv_h<T>(d, 0), by = Y - dt * vs * inv_h<T>(d, 1), bz = Z - dt * ws * inv_h<T>(d, 2);
   ahead[c] = gather<T>(arr, ex, ey, ez, bx - ox, by - oy, bz - oz, nullptr, nullptr);
 }
@@ -177,7 +198,7 @@ __device__ __forceinline__ void mac_correct_face(const Dims& d, int comp, const 
   const int c = ((int)k * ey + j) * ex + i;
   const T X = (T)i + ox, Y = (T)j + oy, Z = (T)k + oz;
   T us, vs, ws;
-  velocity_at<T>(d, comp, u, v, w, i, j, k, us, vs, ws);
+  face_velocity<T>(d, comp, u, v, w, i, j, k, us, vs, ws);
   T mn, mx;
   const T sx = dt * us * inv_h<T>(d, 0), sy = dt * vs * inv_h<T>(d, 1), sz = dt * ws * inv_h<T>(d, 2);
   const T bx = X - sx, by = Y - sy, bz = Z - sz;
