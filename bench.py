@@ -33,6 +33,8 @@ PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
 # algorithmic bytes: per step 164*N + 44*I*Nu (+8*Nu); the PCG
 # launch moves 20*N (divergence -> r0) + 8*Nu (z0 = W r0) + 44*I*Nu
 PCG_B_PER_UNKNOWN_ITER = 44
+ADV_PREDICT_B_PER_CELL = 40   # SURVEY.md 8d phase P1: 5 fields in, 5 out, fp32
+ADV_CORRECT_B_PER_CELL = 36   # 6 fields in (velocity, predictor), 3 out, fp32
 # PCG iterations of C3 steps 1..60 at dt 0.2 (device run; the parity gates
 # hold the device's per-step counts equal to the reference's) -- used only to
 # extrapolate the CPU reference's bounded samples to the same steps the B200
@@ -386,6 +388,11 @@ def run_b200(args):
     got = C.c_int()
     N.check(lib.cw_read_pcg_timing(ctx.h, pcg_ms, args.steps, C.byref(got)))
     pcg_ms = np.array(pcg_ms[:got.value], float)
+    pred_ms, corr_ms = (C.c_float * args.steps)(), (C.c_float * args.steps)()
+    got_a = C.c_int()
+    N.check(lib.cw_read_adv_timing(ctx.h, pred_ms, corr_ms, args.steps, C.byref(got_a)))
+    pred_ms = np.array(pred_ms[:got_a.value], float)
+    corr_ms = np.array(corr_ms[:got_a.value], float)
     ms_max = ms
     if dist is not None:
         t = torch.tensor([ms], device="cuda", dtype=torch.float64)
@@ -413,6 +420,17 @@ def run_b200(args):
                 "bytes_model": "20*N + 8*Nu + 44*I*Nu per launch (SURVEY.md 8d, fp32 vectors)",
                 "pcg_ms_per_launch": float(np.mean(pcg_ms)) if len(pcg_ms) else None,
                 "pcg_share_of_step": float(np.sum(pcg_ms) / ms) if len(pcg_ms) else None}
+    # the advection kernels (MacCormack predictor with the k/omega upwind, corrector)
+    adv = {}
+    for name, t_ms, bpc, what in (
+            ("k_mac_predict", pred_ms, ADV_PREDICT_B_PER_CELL, "u,v,w,k,omega in; u~,v~,w~,k',omega' out"),
+            ("k_mac_correct", corr_ms, ADV_CORRECT_B_PER_CELL, "u,v,w and u~,v~,w~ in; u',v',w' out")):
+        if len(t_ms):
+            ach = bpc * ncell / (np.mean(t_ms) * 1e-3) / 1e9
+            adv[name] = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+                         "us_per_launch": float(np.mean(t_ms) * 1e3),
+                         "bytes_model": f"{bpc} B/cell ({what}), fp32"}
+    roofline["advection"] = adv
 
     # end to end through the reference-facing API: host state in, host state out
     names = ("u", "v", "w", "p", "k", "omega", "nu_t")

@@ -206,6 +206,10 @@ int cw_read_stage_timings(cw_ctx *ctx, float out_ms[7]);
  * the call), and the number of kernels this context has enqueued. */
 int cw_pcg_timing(cw_ctx *ctx, int max_launches);
 int cw_read_pcg_timing(cw_ctx *ctx, float *ms, int n, int *n_out);
+/* device time of the MacCormack predictor and corrector launches of the steps
+   timed since cw_pcg_timing (bench.py advection roofline); no reference
+   counterpart (instrumentation) */
+int cw_read_adv_timing(cw_ctx *ctx, float *predict_ms, float *correct_ms, int n, int *n_out);
 long long cw_launch_count(cw_ctx *ctx, int reset);
 
 /* region_average_speed (ref solver.py:535-549) for n boxes in one pass:

@@ -129,6 +129,8 @@ SIGNATURES = {
     "cw_read_stage_timings": (C.c_int, [_P, C.POINTER(C.c_float)]),
     "cw_pcg_timing": (C.c_int, [_P, C.c_int]),
     "cw_read_pcg_timing": (C.c_int, [_P, C.POINTER(C.c_float), C.c_int, C.POINTER(C.c_int)]),
+    "cw_read_adv_timing": (C.c_int, [_P, C.POINTER(C.c_float), C.POINTER(C.c_float), C.c_int,
+                                     C.POINTER(C.c_int)]),
     "cw_launch_count": (C.c_longlong, [_P, C.c_int]),
     "cw_region_speed": (C.c_int, [_P, C.POINTER(cw_fields), C.c_int, C.POINTER(C.c_double),
                                   C.POINTER(C.c_double), C.POINTER(C.c_double),

@@ -109,6 +109,9 @@ struct cw_ctx {
   // per-launch device time of the PCG kernel (bench roofline), when enabled
   std::vector<cudaEvent_t> pev;
   int pcg_timed = 0;
+  // advection kernels (bench roofline): before predict, after predict, after correct
+  std::vector<cudaEvent_t> aev;
+  int adv_timed = 0;
 };
 
 extern "C" int cw_abi_version(void) { return CW_ABI_VERSION; }
@@ -343,6 +346,7 @@ extern "C" void cw_ctx_destroy(cw_ctx* c) {
   if (c->ev_made)
     for (auto& e : c->ev) cudaEventDestroy(e);
   for (auto& e : c->pev) cudaEventDestroy(e);
+  for (auto& e : c->aev) cudaEventDestroy(e);
   delete c;
 }
 
@@ -683,12 +687,16 @@ static void st_advect(cw_ctx* c, const StepPtrs<T>& P, const cw_params* prm, T* 
   const Dims& d = c->d;
   const T dt = (T)prm->dt;
   const bool turb = prm->turbulence != 0;    // upwind k, omega ride along in the predictor launch
+  const bool timed = c->adv_timed < (int)c->aev.size() / 3;
+  if (timed) cudaEventRecord(c->aev[3 * c->adv_timed], st);
   (k_mac_predict<T><<<g3(d.nx + 1, d.ny + 1, d.nz + 1), B3, 0, st>>>(
        d, P.u, P.v, P.w, (T*)c->ahead[0], (T*)c->ahead[1], (T*)c->ahead[2], dt, (const T*)P.k, (const T*)P.om,
        turb ? kout : (T*)nullptr, turb ? wout : (T*)nullptr, c->gate), ++c->launches);
+  if (timed) cudaEventRecord(c->aev[3 * c->adv_timed + 1], st);
   (k_mac_correct<T><<<g3(d.nx + 1, d.ny + 1, d.nz + 1), B3, 0, st>>>(
        d, P.u, P.v, P.w, (const T*)c->ahead[0], (const T*)c->ahead[1], (const T*)c->ahead[2], (T*)c->adv[0],
        (T*)c->adv[1], (T*)c->adv[2], dt, c->gate), ++c->launches);
+  if (timed) cudaEventRecord(c->aev[3 * c->adv_timed++ + 2], st);
 }
 
 template <typename T>
@@ -1170,6 +1178,10 @@ extern "C" int cw_pcg_timing(cw_ctx* c, int max_launches) {
   c->pev.assign(2 * (size_t)max_launches, nullptr);
   for (auto& e : c->pev) CW_CUDA(cudaEventCreate(&e));
   c->pcg_timed = 0;
+  for (auto& e : c->aev) cudaEventDestroy(e);
+  c->aev.assign(3 * (size_t)max_launches, nullptr);
+  for (auto& e : c->aev) CW_CUDA(cudaEventCreate(&e));
+  c->adv_timed = 0;
   return CW_OK;
 }
 
@@ -1183,6 +1195,20 @@ extern "C" int cw_read_pcg_timing(cw_ctx* c, float* ms, int n, int* n_out) {
   }
   if (n_out) *n_out = m;
   c->pcg_timed = 0;
+  return CW_OK;
+}
+
+extern "C" int cw_read_adv_timing(cw_ctx* c, float* predict_ms, float* correct_ms, int n, int* n_out) {
+  if (!c) return fail(CW_ERR_INVALID, "null argument");
+  CW_CUDA(cudaSetDevice(c->device));
+  const int m = std::min(n, c->adv_timed);
+  for (int i = 0; i < m; ++i) {
+    CW_CUDA(cudaEventSynchronize(c->aev[3 * i + 2]));
+    CW_CUDA(cudaEventElapsedTime(&predict_ms[i], c->aev[3 * i], c->aev[3 * i + 1]));
+    CW_CUDA(cudaEventElapsedTime(&correct_ms[i], c->aev[3 * i + 1], c->aev[3 * i + 2]));
+  }
+  if (n_out) *n_out = m;
+  c->adv_timed = 0;
   return CW_OK;
 }
 
