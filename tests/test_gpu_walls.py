@@ -48,3 +48,45 @@ def test_interior_walls_match_oracle(prec):
     # no-slip: every face touching a wall cell is zero
     u = got["u"]
     assert np.all(u[1:6, 7:13, 10:15] == 0.0)
+
+
+def test_boundary_lists_follow_labels_changed_in_place():
+    """The boundary writes replay per-labels lists (cw_capi.cu build_bc_lists):
+    changing the labels of a state in place (same device tensor) must rebuild
+    them -- the result equals the oracle's apply_boundary_conditions
+    (solver.py:330-400) on the new labels, bit for bit in float64."""
+    from oracle import citywind_oracle as co
+    from paper_2204_01117_b200 import solver
+    doc = scenes.cuboid(24, 16, 8, 1.0, 0.1)
+    doc["objects"] = []
+    sc = co.scene_from_dict(doc)
+    g = sc.grid
+    labels = co.classify_boundary(g, sc.faces)
+    phi, lad = np.ones(g.cshape), np.zeros(g.cshape)
+    ost = co.make_initial_state(g, labels, phi, lad, sc.params, sc.inlet, mode="rest")
+    rng = np.random.default_rng(5)
+    for n in FIELDS:
+        setattr(ost, n, rng.standard_normal(getattr(ost, n).shape))
+    dst = device_state(ost, torch.float64)
+    p, prof = device_params(sc)
+    solver.apply_boundary_conditions(dst, prof, p)        # builds the lists for the first labels
+    co.apply_boundary_conditions(ost, sc.inlet, sc.params)
+    got = fields_of(dst)
+    for n in FIELDS:
+        np.testing.assert_array_equal(got[n], getattr(ost, n), err_msg=n)
+    # new labels, written into the same device tensor: an interior wall block
+    # and an outlet patch turned into wall
+    lab2 = labels.copy()
+    lab2[2:5, 5:9, 8:12] = 5
+    lab2[-1, :, :4] = 5
+    dst.labels_dev.copy_(torch.from_numpy(np.ascontiguousarray(lab2)).to(dst.labels_dev.device))
+    ost.labels = lab2
+    for n in FIELDS:
+        a = rng.standard_normal(getattr(ost, n).shape)
+        setattr(ost, n, a)
+        dst.fields[n].copy_(torch.from_numpy(np.ascontiguousarray(a)))
+    solver.apply_boundary_conditions(dst, prof, p)
+    co.apply_boundary_conditions(ost, sc.inlet, sc.params)
+    got = fields_of(dst)
+    for n in FIELDS:
+        np.testing.assert_array_equal(got[n], getattr(ost, n), err_msg=n)
