@@ -63,13 +63,9 @@ __device__ __forceinline__ T gather_at(const T* __restrict__ a, int ex, int ey, 
   const T c00 = c000 * ox + c100 * tx, c10 = c010 * ox + c110 * tx;
   const T c01 = c001 * ox + c101 * tx, c11 = c011 * ox + c111 * tx;
   const T c0 = c00 * oy + c10 * ty, c1 = c01 * oy + c11 * ty;
-  if (mn) {
-    T lo = c000, hi = c000;
-#define CW_MM(v) lo = (v) < lo ? (v) : lo; hi = (v) > hi ? (v) : hi;
-    CW_MM(c100) CW_MM(c010) CW_MM(c110) CW_MM(c001) CW_MM(c101) CW_MM(c011) CW_MM(c111)
-#undef CW_MM
-    *mn = lo;
-    *mx = hi;
+  if (mn) {   // the stencil's min / max (finite values: order-independent, one FMNMX each)
+    *mn = fmin(fmin(fmin(c000, c100), fmin(c010, c110)), fmin(fmin(c001, c101), fmin(c011, c111)));
+    *mx = fmax(fmax(fmax(c000, c100), fmax(c010, c110)), fmax(fmax(c001, c101), fmax(c011, c111)));
   }
   return c0 * oz + c1 * tz;
 }
