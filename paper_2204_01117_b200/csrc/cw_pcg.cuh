@@ -297,7 +297,10 @@ struct StageLayout {
   static constexpr int B_C = B_AP + align128((int)Halo<T>::BYTES);
   static constexpr int B_END = B_C + align128((int)Halo<uint8_t>::BYTES);
   static constexpr int STAGE = A_END > B_END ? A_END : B_END;
-  static constexpr int DEPTH = sizeof(T) == 4 ? 4 : 3;
+#ifndef CW_PCG_DEPTH
+#define CW_PCG_DEPTH 4
+#endif
+  static constexpr int DEPTH = sizeof(T) == 4 ? CW_PCG_DEPTH : 3;
   static constexpr unsigned BYTES_A_HALO = 2u * Halo<T>::BYTES;
   static constexpr unsigned BYTES_A_X = PCG_TX * PCG_TY * (sizeof(T) + 1);   // x + code, own box
   static constexpr unsigned BYTES_B = Halo<double>::BYTES + Halo<T>::BYTES + Halo<uint8_t>::BYTES;
