@@ -778,11 +778,16 @@ __device__ void phaseA(const PcgArgs<T>& A, const Blk& blk, double* part, PcgSha
       }
       const bool live = cursor_next<T>(A, cons);
       ++j;
-      __syncthreads();   // every thread is done with this job's stage: refill it
-      if (threadIdx.x == 0) ring_fill<T>(A, prod, more, issued, j + L::DEPTH, issue);
       return live;
     };
-    while (plane(pa, pb) && plane(pb, pa)) {
+    // two planes per block barrier: their dependent chains interleave (the
+    // second plane's stage is waited for before the first one is computed)
+    for (;;) {
+      const bool live = plane(pa, pb);
+      const bool live2 = live && plane(pb, pa);
+      __syncthreads();   // every thread is done with these jobs' stages: refill them
+      if (threadIdx.x == 0) ring_fill<T>(A, prod, more, issued, j + L::DEPTH, issue);
+      if (!live2) break;
     }
     if (timing && threadIdx.x == 0) S.pt[2] = globaltimer();
     ticket = t0 + j;
