@@ -570,7 +570,7 @@ __device__ __forceinline__ double ap_finish(ApAcc<T> part, T wz, T pc, T pzp, bo
 // fields hold < 2^31 elements, cw_capi.cu).
 constexpr int QX = PCG_TX / 4;
 #ifndef CW_ABL
-#define CW_ABL 0   // developer ablations of phase B (timing only; results are wrong when set)
+#define CW_ABL 0   // developer ablations (timing only; results are wrong when set): B ring 1, B y edge 2, B stores 4, B pass 2 8, A stores 16
 #endif
 static_assert(PCG_THREADS == QX * PCG_TY, "one thread per x quad of a 32 x 32 plane");
 
@@ -727,7 +727,7 @@ __device__ void phaseA(const PcgArgs<T>& A, const Blk& blk, double* part, PcgSha
             apv[c] = (T)ap;
             acc += (double)pcur[c] * ap;
           }
-          if (rows) {
+          if (rows && !(CW_ABL & 16)) {
             const int g = (kk - 1) * pplane + e;
             stg4h<T>(pout + g, pcur, drop);
             stg4h<T>(apout + g, apv, keep);
