@@ -237,6 +237,63 @@ def step(state: FlowState, params: SolverParams, psys: PressureSystem, precondit
     return reps[0] if reps else StepReport()
 
 
+class HostStepper:
+    """Steps a host-resident state: the reference's drop-in for callers whose
+    ``FlowState`` lives in host memory (solver.py:407-461 on numpy arrays).
+
+    ``host`` maps the seven field names to pinned CPU tensors in the device
+    layout; ``state`` is the device ``FlowState`` the steps run on.  Every
+    ``step`` uploads all seven fields, runs one step and downloads all seven
+    fields again.  The copies run on their own streams, in pieces (CHUNKS per
+    field), and overlap across the two copy directions: a piece of step s+1
+    starts uploading as soon as the same piece of step s is back in host
+    memory, while the later pieces are still coming down.  ``synchronize()``
+    waits for the last download.
+    """
+
+    CHUNKS = 1   # pieces per field (4 measured the same at C3: the duplex link is the limit)
+
+    def __init__(self, state: FlowState, host: dict):
+        from .grid import FIELDS
+        self.names = FIELDS
+        self.state = state
+        self.host = host
+        dev = state.fields[self.names[0]].device
+        self._up = torch.cuda.Stream(dev)
+        self._down = torch.cuda.Stream(dev)
+        # (device piece, host piece) views, and the events marking each piece back on the host
+        self._pieces = []
+        for n in self.names:
+            d, h = state.fields[n].view(-1), host[n].view(-1)
+            b = np.linspace(0, d.numel(), self.CHUNKS + 1).astype(int)
+            self._pieces += [(d[b[q]:b[q + 1]], h[b[q]:b[q + 1]]) for q in range(self.CHUNKS)]
+        self._back = [None] * len(self._pieces)
+
+    def step(self, params: SolverParams, psys: PressureSystem, preconditioner, profile: InletProfile,
+             pcg_tol: float | None = None) -> StepReport:
+        cur = torch.cuda.current_stream()
+        with torch.cuda.stream(self._up):
+            for q, (d, h) in enumerate(self._pieces):
+                if self._back[q] is not None:
+                    self._up.wait_event(self._back[q])
+                d.copy_(h, non_blocking=True)
+        cur.wait_stream(self._up)
+        rep = step(self.state, params, psys, preconditioner, profile, pcg_tol=pcg_tol)
+        done = torch.cuda.Event()
+        done.record(cur)
+        with torch.cuda.stream(self._down):
+            self._down.wait_event(done)
+            for q, (d, h) in enumerate(self._pieces):
+                h.copy_(d, non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(self._down)
+                self._back[q] = ev
+        return rep
+
+    def synchronize(self):
+        self._down.synchronize()
+
+
 def step_many(state: FlowState, params: SolverParams, psys: PressureSystem, preconditioner,
               profile: InletProfile, nsteps: int, pcg_tol: float | None = None,
               stage_timings: bool = False, read_back: bool = True) -> list:

@@ -129,3 +129,26 @@ def test_gradient_descent_trajectory_matches_oracle():
         np.testing.assert_allclose(a, b, rtol=1e-4, atol=1e-4 * max(1.0, float(np.abs(b).max())))
     np.testing.assert_allclose(res.history, losses, rtol=1e-4)
     assert not np.allclose(thetas[0], thetas[-1])      # the design moved
+
+
+def test_host_stepper_equals_device_steps():
+    """HostStepper (host-resident state, overlapped upload/download per field)
+    gives bit for bit the fields of the same steps on a device-resident state."""
+    from paper_2204_01117_b200 import solver
+    from paper_2204_01117_b200.grid import FIELDS as NAMES
+    from paper_2204_01117_b200.scenario import CompiledScenario, scenario_from_dict
+    comp = CompiledScenario.compile(scenario_from_dict(scenes.cuboid(24, 24, 12, 2.0, 0.3, steps=6)))
+    sc = comp.scenario
+    ref = comp.make_state()
+    work = ref.copy()
+    host = {n: torch.empty(ref.fields[n].shape, dtype=ref.fields[n].dtype, pin_memory=True) for n in NAMES}
+    for n in NAMES:
+        host[n].copy_(ref.fields[n])
+        work.fields[n].zero_()                      # the device copy is overwritten by every upload
+    stepper = solver.HostStepper(work, host)
+    its = [stepper.step(sc.solver, comp.psys, comp.preconditioner, sc.inlet).pcg.iterations for _ in range(6)]
+    stepper.synchronize()
+    want = solver.step_many(ref, sc.solver, comp.psys, comp.preconditioner, sc.inlet, 6)
+    assert its == [r.pcg.iterations for r in want]
+    for n in NAMES:
+        assert torch.equal(host[n], ref.fields[n].cpu()), n
