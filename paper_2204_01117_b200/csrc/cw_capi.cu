@@ -356,9 +356,11 @@ static inline dim3 g3(int ex, int ey, int ez) {   // 3-D stage-kernel grid (cw_s
               (unsigned)((ez + ST_BZ - 1) / ST_BZ));
 }
 static const dim3 B3(ST_BX, ST_BY, ST_BZ);
-// owned-plane reductions (CW_IJK_OWN): one plane per block
+// owned-plane max reductions (k_div_max, k_speed_max): each block strides
+// over the planes, about 2048 blocks in all, one atomic per block
 static inline dim3 g3r(int ex, int ey, int nz) {
-  return dim3((unsigned)((ex + ST_BX - 1) / ST_BX), (unsigned)((ey + 7) / 8), (unsigned)nz);
+  const int bx = (ex + ST_BX - 1) / ST_BX, by = (ey + 7) / 8;
+  return dim3((unsigned)bx, (unsigned)by, (unsigned)std::max(1, std::min(nz, 2048 / std::max(1, bx * by))));
 }
 static const dim3 B3R(ST_BX, 8, 1);
 static inline dim3 g3c(const Dims& d, int comp) {

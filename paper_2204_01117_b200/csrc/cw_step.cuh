@@ -54,13 +54,6 @@ constexpr int ST_BX = 32, ST_BY = CW_ST_BY, ST_BZ = CW_ST_BZ;
   const int j = (int)(blockIdx.y * ST_BY + threadIdx.y);         \
   const int k = (int)(blockIdx.z * ST_BZ + threadIdx.z);         \
   const bool inb = i < (ex) && j < (ey) && k < (ez)
-// the same over the owned planes of a z-slab window only (grid z = o1 - o0 [+1])
-#define CW_IJK_OWN(ex, ey, kend, inb)                            \
-  const int i = (int)(blockIdx.x * ST_BX + threadIdx.x);         \
-  const int j = (int)(blockIdx.y * 8 + threadIdx.y);             \
-  const int k = d.o0 + (int)blockIdx.z;                          \
-  const bool inb = i < (ex) && j < (ey) && k < (kend)
-
 __device__ __forceinline__ int clampi(int a, int lo, int hi) { return a < lo ? lo : (a > hi ? hi : a); }
 
 // ---------------------------------------------------------------------------
@@ -617,15 +610,19 @@ __global__ void k_div_max(Dims d, const T* __restrict__ u, const T* __restrict__
   if (*gate) return;
   __shared__ T scratch[32];
   T m = (T)0;
-  CW_IJK_OWN(d.nx, d.ny, d.o1, inb);
-  const int c = d.cidx32(i, j, k);
-  if (inb && is_unknown(lab[c])) {
-    const int ui = ((int)k * d.ny + j) * (d.nx + 1) + i;
-    const int vi = ((int)k * (d.ny + 1) + j) * d.nx + i;
-    T div = (u[ui + 1] - u[ui]) * inv_h<T>(d, 0) + (v[vi + d.nx] - v[vi]) * inv_h<T>(d, 1);
-    if (!d.is2d) div = div + (w[c + (int)d.nx * d.ny] - w[c]) * inv_h<T>(d, 2);
-    const T a = fabs(div);
-    m = (a > m || a != a) ? a : m;
+  // planes d.o0 + blockIdx.z, + gridDim.z, ...: a few blocks per column, one atomic each
+  const int i = (int)(blockIdx.x * ST_BX + threadIdx.x), j = (int)(blockIdx.y * 8 + threadIdx.y);
+  if (i < d.nx && j < d.ny) {
+    for (int k = d.o0 + (int)blockIdx.z; k < d.o1; k += (int)gridDim.z) {
+      const int c = d.cidx32(i, j, k);
+      if (!is_unknown(lab[c])) continue;
+      const int ui = ((int)k * d.ny + j) * (d.nx + 1) + i;
+      const int vi = ((int)k * (d.ny + 1) + j) * d.nx + i;
+      T div = (u[ui + 1] - u[ui]) * inv_h<T>(d, 0) + (v[vi + d.nx] - v[vi]) * inv_h<T>(d, 1);
+      if (!d.is2d) div = div + (w[c + (int)d.nx * d.ny] - w[c]) * inv_h<T>(d, 2);
+      const T a = fabs(div);
+      m = (a > m || a != a) ? a : m;
+    }
   }
   m = block_max_2d(m, scratch);
   if (threadIdx.x == 0 && threadIdx.y == 0) report_max<T>(rep, slot, m);
@@ -640,15 +637,17 @@ __global__ void k_speed_max(Dims d, const T* __restrict__ u, const T* __restrict
   if (*gate) return;
   __shared__ T scratch[32];
   T m = (T)0;
-  CW_IJK_OWN(d.nx + 1, d.ny + 1, d.o1 + 1, inb);
-  if (inb) {
-    if (k < d.o1) {
-      if (j < d.ny) { const T a = fabs(u[((int)k * d.ny + j) * (d.nx + 1) + i]); m = (a > m || a != a) ? a : m; }
-      if (i < d.nx) { const T a = fabs(v[((int)k * (d.ny + 1) + j) * d.nx + i]); m = (a > m || a != a) ? a : m; }
-    }
-    if (i < d.nx && j < d.ny) {
-      const T a = fabs(w[((int)k * d.ny + j) * d.nx + i]);
-      m = (a > m || a != a) ? a : m;
+  const int i = (int)(blockIdx.x * ST_BX + threadIdx.x), j = (int)(blockIdx.y * 8 + threadIdx.y);
+  if (i < d.nx + 1 && j < d.ny + 1) {
+    for (int k = d.o0 + (int)blockIdx.z; k < d.o1 + 1; k += (int)gridDim.z) {
+      if (k < d.o1) {
+        if (j < d.ny) { const T a = fabs(u[((int)k * d.ny + j) * (d.nx + 1) + i]); m = (a > m || a != a) ? a : m; }
+        if (i < d.nx) { const T a = fabs(v[((int)k * (d.ny + 1) + j) * d.nx + i]); m = (a > m || a != a) ? a : m; }
+      }
+      if (i < d.nx && j < d.ny) {
+        const T a = fabs(w[((int)k * d.ny + j) * d.nx + i]);
+        m = (a > m || a != a) ? a : m;
+      }
     }
   }
   m = block_max_2d(m, scratch);
