@@ -356,6 +356,11 @@ static inline dim3 g3(int ex, int ey, int ez) {   // 3-D stage-kernel grid (cw_s
               (unsigned)((ez + ST_BZ - 1) / ST_BZ));
 }
 static const dim3 B3(ST_BX, ST_BY, ST_BZ);
+// z-coarsened stage kernels (CW_ZT planes per thread)
+static inline dim3 g3z(int ex, int ey, int ez) {
+  return dim3((unsigned)((ex + ST_BX - 1) / ST_BX), (unsigned)((ey + ST_BY - 1) / ST_BY),
+              (unsigned)((ez + CW_ZT - 1) / CW_ZT));
+}
 // owned-plane max reductions (k_div_max, k_speed_max): each block strides
 // over the planes, about 2048 blocks in all, one atomic per block
 static inline dim3 g3r(int ex, int ey, int nz) {
@@ -708,7 +713,7 @@ static void st_diffuse(cw_ctx* c, const StepPtrs<T>& P, const cw_params* prm, cu
   T* cu[3] = {P.u, P.v, P.w};
   double cap = nu_stable<T>(c, prm->dt) - prm->nu;
   if (cap <= 0) cap = 0.0;                               // solver.py:195-201
-  (k_diffuse<T><<<g3(d.nx + 1, d.ny + 1, d.nz + 1), B3, 0, st>>>(
+  (k_diffuse<T><<<g3z(d.nx + 1, d.ny + 1, d.nz + 1), B3, 0, st>>>(
        d, (const T*)c->adv[0], (const T*)c->adv[1], (const T*)c->adv[2], cu[0], cu[1], cu[2], P.nut, (T)prm->dt,
        (T)prm->nu, (T)cap, c->gate), ++c->launches);
 }
@@ -748,7 +753,7 @@ template <typename T>
 static void st_project_tail(cw_ctx* c, const StepPtrs<T>& P, const cw_params* prm, DevReport* rep, cudaStream_t st) {
   const Dims& d = c->d;
   T* cu[3] = {P.u, P.v, P.w};
-  (k_gradient<T><<<g3(d.nx + 1, d.ny + 1, d.nz + 1), B3, 0, st>>>(d, cu[0], cu[1], cu[2], P.p, P.lab, (T)prm->dt,
+  (k_gradient<T><<<g3z(d.nx + 1, d.ny + 1, d.nz + 1), B3, 0, st>>>(d, cu[0], cu[1], cu[2], P.p, P.lab, (T)prm->dt,
                                                                     c->gate), ++c->launches);
   (k_div_max<T><<<g3r(d.nx, d.ny, d.o1 - d.o0), B3R, 0, st>>>(d, P.u, P.v, P.w, P.lab, rep, SLOT_DIV_AFTER, c->gate), ++c->launches);
 }
@@ -763,7 +768,8 @@ static void st_turb(cw_ctx* c, const StepPtrs<T>& P, const cw_params* prm, const
   sc.c_mu = prm->c_mu; sc.alpha = prm->alpha; sc.beta = prm->beta;
   sc.sigma = prm->sigma; sc.sigma_star = prm->sigma_star; sc.c_lim = prm->c_lim;
   sc.k_in = prm->k_in; sc.om_in = prm->omega_in; sc.nut_in = prm->k_in / prm->omega_in;
-  (k_turbulence<T><<<g3(c->d.nx, c->d.ny, c->d.nz), B3, 0, st>>>(c->d, P.u, P.v, P.w, kin, win, P.k, P.om, P.nut, sc, rep, c->gate), ++c->launches);
+  (k_turbulence<T><<<dim3((c->d.nx + ST_BX - 1) / ST_BX, (c->d.ny + ST_BY - 1) / ST_BY,
+                          (c->d.nz + ZT_TURB - 1) / ZT_TURB), B3, 0, st>>>(c->d, P.u, P.v, P.w, kin, win, P.k, P.om, P.nut, sc, rep, c->gate), ++c->launches);
   (k_turb_check<<<1, 1, 0, st>>>(rep, c->gate), ++c->launches);
 }
 
