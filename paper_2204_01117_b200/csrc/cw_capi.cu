@@ -696,11 +696,11 @@ static void st_advect(cw_ctx* c, const StepPtrs<T>& P, const cw_params* prm, T* 
   const bool turb = prm->turbulence != 0;    // upwind k, omega ride along in the predictor launch
   const bool timed = c->adv_timed < (int)c->aev.size() / 3;
   if (timed) cudaEventRecord(c->aev[3 * c->adv_timed], st);
-  (k_mac_predict<T><<<g3(d.nx + 1, d.ny + 1, d.nz + 1), B3, 0, st>>>(
+  (k_mac_predict<T><<<dim3((d.nx + 1 + ST_BX - 1) / ST_BX, (d.ny + 1 + ST_BY - 1) / ST_BY, (d.nz + 1 + ZT_MAC - 1) / ZT_MAC), B3, 0, st>>>(
        d, P.u, P.v, P.w, (T*)c->ahead[0], (T*)c->ahead[1], (T*)c->ahead[2], dt, (const T*)P.k, (const T*)P.om,
        turb ? kout : (T*)nullptr, turb ? wout : (T*)nullptr, c->gate), ++c->launches);
   if (timed) cudaEventRecord(c->aev[3 * c->adv_timed + 1], st);
-  (k_mac_correct<T><<<g3(d.nx + 1, d.ny + 1, d.nz + 1), B3, 0, st>>>(
+  (k_mac_correct<T><<<dim3((d.nx + 1 + ST_BX - 1) / ST_BX, (d.ny + 1 + ST_BY - 1) / ST_BY, (d.nz + 1 + ZT_MAC - 1) / ZT_MAC), B3, 0, st>>>(
        d, P.u, P.v, P.w, (const T*)c->ahead[0], (const T*)c->ahead[1], (const T*)c->ahead[2], (T*)c->adv[0],
        (T*)c->adv[1], (T*)c->adv[2], dt, c->gate), ++c->launches);
   if (timed) cudaEventRecord(c->aev[3 * c->adv_timed++ + 2], st);
@@ -725,7 +725,7 @@ static void st_drag(cw_ctx* c, const StepPtrs<T>& P, const cw_params* prm, int h
   const long long nf[3] = {c->nu_, c->nv_, c->nw_};
   T* cu[3] = {P.u, P.v, P.w};
   (k_cell_speed<T><<<g3(d.nx, d.ny, d.nz), B3, 0, st>>>(d, P.u, P.v, P.w, (T*)c->speed, c->gate), ++c->launches);
-  (k_drag<T><<<g3(d.nx + 1, d.ny + 1, d.nz + 1), B3, 0, st>>>(d, cu[0], cu[1], cu[2], P.g, (const T*)c->speed,
+  (k_drag<T><<<g3z(d.nx + 1, d.ny + 1, d.nz + 1), B3, 0, st>>>(d, cu[0], cu[1], cu[2], P.g, (const T*)c->speed,
                                                                 (T)prm->dt, c->gate), ++c->launches);
 }
 

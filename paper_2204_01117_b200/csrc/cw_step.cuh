@@ -62,6 +62,10 @@ constexpr int ST_BX = 32, ST_BY = CW_ST_BY, ST_BZ = CW_ST_BZ;
 #endif
 static_assert(ST_BZ == 1, "z-coarsened kernels take one plane per block row");
 constexpr int ZT_TURB = 1;   // k_turbulence: coarsening measured slower (90 -> 100 us at C3)
+#ifndef CW_ZT_MAC
+#define CW_ZT_MAC 2
+#endif
+constexpr int ZT_MAC = CW_ZT_MAC;   // MacCormack predictor / corrector
 
 __device__ __forceinline__ int clampi(int a, int lo, int hi) { return a < lo ? lo : (a > hi ? hi : a); }
 
@@ -179,12 +183,17 @@ __global__ void k_mac_predict(Dims d, const T* __restrict__ u, const T* __restri
                               T* __restrict__ a2, T dt, const T* __restrict__ kin, const T* __restrict__ win,
                               T* __restrict__ kout, T* __restrict__ wout, const int* gate) {
   if (*gate) return;
-  CW_IJK(d.nx + 1, d.ny + 1, d.nz + 1, inb);
-  if (!inb) return;
-  if (kout) upwind_cell<T>(d, u, v, w, kin, win, kout, wout, dt, i, j, k);
-  mac_predict_face<T>(d, 0, u, v, w, a0, dt, i, j, k);
-  mac_predict_face<T>(d, 1, u, v, w, a1, dt, i, j, k);
-  if (!d.is2d) mac_predict_face<T>(d, 2, u, v, w, a2, dt, i, j, k);
+  const int i = (int)(blockIdx.x * ST_BX + threadIdx.x), j = (int)(blockIdx.y * ST_BY + threadIdx.y);
+  if (i > d.nx || j > d.ny) return;
+#pragma unroll
+  for (int kz = 0; kz < ZT_MAC; ++kz) {
+    const int k = (int)blockIdx.z * ZT_MAC + kz;
+    if (k > d.nz) break;
+    if (kout) upwind_cell<T>(d, u, v, w, kin, win, kout, wout, dt, i, j, k);
+    mac_predict_face<T>(d, 0, u, v, w, a0, dt, i, j, k);
+    mac_predict_face<T>(d, 1, u, v, w, a1, dt, i, j, k);
+    if (!d.is2d) mac_predict_face<T>(d, 2, u, v, w, a2, dt, i, j, k);
+  }
 }
 
 template <typename T>
@@ -219,11 +228,16 @@ __global__ void k_mac_correct(Dims d, const T* __restrict__ u, const T* __restri
                               const T* __restrict__ a2, T* __restrict__ o0, T* __restrict__ o1,
                               T* __restrict__ o2, T dt, const int* gate) {
   if (*gate) return;
-  CW_IJK(d.nx + 1, d.ny + 1, d.nz + 1, inb);
-  if (!inb) return;
-  mac_correct_face<T>(d, 0, u, v, w, a0, o0, dt, i, j, k);
-  mac_correct_face<T>(d, 1, u, v, w, a1, o1, dt, i, j, k);
-  if (!d.is2d) mac_correct_face<T>(d, 2, u, v, w, a2, o2, dt, i, j, k);
+  const int i = (int)(blockIdx.x * ST_BX + threadIdx.x), j = (int)(blockIdx.y * ST_BY + threadIdx.y);
+  if (i > d.nx || j > d.ny) return;
+#pragma unroll
+  for (int kz = 0; kz < ZT_MAC; ++kz) {
+    const int k = (int)blockIdx.z * ZT_MAC + kz;
+    if (k > d.nz) break;
+    mac_correct_face<T>(d, 0, u, v, w, a0, o0, dt, i, j, k);
+    mac_correct_face<T>(d, 1, u, v, w, a1, o1, dt, i, j, k);
+    if (!d.is2d) mac_correct_face<T>(d, 2, u, v, w, a2, o2, dt, i, j, k);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -331,11 +345,16 @@ template <typename T>
 __global__ void k_drag(Dims d, T* __restrict__ u, T* __restrict__ v, T* __restrict__ w, const T* __restrict__ g,
                        const T* __restrict__ speed, T dt, const int* gate) {
   if (*gate) return;
-  CW_IJK(d.nx + 1, d.ny + 1, d.nz + 1, inb);
-  if (!inb) return;
-  drag_face<T>(d, 0, u, g, speed, dt, i, j, k);
-  drag_face<T>(d, 1, v, g, speed, dt, i, j, k);
-  if (!d.is2d) drag_face<T>(d, 2, w, g, speed, dt, i, j, k);
+  const int i = (int)(blockIdx.x * ST_BX + threadIdx.x), j = (int)(blockIdx.y * ST_BY + threadIdx.y);
+  if (i > d.nx || j > d.ny) return;
+#pragma unroll
+  for (int kz = 0; kz < CW_ZT; ++kz) {
+    const int k = (int)blockIdx.z * CW_ZT + kz;
+    if (k > d.nz) break;
+    drag_face<T>(d, 0, u, g, speed, dt, i, j, k);
+    drag_face<T>(d, 1, v, g, speed, dt, i, j, k);
+    if (!d.is2d) drag_face<T>(d, 2, w, g, speed, dt, i, j, k);
+  }
 }
 
 // ---------------------------------------------------------------------------
