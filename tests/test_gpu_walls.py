@@ -90,3 +90,28 @@ def test_boundary_lists_follow_labels_changed_in_place():
     got = fields_of(dst)
     for n in FIELDS:
         np.testing.assert_array_equal(got[n], getattr(ost, n), err_msg=n)
+
+
+def test_boundary_full_volume_path_without_labels_version(monkeypatch):
+    """labels_version 0 (a C caller that does not version its labels) keeps
+    the full-volume boundary kernels: same result as the oracle."""
+    from oracle import citywind_oracle as co
+    from paper_2204_01117_b200 import _native as N
+    from paper_2204_01117_b200 import solver
+    monkeypatch.setattr(N, "labels_version", lambda t: 0)
+    doc = scenes.cuboid(20, 12, 6, 1.0, 0.1)
+    sc = co.scene_from_dict(doc)
+    g = sc.grid
+    labels = co.classify_boundary(g, sc.faces)
+    labels[1:3, 3:6, 5:9] = 5
+    ost = co.make_initial_state(g, labels, np.ones(g.cshape), np.zeros(g.cshape), sc.params, sc.inlet, mode="rest")
+    rng = np.random.default_rng(9)
+    for n in FIELDS:
+        setattr(ost, n, rng.standard_normal(getattr(ost, n).shape))
+    dst = device_state(ost, torch.float64)
+    p, prof = device_params(sc)
+    solver.apply_boundary_conditions(dst, prof, p)
+    co.apply_boundary_conditions(ost, sc.inlet, sc.params)
+    got = fields_of(dst)
+    for n in FIELDS:
+        np.testing.assert_array_equal(got[n], getattr(ost, n), err_msg=n)
