@@ -767,6 +767,7 @@ static void st_turb(cw_ctx* c, const StepPtrs<T>& P, const cw_params* prm, const
   sc.cap_turb = std::max(nus - prm->nu, 0.0);            // turbulence.py:110
   sc.c_mu = prm->c_mu; sc.alpha = prm->alpha; sc.beta = prm->beta;
   sc.sigma = prm->sigma; sc.sigma_star = prm->sigma_star; sc.c_lim = prm->c_lim;
+  sc.lim_scale = (double)((T)2 / (T)prm->c_mu);   // the kernel's former per-cell (T)2 / (T)c_mu, bit for bit
   sc.k_in = prm->k_in; sc.om_in = prm->omega_in; sc.nut_in = prm->k_in / prm->omega_in;
   (k_turbulence<T><<<dim3((c->d.nx + ST_BX - 1) / ST_BX, (c->d.ny + ST_BY - 1) / ST_BY,
                           (c->d.nz + ZT_TURB - 1) / ZT_TURB), B3, 0, st>>>(c->d, P.u, P.v, P.w, kin, win, P.k, P.om, P.nut, sc, rep, c->gate), ++c->launches);

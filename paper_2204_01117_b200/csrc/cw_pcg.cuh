@@ -573,6 +573,8 @@ constexpr int QX = PCG_TX / 4;
 #define CW_ABL 0   // developer ablations (timing only; results are wrong when set): B ring 1, B y edge 2, B stores 4, B pass 2 8, A stores 16
 #endif
 static_assert(PCG_THREADS == QX * PCG_TY, "one thread per x quad of a 32 x 32 plane");
+static_assert(PCG_THREADS - (2 * (PCG_TX + 2) + 2 * PCG_TY) >= (PCG_TX + 1) + PCG_TY,
+              "the q ring and the y-tile edge run on disjoint warps");
 
 __device__ __forceinline__ float fmat(float a, float b, float c) { return __fmaf_rn(a, b, c); }
 __device__ __forceinline__ double fmat(double a, double b, double c) { return __fma_rn(a, b, c); }
@@ -835,11 +837,14 @@ __device__ void phaseB(const PcgArgs<T>& A, const Blk& blk, double* part, PcgSha
   const int o_r = HD::at(hy, hx0), o_a = H::at(hy, hx0), o_c = HC::at(hy, hx0);
   const int q_own = hy * PCG_QW + hx0 + PCG_QOFF, q_dn = q_own - PCG_QW, q_e = hy * PCG_QW + PCG_QOFF;
   const int y_own = ty * PCG_YP + 4 * tx, y_up = y_own + PCG_YP, y_e = ty * PCG_YP + PCG_TX;
-  // ring cell of q (threads < 132): rows 0 and 33, columns 0 and 33
+  // ring cell of q (pass 1): rows 0 and 33, columns 0 and 33, on the last 132
+  // threads (warps 3-7); the y-tile edge of pass 2 runs on warps 0-2, so no
+  // warp carries extra work in both passes
   const int t = threadIdx.x;
-  const bool ring_t = t < 2 * HW + 2 * PCG_TY;
-  const int ry = t < HW ? 0 : (t < 2 * HW ? HH - 1 : (t < 2 * HW + PCG_TY ? t - 2 * HW + 1 : t - 2 * HW - PCG_TY + 1));
-  const int rx = t < HW ? t : (t < 2 * HW ? t - HW : (t < 2 * HW + PCG_TY ? 0 : HW - 1));
+  const int rt = t - (PCG_THREADS - (2 * HW + 2 * PCG_TY));
+  const bool ring_t = rt >= 0;
+  const int ry = rt < HW ? 0 : (rt < 2 * HW ? HH - 1 : (rt < 2 * HW + PCG_TY ? rt - 2 * HW + 1 : rt - 2 * HW - PCG_TY + 1));
+  const int rx = rt < HW ? rt : (rt < 2 * HW ? rt - HW : (rt < 2 * HW + PCG_TY ? 0 : HW - 1));
   const int ro_r = HD::at(ry, rx), ro_a = H::at(ry, rx), ro_c = HC::at(ry, rx), ro_q = ry * PCG_QW + rx + PCG_QOFF;
   // y-tile row 32 and column 32 (threads < 65)
   const bool yh_t = t < YW + PCG_TY;
@@ -1004,23 +1009,28 @@ __device__ void phaseB(const PcgArgs<T>& A, const Blk& blk, double* part, PcgSha
   __syncthreads();
 }
 
-// final: state p = x (+ alpha p pending) on the unknowns
+// final: state p = x (+ alpha p pending) on the unknowns, x quads (4 planes in flight)
 template <typename T>
 __device__ void finish_x(const PcgArgs<T>& A, int unit, T alpha, const T* __restrict__ p, bool zero) {
   const Dims& d = A.d;
   const Unit t = unit_of<T>(A, unit);
-  const int lx = threadIdx.x % PCG_TX, ly0 = threadIdx.x / PCG_TX;
-  const int i = t.i0 + lx;
-  if (i >= d.nx) return;
-  const long long plane = (long long)d.nx * d.ny, pplane = (long long)A.nxp * d.ny;
-  for (int q = 0; q < PCG_RPT; ++q) {
-    const int j = t.j0 + ly0 + q * PCG_RSTEP;
-    if (j >= d.ny) continue;
-    for (int k = t.k0; k < t.k1; ++k) {
-      const long long c = k * plane + (long long)j * d.nx + i;
-      const long long pc_ = k * pplane + (long long)j * A.nxp + i;
-      if (zero) { A.state_p[c] = (T)0; continue; }
-      if (A.code[pc_] & 64) A.state_p[c] = alpha != (T)0 ? A.x[pc_] + alpha * p[pc_] : A.x[pc_];
+  const int tx = threadIdx.x % QX, ty = threadIdx.x / QX;
+  const int i = t.i0 + 4 * tx, j = t.j0 + ty;
+  if (i >= d.nx || j >= d.ny) return;
+  const int plane = d.nx * d.ny, pplane = A.nxp * d.ny;
+#pragma unroll 4
+  for (int k = t.k0; k < t.k1; ++k) {
+    const int g = k * pplane + j * A.nxp + i;   // pitched PCG vectors: quad-aligned
+    const int c = k * plane + j * d.nx + i;      // state pressure (unpitched)
+    const uint32_t cw4 = *reinterpret_cast<const uint32_t*>(A.code + g);
+    T xv[4], pv[4];
+    ld4<T>(A.x + g, xv);
+    if (alpha != (T)0) ld4<T>(p + g, pv);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      if (i + q >= d.nx) break;
+      if (zero) A.state_p[c + q] = (T)0;
+      else if ((cw4 >> (8 * q + 6)) & 1u) A.state_p[c + q] = alpha != (T)0 ? xv[q] + alpha * pv[q] : xv[q];
     }
   }
 }

@@ -10,6 +10,7 @@ struct StepConsts {
   double dt, nu, cap_diffuse, cap_turb;   // cap_diffuse: solver.py:195-201; cap_turb: turbulence.py:110
   double c_mu, alpha, beta, sigma, sigma_star, c_lim;
   double k_in, om_in, nut_in;             // inlet turbulence (turbulence.py:26-33)
+  double lim_scale;                       // c_lim / (c_mu / 2), the limiter's factor (turbulence.py:93-97)
 };
 
 // Per-step device report (one slot per step in a batch).
@@ -784,7 +785,7 @@ __global__ void k_turbulence(Dims d, const T* __restrict__ u, const T* __restric
     }
     const T kf = kn > (T)1e-12 ? kn : (T)1e-12;
     const T wf = wn > (T)1e-8 ? wn : (T)1e-8;
-    T omt = (T)sc.c_lim * sqrt(s2) * ((T)2 / (T)sc.c_mu);
+    T omt = (T)sc.c_lim * sqrt(s2) * (T)sc.lim_scale;
     omt = wf > omt ? wf : omt;
     omt = omt > (T)1e-8 ? omt : (T)1e-8;
     kout[c] = kf;
