@@ -85,17 +85,6 @@ __device__ __forceinline__ T gather(const T* __restrict__ a, int ex, int ey, int
   return gather_at<T>(a, ex, ey, ez, i0, j0, k0, tx, ty, tz, mn, mx);
 }
 
-// The same gather at a point i + half/2 on one axis (half in {-1, 0, 1}):
-// floor, clamp and fraction in integer arithmetic.  Every value involved is
-// an exact small integer or half, so i0 and t equal gather()'s bit for bit.
-template <typename T>
-__device__ __forceinline__ void axis_at(int i, int half, int e, int& i0, T& t) {
-  const int fl = half < 0 ? i - 1 : i;
-  const int im = e - 2 > 0 ? e - 2 : 0;
-  i0 = fl < 0 ? 0 : (fl > im ? im : fl);
-  const int h2 = 2 * (i - i0) + half;      // 2 (x - i0)
-  t = h2 <= 0 ? (T)0 : (h2 >= 2 ? (T)1 : (T)0.5);
-}
 
 // ---------------------------------------------------------------------------
 // Order-independent max reductions on non-negative values (bit patterns of
