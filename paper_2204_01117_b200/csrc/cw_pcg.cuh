@@ -417,106 +417,6 @@ __device__ __forceinline__ void issue_B(const PcgArgs<T>& A, uint8_t* ring, uint
   tma_load_3d_hint(st + L::B_C, &A.tm_code, &full[s], c.t.i0 - Halo<uint8_t>::SH, c.t.j0 - 1, c.kk, keep);
 }
 
-// ---- phase 0: b = -div/dt, r0 = b - A x0 with x0 = p on the unknowns ------
-// (once per projection; plain loads)
-template <typename T, bool SLABS>
-__device__ void phase0(const PcgArgs<T>& A, double* part, int unit, PcgShared<T>& S) {
-  const Dims& d = A.d;
-  const Unit t = unit_of<T>(A, unit);
-  const int lx = threadIdx.x % PCG_TX, ly0 = threadIdx.x / PCG_TX;
-  const int i = t.i0 + lx;
-  const long long plane = (long long)d.nx * d.ny;
-  const long long pplane = (long long)A.nxp * d.ny;
-  // x0 = state p on the unknowns, 0 elsewhere and outside the grid: the code
-  // byte and p are loaded independently (clamped address), then selected
-  auto xval = [&](int kk, int gi, int gj) -> T {
-    const bool in = kk >= 0 && kk < d.nz && gi >= 0 && gi < d.nx && gj >= 0 && gj < d.ny;
-    const int ck = in ? kk : 0, ci = in ? gi : 0, cj = in ? gj : 0;
-    const uint8_t cd = __ldg(A.code + (ck * pplane + (long long)cj * A.nxp + ci));
-    const T pv = __ldg(A.state_p + (ck * plane + (long long)cj * d.nx + ci));
-    return (in && (cd & 64)) ? pv : (T)0;
-  };
-  constexpr int NL = (HH * HW + PCG_THREADS - 1) / PCG_THREADS;   // halo elements per thread
-  T nxt[NL];
-  auto fetch = [&](int kk) {   // plane kk's halo tile into registers
-#pragma unroll
-    for (int m = 0; m < NL; ++m) {
-      const int e = threadIdx.x + m * PCG_THREADS;
-      nxt[m] = e < HH * HW ? xval(kk, t.i0 + e % HW - 1, t.j0 + e / HW - 1) : (T)0;
-    }
-  };
-  auto store = [&](int b) {
-#pragma unroll
-    for (int m = 0; m < NL; ++m) {
-      const int e = threadIdx.x + m * PCG_THREADS;
-      if (e < HH * HW) S.pa[b][e / HW][e % HW] = nxt[m];
-    }
-  };
-  double b2 = 0.0, bmax = 0.0, dmax = 0.0;
-  const double rdt = 1.0 / A.dt;
-  T pm[PCG_RPT];
-#pragma unroll
-  for (int q = 0; q < PCG_RPT; ++q) pm[q] = xval(t.k0 - 1, i, t.j0 + ly0 + q * PCG_RSTEP);
-  int bc = 0, bn = 1;
-  fetch(t.k0);
-  store(bc);
-  fetch(t.k0 + 1);
-  store(bn);
-  __syncthreads();
-  for (int k = t.k0; k < t.k1; ++k) {
-    if (k + 2 <= t.k1) fetch(k + 2);   // in flight while plane k is computed
-#pragma unroll
-    for (int q = 0; q < PCG_RPT; ++q) {
-      const int ly = ly0 + q * PCG_RSTEP, j = t.j0 + ly;
-      if (i >= d.nx || j >= d.ny) continue;
-      const long long c = k * plane + (long long)j * d.nx + i;
-      const long long pc_ = k * pplane + (long long)j * A.nxp + i;
-      const uint8_t cd = __ldg(A.code + pc_);
-      const T pc = S.pa[bc][ly + 1][lx + 1];
-      const T pn = S.pa[bn][ly + 1][lx + 1];
-      if (cd & 64) {
-        const long long ui = ((long long)k * d.ny + j) * (d.nx + 1) + i;
-        const long long vi = ((long long)k * (d.ny + 1) + j) * d.nx + i;
-        // divergence and A x0 in float64 from the stored fields
-        double div = ((double)A.u[ui + 1] - (double)A.u[ui]) * d.drh[0] +
-                     ((double)A.v[vi + d.nx] - (double)A.v[vi]) * d.drh[1];
-        if (!d.is2d) div = div + ((double)A.w[c + plane] - (double)A.w[c]) * d.drh[2];
-        const double b = -div * rdt;
-        const double ax = (double)S.lut[(cd & 63) * 4] * (double)pc -
-                          ((double)A.wx * ((double)S.pa[bc][ly + 1][lx] + (double)S.pa[bc][ly + 1][lx + 2]) +
-                           (double)A.wy * ((double)S.pa[bc][ly][lx + 1] + (double)S.pa[bc][ly + 2][lx + 1]) +
-                           (double)A.wz * ((double)pm[q] + (double)pn));
-        A.r0[pc_] = b - ax;
-        A.x[pc_] = pc;
-        if (SLABS && k == A.o0 && A.lo.r0) A.lo.r0[A.lo.plane_off + (pc_ - k * pplane)] = b - ax;       // z-slab halo push
-        if (SLABS && k == A.o1 - 1 && A.hi.r0) A.hi.r0[A.hi.plane_off + (pc_ - k * pplane)] = b - ax;
-        b2 += b * b;
-        const double ab = fabs(b), ad = fabs(div);
-        bmax = (ab > bmax || ab != ab) ? ab : bmax;
-        dmax = (ad > dmax || ad != ad) ? ad : dmax;
-      } else {
-        A.state_p[c] = (T)0;   // project() sets p = 0 off the unknowns (solver.py:278-280)
-      }
-      pm[q] = pc;
-    }
-    __syncthreads();             // plane k's tile is consumed: plane k+2 takes its buffer
-    if (k + 2 <= t.k1) store(bc);
-    __syncthreads();
-    const int tmp = bc; bc = bn; bn = tmp;
-  }
-  const double s0 = block_sum(b2, S.red);
-  __syncthreads();
-  const double m1 = block_max(bmax, S.red);
-  __syncthreads();
-  const double m2 = block_max(dmax, S.red);
-  if (threadIdx.x == 0) {
-    part[unit] = s0;
-    part[A.PS + unit] = m1;
-    part[2 * A.PS + unit] = m2;
-  }
-  __syncthreads();
-}
-
 // A p' per cell.  float32 state: the difference form sum_a w_a (p_i - p_a)
 // over the neighbours a that are unknowns or outlets (p_a = 0 at an outlet).
 // The 7-point combination of a smooth p cancels d*p almost entirely, so the
@@ -657,6 +557,112 @@ __device__ __forceinline__ void ring_fill(const PcgArgs<T>& A, JobCursor& prod, 
     ++issued;
     more = cursor_next<T>(A, prod);
   }
+}
+
+// ---- phase 0: b = -div/dt, r0 = b - A x0 with x0 = p on the unknowns ------
+// (once per projection; plain loads).  x quads like the ring phases: plane k's
+// halo tile of x0 goes to a shared double buffer (own quads plus the 132-cell
+// ring), the z neighbours are the own quads of planes k-1, k+1 in registers.
+template <typename T, bool SLABS>
+__device__ void phase0(const PcgArgs<T>& A, double* part, int unit, PcgShared<T>& S) {
+  const Dims& d = A.d;
+  const Unit t = unit_of<T>(A, unit);
+  const int tx = threadIdx.x % QX, ty = threadIdx.x / QX;
+  const bool lft = tx == 0, rgt = tx == QX - 1;
+  const int hy = ty + 1, hx0 = 1 + 4 * tx;
+  const int i = t.i0 + 4 * tx, jj = t.j0 + ty;
+  const int plane = d.nx * d.ny, pplane = A.nxp * d.ny;
+  // x0 = state p on the unknowns, 0 elsewhere and outside the grid: the code
+  // byte and p are loaded independently (clamped address), then selected
+  auto x0_at = [&](int kk, int gi, int gj) -> T {
+    const bool in = kk >= 0 && kk < d.nz && gi >= 0 && gi < d.nx && gj >= 0 && gj < d.ny;
+    const int ck = in ? kk : 0, ci = in ? gi : 0, cj = in ? gj : 0;
+    const uint8_t cd = __ldg(A.code + (ck * pplane + cj * A.nxp + ci));
+    const T pv = __ldg(A.state_p + (ck * plane + cj * d.nx + ci));
+    return (in && (cd & 64)) ? pv : (T)0;
+  };
+  auto x0_quad = [&](int kk, T (&q)[4]) {
+#pragma unroll
+    for (int c = 0; c < 4; ++c) q[c] = x0_at(kk, i + c, jj);
+  };
+  // the tile's ring cell of this thread (the last 132 threads, as in phase B)
+  const int rt = (int)threadIdx.x - (PCG_THREADS - (2 * HW + 2 * PCG_TY));
+  const bool ring_t = rt >= 0;
+  const int ry = rt < HW ? 0 : (rt < 2 * HW ? HH - 1 : (rt < 2 * HW + PCG_TY ? rt - 2 * HW + 1 : rt - 2 * HW - PCG_TY + 1));
+  const int rx = rt < HW ? rt : (rt < 2 * HW ? rt - HW : (rt < 2 * HW + PCG_TY ? 0 : HW - 1));
+  constexpr int QPL = HH * PCG_QW;
+  T* tile = &S.wk.qb[0][0][0];                  // two planes of the phase-B q ring (free here)
+  const int q_own = hy * PCG_QW + hx0 + PCG_QOFF;
+  const int q_e = hy * PCG_QW + PCG_QOFF + (lft ? 0 : (rgt ? PCG_TX + 1 : hx0));
+  const int ro_q = ry * PCG_QW + rx + PCG_QOFF;
+  const bool rows = jj < d.ny && i < A.nxp;
+  const double rdt = 1.0 / A.dt;
+  const double wx = (double)A.wx, wy = (double)A.wy, wz = (double)A.wz;
+  double b2 = 0.0, bmax = 0.0, dmax = 0.0;
+  T xm[4], xc[4], xn[4];
+  x0_quad(t.k0 - 1, xm);
+  x0_quad(t.k0, xc);
+  for (int k = t.k0; k < t.k1; ++k) {
+    T* tl = tile + (k & 1) * QPL;
+    st4<T>(tl + q_own, xc);
+    if (ring_t) tl[ro_q] = x0_at(k, t.i0 + rx - 1, t.j0 + ry - 1);
+    x0_quad(k + 1, xn);                         // the next plane's own quad, in flight over the barrier
+    __syncthreads();
+    T ym[4], yp[4];
+    ld4<T>(tl + q_own - PCG_QW, ym);
+    ld4<T>(tl + q_own + PCG_QW, yp);
+    const T xe = tl[q_e];
+    T left = from_left(xc[3]), right = from_right(xc[0]);
+    left = lft ? xe : left;
+    right = rgt ? xe : right;
+    if (rows) {
+      const int g = k * pplane + jj * A.nxp + i;   // pitched, quad-aligned
+      const uint32_t cw4 = *reinterpret_cast<const uint32_t*>(A.code + g);
+      const int ui = (k * d.ny + jj) * (d.nx + 1) + i;
+      const int vi = (k * (d.ny + 1) + jj) * d.nx + i;
+      const int c0 = k * plane + jj * d.nx + i;
+      double rv[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        rv[c] = 0.0;
+        const unsigned cd = (cw4 >> (8 * c)) & 0xffu;   // 0 beyond the grid's x extent (pitched padding)
+        if (cd & 64u) {
+          // divergence and A x0 in float64 from the stored fields
+          double div = ((double)A.u[ui + c + 1] - (double)A.u[ui + c]) * d.drh[0] +
+                       ((double)A.v[vi + c + d.nx] - (double)A.v[vi + c]) * d.drh[1];
+          if (!d.is2d) div = div + ((double)A.w[c0 + c + plane] - (double)A.w[c0 + c]) * d.drh[2];
+          const double b = -div * rdt;
+          const double ax = (double)lut_at(S.lut, cd, 0) * (double)xc[c] -
+                            (wx * ((double)(c == 0 ? left : xc[c - 1]) + (double)(c == 3 ? right : xc[c + 1])) +
+                             wy * ((double)ym[c] + (double)yp[c]) + wz * ((double)xm[c] + (double)xn[c]));
+          rv[c] = b - ax;
+          b2 += b * b;
+          const double ab = fabs(b), ad = fabs(div);
+          bmax = (ab > bmax || ab != ab) ? ab : bmax;
+          dmax = (ad > dmax || ad != ad) ? ad : dmax;
+        } else if (i + c < d.nx) {
+          A.state_p[c0 + c] = (T)0;   // project() sets p = 0 off the unknowns (solver.py:278-280)
+        }
+      }
+      stg4<double>(A.r0 + g, rv);
+      stg4<T>(A.x + g, xc);
+      if (SLABS && k == A.o0 && A.lo.r0) stg4<double>(A.lo.r0 + A.lo.plane_off + (g - k * pplane), rv);   // z-slab halo push
+      if (SLABS && k == A.o1 - 1 && A.hi.r0) stg4<double>(A.hi.r0 + A.hi.plane_off + (g - k * pplane), rv);
+    }
+#pragma unroll
+    for (int c = 0; c < 4; ++c) { xm[c] = xc[c]; xc[c] = xn[c]; }
+  }
+  const double s0 = block_sum(b2, S.red);
+  __syncthreads();
+  const double m1 = block_max(bmax, S.red);
+  __syncthreads();
+  const double m2 = block_max(dmax, S.red);
+  if (threadIdx.x == 0) {
+    part[unit] = s0;
+    part[A.PS + unit] = m1;
+    part[2 * A.PS + unit] = m2;
+  }
+  __syncthreads();
 }
 
 // ---- phase A: p' = z + beta p, x += alpha_prev p, Ap = A p' ---------------
