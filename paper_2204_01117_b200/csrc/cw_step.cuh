@@ -62,7 +62,10 @@ constexpr int ST_BX = 32, ST_BY = CW_ST_BY, ST_BZ = CW_ST_BZ;
 #define CW_ZT 4
 #endif
 static_assert(ST_BZ == 1, "z-coarsened kernels take one plane per block row");
-constexpr int ZT_TURB = 1;   // k_turbulence: coarsening measured slower (90 -> 100 us at C3)
+#ifndef CW_ZT_TURB
+#define CW_ZT_TURB 1
+#endif
+constexpr int ZT_TURB = CW_ZT_TURB;   // k_turbulence planes per thread (2 and 4 measured slower: 90 -> 98 / 100 us at C3)
 #ifndef CW_ZT_MAC
 #define CW_ZT_MAC 2
 #endif
