@@ -1,5 +1,5 @@
 set -x
-T=r1g
+T=r1h
 python bench.py > gpurun_out/bench_full_$T.log 2>&1; tail -1 gpurun_out/bench_full_$T.log > gpurun_out/bench_$T.json
 python bench.py --impl reference > gpurun_out/bench_ref_full_$T.log 2>&1; tail -1 gpurun_out/bench_ref_full_$T.log > gpurun_out/bench_ref_$T.json
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$T.csv python bench.py --steps 3 --warmup 3 --no-cpu --no-design > gpurun_out/ncu_ll_$T.log 2>&1
