@@ -90,6 +90,11 @@ class ClockSampler:
             self.nvml = (pynvml, h)
             self.t = threading.Thread(target=self._poll, daemon=True)
             self.t.start()
+            t0 = time.perf_counter()   # the poll loop is warm before the timed region starts
+            while len(self.sm) < 2 and time.perf_counter() - t0 < 2.0:
+                time.sleep(0.002)
+            self.sm.clear()
+            self.reasons.clear()
             return self
         except Exception:
             self.nvml = None

@@ -361,7 +361,7 @@ static inline dim3 g3z(int ex, int ey, int ez) {
   return dim3((unsigned)((ex + ST_BX - 1) / ST_BX), (unsigned)((ey + ST_BY - 1) / ST_BY),
               (unsigned)((ez + CW_ZT - 1) / CW_ZT));
 }
-// owned-plane max reductions (k_div_max, k_speed_max): each block strides
+// owned-plane max reduction (k_div_max): each block strides
 // over the planes, about 2048 blocks in all, one atomic per block
 static inline dim3 g3r(int ex, int ey, int nz) {
   const int bx = (ex + ST_BX - 1) / ST_BX, by = (ey + 7) / 8;
@@ -810,7 +810,7 @@ static int enqueue_step(cw_ctx* c, const cw_fields* f, const cw_params* prm, dou
   mark(6);
   BcFields<T> F2{P.u, P.v, P.w, P.p, P.k, P.om, P.nut};
   launch_bc<T>(c, F2, P.lab, P.lab_ver, prm, st);                        // "boundary2"
-  (k_speed_max<T><<<g3r(c->d.nx + 1, c->d.ny + 1, c->d.o1 - c->d.o0 + 1), B3R, 0, st>>>(c->d, P.u, P.v, P.w, rep, c->gate),
+  (k_speed_max_flat<T><<<4 * 148, B3R, 0, st>>>(c->d, P.u, P.v, P.w, rep, c->gate),
    ++c->launches);
   mark(7);
   CW_CUDA(cudaGetLastError());
@@ -882,7 +882,7 @@ static int enqueue_stage(cw_ctx* c, const cw_fields* f, const cw_params* prm, in
       if (prm->turbulence) st_turb<T>(c, P, prm, (const T*)c->tk, (const T*)c->tw, rep, st);
       BcFields<T> F2{P.u, P.v, P.w, P.p, P.k, P.om, P.nut};
       launch_bc<T>(c, F2, P.lab, P.lab_ver, prm, st);
-      (k_speed_max<T><<<g3r(d.nx + 1, d.ny + 1, d.o1 - d.o0 + 1), B3R, 0, st>>>(d, P.u, P.v, P.w, rep, c->gate),
+      (k_speed_max_flat<T><<<4 * 148, B3R, 0, st>>>(d, P.u, P.v, P.w, rep, c->gate),
        ++c->launches);
       break;
     }

@@ -75,17 +75,13 @@ __device__ __forceinline__ int clampi(int a, int lo, int hi) { return a < lo ? l
 
 // ---------------------------------------------------------------------------
 // upwind k and omega (advection.py:154-173), old velocity, axes x,y,z in turn
+// the upwind update of cell (i, j, k) given its cell-centred velocity a
 template <typename T>
-__device__ __forceinline__ void upwind_cell(const Dims& d, const T* __restrict__ u, const T* __restrict__ v,
-                                            const T* __restrict__ w, const T* __restrict__ kin,
-                                            const T* __restrict__ win, T* __restrict__ kout, T* __restrict__ wout,
-                                            T dt, int i, int j, int k) {
-  if (i < d.nx && j < d.ny && k < d.nz) {
+__device__ __forceinline__ void upwind_cell_a(const Dims& d, const T (&a)[3], const T* __restrict__ kin,
+                                              const T* __restrict__ win, T* __restrict__ kout, T* __restrict__ wout,
+                                              T dt, int i, int j, int k) {
+  {
     const int c = d.cidx32(i, j, k);
-    T a[3];
-    a[0] = (T)0.5 * (u[((int)k * d.ny + j) * (d.nx + 1) + i] + u[((int)k * d.ny + j) * (d.nx + 1) + i + 1]);
-    a[1] = (T)0.5 * (v[((int)k * (d.ny + 1) + j) * d.nx + i] + v[((int)k * (d.ny + 1) + j + 1) * d.nx + i]);
-    a[2] = (T)0.5 * (w[c] + w[c + (int)d.nx * d.ny]);
     const int pos[3] = {i, j, k};
     const int ext[3] = {d.nx, d.ny, d.nz};
     const int str[3] = {1, d.nx, (int)d.nx * d.ny};
@@ -106,6 +102,21 @@ __device__ __forceinline__ void upwind_cell(const Dims& d, const T* __restrict__
       }
       (f ? wout : kout)[c] = out;
     }
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ void upwind_cell(const Dims& d, const T* __restrict__ u, const T* __restrict__ v,
+                                            const T* __restrict__ w, const T* __restrict__ kin,
+                                            const T* __restrict__ win, T* __restrict__ kout, T* __restrict__ wout,
+                                            T dt, int i, int j, int k) {
+  if (i < d.nx && j < d.ny && k < d.nz) {
+    const int c = d.cidx32(i, j, k);
+    T a[3];
+    a[0] = (T)0.5 * (u[((int)k * d.ny + j) * (d.nx + 1) + i] + u[((int)k * d.ny + j) * (d.nx + 1) + i + 1]);
+    a[1] = (T)0.5 * (v[((int)k * (d.ny + 1) + j) * d.nx + i] + v[((int)k * (d.ny + 1) + j + 1) * d.nx + i]);
+    a[2] = (T)0.5 * (w[c] + w[c + (int)d.nx * d.ny]);
+    upwind_cell_a<T>(d, a, kin, win, kout, wout, dt, i, j, k);
   }
 }
 
@@ -159,6 +170,68 @@ __device__ __forceinline__ void face_velocity(const Dims& d, int comp, const T* 
   }
 }
 
+// The velocities of a thread whose (i, j, k) is inside all three face extents
+// and the cell grid (3-D): the u, v and w face points and the cell centre need
+// 6 distinct values of each velocity array (18 loads, against 39 when
+// face_velocity runs per component and the upwind step loads its own);
+// every average is the same expression on the same values, bit for bit.
+template <typename T>
+struct VelNbhd {
+  T fu[3], fv[3], fw[3];   // velocity (u, v, w) at the face point of component c
+  T a[3];                  // cell-centred velocity (upwind step)
+};
+
+template <typename T>
+__device__ __forceinline__ void vel_nbhd(const Dims& d, const T* __restrict__ u, const T* __restrict__ v,
+                                         const T* __restrict__ w, int i, int j, int k, VelNbhd<T>& n) {
+  const int nx = d.nx, ny = d.ny;
+  const int uy = nx + 1, uz = (nx + 1) * ny;
+  const int vy = nx, vz = nx * (ny + 1);
+  const int wy = nx, wz = nx * ny;
+  const int im = max(i - 1, 0), jm = max(j - 1, 0), km = max(k - 1, 0);
+  const T* ur = u + k * uz + j * uy + i;
+  const T U0 = ur[0], U1 = ur[1];                                   // u(i..i+1, j, k)
+  const T U2 = u[k * uz + jm * uy + i], U3 = u[k * uz + jm * uy + i + 1];   // u(i..i+1, jm, k)
+  const T U4 = u[km * uz + j * uy + i], U5 = u[km * uz + j * uy + i + 1];   // u(i..i+1, j, km)
+  const T V0 = v[k * vz + j * vy + i], V1 = v[k * vz + (j + 1) * vy + i];   // v(i, j..j+1, k)
+  const T V2 = v[k * vz + j * vy + im], V3 = v[k * vz + (j + 1) * vy + im]; // v(im, j..j+1, k)
+  const T V4 = v[km * vz + j * vy + i], V5 = v[km * vz + (j + 1) * vy + i]; // v(i, j..j+1, km)
+  const T W0 = w[k * wz + j * wy + i], W1 = w[(k + 1) * wz + j * wy + i];   // w(i, j, k..k+1)
+  const T W2 = w[k * wz + j * wy + im], W3 = w[(k + 1) * wz + j * wy + im]; // w(im, j, k..k+1)
+  const T W4 = w[k * wz + jm * wy + i], W5 = w[(k + 1) * wz + jm * wy + i]; // w(i, jm, k..k+1)
+  // u face (face_velocity comp 0: ip = i)
+  n.fu[0] = U0;
+  n.fv[0] = avg2(avg2(V2, V0), avg2(V3, V1));
+  n.fw[0] = avg2(avg2(W2, W0), avg2(W3, W1));
+  // v face (comp 1: jp = j)
+  n.fu[1] = avg2(avg2(U2, U3), avg2(U0, U1));
+  n.fv[1] = V0;
+  n.fw[1] = avg2(avg2(W4, W0), avg2(W5, W1));
+  // w face (comp 2: kp = k)
+  n.fu[2] = avg2(avg2(U4, U5), avg2(U0, U1));
+  n.fv[2] = avg2(avg2(V4, V5), avg2(V0, V1));
+  n.fw[2] = W0;
+  // cell centre (upwind_cell)
+  n.a[0] = (T)0.5 * (U0 + U1);
+  n.a[1] = (T)0.5 * (V0 + V1);
+  n.a[2] = (T)0.5 * (W0 + W1);
+}
+
+// the predictor for one face given the face-point velocity
+template <typename T>
+__device__ __forceinline__ void mac_predict_face_v(const Dims& d, int comp, const T* arr, T* ahead, T dt, int i,
+                                                   int j, int k, T us, T vs, T ws) {
+  int ex, ey, ez;
+  comp_extent(d, comp, ex, ey, ez);
+  float fox, foy, foz;
+  comp_offset(comp, fox, foy, foz);
+  const T ox = (T)fox, oy = (T)foy, oz = (T)foz;
+  const int c = ((int)k * ey + j) * ex + i;
+  const T X = (T)i + ox, Y = (T)j + oy, Z = (T)k + oz;
+  const T bx = X - dt * us * inv_h<T>(d, 0), by = Y - dt * vs * inv_h<T>(d, 1), bz = Z - dt * ws * inv_h<T>(d, 2);
+  ahead[c] = gather<T>(arr, ex, ey, ez, bx - ox, by - oy, bz - oz, nullptr, nullptr);
+}
+
 // One thread per (i, j, k) of the union of the face extents handles the u, v
 // and w faces there (all three read the same pre-advection velocity).
 template <typename T>
@@ -167,22 +240,21 @@ __device__ __forceinline__ void mac_predict_face(const Dims& d, int comp, const 
   int ex, ey, ez;
   comp_extent(d, comp, ex, ey, ez);
   if (i >= ex || j >= ey || k >= ez) return;
-  float fox, foy, foz;
-  comp_offset(comp, fox, foy, foz);
-  const T ox = (T)fox, oy = (T)foy, oz = (T)foz;
   const T* arr = comp == 0 ? u : (comp == 1 ? v : w);
-  const int c = ((int)k * ey + j) * ex + i;
-  const T X = (T)i + ox, Y = (T)j + oy, Z = (T)k + oz;
   T us, vs, ws;
   face_velocity<T>(d, comp, u, v, w, i, j, k, us, vs, ws);
-  const T bx = X - dt * us * inv_h<T>(d, 0), by = Y - dt * vs * inv_h<T>(d, 1), bz = Z - dt * ws * inv_h<T>(d, 2);
-  ahead[c] = gather<T>(arr, ex, ey, ez, bx - ox, by - oy, bz - oz, nullptr, nullptr);
+  mac_predict_face_v<T>(d, comp, arr, ahead, dt, i, j, k, us, vs, ws);
 }
 
 // the predictor launch also runs the upwind step of k and omega (cells,
 // advection.py:154-173) when kout != nullptr: both read the old velocity
+#ifndef CW_MAC_PRED_MINB
+#define CW_MAC_PRED_MINB 8
+#endif
+// 8 resident blocks per SM (<= 32 registers): measured 102 us at C3, against
+// 106 us at 6 blocks and 223 us uncapped
 template <typename T>
-__global__ void k_mac_predict(Dims d, const T* __restrict__ u, const T* __restrict__ v,
+__global__ void __launch_bounds__(256, CW_MAC_PRED_MINB) k_mac_predict(Dims d, const T* __restrict__ u, const T* __restrict__ v,
                               const T* __restrict__ w, T* __restrict__ a0, T* __restrict__ a1,
                               T* __restrict__ a2, T dt, const T* __restrict__ kin, const T* __restrict__ win,
                               T* __restrict__ kout, T* __restrict__ wout, const int* gate) {
@@ -193,11 +265,43 @@ __global__ void k_mac_predict(Dims d, const T* __restrict__ u, const T* __restri
   for (int kz = 0; kz < ZT_MAC; ++kz) {
     const int k = (int)blockIdx.z * ZT_MAC + kz;
     if (k > d.nz) break;
+    if (!d.is2d && i < d.nx && j < d.ny && k < d.nz) {   // interior: shared velocity loads
+      VelNbhd<T> n;
+      vel_nbhd<T>(d, u, v, w, i, j, k, n);
+      if (kout) upwind_cell_a<T>(d, n.a, kin, win, kout, wout, dt, i, j, k);
+      mac_predict_face_v<T>(d, 0, u, a0, dt, i, j, k, n.fu[0], n.fv[0], n.fw[0]);
+      mac_predict_face_v<T>(d, 1, v, a1, dt, i, j, k, n.fu[1], n.fv[1], n.fw[1]);
+      mac_predict_face_v<T>(d, 2, w, a2, dt, i, j, k, n.fu[2], n.fv[2], n.fw[2]);
+      continue;
+    }
     if (kout) upwind_cell<T>(d, u, v, w, kin, win, kout, wout, dt, i, j, k);
     mac_predict_face<T>(d, 0, u, v, w, a0, dt, i, j, k);
     mac_predict_face<T>(d, 1, u, v, w, a1, dt, i, j, k);
     if (!d.is2d) mac_predict_face<T>(d, 2, u, v, w, a2, dt, i, j, k);
   }
+}
+
+// the corrector for one face given the face-point velocity
+template <typename T>
+__device__ __forceinline__ void mac_correct_face_v(const Dims& d, int comp, const T* arr, const T* ahead, T* out,
+                                                   T dt, int i, int j, int k, T us, T vs, T ws, T self) {
+  int ex, ey, ez;
+  comp_extent(d, comp, ex, ey, ez);
+  float fox, foy, foz;
+  comp_offset(comp, fox, foy, foz);
+  const T ox = (T)fox, oy = (T)foy, oz = (T)foz;
+  const int c = ((int)k * ey + j) * ex + i;
+  const T X = (T)i + ox, Y = (T)j + oy, Z = (T)k + oz;
+  T mn, mx;
+  const T sx = dt * us * inv_h<T>(d, 0), sy = dt * vs * inv_h<T>(d, 1), sz = dt * ws * inv_h<T>(d, 2);
+  const T bx = X - sx, by = Y - sy, bz = Z - sz;
+  (void)gather<T>(arr, ex, ey, ez, bx - ox, by - oy, bz - oz, &mn, &mx);
+  const T fx = X + sx, fy = Y + sy, fz = Z + sz;
+  const T back = gather<T>(ahead, ex, ey, ez, fx - ox, fy - oy, fz - oz, nullptr, nullptr);
+  T cor = ahead[c] + (T)0.5 * (self - back);   // self = arr[c]
+  cor = cor < mn ? mn : cor;
+  cor = cor > mx ? mx : cor;
+  out[c] = cor;
 }
 
 template <typename T>
@@ -206,28 +310,20 @@ __device__ __forceinline__ void mac_correct_face(const Dims& d, int comp, const 
   int ex, ey, ez;
   comp_extent(d, comp, ex, ey, ez);
   if (i >= ex || j >= ey || k >= ez) return;
-  float fox, foy, foz;
-  comp_offset(comp, fox, foy, foz);
-  const T ox = (T)fox, oy = (T)foy, oz = (T)foz;
   const T* arr = comp == 0 ? u : (comp == 1 ? v : w);
-  const int c = ((int)k * ey + j) * ex + i;
-  const T X = (T)i + ox, Y = (T)j + oy, Z = (T)k + oz;
   T us, vs, ws;
   face_velocity<T>(d, comp, u, v, w, i, j, k, us, vs, ws);
-  T mn, mx;
-  const T sx = dt * us * inv_h<T>(d, 0), sy = dt * vs * inv_h<T>(d, 1), sz = dt * ws * inv_h<T>(d, 2);
-  const T bx = X - sx, by = Y - sy, bz = Z - sz;
-  (void)gather<T>(arr, ex, ey, ez, bx - ox, by - oy, bz - oz, &mn, &mx);
-  const T fx = X + sx, fy = Y + sy, fz = Z + sz;
-  const T back = gather<T>(ahead, ex, ey, ez, fx - ox, fy - oy, fz - oz, nullptr, nullptr);
-  T cor = ahead[c] + (T)0.5 * (arr[c] - back);
-  cor = cor < mn ? mn : cor;
-  cor = cor > mx ? mx : cor;
-  out[c] = cor;
+  mac_correct_face_v<T>(d, comp, arr, ahead, out, dt, i, j, k, us, vs, ws, arr[((int)k * ey + j) * ex + i]);
 }
 
+#ifndef CW_MAC_CORR_MINB
+#define CW_MAC_CORR_MINB 5
+#endif
+// 5 resident blocks per SM (<= 51 registers): the gathers are latency-bound,
+// occupancy beats the few reloads the register cap costs (141 us uncapped at
+// 72 registers, 108 us at 5 or 6 blocks)
 template <typename T>
-__global__ void k_mac_correct(Dims d, const T* __restrict__ u, const T* __restrict__ v,
+__global__ void __launch_bounds__(256, CW_MAC_CORR_MINB) k_mac_correct(Dims d, const T* __restrict__ u, const T* __restrict__ v,
                               const T* __restrict__ w, const T* __restrict__ a0, const T* __restrict__ a1,
                               const T* __restrict__ a2, T* __restrict__ o0, T* __restrict__ o1,
                               T* __restrict__ o2, T dt, const int* gate) {
@@ -238,6 +334,14 @@ __global__ void k_mac_correct(Dims d, const T* __restrict__ u, const T* __restri
   for (int kz = 0; kz < ZT_MAC; ++kz) {
     const int k = (int)blockIdx.z * ZT_MAC + kz;
     if (k > d.nz) break;
+    if (!d.is2d && i < d.nx && j < d.ny && k < d.nz) {   // interior: shared velocity loads
+      VelNbhd<T> n;
+      vel_nbhd<T>(d, u, v, w, i, j, k, n);
+      mac_correct_face_v<T>(d, 0, u, a0, o0, dt, i, j, k, n.fu[0], n.fv[0], n.fw[0], n.fu[0]);
+      mac_correct_face_v<T>(d, 1, v, a1, o1, dt, i, j, k, n.fu[1], n.fv[1], n.fw[1], n.fv[1]);
+      mac_correct_face_v<T>(d, 2, w, a2, o2, dt, i, j, k, n.fu[2], n.fv[2], n.fw[2], n.fw[2]);
+      continue;
+    }
     mac_correct_face<T>(d, 0, u, v, w, a0, o0, dt, i, j, k);
     mac_correct_face<T>(d, 1, u, v, w, a1, o1, dt, i, j, k);
     if (!d.is2d) mac_correct_face<T>(d, 2, u, v, w, a2, o2, dt, i, j, k);
@@ -671,27 +775,55 @@ __global__ void k_div_max(Dims d, const T* __restrict__ u, const T* __restrict__
 }
 
 // max |u|,|v|,|w| for the CFL number (solver.py:456-458), over the owned
-// planes (w: faces o0..o1; a face shared with the slab above is counted by
-// both, which a max does not notice)
+// planes (a w face shared with the slab above is counted by both, which a
+// max does not notice).
+// The owned part of each face array is one contiguous run of planes (u, v:
+// planes o0..o1-1; w: faces o0..o1), so the CFL max runs over three flat
+// ranges with 16-byte vector loads, grid-stride over a few blocks per SM.
 template <typename T>
-__global__ void k_speed_max(Dims d, const T* __restrict__ u, const T* __restrict__ v, const T* __restrict__ w,
-                            DevReport* rep, const int* gate) {
+__device__ __forceinline__ T amax1(T m, T x) {
+  const T a = fabs(x);
+  return (a > m || a != a) ? a : m;   // NaN sticks (numpy max)
+}
+template <typename T> struct Vec16;
+template <> struct Vec16<float> { typedef float4 type; static constexpr int n = 4; };
+template <> struct Vec16<double> { typedef double2 type; static constexpr int n = 2; };
+
+template <typename T>
+__device__ __forceinline__ T absmax_run(const T* __restrict__ a, long long lo, long long hi, T m, long long gt,
+                                        long long gs) {
+  const T* p = a + lo;
+  long long n = hi - lo;
+  long long head = (long long)(((16u - ((uintptr_t)p & 15u)) & 15u) / sizeof(T));
+  head = head < n ? head : n;
+  for (long long e = gt; e < head; e += gs) m = amax1(m, p[e]);
+  p += head;
+  n -= head;
+  using V = Vec16<T>;
+  const long long nv = n / V::n;
+  const typename V::type* pv = reinterpret_cast<const typename V::type*>(p);
+  for (long long e = gt; e < nv; e += gs) {
+    const typename V::type q = __ldcs(pv + e);
+    const T* qq = reinterpret_cast<const T*>(&q);
+#pragma unroll
+    for (int c = 0; c < V::n; ++c) m = amax1(m, qq[c]);
+  }
+  for (long long e = nv * V::n + gt; e < n; e += gs) m = amax1(m, p[e]);
+  return m;
+}
+
+template <typename T>
+__global__ void k_speed_max_flat(Dims d, const T* __restrict__ u, const T* __restrict__ v, const T* __restrict__ w,
+                                 DevReport* rep, const int* gate) {
   if (*gate) return;
   __shared__ T scratch[32];
+  const long long gs = (long long)gridDim.x * blockDim.x * blockDim.y;
+  const long long gt = (long long)blockIdx.x * blockDim.x * blockDim.y + threadIdx.y * blockDim.x + threadIdx.x;
+  const long long pu = (long long)(d.nx + 1) * d.ny, pv = (long long)d.nx * (d.ny + 1), pw = (long long)d.nx * d.ny;
   T m = (T)0;
-  const int i = (int)(blockIdx.x * ST_BX + threadIdx.x), j = (int)(blockIdx.y * 8 + threadIdx.y);
-  if (i < d.nx + 1 && j < d.ny + 1) {
-    for (int k = d.o0 + (int)blockIdx.z; k < d.o1 + 1; k += (int)gridDim.z) {
-      if (k < d.o1) {
-        if (j < d.ny) { const T a = fabs(u[((int)k * d.ny + j) * (d.nx + 1) + i]); m = (a > m || a != a) ? a : m; }
-        if (i < d.nx) { const T a = fabs(v[((int)k * (d.ny + 1) + j) * d.nx + i]); m = (a > m || a != a) ? a : m; }
-      }
-      if (i < d.nx && j < d.ny) {
-        const T a = fabs(w[((int)k * d.ny + j) * d.nx + i]);
-        m = (a > m || a != a) ? a : m;
-      }
-    }
-  }
+  m = absmax_run<T>(u, d.o0 * pu, d.o1 * pu, m, gt, gs);
+  m = absmax_run<T>(v, d.o0 * pv, d.o1 * pv, m, gt, gs);
+  m = absmax_run<T>(w, d.o0 * pw, (d.o1 + 1) * pw, m, gt, gs);
   m = block_max_2d(m, scratch);
   if (threadIdx.x == 0 && threadIdx.y == 0) report_max<T>(rep, SLOT_SPEED, m);
 }
