@@ -23,7 +23,12 @@ ALGO = {                         # algorithmic bytes per launch (f
     "k_speed_max_flat": 12 * N,  # u,v,w in
     "k_div_max": 13 * N,         # u,v,w,labels in
     "k_cell_speed": 16 * N,      # u,v,w in; speed out
+    "k_diffuse": 28 * N,         # u,v,w,nu_t in; u,v,w out
+    "k_drag": 32 * N,            # u,v,w,g,speed in; u,v,w out
+    "k_gradient": 29 * N,        # u,v,w,p,labels in; u,v,w out
+    "k_turbulence": 36 * N,      # u,v,w,k,omega,nu_t in; k,omega,nu_t out
 }
+# k_pcg: 20 N + 8 Nu + 44 I Nu per launch with I that launch's iterations (bench.py roofline)
 
 
 def load(path):
