@@ -461,7 +461,7 @@ def run_b200(args):
            "d2h_bytes_per_step": xfer,
            "path": "solver.HostStepper.step() on a host-resident state: every step uploads the 7 fields from "
                    "pinned host memory, steps, and downloads the 7 fields; the two copy directions overlap "
-                   "field by field across consecutive steps"}
+                   "field by field across consecutive steps, and nu_t and p upload while the advection runs"}
 
     kmax = float(state.fields["k"].max())
 

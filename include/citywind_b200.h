@@ -170,6 +170,15 @@ int cw_apply_boundary(cw_ctx *ctx, const cw_fields *f, const cw_params *prm,
 int cw_step(cw_ctx *ctx, const cw_fields *f, const cw_params *prm, const cw_inlet *inl,
             double pcg_tol, int nsteps, void *stream);
 
+/* Let the NEXT step enqueued on this ctx start before nu_t and p are on the
+ * device: the step waits for nu_t_ready (a cudaEvent_t) before its diffusion,
+ * the first stage that reads nu_t, and for p_ready before its first boundary
+ * pass, the first stage that touches p.  One-shot; NULL = no wait.  A caller
+ * that copies the state in from host memory every step (solver.HostStepper)
+ * uploads those two fields while the advection runs.  Same stage order as
+ * step() (ref solver.py:407-461); no reference counterpart. */
+int cw_step_defer(cw_ctx *ctx, void *nu_t_ready, void *p_ready);
+
 /* Run ONE stage function of the reference on a state, with dt = prm->dt:
  * advect (advect_velocity + upwind_scalar k/omega, advection.py:125-173),
  * diffuse (solver.py:193-208), apply_drag (:150-168), apply_boundary_conditions

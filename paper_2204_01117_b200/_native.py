@@ -125,6 +125,7 @@ SIGNATURES = {
     "cw_run_stage": (C.c_int, [_P, C.POINTER(cw_fields), C.POINTER(cw_params), C.POINTER(cw_inlet),
                                C.c_int, C.c_double, _P]),
     "cw_read_reports": (C.c_int, [_P, C.POINTER(cw_report), C.c_int, C.POINTER(C.c_int), _P]),
+    "cw_step_defer": (C.c_int, [_P, _P, _P]),
     "cw_set_stage_timing": (C.c_int, [_P, C.c_int]),
     "cw_read_stage_timings": (C.c_int, [_P, C.POINTER(C.c_float)]),
     "cw_pcg_timing": (C.c_int, [_P, C.c_int]),

@@ -102,6 +102,8 @@ struct cw_ctx {
   int* bc_count = nullptr;
   // stage timing
   bool timing = false;
+  // one-shot waits of the next enqueued step (cw_step_defer): first use of nu_t / p
+  cudaEvent_t wait_nut = nullptr, wait_p = nullptr;
   cudaEvent_t ev[8] = {};
   bool ev_made = false;
   float stage_ms[7] = {0, 0, 0, 0, 0, 0, 0};
@@ -794,6 +796,10 @@ static int enqueue_step(cw_ctx* c, const cw_fields* f, const cw_params* prm, dou
   mark(0);
   st_advect<T>(c, P, prm, (T*)c->tk, (T*)c->tw, st);        // "advect"
   mark(1);
+  if (c->wait_nut) {   // nu_t is first read by the diffusion
+    CW_CUDA(cudaStreamWaitEvent(st, c->wait_nut, 0));
+    c->wait_nut = nullptr;
+  }
   st_diffuse<T>(c, P, prm, st);                               // "diffuse"
   mark(2);
   st_drag<T>(c, P, prm, f->has_drag, st);                     // "drag"
@@ -801,6 +807,10 @@ static int enqueue_step(cw_ctx* c, const cw_fields* f, const cw_params* prm, dou
   StepPtrs<T> B = P;                                          // k, omega after upwind live in tk, tw
   if (turb) { B.k = (T*)c->tk; B.om = (T*)c->tw; }
   BcFields<T> F1{B.u, B.v, B.w, B.p, B.k, B.om, B.nut};
+  if (c->wait_p) {     // p is first touched by the boundary writes (outlet copies)
+    CW_CUDA(cudaStreamWaitEvent(st, c->wait_p, 0));
+    c->wait_p = nullptr;
+  }
   launch_bc<T>(c, F1, P.lab, P.lab_ver, prm, st);                        // "boundary"
   mark(4);
   int rc = st_project<T>(c, P, f, prm, tol, rep, st);         // "project"
@@ -1226,6 +1236,13 @@ extern "C" long long cw_launch_count(cw_ctx* c, int reset) {
   const long long v = c->launches;
   if (reset) c->launches = 0;
   return v;
+}
+
+extern "C" int cw_step_defer(cw_ctx* c, void* nu_t_ready, void* p_ready) {
+  if (!c) return fail(CW_ERR_INVALID, "null argument");
+  c->wait_nut = (cudaEvent_t)nu_t_ready;
+  c->wait_p = (cudaEvent_t)p_ready;
+  return CW_OK;
 }
 
 extern "C" int cw_set_stage_timing(cw_ctx* c, int enabled) {

@@ -230,10 +230,12 @@ def _warn_cap(state, params, dt):
 # the step
 
 def step(state: FlowState, params: SolverParams, psys: PressureSystem, preconditioner,
-         profile: InletProfile, advector=None, pcg_tol: float | None = None) -> StepReport:
+         profile: InletProfile, advector=None, pcg_tol: float | None = None, _defer=None) -> StepReport:
     """One time-split step (solver.py:407-461); returns per-stage device
-    timings (seconds) and the solver statistics."""
-    reps = step_many(state, params, psys, preconditioner, profile, 1, pcg_tol, stage_timings=True)
+    timings (seconds) and the solver statistics.  ``_defer`` (internal):
+    (nu_t_ready, p_ready) CUDA events the step waits for before the first
+    stage that uses that field (``cw_step_defer``)."""
+    reps = step_many(state, params, psys, preconditioner, profile, 1, pcg_tol, stage_timings=True, _defer=_defer)
     return reps[0] if reps else StepReport()
 
 
@@ -247,15 +249,21 @@ class HostStepper:
     fields again.  The copies run on their own streams, in pieces (CHUNKS per
     field), and overlap across the two copy directions: a piece of step s+1
     starts uploading as soon as the same piece of step s is back in host
-    memory, while the later pieces are still coming down.  ``synchronize()``
-    waits for the last download.
+    memory, while the later pieces are still coming down.  The step starts
+    once u, v, w, k and omega are up; nu_t and p travel last and the step
+    waits for them only before its first stage that uses them (the diffusion
+    and the first boundary pass, ``cw_step_defer``), so their copies overlap
+    the advection.  ``synchronize()`` waits for the last download.
     """
 
     CHUNKS = 1   # pieces per field (4 measured the same at C3: the duplex link is the limit)
+    LATE = ("nu_t", "p")   # fields whose upload may overlap the start of the step, in use order
 
     def __init__(self, state: FlowState, host: dict):
         from .grid import FIELDS
-        self.names = FIELDS
+        assert set(self.LATE) in (set(), {"nu_t", "p"}), "cw_step_defer knows nu_t and p"
+        self.names = tuple(n for n in FIELDS if n not in self.LATE) + tuple(self.LATE)
+        self._n_early = len(self.names) - len(self.LATE)
         self.state = state
         self.host = host
         dev = state.fields[self.names[0]].device
@@ -272,13 +280,20 @@ class HostStepper:
     def step(self, params: SolverParams, psys: PressureSystem, preconditioner, profile: InletProfile,
              pcg_tol: float | None = None) -> StepReport:
         cur = torch.cuda.current_stream()
+        ready = {}   # field name (None: all early fields) -> upload-complete event
         with torch.cuda.stream(self._up):
             for q, (d, h) in enumerate(self._pieces):
                 if self._back[q] is not None:
                     self._up.wait_event(self._back[q])
                 d.copy_(h, non_blocking=True)
-        cur.wait_stream(self._up)
-        rep = step(self.state, params, psys, preconditioner, profile, pcg_tol=pcg_tol)
+                nf = (q + 1) // self.CHUNKS          # fields complete after this piece
+                if (q + 1) % self.CHUNKS == 0 and nf >= self._n_early:
+                    ev = torch.cuda.Event()
+                    ev.record(self._up)
+                    ready[None if nf == self._n_early else self.names[nf - 1]] = ev
+        cur.wait_event(ready[None])
+        defer = (ready["nu_t"], ready["p"]) if "nu_t" in ready and "p" in ready else None
+        rep = step(self.state, params, psys, preconditioner, profile, pcg_tol=pcg_tol, _defer=defer)
         done = torch.cuda.Event()
         done.record(cur)
         with torch.cuda.stream(self._down):
@@ -296,7 +311,7 @@ class HostStepper:
 
 def step_many(state: FlowState, params: SolverParams, psys: PressureSystem, preconditioner,
               profile: InletProfile, nsteps: int, pcg_tol: float | None = None,
-              stage_timings: bool = False, read_back: bool = True) -> list:
+              stage_timings: bool = False, read_back: bool = True, _defer=None) -> list:
     """``nsteps`` calls of ``step`` enqueued back to back on the device (no
     host synchronisation between steps).  If a step fails, the following
     steps of the batch are skipped on the device and the exception of the
@@ -315,6 +330,8 @@ def step_many(state: FlowState, params: SolverParams, psys: PressureSystem, prec
         lib = N.lib()
         if stage_timings:
             lib.cw_set_stage_timing(ctx.h, 1)
+        if _defer is not None:
+            N.check(lib.cw_step_defer(ctx.h, C.c_void_p(_defer[0].cuda_event), C.c_void_p(_defer[1].cuda_event)))
         t0 = time.perf_counter()
         done = 0
         reports = []
