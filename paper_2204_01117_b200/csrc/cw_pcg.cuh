@@ -182,6 +182,9 @@ __device__ __forceinline__ unsigned long long globaltimer() {
   return t;
 }
 
+#ifndef CW_BAR_NS
+#define CW_BAR_NS 32   // back-off between polls of the arrival counter (ns)
+#endif
 // Grid barrier for a cooperative launch (all blocks co-resident).  The
 // arrival counter only grows during a launch (zeroed before it): barrier e
 // (0-based, counted per block in `epoch`) completes when it reaches
@@ -200,7 +203,7 @@ __device__ __forceinline__ void grid_barrier(unsigned* bar, int* gate, DevReport
       const unsigned long long t0 = globaltimer();
       unsigned spins = 0;
       while (ld_acquire(count) < target) {
-        __nanosleep(32);
+        if (CW_BAR_NS > 0) __nanosleep(CW_BAR_NS);
         if ((++spins & 1023u) == 0 && (long long)(globaltimer() - t0) > timeout_ns) {
           rep->status = 3;
           *gate = 3;

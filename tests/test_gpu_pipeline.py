@@ -152,3 +152,37 @@ def test_host_stepper_equals_device_steps():
     assert its == [r.pcg.iterations for r in want]
     for n in NAMES:
         assert torch.equal(host[n], ref.fields[n].cpu()), n
+
+
+def test_step_defer_waits_for_late_fields():
+    """cw_step_defer: a step started before nu_t and p are on the device waits
+    for their events before the first stage that uses them.  The true values
+    land on a side stream only after a long sleep, the device copies hold
+    poison until then, and the step still equals the ordinary step bit for bit."""
+    from paper_2204_01117_b200 import solver
+    from paper_2204_01117_b200.grid import FIELDS as NAMES
+    from paper_2204_01117_b200.scenario import CompiledScenario, scenario_from_dict
+    comp = CompiledScenario.compile(scenario_from_dict(scenes.cuboid(24, 24, 12, 2.0, 0.3, steps=6)))
+    sc = comp.scenario
+    ref = comp.make_state()
+    solver.step_many(ref, sc.solver, comp.psys, comp.preconditioner, sc.inlet, 2)   # non-zero p, nu_t
+    work = ref.copy()
+    solver.step_many(ref, sc.solver, comp.psys, comp.preconditioner, sc.inlet, 1)
+    true_nut, true_p = work.fields["nu_t"].clone(), work.fields["p"].clone()
+    work.fields["nu_t"].fill_(1e3)
+    work.fields["p"].fill_(1e3)
+    torch.cuda.synchronize()
+    side = torch.cuda.Stream()
+    with torch.cuda.stream(side):
+        torch.cuda._sleep(40_000_000)                 # ~20 ms: the step reaches its waits first
+        work.fields["nu_t"].copy_(true_nut)
+        ev_nut = torch.cuda.Event()
+        ev_nut.record(side)
+        work.fields["p"].copy_(true_p)
+        ev_p = torch.cuda.Event()
+        ev_p.record(side)
+    rep = solver.step(work, sc.solver, comp.psys, comp.preconditioner, sc.inlet, _defer=(ev_nut, ev_p))
+    torch.cuda.synchronize()
+    assert rep.pcg.iterations > 0
+    for n in NAMES:
+        assert torch.equal(work.fields[n], ref.fields[n]), n
