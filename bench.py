@@ -447,8 +447,10 @@ def run_b200(args):
     torch.cuda.synchronize()
     barrier()
     t0 = time.perf_counter()
+    e2e_iters = []
     for _ in range(k_e2e):
-        stepper.step(sc.solver, comp.psys, comp.preconditioner, sc.inlet, pcg_tol=sc.pcg_tol)
+        e2e_iters.append(stepper.step(sc.solver, comp.psys, comp.preconditioner, sc.inlet,
+                                      pcg_tol=sc.pcg_tol).pcg.iterations)
     stepper.synchronize()
     torch.cuda.synchronize()
     e2e_s = time.perf_counter() - t0
@@ -458,7 +460,7 @@ def run_b200(args):
         e2e_s = float(t.item())
     xfer = sum(int(host[n].numel() * host[n].element_size()) for n in names)
     e2e = {"value": world * ncell * k_e2e / e2e_s, "unit": UNIT, "h2d_bytes_per_step": xfer,
-           "d2h_bytes_per_step": xfer,
+           "d2h_bytes_per_step": xfer, "steps": k_e2e, "pcg_iterations": e2e_iters,
            "path": "solver.HostStepper.step() on a host-resident state: every step uploads the 7 fields from "
                    "pinned host memory, steps, and downloads the 7 fields; the two copy directions overlap "
                    "field by field across consecutive steps, and nu_t and p upload while the advection runs"}

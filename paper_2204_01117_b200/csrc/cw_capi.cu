@@ -370,11 +370,6 @@ static inline dim3 g3r(int ex, int ey, int nz) {
   return dim3((unsigned)bx, (unsigned)by, (unsigned)std::max(1, std::min(nz, 2048 / std::max(1, bx * by))));
 }
 static const dim3 B3R(ST_BX, 8, 1);
-static inline dim3 g3c(const Dims& d, int comp) {
-  int ex, ey, ez;
-  comp_extent(d, comp, ex, ey, ez);
-  return g3(ex, ey, ez);
-}
 static inline int nblk(long long n, int bs = 256) {
   long long b = (n + bs - 1) / bs;
   return (int)std::max<long long>(1, std::min<long long>(b, 148LL * 32));
@@ -574,7 +569,6 @@ static void launch_bc(cw_ctx* c, BcFields<T> F, const int8_t* lab, long long ver
     const int e1 = axis == 0 ? d.ny : d.nx, e2 = axis == 2 ? d.ny : d.nz;
     (k_bc_outlet_side<T><<<nblk((long long)(e1 + 1) * (e2 + 1)), 256, 0, st>>>(d, axis, pos, F, lab, c->gate), ++c->launches);
   }
-  const long long n = c->ncell + c->nu_ + c->nv_ + (d.is2d ? 0 : c->nw_);
   (k_bc_inlet_wall<T><<<g3(d.nx + 1, d.ny + 1, d.nz + 1), B3, 0, st>>>(d, F, lab, (const T*)c->uzx, (const T*)c->uzy, (T)prm->k_in,
                                               (T)prm->omega_in, (T)(prm->k_in / prm->omega_in), c->gate), ++c->launches);
 }
@@ -711,7 +705,6 @@ static void st_advect(cw_ctx* c, const StepPtrs<T>& P, const cw_params* prm, T* 
 template <typename T>
 static void st_diffuse(cw_ctx* c, const StepPtrs<T>& P, const cw_params* prm, cudaStream_t st) {
   const Dims& d = c->d;
-  const long long nf[3] = {c->nu_, c->nv_, c->nw_};
   T* cu[3] = {P.u, P.v, P.w};
   double cap = nu_stable<T>(c, prm->dt) - prm->nu;
   if (cap <= 0) cap = 0.0;                               // solver.py:195-201
@@ -724,7 +717,6 @@ template <typename T>
 static void st_drag(cw_ctx* c, const StepPtrs<T>& P, const cw_params* prm, int has_drag, cudaStream_t st) {
   if (!has_drag) return;                                 // solver.py:157-158
   const Dims& d = c->d;
-  const long long nf[3] = {c->nu_, c->nv_, c->nw_};
   T* cu[3] = {P.u, P.v, P.w};
   (k_cell_speed<T><<<g3(d.nx, d.ny, d.nz), B3, 0, st>>>(d, P.u, P.v, P.w, (T*)c->speed, c->gate), ++c->launches);
   (k_drag<T><<<g3z(d.nx + 1, d.ny + 1, d.nz + 1), B3, 0, st>>>(d, cu[0], cu[1], cu[2], P.g, (const T*)c->speed,
@@ -737,8 +729,6 @@ static void st_project_tail(cw_ctx* c, const StepPtrs<T>& P, const cw_params* pr
 template <typename T>
 static int st_project(cw_ctx* c, const StepPtrs<T>& P, const cw_fields* f, const cw_params* prm, double tol,
                       DevReport* rep, cudaStream_t st) {
-  const Dims& d = c->d;
-  const long long nf[3] = {c->nu_, c->nv_, c->nw_};
   T* cu[3] = {P.u, P.v, P.w};
   const bool tpcg = c->pcg_timed < (int)c->pev.size() / 2;
   if (tpcg) cudaEventRecord(c->pev[2 * c->pcg_timed], st);
