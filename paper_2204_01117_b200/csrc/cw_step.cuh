@@ -759,15 +759,17 @@ __global__ void k_div_max(Dims d, const T* __restrict__ u, const T* __restrict__
   // planes d.o0 + blockIdx.z, + gridDim.z, ...: a few blocks per column, one atomic each
   const int i = (int)(blockIdx.x * ST_BX + threadIdx.x), j = (int)(blockIdx.y * 8 + threadIdx.y);
   if (i < d.nx && j < d.ny) {
+    // the label does not gate the loads (one memory round trip per plane, not two)
+#pragma unroll 2
     for (int k = d.o0 + (int)blockIdx.z; k < d.o1; k += (int)gridDim.z) {
       const int c = d.cidx32(i, j, k);
-      if (!is_unknown(lab[c])) continue;
+      const bool unk = is_unknown(lab[c]);
       const int ui = ((int)k * d.ny + j) * (d.nx + 1) + i;
       const int vi = ((int)k * (d.ny + 1) + j) * d.nx + i;
       T div = (u[ui + 1] - u[ui]) * inv_h<T>(d, 0) + (v[vi + d.nx] - v[vi]) * inv_h<T>(d, 1);
       if (!d.is2d) div = div + (w[c + (int)d.nx * d.ny] - w[c]) * inv_h<T>(d, 2);
       const T a = fabs(div);
-      m = (a > m || a != a) ? a : m;
+      if (unk) m = (a > m || a != a) ? a : m;
     }
   }
   m = block_max_2d(m, scratch);
