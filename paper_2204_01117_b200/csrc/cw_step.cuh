@@ -722,13 +722,14 @@ __device__ __forceinline__ void gradient_face(const Dims& d, int comp, T* __rest
     q[comp] = f;
     const int hi = d.cidx32(q[0], q[1], q[2]);
     const int8_t la = lab[lo], lb = lab[hi];
+    const T plo = p[lo], phi = p[hi], a = arr[c];   // not gated on the labels: one memory round trip
     const bool au = is_unknown(la), bu = is_unknown(lb);
     T grad = (T)0;
-    if (au && bu) grad = (p[hi] - p[lo]) * rh;
-    else if (au && lb == OUTLET) grad = -p[lo] * rh;
-    else if (bu && la == OUTLET) grad = p[hi] * rh;
+    if (au && bu) grad = (phi - plo) * rh;
+    else if (au && lb == OUTLET) grad = -plo * rh;
+    else if (bu && la == OUTLET) grad = phi * rh;
     else return;
-    arr[c] -= dt * grad;
+    arr[c] = a - dt * grad;
   }
 }
 
