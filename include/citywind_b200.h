@@ -205,6 +205,18 @@ int cw_run_stage(cw_ctx *ctx, const cw_fields *f, const cw_params *prm, const cw
  * the status of the first failed step (CW_OK if none). */
 int cw_read_reports(cw_ctx *ctx, cw_report *out, int n, int *n_out, void *stream);
 
+/* Iteration cap of the projection's PCG (ref project(max_iter=10_000),
+ * solver.py:246-249 -> pcg_solve(max_iter), linalg.py:310-368): a solve that
+ * has not met the stopping rule after max_iter iterations reports
+ * CW_ERR_PCG with iterations == max_iter.  Default 10000. */
+int cw_set_max_iter(cw_ctx *ctx, int max_iter);
+
+/* After a step reported CW_ERR_NONFINITE: put the state back as the
+ * reference leaves it when update_turbulence raises (ref turbulence.py:121-131,
+ * before any assignment) -- k and omega as advected this step, nu_t as before
+ * the step.  Synchronises `stream`. */
+int cw_turb_rollback(cw_ctx *ctx, const cw_fields *f, void *stream);
+
 /* Per-stage device timings of the next cw_step call (ms per stage, keys of
  * StepReport.timings, ref solver.py:418-454): enable before, read after. */
 int cw_set_stage_timing(cw_ctx *ctx, int enabled);
@@ -226,6 +238,15 @@ long long cw_launch_count(cw_ctx *ctx, int reset);
  * count_out[b] = 0 means "region contains no air cells". Deterministic. */
 int cw_region_speed(cw_ctx *ctx, const cw_fields *f, int n, const double *lo3n,
                     const double *hi3n, double *mean_out, long long *count_out, void *stream);
+
+/* The trailing window of evaluate_objective (ref optimize.py:93-99,
+ * `sums[ri] += region_average_speed(state, r.lo, r.hi)` after every step):
+ * while n > 0, every following cw_step adds the n region means of the
+ * stepped state to the device array d_sums (float64, in step order) and
+ * writes the air-cell counts to d_counts -- no host synchronisation per step.
+ * n = 0 turns it off.  Boxes as for cw_region_speed. */
+int cw_step_regions(cw_ctx *ctx, int n, const double *lo3n, const double *hi3n, double *d_sums,
+                    long long *d_counts);
 
 /* Velocity at physical points, float64 trilinear samples of the staggered
  * grids (the probes of run_simulation, ref scenario.py:473-478, via

@@ -126,6 +126,8 @@ SIGNATURES = {
                                C.c_int, C.c_double, _P]),
     "cw_read_reports": (C.c_int, [_P, C.POINTER(cw_report), C.c_int, C.POINTER(C.c_int), _P]),
     "cw_step_defer": (C.c_int, [_P, _P, _P]),
+    "cw_set_max_iter": (C.c_int, [_P, C.c_int]),
+    "cw_turb_rollback": (C.c_int, [_P, C.POINTER(cw_fields), _P]),
     "cw_set_stage_timing": (C.c_int, [_P, C.c_int]),
     "cw_read_stage_timings": (C.c_int, [_P, C.POINTER(C.c_float)]),
     "cw_pcg_timing": (C.c_int, [_P, C.c_int]),
@@ -136,6 +138,7 @@ SIGNATURES = {
     "cw_region_speed": (C.c_int, [_P, C.POINTER(cw_fields), C.c_int, C.POINTER(C.c_double),
                                   C.POINTER(C.c_double), C.POINTER(C.c_double),
                                   C.POINTER(C.c_longlong), _P]),
+    "cw_step_regions": (C.c_int, [_P, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double), _P, _P]),
     "cw_voxelize": (C.c_int, [_P, C.POINTER(cw_object), C.c_int, C.POINTER(C.c_double),
                               C.POINTER(C.c_int), C.c_int, _P, _P, _P, _P, C.POINTER(C.c_int), _P]),
 }

@@ -173,6 +173,21 @@ __global__ void k_region_fold(int nblocks, int n, const double* part, const long
   cout[b] = m;
 }
 
+// the same fold, added to running sums in step order (the reference's
+// sums[ri] += region_average_speed(...), optimize.py:96-99); counts keep the
+// latest step's air-cell count (labels are fixed: the same every step)
+__global__ void k_region_accum(int nblocks, int n, const double* part, const long long* cnt, double* sums,
+                               long long* counts, const int* gate) {
+  if (*gate) return;
+  const int b = threadIdx.x;
+  if (b >= n) return;
+  double s = 0.0;
+  long long m = 0;
+  for (int q = 0; q < nblocks; ++q) { s += part[q * 16 + b]; m += cnt[q * 16 + b]; }
+  sums[b] += m > 0 ? s / (double)m : 0.0;
+  counts[b] = m;
+}
+
 }  // namespace cw
 
 namespace cw {

@@ -64,12 +64,20 @@ struct cw_ctx {
   long long* reg_cnt = nullptr;
   double* reg_out = nullptr;
   long long* reg_cout = nullptr;
+  // per-step region-speed accumulation (cw_step_regions): after every step
+  // the region means are added to reg_sums (the trailing window of
+  // evaluate_objective, optimize.py:93-99), no host round trip
+  int reg_n = 0;
+  RegionBoxes reg_boxes{};
+  double* reg_sums = nullptr;
+  long long* reg_counts = nullptr;
   int* flag = nullptr;
   // operator
   bool have_op = false;
   double omega = 1.65, tol_default = 0.0;
   double tol_kind[3] = {1e-8, 0.0, 0.0};   // default_projection_tol per preconditioner kind
   int precond = 2;
+  int max_iter = 10000;        // project(max_iter=10_000), solver.py:249; cw_set_max_iter
   long long n_unknown = 0;
   double op_sum[2] = {0.0, 0.0};   // owned-plane sums of diag(W) (AI1) and 1/d (Jacobi)
   long long op_n = 0;
@@ -617,7 +625,7 @@ static void fill_pcg_args(PcgArgs<T>& A, cw_ctx* c, const cw_fields* f, DevRepor
   A.dt = dt;
   A.tol = tol;
   A.res_factor = std::pow(10.0, -4.5);   // DIV_REDUCTION_TARGET, solver.py:232
-  A.max_iter = 10000;                    // project(max_iter=10_000), solver.py:249
+  A.max_iter = c->max_iter;              // project(max_iter=10_000) by default, solver.py:249
   A.precond = c->precond;
   A.ntx = c->ntx; A.nty = c->nty; A.zc = c->zc; A.U = c->U;
   A.o0 = c->d.o0; A.o1 = c->d.o1;
@@ -762,7 +770,7 @@ static void st_turb(cw_ctx* c, const StepPtrs<T>& P, const cw_params* prm, const
   sc.lim_scale = (double)((T)2 / (T)prm->c_mu);   // the kernel's former per-cell (T)2 / (T)c_mu, bit for bit
   sc.k_in = prm->k_in; sc.om_in = prm->omega_in; sc.nut_in = prm->k_in / prm->omega_in;
   (k_turbulence<T><<<dim3((c->d.nx + ST_BX - 1) / ST_BX, (c->d.ny + ST_BY - 1) / ST_BY,
-                          (c->d.nz + ZT_TURB - 1) / ZT_TURB), B3, 0, st>>>(c->d, P.u, P.v, P.w, kin, win, P.k, P.om, P.nut, sc, rep, c->gate), ++c->launches);
+                          (c->d.nz + ZT_TURB - 1) / ZT_TURB), B3, 0, st>>>(c->d, P.u, P.v, P.w, kin, win, P.k, P.om, P.nut, (T*)c->speed, sc, rep, c->gate), ++c->launches);
   (k_turb_check<<<1, 1, 0, st>>>(rep, c->gate), ++c->launches);
 }
 
@@ -773,6 +781,22 @@ static StepPtrs<T> ptrs_of(const cw_fields* f) {
   P.k = (T*)f->k; P.om = (T*)f->omega; P.nut = (T*)f->nu_t;
   P.lab = (const int8_t*)f->labels; P.lab_ver = f->labels_version; P.g = (const T*)f->g;
   return P;
+}
+
+// region means of the current state (k_region_partials + a fold): into
+// reg_out / reg_cout, or (accumulate) added to reg_sums in step order
+template <typename T>
+static void launch_regions(cw_ctx* c, const cw_fields* f, bool accumulate, cudaStream_t st) {
+  const RegionBoxes& B = c->reg_boxes;
+  const int nb = std::min(nblk(c->ncell), 1024);
+  (k_region_partials<T><<<nb, 256, 0, st>>>(c->d, c->grid.origin[0], c->grid.origin[1], c->grid.origin[2],
+      (const T*)f->u, (const T*)f->v, (const T*)f->w, (const int8_t*)f->labels, B, c->reg_part, c->reg_cnt),
+   ++c->launches);
+  if (accumulate)
+    (k_region_accum<<<1, 64, 0, st>>>(nb, B.n, c->reg_part, c->reg_cnt, c->reg_sums, c->reg_counts, c->gate),
+     ++c->launches);
+  else
+    (k_region_fold<<<1, 64, 0, st>>>(nb, B.n, c->reg_part, c->reg_cnt, c->reg_out, c->reg_cout), ++c->launches);
 }
 
 // one full step (solver.py:407-461): no copies, stage temporaries chained
@@ -813,6 +837,7 @@ static int enqueue_step(cw_ctx* c, const cw_fields* f, const cw_params* prm, dou
   (k_speed_max_flat<T><<<4 * 148, B3R, 0, st>>>(c->d, P.u, P.v, P.w, rep, c->gate),
    ++c->launches);
   mark(7);
+  if (c->reg_n > 0) launch_regions<T>(c, f, true, st);        // trailing-window region sums
   CW_CUDA(cudaGetLastError());
   return CW_OK;
 }
@@ -1085,7 +1110,14 @@ extern "C" int cw_run_stage(cw_ctx* c, const cw_fields* f, const cw_params* prm,
 
 extern "C" int cw_step(cw_ctx* c, const cw_fields* f, const cw_params* prm, const cw_inlet* inl, double pcg_tol,
                        int nsteps, void* stream) {
-  if (!c || !f || !prm || !inl) return fail(CW_ERR_INVALID, "null argument");
+  if (!c) return fail(CW_ERR_INVALID, "null argument");
+  // the one-shot waits of cw_step_defer belong to this call only: cleared on
+  // every exit (the first enqueued step consumes them)
+  struct DeferGuard {
+    cw_ctx* c;
+    ~DeferGuard() { c->wait_nut = nullptr; c->wait_p = nullptr; }
+  } defer_guard{c};
+  if (!f || !prm || !inl) return fail(CW_ERR_INVALID, "null argument");
   if (!c->have_op) return fail(CW_ERR_INVALID, "cw_set_operator has not been called");
   if (nsteps < 0) return fail(CW_ERR_INVALID, "nsteps < 0");
   if (c->head + nsteps > RING) return fail(CW_ERR_INVALID, "report ring full: call cw_read_reports");
@@ -1228,6 +1260,27 @@ extern "C" long long cw_launch_count(cw_ctx* c, int reset) {
   return v;
 }
 
+extern "C" int cw_turb_rollback(cw_ctx* c, const cw_fields* f, void* stream) {
+  if (!c || !f) return fail(CW_ERR_INVALID, "null argument");
+  CW_CUDA(cudaSetDevice(c->device));
+  const int nb = std::min(nblk(c->ncell), 4 * c->num_sms * 8);
+  if (c->prec == 4)
+    (k_turb_rollback<float><<<nb, 256, 0, S(stream)>>>(c->ncell, (const float*)c->tk, (const float*)c->tw,
+        (const float*)c->speed, (float*)f->k, (float*)f->omega, (float*)f->nu_t), ++c->launches);
+  else
+    (k_turb_rollback<double><<<nb, 256, 0, S(stream)>>>(c->ncell, (const double*)c->tk, (const double*)c->tw,
+        (const double*)c->speed, (double*)f->k, (double*)f->omega, (double*)f->nu_t), ++c->launches);
+  CW_CUDA(cudaGetLastError());
+  CW_CUDA(cudaStreamSynchronize(S(stream)));
+  return CW_OK;
+}
+
+extern "C" int cw_set_max_iter(cw_ctx* c, int max_iter) {
+  if (!c || max_iter < 0) return fail(CW_ERR_INVALID, "max_iter must be >= 0");
+  c->max_iter = max_iter;
+  return CW_OK;
+}
+
 extern "C" int cw_step_defer(cw_ctx* c, void* nu_t_ready, void* p_ready) {
   if (!c) return fail(CW_ERR_INVALID, "null argument");
   c->wait_nut = (cudaEvent_t)nu_t_ready;
@@ -1254,21 +1307,30 @@ extern "C" int cw_region_speed(cw_ctx* c, const cw_fields* f, int n, const doubl
                                double* mean_out, long long* count_out, void* stream) {
   if (!c || !f || n < 1 || n > 16 || !lo || !hi) return fail(CW_ERR_INVALID, "bad region arguments (1..16 boxes)");
   CW_CUDA(cudaSetDevice(c->device));
-  RegionBoxes B;
+  const RegionBoxes keep = c->reg_boxes;
+  RegionBoxes& B = c->reg_boxes;
   B.n = n;
   for (int b = 0; b < n; ++b)
     for (int a = 0; a < 3; ++a) { B.lo[b][a] = lo[3 * b + a]; B.hi[b][a] = hi[3 * b + a]; }
-  const int nb = std::min(nblk(c->ncell), 1024);
-  if (c->prec == 4)
-    (k_region_partials<float><<<nb, 256, 0, S(stream)>>>(c->d, c->grid.origin[0], c->grid.origin[1], c->grid.origin[2],
-        (const float*)f->u, (const float*)f->v, (const float*)f->w, (const int8_t*)f->labels, B, c->reg_part, c->reg_cnt), ++c->launches);
-  else
-    (k_region_partials<double><<<nb, 256, 0, S(stream)>>>(c->d, c->grid.origin[0], c->grid.origin[1], c->grid.origin[2],
-        (const double*)f->u, (const double*)f->v, (const double*)f->w, (const int8_t*)f->labels, B, c->reg_part, c->reg_cnt), ++c->launches);
-  (k_region_fold<<<1, 64, 0, S(stream)>>>(nb, n, c->reg_part, c->reg_cnt, c->reg_out, c->reg_cout), ++c->launches);
+  if (c->prec == 4) launch_regions<float>(c, f, false, S(stream));
+  else launch_regions<double>(c, f, false, S(stream));
+  c->reg_boxes = keep;   // a pending cw_step_regions set stays in force
   CW_CUDA(cudaGetLastError());
   CW_CUDA(cudaMemcpyAsync(mean_out, c->reg_out, n * sizeof(double), cudaMemcpyDeviceToHost, S(stream)));
   CW_CUDA(cudaMemcpyAsync(count_out, c->reg_cout, n * sizeof(long long), cudaMemcpyDeviceToHost, S(stream)));
   CW_CUDA(cudaStreamSynchronize(S(stream)));
+  return CW_OK;
+}
+
+extern "C" int cw_step_regions(cw_ctx* c, int n, const double* lo, const double* hi, double* sums_dev,
+                               long long* counts_dev) {
+  if (!c || n < 0 || n > 16) return fail(CW_ERR_INVALID, "bad region arguments (0..16 boxes)");
+  if (n > 0 && (!lo || !hi || !sums_dev || !counts_dev)) return fail(CW_ERR_INVALID, "null argument");
+  c->reg_n = n;
+  c->reg_boxes.n = n;
+  for (int b = 0; b < n; ++b)
+    for (int a = 0; a < 3; ++a) { c->reg_boxes.lo[b][a] = lo[3 * b + a]; c->reg_boxes.hi[b][a] = hi[3 * b + a]; }
+  c->reg_sums = sums_dev;
+  c->reg_counts = counts_dev;
   return CW_OK;
 }

@@ -888,7 +888,8 @@ template <typename T>
 __global__ void k_turbulence(Dims d, const T* __restrict__ u, const T* __restrict__ v,
                              const T* __restrict__ w, const T* __restrict__ kin,
                              const T* __restrict__ win, T* __restrict__ kout, T* __restrict__ wout,
-                             T* __restrict__ nut, StepConsts sc, DevReport* rep, const int* gate) {
+                             T* __restrict__ nut, T* __restrict__ nut_prev, StepConsts sc, DevReport* rep,
+                             const int* gate) {
   if (*gate) return;
   const T dt = (T)sc.dt, nu = (T)sc.nu, cap = (T)sc.cap_turb;
   const int i = (int)(blockIdx.x * ST_BX + threadIdx.x), j = (int)(blockIdx.y * ST_BY + threadIdx.y);
@@ -928,7 +929,23 @@ __global__ void k_turbulence(Dims d, const T* __restrict__ u, const T* __restric
     omt = omt > (T)1e-8 ? omt : (T)1e-8;
     kout[c] = kf;
     wout[c] = wf;
+    nut_prev[c] = nt;   // kept for cw_turb_rollback (the reference raises before it assigns)
     nut[c] = kf / omt;
+  }
+}
+
+// After a non-finite k / omega (status 2) the reference has raised before it
+// assigned anything (turbulence.py:121-131): the state keeps the advected
+// k, omega (still in the step's upwind buffers) and the previous nu_t
+// (k_turbulence saved it).  Launched by cw_turb_rollback on the error path only.
+template <typename T>
+__global__ void k_turb_rollback(long long n, const T* __restrict__ k_adv, const T* __restrict__ w_adv,
+                                const T* __restrict__ nut_prev, T* __restrict__ k, T* __restrict__ w,
+                                T* __restrict__ nut) {
+  CW_GRID_STRIDE(c, n) {
+    k[c] = k_adv[c];
+    w[c] = w_adv[c];
+    nut[c] = nut_prev[c];
   }
 }
 

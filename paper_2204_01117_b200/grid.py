@@ -249,11 +249,57 @@ def default_device():
     return torch.device("cuda", torch.cuda.current_device())
 
 
+class FieldView(np.ndarray):
+    """Reference-layout float64 host copy of one device field that writes
+    through.  ``state.u`` in the reference is the live array: code such as
+    ``arr = state.u; arr *= fac`` or ``state.k[i, j, k] = x`` mutates the
+    state (reference solver.py:164-167).  Item assignment and in-place
+    ufuncs on a FieldView (or any slice of it) therefore copy the whole
+    field back to the device.  A view taken before the state was stepped is
+    detached, as the reference's arrays are once ``step`` reassigns them
+    (solver.py:423-425): writing to it no longer touches the state."""
+
+    def _wt(self):
+        return getattr(self, "_cw", None)
+
+    def __array_finalize__(self, obj):
+        if obj is not None and type(obj) is FieldView:
+            self._cw = getattr(obj, "_cw", None)
+
+    def _push(self):
+        cw = self._wt()
+        if cw is None:
+            return
+        state, name, root = cw
+        if state._views.get(name, (None, None))[1] is root:   # still the state's live view
+            state._set(name, root.view(np.ndarray), _touch=False)
+            state._views[name] = (state._view_key(name), root)
+
+    def __setitem__(self, key, value):
+        np.ndarray.__setitem__(self.view(np.ndarray), key, value)
+        self._push()
+
+    def __array_ufunc__(self, ufunc, method, *inputs, out=None, **kwargs):
+        plain = lambda a: a.view(np.ndarray) if isinstance(a, FieldView) else a  # noqa: E731
+        args = [plain(a) for a in inputs]
+        if out is not None:
+            kwargs["out"] = tuple(plain(o) for o in out)
+        res = getattr(ufunc, method)(*args, **kwargs)
+        if out is not None:
+            for o in out:
+                if isinstance(o, FieldView):
+                    o._push()
+            return out[0] if len(out) == 1 else out
+        return res
+
+
 class FlowState:
     """Device-resident simulation state (grid.py:492-571).
 
     ``fields[name]`` are CUDA tensors in the x-fastest layout; ``labels_dev``
     is int8, ``phi_dev``/``lad_dev`` float64 (bit-exact voxelizer output).
+    Attribute access ``state.u`` etc. returns a write-through reference-layout
+    float64 copy (``FieldView``).
     """
 
     def __init__(self, grid: GridSpec, fields: dict, labels_dev, phi_dev, lad_dev,
@@ -268,6 +314,17 @@ class FlowState:
         self._drag_key = None
         self._g = None
         self._has_drag = False
+        self._version = 0
+        self._views = {}
+
+    def touch(self):
+        """Mark the device fields as changed (a step or stage ran): field
+        views taken before are detached from the state."""
+        self._version += 1
+        self._views.clear()
+
+    def _view_key(self, name):
+        return (self._version, self.fields[name]._version, self.fields[name].data_ptr())
 
     # construction ----------------------------------------------------------
     @classmethod
@@ -300,16 +357,25 @@ class FlowState:
     def _get(self, name):
         return to_ref_layout(self.fields[name].detach().cpu().numpy().astype(np.float64))
 
-    def _set(self, name, value):
+    def _set(self, name, value, _touch=True):
         value = np.asarray(value, dtype=np.float64)
         shp = self.grid.dshape(name)[::-1]
         if value.shape != shp:
             value = np.broadcast_to(value, shp)
         self.fields[name].copy_(torch.from_numpy(to_device_layout(value)).to(self.dtype))
+        if _touch:
+            self.touch()
 
     def __getattr__(self, name):
-        if name in FIELDS:
-            return self._get(name)
+        if name in FIELDS and "fields" in self.__dict__:
+            # one live view per field while the device copy is unchanged, so
+            # two reads alias like the reference's arrays
+            key, arr = self._views.get(name, (None, None))
+            if arr is None or key != self._view_key(name):
+                arr = np.ascontiguousarray(self._get(name)).view(FieldView)
+                arr._cw = (self, name, arr)
+                self._views[name] = (self._view_key(name), arr)
+            return arr
         raise AttributeError(name)
 
     def __setattr__(self, name, value):
@@ -337,6 +403,11 @@ class FlowState:
         self.phi_dev.copy_(torch.from_numpy(to_device_layout(np.asarray(por.phi, np.float64))))
         self.lad_dev.copy_(torch.from_numpy(to_device_layout(np.asarray(por.lad, np.float64))))
         self._drag_key = None
+
+    def __getstate__(self):
+        d = dict(self.__dict__)
+        d["_views"] = {}
+        return d
 
     def copy(self) -> "FlowState":
         return FlowState(self.grid, {n: t.clone() for n, t in self.fields.items()},

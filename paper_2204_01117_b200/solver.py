@@ -215,6 +215,14 @@ def _raise_for(rc: int, rep, grid: GridSpec):
     N.check(rc)
 
 
+def _rollback(ctx, f, rep):
+    """A non-finite turbulence update: leave the state as the reference does
+    when update_turbulence raises (turbulence.py:121-131, before it assigns):
+    advected k and omega, the previous nu_t (``cw_turb_rollback``)."""
+    if rep.status == N.CW_ERR_NONFINITE:
+        N.check(N.lib().cw_turb_rollback(ctx.h, C.byref(f), ctx.stream))
+
+
 def _report_of(r, timings) -> StepReport:
     return StepReport(timings=timings, pcg=PcgReport(int(r.iterations), bool(r.converged), float(r.criterion)),
                       cfl=float(r.cfl), div_before=float(r.div_before), div_after=float(r.div_after))
@@ -311,16 +319,23 @@ class HostStepper:
 
 def step_many(state: FlowState, params: SolverParams, psys: PressureSystem, preconditioner,
               profile: InletProfile, nsteps: int, pcg_tol: float | None = None,
-              stage_timings: bool = False, read_back: bool = True, _defer=None) -> list:
+              stage_timings: bool = False, read_back: bool = True, _defer=None, regions=None) -> list:
     """``nsteps`` calls of ``step`` enqueued back to back on the device (no
     host synchronisation between steps).  If a step fails, the following
     steps of the batch are skipped on the device and the exception of the
-    failing step is raised with the state as it was at the failure."""
+    failing step is raised with the state as it was at the failure.
+
+    ``regions=(lo, hi, sums, counts)``: after every step the mean speeds of
+    the boxes (rows of lo / hi) are added on the device to the float64
+    tensor ``sums`` and the air-cell counts written to ``counts`` (int64) --
+    the trailing window of evaluate_objective (optimize.py:93-99) without a
+    host round trip per step (``cw_step_regions``)."""
     dt = params.dt
     if dt == 0.0 or nsteps <= 0:
         return [StepReport() for _ in range(max(nsteps, 0))]
     _warn_cap(state, params, dt)
     ctx = _acquire(psys, preconditioner, state)
+    state.touch()
     try:
         g, has_drag = drag_coefficient(state, params)
         f = ctx.fields(state, g, has_drag)
@@ -332,6 +347,15 @@ def step_many(state: FlowState, params: SolverParams, psys: PressureSystem, prec
             lib.cw_set_stage_timing(ctx.h, 1)
         if _defer is not None:
             N.check(lib.cw_step_defer(ctx.h, C.c_void_p(_defer[0].cuda_event), C.c_void_p(_defer[1].cuda_event)))
+        if regions is not None:
+            rlo, rhi, rsums, rcounts = regions
+            rlo = np.ascontiguousarray(np.atleast_2d(rlo), dtype=np.float64)
+            rhi = np.ascontiguousarray(np.atleast_2d(rhi), dtype=np.float64)
+            if rsums.dtype != torch.float64 or rcounts.dtype != torch.int64 or rsums.numel() < len(rlo):
+                raise ValueError("regions: sums must be float64 and counts int64 device tensors of n entries")
+            N.check(lib.cw_step_regions(ctx.h, len(rlo), rlo.ctypes.data_as(C.POINTER(C.c_double)),
+                                        rhi.ctypes.data_as(C.POINTER(C.c_double)), N.ptr(rsums),
+                                        N.ptr(rcounts)))
         t0 = time.perf_counter()
         done = 0
         reports = []
@@ -353,6 +377,7 @@ def step_many(state: FlowState, params: SolverParams, psys: PressureSystem, prec
                 timings = {k: float(ms[i]) * 1e-3 for i, k in enumerate(STAGE_KEYS)}
             for r in reps:
                 if r.status != N.CW_OK:
+                    _rollback(ctx, f, r)
                     _raise_for(r.status, r, state.grid)
                 reports.append(_report_of(r, dict(timings)))
                 state.time += dt
@@ -364,6 +389,8 @@ def step_many(state: FlowState, params: SolverParams, psys: PressureSystem, prec
             state.step_count += nsteps
         return reports
     finally:
+        if regions is not None:
+            N.lib().cw_step_regions(ctx.h, 0, None, None, None, None)
         psys.pool.release(ctx)
 
 
@@ -374,6 +401,7 @@ def finish(state: FlowState, psys: PressureSystem, preconditioner, nsteps: int):
         rc, reps = ctx.read_reports(nsteps)
         for r in reps:
             if r.status != N.CW_OK:
+                _rollback(ctx, ctx.fields(state, state._g, state._has_drag), r)
                 _raise_for(r.status, r, state.grid)
         return [_report_of(r, {}) for r in reps]
     finally:
@@ -383,12 +411,15 @@ def finish(state: FlowState, psys: PressureSystem, preconditioner, nsteps: int):
 # ---------------------------------------------------------------------------
 # stage functions (same names as the reference; each runs its device kernels)
 
-def _stage(state, params, profile, stage, dt, psys=None, preconditioner=None, tol=None):
+def _stage(state, params, profile, stage, dt, psys=None, preconditioner=None, tol=None, max_iter=None):
     if psys is not None:
         ctx = _acquire(psys, preconditioner, state)
     else:
         ctx = _scratch_ctx(state)
+    state.touch()
     try:
+        if max_iter is not None:
+            N.check(N.lib().cw_set_max_iter(ctx.h, int(max_iter)))
         g, has_drag = drag_coefficient(state, params) if stage == N.STAGE_DRAG else (None, False)
         f = ctx.fields(state, g, has_drag)
         prm = params.native(dt)
@@ -399,9 +430,12 @@ def _stage(state, params, profile, stage, dt, psys=None, preconditioner=None, to
         if rc != N.CW_OK:
             if not reps:
                 N.check(rc)
+            _rollback(ctx, f, reps[0])
             _raise_for(rc, reps[0], state.grid)
         return reps[0]
     finally:
+        if max_iter is not None:
+            N.lib().cw_set_max_iter(ctx.h, 10_000)
         if psys is not None:
             psys.pool.release(ctx)
 
@@ -441,10 +475,13 @@ def update_turbulence(state: FlowState, params: SolverParams, dt: float) -> Flow
 
 def project(state: FlowState, psys: PressureSystem, dt: float, preconditioner=None,
             tol: float | None = None, max_iter: int = 10_000):
-    """solver.py:246-304: warm-started PCG + gradient update, on the device."""
-    if max_iter != 10_000:
-        raise NotImplementedError("the device projection uses the reference's max_iter=10000")
-    r = _stage(state, SolverParams(dt=dt), None, N.STAGE_PROJECT, dt, psys, preconditioner, tol)
+    """solver.py:246-304: warm-started PCG + gradient update, on the device.
+    A solve that has not converged after ``max_iter`` iterations raises
+    ProjectionError (pcg_solve(max_iter), linalg.py:310-368)."""
+    if max_iter < 0:
+        raise ValueError("max_iter must be >= 0")
+    r = _stage(state, SolverParams(dt=dt), None, N.STAGE_PROJECT, dt, psys, preconditioner, tol,
+               max_iter=None if max_iter == 10_000 else max_iter)
     return state, PcgReport(int(r.iterations), bool(r.converged), float(r.criterion))
 
 

@@ -75,3 +75,38 @@ def test_fd_gradient_sharded_equals_serial():
     from paper_2204_01117_b200.optimize import fd_jobs
     steps, _ = fd_jobs(theta, design, 0.1)
     assert steps == [0.1, 0.1, -0.1, 0.1, 0.1]
+
+
+def _failing_eval(compiled, theta, spec=None, profile=None):
+    t = np.asarray(theta, float)
+    if t[3] > 0.55:      # the job perturbing p3, owned by rank 1 (round robin)
+        raise FloatingPointError("objective evaluation produced nan")
+    return _fake_eval(compiled, theta, spec, profile)
+
+
+def _failing_worker(rank, world, port, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2204_01117_b200.optimize import DesignVector, finite_diff_gradient
+    comp = _Comp()
+    design = DesignVector.from_scenario(comp.scenario)
+    theta = np.array([0.1, -0.2, 0.0, 0.5, 0.9])
+    try:
+        finite_diff_gradient(comp, theta, None, eps=0.1, design=design, group=dist.group.WORLD,
+                             evaluate=_failing_eval)
+        out[rank] = "returned"
+    except FloatingPointError as exc:
+        out[rank] = f"FloatingPointError: {exc}"
+    dist.destroy_process_group()
+
+
+def test_fd_gradient_sharded_job_error_raises_on_every_rank():
+    """a job that raises on one rank must not leave the others
+    waiting in the all-reduce; every rank raises the same exception type."""
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_failing_worker, args=(2, _free_port(), out), nprocs=2, join=True)
+    for r in range(2):
+        assert out[r].startswith("FloatingPointError"), out[r]
+        assert "job 3" in out[r]

@@ -287,8 +287,14 @@ def test_turbulence_nan_names_the_cell():
     k[1, 2, 0] = np.inf
     st.k = k
     st.omega = np.ones(g.shape)
+    st.nu_t = np.full(g.shape, 0.25)
+    before = {n: np.array(getattr(st, n)) for n in ("k", "omega", "nu_t")}
     with pytest.raises(FloatingPointError, match=r"at cell \(\d+, \d+, \d+\)") as ei:
         solver.update_turbulence(st, SolverParams(dt=0.1), 1e30)
+    # the reference raises before it assigns (turbulence.py:121-131): the
+    # state keeps its k, omega and nu_t (cw_turb_rollback)
+    for n, a in before.items():
+        np.testing.assert_array_equal(np.array(getattr(st, n)), a, err_msg=n)
     og = co.Grid(4, 4, 1, 1.0, 1.0, 1.0)
     ost = co.State.zeros(og)
     ost.k[0, 2, 1] = np.inf
