@@ -205,6 +205,14 @@ int cw_run_stage(cw_ctx *ctx, const cw_fields *f, const cw_params *prm, const cw
  * the status of the first failed step (CW_OK if none). */
 int cw_read_reports(cw_ctx *ctx, cw_report *out, int n, int *n_out, void *stream);
 
+/* Layout conversion for a reference-layout caller (refbind.py): the
+ * reference's FlowState holds float64 C-order arrays (ex, ey, ez), x slowest
+ * (ref grid.py:492-571); device fields are x-fastest (ez, ey, ex) in the
+ * context precision.  direction 0: reference float64 (device copy) -> device
+ * field; 1: device field -> reference float64.  field 0 u, 1 v, 2 w, 3 a cell
+ * field (p, k, omega, nu_t).  Device pointers; no synchronisation. */
+int cw_ref_layout(cw_ctx *ctx, int direction, int field, const void *src, void *dst, void *stream);
+
 /* Iteration cap of the projection's PCG (ref project(max_iter=10_000),
  * solver.py:246-249 -> pcg_solve(max_iter), linalg.py:310-368): a solve that
  * has not met the stopping rule after max_iter iterations reports

@@ -127,6 +127,7 @@ SIGNATURES = {
     "cw_read_reports": (C.c_int, [_P, C.POINTER(cw_report), C.c_int, C.POINTER(C.c_int), _P]),
     "cw_step_defer": (C.c_int, [_P, _P, _P]),
     "cw_set_max_iter": (C.c_int, [_P, C.c_int]),
+    "cw_ref_layout": (C.c_int, [_P, C.c_int, C.c_int, _P, _P, _P]),
     "cw_turb_rollback": (C.c_int, [_P, C.POINTER(cw_fields), _P]),
     "cw_set_stage_timing": (C.c_int, [_P, C.c_int]),
     "cw_read_stage_timings": (C.c_int, [_P, C.POINTER(C.c_float)]),
@@ -199,3 +200,8 @@ def dbl3(a) -> C.Array:
 def as_cdouble_array(a: np.ndarray):
     a = np.ascontiguousarray(a, dtype=np.float64)
     return a, a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+def c_stream(stream) -> C.c_void_p:
+    """The cudaStream_t of a torch stream, for the C ABI's `void *stream`."""
+    return C.c_void_p(stream.cuda_stream)

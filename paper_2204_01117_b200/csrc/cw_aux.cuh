@@ -173,6 +173,44 @@ __global__ void k_region_fold(int nblocks, int n, const double* part, const long
   cout[b] = m;
 }
 
+// ---------------------------------------------------------------------------
+// Reference layout <-> device layout (the drop-in binding of refbind.py).
+// The reference's FlowState arrays are float64, C-order (ex, ey, ez) with x
+// slowest (grid.py:492-571); device fields are x-fastest (ez, ey, ex) in the
+// context precision.  For every y the (x, z) plane is a 2-D transpose: 32 x 32
+// tiles through shared memory, both global sides coalesced.  blockIdx.z = y.
+template <typename T>
+__global__ void k_ref_to_dev(const double* __restrict__ src, T* __restrict__ dst, int ex, int ey, int ez) {
+  __shared__ double tile[32][33];
+  const int y = blockIdx.z;
+  const int z0 = blockIdx.x * 32, x0 = blockIdx.y * 32;
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {          // read rows x, contiguous z
+    const int x = x0 + r, z = z0 + threadIdx.x;
+    if (x < ex && z < ez) tile[r][threadIdx.x] = src[((long long)x * ey + y) * ez + z];
+  }
+  __syncthreads();
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {          // write rows z, contiguous x
+    const int z = z0 + r, x = x0 + threadIdx.x;
+    if (x < ex && z < ez) dst[((long long)z * ey + y) * ex + x] = (T)tile[threadIdx.x][r];
+  }
+}
+
+template <typename T>
+__global__ void k_dev_to_ref(const T* __restrict__ src, double* __restrict__ dst, int ex, int ey, int ez) {
+  __shared__ double tile[32][33];
+  const int y = blockIdx.z;
+  const int z0 = blockIdx.y * 32, x0 = blockIdx.x * 32;
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {          // read rows z, contiguous x
+    const int z = z0 + r, x = x0 + threadIdx.x;
+    if (x < ex && z < ez) tile[r][threadIdx.x] = (double)src[((long long)z * ey + y) * ex + x];
+  }
+  __syncthreads();
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {          // write rows x, contiguous z
+    const int x = x0 + r, z = z0 + threadIdx.x;
+    if (x < ex && z < ez) dst[((long long)x * ey + y) * ez + z] = tile[threadIdx.x][r];
+  }
+}
+
 // the same fold, added to running sums in step order (the reference's
 // sums[ri] += region_average_speed(...), optimize.py:96-99); counts keep the
 // latest step's air-cell count (labels are fixed: the same every step)

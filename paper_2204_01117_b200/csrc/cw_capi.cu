@@ -1275,6 +1275,26 @@ extern "C" int cw_turb_rollback(cw_ctx* c, const cw_fields* f, void* stream) {
   return CW_OK;
 }
 
+extern "C" int cw_ref_layout(cw_ctx* c, int direction, int field, const void* src, void* dst, void* stream) {
+  if (!c || !src || !dst || direction < 0 || direction > 1 || field < 0 || field > 3)
+    return fail(CW_ERR_INVALID, "cw_ref_layout: bad argument");
+  CW_CUDA(cudaSetDevice(c->device));
+  int ex = c->d.nx, ey = c->d.ny, ez = c->d.nz;
+  if (field < 3) comp_extent(c->d, field, ex, ey, ez);
+  const dim3 blk(32, 8);
+  if (direction == 0) {
+    const dim3 grd((ez + 31) / 32, (ex + 31) / 32, ey);
+    if (c->prec == 4) (k_ref_to_dev<float><<<grd, blk, 0, S(stream)>>>((const double*)src, (float*)dst, ex, ey, ez), ++c->launches);
+    else (k_ref_to_dev<double><<<grd, blk, 0, S(stream)>>>((const double*)src, (double*)dst, ex, ey, ez), ++c->launches);
+  } else {
+    const dim3 grd((ex + 31) / 32, (ez + 31) / 32, ey);
+    if (c->prec == 4) (k_dev_to_ref<float><<<grd, blk, 0, S(stream)>>>((const float*)src, (double*)dst, ex, ey, ez), ++c->launches);
+    else (k_dev_to_ref<double><<<grd, blk, 0, S(stream)>>>((const double*)src, (double*)dst, ex, ey, ez), ++c->launches);
+  }
+  CW_CUDA(cudaGetLastError());
+  return CW_OK;
+}
+
 extern "C" int cw_set_max_iter(cw_ctx* c, int max_iter) {
   if (!c || max_iter < 0) return fail(CW_ERR_INVALID, "max_iter must be >= 0");
   c->max_iter = max_iter;

@@ -1,0 +1,71 @@
+"""Certify the config goldens (SURVEY.md 8c protocol): does the REFERENCE
+algorithm itself keep its per-step PCG iteration counts when its state is
+perturbed at the level of float32 arithmetic (relative noise 1e-6 on the
+velocity and turbulence fields after every step)?  A scene whose counts
+survive is certified for exact iteration-count parity in fp32.
+
+Runs the oracle (pinned to the reference by tests/test_oracle_golden.py) and
+compares with the reference goldens (tests/golden/cfg_<name>.npz).  Results
+go to tests/golden/cert_<name>.json (one file per scene, so several scenes
+can be certified in parallel processes).
+
+    python scripts/certify_configs.py NAME [NAME ...]
+"""
+from __future__ import annotations
+
+import json
+import os
+import sys
+import time
+
+os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+from oracle import citywind_oracle as co  # noqa: E402
+
+GOLD = os.path.join(ROOT, "tests", "golden")
+
+
+def certify(name, amp=1e-6, seed=0):
+    g = np.load(os.path.join(GOLD, f"cfg_{name}.npz"))
+    doc = json.loads(str(g["doc"]))
+    comp = co.Compiled(co.scene_from_dict(doc))
+    theta = g["theta"] if g["theta"].size else None
+    st = comp.make_state(theta)
+    rng = np.random.default_rng(seed)
+    its = []
+    t0 = time.perf_counter()
+    for _ in range(int(g["steps"])):
+        its.append(comp.step_state(st).pcg.iterations)
+        for f in ("u", "v", "w", "k", "omega", "nu_t"):
+            a = getattr(st, f)
+            setattr(st, f, a * (1 + amp * rng.standard_normal(a.shape)))
+    gold = g["pcg_iterations"].tolist()
+    off = [i + 1 for i, (a, b) in enumerate(zip(its, gold)) if a != b]
+    # the field noise floor: the perturbed reference algorithm's end fields
+    # against the reference's own (whole fields or the golden's subsample)
+    stride = int(g["stride"])
+    floor = {}
+    for n in ("u", "v", "w", "p", "k", "omega", "nu_t"):
+        a = np.asarray(getattr(st, n)).ravel()
+        b = g[f"sub_{n}"] if stride else g[n].ravel()
+        if stride:
+            a = a[::stride]
+        floor[n] = float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+    return {"steps": len(gold), "noise": amp, "mismatched_steps": off, "certified": not off,
+            "field_floor_rel_l2": floor, "oracle_seconds": round(time.perf_counter() - t0, 1)}
+
+
+def main():
+    for name in sys.argv[1:]:
+        res = certify(name)
+        print(name, res, flush=True)
+        with open(os.path.join(GOLD, f"cert_{name}.json"), "w") as fh:
+            json.dump(res, fh, indent=1, sort_keys=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -10,6 +10,7 @@ import pytest
 from oracle import citywind_oracle as co
 from oracle import voxel_oracle as vo
 from paper_2204_01117_b200 import scenes
+from helpers import golden, oracle_compiled
 
 GOLD = os.path.join(os.path.dirname(__file__), "golden")
 
@@ -95,3 +96,20 @@ def test_oracle_voxelizer_full_size_bitexact(name):
     assert sha(phi) == str(g["phi_sha"])
     assert sha(lad) == str(g["lad_sha"])
     assert sha(comp.psys.index) == str(g["index_sha"])
+
+
+@pytest.mark.parametrize("name,steps", [("c1_cuboid_64", 15), ("chopt_sim_120", 15), ("bielefeld_120", 4)])
+def test_oracle_matches_config_golden_prefix(name, steps):
+    """The oracle against the reference's config goldens
+    (scripts/make_golden_configs.py): the first steps' PCG counts and per-step
+    field L2 norms."""
+    import json
+    g = golden(f"cfg_{name}")
+    comp = oracle_compiled(json.loads(str(g["doc"])))
+    theta = g["theta"] if g["theta"].size else None
+    st = comp.make_state(theta)
+    for s in range(steps):
+        assert comp.step_state(st).pcg.iterations == g["pcg_iterations"][s]
+        for n in ("u", "v", "w", "p", "k", "omega", "nu_t"):
+            a = float(np.linalg.norm(getattr(st, n)))
+            assert abs(a - g[f"norm_{n}"][s]) <= 1e-11 * abs(g[f"norm_{n}"][s]), (s, n)
