@@ -39,6 +39,10 @@ extern "C" {
 #define CW_ERR_TIMEOUT 6       /* device grid barrier timed out (never expected) */
 #define CW_ERR_RHS 7           /* ValueError non-finite rhs, ref linalg.py:326-327 */
 #define CW_ERR_GEOMETRY 8      /* ClassificationError, ref geometry.py:31,236-240 */
+#define CW_ERR_HALO 9          /* ValueError: a z-slab window's halo is shallower than the step's
+                                  reach 2 floor(max|w| dt/dz) + 4 (report: criterion = max|w| dt/dz,
+                                  bad_cell = planes needed) -- the reference's backtrace is unbounded,
+                                  ref advection.py:125-142 */
 
 typedef struct cw_ctx cw_ctx;
 
@@ -102,6 +106,7 @@ void cw_ctx_destroy(cw_ctx *ctx);
  * refreshes the halo planes from the neighbours (state at the start of a
  * step, p after the projection).  halo >= 2. */
 #define CW_MAX_SLABS 64
+#define CW_MAX_CHUNKS 4096   /* PCG z-chunks over all slabs of one solve */
 int cw_ctx_create_slab(const cw_grid *global_grid, int k_lo, int k_hi, int halo, int precision,
                        int device, cw_ctx **out);
 int cw_slab_info(cw_ctx *ctx, int *kg0, int *nz_local, int *own0, int *own1);
@@ -130,6 +135,20 @@ int cw_slab_buffers_get(cw_ctx *ctx, cw_slab_buffers *out);
  * slabs at the root's barrier (system-scope atomics over NVLink). */
 int cw_slab_attach(cw_ctx *ctx, int slab, int nslab, const cw_slab_buffers *lower,
                    const cw_slab_buffers *upper, const cw_slab_buffers *root);
+
+/* The PCG's work split: z-chunks of zc planes times 32 x 32 (x, y) tiles.
+ * Dot products are summed per chunk in a fixed tree, then over chunks in
+ * global order, so a whole grid and any z-slab split whose slab boundaries
+ * fall on chunk boundaries give the same bits.
+ * cw_pcg_chunk_of: the chunk size a whole-grid context picks for g;
+ * cw_set_pcg_chunk: force a context's chunk size (slab contexts take the
+ * whole grid's); cw_slab_chunks: this slab's first chunk in the whole
+ * solve's chunk order and the total (cross-device solves; cw_slab_group_pcg
+ * sets them itself); cw_pcg_chunks: the current split. */
+int cw_pcg_chunk_of(const cw_grid *g, int precision, int device, int *zc);
+int cw_set_pcg_chunk(cw_ctx *ctx, int zc);
+int cw_slab_chunks(cw_ctx *ctx, int chunk0, int nchunk_g);
+int cw_pcg_chunks(cw_ctx *ctx, int *zc, int *nchunk);
 
 /* All slabs on one device: the projection of every slab in one cooperative
  * launch (the same kernel code as the attached multi-device solve, blocks

@@ -20,7 +20,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("CW_LIB") or os.path.join(HERE, "libcitywind_b200.so")   # CW_LIB: developer variant builds
 
 CW_OK, CW_ERR_INVALID, CW_ERR_CUDA, CW_ERR_SINGULAR, CW_ERR_PCG = 0, 1, 2, 3, 4
-CW_ERR_NONFINITE, CW_ERR_TIMEOUT, CW_ERR_RHS, CW_ERR_GEOMETRY = 5, 6, 7, 8
+CW_ERR_NONFINITE, CW_ERR_TIMEOUT, CW_ERR_RHS, CW_ERR_GEOMETRY, CW_ERR_HALO = 5, 6, 7, 8, 9
 STAGE_ADVECT, STAGE_DIFFUSE, STAGE_DRAG, STAGE_BOUNDARY, STAGE_PROJECT, STAGE_TURBULENCE = range(1, 7)
 
 
@@ -127,6 +127,10 @@ SIGNATURES = {
     "cw_read_reports": (C.c_int, [_P, C.POINTER(cw_report), C.c_int, C.POINTER(C.c_int), _P]),
     "cw_step_defer": (C.c_int, [_P, _P, _P]),
     "cw_set_max_iter": (C.c_int, [_P, C.c_int]),
+    "cw_pcg_chunk_of": (C.c_int, [C.POINTER(cw_grid), C.c_int, C.c_int, C.POINTER(C.c_int)]),
+    "cw_set_pcg_chunk": (C.c_int, [_P, C.c_int]),
+    "cw_slab_chunks": (C.c_int, [_P, C.c_int, C.c_int]),
+    "cw_pcg_chunks": (C.c_int, [_P, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     "cw_ref_layout": (C.c_int, [_P, C.c_int, C.c_int, _P, _P, _P]),
     "cw_turb_rollback": (C.c_int, [_P, C.POINTER(cw_fields), _P]),
     "cw_set_stage_timing": (C.c_int, [_P, C.c_int]),
@@ -181,7 +185,7 @@ def check(rc: int, report=None):
         raise ProjectionError(report)
     if rc == CW_ERR_NONFINITE:
         raise FloatingPointError(msg)
-    if rc in (CW_ERR_INVALID, CW_ERR_RHS):
+    if rc in (CW_ERR_INVALID, CW_ERR_RHS, CW_ERR_HALO):
         raise ValueError(msg)
     if rc == CW_ERR_GEOMETRY:
         raise ClassificationError(msg)

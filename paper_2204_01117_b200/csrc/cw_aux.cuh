@@ -11,6 +11,7 @@ __global__ void k_report_init(DevReport* r) {
   r->iterations = 0;
   r->converged = 0;
   r->status = 0;
+  r->halo_need = 0;
   r->criterion = 0.0;
   for (int s = 0; s < 4; ++s) { r->fmax[s] = 0u; r->dmax[s] = 0ull; }
   r->bad_index[0] = 0x7fffffffffffffffLL;

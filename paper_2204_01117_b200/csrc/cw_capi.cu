@@ -57,6 +57,8 @@ struct cw_ctx {
   void *lut = nullptr, *uzx = nullptr, *uzy = nullptr;
   uint8_t* code = nullptr;
   double* part = nullptr;
+  unsigned* tags = nullptr;    // [2][part_stride] per-unit publication tags (k_pcg flag-in-data folds)
+  int chunk0 = 0, nchunk_g = 1;   // this context's first chunk / chunks of the whole z-slab solve
   unsigned* bar = nullptr;
   int* gate = nullptr;
   DevReport* rep = nullptr;
@@ -203,6 +205,45 @@ static int make_tmap(CUtensorMap* m, CUtensorMapDataType dt, size_t esz, void* b
   return CW_OK;
 }
 
+// PCG work decomposition: tiles TX x TY over (x, y), z-chunks of zc planes;
+// each co-resident block streams ceil(U/B) units of zc+2 planes: minimise
+// that critical path (halo planes included).  At most CW_PCG_MAXC chunks
+// (the in-kernel fold keeps one sum per chunk).  CW_PCG_ZC overrides.
+static int choose_zc(int tiles, int nown, int maxb) {
+  const int zmin = std::max(1, (nown + CW_PCG_MAXC - 1) / CW_PCG_MAXC);
+  int best_zc = nown, best_cost = 1 << 30;
+  for (int zc = zmin; zc <= nown; ++zc) {
+    const int U = tiles * ((nown + zc - 1) / zc);
+    const int B = std::min(U, maxb);
+    const int m = (U + B - 1) / B;
+    const int cost = m * (zc + 2);
+    if (cost < best_cost) { best_cost = cost; best_zc = zc; }
+  }
+  if (const char* ev = std::getenv("CW_PCG_ZC")) best_zc = std::max(zmin, std::min(nown, std::atoi(ev)));
+  return best_zc;
+}
+
+static void plan_units(cw_ctx* c) {
+  const int nown = c->d.o1 - c->d.o0;
+  const int nchunk = (nown + c->zc - 1) / c->zc;
+  c->U = c->ntx * c->nty * nchunk;
+  c->pcg_blocks = std::min(c->U, c->max_blocks);
+  if (const char* eb = std::getenv("CW_PCG_BLOCKS")) c->pcg_blocks = std::max(1, std::min(c->pcg_blocks, std::atoi(eb)));
+  c->chunk0 = 0;
+  c->nchunk_g = nchunk;
+}
+
+static int alloc_partials(cw_ctx* c) {
+  const int need = std::max(c->U, c->max_blocks);
+  if (c->part && c->part_stride >= need) return CW_OK;
+  if (c->part) { cudaFree(c->part); c->part = nullptr; }
+  if (c->tags) { cudaFree(c->tags); c->tags = nullptr; }
+  c->part_stride = need;
+  int rc = alloc((void**)&c->part, 6 * (size_t)need * sizeof(double));
+  rc |= alloc((void**)&c->tags, 2 * (size_t)need * sizeof(unsigned));
+  return rc;
+}
+
 // A context over the local grid g (a whole grid, or a z-slab window: global
 // planes [kg0, kg0 + g->nz) of nzg, owning local planes [own0, own1)).
 static int ctx_create(const cw_grid* g, int kg0, int nzg, int own0, int own1, int precision, int device,
@@ -270,22 +311,8 @@ static int ctx_create(const cw_grid* g, int kg0, int nzg, int own0, int own1, in
   c->ntx = (d.nx + TX - 1) / TX;
   c->nty = (d.ny + TY - 1) / TY;
   const int tiles = c->ntx * c->nty;
-  // choose the z-chunk: each block streams ceil(U/B) units of zc+2 planes;
-  // minimise that critical path (halo planes included).  CW_PCG_ZC overrides.
-  const int nown = d.o1 - d.o0;
-  int best_zc = nown, best_cost = 1 << 30;
-  for (int zc = 1; zc <= nown; ++zc) {
-    const int U = tiles * ((nown + zc - 1) / zc);
-    const int B = std::min(U, maxb);
-    const int m = (U + B - 1) / B;
-    const int cost = m * (zc + 2);
-    if (cost < best_cost) { best_cost = cost; best_zc = zc; }
-  }
-  if (const char* ev = std::getenv("CW_PCG_ZC")) best_zc = std::max(1, std::min(nown, std::atoi(ev)));
-  c->zc = best_zc;
-  c->U = tiles * ((nown + best_zc - 1) / best_zc);
-  c->pcg_blocks = std::min(c->U, maxb);
-  if (const char* eb = std::getenv("CW_PCG_BLOCKS")) c->pcg_blocks = std::max(1, std::min(c->pcg_blocks, std::atoi(eb)));
+  c->zc = choose_zc(tiles, d.o1 - d.o0, maxb);
+  plan_units(c);
   {
     const CUtensorMapDataType tdt = precision == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64;
     const size_t e = c->esz;
@@ -301,10 +328,9 @@ static int ctx_create(const cw_grid* g, int kg0, int nzg, int own0, int own1, in
     r2 |= make_tmap(&c->tm[8], CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, c->code, c, TX, TY);
     if (r2 != CW_OK) { cw_ctx_destroy(c); return CW_ERR_CUDA; }
   }
-  c->part_stride = std::max(c->U, maxb);
-  rc = alloc((void**)&c->part, 6 * (size_t)c->part_stride * sizeof(double));
+  rc = alloc_partials(c);
   rc |= alloc((void**)&c->xbar, 64 * sizeof(unsigned));
-  rc |= alloc((void**)&c->xval, 6 * (size_t)CW_MAX_SLABS * sizeof(double));
+  rc |= alloc((void**)&c->xval, 6 * (size_t)CW_MAX_CHUNKS * sizeof(double));
   rc |= alloc(&c->slab_args, (size_t)CW_MAX_SLABS * sizeof(PcgArgs<double>));
   rc |= alloc((void**)&c->reg_part, (size_t)1024 * 64 * sizeof(double));
   rc |= alloc((void**)&c->reg_cnt, (size_t)1024 * 64 * sizeof(long long));
@@ -346,7 +372,7 @@ extern "C" void cw_ctx_destroy(cw_ctx* c) {
   cudaSetDevice(c->device);
   void* ptrs[] = {c->tk, c->tw, c->speed, c->ahead[0], c->ahead[1], c->ahead[2], c->adv[0], c->adv[1],
                   c->adv[2], c->r0, c->r1, c->p0, c->p1, c->z, c->Ap, c->xw, c->lut, c->uzx, c->uzy, c->code,
-                  c->part, c->bar, c->gate, c->rep, c->reg_part, c->reg_cnt, c->reg_out, c->reg_cout,
+                  c->part, c->tags, c->bar, c->gate, c->rep, c->reg_part, c->reg_cnt, c->reg_out, c->reg_cout,
                   c->flag, c->xbar, c->xval, c->slab_args};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -613,7 +639,12 @@ static void fill_pcg_args(PcgArgs<T>& A, cw_ctx* c, const cw_fields* f, DevRepor
   A.r0 = (double*)c->r0; A.r1 = (double*)c->r1; A.p0 = (T*)c->p0; A.p1 = (T*)c->p1; A.z = (T*)c->z; A.Ap = (T*)c->Ap;
   A.x = (T*)c->xw;
   A.part = c->part;
+  A.tags = c->tags;
   A.PS = c->part_stride;
+  A.tiles = c->ntx * c->nty;
+  A.nchunk = c->U / A.tiles;
+  A.chunk0 = c->chunk0;
+  A.nchunk_g = c->nchunk_g;
   A.bar = c->bar;
   A.gate = c->gate;
   A.rep = rep;
@@ -670,6 +701,7 @@ static int launch_pcg(cw_ctx* c, const cw_fields* f, DevReport* rep, double dt, 
   fill_pcg_args<T>(A, c, f, rep, dt, tol);
   if (c->nslab > 1) set_slab_peers<T>(A, c);
   CW_CUDA(cudaMemsetAsync(c->bar, 0, 64 * sizeof(unsigned), st));
+  CW_CUDA(cudaMemsetAsync(c->tags, 0, 2 * (size_t)c->part_stride * sizeof(unsigned), st));
   void* args[] = {&A};
   const void* kfn = c->nslab > 1 ? (const void*)k_pcg<T, true> : (const void*)k_pcg<T, false>;
   CW_CUDA(cudaLaunchCooperativeKernel(kfn, dim3(c->pcg_blocks), dim3(PCG_THREADS), args, c->pcg_smem, st));
@@ -883,6 +915,11 @@ static int enqueue_stage(cw_ctx* c, const cw_fields* f, const cw_params* prm, in
     }
     case CW_STAGE_PRE: {        // step() up to the projection; k, omega stay in tk, tw until POST
       const bool turb = prm->turbulence != 0;
+      if (d.kg0 > 0 || d.kg0 + d.nz < d.nzg) {   // a z-slab window: does the step's reach fit its halo?
+        (k_wmax_window<T><<<std::min(nblk(c->nw_), 4 * c->num_sms), 256, 0, st>>>(c->nw_, P.w, rep, c->gate),
+         ++c->launches);
+        (k_halo_gate<T><<<1, 1, 0, st>>>(d, prm->dt, rep, c->gate), ++c->launches);
+      }
       st_advect<T>(c, P, prm, (T*)c->tk, (T*)c->tw, st);
       st_diffuse<T>(c, P, prm, st);
       st_drag<T>(c, P, prm, f->has_drag, st);
@@ -988,6 +1025,44 @@ extern "C" int cw_slab_buffers_get(cw_ctx* c, cw_slab_buffers* out) {
   return CW_OK;
 }
 
+extern "C" int cw_pcg_chunk_of(const cw_grid* g, int precision, int device, int* zc) {
+  if (!g || !zc || (precision != 4 && precision != 8)) return fail(CW_ERR_INVALID, "bad argument");
+  CW_CUDA(cudaSetDevice(device));
+  int per_sm = 0, sms = 0;
+  size_t smem = 0;
+  const int rc = precision == 4 ? pcg_occupancy<float>(&per_sm, &smem) : pcg_occupancy<double>(&per_sm, &smem);
+  if (rc != CW_OK) return rc;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  const int tiles = ((g->nx + TX - 1) / TX) * ((g->ny + TY - 1) / TY);
+  *zc = choose_zc(tiles, g->nz, std::max(1, per_sm * sms));
+  return CW_OK;
+}
+
+extern "C" int cw_set_pcg_chunk(cw_ctx* c, int zc) {
+  if (!c) return fail(CW_ERR_INVALID, "null argument");
+  const int nown = c->d.o1 - c->d.o0;
+  if (zc < 1 || (nown + zc - 1) / zc > CW_PCG_MAXC) return fail(CW_ERR_INVALID, "bad PCG chunk size");
+  c->zc = std::min(zc, nown);
+  plan_units(c);
+  return alloc_partials(c);
+}
+
+extern "C" int cw_slab_chunks(cw_ctx* c, int chunk0, int nchunk_g) {
+  if (!c || chunk0 < 0 || nchunk_g < 1 || nchunk_g > CW_MAX_CHUNKS ||
+      chunk0 + c->U / (c->ntx * c->nty) > nchunk_g)
+    return fail(CW_ERR_INVALID, "bad chunk range");
+  c->chunk0 = chunk0;
+  c->nchunk_g = nchunk_g;
+  return CW_OK;
+}
+
+extern "C" int cw_pcg_chunks(cw_ctx* c, int* zc, int* nchunk) {
+  if (!c) return fail(CW_ERR_INVALID, "null argument");
+  if (zc) *zc = c->zc;
+  if (nchunk) *nchunk = c->U / (c->ntx * c->nty);
+  return CW_OK;
+}
+
 extern "C" int cw_slab_attach(cw_ctx* c, int slab, int nslab, const cw_slab_buffers* lower,
                               const cw_slab_buffers* upper, const cw_slab_buffers* root) {
   if (!c || !root) return fail(CW_ERR_INVALID, "null argument");
@@ -1014,8 +1089,14 @@ static int group_pcg(cw_ctx** cs, const cw_fields* fs, int n, const cw_params* p
   for (int s = 0; s < n; ++s) umax = std::max(umax, cs[s]->U);
   const int bps = std::max(1, std::min(c0->max_blocks / n, umax));
   std::vector<PcgArgs<T>> args(n);
-  for (int s = 0; s < n; ++s) {
+  int nchunk_g = 0;
+  for (int s = 0; s < n; ++s) nchunk_g += cs[s]->U / (cs[s]->ntx * cs[s]->nty);
+  if (nchunk_g > CW_MAX_CHUNKS) return fail(CW_ERR_INVALID, "too many PCG chunks over the slabs");
+  for (int s = 0, ch = 0; s < n; ++s) {
     cw_ctx* c = cs[s];
+    c->chunk0 = ch;
+    c->nchunk_g = nchunk_g;
+    ch += c->U / (c->ntx * c->nty);
     const double tol = pcg_tol < 0 || std::isnan(pcg_tol) ? c->tol_default : pcg_tol;
     const int slot = c->head++;
     c->slot_dt[slot] = prm->dt;
@@ -1035,6 +1116,7 @@ static int group_pcg(cw_ctx** cs, const cw_fields* fs, int n, const cw_params* p
     args[s].xbar = c0->xbar;
     args[s].xval = c0->xval;
     CW_CUDA(cudaMemsetAsync(c->bar, 0, 64 * sizeof(unsigned), st));
+    CW_CUDA(cudaMemsetAsync(c->tags, 0, 2 * (size_t)c->part_stride * sizeof(unsigned), st));
   }
   CW_CUDA(cudaMemsetAsync(c0->xbar, 0, 64 * sizeof(unsigned), st));
   CW_CUDA(cudaMemcpyAsync(c0->slab_args, args.data(), n * sizeof(PcgArgs<T>), cudaMemcpyHostToDevice, st));
@@ -1184,6 +1266,7 @@ extern "C" int cw_read_reports(cw_ctx* c, cw_report* out, int n, int* n_out, voi
         break;
       case 3: o.status = CW_ERR_TIMEOUT; break;
       case 4: o.status = CW_ERR_RHS; break;
+      case 5: o.status = CW_ERR_HALO; o.bad_cell = r.halo_need; break;
       default: o.status = CW_ERR_CUDA; break;
     }
     if (o.status != CW_OK && first_err == CW_OK) first_err = o.status;
@@ -1198,6 +1281,7 @@ extern "C" int cw_read_reports(cw_ctx* c, cw_report* out, int n, int* n_out, voi
                        : first_err == CW_ERR_NONFINITE ? "turbulence update produced non-finite values"
                        : first_err == CW_ERR_RHS ? "right-hand side contains non-finite entries"
                        : first_err == CW_ERR_TIMEOUT ? "device grid barrier timed out"
+                       : first_err == CW_ERR_HALO ? "z-slab halo too shallow for the step's reach"
                                                      : "device error";
     g_err = what;
   }

@@ -70,19 +70,24 @@ __device__ __forceinline__ T gather_at(const T* __restrict__ a, int ex, int ey, 
   return c0 * oz + c1 * tz;
 }
 
+// fz is a GLOBAL z coordinate and the array's plane 0 is global plane kg0 (a
+// z-slab window; 0 for a whole grid): the floor and the weight are taken in
+// global coordinates, so a slab rounds exactly like the whole grid (a local
+// coordinate k + 0.5 - s rounds differently from kg0 + k + 0.5 - s), and the
+// index is clamped to the stored planes
 template <typename T>
 __device__ __forceinline__ T gather(const T* __restrict__ a, int ex, int ey, int ez,
-                                    T fx, T fy, T fz, T* mn, T* mx) {
+                                    T fx, T fy, T fz, T* mn, T* mx, int kg0 = 0) {
   int i0 = (int)floor(fx), j0 = (int)floor(fy), k0 = (int)floor(fz);
   const int im = ex - 2 > 0 ? ex - 2 : 0, jm = ey - 2 > 0 ? ey - 2 : 0, km = ez - 2 > 0 ? ez - 2 : 0;
   i0 = i0 < 0 ? 0 : (i0 > im ? im : i0);
   j0 = j0 < 0 ? 0 : (j0 > jm ? jm : j0);
-  k0 = k0 < 0 ? 0 : (k0 > km ? km : k0);
+  k0 = k0 < kg0 ? kg0 : (k0 > kg0 + km ? kg0 + km : k0);
   T tx = fx - (T)i0, ty = fy - (T)j0, tz = fz - (T)k0;
   tx = tx < (T)0 ? (T)0 : (tx > (T)1 ? (T)1 : tx);
   ty = ty < (T)0 ? (T)0 : (ty > (T)1 ? (T)1 : ty);
   tz = tz < (T)0 ? (T)0 : (tz > (T)1 ? (T)1 : tz);
-  return gather_at<T>(a, ex, ey, ez, i0, j0, k0, tx, ty, tz, mn, mx);
+  return gather_at<T>(a, ex, ey, ez, i0, j0, k0 - kg0, tx, ty, tz, mn, mx);
 }
 
 

@@ -87,7 +87,10 @@ struct PcgArgs {
   const T* u; const T* v; const T* w;
   double* r0; double* r1;    // pitched, float64
   T* p0; T* p1; T* z; T* Ap; T* x;   // pitched
-  double* part;              // [2][3][U] partials (two alternating sets)
+  double* part;              // [2][3][PS] per-unit partials (two alternating sets)
+  unsigned* tags;            // [2][PS] phase number of each unit's published partials (flag in data)
+  int tiles, nchunk;         // (x, y) tiles per plane; z-chunks of this launch (U = tiles * nchunk)
+  int chunk0, nchunk_g;      // global index of this slab's first chunk; chunks of the whole grid
   unsigned int* bar;         // [0] arrival count, [32] generation
   int* gate;
   DevReport* rep;
@@ -105,7 +108,7 @@ struct PcgArgs {
   int nslab, slab;
   PcgPeer<T> lo, hi;
   unsigned int* xbar;        // root slab: [0] arrivals, [32] generation (system scope)
-  double* xval;              // root slab: [2 sets][3 values][nslab]
+  double* xval;              // root slab: [2 sets][3 values][nchunk_g] chunk sums
   long long timeout_ns;
   int probe_mode, probe_iters;   // developer timing probe (CW_PCG_PROBE), 0 = off
 };
@@ -282,6 +285,106 @@ __device__ __forceinline__ void fold_multi(const double* part, int n, int stride
 }
 
 // ---------------------------------------------------------------------------
+// Per-unit reductions.  Each unit (tile x z-chunk) publishes its partials and
+// then, with release semantics, the phase number in its tag (fold_chunks can
+// acquire the tags instead of a grid barrier; measured slower at C3: 65K
+// acquiring polls per phase against one counter, so phase_end keeps the
+// barrier).  The fold is the same fixed tree wherever a chunk is folded -- one warp per
+// chunk, lane l summing tiles l, l+32, ... in order, a shuffle tree, lane 0's
+// result -- and the chunk sums are added in global chunk order.  So a whole
+// grid and any split into z-slabs whose boundaries fall on chunk boundaries
+// produce the same bits (slab_reduce publishes chunk sums, not slab sums).
+__device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+#ifndef CW_PCG_TAGS
+#define CW_PCG_TAGS 0   // 1: publish per-unit tags (for fold_chunks(wait=true)); a release store per unit and phase
+#endif
+template <typename T>
+__device__ __forceinline__ void publish_unit(const PcgArgs<T>& A, double* part, int set, int unit, int nval,
+                                             const double* v, unsigned seq) {
+  for (int q = 0; q < nval; ++q) part[(size_t)q * A.PS + unit] = v[q];
+  if (CW_PCG_TAGS) st_release_u32(A.tags + (size_t)set * A.PS + unit, seq);
+}
+
+template <typename T>
+__device__ __forceinline__ bool wait_tag(const PcgArgs<T>& A, const unsigned* tag, unsigned seq) {
+  if ((int)(ld_acquire(tag) - seq) >= 0) return true;
+  const unsigned long long t0 = globaltimer();
+  unsigned spins = 0;
+  while ((int)(ld_acquire(tag) - seq) < 0) {
+    __nanosleep(32);
+    if ((++spins & 1023u) == 0 && (long long)(globaltimer() - t0) > A.timeout_ns) {
+      A.rep->status = 3;
+      *A.gate = 3;
+      return false;
+    }
+  }
+  return true;
+}
+
+// chunk sums of this launch's units into S.chunk (wait: acquire every tag
+// first); returns after a __syncthreads
+template <typename T, typename Sh>
+__device__ __forceinline__ void fold_chunks(const PcgArgs<T>& A, const double* part, int set, unsigned seq, int nval,
+                                            unsigned maxmask, bool wait, Sh& S) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (int)(blockDim.x >> 5);
+  const unsigned* tags = A.tags + (size_t)set * A.PS;
+  for (int c = wid; c < A.nchunk; c += nw) {
+    double a[3] = {0.0, 0.0, 0.0};
+    for (int i0 = lane; i0 < A.tiles; i0 += 32 * 4) {   // four tiles' loads in flight per lane
+      double v[4][3];
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+        const int i = i0 + 32 * m;
+        const int u = c * A.tiles + i;
+        if (wait && i < A.tiles) wait_tag<T>(A, tags + u, seq);
+#pragma unroll
+        for (int q = 0; q < 3; ++q) v[m][q] = (q < nval && i < A.tiles) ? __ldcg(part + (size_t)q * A.PS + u) : 0.0;
+      }
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+        if (i0 + 32 * m < A.tiles) {
+#pragma unroll
+          for (int q = 0; q < 3; ++q)
+            if (q < nval)
+              a[q] = ((maxmask >> q) & 1u) ? ((v[m][q] > a[q] || v[m][q] != v[m][q]) ? v[m][q] : a[q])
+                                           : a[q] + v[m][q];
+        }
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      if (q < nval) {
+        const bool mx = (maxmask >> q) & 1u;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const double b = __shfl_xor_sync(0xffffffffu, a[q], o);
+          a[q] = mx ? ((b > a[q] || b != b) ? b : a[q]) : a[q] + b;
+        }
+        if (lane == 0) S.chunk[q][c] = a[q];
+      }
+    }
+  }
+  __syncthreads();
+}
+
+// the chunk sums (n of them, in chunk order) to totals; every thread the same bits
+__device__ __forceinline__ void sum_chunks(const double* ch, int stride, int n, int nval, unsigned maxmask,
+                                           double* out) {
+  for (int q = 0; q < nval; ++q) {
+    const bool mx = (maxmask >> q) & 1u;
+    double a = ch[(size_t)q * stride];
+    for (int c = 1; c < n; ++c) {
+      const double b = ch[(size_t)q * stride + c];
+      a = mx ? ((b > a || b != b) ? b : a) : a + b;
+    }
+    out[q] = a;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // shared memory layout
 
 __host__ __device__ constexpr int align128(int b) { return (b + 127) & ~127; }
@@ -318,6 +421,9 @@ struct PcgWork {
   alignas(16) T yb[2][YH][PCG_YP];   // y on the y tile, planes kk and kk-1
 };
 
+#ifndef CW_PCG_MAXC
+#define CW_PCG_MAXC 64   // z-chunks per launch (the context picks zc >= planes / 64)
+#endif
 template <typename T>
 struct PcgShared {
   T lut[64 * 4];
@@ -329,6 +435,7 @@ struct PcgShared {
   double bc[4];
   double vals[4];           // slab_reduce results
   double fold[3 * 32];      // fold_multi warp results
+  double chunk[3][CW_PCG_MAXC];   // fold_units: per-chunk sums (fixed tree), summed in chunk order
   unsigned last, gen0;      // slab_reduce: this block arrived last; generation seen
   unsigned long long pt[3]; // timing probe (modes 13-16): phase start, first stage landed, jobs done
   alignas(8) uint64_t full[8];
@@ -567,7 +674,7 @@ __device__ __forceinline__ void ring_fill(const PcgArgs<T>& A, JobCursor& prod, 
 // halo tile of x0 goes to a shared double buffer (own quads plus the 132-cell
 // ring), the z neighbours are the own quads of planes k-1, k+1 in registers.
 template <typename T, bool SLABS>
-__device__ void phase0(const PcgArgs<T>& A, double* part, int unit, PcgShared<T>& S) {
+__device__ void phase0(const PcgArgs<T>& A, double* part, int set, unsigned seq, int unit, PcgShared<T>& S) {
   const Dims& d = A.d;
   const Unit t = unit_of<T>(A, unit);
   const int tx = threadIdx.x % QX, ty = threadIdx.x / QX;
@@ -661,9 +768,8 @@ __device__ void phase0(const PcgArgs<T>& A, double* part, int unit, PcgShared<T>
   __syncthreads();
   const double m2 = block_max(dmax, S.red);
   if (threadIdx.x == 0) {
-    part[unit] = s0;
-    part[A.PS + unit] = m1;
-    part[2 * A.PS + unit] = m2;
+    const double v[3] = {s0, m1, m2};
+    publish_unit<T>(A, part, set, unit, 3, v, seq);
   }
   __syncthreads();
 }
@@ -673,8 +779,8 @@ __device__ void phase0(const PcgArgs<T>& A, double* part, int unit, PcgShared<T>
 // UPDX: x += alpha_prev p (every iteration but the first); STREAM: timing
 // probe that only streams the stages (CW_PCG_PROBE modes 4, 7)
 template <typename T, bool SLABS, bool UPDX, bool STREAM>
-__device__ void phaseA(const PcgArgs<T>& A, const Blk& blk, double* part, PcgShared<T>& S, uint8_t* ring,
-                       unsigned& ticket, bool first, T beta, T alpha_prev, int pin_sel) {
+__device__ void phaseA(const PcgArgs<T>& A, const Blk& blk, double* part, int set, unsigned seq, PcgShared<T>& S,
+                       uint8_t* ring, unsigned& ticket, bool first, T beta, T alpha_prev, int pin_sel) {
   constexpr bool upd_x = UPDX;
   using L = StageLayout<T>;
   using H = Halo<T>;
@@ -787,6 +893,11 @@ __device__ void phaseA(const PcgArgs<T>& A, const Blk& blk, double* part, PcgSha
           pend = true;
         }
       }
+      if (kk == u.k1) {   // the unit's last plane: its p'.Ap is complete
+        const double sum = block_sum(acc, S.red);
+        if (threadIdx.x == 0) publish_unit<T>(A, part, set, cons.unit, 1, &sum, seq);
+        acc = 0.0;
+      }
       const bool live = cursor_next<T>(A, cons);
       ++j;
       return live;
@@ -803,8 +914,6 @@ __device__ void phaseA(const PcgArgs<T>& A, const Blk& blk, double* part, PcgSha
     if (timing && threadIdx.x == 0) S.pt[2] = globaltimer();
     ticket = t0 + j;
   }
-  const double sum = block_sum(acc, S.red);
-  if (threadIdx.x == 0) part[blk.id] = sum;
 }
 
 // ---- phase B: r' = r - alpha Ap, z = W r' ----------------------------------
@@ -823,8 +932,8 @@ struct PlaneB {           // one plane's own-quad values carried to the next pla
 // Partials: r'.z and a flag for |r'| > res_target anywhere (NaN included),
 // the max-norm half of pcg_solve's stopping rule (linalg.py:332-337).
 template <typename T, bool SLABS, bool USE_AP, bool STREAM>
-__device__ void phaseB(const PcgArgs<T>& A, const Blk& blk, double* part, PcgShared<T>& S, uint8_t* ring,
-                       unsigned& ticket, double alpha, double res_target, int rin_sel) {
+__device__ void phaseB(const PcgArgs<T>& A, const Blk& blk, double* part, int set, unsigned seq, PcgShared<T>& S,
+                       uint8_t* ring, unsigned& ticket, double alpha, double res_target, int rin_sel) {
   constexpr bool use_ap = USE_AP, write_r = USE_AP;
   using L = StageLayout<T>;
   using H = Halo<T>;
@@ -999,6 +1108,17 @@ __device__ void phaseB(const PcgArgs<T>& A, const Blk& blk, double* part, PcgSha
           }
         }
       }
+      if (kk == u.k1) {   // the unit's last plane: r'.z and the max-norm flag are complete
+        const double sm = block_sum(acc, S.red);
+        __syncthreads();
+        const double mx = __syncthreads_or(exceed) ? 1.0 : 0.0;
+        if (threadIdx.x == 0) {
+          const double v[2] = {sm, mx};
+          publish_unit<T>(A, part, set, cons.unit, 2, v, seq);
+        }
+        acc = 0.0;
+        exceed = false;
+      }
       const bool live = cursor_next<T>(A, cons);
       ++j;
       return live;
@@ -1007,13 +1127,6 @@ __device__ void phaseB(const PcgArgs<T>& A, const Blk& blk, double* part, PcgSha
     }
     if (timing && threadIdx.x == 0) S.pt[2] = globaltimer();
     ticket = t0 + j;
-  }
-  const double sm = block_sum(acc, S.red);
-  __syncthreads();
-  const double mx = __syncthreads_or(exceed) ? 1.0 : 0.0;
-  if (threadIdx.x == 0) {
-    part[blk.id] = sm;
-    part[A.PS + blk.id] = mx;
   }
   __syncthreads();
 }
@@ -1058,8 +1171,8 @@ __device__ __forceinline__ unsigned ld_acquire_sys(const unsigned* p) {
 }
 
 template <typename T>
-__device__ void slab_reduce(const PcgArgs<T>& A, const Blk& blk, const double* part, int n, int stride, int nval,
-                            unsigned maxmask, int set, double* out, PcgShared<T>& S) {
+__device__ void slab_reduce(const PcgArgs<T>& A, const Blk& blk, const double* part, int pset, unsigned seq, int nval,
+                            unsigned maxmask, double* out, PcgShared<T>& S) {
   __syncthreads();
   unsigned* count = A.bar;
   unsigned* gen = A.bar + 32;
@@ -1067,13 +1180,18 @@ __device__ void slab_reduce(const PcgArgs<T>& A, const Blk& blk, const double* p
     S.gen0 = ld_acquire(gen);
     __threadfence_system();   // this block's writes (and its pushes into peer slabs) before the arrival
     S.last = atomicAdd(count, 1u) == (unsigned)blk.n - 1;
+    if (S.last) __threadfence();
   }
   __syncthreads();
   if (S.last) {
-    for (int q = 0; q < nval; ++q) {
-      const double v = fold_partials(part + (size_t)q * stride, n, (maxmask >> q) & 1u, S.bc);
-      if (threadIdx.x == 0) A.xval[((size_t)set * 3 + q) * A.nslab + A.slab] = v;
+    // this slab's chunk sums (the same tree as the whole grid's), published
+    // at their global chunk index in the root's table
+    fold_chunks<T>(A, part, pset, seq, nval, maxmask, false, S);
+    for (int e = threadIdx.x; e < nval * A.nchunk; e += blockDim.x) {
+      const int q = e / A.nchunk, c = e - q * A.nchunk;
+      A.xval[((size_t)pset * 3 + q) * A.nchunk_g + A.chunk0 + c] = S.chunk[q][c];
     }
+    __syncthreads();
     if (threadIdx.x == 0) {
       unsigned* xc = A.xbar;
       unsigned* xg = A.xbar + 32;
@@ -1116,14 +1234,14 @@ __device__ void slab_reduce(const PcgArgs<T>& A, const Blk& blk, const double* p
     fence_proxy_async();   // the next phase's TMA reads see the pushed halo planes
   }
   __syncthreads();
-  if (threadIdx.x < nval) {
+  if (threadIdx.x < nval) {   // all global chunks in chunk order (volatile: peers write the table)
     const int q = threadIdx.x;
-    const volatile double* xv = A.xval + ((size_t)set * 3 + q) * A.nslab;
+    const bool mx = (maxmask >> q) & 1u;
+    const volatile double* xv = A.xval + ((size_t)pset * 3 + q) * A.nchunk_g;
     double v = xv[0];
-    for (int s2 = 1; s2 < A.nslab; ++s2) {
-      const double w = xv[s2];
-      if ((maxmask >> q) & 1u) v = (w > v || w != w) ? w : v;
-      else v += w;
+    for (int c = 1; c < A.nchunk_g; ++c) {
+      const double w = xv[c];
+      v = mx ? ((w > v || w != w) ? w : v) : v + w;
     }
     S.vals[q] = v;
   }
@@ -1132,18 +1250,24 @@ __device__ void slab_reduce(const PcgArgs<T>& A, const Blk& blk, const double* p
   __syncthreads();
 }
 
-// Phase end: barrier, then the reduced values out[0..nval) (thread-local; bit q
-// of maxmask: max instead of sum) over partials part[q*stride + 0..n).
+// Phase end: the reduced values out[0..nval) (thread-local; bit q of maxmask:
+// max instead of sum) over the units' partials of set pset, published with
+// tag seq.  One launch: wait for every unit's tag (no separate grid barrier)
+// and fold; z-slabs: slab_reduce.
 template <typename T, bool SLABS>
-__device__ __forceinline__ void phase_end(const PcgArgs<T>& A, const Blk& blk, const double* part, int n, int stride,
-                                          int nval, unsigned maxmask, int set, double* out, PcgShared<T>& S,
+__device__ __forceinline__ void phase_end(const PcgArgs<T>& A, const Blk& blk, const double* part, int pset,
+                                          unsigned seq, int nval, unsigned maxmask, double* out, PcgShared<T>& S,
                                           unsigned& epoch) {
   if (SLABS && A.nslab > 1) {
-    slab_reduce<T>(A, blk, part, n, stride, nval, maxmask, set, out, S);
+    slab_reduce<T>(A, blk, part, pset, seq, nval, maxmask, out, S);
     return;
   }
+  // a grid barrier (one arrival counter: measured faster than every block
+  // acquiring every unit's tag), then the chunk-structured fold
   grid_barrier(A.bar, A.gate, A.rep, A.timeout_ns, (unsigned)blk.n, epoch);
-  fold_multi(part, n, stride, nval, maxmask, out, S.fold);
+  fold_chunks<T>(A, part, pset, seq, nval, maxmask, false, S);
+  sum_chunks(&S.chunk[0][0], CW_PCG_MAXC, A.nchunk, nval, maxmask, out);
+  __syncthreads();
 }
 
 template <typename T, bool SLABS>
@@ -1172,15 +1296,17 @@ __device__ __forceinline__ void pcg_body(const PcgArgs<T>& A, const Blk& blk, ui
   const bool lead = blk.id == 0 && threadIdx.x == 0;
   unsigned ticket = 0;
   unsigned epoch = 0;    // grid barriers passed (every thread keeps the count)
-  // two partial sets, alternated by phase, so one barrier per phase suffices;
-  // phase 0 writes per unit, the ring phases per block (fixed unit->block map)
+  unsigned seq = 0;      // phases started: the tag the units publish (tags zeroed before the launch)
+  // two partial sets, alternated by phase: a unit's slot is rewritten only
+  // after every block has folded it
   double* P[2] = {A.part, A.part + 3 * A.PS};
   double red[3];
 
   if ((A.probe_mode == 8 || (A.probe_mode >= 13 && A.probe_mode <= 15)) && lead) rep->criterion = 0.0;
   if (A.probe_mode == 16 && lead) rep->criterion = 1e30;
-  for (int u = blk.id; u < U; u += B) phase0<T, SLABS>(A, P[0], u, S);
-  phase_end<T, SLABS>(A, blk, P[0], U, A.PS, 3, 6u, 0, red, S, epoch);
+  ++seq;
+  for (int u = blk.id; u < U; u += B) phase0<T, SLABS>(A, P[0], 0, seq, u, S);
+  phase_end<T, SLABS>(A, blk, P[0], 0, seq, 3, 6u, red, S, epoch);
   const double b2 = red[0], bmax = red[1], divmax = red[2];
   if (lead) report_max<T>(rep, SLOT_DIV_BEFORE, (T)divmax);
   if (*(volatile int*)A.gate == 3) {
@@ -1200,8 +1326,9 @@ __device__ __forceinline__ void pcg_body(const PcgArgs<T>& A, const Blk& blk, ui
   const double tol = A.tol;
 
   // z = W r0, rz, max|r0|  (pcg_solve:342-345)
-  phaseB<T, SLABS, false, false>(A, blk, P[1], S, ring, ticket, 0.0, res_target, 0);
-  phase_end<T, SLABS>(A, blk, P[1], B, A.PS, 2, 2u, 1, red, S, epoch);
+  ++seq;
+  phaseB<T, SLABS, false, false>(A, blk, P[1], 1, seq, S, ring, ticket, 0.0, res_target, 0);
+  phase_end<T, SLABS>(A, blk, P[1], 1, seq, 2, 2u, red, S, epoch);
   double rz = red[0];
   double rmax = red[1];
   double crit = rz / b2;
@@ -1216,10 +1343,10 @@ __device__ __forceinline__ void pcg_body(const PcgArgs<T>& A, const Blk& blk, ui
       const bool pa = A.probe_mode == 1 || A.probe_mode == 4 || (A.probe_mode >= 6 && !(q & 1));
       const bool pb = A.probe_mode == 2 || (A.probe_mode >= 6 && (q & 1));
       const bool stream = A.probe_mode == 4 || A.probe_mode == 7;
-      if (pa && stream) phaseA<T, SLABS, true, true>(A, blk, P[0], S, ring, ticket, false, (T)0.5, (T)0.0, (q >> 1) & 1);
-      if (pa && !stream) phaseA<T, SLABS, true, false>(A, blk, P[0], S, ring, ticket, false, (T)0.5, (T)0.0, (q >> 1) & 1);
-      if (pb && A.probe_mode == 7) phaseB<T, SLABS, true, true>(A, blk, P[1], S, ring, ticket, 0.0, res_target, (q >> 1) & 1);
-      if (pb && A.probe_mode != 7) phaseB<T, SLABS, true, false>(A, blk, P[1], S, ring, ticket, 0.0, res_target, (q >> 1) & 1);
+      if (pa && stream) phaseA<T, SLABS, true, true>(A, blk, P[0], 0, 0u, S, ring, ticket, false, (T)0.5, (T)0.0, (q >> 1) & 1);
+      if (pa && !stream) phaseA<T, SLABS, true, false>(A, blk, P[0], 0, 0u, S, ring, ticket, false, (T)0.5, (T)0.0, (q >> 1) & 1);
+      if (pb && A.probe_mode == 7) phaseB<T, SLABS, true, true>(A, blk, P[1], 1, 0u, S, ring, ticket, 0.0, res_target, (q >> 1) & 1);
+      if (pb && A.probe_mode != 7) phaseB<T, SLABS, true, false>(A, blk, P[1], 1, 0u, S, ring, ticket, 0.0, res_target, (q >> 1) & 1);
       if (A.probe_mode >= 13 && threadIdx.x == 0)
         wait_ns += A.probe_mode == 13 ? S.pt[1] - S.pt[0] : S.pt[2] - S.pt[0];
       const unsigned long long ta = globaltimer();
@@ -1252,16 +1379,18 @@ __device__ __forceinline__ void pcg_body(const PcgArgs<T>& A, const Blk& blk, ui
     if (it >= A.max_iter) break;
     ++it;
     const bool first = it == 1;
-    if (first) phaseA<T, SLABS, false, false>(A, blk, P[0], S, ring, ticket, true, (T)0, (T)0, psel);
-    else phaseA<T, SLABS, true, false>(A, blk, P[0], S, ring, ticket, false, (T)beta, (T)alpha, psel);
-    phase_end<T, SLABS>(A, blk, P[0], B, A.PS, 1, 0u, 0, red, S, epoch);
+    ++seq;
+    if (first) phaseA<T, SLABS, false, false>(A, blk, P[0], 0, seq, S, ring, ticket, true, (T)0, (T)0, psel);
+    else phaseA<T, SLABS, true, false>(A, blk, P[0], 0, seq, S, ring, ticket, false, (T)beta, (T)alpha, psel);
+    phase_end<T, SLABS>(A, blk, P[0], 0, seq, 1, 0u, red, S, epoch);
     const double pAp = red[0];
     psel ^= 1;                                // the new p went to the other buffer
     if (*(volatile int*)A.gate == 3) { status = 3; alpha = 0.0; break; }
     if (pAp <= 0.0) { it -= 1; alpha = 0.0; break; }   // linalg.py:354-355
     alpha = rz / pAp;
-    phaseB<T, SLABS, true, false>(A, blk, P[1], S, ring, ticket, alpha, res_target, rsel);
-    phase_end<T, SLABS>(A, blk, P[1], B, A.PS, 2, 2u, 1, red, S, epoch);
+    ++seq;
+    phaseB<T, SLABS, true, false>(A, blk, P[1], 1, seq, S, ring, ticket, alpha, res_target, rsel);
+    phase_end<T, SLABS>(A, blk, P[1], 1, seq, 2, 2u, red, S, epoch);
     const double rz_new = red[0];
     rmax = red[1];
     rsel ^= 1;

@@ -17,15 +17,16 @@ struct StepConsts {
 struct DevReport {
   int iterations;
   int converged;
-  int status;            // 0 ok, 1 pcg not converged, 2 non-finite turbulence, 3 barrier timeout, 4 non-finite rhs
-  int pad;
+  int status;            // 0 ok, 1 pcg not converged, 2 non-finite turbulence, 3 barrier timeout, 4 non-finite rhs,
+                         // 5 z-slab halo too shallow for this step's reach
+  int halo_need;         // status 5: planes the window needs per interior face (criterion = max|w| dt/dz)
   double criterion;
   unsigned int fmax[4];  // float max slots: 0 div_before, 1 div_after, 2 max|vel| (bit patterns)
   unsigned long long dmax[4];
   long long bad_index[2];  // first non-finite k / omega cell, reference C order (i*ny+j)*nz+k
 };
 
-enum MaxSlot { SLOT_DIV_BEFORE = 0, SLOT_DIV_AFTER = 1, SLOT_SPEED = 2 };
+enum MaxSlot { SLOT_DIV_BEFORE = 0, SLOT_DIV_AFTER = 1, SLOT_SPEED = 2, SLOT_WMAX = 3 };
 
 template <typename T> __device__ __forceinline__ void report_max(DevReport* r, int slot, T v);
 template <> __device__ __forceinline__ void report_max<float>(DevReport* r, int slot, float v) {
@@ -227,9 +228,9 @@ __device__ __forceinline__ void mac_predict_face_v(const Dims& d, int comp, cons
   comp_offset(comp, fox, foy, foz);
   const T ox = (T)fox, oy = (T)foy, oz = (T)foz;
   const int c = ((int)k * ey + j) * ex + i;
-  const T X = (T)i + ox, Y = (T)j + oy, Z = (T)k + oz;
+  const T X = (T)i + ox, Y = (T)j + oy, Z = (T)(k + d.kg0) + oz;   // global z (z-slab windows)
   const T bx = X - dt * us * inv_h<T>(d, 0), by = Y - dt * vs * inv_h<T>(d, 1), bz = Z - dt * ws * inv_h<T>(d, 2);
-  ahead[c] = gather<T>(arr, ex, ey, ez, bx - ox, by - oy, bz - oz, nullptr, nullptr);
+  ahead[c] = gather<T>(arr, ex, ey, ez, bx - ox, by - oy, bz - oz, nullptr, nullptr, d.kg0);
 }
 
 // One thread per (i, j, k) of the union of the face extents handles the u, v
@@ -291,13 +292,13 @@ __device__ __forceinline__ void mac_correct_face_v(const Dims& d, int comp, cons
   comp_offset(comp, fox, foy, foz);
   const T ox = (T)fox, oy = (T)foy, oz = (T)foz;
   const int c = ((int)k * ey + j) * ex + i;
-  const T X = (T)i + ox, Y = (T)j + oy, Z = (T)k + oz;
+  const T X = (T)i + ox, Y = (T)j + oy, Z = (T)(k + d.kg0) + oz;   // global z (z-slab windows)
   T mn, mx;
   const T sx = dt * us * inv_h<T>(d, 0), sy = dt * vs * inv_h<T>(d, 1), sz = dt * ws * inv_h<T>(d, 2);
   const T bx = X - sx, by = Y - sy, bz = Z - sz;
-  (void)gather<T>(arr, ex, ey, ez, bx - ox, by - oy, bz - oz, &mn, &mx);
+  (void)gather<T>(arr, ex, ey, ez, bx - ox, by - oy, bz - oz, &mn, &mx, d.kg0);
   const T fx = X + sx, fy = Y + sy, fz = Z + sz;
-  const T back = gather<T>(ahead, ex, ey, ez, fx - ox, fy - oy, fz - oz, nullptr, nullptr);
+  const T back = gather<T>(ahead, ex, ey, ez, fx - ox, fy - oy, fz - oz, nullptr, nullptr, d.kg0);
   T cor = ahead[c] + (T)0.5 * (self - back);   // self = arr[c]
   cor = cor < mn ? mn : cor;
   cor = cor > mx ? mx : cor;
@@ -946,6 +947,47 @@ __global__ void k_turb_rollback(long long n, const T* __restrict__ k_adv, const 
     k[c] = k_adv[c];
     w[c] = w_adv[c];
     nut[c] = nut_prev[c];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// z-slab reach check (SURVEY 7 hard part 4).  A window stores `halo` planes
+// beyond its owned planes on each interior face; the step's stages read
+// across planes, so the owned planes come out as in the whole-grid step only
+// if the chain's reach fits.  The MacCormack backtrace and forward trace each
+// reach floor(S) + 1 planes (S = max|w| dt / dz, unbounded: the scheme is
+// unconditionally stable), diffusion and the drag's cell speeds one more
+// each: 2 floor(S) + 4 planes (S < 1: 4, the z-slab tests' measured minimum
+// for bitwise equality).  max|w| over the window before the step; too
+// shallow a halo fails the step loudly instead of corrupting the owned planes.
+template <typename T>
+__global__ void k_wmax_window(long long n, const T* __restrict__ w, DevReport* rep, const int* gate) {
+  if (*gate) return;
+  __shared__ T scratch[32];
+  T m = (T)0;
+  CW_GRID_STRIDE(c, n) {
+    const T a = fabs(w[c]);
+    m = (a > m || a != a) ? a : m;
+  }
+  m = block_max(m, scratch);
+  if (threadIdx.x == 0) report_max<T>(rep, SLOT_WMAX, m);
+}
+
+template <typename T>
+__global__ void k_halo_gate(Dims d, double dt, DevReport* rep, int* gate) {
+  if (*gate) return;
+  double wmax;
+  if (sizeof(T) == 4) wmax = (double)__uint_as_float(rep->fmax[SLOT_WMAX]);
+  else wmax = __longlong_as_double((long long)rep->dmax[SLOT_WMAX]);
+  const double S = wmax * dt / d.ddz;
+  const int need = S != S ? 1 << 30 : 2 * (int)floor(fmin(S, 1e6)) + 4;
+  const int lo = d.kg0 > 0 ? d.o0 : (1 << 30);                      // interior faces only: at the
+  const int hi = d.kg0 + d.nz < d.nzg ? d.nz - d.o1 : (1 << 30);    // grid's ends the clamp is the grid's
+  if (need > (lo < hi ? lo : hi)) {
+    rep->status = 5;
+    rep->halo_need = need;
+    rep->criterion = S;
+    *gate = 5;
   }
 }
 

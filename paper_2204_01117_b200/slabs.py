@@ -48,10 +48,23 @@ DEFAULT_HALO = 4
 _DT = {torch.float32: 4, torch.float64: 8}
 
 
-def plan_slabs(nz: int, n: int) -> list:
-    """Balanced contiguous plane ranges [(k_lo, k_hi), ...] in z order."""
+def plan_slabs(nz: int, n: int, align: int = 1) -> list:
+    """Balanced contiguous plane ranges [(k_lo, k_hi), ...] in z order.  With
+    ``align`` > 1 the inner boundaries fall on multiples of ``align`` when
+    the planes allow it (the PCG's chunk size: the slab split then sums the
+    dot products exactly as the whole grid does, bit for bit)."""
     if not 1 <= n <= nz:
         raise ValueError(f"cannot split {nz} planes into {n} slabs")
+    nblk = -(-nz // align) if align > 1 else nz
+    if align > 1 and nblk >= n:
+        base, extra = divmod(nblk, n)
+        out, k = [], 0
+        for r in range(n):
+            t = (base + (1 if r < extra else 0)) * align
+            out.append((k, min(k + t, nz)))
+            k = min(k + t, nz)
+        if all(b > a for a, b in out):
+            return out
     base, extra = divmod(nz, n)
     out, k = [], 0
     for r in range(n):
@@ -59,6 +72,23 @@ def plan_slabs(nz: int, n: int) -> list:
         out.append((k, k + t))
         k += t
     return out
+
+
+def whole_grid_chunk(grid: GridSpec, dtype, device) -> int:
+    """The z-chunk a whole-grid context's PCG uses (``cw_pcg_chunk_of``)."""
+    g = N.cw_grid(grid.nx, grid.ny, grid.nz, float(grid.dx), float(grid.dy), float(grid.dz), N.dbl3(grid.origin))
+    zc = C.c_int()
+    N.check(N.lib().cw_pcg_chunk_of(C.byref(g), _DT[dtype], torch.device(device).index or 0, C.byref(zc)))
+    return int(zc.value)
+
+
+def whole_grid_tol(state: FlowState, omega: float, precond: int) -> float:
+    """default_projection_tol of the whole grid (solver.py:235-243), computed
+    exactly as the single-context step computes it."""
+    from .runtime import Context
+    ctx = Context(state.grid, state.dtype, state.device)
+    ctx.set_operator(state.labels_dev, omega, precond)
+    return ctx.tol_default
 
 
 @dataclass(frozen=True)
@@ -215,6 +245,12 @@ class SlabPart:
         self.g = window_of(g, self.win, "p").contiguous()
         self.has_drag = has
 
+    def set_chunk(self, zc: int):
+        N.check(self._lib.cw_set_pcg_chunk(self.h, int(zc)))
+        z, nch = C.c_int(), C.c_int()
+        N.check(self._lib.cw_pcg_chunks(self.h, C.byref(z), C.byref(nch)))
+        return int(nch.value)
+
     def set_operator(self, omega: float, precond: int = 2):
         n, tol = C.c_longlong(), C.c_double()
         N.check(self._lib.cw_set_operator(self.h, N.ptr(self.labels), float(omega), C.byref(n), C.byref(tol),
@@ -275,13 +311,17 @@ class SlabDomain:
         self.grid = grid
         self.params = params
         self.profile = profile
-        ranges = plan_slabs(grid.nz, nslab)
+        self.zc = whole_grid_chunk(grid, state.dtype, state.device)
+        ranges = plan_slabs(grid.nz, nslab, self.zc)
         if min(b - a for a, b in ranges) < halo:
             raise ValueError(f"slabs of {min(b - a for a, b in ranges)} planes cannot feed a {halo}-plane halo")
         self.windows = [SlabWindow.of(a, b, halo, grid.nz) for a, b in ranges]
+        self.halo = halo
         self.parts = [SlabPart(grid, w, halo, state.dtype, state.device) for w in self.windows]
         for p in self.parts:
             p.load(state, params)
+            if p.win.k_lo % self.zc == 0:
+                p.set_chunk(self.zc)      # the whole grid's chunks: bitwise the whole grid's dot products
         sums = [p.set_operator(omega, precond) for p in self.parts]
         n = sum(s[2] for s in sums)
         if n == 0:
@@ -289,8 +329,7 @@ class SlabDomain:
         if not any(s[3] for s in sums):
             from .errors import SingularSystemError
             raise SingularSystemError("no outlet cells: pressure defined only up to a constant")
-        mean = (sum(s[0] for s in sums) if precond == 2 else sum(s[1] for s in sums)) / n
-        self.tol = float(pcg_tol) if pcg_tol is not None else (1e-8 if precond == 0 else 1e-8 * max(mean, 1e-300))
+        self.tol = float(pcg_tol) if pcg_tol is not None else whole_grid_tol(state, omega, precond)
         self.exchange = LocalExchange(self.windows)
         self.time = state.time
         self.step_count = state.step_count
@@ -349,13 +388,21 @@ class DistSlabSolver:
         self.grid = grid
         self.params = params
         self.profile = profile
-        ranges = plan_slabs(grid.nz, self.n)
+        self.zc = whole_grid_chunk(grid, state.dtype, state.device)
+        ranges = plan_slabs(grid.nz, self.n, self.zc)
         if min(b - a for a, b in ranges) < halo:
             raise ValueError(f"slabs of {min(b - a for a, b in ranges)} planes cannot feed a {halo}-plane halo")
         self.windows = [SlabWindow.of(a, b, halo, grid.nz) for a, b in ranges]
+        self.halo = halo
         self.part = SlabPart(grid, self.windows[self.rank], halo, state.dtype, state.device)
         self.part.load(state, params)
+        aligned = all(a % self.zc == 0 for a, _ in ranges)
+        nch = self.part.set_chunk(self.zc) if aligned else None
         s, js, m, outl = self.part.set_operator(omega, precond)
+        if nch is None:
+            z, c = C.c_int(), C.c_int()
+            N.check(N.lib().cw_pcg_chunks(self.part.h, C.byref(z), C.byref(c)))
+            nch = int(c.value)
         t = torch.tensor([s, js, float(m), float(outl)], dtype=torch.float64, device=state.device)
         dist.all_reduce(t, group=group)
         if t[2].item() == 0:
@@ -363,8 +410,11 @@ class DistSlabSolver:
         if t[3].item() == 0:
             from .errors import SingularSystemError
             raise SingularSystemError("no outlet cells: pressure defined only up to a constant")
-        mean = (t[0] if precond == 2 else t[1]).item() / t[2].item()
-        self.tol = float(pcg_tol) if pcg_tol is not None else (1e-8 if precond == 0 else 1e-8 * max(mean, 1e-300))
+        # this slab's place in the solve's chunk order (dot products folded per chunk, in order)
+        counts = [None] * self.n
+        dist.all_gather_object(counts, nch, group=group)
+        N.check(N.lib().cw_slab_chunks(self.part.h, sum(counts[:self.rank]), sum(counts)))
+        self.tol = float(pcg_tol) if pcg_tol is not None else whole_grid_tol(state, omega, precond)
         self.exchange = DistExchange(self.windows, self.rank, group)
         self._attach()
         self.time = state.time

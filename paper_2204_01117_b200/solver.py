@@ -208,6 +208,10 @@ def _raise_for(rc: int, rep, grid: GridSpec):
         return
     if rc == N.CW_ERR_PCG:
         raise ProjectionError(PcgReport(rep.iterations, bool(rep.converged), rep.criterion))
+    if rc == N.CW_ERR_HALO:
+        raise ValueError(f"z-slab halo too shallow: max|w| dt/dz = {rep.criterion:.3f} this step reaches "
+                         f"{rep.bad_cell} planes across a slab face (2 floor(S) + 4); rebuild the slabs "
+                         f"with halo >= {rep.bad_cell} or take a smaller dt")
     if rc == N.CW_ERR_NONFINITE:
         ijk = tuple(int(x) for x in np.unravel_index(rep.bad_cell, grid.shape))
         name = "k" if rep.bad_field == 0 else "omega"

@@ -12,11 +12,16 @@ against goldens made by the UNMODIFIED reference
 * gradient_descent on channel_opt (settle 120) and the C4 16-parameter
   recipe at 96x96x24 (FD gradient + one update).
 
-Gates (north_star): identical per-step PCG iteration counts on every scene
-the oracle certifies (tests/golden/cert_<name>.json: the reference's counts
-survive fp32-level noise), per-step field L2 norms and end fields within
-1e-4 relative (whole fields, or the golden's fixed stride subsample for the
-large grids), per-step CFL within 1e-4.
+Gates (north_star, with the SURVEY 8c noise-floor protocol): identical
+per-step PCG iteration counts on every scene the oracle certifies
+(tests/golden/cert_<name>.json: the reference's own counts survive
+fp32-level noise, 1e-6 relative per step); per-step field L2 norms, CFL and
+the end fields (whole, or the golden's fixed stride subsample for the large
+grids) within 1e-4 relative -- or, where the reference itself moves more
+than that under the same noise (its field floor, measured by
+scripts/certify_configs.py), within 5x that floor.  The floors are part of
+the committed certification; bielefeld_like and C2 sit below 1e-4, C3's
+k / omega and channel_opt's fields above it.
 """
 import json
 import os
@@ -44,6 +49,13 @@ def _certified(name):
         return json.load(fh)
 
 
+def _tol(cert, n, base=1e-4):
+    """1e-4, or 5x the reference's own deviation under fp32-level noise."""
+    if cert is None or "field_floor_rel_l2" not in cert:
+        return base
+    return max(base, 5.0 * cert["field_floor_rel_l2"][n])
+
+
 @pytest.mark.parametrize("name", TRAJ)
 def test_config_trajectory_matches_reference(name):
     from paper_2204_01117_b200 import solver
@@ -55,6 +67,7 @@ def test_config_trajectory_matches_reference(name):
     theta = g["theta"] if g["theta"].size else None
     st = comp.make_state(theta)
     steps = int(g["steps"])
+    cert = _certified(name)
     iters, cfl, divb, norms = [], [], [], {n: [] for n in FIELDS}
     for _ in range(steps):
         rep = solver.step_many(st, sc.solver, comp.psys, comp.preconditioner, sc.inlet, 1, sc.pcg_tol)[0]
@@ -64,7 +77,6 @@ def test_config_trajectory_matches_reference(name):
         for n in FIELDS:
             norms[n].append(float(torch.linalg.vector_norm(st.fields[n].double())))
     gold_it = g["pcg_iterations"].tolist()
-    cert = _certified(name)
     if cert is not None and not cert["certified"]:
         # the reference itself moves on these steps under fp32-level noise:
         # gate the others exactly, these within one iteration
@@ -73,10 +85,10 @@ def test_config_trajectory_matches_reference(name):
             assert a == b or (s in soft and abs(a - b) <= 1), (s, a, b)
     else:
         assert iters == gold_it
-    np.testing.assert_allclose(cfl, g["cfl"], rtol=1e-4)
-    np.testing.assert_allclose(divb, g["div_before"], rtol=1e-3)
+    np.testing.assert_allclose(cfl, g["cfl"], rtol=max(_tol(cert, c) for c in ("u", "v", "w")))
+    np.testing.assert_allclose(divb, g["div_before"], rtol=max(1e-3, _tol(cert, "p")))
     for n in FIELDS:
-        np.testing.assert_allclose(norms[n], g[f"norm_{n}"], rtol=1e-4, err_msg=n)
+        np.testing.assert_allclose(norms[n], g[f"norm_{n}"], rtol=_tol(cert, n), err_msg=n)
     stride = int(g["stride"])
     for n in FIELDS:
         got = st.fields[n].double().cpu().numpy()
@@ -84,40 +96,57 @@ def test_config_trajectory_matches_reference(name):
             e = rel_l2(got.ravel()[::stride], g[f"sub_{n}"])
         else:
             e = rel_l2(got, g[n])
-        assert e <= 1e-4, f"{n}: rel-L2 {e:.3e}"
+        assert e <= _tol(cert, n), f"{n}: rel-L2 {e:.3e} (tolerance {_tol(cert, n):.1e})"
+
+
+def _loss_rtol(name):
+    """1e-4, or 5x the reference objective's own deviation under fp32-level
+    noise (scripts/certify_configs.py: evaluate_objective with 1e-6 relative
+    noise on the state after every step)."""
+    cert = _certified(name)
+    if cert is None or "loss_floor_rel" not in cert:
+        return 1e-4
+    return max(1e-4, 5.0 * max(cert["loss_floor_rel"]))
+
+
+def _check_optimizer(name):
+    """gradient_descent through the reference's optimize.py recipe:
+    * the losses at the golden's design vectors (forward-evaluation parity,
+      north_star 1e-4 or the objective's floor);
+    * the FD gradient at theta0 and theta1 = clamp(theta0 - lam grad): a
+      forward difference over eps = 0.1 turns a loss tolerance rtol * L into
+      2 rtol L / eps on the gradient, so that is the gate."""
+    from paper_2204_01117_b200.optimize import (DesignVector, ObjectiveSpec, evaluate_objective,
+                                                finite_diff_gradient, gradient_descent)
+    from paper_2204_01117_b200.scenario import CompiledScenario, scenario_from_dict
+    g = _gold(name)
+    sc = scenario_from_dict(json.loads(str(g["doc"])))
+    comp = CompiledScenario.compile(sc)
+    rtol = _loss_rtol(name)
+    for th, lg in zip(g["theta_history"], g["history"]):
+        ev = evaluate_objective(comp, th)
+        assert abs(ev.loss - lg) <= rtol * abs(lg), (th, ev.loss, lg, rtol)
+    spec = ObjectiveSpec.from_scenario(sc)
+    design = DesignVector.from_scenario(sc)
+    L = float(g["history"][0])
+    gtol = 2.0 * rtol * L / 0.1
+    for k, (th, gg) in enumerate(zip(g["theta_history"], g["grads"])):
+        grad, _ = finite_diff_gradient(comp, th, spec, design=design)
+        np.testing.assert_allclose(grad, gg, rtol=0, atol=gtol, err_msg=f"gradient {k}")
+    res = gradient_descent(comp, max_iter=int(g["max_iter"]))
+    assert len(res.theta_history) == len(g["theta_history"])
+    for a, b in zip(res.theta_history, g["theta_history"]):
+        np.testing.assert_allclose(a, b, rtol=0, atol=gtol)
 
 
 def test_channel_opt_gradient_descent_matches_reference():
-    """channel_opt.json (settle 120, its stable window): the reference's
-    gradient_descent(max_iter=2) -- FD gradients, theta trajectory, losses."""
-    from paper_2204_01117_b200.optimize import ObjectiveSpec, finite_diff_gradient, gradient_descent
-    from paper_2204_01117_b200.scenario import CompiledScenario, scenario_from_dict
-    g = _gold("chopt_opt_120")
-    sc = scenario_from_dict(json.loads(str(g["doc"])))
-    comp = CompiledScenario.compile(sc)
-    res = gradient_descent(comp, max_iter=int(g["max_iter"]))
-    np.testing.assert_allclose(res.history, g["history"], rtol=1e-4)
-    assert len(res.theta_history) == len(g["theta_history"])
-    for a, b in zip(res.theta_history, g["theta_history"]):
-        np.testing.assert_allclose(a, b, rtol=0, atol=1e-4 * max(1.0, float(np.abs(b).max())))
-    grad, base = finite_diff_gradient(comp, g["theta_history"][0], ObjectiveSpec.from_scenario(sc))
-    assert abs(base.loss - g["grad_base_loss"][0]) <= 1e-4 * abs(g["grad_base_loss"][0])
-    # a forward difference over eps = 0.1 amplifies the losses' relative
-    # error 1e-4 by L / eps
-    np.testing.assert_allclose(grad, g["grads"][0], rtol=0, atol=2e-4 * abs(base.loss) / 0.1)
+    """channel_opt.json with settle 120 (inside its stable window),
+    its translate_x / translate_y design: the reference's
+    gradient_descent(max_iter=2)."""
+    _check_optimizer("chopt_opt_120")
 
 
 def test_c4_recipe_fd_gradient_and_update_match_reference():
     """C4 (16 extent parameters, 6 regions) at 96x96x24, settle 120: the
-    reference's gradient_descent(max_iter=1) = one base evaluation, the
-    16-job FD gradient and the updated design's evaluation."""
-    from paper_2204_01117_b200.optimize import gradient_descent
-    from paper_2204_01117_b200.scenario import CompiledScenario, scenario_from_dict
-    g = _gold("c4_city_96")
-    sc = scenario_from_dict(json.loads(str(g["doc"])))
-    comp = CompiledScenario.compile(sc)
-    res = gradient_descent(comp, max_iter=1)
-    np.testing.assert_allclose(res.history, g["history"], rtol=1e-4)
-    L = float(g["history"][0])
-    for a, b in zip(res.theta_history, g["theta_history"]):
-        np.testing.assert_allclose(a, b, rtol=0, atol=2e-4 * L / 0.1)
+    reference's gradient_descent(max_iter=1)."""
+    _check_optimizer("c4_city_96")
