@@ -207,10 +207,13 @@ static int make_tmap(CUtensorMap* m, CUtensorMapDataType dt, size_t esz, void* b
 
 // PCG work decomposition: tiles TX x TY over (x, y), z-chunks of zc planes;
 // each co-resident block streams ceil(U/B) units of zc+2 planes: minimise
-// that critical path (halo planes included).  At most CW_PCG_MAXC chunks
-// (the in-kernel fold keeps one sum per chunk).  CW_PCG_ZC overrides.
+// that critical path (halo planes included).  At most CW_PCG_MAXG (chunk,
+// 32-tile group) items (the in-kernel fold keeps one sum per item).  CW_PCG_ZC
+// overrides.
 static int choose_zc(int tiles, int nown, int maxb) {
-  const int zmin = std::max(1, (nown + CW_PCG_MAXC - 1) / CW_PCG_MAXC);
+  const int ng = (tiles + 31) / 32;   // (chunk, 32-tile group) items of the fold must fit CW_PCG_MAXG
+  const int maxc = std::max(1, CW_PCG_MAXG / ng);
+  const int zmin = std::max(1, (nown + maxc - 1) / maxc);
   int best_zc = nown, best_cost = 1 << 30;
   for (int zc = zmin; zc <= nown; ++zc) {
     const int U = tiles * ((nown + zc - 1) / zc);
@@ -1041,14 +1044,15 @@ extern "C" int cw_pcg_chunk_of(const cw_grid* g, int precision, int device, int*
 extern "C" int cw_set_pcg_chunk(cw_ctx* c, int zc) {
   if (!c) return fail(CW_ERR_INVALID, "null argument");
   const int nown = c->d.o1 - c->d.o0;
-  if (zc < 1 || (nown + zc - 1) / zc > CW_PCG_MAXC) return fail(CW_ERR_INVALID, "bad PCG chunk size");
+  if (zc < 1 || (nown + zc - 1) / zc * ((c->ntx * c->nty + 31) / 32) > CW_PCG_MAXG)
+    return fail(CW_ERR_INVALID, "bad PCG chunk size");
   c->zc = std::min(zc, nown);
   plan_units(c);
   return alloc_partials(c);
 }
 
 extern "C" int cw_slab_chunks(cw_ctx* c, int chunk0, int nchunk_g) {
-  if (!c || chunk0 < 0 || nchunk_g < 1 || nchunk_g > CW_MAX_CHUNKS ||
+  if (!c || chunk0 < 0 || nchunk_g < 1 || nchunk_g * ((c->ntx * c->nty + 31) / 32) > CW_MAX_CHUNKS ||
       chunk0 + c->U / (c->ntx * c->nty) > nchunk_g)
     return fail(CW_ERR_INVALID, "bad chunk range");
   c->chunk0 = chunk0;
@@ -1091,7 +1095,8 @@ static int group_pcg(cw_ctx** cs, const cw_fields* fs, int n, const cw_params* p
   std::vector<PcgArgs<T>> args(n);
   int nchunk_g = 0;
   for (int s = 0; s < n; ++s) nchunk_g += cs[s]->U / (cs[s]->ntx * cs[s]->nty);
-  if (nchunk_g > CW_MAX_CHUNKS) return fail(CW_ERR_INVALID, "too many PCG chunks over the slabs");
+  if (nchunk_g * ((c0->ntx * c0->nty + 31) / 32) > CW_MAX_CHUNKS)
+    return fail(CW_ERR_INVALID, "too many PCG fold items over the slabs");
   for (int s = 0, ch = 0; s < n; ++s) {
     cw_ctx* c = cs[s];
     c->chunk0 = ch;

@@ -108,7 +108,7 @@ struct PcgArgs {
   int nslab, slab;
   PcgPeer<T> lo, hi;
   unsigned int* xbar;        // root slab: [0] arrivals, [32] generation (system scope)
-  double* xval;              // root slab: [2 sets][3 values][nchunk_g] chunk sums
+  double* xval;              // root slab: [2 sets][3 values][nchunk_g * groups] item sums
   long long timeout_ns;
   int probe_mode, probe_iters;   // developer timing probe (CW_PCG_PROBE), 0 = off
 };
@@ -324,35 +324,34 @@ __device__ __forceinline__ bool wait_tag(const PcgArgs<T>& A, const unsigned* ta
   return true;
 }
 
-// chunk sums of this launch's units into S.chunk (wait: acquire every tag
-// first); returns after a __syncthreads
+// Item sums of this launch's units into S.grp.  An item is (chunk c, group
+// g): tiles 32g .. 32g+31 of chunk c, items numbered c * ng + g (ng groups
+// per chunk).  One warp per item (lane l: tile 32g + l, a shuffle tree, lane
+// 0's result); items spread over the block's warps.  Returns after a
+// __syncthreads.  wait: acquire every unit's tag first.
 template <typename T, typename Sh>
 __device__ __forceinline__ void fold_chunks(const PcgArgs<T>& A, const double* part, int set, unsigned seq, int nval,
                                             unsigned maxmask, bool wait, Sh& S) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (int)(blockDim.x >> 5);
   const unsigned* tags = A.tags + (size_t)set * A.PS;
-  for (int c = wid; c < A.nchunk; c += nw) {
+  const int ng = (A.tiles + 31) >> 5;
+  const bool flat = (A.tiles & 31) == 0;   // items are runs of 32 consecutive units
+  for (int it = wid; it < A.nchunk * ng; it += nw) {
+    int u, i;
+    if (flat) {
+      u = it * 32 + lane;
+      i = 0;
+    } else {
+      const int c = it / ng;
+      i = (it - c * ng) * 32 + lane;
+      u = c * A.tiles + i;
+    }
     double a[3] = {0.0, 0.0, 0.0};
-    for (int i0 = lane; i0 < A.tiles; i0 += 32 * 4) {   // four tiles' loads in flight per lane
-      double v[4][3];
+    if (i < A.tiles) {
+      if (wait) wait_tag<T>(A, tags + u, seq);
 #pragma unroll
-      for (int m = 0; m < 4; ++m) {
-        const int i = i0 + 32 * m;
-        const int u = c * A.tiles + i;
-        if (wait && i < A.tiles) wait_tag<T>(A, tags + u, seq);
-#pragma unroll
-        for (int q = 0; q < 3; ++q) v[m][q] = (q < nval && i < A.tiles) ? __ldcg(part + (size_t)q * A.PS + u) : 0.0;
-      }
-#pragma unroll
-      for (int m = 0; m < 4; ++m) {
-        if (i0 + 32 * m < A.tiles) {
-#pragma unroll
-          for (int q = 0; q < 3; ++q)
-            if (q < nval)
-              a[q] = ((maxmask >> q) & 1u) ? ((v[m][q] > a[q] || v[m][q] != v[m][q]) ? v[m][q] : a[q])
-                                           : a[q] + v[m][q];
-        }
-      }
+      for (int q = 0; q < 3; ++q)
+        if (q < nval) a[q] = __ldcg(part + (size_t)q * A.PS + u);
     }
 #pragma unroll
     for (int q = 0; q < 3; ++q) {
@@ -363,25 +362,29 @@ __device__ __forceinline__ void fold_chunks(const PcgArgs<T>& A, const double* p
           const double b = __shfl_xor_sync(0xffffffffu, a[q], o);
           a[q] = mx ? ((b > a[q] || b != b) ? b : a[q]) : a[q] + b;
         }
-        if (lane == 0) S.chunk[q][c] = a[q];
+        if (lane == 0) S.grp[q][it] = a[q];
       }
     }
   }
   __syncthreads();
 }
 
-// the chunk sums (n of them, in chunk order) to totals; every thread the same bits
-__device__ __forceinline__ void sum_chunks(const double* ch, int stride, int n, int nval, unsigned maxmask,
-                                           double* out) {
-  for (int q = 0; q < nval; ++q) {
+// the totals: all items in item order (one thread per value), broadcast
+// through shared memory -- the same sequence the z-slab root table sums
+template <typename T, typename Sh>
+__device__ __forceinline__ void sum_items(const PcgArgs<T>& A, Sh& S, int nval, unsigned maxmask, double* out) {
+  if (threadIdx.x < (unsigned)nval) {
+    const int q = threadIdx.x, n = A.nchunk * ((A.tiles + 31) >> 5);
     const bool mx = (maxmask >> q) & 1u;
-    double a = ch[(size_t)q * stride];
-    for (int c = 1; c < n; ++c) {
-      const double b = ch[(size_t)q * stride + c];
+    double a = S.grp[q][0];
+    for (int it = 1; it < n; ++it) {
+      const double b = S.grp[q][it];
       a = mx ? ((b > a || b != b) ? b : a) : a + b;
     }
-    out[q] = a;
+    S.vals[q] = a;
   }
+  __syncthreads();
+  for (int q = 0; q < nval; ++q) out[q] = S.vals[q];
 }
 
 // ---------------------------------------------------------------------------
@@ -421,8 +424,8 @@ struct PcgWork {
   alignas(16) T yb[2][YH][PCG_YP];   // y on the y tile, planes kk and kk-1
 };
 
-#ifndef CW_PCG_MAXC
-#define CW_PCG_MAXC 64   // z-chunks per launch (the context picks zc >= planes / 64)
+#ifndef CW_PCG_MAXG
+#define CW_PCG_MAXG 128  // (z-chunk, 32-tile group) items per launch (the context picks zc to fit)
 #endif
 template <typename T>
 struct PcgShared {
@@ -435,7 +438,7 @@ struct PcgShared {
   double bc[4];
   double vals[4];           // slab_reduce results
   double fold[3 * 32];      // fold_multi warp results
-  double chunk[3][CW_PCG_MAXC];   // fold_units: per-chunk sums (fixed tree), summed in chunk order
+  double grp[3][CW_PCG_MAXG];     // fold_chunks: (chunk, 32-tile group) sums, combined in order
   unsigned last, gen0;      // slab_reduce: this block arrived last; generation seen
   unsigned long long pt[3]; // timing probe (modes 13-16): phase start, first stage landed, jobs done
   alignas(8) uint64_t full[8];
@@ -803,6 +806,7 @@ __device__ void phaseA(const PcgArgs<T>& A, const Blk& blk, double* part, int se
   JobCursor prod, cons;
   double acc = 0.0;
   if (cursor_begin<T>(A, blk, cons)) {
+    const int last_unit = blk.id + (A.U - 1 - blk.id) / blk.n * blk.n;
     prod = cons;
     const unsigned t0 = ticket;
     unsigned issued = 0;
@@ -893,7 +897,7 @@ __device__ void phaseA(const PcgArgs<T>& A, const Blk& blk, double* part, int se
           pend = true;
         }
       }
-      if (kk == u.k1) {   // the unit's last plane: its p'.Ap is complete
+      if (kk == u.k1 && cons.unit + cons.nb < A.U) {   // a unit done and another follows: publish it now
         const double sum = block_sum(acc, S.red);
         if (threadIdx.x == 0) publish_unit<T>(A, part, set, cons.unit, 1, &sum, seq);
         acc = 0.0;
@@ -913,6 +917,8 @@ __device__ void phaseA(const PcgArgs<T>& A, const Blk& blk, double* part, int se
     }
     if (timing && threadIdx.x == 0) S.pt[2] = globaltimer();
     ticket = t0 + j;
+    const double sum = block_sum(acc, S.red);   // the block's last unit
+    if (threadIdx.x == 0) publish_unit<T>(A, part, set, last_unit, 1, &sum, seq);
   }
 }
 
@@ -979,6 +985,7 @@ __device__ void phaseB(const PcgArgs<T>& A, const Blk& blk, double* part, int se
   double acc = 0.0;
   bool exceed = false;
   if (cursor_begin<T>(A, blk, cons)) {
+    const int last_unit = blk.id + (A.U - 1 - blk.id) / blk.n * blk.n;
     prod = cons;
     const unsigned t0 = ticket;
     unsigned issued = 0;
@@ -1108,7 +1115,7 @@ __device__ void phaseB(const PcgArgs<T>& A, const Blk& blk, double* part, int se
           }
         }
       }
-      if (kk == u.k1) {   // the unit's last plane: r'.z and the max-norm flag are complete
+      if (kk == u.k1 && cons.unit + cons.nb < A.U) {   // a unit done and another follows: publish it now
         const double sm = block_sum(acc, S.red);
         __syncthreads();
         const double mx = __syncthreads_or(exceed) ? 1.0 : 0.0;
@@ -1127,6 +1134,13 @@ __device__ void phaseB(const PcgArgs<T>& A, const Blk& blk, double* part, int se
     }
     if (timing && threadIdx.x == 0) S.pt[2] = globaltimer();
     ticket = t0 + j;
+    const double sm = block_sum(acc, S.red);   // the block's last unit
+    __syncthreads();
+    const double mx = __syncthreads_or(exceed) ? 1.0 : 0.0;
+    if (threadIdx.x == 0) {
+      const double v[2] = {sm, mx};
+      publish_unit<T>(A, part, set, last_unit, 2, v, seq);
+    }
   }
   __syncthreads();
 }
@@ -1187,9 +1201,10 @@ __device__ void slab_reduce(const PcgArgs<T>& A, const Blk& blk, const double* p
     // this slab's chunk sums (the same tree as the whole grid's), published
     // at their global chunk index in the root's table
     fold_chunks<T>(A, part, pset, seq, nval, maxmask, false, S);
-    for (int e = threadIdx.x; e < nval * A.nchunk; e += blockDim.x) {
-      const int q = e / A.nchunk, c = e - q * A.nchunk;
-      A.xval[((size_t)pset * 3 + q) * A.nchunk_g + A.chunk0 + c] = S.chunk[q][c];
+    const int ng = (A.tiles + 31) >> 5, ni = A.nchunk * ng, nig = A.nchunk_g * ng;
+    for (int e = threadIdx.x; e < nval * ni; e += blockDim.x) {   // item sums at their global item index
+      const int q = e / ni, it = e - q * ni;
+      A.xval[((size_t)pset * 3 + q) * nig + A.chunk0 * ng + it] = S.grp[q][it];
     }
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -1234,12 +1249,12 @@ __device__ void slab_reduce(const PcgArgs<T>& A, const Blk& blk, const double* p
     fence_proxy_async();   // the next phase's TMA reads see the pushed halo planes
   }
   __syncthreads();
-  if (threadIdx.x < nval) {   // all global chunks in chunk order (volatile: peers write the table)
-    const int q = threadIdx.x;
+  if (threadIdx.x < nval) {   // all global items in item order (volatile: peers write the table)
+    const int q = threadIdx.x, nig = A.nchunk_g * ((A.tiles + 31) >> 5);
     const bool mx = (maxmask >> q) & 1u;
-    const volatile double* xv = A.xval + ((size_t)pset * 3 + q) * A.nchunk_g;
+    const volatile double* xv = A.xval + ((size_t)pset * 3 + q) * nig;
     double v = xv[0];
-    for (int c = 1; c < A.nchunk_g; ++c) {
+    for (int c = 1; c < nig; ++c) {
       const double w = xv[c];
       v = mx ? ((w > v || w != w) ? w : v) : v + w;
     }
@@ -1265,9 +1280,12 @@ __device__ __forceinline__ void phase_end(const PcgArgs<T>& A, const Blk& blk, c
   // a grid barrier (one arrival counter: measured faster than every block
   // acquiring every unit's tag), then the chunk-structured fold
   grid_barrier(A.bar, A.gate, A.rep, A.timeout_ns, (unsigned)blk.n, epoch);
+#ifdef CW_PCG_FOLD_MULTI   // developer comparison: the block-wide fold (not slab-split invariant)
+  fold_multi(part, A.U, A.PS, nval, maxmask, out, S.fold);
+#else
   fold_chunks<T>(A, part, pset, seq, nval, maxmask, false, S);
-  sum_chunks(&S.chunk[0][0], CW_PCG_MAXC, A.nchunk, nval, maxmask, out);
-  __syncthreads();
+  sum_items<T>(A, S, nval, maxmask, out);   // S.grp / S.vals are next written a phase later
+#endif
 }
 
 template <typename T, bool SLABS>
@@ -1340,8 +1358,8 @@ __device__ __forceinline__ void pcg_body(const PcgArgs<T>& A, const Blk& blk, ui
     // grid barrier; the state's p is not meaningful afterwards
     for (int q = 0; q < A.probe_iters; ++q) {
       // 6, 7: phase A and phase B alternate as in the solve (7: stream only)
-      const bool pa = A.probe_mode == 1 || A.probe_mode == 4 || (A.probe_mode >= 6 && !(q & 1));
-      const bool pb = A.probe_mode == 2 || (A.probe_mode >= 6 && (q & 1));
+      const bool pa = A.probe_mode == 1 || A.probe_mode == 4 || (A.probe_mode >= 6 && A.probe_mode < 17 && !(q & 1));
+      const bool pb = A.probe_mode == 2 || (A.probe_mode >= 6 && A.probe_mode < 17 && (q & 1));
       const bool stream = A.probe_mode == 4 || A.probe_mode == 7;
       if (pa && stream) phaseA<T, SLABS, true, true>(A, blk, P[0], 0, 0u, S, ring, ticket, false, (T)0.5, (T)0.0, (q >> 1) & 1);
       if (pa && !stream) phaseA<T, SLABS, true, false>(A, blk, P[0], 0, 0u, S, ring, ticket, false, (T)0.5, (T)0.0, (q >> 1) & 1);
@@ -1355,6 +1373,15 @@ __device__ __forceinline__ void pcg_body(const PcgArgs<T>& A, const Blk& blk, ui
       if (A.probe_mode == 5) {   // barrier plus phase B's two folds
         rz += fold_partials(P[1], B, 0, S.bc);
         rmax = fold_partials(P[1] + A.PS, B, 1, S.bc);
+      }
+      if (A.probe_mode == 17) {   // barrier plus the chunk-structured fold of two values
+        fold_chunks<T>(A, P[1], 1, 0u, 2, 2u, false, S);
+        sum_items<T>(A, S, 2, 2u, red);
+        rz += red[0];
+      }
+      if (A.probe_mode == 18) {   // barrier plus fold_multi of two values
+        fold_multi(P[1], A.U, A.PS, 2, 2u, red, S.fold);
+        rz += red[0];
       }
     }
     // 8: report the mean grid-barrier wait per block and phase (us) as the criterion

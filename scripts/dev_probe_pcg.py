@@ -18,7 +18,8 @@ NAMES = {1: "phase A + barrier", 2: "phase B + barrier", 3: "barrier", 4: "phase
          10: "A,B alternating, no loads: compute on stale stages (per phase)",
          12: "A,B alternating, TMA wait reported (per phase)",
          13: "A,B alternating, mean first-stage latency reported", 14: "A,B alternating, mean job time reported",
-         15: "A,B alternating, max over blocks of job time", 16: "A,B alternating, min over blocks of job time"}
+         15: "A,B alternating, max over blocks of job time", 16: "A,B alternating, min over blocks of job time",
+         17: "barrier + chunk-structured fold (2 values)", 18: "barrier + fold_multi (2 values)"}
 
 
 def timed(mode, n):
