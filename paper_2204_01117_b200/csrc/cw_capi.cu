@@ -804,8 +804,18 @@ static void st_turb(cw_ctx* c, const StepPtrs<T>& P, const cw_params* prm, const
   sc.sigma = prm->sigma; sc.sigma_star = prm->sigma_star; sc.c_lim = prm->c_lim;
   sc.lim_scale = (double)((T)2 / (T)prm->c_mu);   // the kernel's former per-cell (T)2 / (T)c_mu, bit for bit
   sc.k_in = prm->k_in; sc.om_in = prm->omega_in; sc.nut_in = prm->k_in / prm->omega_in;
+#ifdef CW_TURB_PERCELL   // developer comparison: the per-cell kernel
   (k_turbulence<T><<<dim3((c->d.nx + ST_BX - 1) / ST_BX, (c->d.ny + ST_BY - 1) / ST_BY,
                           (c->d.nz + ZT_TURB - 1) / ZT_TURB), B3, 0, st>>>(c->d, P.u, P.v, P.w, kin, win, P.k, P.om, P.nut, (T*)c->speed, sc, rep, c->gate), ++c->launches);
+#elif defined(CW_TURB_ZMARCH)   // developer comparison: the z-march kernel
+  (k_turbulence_z<T><<<dim3((c->d.nx + 31) / 32, (c->d.ny + 7) / 8, (c->d.nz + TURB_CZ - 1) / TURB_CZ), dim3(32, 8), 0,
+                       st>>>(c->d, P.u, P.v, P.w, kin, win, P.k, P.om, P.nut, (T*)c->speed, sc, rep, c->gate),
+   ++c->launches);
+#else
+  (k_turbulence_c<T><<<g3(c->d.nx, c->d.ny, c->d.nz), B3, 0, st>>>(c->d, P.u, P.v, P.w, kin, win, P.k, P.om, P.nut,
+                                                                   (T*)c->speed, sc, rep, c->gate),
+   ++c->launches);
+#endif
   (k_turb_check<<<1, 1, 0, st>>>(rep, c->gate), ++c->launches);
 }
 

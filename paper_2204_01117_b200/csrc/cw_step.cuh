@@ -935,6 +935,244 @@ __global__ void k_turbulence(Dims d, const T* __restrict__ u, const T* __restric
   }
 }
 
+// The same k-omega update as a z march (one launch of (32, 8)-thread blocks,
+// each thread a column (i, j) through TURB_CZ planes).  Per plane a thread
+// loads its own cell once -- the six faces, k, omega, nu_t -- and forms the
+// cell-centred velocities; x and y neighbours come from a shared plane tile
+// (edge threads fill the one-cell halo), z neighbours from registers carried
+// down the column.  Three shared planes rotate, so one barrier per plane
+// suffices.  The arithmetic is the per-cell kernel's expression for
+// expression: np.gradient (central, one-sided at the array ends) of the
+// cell velocities, the edge-padded Laplacians of k and omega, the Patankar
+// update, floors and limiter (turbulence.py:36-132).  ~530 instructions per
+// cell in k_turbulence (ncu), most of them index arithmetic of the
+// neighbour loads.
+#ifndef CW_TURB_CZ
+#define CW_TURB_CZ 8
+#endif
+constexpr int TURB_CZ = CW_TURB_CZ;
+
+template <typename T>
+struct TurbCell {
+  T uc, vc, wc, k, om;
+};
+
+// np.gradient along one axis at position q of n (edge_order 1)
+template <typename T>
+__device__ __forceinline__ T grad3(T fm, T f0, T fp, int q, int n, T rh) {
+  if (n == 1) return (T)0;
+  if (q == 0) return (fp - f0) * rh;
+  if (q == n - 1) return (f0 - fm) * rh;
+  return (fp - fm) * ((T)0.5 * rh);
+}
+// one axis of the edge-padded Laplacian (turbulence.py:36-63)
+template <typename T>
+__device__ __forceinline__ T lap3(T fm, T f0, T fp, int q, int n, T r2) {
+  if (n == 1) return (T)0;
+  if (q == 0) return (fp - f0) * r2;
+  if (q == n - 1) return (fm - f0) * r2;
+  return (fm - (T)2 * f0 + fp) * r2;
+}
+
+template <typename T>
+__device__ __forceinline__ TurbCell<T> turb_cell(const Dims& d, const T* __restrict__ u, const T* __restrict__ v,
+                                                 const T* __restrict__ w, const T* __restrict__ kin,
+                                                 const T* __restrict__ win, int i, int j, int k) {
+  TurbCell<T> q;
+  const int c = d.cidx32(i, j, k);
+  const int ui = (k * d.ny + j) * (d.nx + 1) + i;
+  const int vi = (k * (d.ny + 1) + j) * d.nx + i;
+  q.uc = (T)0.5 * (u[ui] + u[ui + 1]);
+  q.vc = (T)0.5 * (v[vi] + v[vi + d.nx]);
+  q.wc = (T)0.5 * (w[c] + w[c + d.nx * d.ny]);
+  q.k = kin[c];
+  q.om = win[c];
+  return q;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_turbulence_z(Dims d, const T* __restrict__ u, const T* __restrict__ v,
+                                                      const T* __restrict__ w, const T* __restrict__ kin,
+                                                      const T* __restrict__ win, T* __restrict__ kout,
+                                                      T* __restrict__ wout, T* __restrict__ nut,
+                                                      T* __restrict__ nut_prev, StepConsts sc, DevReport* rep,
+                                                      const int* gate) {
+  if (*gate) return;
+  // [rotating plane][quantity uc, vc, wc, k, om][row j0-1 .. j0+8][column i0-1 .. i0+32]
+  __shared__ T tile[3][5][10][34];
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const int i = (int)blockIdx.x * 32 + tx, j = (int)blockIdx.y * 8 + ty;
+  const int kb = (int)blockIdx.z * TURB_CZ, ke = min(kb + TURB_CZ, d.nz);
+  const bool in = i < d.nx && j < d.ny;
+  const T dt = (T)sc.dt, nu = (T)sc.nu, cap = (T)sc.cap_turb;
+  const T rh0 = inv_h<T>(d, 0), rh1 = inv_h<T>(d, 1), rh2 = inv_h<T>(d, 2);
+  const T r20 = inv_h2<T>(d, 0), r21 = inv_h2<T>(d, 1), r22 = inv_h2<T>(d, 2);
+  const int m0 = max(kb - 1, 0), m1 = min(ke, d.nz - 1);   // planes whose cells the chunk reads
+  TurbCell<T> qm{}, q0{}, qp{};   // planes m-2, m-1, m of this column
+  auto put = [&](T (*t)[10][34], int r, int cl, const TurbCell<T>& q) {
+    t[0][r][cl] = q.uc; t[1][r][cl] = q.vc; t[2][r][cl] = q.wc; t[3][r][cl] = q.k; t[4][r][cl] = q.om;
+  };
+  for (int m = m0; m <= m1 + 1; ++m) {
+    if (m <= m1) {
+      T (*t)[10][34] = tile[m % 3];
+      if (in) {
+        qp = turb_cell<T>(d, u, v, w, kin, win, i, j, m);
+        put(t, ty + 1, tx + 1, qp);
+        // the one-cell halo of the tile (not at the grid's ends)
+        if (tx == 0 && i > 0) put(t, ty + 1, 0, turb_cell<T>(d, u, v, w, kin, win, i - 1, j, m));
+        if ((tx == 31 || i == d.nx - 1) && i + 1 < d.nx)
+          put(t, ty + 1, tx + 2, turb_cell<T>(d, u, v, w, kin, win, i + 1, j, m));
+        if (ty == 0 && j > 0) put(t, 0, tx + 1, turb_cell<T>(d, u, v, w, kin, win, i, j - 1, m));
+        if ((ty == 7 || j == d.ny - 1) && j + 1 < d.ny)
+          put(t, ty + 2, tx + 1, turb_cell<T>(d, u, v, w, kin, win, i, j + 1, m));
+      }
+    }
+    __syncthreads();
+    const int k = m - 1;   // the plane whose update is complete: m-2, m-1, m are in hand
+    if (in && k >= kb && k < ke) {
+      const T (*t)[10][34] = tile[k % 3];
+      const int r = ty + 1, cl = tx + 1;
+      const int c = d.cidx32(i, j, k);
+      const int ui = (k * d.ny + j) * (d.nx + 1) + i;
+      const int vi = (k * (d.ny + 1) + j) * d.nx + i;
+      const T dudx = (u[ui + 1] - u[ui]) * rh0;
+      const T dvdy = (v[vi + d.nx] - v[vi]) * rh1;
+      const T dwdz = (w[c + d.nx * d.ny] - w[c]) * rh2;
+      const TurbCell<T>& zc = q0;   // this cell (plane k)
+      const TurbCell<T>& zm = k > 0 ? qm : q0;
+      const TurbCell<T>& zp = k < d.nz - 1 ? qp : q0;
+      const T dudy = grad3<T>(t[0][r - 1][cl], t[0][r][cl], t[0][r + 1][cl], j, d.ny, rh1);
+      const T dudz = grad3<T>(zm.uc, zc.uc, zp.uc, k, d.nz, rh2);
+      const T dvdx = grad3<T>(t[1][r][cl - 1], t[1][r][cl], t[1][r][cl + 1], i, d.nx, rh0);
+      const T dvdz = grad3<T>(zm.vc, zc.vc, zp.vc, k, d.nz, rh2);
+      const T dwdx = grad3<T>(t[2][r][cl - 1], t[2][r][cl], t[2][r][cl + 1], i, d.nx, rh0);
+      const T dwdy = grad3<T>(t[2][r - 1][cl], t[2][r][cl], t[2][r + 1][cl], j, d.ny, rh1);
+      const T a = dudy + dvdx, b = dudz + dwdx, e = dvdz + dwdy;
+      const T s2 = (dudx * dudx + dvdy * dvdy + dwdz * dwdz) + (T)0.5 * (a * a + b * b + e * e);
+      T lk = (T)0, lw = (T)0;
+      lk += lap3<T>(t[3][r][cl - 1], zc.k, t[3][r][cl + 1], i, d.nx, r20);
+      lw += lap3<T>(t[4][r][cl - 1], zc.om, t[4][r][cl + 1], i, d.nx, r20);
+      lk += lap3<T>(t[3][r - 1][cl], zc.k, t[3][r + 1][cl], j, d.ny, r21);
+      lw += lap3<T>(t[4][r - 1][cl], zc.om, t[4][r + 1][cl], j, d.ny, r21);
+      lk += lap3<T>(zm.k, zc.k, zp.k, k, d.nz, r22);
+      lw += lap3<T>(zm.om, zc.om, zp.om, k, d.nz, r22);
+      const T nt = nut[c];
+      const T kc = zc.k, wc = zc.om;
+      const T pk = (T)2 * nt * s2;
+      T sk = (T)sc.sigma_star * nt; sk = sk < cap ? sk : cap;
+      T sw = (T)sc.sigma * nt; sw = sw < cap ? sw : cap;
+      const T dk = nu + sk, dw = nu + sw;
+      const T kn = (kc + dt * (pk + dk * lk)) / ((T)1 + dt * (T)sc.c_mu * wc);
+      const T wn = (wc + dt * ((T)2 * (T)sc.alpha * s2 + dw * lw)) / ((T)1 + dt * (T)sc.beta * wc);
+      if (k >= d.o0 && k < d.o1) {   // reference C order over the global grid
+        const long long refi = ((long long)i * d.ny + j) * d.nzg + (k + d.kg0);
+        if (!isfinite(kn)) atomicMin(&rep->bad_index[0], refi);
+        if (!isfinite(wn)) atomicMin(&rep->bad_index[1], refi);
+      }
+      const T kf = kn > (T)1e-12 ? kn : (T)1e-12;
+      const T wf = wn > (T)1e-8 ? wn : (T)1e-8;
+      T omt = (T)sc.c_lim * sqrt(s2) * (T)sc.lim_scale;
+      omt = wf > omt ? wf : omt;
+      omt = omt > (T)1e-8 ? omt : (T)1e-8;
+      kout[c] = kf;
+      wout[c] = wf;
+      nut_prev[c] = nt;
+      nut[c] = kf / omt;
+    }
+    qm = q0;
+    q0 = qp;
+  }
+}
+
+// The k-omega update per cell with straight-line neighbour access: the
+// array-end rules of np.gradient and the edge-padded Laplacian become clamped
+// neighbour indices (a clamped neighbour equals the cell itself, and
+// (f - 2 f) + f_p == f_p - f exactly), so the interior and the edges run the
+// same instructions; the one-sided gradient keeps its 1/h, the central one
+// its 1/(2h).  Same arithmetic as k_turbulence, far fewer instructions.
+template <typename T>
+__global__ void __launch_bounds__(256) k_turbulence_c(Dims d, const T* __restrict__ u, const T* __restrict__ v,
+                                                      const T* __restrict__ w, const T* __restrict__ kin,
+                                                      const T* __restrict__ win, T* __restrict__ kout,
+                                                      T* __restrict__ wout, T* __restrict__ nut,
+                                                      T* __restrict__ nut_prev, StepConsts sc, DevReport* rep,
+                                                      const int* gate) {
+  if (*gate) return;
+  const int i = (int)(blockIdx.x * ST_BX + threadIdx.x), j = (int)(blockIdx.y * ST_BY + threadIdx.y);
+  const int k = (int)blockIdx.z;
+  if (i >= d.nx || j >= d.ny || k >= d.nz) return;
+  const T dt = (T)sc.dt, nu = (T)sc.nu, cap = (T)sc.cap_turb;
+  const T rh0 = inv_h<T>(d, 0), rh1 = inv_h<T>(d, 1), rh2 = inv_h<T>(d, 2);
+  const int nx = d.nx, ny = d.ny, nz = d.nz;
+  const int im = max(i - 1, 0), ip = min(i + 1, nx - 1);
+  const int jm = max(j - 1, 0), jp = min(j + 1, ny - 1);
+  const int km = max(k - 1, 0), kp = min(k + 1, nz - 1);
+  const T gx = (ip - im == 2) ? (T)0.5 * rh0 : rh0;   // central / one-sided (n == 1: both 0, any scale)
+  const T gy = (jp - jm == 2) ? (T)0.5 * rh1 : rh1;
+  const T gz = (kp - km == 2) ? (T)0.5 * rh2 : rh2;
+  const int uy = nx + 1, uz = (nx + 1) * ny;   // u strides
+  const int vy = nx, vz = nx * (ny + 1);       // v strides
+  const int cy = nx, cz = nx * ny;             // cell / w strides
+  const int c = k * cz + j * cy + i;
+  // own faces
+  const T* ur = u + k * uz + j * uy;
+  const T* vr = v + k * vz + j * vy;
+  const T u0 = ur[i], u1 = ur[i + 1];
+  const T v0 = vr[i], v1 = vr[i + vy];
+  const T w0 = w[c], w1 = w[c + cz];
+  const T dudx = (u1 - u0) * rh0;
+  const T dvdy = (v1 - v0) * rh1;
+  const T dwdz = (w1 - w0) * rh2;
+  // cell-centred velocities of the neighbours (cell_vel: 0.5 * (a + b))
+  const T* urm = u + k * uz + jm * uy; const T* urp = u + k * uz + jp * uy;       // rows jm, jp
+  const T* uzm = u + km * uz + j * uy; const T* uzp = u + kp * uz + j * uy;       // planes km, kp
+  const T uc_jm = (T)0.5 * (urm[i] + urm[i + 1]), uc_jp = (T)0.5 * (urp[i] + urp[i + 1]);
+  const T uc_km = (T)0.5 * (uzm[i] + uzm[i + 1]), uc_kp = (T)0.5 * (uzp[i] + uzp[i + 1]);
+  const T vc_im = (T)0.5 * (vr[im] + vr[im + vy]), vc_ip = (T)0.5 * (vr[ip] + vr[ip + vy]);
+  const T* vzm = v + km * vz + j * vy; const T* vzp = v + kp * vz + j * vy;
+  const T vc_km = (T)0.5 * (vzm[i] + vzm[i + vy]), vc_kp = (T)0.5 * (vzp[i] + vzp[i + vy]);
+  const T* wr = w + k * cz + j * cy;
+  const T wc_im = (T)0.5 * (wr[im] + wr[im + cz]), wc_ip = (T)0.5 * (wr[ip] + wr[ip + cz]);
+  const T* wrm = w + k * cz + jm * cy; const T* wrp = w + k * cz + jp * cy;
+  const T wc_jm = (T)0.5 * (wrm[i] + wrm[i + cz]), wc_jp = (T)0.5 * (wrp[i] + wrp[i + cz]);
+  const T dudy = (uc_jp - uc_jm) * gy, dudz = (uc_kp - uc_km) * gz;
+  const T dvdx = (vc_ip - vc_im) * gx, dvdz = (vc_kp - vc_km) * gz;
+  const T dwdx = (wc_ip - wc_im) * gx, dwdy = (wc_jp - wc_jm) * gy;
+  const T a = dudy + dvdx, b = dudz + dwdx, e = dvdz + dwdy;
+  const T s2 = (dudx * dudx + dvdy * dvdy + dwdz * dwdz) + (T)0.5 * (a * a + b * b + e * e);
+  // edge-padded Laplacians (pad_lap): clamped neighbours
+  const T r20 = inv_h2<T>(d, 0), r21 = inv_h2<T>(d, 1), r22 = inv_h2<T>(d, 2);
+  const int cxm = k * cz + j * cy + im, cxp = k * cz + j * cy + ip;
+  const int cym = k * cz + jm * cy + i, cyp = k * cz + jp * cy + i;
+  const int czm = km * cz + j * cy + i, czp = kp * cz + j * cy + i;
+  const T kc = kin[c], wc = win[c];
+  T lk = (T)0, lw = (T)0;
+  if (nx > 1) { lk += (kin[cxm] - (T)2 * kc + kin[cxp]) * r20; lw += (win[cxm] - (T)2 * wc + win[cxp]) * r20; }
+  if (ny > 1) { lk += (kin[cym] - (T)2 * kc + kin[cyp]) * r21; lw += (win[cym] - (T)2 * wc + win[cyp]) * r21; }
+  if (nz > 1) { lk += (kin[czm] - (T)2 * kc + kin[czp]) * r22; lw += (win[czm] - (T)2 * wc + win[czp]) * r22; }
+  const T nt = nut[c];
+  const T pk = (T)2 * nt * s2;
+  T sk = (T)sc.sigma_star * nt; sk = sk < cap ? sk : cap;
+  T sw = (T)sc.sigma * nt; sw = sw < cap ? sw : cap;
+  const T dk = nu + sk, dw = nu + sw;
+  const T kn = (kc + dt * (pk + dk * lk)) / ((T)1 + dt * (T)sc.c_mu * wc);
+  const T wn = (wc + dt * ((T)2 * (T)sc.alpha * s2 + dw * lw)) / ((T)1 + dt * (T)sc.beta * wc);
+  if (k >= d.o0 && k < d.o1) {   // reference C order over the global grid
+    const long long refi = ((long long)i * d.ny + j) * d.nzg + (k + d.kg0);
+    if (!isfinite(kn)) atomicMin(&rep->bad_index[0], refi);
+    if (!isfinite(wn)) atomicMin(&rep->bad_index[1], refi);
+  }
+  const T kf = kn > (T)1e-12 ? kn : (T)1e-12;
+  const T wf = wn > (T)1e-8 ? wn : (T)1e-8;
+  T omt = (T)sc.c_lim * sqrt(s2) * (T)sc.lim_scale;
+  omt = wf > omt ? wf : omt;
+  omt = omt > (T)1e-8 ? omt : (T)1e-8;
+  kout[c] = kf;
+  wout[c] = wf;
+  nut_prev[c] = nt;
+  nut[c] = kf / omt;
+}
+
 // After a non-finite k / omega (status 2) the reference has raised before it
 // assigned anything (turbulence.py:121-131): the state keeps the advected
 // k, omega (still in the step's upwind buffers) and the previous nu_t
