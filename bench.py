@@ -482,7 +482,25 @@ def run_b200(args):
         ev = evaluate_objective(dcomp, theta)
         torch.cuda.synchronize()
         t_eval = max_over_ranks(time.perf_counter() - t0)
+        # the two recipes the CPU baseline times (profiles/cpu_baselines_r2.json,
+        # scripts/cpu_baselines.py): channel_opt.json at its own settle 260 and
+        # C4 at 96x96x24 (settle 120), initial designs
+        small = {}
+        # channel_opt.json as recorded with the reference goldens (tests/golden)
+        chopt_doc = json.loads(str(np.load(os.path.join(ROOT, "tests", "golden", "cfg_chopt_sim_120.npz"))["doc"]))
+        for tag, sc_small in (("channel_opt_settle260", scenario_from_dict(chopt_doc)),
+                              ("c4_96x96x24_settle120", scenario_from_dict(
+                                  _sc.block_city_design(96, 96, 24, 2.0, seed=0, nb=6, dt=0.2, settle_steps=120)))):
+            c_small = CompiledScenario.compile(sc_small, dtype=torch.float32)
+            th = np.array([p.initial for p in sc_small.design])
+            evaluate_objective(c_small, th)
+            torch.cuda.synchronize()
+            t1 = time.perf_counter()
+            e_small = evaluate_objective(c_small, th)
+            torch.cuda.synchronize()
+            small[tag] = {"seconds_per_evaluation": time.perf_counter() - t1, "loss": e_small.loss}
         design = {"seconds_per_evaluation": t_eval, "evaluations_per_hour": 3600.0 * world / t_eval,
+                  "cpu_baseline_recipes": small,
                   "settle_steps": args.settle, "n_params": len(theta), "designs_in_parallel": world,
                   "loss": ev.loss,
                   "note": "C4 recipe (16 params, 6 regions) on the C3 city, dt %.2f; voxelize + settle steps + "

@@ -18,6 +18,15 @@ __global__ void k_report_init(DevReport* r) {
   r->bad_index[1] = 0x7fffffffffffffffLL;
 }
 
+// the step's report (written to rep_live by its kernels) into the ring slot
+// the device counts; enqueue_stage / slab solves write their slot directly
+// and only advance the count
+__global__ void k_report_commit(const DevReport* live, DevReport* ring, int* slot) {
+  ring[*slot] = *live;
+  *slot += 1;
+}
+__global__ void k_slot_bump(int* slot) { *slot += 1; }
+
 // Per-cell operator code (build_pressure_matrix, linalg.py:67-112):
 // bit 6 = unknown (interior_mask, grid.py:481-484); bit q (q = 0..5 for
 // +x,-x,+y,-y,+z,-z) = that neighbour is an unknown (off-diagonal -1/h^2 and
