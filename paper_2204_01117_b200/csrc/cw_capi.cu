@@ -784,9 +784,15 @@ static void st_diffuse(cw_ctx* c, const StepPtrs<T>& P, const cw_params* prm, cu
   T* cu[3] = {P.u, P.v, P.w};
   double cap = nu_stable<T>(c, prm->dt) - prm->nu;
   if (cap <= 0) cap = 0.0;                               // solver.py:195-201
+#ifdef CW_DIFFUSE_GENERIC   // developer comparison: the per-axis-loop kernel
   (k_diffuse<T><<<g3z(d.nx + 1, d.ny + 1, d.nz + 1), B3, 0, st>>>(
        d, (const T*)c->adv[0], (const T*)c->adv[1], (const T*)c->adv[2], cu[0], cu[1], cu[2], P.nut, (T)prm->dt,
        (T)prm->nu, (T)cap, c->gate), ++c->launches);
+#else
+  (k_diffuse_c<T><<<g3z(d.nx + 1, d.ny + 1, d.nz + 1), B3, 0, st>>>(
+       d, (const T*)c->adv[0], (const T*)c->adv[1], (const T*)c->adv[2], cu[0], cu[1], cu[2], P.nut, (T)prm->dt,
+       (T)prm->nu, (T)cap, c->gate), ++c->launches);
+#endif
 }
 
 template <typename T>

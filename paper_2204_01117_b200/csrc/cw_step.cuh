@@ -410,6 +410,74 @@ __global__ void k_diffuse(Dims d, const T* __restrict__ s0, const T* __restrict_
   }
 }
 
+// The same diffusion with straight-line access: the edge-replicated
+// neighbours are clamped indices (a clamped neighbour is the face itself:
+// (mid - 2 mid) + hi == hi - mid exactly, as the generic per-axis loop
+// computes), the three components of one (i, j, k) share the capped cell
+// viscosities they read (cells (i,j,k), (i-1,j,k), (i,j-1,k), (i,j,k-1)).
+// Same arithmetic as diffuse_face, axis sums in x, y, z order.
+template <typename T>
+__device__ __forceinline__ T lap_face(const T* __restrict__ a, int c, T mid, int sxm, int sxp, int sym, int syp,
+                                      int szm, int szp, T r20, T r21, T r22, bool hx, bool hy, bool hz) {
+  T lap = (T)0;
+  if (hx) lap += (a[c - sxm] - (T)2 * mid + a[c + sxp]) * r20;
+  if (hy) lap += (a[c - sym] - (T)2 * mid + a[c + syp]) * r21;
+  if (hz) lap += (a[c - szm] - (T)2 * mid + a[c + szp]) * r22;
+  return lap;
+}
+
+template <typename T>
+__global__ void k_diffuse_c(Dims d, const T* __restrict__ s0, const T* __restrict__ s1, const T* __restrict__ s2,
+                            T* __restrict__ d0, T* __restrict__ d1, T* __restrict__ d2, const T* __restrict__ nut,
+                            T dt, T nu, T cap, const int* gate) {
+  if (*gate) return;
+  const int i = (int)(blockIdx.x * ST_BX + threadIdx.x), j = (int)(blockIdx.y * ST_BY + threadIdx.y);
+  const int nx = d.nx, ny = d.ny, nz = d.nz;
+  if (i > nx || j > ny) return;
+  const T r20 = inv_h2<T>(d, 0), r21 = inv_h2<T>(d, 1), r22 = inv_h2<T>(d, 2);
+  const bool z3 = !d.is2d;
+#pragma unroll
+  for (int kz = 0; kz < CW_ZT; ++kz) {
+    const int k = (int)blockIdx.z * CW_ZT + kz;
+    if (k > nz) break;
+    // capped viscosities of the cells around (i, j, k), clamped to the grid
+    const int ci = min(i, nx - 1), cj = min(j, ny - 1), ck = min(k, nz - 1);
+    const T n0 = nu_eff(nut, d.cidx32(ci, cj, ck), nu, cap);
+    if (i < nx + 1 && j < ny && k < nz) {           // u face (nx+1, ny, nz)
+      const int ex = nx + 1, ey = ny;
+      const int c = (k * ey + j) * ex + i;
+      const T mid = s0[c];
+      const T lap = lap_face<T>(s0, c, mid, i > 0 ? 1 : 0, i < ex - 1 ? 1 : 0, j > 0 ? ex : 0, j < ey - 1 ? ex : 0,
+                                k > 0 ? ex * ey : 0, k < nz - 1 ? ex * ey : 0, r20, r21, r22, ex > 1, ey > 1,
+                                z3 && nz > 1);
+      const T a = nu_eff(nut, d.cidx32(max(i - 1, 0), j, k), nu, cap);
+      const T b = i < nx ? n0 : nu_eff(nut, d.cidx32(nx - 1, j, k), nu, cap);
+      d0[c] = mid + dt * ((T)0.5 * (a + b)) * lap;
+    }
+    if (i < nx && j < ny + 1 && k < nz) {           // v face (nx, ny+1, nz)
+      const int ex = nx, ey = ny + 1;
+      const int c = (k * ey + j) * ex + i;
+      const T mid = s1[c];
+      const T lap = lap_face<T>(s1, c, mid, i > 0 ? 1 : 0, i < ex - 1 ? 1 : 0, j > 0 ? ex : 0, j < ey - 1 ? ex : 0,
+                                k > 0 ? ex * ey : 0, k < nz - 1 ? ex * ey : 0, r20, r21, r22, ex > 1, ey > 1,
+                                z3 && nz > 1);
+      const T a = nu_eff(nut, d.cidx32(i, max(j - 1, 0), k), nu, cap);
+      const T b = j < ny ? n0 : nu_eff(nut, d.cidx32(i, ny - 1, k), nu, cap);
+      d1[c] = mid + dt * ((T)0.5 * (a + b)) * lap;
+    }
+    if (z3 && i < nx && j < ny && k < nz + 1) {     // w face (nx, ny, nz+1)
+      const int ex = nx, ey = ny, ez = nz + 1;
+      const int c = (k * ey + j) * ex + i;
+      const T mid = s2[c];
+      const T lap = lap_face<T>(s2, c, mid, i > 0 ? 1 : 0, i < ex - 1 ? 1 : 0, j > 0 ? ex : 0, j < ey - 1 ? ex : 0,
+                                k > 0 ? ex * ey : 0, k < ez - 1 ? ex * ey : 0, r20, r21, r22, ex > 1, ey > 1, ez > 1);
+      const T a = nu_eff(nut, d.cidx32(i, j, max(k - 1, 0)), nu, cap);
+      const T b = k < nz ? n0 : nu_eff(nut, d.cidx32(i, j, nz - 1), nu, cap);
+      d2[c] = mid + dt * ((T)0.5 * (a + b)) * lap;
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // porosity drag (solver.py:123-168)
 template <typename T>
