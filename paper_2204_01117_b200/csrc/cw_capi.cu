@@ -93,6 +93,9 @@ struct cw_ctx {
   unsigned* xbar = nullptr;    // this context's cross-slab barrier (used when it is the root)
   double* xval = nullptr;
   void* slab_args = nullptr;   // device array of per-slab kernel arguments (group launches)
+  // grow-only device scratch of cw_voxelize (cw_internal_scratch slots)
+  void* vscr[32] = {};
+  size_t vscr_n[32] = {};
   // painted-porosity layer for cw_voxelize (device buffers owned by the caller)
   const uint8_t* paint = nullptr;
   const uint8_t* paint_mask = nullptr;
@@ -148,6 +151,18 @@ extern "C" int cw_abi_version(void) { return CW_ABI_VERSION; }
 
 // shared with cw_voxel.cu
 int cw_internal_fail(int code, const char* msg) { return fail(code, msg); }
+void* cw_internal_scratch(cw_ctx* c, int slot, size_t bytes) {
+  if (slot < 0 || slot >= 32) return nullptr;
+  if (c->vscr_n[slot] < bytes) {
+    if (c->vscr[slot]) cudaFree(c->vscr[slot]);
+    c->vscr[slot] = nullptr;
+    c->vscr_n[slot] = 0;
+    const size_t grow = bytes + bytes / 4;   // a little headroom: designs change the object extents
+    if (cudaMalloc(&c->vscr[slot], grow) != cudaSuccess) { cudaGetLastError(); return nullptr; }
+    c->vscr_n[slot] = grow;
+  }
+  return c->vscr[slot];
+}
 int cw_internal_device(cw_ctx* c, int* nx, int* ny, int* nz, double* h, double* origin) {
   if (c->d.kg0 != 0 || c->d.nz != c->d.nzg)
     return fail(CW_ERR_INVALID, "voxelize on a whole-grid context and copy the slab's window");
@@ -396,6 +411,8 @@ extern "C" int cw_slab_info(cw_ctx* c, int* kg0, int* nz_local, int* own0, int* 
 
 extern "C" void cw_ctx_destroy(cw_ctx* c) {
   if (!c) return;
+  for (int q = 0; q < 32; ++q)
+    if (c->vscr[q]) cudaFree(c->vscr[q]);
   for (auto& e : c->gcache) cudaGraphExecDestroy(e.exec);
   c->gcache.clear();
   if (c->cap_stream) cudaStreamDestroy(c->cap_stream);

@@ -464,14 +464,13 @@ struct cw_ctx;
 extern int cw_internal_fail(int code, const char* msg);
 extern int cw_internal_device(cw_ctx* c, int* nx, int* ny, int* nz, double* h, double* origin);
 extern void cw_internal_paint(cw_ctx* c, const uint8_t** image, const uint8_t** mask, int* kmax, double* tree_lad);
+extern void* cw_internal_scratch(cw_ctx* c, int slot, size_t bytes);
 
 #define VCUDA(call)                                                                        \
   do {                                                                                     \
     cudaError_t e_ = (call);                                                               \
-    if (e_ != cudaSuccess) {                                                               \
-      for (void* p_ : allocs) cudaFree(p_);                                                \
+    if (e_ != cudaSuccess)                                                                 \
       return cw_internal_fail(CW_ERR_CUDA, (std::string(#call) + ": " + cudaGetErrorString(e_)).c_str()); \
-    }                                                                                      \
   } while (0)
 
 extern "C" int cw_voxelize(cw_ctx* ctx, const cw_object* objs, int n_obj, const double* verts, const int* tris,
@@ -487,7 +486,6 @@ extern "C" int cw_voxelize(cw_ctx* ctx, const cw_object* objs, int n_obj, const 
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const int dims[3] = {nx, ny, nz};
   const int sd = subdiv;
-  std::vector<void*> allocs;
 
   std::vector<VoxObj> vobj(n_obj);
   std::vector<MeshObj> meshes;
@@ -591,10 +589,12 @@ extern "C" int cw_voxelize(cw_ctx* ctx, const cw_object* objs, int n_obj, const 
   for (auto& v : vobj)
     if (!(v.is_mesh && v.mesh == -2)) live.push_back(v);
 
+  // device scratch from the context's grow-only arena (one slot per buffer):
+  // no cudaMalloc / cudaFree per design evaluation
+  int slot_n = 0;
   auto dalloc = [&](void** p, size_t b) -> cudaError_t {
-    cudaError_t e = cudaMalloc(p, std::max<size_t>(b, 16));
-    if (e == cudaSuccess) allocs.push_back(*p);
-    return e;
+    *p = cw_internal_scratch(ctx, slot_n++, std::max<size_t>(b, 16));
+    return *p ? cudaSuccess : cudaErrorMemoryAllocation;
   };
   VoxObj* d_obj = nullptr;
   MeshObj* d_mesh = nullptr;
@@ -623,30 +623,43 @@ extern "C" int cw_voxelize(cw_ctx* ctx, const cw_object* objs, int n_obj, const 
   if (!xs.empty()) VCUDA(cudaMemcpyAsync(d_xs, xs.data(), xs.size() * 8, cudaMemcpyHostToDevice, st));
   if (!ys.empty()) VCUDA(cudaMemcpyAsync(d_ys, ys.data(), ys.size() * 8, cudaMemcpyHostToDevice, st));
   if (!zs.empty()) VCUDA(cudaMemcpyAsync(d_zs, zs.data(), zs.size() * 8, cudaMemcpyHostToDevice, st));
-  // 1) column casts, 2) point casts for ambiguous columns
-  long long maxcol = 1;
-  for (const MeshObj& m : meshes) maxcol = std::max(maxcol, (long long)m.NS[0] * m.NS[1]);
-  VCUDA(dalloc((void**)&d_amb, maxcol));
-  VCUDA(dalloc((void**)&d_cols, maxcol * sizeof(int)));
+  // 1) column casts of every mesh, one read-back of all ambiguous-column
+  // flags, 2) point casts of the ambiguous columns of every mesh
+  std::vector<long long> col_off(meshes.size() + 1, 0);
+  for (size_t mi = 0; mi < meshes.size(); ++mi)
+    col_off[mi + 1] = col_off[mi] + (long long)meshes[mi].NS[0] * meshes[mi].NS[1];
+  const long long ncol_all = std::max(col_off.back(), 1LL);
+  VCUDA(dalloc((void**)&d_amb, ncol_all));
+  VCUDA(dalloc((void**)&d_cols, ncol_all * sizeof(int)));
   for (size_t mi = 0; mi < meshes.size(); ++mi) {
     const MeshObj& m = meshes[mi];
-    const long long ncol = (long long)m.NS[0] * m.NS[1];
+    const long long ncol = col_off[mi + 1] - col_off[mi];
     const int nb = (int)std::min<long long>((ncol + 127) / 128, 4096);
-    k_vox_columns<<<nb, 128, 0, st>>>(m, d_ct, d_xs, d_ys, d_zs, d_bits, d_amb, d_err);
+    k_vox_columns<<<nb, 128, 0, st>>>(m, d_ct, d_xs, d_ys, d_zs, d_bits, d_amb + col_off[mi], d_err);
     VCUDA(cudaGetLastError());
-    std::vector<uint8_t> amb(ncol);
-    VCUDA(cudaMemcpyAsync(amb.data(), d_amb, ncol, cudaMemcpyDeviceToHost, st));
+  }
+  if (!meshes.empty()) {
+    std::vector<uint8_t> amb(col_off.back());
+    VCUDA(cudaMemcpyAsync(amb.data(), d_amb, col_off.back(), cudaMemcpyDeviceToHost, st));
     VCUDA(cudaStreamSynchronize(st));
     std::vector<int> cols;
-    for (long long q = 0; q < ncol; ++q)
-      if (amb[q]) cols.push_back((int)q);
+    std::vector<long long> cbeg(meshes.size() + 1, 0);
+    for (size_t mi = 0; mi < meshes.size(); ++mi) {
+      for (long long q = col_off[mi]; q < col_off[mi + 1]; ++q)
+        if (amb[q]) cols.push_back((int)(q - col_off[mi]));
+      cbeg[mi + 1] = (long long)cols.size();
+    }
     if (!cols.empty()) {
       VCUDA(cudaMemcpyAsync(d_cols, cols.data(), cols.size() * sizeof(int), cudaMemcpyHostToDevice, st));
-      const long long np = (long long)cols.size() * m.NS[2];
-      k_vox_points<<<(int)std::min<long long>((np + 127) / 128, 4096), 128, 0, st>>>(
-          m, d_pt, d_xs, d_ys, d_zs, d_cols, (int)cols.size(), PRIMARY[0], PRIMARY[1], PRIMARY[2], d_bits, d_err);
-      VCUDA(cudaGetLastError());
-      VCUDA(cudaStreamSynchronize(st));
+      for (size_t mi = 0; mi < meshes.size(); ++mi) {
+        const long long nc = cbeg[mi + 1] - cbeg[mi];
+        if (nc == 0) continue;
+        const MeshObj& m = meshes[mi];
+        const long long np = nc * m.NS[2];
+        k_vox_points<<<(int)std::min<long long>((np + 127) / 128, 4096), 128, 0, st>>>(
+            m, d_pt, d_xs, d_ys, d_zs, d_cols + cbeg[mi], (int)nc, PRIMARY[0], PRIMARY[1], PRIMARY[2], d_bits, d_err);
+        VCUDA(cudaGetLastError());
+      }
     }
   }
   // 3) merge
@@ -668,7 +681,6 @@ extern "C" int cw_voxelize(cw_ctx* ctx, const cw_object* objs, int n_obj, const 
     VCUDA(cudaMemcpyAsync(h_err, d_err, sizeof(h_err), cudaMemcpyDeviceToHost, st));
     VCUDA(cudaStreamSynchronize(st));
   }
-  for (void* p : allocs) cudaFree(p);
   if (n_overlap) *n_overlap = h_err[2];
   if (h_err[0]) return cw_internal_fail(CW_ERR_GEOMETRY, "point unclassifiable by the primary cast (needs re-casts)");
   return CW_OK;

@@ -10,11 +10,14 @@ device sees bit-identical triangles.
 """
 from __future__ import annotations
 
+import hashlib
 from dataclasses import dataclass
 
 import numpy as np
 
 from .errors import ClassificationError, MeshError
+
+_CLOSED = set()   # triangle connectivities already shown to be closed
 
 __all__ = ["TriangleMesh", "Aabb", "mesh_aabb", "box_mesh", "cylinder_mesh", "load_obj",
            "MeshError", "ClassificationError"]
@@ -46,11 +49,15 @@ class TriangleMesh:
 
     def validate_closed(self):
         t = self.triangles
+        key = hashlib.sha1(np.ascontiguousarray(t).tobytes()).digest()
+        if key in _CLOSED:         # closedness depends on the connectivity only
+            return
         edges = np.sort(np.concatenate([t[:, [0, 1]], t[:, [1, 2]], t[:, [2, 0]]]), axis=1)
         _, counts = np.unique(edges, axis=0, return_counts=True)
         if np.any(counts != 2):
             raise MeshError(f"mesh is not closed: {int(np.sum(counts != 2))} edges not shared "
                             "by exactly 2 triangles")
+        _CLOSED.add(key)
 
     def translated(self, offset):
         return TriangleMesh(self.vertices + np.asarray(offset, dtype=float), self.triangles.copy())
