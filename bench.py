@@ -502,11 +502,12 @@ def run_b200(args):
         # the reference's default settle of 300 steps (optimize.py:46-48), timed
         # only: the C3 city at dt 0.2 leaves the reference model's stable window
         # after ~30 steps, so no parity claim rides on it
-        ddoc300 = _sc.block_city_design(256, 256, 64, 2.0, 0, 6, args.dt, settle_steps=300)
-        dcomp300 = CompiledScenario.compile(scenario_from_dict(ddoc300), dtype=torch.float32)
+        from paper_2204_01117_b200.optimize import ObjectiveSpec
+        spec300 = ObjectiveSpec.from_scenario(dcomp.scenario)
+        spec300.settle_steps = 300
         torch.cuda.synchronize()
         t1 = time.perf_counter()
-        evaluate_objective(dcomp300, theta)
+        evaluate_objective(dcomp, theta, spec300)
         torch.cuda.synchronize()
         t300 = max_over_ranks(time.perf_counter() - t1)
         design = {"seconds_per_evaluation": t_eval, "evaluations_per_hour": 3600.0 * world / t_eval,
