@@ -12,6 +12,7 @@ Fixtures (tests/golden/cfg_<name>.npz; arrays x-fastest, (nz, ny, nx[+1])):
   float64 field's SHA-256:
     c1_cuboid_64    C1 64x64x32 cuboid, dt 0.3, 200 steps (whole fields)
     c2_canyon_128   C2 128x128x64 canyon, dt 0.2, 20 steps (stride 16)
+    c2_canyon_128_500  the same over BASELINE.json's full 500 steps
     c3_city_256     C3 256x256x64 block city, dt 0.2, 25 steps (stride 64) --
                     the bench scene and horizon (bench.py times steps 6-25)
     bielefeld_120   src/scenarios/bielefeld_like.json, 120 steps (stride 4)
@@ -85,6 +86,7 @@ def c4_96():
 TRAJ = {
     "c1_cuboid_64": (lambda: scenes.cuboid(64, 64, 32, 2.0, 0.3), 200, 0, None),
     "c2_canyon_128": (lambda: scenes.canyon(128, 128, 64, 1.0, 0.2), 20, 16, None),
+    "c2_canyon_128_500": (lambda: scenes.canyon(128, 128, 64, 1.0, 0.2), 500, 16, None),
     "c3_city_256": (lambda: scenes.block_city(256, 256, 64, 2.0, 0, 6, 0.2), 25, 64, None),
     "bielefeld_120": (lambda: bundled("bielefeld_like.json"), 120, 4, None),
     "chopt_sim_120": (lambda: chopt(), 120, 0, "initial"),
