@@ -186,3 +186,21 @@ def test_step_defer_waits_for_late_fields():
     assert rep.pcg.iterations > 0
     for n in NAMES:
         assert torch.equal(work.fields[n], ref.fields[n]), n
+
+
+def test_robustness_check_matches_oracle():
+    """optimize.robustness_check (optimize.py:195-207): one evaluation per
+    wind-direction offset, against the oracle's evaluate_objective with the
+    rotated inlet profile."""
+    from oracle import citywind_oracle as co
+    from paper_2204_01117_b200.optimize import robustness_check
+    from paper_2204_01117_b200.scenario import CompiledScenario, scenario_from_dict
+    doc = _design_doc()
+    comp = CompiledScenario.compile(scenario_from_dict(doc))
+    theta = np.array([d["initial"] for d in doc["design"]])
+    rows = robustness_check(comp, theta, offsets_deg=(-10.0, 0.0, 10.0))
+    oc = oracle_compiled(doc)
+    for row in rows:
+        oloss, ospeeds = co.evaluate_objective(oc, theta, profile=oc.scene.inlet.rotated(row["offset_deg"]))
+        assert abs(row["loss"] - oloss) <= 1e-4 * abs(oloss), (row, oloss)
+        np.testing.assert_allclose(row["region_speeds"], ospeeds, rtol=1e-4)
