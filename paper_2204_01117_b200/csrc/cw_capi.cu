@@ -53,6 +53,7 @@ struct cw_ctx {
   // workspace (context precision)
   void *tk = nullptr, *tw = nullptr, *speed = nullptr;
   void *ahead[3] = {nullptr, nullptr, nullptr}, *adv[3] = {nullptr, nullptr, nullptr};
+  void *clip_mn[3] = {nullptr, nullptr, nullptr}, *clip_mx[3] = {nullptr, nullptr, nullptr};   // MacCormack clip range
   void *r0 = nullptr, *r1 = nullptr, *p0 = nullptr, *p1 = nullptr, *z = nullptr, *Ap = nullptr;
   void *lut = nullptr, *uzx = nullptr, *uzy = nullptr;
   uint8_t* code = nullptr;
@@ -326,6 +327,9 @@ static int ctx_create(const cw_grid* g, int kg0, int nzg, int own0, int own1, in
   int rc = CW_OK;
   rc |= alloc(&c->tk, cb); rc |= alloc(&c->tw, cb); rc |= alloc(&c->speed, cb);
   for (int a = 0; a < 3; ++a) { rc |= alloc(&c->ahead[a], fb[a]); rc |= alloc(&c->adv[a], fb[a]); }
+#if CW_MAC_CLIP
+  for (int a = 0; a < 3; ++a) { rc |= alloc(&c->clip_mn[a], fb[a]); rc |= alloc(&c->clip_mx[a], fb[a]); }
+#endif
   c->nxp = (d.nx + 15) / 16 * 16;
   c->ncellp = (long long)c->nxp * d.ny * d.nz;
   const size_t pb = c->ncellp * c->esz;
@@ -417,7 +421,7 @@ extern "C" void cw_ctx_destroy(cw_ctx* c) {
   c->gcache.clear();
   if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
   cudaSetDevice(c->device);
-  void* ptrs[] = {c->tk, c->tw, c->speed, c->ahead[0], c->ahead[1], c->ahead[2], c->adv[0], c->adv[1],
+  void* ptrs[] = {c->tk, c->tw, c->speed, c->ahead[0], c->ahead[1], c->ahead[2], c->clip_mn[0], c->clip_mn[1], c->clip_mn[2], c->clip_mx[0], c->clip_mx[1], c->clip_mx[2], c->adv[0], c->adv[1],
                   c->adv[2], c->r0, c->r1, c->p0, c->p1, c->z, c->Ap, c->xw, c->lut, c->uzx, c->uzy, c->code,
                   c->part, c->tags, c->bar, c->gate, c->rep, c->rep_live, c->slot_dev, c->reg_part, c->reg_cnt, c->reg_out, c->reg_cout,
                   c->flag, c->xbar, c->xval, c->slab_args};
@@ -785,13 +789,15 @@ static void st_advect(cw_ctx* c, const StepPtrs<T>& P, const cw_params* prm, T* 
   const bool turb = prm->turbulence != 0;    // upwind k, omega ride along in the predictor launch
   const bool timed = c->adv_timed < (int)c->aev.size() / 3;
   if (timed) cudaEventRecord(c->aev[3 * c->adv_timed], st);
+  const MacClip<T> clip{{(T*)c->clip_mn[0], (T*)c->clip_mn[1], (T*)c->clip_mn[2]},
+                        {(T*)c->clip_mx[0], (T*)c->clip_mx[1], (T*)c->clip_mx[2]}};
   (k_mac_predict<T><<<dim3((d.nx + 1 + ST_BX - 1) / ST_BX, (d.ny + 1 + ST_BY - 1) / ST_BY, (d.nz + 1 + ZT_MAC - 1) / ZT_MAC), B3, 0, st>>>(
        d, P.u, P.v, P.w, (T*)c->ahead[0], (T*)c->ahead[1], (T*)c->ahead[2], dt, (const T*)P.k, (const T*)P.om,
-       turb ? kout : (T*)nullptr, turb ? wout : (T*)nullptr, c->gate), ++c->launches);
+       turb ? kout : (T*)nullptr, turb ? wout : (T*)nullptr, clip, c->gate), ++c->launches);
   if (timed) cudaEventRecord(c->aev[3 * c->adv_timed + 1], st);
   (k_mac_correct<T><<<dim3((d.nx + 1 + ST_BX - 1) / ST_BX, (d.ny + 1 + ST_BY - 1) / ST_BY, (d.nz + 1 + ZT_MAC - 1) / ZT_MAC), B3, 0, st>>>(
        d, P.u, P.v, P.w, (const T*)c->ahead[0], (const T*)c->ahead[1], (const T*)c->ahead[2], (T*)c->adv[0],
-       (T*)c->adv[1], (T*)c->adv[2], dt, c->gate), ++c->launches);
+       (T*)c->adv[1], (T*)c->adv[2], dt, clip, c->gate), ++c->launches);
   if (timed) cudaEventRecord(c->aev[3 * c->adv_timed++ + 2], st);
 }
 

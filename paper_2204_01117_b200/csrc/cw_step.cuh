@@ -218,10 +218,23 @@ __device__ __forceinline__ void vel_nbhd(const Dims& d, const T* __restrict__ u,
   n.a[2] = (T)0.5 * (W0 + W1);
 }
 
+// The clip range of each face: the predictor's gather already visits the 8
+// corners whose min / max the corrector clips to (advection.py:130-134 takes
+// `ahead, mn, mx` from that one sample), so it stores them (CW_MAC_CLIP=1) and
+// the corrector reads two values instead of gathering the same corners again.
+#ifndef CW_MAC_CLIP
+#define CW_MAC_CLIP 1
+#endif
+template <typename T>
+struct MacClip {
+  T* mn[3];
+  T* mx[3];
+};
+
 // the predictor for one face given the face-point velocity
 template <typename T>
 __device__ __forceinline__ void mac_predict_face_v(const Dims& d, int comp, const T* arr, T* ahead, T dt, int i,
-                                                   int j, int k, T us, T vs, T ws) {
+                                                   int j, int k, T us, T vs, T ws, const MacClip<T>& clip) {
   int ex, ey, ez;
   comp_extent(d, comp, ex, ey, ez);
   float fox, foy, foz;
@@ -229,22 +242,32 @@ __device__ __forceinline__ void mac_predict_face_v(const Dims& d, int comp, cons
   const T ox = (T)fox, oy = (T)foy, oz = (T)foz;
   const int c = ((int)k * ey + j) * ex + i;
   const T X = (T)i + ox, Y = (T)j + oy, Z = (T)(k + d.kg0) + oz;   // global z (z-slab windows)
+#if CW_MAC_CLIP
+  // the corrector's expressions for the trace (X - s with s rounded on its own)
+  const T sx = dt * us * inv_h<T>(d, 0), sy = dt * vs * inv_h<T>(d, 1), sz = dt * ws * inv_h<T>(d, 2);
+  const T bx = X - sx, by = Y - sy, bz = Z - sz;
+  T mn, mx;
+  ahead[c] = gather<T>(arr, ex, ey, ez, bx - ox, by - oy, bz - oz, &mn, &mx, d.kg0);
+  clip.mn[comp][c] = mn;
+  clip.mx[comp][c] = mx;
+#else
   const T bx = X - dt * us * inv_h<T>(d, 0), by = Y - dt * vs * inv_h<T>(d, 1), bz = Z - dt * ws * inv_h<T>(d, 2);
   ahead[c] = gather<T>(arr, ex, ey, ez, bx - ox, by - oy, bz - oz, nullptr, nullptr, d.kg0);
+#endif
 }
 
 // One thread per (i, j, k) of the union of the face extents handles the u, v
 // and w faces there (all three read the same pre-advection velocity).
 template <typename T>
 __device__ __forceinline__ void mac_predict_face(const Dims& d, int comp, const T* u, const T* v, const T* w,
-                                                 T* ahead, T dt, int i, int j, int k) {
+                                                 T* ahead, T dt, int i, int j, int k, const MacClip<T>& clip) {
   int ex, ey, ez;
   comp_extent(d, comp, ex, ey, ez);
   if (i >= ex || j >= ey || k >= ez) return;
   const T* arr = comp == 0 ? u : (comp == 1 ? v : w);
   T us, vs, ws;
   face_velocity<T>(d, comp, u, v, w, i, j, k, us, vs, ws);
-  mac_predict_face_v<T>(d, comp, arr, ahead, dt, i, j, k, us, vs, ws);
+  mac_predict_face_v<T>(d, comp, arr, ahead, dt, i, j, k, us, vs, ws, clip);
 }
 
 // the predictor launch also runs the upwind step of k and omega (cells,
@@ -258,7 +281,7 @@ template <typename T>
 __global__ void __launch_bounds__(256, CW_MAC_PRED_MINB) k_mac_predict(Dims d, const T* __restrict__ u, const T* __restrict__ v,
                               const T* __restrict__ w, T* __restrict__ a0, T* __restrict__ a1,
                               T* __restrict__ a2, T dt, const T* __restrict__ kin, const T* __restrict__ win,
-                              T* __restrict__ kout, T* __restrict__ wout, const int* gate) {
+                              T* __restrict__ kout, T* __restrict__ wout, MacClip<T> clip, const int* gate) {
   if (*gate) return;
   const int i = (int)(blockIdx.x * ST_BX + threadIdx.x), j = (int)(blockIdx.y * ST_BY + threadIdx.y);
   if (i > d.nx || j > d.ny) return;
@@ -270,22 +293,23 @@ __global__ void __launch_bounds__(256, CW_MAC_PRED_MINB) k_mac_predict(Dims d, c
       VelNbhd<T> n;
       vel_nbhd<T>(d, u, v, w, i, j, k, n);
       if (kout) upwind_cell_a<T>(d, n.a, kin, win, kout, wout, dt, i, j, k);
-      mac_predict_face_v<T>(d, 0, u, a0, dt, i, j, k, n.fu[0], n.fv[0], n.fw[0]);
-      mac_predict_face_v<T>(d, 1, v, a1, dt, i, j, k, n.fu[1], n.fv[1], n.fw[1]);
-      mac_predict_face_v<T>(d, 2, w, a2, dt, i, j, k, n.fu[2], n.fv[2], n.fw[2]);
+      mac_predict_face_v<T>(d, 0, u, a0, dt, i, j, k, n.fu[0], n.fv[0], n.fw[0], clip);
+      mac_predict_face_v<T>(d, 1, v, a1, dt, i, j, k, n.fu[1], n.fv[1], n.fw[1], clip);
+      mac_predict_face_v<T>(d, 2, w, a2, dt, i, j, k, n.fu[2], n.fv[2], n.fw[2], clip);
       continue;
     }
     if (kout) upwind_cell<T>(d, u, v, w, kin, win, kout, wout, dt, i, j, k);
-    mac_predict_face<T>(d, 0, u, v, w, a0, dt, i, j, k);
-    mac_predict_face<T>(d, 1, u, v, w, a1, dt, i, j, k);
-    if (!d.is2d) mac_predict_face<T>(d, 2, u, v, w, a2, dt, i, j, k);
+    mac_predict_face<T>(d, 0, u, v, w, a0, dt, i, j, k, clip);
+    mac_predict_face<T>(d, 1, u, v, w, a1, dt, i, j, k, clip);
+    if (!d.is2d) mac_predict_face<T>(d, 2, u, v, w, a2, dt, i, j, k, clip);
   }
 }
 
 // the corrector for one face given the face-point velocity
 template <typename T>
 __device__ __forceinline__ void mac_correct_face_v(const Dims& d, int comp, const T* arr, const T* ahead, T* out,
-                                                   T dt, int i, int j, int k, T us, T vs, T ws, T self) {
+                                                   T dt, int i, int j, int k, T us, T vs, T ws, T self,
+                                                   const MacClip<T>& clip) {
   int ex, ey, ez;
   comp_extent(d, comp, ex, ey, ez);
   float fox, foy, foz;
@@ -295,8 +319,14 @@ __device__ __forceinline__ void mac_correct_face_v(const Dims& d, int comp, cons
   const T X = (T)i + ox, Y = (T)j + oy, Z = (T)(k + d.kg0) + oz;   // global z (z-slab windows)
   T mn, mx;
   const T sx = dt * us * inv_h<T>(d, 0), sy = dt * vs * inv_h<T>(d, 1), sz = dt * ws * inv_h<T>(d, 2);
+#if CW_MAC_CLIP
+  mn = clip.mn[comp][c];
+  mx = clip.mx[comp][c];
+  (void)arr;
+#else
   const T bx = X - sx, by = Y - sy, bz = Z - sz;
   (void)gather<T>(arr, ex, ey, ez, bx - ox, by - oy, bz - oz, &mn, &mx, d.kg0);
+#endif
   const T fx = X + sx, fy = Y + sy, fz = Z + sz;
   const T back = gather<T>(ahead, ex, ey, ez, fx - ox, fy - oy, fz - oz, nullptr, nullptr, d.kg0);
   T cor = ahead[c] + (T)0.5 * (self - back);   // self = arr[c]
@@ -307,14 +337,15 @@ __device__ __forceinline__ void mac_correct_face_v(const Dims& d, int comp, cons
 
 template <typename T>
 __device__ __forceinline__ void mac_correct_face(const Dims& d, int comp, const T* u, const T* v, const T* w,
-                                                 const T* ahead, T* out, T dt, int i, int j, int k) {
+                                                 const T* ahead, T* out, T dt, int i, int j, int k,
+                                                 const MacClip<T>& clip) {
   int ex, ey, ez;
   comp_extent(d, comp, ex, ey, ez);
   if (i >= ex || j >= ey || k >= ez) return;
   const T* arr = comp == 0 ? u : (comp == 1 ? v : w);
   T us, vs, ws;
   face_velocity<T>(d, comp, u, v, w, i, j, k, us, vs, ws);
-  mac_correct_face_v<T>(d, comp, arr, ahead, out, dt, i, j, k, us, vs, ws, arr[((int)k * ey + j) * ex + i]);
+  mac_correct_face_v<T>(d, comp, arr, ahead, out, dt, i, j, k, us, vs, ws, arr[((int)k * ey + j) * ex + i], clip);
 }
 
 #ifndef CW_MAC_CORR_MINB
@@ -327,7 +358,7 @@ template <typename T>
 __global__ void __launch_bounds__(256, CW_MAC_CORR_MINB) k_mac_correct(Dims d, const T* __restrict__ u, const T* __restrict__ v,
                               const T* __restrict__ w, const T* __restrict__ a0, const T* __restrict__ a1,
                               const T* __restrict__ a2, T* __restrict__ o0, T* __restrict__ o1,
-                              T* __restrict__ o2, T dt, const int* gate) {
+                              T* __restrict__ o2, T dt, MacClip<T> clip, const int* gate) {
   if (*gate) return;
   const int i = (int)(blockIdx.x * ST_BX + threadIdx.x), j = (int)(blockIdx.y * ST_BY + threadIdx.y);
   if (i > d.nx || j > d.ny) return;
@@ -338,14 +369,14 @@ __global__ void __launch_bounds__(256, CW_MAC_CORR_MINB) k_mac_correct(Dims d, c
     if (!d.is2d && i < d.nx && j < d.ny && k < d.nz) {   // interior: shared velocity loads
       VelNbhd<T> n;
       vel_nbhd<T>(d, u, v, w, i, j, k, n);
-      mac_correct_face_v<T>(d, 0, u, a0, o0, dt, i, j, k, n.fu[0], n.fv[0], n.fw[0], n.fu[0]);
-      mac_correct_face_v<T>(d, 1, v, a1, o1, dt, i, j, k, n.fu[1], n.fv[1], n.fw[1], n.fv[1]);
-      mac_correct_face_v<T>(d, 2, w, a2, o2, dt, i, j, k, n.fu[2], n.fv[2], n.fw[2], n.fw[2]);
+      mac_correct_face_v<T>(d, 0, u, a0, o0, dt, i, j, k, n.fu[0], n.fv[0], n.fw[0], n.fu[0], clip);
+      mac_correct_face_v<T>(d, 1, v, a1, o1, dt, i, j, k, n.fu[1], n.fv[1], n.fw[1], n.fv[1], clip);
+      mac_correct_face_v<T>(d, 2, w, a2, o2, dt, i, j, k, n.fu[2], n.fv[2], n.fw[2], n.fw[2], clip);
       continue;
     }
-    mac_correct_face<T>(d, 0, u, v, w, a0, o0, dt, i, j, k);
-    mac_correct_face<T>(d, 1, u, v, w, a1, o1, dt, i, j, k);
-    if (!d.is2d) mac_correct_face<T>(d, 2, u, v, w, a2, o2, dt, i, j, k);
+    mac_correct_face<T>(d, 0, u, v, w, a0, o0, dt, i, j, k, clip);
+    mac_correct_face<T>(d, 1, u, v, w, a1, o1, dt, i, j, k, clip);
+    if (!d.is2d) mac_correct_face<T>(d, 2, u, v, w, a2, o2, dt, i, j, k, clip);
   }
 }
 
