@@ -874,7 +874,8 @@ static void st_turb(cw_ctx* c, const StepPtrs<T>& P, const cw_params* prm, const
                        st>>>(c->d, P.u, P.v, P.w, kin, win, P.k, P.om, P.nut, (T*)c->speed, sc, rep, c->gate),
    ++c->launches);
 #else
-  (k_turbulence_c<T><<<g3(c->d.nx, c->d.ny, c->d.nz), B3, 0, st>>>(c->d, P.u, P.v, P.w, kin, win, P.k, P.om, P.nut,
+  (k_turbulence_c<T><<<dim3((c->d.nx + ST_BX - 1) / ST_BX, (c->d.ny + ST_BY - 1) / ST_BY,
+                            (c->d.nz + TURB_ZT - 1) / TURB_ZT), B3, 0, st>>>(c->d, P.u, P.v, P.w, kin, win, P.k, P.om, P.nut,
                                                                    (T*)c->speed, sc, rep, c->gate),
    ++c->launches);
 #endif

@@ -1189,6 +1189,11 @@ __global__ void __launch_bounds__(256) k_turbulence_z(Dims d, const T* __restric
 // (f - 2 f) + f_p == f_p - f exactly), so the interior and the edges run the
 // same instructions; the one-sided gradient keeps its 1/h, the central one
 // its 1/(2h).  Same arithmetic as k_turbulence, far fewer instructions.
+#ifndef CW_TURB_ZT
+#define CW_TURB_ZT 1
+#endif
+constexpr int TURB_ZT = CW_TURB_ZT;   // planes per thread of k_turbulence_c
+
 template <typename T>
 __global__ void __launch_bounds__(256) k_turbulence_c(Dims d, const T* __restrict__ u, const T* __restrict__ v,
                                                       const T* __restrict__ w, const T* __restrict__ kin,
@@ -1198,8 +1203,11 @@ __global__ void __launch_bounds__(256) k_turbulence_c(Dims d, const T* __restric
                                                       const int* gate) {
   if (*gate) return;
   const int i = (int)(blockIdx.x * ST_BX + threadIdx.x), j = (int)(blockIdx.y * ST_BY + threadIdx.y);
-  const int k = (int)blockIdx.z;
-  if (i >= d.nx || j >= d.ny || k >= d.nz) return;
+  if (i >= d.nx || j >= d.ny) return;
+#pragma unroll
+  for (int kz = 0; kz < TURB_ZT; ++kz) {
+  const int k = (int)blockIdx.z * TURB_ZT + kz;
+  if (k >= d.nz) break;
   const T dt = (T)sc.dt, nu = (T)sc.nu, cap = (T)sc.cap_turb;
   const T rh0 = inv_h<T>(d, 0), rh1 = inv_h<T>(d, 1), rh2 = inv_h<T>(d, 2);
   const int nx = d.nx, ny = d.ny, nz = d.nz;
@@ -1270,6 +1278,7 @@ __global__ void __launch_bounds__(256) k_turbulence_c(Dims d, const T* __restric
   wout[c] = wf;
   nut_prev[c] = nt;
   nut[c] = kf / omt;
+  }
 }
 
 // After a non-finite k / omega (status 2) the reference has raised before it
