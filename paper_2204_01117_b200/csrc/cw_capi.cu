@@ -6,6 +6,8 @@
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 
+#include <cub/cub.cuh>
+
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
@@ -132,6 +134,11 @@ struct cw_ctx {
   BcEntry* bc_list[7] = {};   // 6 outlet sides in the reference's order, then inlet/wall
   int bc_n[7] = {};
   int* bc_count = nullptr;
+  // their composition (k_bc_compose_*): one k_bc_replay launch per pass;
+  // bc_nf < 0: not composed (CW_BC_COMPOSE=0, or too many ordered writes)
+  BcOp* bc_ops = nullptr;     // bc_nf independent writes, then bc_no ordered ones
+  int bc_nf = -1, bc_no = 0;
+  size_t bc_cap[7] = {}, bc_ops_cap = 0;   // grow-only capacities (bytes)
   // stage timing
   bool timing = false;
   // one-shot waits of the next enqueued step (cw_step_defer): first use of nu_t / p
@@ -430,6 +437,7 @@ extern "C" void cw_ctx_destroy(cw_ctx* c) {
   for (int q = 0; q < 7; ++q)
     if (c->bc_list[q]) cudaFree(c->bc_list[q]);
   if (c->bc_count) cudaFree(c->bc_count);
+  if (c->bc_ops) cudaFree(c->bc_ops);
   if (c->ev_made)
     for (auto& e : c->ev) cudaEventDestroy(e);
   for (auto& e : c->pev) cudaEventDestroy(e);
@@ -596,14 +604,30 @@ static void drop_graphs(cw_ctx* c) {
   c->gcache.clear();
 }
 
+static void compose_bc(cw_ctx* c, cudaStream_t st);
+
+// grow-only device buffer (the boundary lists and their composition are
+// rebuilt for every design's labels: no cudaFree / cudaMalloc churn)
+static bool grow(void** p, size_t* cap, size_t need) {
+  if (*cap >= need && *p) return true;
+  if (*p) cudaFree(*p);
+  *p = nullptr;
+  *cap = 0;
+  const size_t n = need + need / 4;
+  if (cudaMalloc(p, n) != cudaSuccess) {
+    cudaGetLastError();
+    *p = nullptr;
+    return false;
+  }
+  *cap = n;
+  return true;
+}
+
 static int build_bc_lists(cw_ctx* c, const int8_t* lab, long long ver, cudaStream_t st) {
   const Dims& d = c->d;
-  drop_graphs(c);   // captured steps reference the lists freed below
-  for (int q = 0; q < 7; ++q) {
-    if (c->bc_list[q]) cudaFree(c->bc_list[q]);
-    c->bc_list[q] = nullptr;
-    c->bc_n[q] = 0;
-  }
+  drop_graphs(c);   // captured steps reference the lists rebuilt below
+  c->bc_nf = -1;
+  for (int q = 0; q < 7; ++q) c->bc_n[q] = 0;
   c->bc_lab = nullptr;
   if (!c->bc_count && alloc((void**)&c->bc_count, 8 * sizeof(int)) != CW_OK) return 1;
   const int sides = d.is2d ? 4 : 6;
@@ -623,7 +647,7 @@ static int build_bc_lists(cw_ctx* c, const int8_t* lab, long long ver, cudaStrea
   if (cudaStreamSynchronize(st) != cudaSuccess) return 1;
   // pass 2: the entries
   for (int q = 0; q < 7; ++q)
-    if (cnt[q] > 0 && alloc((void**)&c->bc_list[q], (size_t)cnt[q] * sizeof(BcEntry)) != CW_OK) return 1;
+    if (cnt[q] > 0 && !grow((void**)&c->bc_list[q], &c->bc_cap[q], (size_t)cnt[q] * sizeof(BcEntry))) return 1;
   if (cudaMemsetAsync(c->bc_count, 0, 8 * sizeof(int), st) != cudaSuccess) return 1;
   for (int s = 0; s < sides; ++s)
     if (cnt[s] > 0) side_launch(s, c->bc_list[s], cnt[s]);
@@ -633,7 +657,85 @@ static int build_bc_lists(cw_ctx* c, const int8_t* lab, long long ver, cudaStrea
   for (int q = 0; q < 7; ++q) c->bc_n[q] = cnt[q];
   c->bc_lab = lab;
   c->bc_ver = ver;
+  compose_bc(c, st);   // on failure the ordered list launches stay in use
   return 0;
+}
+
+// The lists' composition for k_bc_replay (see k_bc_compose_expand).  Sets
+// bc_ops / bc_nf / bc_no, or leaves bc_nf = -1.
+static void compose_bc(cw_ctx* c, cudaStream_t st) {
+  c->bc_nf = -1;
+  c->bc_no = 0;
+  const char* env = getenv("CW_BC_COMPOSE");
+  if (env && env[0] == '0') return;
+  long long base[7], tot = 0;
+  for (int q = 0; q < 7; ++q) {
+    base[q] = tot;
+    tot += 4LL * c->bc_n[q];
+  }
+  if (tot == 0) {
+    c->bc_nf = 0;
+    return;
+  }
+  BcFieldOff fo;
+  const long long sz[7] = {c->nu_, c->nv_, c->nw_, c->ncell, c->ncell, c->ncell, c->ncell};
+  fo.off[0] = 0;
+  for (int f = 0; f < 7; ++f) fo.off[f + 1] = fo.off[f] + sz[f];
+  constexpr int ORD_CAP = 256 * BC_ORD_PER_THREAD;
+  // temporaries in the context's grow-only scratch (slots 24..29; cw_voxelize uses the low slots)
+  int* wmap = (int*)cw_internal_scratch(c, 29, (size_t)fo.off[7] * sizeof(int));
+  BcOp* ops = (BcOp*)cw_internal_scratch(c, 28, (size_t)tot * sizeof(BcOp));
+  BcOp* outp = (BcOp*)cw_internal_scratch(c, 27, (size_t)(tot + ORD_CAP) * sizeof(BcOp));
+  uint8_t* flag = (uint8_t*)cw_internal_scratch(c, 26, (size_t)tot);
+  if (!wmap || !ops || !outp || !flag) return;
+  int nc[2] = {0, 0};
+  bool ok = cudaMemsetAsync(wmap, 0xff, (size_t)fo.off[7] * sizeof(int), st) == cudaSuccess &&
+            cudaMemsetAsync(c->bc_count, 0, 2 * sizeof(int), st) == cudaSuccess;
+  const int grid = 4 * c->num_sms;
+  for (int q = 0; ok && q < 7; ++q) {
+    if (c->bc_n[q] == 0) continue;
+    k_bc_compose_expand<<<std::min(nblk(c->bc_n[q]), grid), 256, 0, st>>>(c->bc_list[q], c->bc_n[q], q == 6, ops,
+                                                                          base[q], wmap, fo);
+    k_bc_compose_claim<<<std::min(nblk(4LL * c->bc_n[q]), grid), 256, 0, st>>>(ops, base[q], 4LL * c->bc_n[q], wmap,
+                                                                              fo);
+  }
+  k_bc_compose_final<<<std::min(nblk(tot), grid), 256, 0, st>>>(ops, tot, wmap, fo, flag);
+  k_bc_compose_conflict<<<std::min(nblk(tot), grid), 256, 0, st>>>(ops, tot, wmap, fo, flag);
+  k_bc_compose_compact<<<std::min(nblk(tot), grid), 256, 0, st>>>(ops, tot, flag, outp, outp + tot, ORD_CAP,
+                                                                   c->bc_count);
+  ok = ok && cudaGetLastError() == cudaSuccess &&
+       cudaMemcpyAsync(nc, c->bc_count, sizeof(nc), cudaMemcpyDeviceToHost, st) == cudaSuccess &&
+       cudaStreamSynchronize(st) == cudaSuccess;
+  if (!ok || nc[1] > ORD_CAP) {
+    cudaGetLastError();
+    return;
+  }
+  const int n = nc[0];
+  if (n + nc[1] > 0) {
+    ok = grow((void**)&c->bc_ops, &c->bc_ops_cap, (size_t)(n + nc[1]) * sizeof(BcOp)) &&
+         cudaMemcpyAsync(c->bc_ops + n, outp + tot, (size_t)nc[1] * sizeof(BcOp), cudaMemcpyDeviceToDevice, st) ==
+             cudaSuccess;
+    if (ok && n > 0) {   // the independent writes sorted by (field, destination): coalesced replay
+      size_t tmp_n = 0;
+      ok = cub::DeviceRadixSort::SortPairs(nullptr, tmp_n, (unsigned long long*)nullptr, (unsigned long long*)nullptr,
+                                           (int*)nullptr, (int*)nullptr, n, 0, 35, st) == cudaSuccess;
+      unsigned long long* keys = (unsigned long long*)cw_internal_scratch(c, 25, 2 * (size_t)n * sizeof(unsigned long long));
+      int* idx = (int*)cw_internal_scratch(c, 24, 2 * (size_t)n * sizeof(int));
+      void* tmp = cw_internal_scratch(c, 23, std::max<size_t>(tmp_n, 16));
+      ok = ok && keys && idx && tmp;
+      if (ok) {
+        k_bc_compose_keys<<<std::min(nblk(n), grid), 256, 0, st>>>(outp, n, keys, idx);
+        ok = cub::DeviceRadixSort::SortPairs(tmp, tmp_n, keys, keys + n, idx, idx + n, n, 0, 35, st) == cudaSuccess;
+        k_bc_compose_gather<<<std::min(nblk(n), grid), 256, 0, st>>>(outp, idx + n, n, c->bc_ops);
+        ok = ok && cudaGetLastError() == cudaSuccess;
+      }
+    }
+  }
+  if (ok) {
+    c->bc_nf = n;
+    c->bc_no = nc[1];
+  }
+  cudaGetLastError();
 }
 
 template <typename T>
@@ -641,6 +743,14 @@ static void launch_bc(cw_ctx* c, BcFields<T> F, const int8_t* lab, long long ver
                       cudaStream_t st) {
   const Dims& d = c->d;
   if (ver != 0 && ((c->bc_lab == lab && c->bc_ver == ver) || build_bc_lists(c, lab, ver, st) == 0)) {
+    if (c->bc_nf >= 0) {   // the composed pass: one launch
+      if (c->bc_nf + c->bc_no > 0)
+        (k_bc_replay<T><<<1 + std::max(1, std::min(nblk(c->bc_nf), 8 * c->num_sms)), 256, 0, st>>>(
+             F, c->bc_ops, c->bc_nf, c->bc_ops + c->bc_nf, c->bc_no, (const T*)c->uzx, (const T*)c->uzy,
+             (T)prm->k_in, (T)prm->omega_in, (T)(prm->k_in / prm->omega_in), c->gate),
+         ++c->launches);
+      return;
+    }
     for (int q = 0; q < 6; ++q)
       if (c->bc_n[q] > 0)
         (k_bc_copy_list<T><<<nblk(c->bc_n[q]), 256, 0, st>>>(F, c->bc_list[q], c->bc_n[q], c->gate), ++c->launches);

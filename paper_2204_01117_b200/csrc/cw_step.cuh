@@ -511,20 +511,40 @@ __global__ void k_diffuse_c(Dims d, const T* __restrict__ s0, const T* __restric
 
 // ---------------------------------------------------------------------------
 // porosity drag (solver.py:123-168)
+__device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ float fma_rn(float a, float b, float c) { return __fmaf_rn(a, b, c); }
+__device__ __forceinline__ double fma_rn(double a, double b, double c) { return __fma_rn(a, b, c); }
+
+// |u| at the centre of cell (i, j, k) (solver.py:160-161), roundings explicit
+template <typename T>
+__device__ __forceinline__ T cell_speed_at(const Dims& d, const T* __restrict__ u, const T* __restrict__ v,
+                                           const T* __restrict__ w, int i, int j, int k) {
+  const int c = d.cidx32(i, j, k);
+  const int ui = ((int)k * d.ny + j) * (d.nx + 1) + i;
+  const int vi = ((int)k * (d.ny + 1) + j) * d.nx + i;
+  const T uc = (T)0.5 * (u[ui] + u[ui + 1]);
+  const T vc = (T)0.5 * (v[vi] + v[vi + d.nx]);
+  const T wc = (T)0.5 * (w[c] + w[c + (int)d.nx * d.ny]);
+  // np.sum(vel * vel, axis=-1) with the two fused multiply-adds nvcc chose
+  // for uc*uc + vc*vc + wc*wc (the arithmetic the parity runs validated)
+  return sqrt(fma_rn(wc, wc, fma_rn(vc, vc, mul_rn(uc, uc))));
+}
+
 template <typename T>
 __global__ void k_cell_speed(Dims d, const T* __restrict__ u, const T* __restrict__ v,
                              const T* __restrict__ w, T* __restrict__ speed, const int* gate) {
   if (*gate) return;
   CW_IJK(d.nx, d.ny, d.nz, inb);
-  if (inb) {
-    const int c = d.cidx32(i, j, k);
-    const int ui = ((int)k * d.ny + j) * (d.nx + 1) + i;
-    const int vi = ((int)k * (d.ny + 1) + j) * d.nx + i;
-    const T uc = (T)0.5 * (u[ui] + u[ui + 1]);
-    const T vc = (T)0.5 * (v[vi] + v[vi + d.nx]);
-    const T wc = (T)0.5 * (w[c] + w[c + (int)d.nx * d.ny]);
-    speed[c] = sqrt(uc * uc + vc * vc + wc * wc);
-  }
+  if (inb) speed[d.cidx32(i, j, k)] = cell_speed_at<T>(d, u, v, w, i, j, k);
+}
+
+// max(0, 1 - dt g_face s_face) with the roundings nvcc chose for the plain
+// expression (dt*g rounded, then one fused multiply-add)
+template <typename T>
+__device__ __forceinline__ T drag_fac(T gf, T sf, T dt) {
+  const T fac = fma_rn(sf, -mul_rn(dt, gf), (T)1);
+  return fac > (T)0 ? fac : (T)0;
 }
 
 template <typename T>
@@ -541,11 +561,7 @@ __device__ __forceinline__ void drag_face(const Dims& d, int comp, T* __restrict
     const int lo = d.cidx32(p[0], p[1], p[2]);
     p[comp] = clampi(f, 0, nc - 1);
     const int hi = d.cidx32(p[0], p[1], p[2]);
-    const T gf = (T)0.5 * (g[lo] + g[hi]);
-    const T sf = (T)0.5 * (speed[lo] + speed[hi]);
-    T fac = (T)1 - dt * gf * sf;
-    fac = fac > (T)0 ? fac : (T)0;
-    arr[c] *= fac;
+    arr[c] *= drag_fac<T>((T)0.5 * (g[lo] + g[hi]), (T)0.5 * (speed[lo] + speed[hi]), dt);
   }
 }
 
@@ -800,6 +816,193 @@ __global__ void k_bc_set_list(BcFields<T> F, const BcEntry* __restrict__ e, int 
       T* a = x.arr == 0 ? F.u : (x.arr == 1 ? F.v : F.w);
       a[x.dst] = x.src < 0 ? (T)0 : (x.arr == 0 ? uz_dirx[x.src] : (x.arr == 1 ? uz_diry[x.src] : (T)0));
     }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// One boundary pass as ONE launch.  The lists above are replayed in order
+// (sides, then inlet/wall), so a later side can overwrite an earlier side's
+// write or read it (edges and corners where two outlet sides meet).  Their
+// composition is fixed by the labels: every location a pass writes ends up
+// holding either the pass-start value of one location, a zero, an inlet
+// profile value or an inlet scalar.  k_bc_compose_* derive that composition
+// once per labels array (per list, in the reference's order: resolve each
+// entry's source through the writer table of the lists before it, then claim
+// its destinations); k_bc_replay then performs only the final writes.  A
+// final write whose source location is itself finally written (or whose
+// destination is such a source) must read before the other writes: those
+// few (edge lines) go to block 0, which loads all their values, barriers and
+// stores; every other write is independent of all the rest.  Pure copies and
+// constants: the fields equal the ordered replay bit for bit.
+// Expanded op: one field per op (fields 0 u, 1 v, 2 w, 3 k, 4 omega, 5 nu_t, 6 p).
+enum BcKind { BK_ORIG = 0, BK_ZERO = 1, BK_INX = 2, BK_INY = 3, BK_KIN = 4, BK_OMIN = 5, BK_NUTIN = 6 };
+struct BcOp {
+  int fk;    // field | kind << 3; -1: unused slot
+  int dst;
+  int src;   // BK_ORIG: source index in the same field; BK_INX / BK_INY: profile row
+};
+struct BcFieldOff {
+  long long off[8];   // writer-table offset of each field (off[7] = table size)
+};
+
+// expand list entries (4 op slots per entry) and resolve their sources
+// through the writers of the earlier lists
+__global__ void k_bc_compose_expand(const BcEntry* __restrict__ e, int n, bool set_list, BcOp* ops, long long base,
+                                    const int* __restrict__ wmap, BcFieldOff fo) {
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
+    const BcEntry x = e[t];
+    BcOp* o = ops + base + 4 * (long long)t;
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+      BcOp op{-1, x.dst, 0};
+      int f = -1, kind = BK_ORIG, src = x.src;
+      if (x.arr < 3) {
+        if (s == 0) {
+          f = x.arr;
+          if (set_list) {
+            kind = x.src < 0 || x.arr == 2 ? BK_ZERO : (x.arr == 0 ? BK_INX : BK_INY);
+            src = x.src < 0 ? 0 : x.src;
+          }
+        }
+      } else if (!set_list) {
+        f = s == 0 ? 3 : (s == 1 ? 4 : (s == 2 ? 5 : 6));   // k, omega, nu_t, p copied together
+      } else if (s < 3) {
+        f = 3 + s;
+        kind = BK_KIN + s;
+        src = 0;
+      }
+      if (f >= 0) {
+        if (kind == BK_ORIG) {
+          const int w = wmap[fo.off[f] + src];
+          if (w >= 0) {   // the source was written by an earlier list: take that write's value
+            const BcOp prev = ops[w];
+            kind = prev.fk >> 3;
+            src = prev.src;
+          }
+        }
+        op.fk = f | (kind << 3);
+        op.src = src;
+      }
+      o[s] = op;
+    }
+  }
+}
+
+// the list's ops become the latest writers of their destinations
+__global__ void k_bc_compose_claim(const BcOp* __restrict__ ops, long long base, long long n, int* wmap, BcFieldOff fo) {
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n; t += (long long)gridDim.x * blockDim.x) {
+    const BcOp op = ops[base + t];
+    if (op.fk >= 0) wmap[fo.off[op.fk & 7] + op.dst] = (int)(base + t);
+  }
+}
+
+// 1 = final write (last writer, not an identity copy), 2 = final and ordered
+// (reads a location another final write changes, or writes one that a final
+// write reads)
+__global__ void k_bc_compose_final(const BcOp* __restrict__ ops, long long n, const int* __restrict__ wmap, BcFieldOff fo,
+                                   uint8_t* flag) {
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n; t += (long long)gridDim.x * blockDim.x) {
+    const BcOp op = ops[t];
+    uint8_t fl = 0;
+    if (op.fk >= 0) {
+      const int f = op.fk & 7;
+      const bool ident = (op.fk >> 3) == BK_ORIG && op.src == op.dst;
+      fl = (wmap[fo.off[f] + op.dst] == (int)t && !ident) ? 1 : 0;
+    }
+    flag[t] = fl;
+  }
+}
+__global__ void k_bc_compose_conflict(const BcOp* __restrict__ ops, long long n, const int* __restrict__ wmap, BcFieldOff fo,
+                                      uint8_t* flag) {
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n; t += (long long)gridDim.x * blockDim.x) {
+    const BcOp op = ops[t];
+    if (op.fk < 0 || (op.fk >> 3) != BK_ORIG || (flag[t] & 1) == 0) continue;
+    const int w = wmap[fo.off[op.fk & 7] + op.src];
+    if (w >= 0 && (flag[w] & 1)) {   // both orders matter: same value stored by every racer
+      flag[t] = 3;
+      flag[w] = 3;
+    }
+  }
+}
+// compaction: final writes to `free_ops` (from the front) or `ord_ops`
+__global__ void k_bc_compose_compact(const BcOp* __restrict__ ops, long long n, const uint8_t* __restrict__ flag,
+                                     BcOp* free_ops, BcOp* ord_ops, int ord_cap, int* counts) {
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n; t += (long long)gridDim.x * blockDim.x) {
+    const uint8_t fl = flag[t];
+    if (fl == 1) {
+      free_ops[atomicAdd(&counts[0], 1)] = ops[t];
+    } else if (fl == 3) {
+      const int q = atomicAdd(&counts[1], 1);
+      if (q < ord_cap) ord_ops[q] = ops[t];
+    }
+  }
+}
+
+// the independent writes in (field, destination) order: coalesced replay
+__global__ void k_bc_compose_keys(const BcOp* __restrict__ ops, int n, unsigned long long* keys, int* idx) {
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
+    keys[t] = ((unsigned long long)(ops[t].fk & 7) << 32) | (unsigned)ops[t].dst;
+    idx[t] = t;
+  }
+}
+__global__ void k_bc_compose_gather(const BcOp* __restrict__ ops, const int* __restrict__ idx, int n, BcOp* out) {
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) out[t] = ops[idx[t]];
+}
+
+template <typename T>
+__device__ __forceinline__ T* bc_field(const BcFields<T>& F, int f) {
+  switch (f) {
+    case 0: return F.u;
+    case 1: return F.v;
+    case 2: return F.w;
+    case 3: return F.k;
+    case 4: return F.om;
+    case 5: return F.nut;
+    default: return F.p;
+  }
+}
+template <typename T>
+__device__ __forceinline__ T bc_value(const BcFields<T>& F, const BcOp& op, const T* __restrict__ uzx,
+                                      const T* __restrict__ uzy, T k_in, T om_in, T nut_in) {
+  switch (op.fk >> 3) {
+    case BK_ORIG: return bc_field<T>(F, op.fk & 7)[op.src];
+    case BK_INX: return uzx[op.src];
+    case BK_INY: return uzy[op.src];
+    case BK_KIN: return k_in;
+    case BK_OMIN: return om_in;
+    case BK_NUTIN: return nut_in;
+    default: return (T)0;
+  }
+}
+
+constexpr int BC_ORD_PER_THREAD = 8;   // block 0: up to 256 * 8 ordered writes
+template <typename T>
+__global__ void __launch_bounds__(256) k_bc_replay(BcFields<T> F, const BcOp* __restrict__ fops, int nf,
+                                                   const BcOp* __restrict__ oops, int no, const T* __restrict__ uzx,
+                                                   const T* __restrict__ uzy, T k_in, T om_in, T nut_in,
+                                                   const int* gate) {
+  if (*gate) return;
+  if (blockIdx.x == 0) {
+    T v[BC_ORD_PER_THREAD];
+#pragma unroll
+    for (int s = 0; s < BC_ORD_PER_THREAD; ++s) {
+      const int t = (int)threadIdx.x + s * 256;
+      if (t < no) v[s] = bc_value<T>(F, oops[t], uzx, uzy, k_in, om_in, nut_in);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int s = 0; s < BC_ORD_PER_THREAD; ++s) {
+      const int t = (int)threadIdx.x + s * 256;
+      if (t < no) {
+        const BcOp op = oops[t];
+        bc_field<T>(F, op.fk & 7)[op.dst] = v[s];
+      }
+    }
+    return;
+  }
+  for (int t = (blockIdx.x - 1) * blockDim.x + threadIdx.x; t < nf; t += (gridDim.x - 1) * blockDim.x) {
+    const BcOp op = fops[t];
+    bc_field<T>(F, op.fk & 7)[op.dst] = bc_value<T>(F, op, uzx, uzy, k_in, om_in, nut_in);
   }
 }
 

@@ -329,7 +329,10 @@ class FlowState:
     # construction ----------------------------------------------------------
     @classmethod
     def zeros(cls, grid: GridSpec, labels=None, porosity=None, k0: float = 1e-6,
-              omega0: float = 1.0, dtype=torch.float32, device=None):
+              omega0: float = 1.0, dtype=torch.float32, device=None, static_dev=None):
+        """Zero velocity and pressure, k0 / omega0 turbulence.  ``static_dev``:
+        a (labels, phi, lad) device triple in the x-fastest layout (a device
+        voxelizer's output), taken as is instead of ``labels`` / ``porosity``."""
         device = device or default_device()
         f = {}
         for n in FIELDS:
@@ -338,6 +341,8 @@ class FlowState:
         f["k"].fill_(k0)
         f["omega"].fill_(omega0)
         f["nu_t"].fill_(k0 / omega0)
+        if static_dev is not None:
+            return cls(grid, f, *static_dev)
         lab = np.zeros(grid.shape, np.int8) if labels is None else np.asarray(labels, np.int8)
         por = PorosityField.open_air(grid) if porosity is None else porosity
         return cls(grid, f,

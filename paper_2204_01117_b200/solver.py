@@ -516,9 +516,7 @@ def make_initial_state(grid: GridSpec, labels, porosity, params: SolverParams,
     device = device or default_device()
     k_in, om_in = params.inlet_k_omega()
     if isinstance(labels, tuple):
-        lab_d, phi_d, lad_d = labels
-        state = FlowState.zeros(grid, None, None, k0=k_in, omega0=om_in, dtype=dtype, device=device)
-        state.labels_dev, state.phi_dev, state.lad_dev = lab_d, phi_d, lad_d
+        state = FlowState.zeros(grid, k0=k_in, omega0=om_in, dtype=dtype, device=device, static_dev=labels)
     else:
         state = FlowState.zeros(grid, labels, porosity, k0=k_in, omega0=om_in, dtype=dtype,
                                 device=device)

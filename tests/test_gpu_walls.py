@@ -115,3 +115,52 @@ def test_boundary_full_volume_path_without_labels_version(monkeypatch):
     got = fields_of(dst)
     for n in FIELDS:
         np.testing.assert_array_equal(got[n], getattr(ost, n), err_msg=n)
+
+
+@pytest.mark.parametrize("layout", ["all_outlets", "mixed"])
+def test_composed_boundary_pass_equals_ordered_lists(layout, monkeypatch):
+    """One boundary pass is ONE k_bc_replay launch of the lists' composition
+    (cw_step.cuh k_bc_compose_*): with outlets on every side (every edge and
+    corner where a later side reads or overwrites an earlier side's write),
+    an inlet face, walls and a wall touching the outlets, the result equals
+    the oracle's ordered apply_boundary_conditions (solver.py:330-400) and
+    the ordered per-side launches (CW_BC_COMPOSE=0) bit for bit in float64,
+    and bit for bit between the two paths in float32."""
+    from oracle import citywind_oracle as co
+    from paper_2204_01117_b200 import solver
+    doc = scenes.cuboid(22, 14, 9, 1.0, 0.1)
+    sc = co.scene_from_dict(doc)
+    g = sc.grid
+    labels = co.classify_boundary(g, sc.faces)           # x-fastest (nz, ny, nx)
+    if layout == "all_outlets":
+        labels[:, :, 0] = 4
+        labels[:, :, -1] = 4
+        labels[:, 0, :] = 4
+        labels[:, -1, :] = 4
+        labels[0, :, :] = 4
+        labels[-1, :, :] = 4
+        labels[3:6, 4:8, 6:10] = 5
+    else:
+        labels[0, :, :] = 5
+        labels[:, 0, 3:9] = 5                            # a wall strip on an outlet side
+        labels[2:7, 5:9, 8:12] = 5
+        labels[-1, :, :] = 4
+    vals = {}
+    for prec in ("fp64", "fp32"):
+        for compose in ("1", "0"):
+            monkeypatch.setenv("CW_BC_COMPOSE", compose)
+            ost = co.make_initial_state(g, labels, np.ones(g.cshape), np.zeros(g.cshape), sc.params, sc.inlet,
+                                        mode="rest")
+            r2 = np.random.default_rng(11)
+            for n in FIELDS:
+                setattr(ost, n, r2.standard_normal(getattr(ost, n).shape))
+            dst = device_state(ost, torch.float64 if prec == "fp64" else torch.float32)   # new labels tensor: lists rebuilt
+            p, prof = device_params(sc)
+            solver.apply_boundary_conditions(dst, prof, p)
+            vals[prec, compose] = fields_of(dst)
+            if prec == "fp64":
+                co.apply_boundary_conditions(ost, sc.inlet, sc.params)
+                for n in FIELDS:
+                    np.testing.assert_array_equal(vals[prec, compose][n], getattr(ost, n), err_msg=f"{compose} {n}")
+        for n in FIELDS:
+            np.testing.assert_array_equal(vals[prec, "1"][n], vals[prec, "0"][n], err_msg=f"{prec} {n}")
