@@ -163,9 +163,10 @@ def test_c2_canyon_500_steps_against_reference(prec):
     chaotic and no implementation tracks it field by field.  Gates:
     * fp64 on the device: the reference's per-step PCG counts exactly through
       step 120 (the device measured 140);
-    * fp32: exactly through the reference's own fp32-noise horizon
-      (tests/golden/cert_c2_canyon_128_500.json: the first step at which the
-      reference's counts move under 1e-6 relative noise), capped at 30;
+    * fp32: exactly through step 30 (the device measured 34; the
+      reference's own counts first move under fp32-level noise at step 50,
+      tests/golden/cert_c2_canyon_128_500.json, so fp32 arithmetic leaves
+      the reference's trajectory somewhat before noise of that size does);
     * both: all 500 steps complete (the reference raises nowhere either) and
       the device shows the same runaway (k_max beyond 1e10 after step 100)."""
     from paper_2204_01117_b200 import solver
@@ -183,12 +184,7 @@ def test_c2_canyon_500_steps_against_reference(prec):
                    .pcg.iterations)
         kmax.append(float(st.fields["k"].max()))
     gold = g["pcg_iterations"].tolist()
-    if prec == "fp64":
-        horizon = 120
-    else:
-        cert = _certified(name)
-        moved = cert.get("mismatched_steps") if cert else None
-        horizon = min(30, min(moved) - 1) if moved else 30
+    horizon = 120 if prec == "fp64" else 30
     assert its[:horizon] == gold[:horizon]
     assert len(its) == 500
     assert max(kmax[99:]) > 1e10 and float(np.max(g["k_max"][99:])) > 1e10
