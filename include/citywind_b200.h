@@ -198,6 +198,18 @@ int cw_step(cw_ctx *ctx, const cw_fields *f, const cw_params *prm, const cw_inle
  * step() (ref solver.py:407-461); no reference counterpart. */
 int cw_step_defer(cw_ctx *ctx, void *nu_t_ready, void *p_ready);
 
+/* With cw_step_defer: let the NEXT step also start before k and omega are on
+ * the device.  Their only readers before the projection are the upwind step
+ * (advection.py:154-173) and the first boundary pass; the step then saves
+ * the old cell-centred velocity in the predictor, runs the projection on
+ * u, v, w, p first and waits for k_omega_ready (a cudaEvent_t) only after
+ * it, before the upwind step and the k / omega / nu_t writes of the first
+ * boundary pass.  Results are bit-identical to the undeferred step.  Needs
+ * turbulence-independent composed boundary lists (labels_version != 0);
+ * otherwise the step waits for the event before its first stage.  One-shot;
+ * NULL = no wait.  No reference counterpart. */
+int cw_step_defer_kw(cw_ctx *ctx, void *k_omega_ready);
+
 /* Run ONE stage function of the reference on a state, with dt = prm->dt:
  * advect (advect_velocity + upwind_scalar k/omega, advection.py:125-173),
  * diffuse (solver.py:193-208), apply_drag (:150-168), apply_boundary_conditions

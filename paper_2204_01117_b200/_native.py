@@ -126,6 +126,7 @@ SIGNATURES = {
                                C.c_int, C.c_double, _P]),
     "cw_read_reports": (C.c_int, [_P, C.POINTER(cw_report), C.c_int, C.POINTER(C.c_int), _P]),
     "cw_step_defer": (C.c_int, [_P, _P, _P]),
+    "cw_step_defer_kw": (C.c_int, [_P, _P]),
     "cw_set_max_iter": (C.c_int, [_P, C.c_int]),
     "cw_pcg_chunk_of": (C.c_int, [C.POINTER(cw_grid), C.c_int, C.c_int, C.POINTER(C.c_int)]),
     "cw_set_pcg_chunk": (C.c_int, [_P, C.c_int]),

@@ -143,6 +143,7 @@ struct cw_ctx {
   bool timing = false;
   // one-shot waits of the next enqueued step (cw_step_defer): first use of nu_t / p
   cudaEvent_t wait_nut = nullptr, wait_p = nullptr;
+  cudaEvent_t wait_kw = nullptr;      // cw_step_defer_kw: k, omega
   cudaEvent_t ev[8] = {};
   bool ev_made = false;
   float stage_ms[7] = {0, 0, 0, 0, 0, 0, 0};
@@ -738,16 +739,24 @@ static void compose_bc(cw_ctx* c, cudaStream_t st) {
   cudaGetLastError();
 }
 
+// the boundary lists of (lab, ver) are built (and composed when enabled)
+static bool have_bc_lists(cw_ctx* c, const int8_t* lab, long long ver, cudaStream_t st) {
+  return ver != 0 && ((c->bc_lab == lab && c->bc_ver == ver) || build_bc_lists(c, lab, ver, st) == 0);
+}
+
+constexpr unsigned BC_ALL = 0x7fu, BC_UVWP = 0x47u, BC_KWN = 0x38u;   // fields u v w k omega nu_t p = bits 0..6
+
+// fmask != BC_ALL only with composed lists (callers check c->bc_nf >= 0)
 template <typename T>
 static void launch_bc(cw_ctx* c, BcFields<T> F, const int8_t* lab, long long ver, const cw_params* prm,
-                      cudaStream_t st) {
+                      cudaStream_t st, unsigned fmask = BC_ALL) {
   const Dims& d = c->d;
-  if (ver != 0 && ((c->bc_lab == lab && c->bc_ver == ver) || build_bc_lists(c, lab, ver, st) == 0)) {
+  if (have_bc_lists(c, lab, ver, st)) {
     if (c->bc_nf >= 0) {   // the composed pass: one launch
       if (c->bc_nf + c->bc_no > 0)
         (k_bc_replay<T><<<1 + std::max(1, std::min(nblk(c->bc_nf), 8 * c->num_sms)), 256, 0, st>>>(
              F, c->bc_ops, c->bc_nf, c->bc_ops + c->bc_nf, c->bc_no, (const T*)c->uzx, (const T*)c->uzy,
-             (T)prm->k_in, (T)prm->omega_in, (T)(prm->k_in / prm->omega_in), c->gate),
+             (T)prm->k_in, (T)prm->omega_in, (T)(prm->k_in / prm->omega_in), fmask, c->gate),
          ++c->launches);
       return;
     }
@@ -892,8 +901,11 @@ static double nu_stable(const cw_ctx* c, double dt) {   // turbulence.py:18-23
 }
 
 // upwind k/omega into (kout, wout); MacCormack u, v, w into the adv buffers
+// acell != nullptr (cw_step_defer_kw): the predictor saves the cell-centred
+// old velocity there instead of running the upwind step
 template <typename T>
-static void st_advect(cw_ctx* c, const StepPtrs<T>& P, const cw_params* prm, T* kout, T* wout, cudaStream_t st) {
+static void st_advect(cw_ctx* c, const StepPtrs<T>& P, const cw_params* prm, T* kout, T* wout, cudaStream_t st,
+                      T* acell = nullptr) {
   const Dims& d = c->d;
   const T dt = (T)prm->dt;
   const bool turb = prm->turbulence != 0;    // upwind k, omega ride along in the predictor launch
@@ -901,9 +913,16 @@ static void st_advect(cw_ctx* c, const StepPtrs<T>& P, const cw_params* prm, T* 
   if (timed) cudaEventRecord(c->aev[3 * c->adv_timed], st);
   const MacClip<T> clip{{(T*)c->clip_mn[0], (T*)c->clip_mn[1], (T*)c->clip_mn[2]},
                         {(T*)c->clip_mx[0], (T*)c->clip_mx[1], (T*)c->clip_mx[2]}};
-  (k_mac_predict<T><<<dim3((d.nx + 1 + ST_BX - 1) / ST_BX, (d.ny + 1 + ST_BY - 1) / ST_BY, (d.nz + 1 + ZT_MAC - 1) / ZT_MAC), B3, 0, st>>>(
-       d, P.u, P.v, P.w, (T*)c->ahead[0], (T*)c->ahead[1], (T*)c->ahead[2], dt, (const T*)P.k, (const T*)P.om,
-       turb ? kout : (T*)nullptr, turb ? wout : (T*)nullptr, clip, c->gate), ++c->launches);
+  const dim3 gp((d.nx + 1 + ST_BX - 1) / ST_BX, (d.ny + 1 + ST_BY - 1) / ST_BY, (d.nz + 1 + ZT_MAC - 1) / ZT_MAC);
+  if (acell)
+    (k_mac_predict<T, true><<<gp, B3, 0, st>>>(d, P.u, P.v, P.w, (T*)c->ahead[0], (T*)c->ahead[1], (T*)c->ahead[2],
+                                               dt, (const T*)P.k, (const T*)P.om, (T*)nullptr, (T*)nullptr, clip,
+                                               c->gate, acell),
+     ++c->launches);
+  else
+    (k_mac_predict<T><<<gp, B3, 0, st>>>(
+         d, P.u, P.v, P.w, (T*)c->ahead[0], (T*)c->ahead[1], (T*)c->ahead[2], dt, (const T*)P.k, (const T*)P.om,
+         turb ? kout : (T*)nullptr, turb ? wout : (T*)nullptr, clip, c->gate), ++c->launches);
   if (timed) cudaEventRecord(c->aev[3 * c->adv_timed + 1], st);
   (k_mac_correct<T><<<dim3((d.nx + 1 + ST_BX - 1) / ST_BX, (d.ny + 1 + ST_BY - 1) / ST_BY, (d.nz + 1 + ZT_MAC - 1) / ZT_MAC), B3, 0, st>>>(
        d, P.u, P.v, P.w, (const T*)c->ahead[0], (const T*)c->ahead[1], (const T*)c->ahead[2], (T*)c->adv[0],
@@ -1025,8 +1044,24 @@ static int enqueue_step(cw_ctx* c, const cw_fields* f, const cw_params* prm, dou
   const bool turb = prm->turbulence != 0;
   auto mark = [&](int i) { if (c->timing) cudaEventRecord(c->ev[i], st); };
   (k_report_init<<<1, 1, 0, st>>>(rep), ++c->launches);
+  // cw_step_defer_kw: k, omega arrive during the projection (their first
+  // readers, the upwind step and the first boundary pass's k / omega / nu_t
+  // writes, move behind it); without composed lists the step waits here
+  T* acell = nullptr;
+  bool defer_kw = false;
+  if (c->wait_kw) {
+    defer_kw = have_bc_lists(c, P.lab, P.lab_ver, st) && c->bc_nf >= 0;
+    if (defer_kw && turb) {
+      acell = (T*)cw_internal_scratch(c, 22, 3 * (size_t)c->ncell * sizeof(T));
+      defer_kw = acell != nullptr;
+    }
+    if (!defer_kw) {
+      CW_CUDA(cudaStreamWaitEvent(st, c->wait_kw, 0));
+      c->wait_kw = nullptr;
+    }
+  }
   mark(0);
-  st_advect<T>(c, P, prm, (T*)c->tk, (T*)c->tw, st);        // "advect"
+  st_advect<T>(c, P, prm, (T*)c->tk, (T*)c->tw, st, acell);  // "advect"
   mark(1);
   if (c->wait_nut) {   // nu_t is first read by the diffusion
     CW_CUDA(cudaStreamWaitEvent(st, c->wait_nut, 0));
@@ -1043,10 +1078,18 @@ static int enqueue_step(cw_ctx* c, const cw_fields* f, const cw_params* prm, dou
     CW_CUDA(cudaStreamWaitEvent(st, c->wait_p, 0));
     c->wait_p = nullptr;
   }
-  launch_bc<T>(c, F1, P.lab, P.lab_ver, prm, st);                        // "boundary"
+  launch_bc<T>(c, F1, P.lab, P.lab_ver, prm, st, defer_kw ? BC_UVWP : BC_ALL);   // "boundary"
   mark(4);
   int rc = st_project<T>(c, P, f, prm, tol, rep, st);         // "project"
   if (rc) return rc;
+  if (defer_kw) {   // the deferred k / omega part of the step, same writes
+    CW_CUDA(cudaStreamWaitEvent(st, c->wait_kw, 0));
+    c->wait_kw = nullptr;
+    if (turb)
+      (k_upwind_saved<T><<<g3(c->d.nx, c->d.ny, c->d.nz), B3, 0, st>>>(c->d, acell, P.k, P.om, (T*)c->tk, (T*)c->tw,
+                                                                       (T)prm->dt, c->gate), ++c->launches);
+    launch_bc<T>(c, F1, P.lab, P.lab_ver, prm, st, BC_KWN);
+  }
   mark(5);
   if (turb) st_turb<T>(c, P, prm, B.k, B.om, rep, st);        // "turbulence"
   mark(6);
@@ -1448,7 +1491,7 @@ extern "C" int cw_step(cw_ctx* c, const cw_fields* f, const cw_params* prm, cons
   // every exit (the first enqueued step consumes them)
   struct DeferGuard {
     cw_ctx* c;
-    ~DeferGuard() { c->wait_nut = nullptr; c->wait_p = nullptr; }
+    ~DeferGuard() { c->wait_nut = nullptr; c->wait_p = nullptr; c->wait_kw = nullptr; }
   } defer_guard{c};
   if (!f || !prm || !inl) return fail(CW_ERR_INVALID, "null argument");
   if (!c->have_op) return fail(CW_ERR_INVALID, "cw_set_operator has not been called");
@@ -1467,7 +1510,7 @@ extern "C" int cw_step(cw_ctx* c, const cw_fields* f, const cw_params* prm, cons
     const int slot = c->head++;
     c->slot_dt[slot] = prm->dt;
     const bool timed = c->timing || c->pcg_timed < (int)c->pev.size() / 2 || c->adv_timed < (int)c->aev.size() / 3;
-    if (c->graphs && !timed && !c->wait_nut && !c->wait_p) {
+    if (c->graphs && !timed && !c->wait_nut && !c->wait_p && !c->wait_kw) {
       rc = graph_step(c, f, prm, tol, S(stream));
       if (rc == CW_OK) continue;
       if (rc != -1) return rc;   // -1: capture not possible here, run the step directly
@@ -1647,6 +1690,12 @@ extern "C" int cw_step_defer(cw_ctx* c, void* nu_t_ready, void* p_ready) {
   if (!c) return fail(CW_ERR_INVALID, "null argument");
   c->wait_nut = (cudaEvent_t)nu_t_ready;
   c->wait_p = (cudaEvent_t)p_ready;
+  return CW_OK;
+}
+
+extern "C" int cw_step_defer_kw(cw_ctx* c, void* k_omega_ready) {
+  if (!c) return fail(CW_ERR_INVALID, "null argument");
+  c->wait_kw = (cudaEvent_t)k_omega_ready;
   return CW_OK;
 }
 

@@ -106,19 +106,40 @@ __device__ __forceinline__ void upwind_cell_a(const Dims& d, const T (&a)[3], co
   }
 }
 
+// cell-centred velocity of cell (i, j, k) (grid.py:561-566)
+template <typename T>
+__device__ __forceinline__ void cell_vel_a(const Dims& d, const T* __restrict__ u, const T* __restrict__ v,
+                                           const T* __restrict__ w, int i, int j, int k, T (&a)[3]) {
+  const int c = d.cidx32(i, j, k);
+  a[0] = (T)0.5 * (u[((int)k * d.ny + j) * (d.nx + 1) + i] + u[((int)k * d.ny + j) * (d.nx + 1) + i + 1]);
+  a[1] = (T)0.5 * (v[((int)k * (d.ny + 1) + j) * d.nx + i] + v[((int)k * (d.ny + 1) + j + 1) * d.nx + i]);
+  a[2] = (T)0.5 * (w[c] + w[c + (int)d.nx * d.ny]);
+}
+
 template <typename T>
 __device__ __forceinline__ void upwind_cell(const Dims& d, const T* __restrict__ u, const T* __restrict__ v,
                                             const T* __restrict__ w, const T* __restrict__ kin,
                                             const T* __restrict__ win, T* __restrict__ kout, T* __restrict__ wout,
                                             T dt, int i, int j, int k) {
   if (i < d.nx && j < d.ny && k < d.nz) {
-    const int c = d.cidx32(i, j, k);
     T a[3];
-    a[0] = (T)0.5 * (u[((int)k * d.ny + j) * (d.nx + 1) + i] + u[((int)k * d.ny + j) * (d.nx + 1) + i + 1]);
-    a[1] = (T)0.5 * (v[((int)k * (d.ny + 1) + j) * d.nx + i] + v[((int)k * (d.ny + 1) + j + 1) * d.nx + i]);
-    a[2] = (T)0.5 * (w[c] + w[c + (int)d.nx * d.ny]);
+    cell_vel_a<T>(d, u, v, w, i, j, k, a);
     upwind_cell_a<T>(d, a, kin, win, kout, wout, dt, i, j, k);
   }
+}
+
+// the upwind step from a saved cell-centred velocity (cw_step_defer_kw)
+template <typename T>
+__global__ void k_upwind_saved(Dims d, const T* __restrict__ acell, const T* __restrict__ kin,
+                               const T* __restrict__ win, T* __restrict__ kout, T* __restrict__ wout, T dt,
+                               const int* gate) {
+  if (*gate) return;
+  CW_IJK(d.nx, d.ny, d.nz, inb);
+  if (!inb) return;
+  const long long ncell = (long long)d.nx * d.ny * d.nz;
+  const int c = d.cidx32(i, j, k);
+  const T a[3] = {acell[c], acell[ncell + c], acell[2 * ncell + c]};
+  upwind_cell_a<T>(d, a, kin, win, kout, wout, dt, i, j, k);
 }
 
 // ---------------------------------------------------------------------------
@@ -277,14 +298,19 @@ __device__ __forceinline__ void mac_predict_face(const Dims& d, int comp, const 
 #endif
 // 8 resident blocks per SM (<= 32 registers): measured 102 us at C3, against
 // 106 us at 6 blocks and 223 us uncapped
-template <typename T>
+// SAVE_A (cw_step_defer_kw): instead of the upwind step, store the cell-centred
+// old velocity (the upwind step's input) in acell[0..2]; k_upwind_saved runs
+// the upwind step from it later
+template <typename T, bool SAVE_A = false>
 __global__ void __launch_bounds__(256, CW_MAC_PRED_MINB) k_mac_predict(Dims d, const T* __restrict__ u, const T* __restrict__ v,
                               const T* __restrict__ w, T* __restrict__ a0, T* __restrict__ a1,
                               T* __restrict__ a2, T dt, const T* __restrict__ kin, const T* __restrict__ win,
-                              T* __restrict__ kout, T* __restrict__ wout, MacClip<T> clip, const int* gate) {
+                              T* __restrict__ kout, T* __restrict__ wout, MacClip<T> clip, const int* gate,
+                              T* __restrict__ acell = nullptr) {
   if (*gate) return;
   const int i = (int)(blockIdx.x * ST_BX + threadIdx.x), j = (int)(blockIdx.y * ST_BY + threadIdx.y);
   if (i > d.nx || j > d.ny) return;
+  const long long ncell = (long long)d.nx * d.ny * d.nz;
 #pragma unroll
   for (int kz = 0; kz < ZT_MAC; ++kz) {
     const int k = (int)blockIdx.z * ZT_MAC + kz;
@@ -292,13 +318,31 @@ __global__ void __launch_bounds__(256, CW_MAC_PRED_MINB) k_mac_predict(Dims d, c
     if (!d.is2d && i < d.nx && j < d.ny && k < d.nz) {   // interior: shared velocity loads
       VelNbhd<T> n;
       vel_nbhd<T>(d, u, v, w, i, j, k, n);
-      if (kout) upwind_cell_a<T>(d, n.a, kin, win, kout, wout, dt, i, j, k);
+      if (SAVE_A) {
+        const int c = d.cidx32(i, j, k);
+        acell[c] = n.a[0];
+        acell[ncell + c] = n.a[1];
+        acell[2 * ncell + c] = n.a[2];
+      } else if (kout) {
+        upwind_cell_a<T>(d, n.a, kin, win, kout, wout, dt, i, j, k);
+      }
       mac_predict_face_v<T>(d, 0, u, a0, dt, i, j, k, n.fu[0], n.fv[0], n.fw[0], clip);
       mac_predict_face_v<T>(d, 1, v, a1, dt, i, j, k, n.fu[1], n.fv[1], n.fw[1], clip);
       mac_predict_face_v<T>(d, 2, w, a2, dt, i, j, k, n.fu[2], n.fv[2], n.fw[2], clip);
       continue;
     }
-    if (kout) upwind_cell<T>(d, u, v, w, kin, win, kout, wout, dt, i, j, k);
+    if (SAVE_A) {
+      if (i < d.nx && j < d.ny && k < d.nz) {
+        T a[3];
+        cell_vel_a<T>(d, u, v, w, i, j, k, a);
+        const int c = d.cidx32(i, j, k);
+        acell[c] = a[0];
+        acell[ncell + c] = a[1];
+        acell[2 * ncell + c] = a[2];
+      }
+    } else if (kout) {
+      upwind_cell<T>(d, u, v, w, kin, win, kout, wout, dt, i, j, k);
+    }
     mac_predict_face<T>(d, 0, u, v, w, a0, dt, i, j, k, clip);
     mac_predict_face<T>(d, 1, u, v, w, a1, dt, i, j, k, clip);
     if (!d.is2d) mac_predict_face<T>(d, 2, u, v, w, a2, dt, i, j, k, clip);
@@ -976,18 +1020,20 @@ __device__ __forceinline__ T bc_value(const BcFields<T>& F, const BcOp& op, cons
 }
 
 constexpr int BC_ORD_PER_THREAD = 8;   // block 0: up to 256 * 8 ordered writes
+// fmask: the fields (bit f) this launch writes -- a pass split by field
+// (cw_step_defer_kw) is the same writes: every op reads its own field only
 template <typename T>
 __global__ void __launch_bounds__(256) k_bc_replay(BcFields<T> F, const BcOp* __restrict__ fops, int nf,
                                                    const BcOp* __restrict__ oops, int no, const T* __restrict__ uzx,
                                                    const T* __restrict__ uzy, T k_in, T om_in, T nut_in,
-                                                   const int* gate) {
+                                                   unsigned fmask, const int* gate) {
   if (*gate) return;
   if (blockIdx.x == 0) {
     T v[BC_ORD_PER_THREAD];
 #pragma unroll
     for (int s = 0; s < BC_ORD_PER_THREAD; ++s) {
       const int t = (int)threadIdx.x + s * 256;
-      if (t < no) v[s] = bc_value<T>(F, oops[t], uzx, uzy, k_in, om_in, nut_in);
+      if (t < no && (fmask >> (oops[t].fk & 7) & 1u)) v[s] = bc_value<T>(F, oops[t], uzx, uzy, k_in, om_in, nut_in);
     }
     __syncthreads();
 #pragma unroll
@@ -995,14 +1041,14 @@ __global__ void __launch_bounds__(256) k_bc_replay(BcFields<T> F, const BcOp* __
       const int t = (int)threadIdx.x + s * 256;
       if (t < no) {
         const BcOp op = oops[t];
-        bc_field<T>(F, op.fk & 7)[op.dst] = v[s];
+        if (fmask >> (op.fk & 7) & 1u) bc_field<T>(F, op.fk & 7)[op.dst] = v[s];
       }
     }
     return;
   }
   for (int t = (blockIdx.x - 1) * blockDim.x + threadIdx.x; t < nf; t += (gridDim.x - 1) * blockDim.x) {
     const BcOp op = fops[t];
-    bc_field<T>(F, op.fk & 7)[op.dst] = bc_value<T>(F, op, uzx, uzy, k_in, om_in, nut_in);
+    if (fmask >> (op.fk & 7) & 1u) bc_field<T>(F, op.fk & 7)[op.dst] = bc_value<T>(F, op, uzx, uzy, k_in, om_in, nut_in);
   }
 }
 

@@ -11,9 +11,12 @@ objects work unchanged, and per call:
 
 1. uploads the seven float64 arrays (pinned staging; arrays this binding
    returned last step are already pinned), converting each to the device's
-   x-fastest precision on the device (``cw_ref_layout``, a tiled transpose);
-   nu_t and p upload last and the step waits for them only before their
-   first use (``cw_step_defer``);
+   x-fastest precision on the device (``cw_ref_layout``, a tiled transpose),
+   in the order the step first uses them: the step starts once u, v, w are
+   up, waits for nu_t before the diffusion and for p before the first
+   boundary pass (``cw_step_defer``), and k / omega arrive while the
+   projection runs (``cw_step_defer_kw``: their upwind step and boundary
+   writes move behind it);
 2. runs one device step (``cw_step``);
 3. converts the seven fields back to float64 C order on the device and
    downloads them into pinned arrays, which it assigns to the state's
@@ -43,8 +46,11 @@ from .linalg import MatrixPreconditioner as _DevPre
 from .linalg import build_pressure_matrix
 from .solver import InletProfile, SolverParams, StepReport, step as _dev_step
 
-# upload order: the step's first stages read u, v, w, k, omega; nu_t and p last
-ORDER = ("u", "v", "w", "k", "omega", "nu_t", "p")
+# upload order, the order of first use in the step: u, v, w (advection),
+# nu_t (diffusion), p (first boundary pass, projection), then k and omega,
+# whose first readers run after the projection (cw_step_defer_kw)
+ORDER = ("u", "v", "w", "nu_t", "p", "k", "omega")
+LATE = ("nu_t", "p", "k", "omega")
 KIND = {"u": 0, "v": 1, "w": 2, "p": 3, "k": 3, "omega": 3, "nu_t": 3}
 _PARAM_FIELDS = tuple(SolverParams.__dataclass_fields__)
 
@@ -191,7 +197,7 @@ class RefStepper:
                 with torch.cuda.stream(s.up):
                     s.d64[n].copy_(host.view(-1), non_blocking=True)
                     self.h2d_bytes += s.d64[n].numel() * 8
-                    if n in ("nu_t", "p"):     # converted on the copy stream: the step waits late
+                    if n in LATE:     # converted on the copy stream: the step waits late
                         N.check(lib.cw_ref_layout(ctx.h, 0, KIND[n], N.ptr(s.d64[n]), N.ptr(s.dev.fields[n]),
                                                   N.c_stream(s.up)))
                         ev = torch.cuda.Event()
@@ -209,7 +215,7 @@ class RefStepper:
         s.dev.touch()
         # 2. one device step
         rep = _dev_step(s.dev, prm, s.psys, pre, _profile(profile), pcg_tol=pcg_tol,
-                        _defer=(late["nu_t"], late["p"]))
+                        _defer=(late["nu_t"], late["p"], late["omega"]))
         # 3. device layout -> float64 C order -> pinned host arrays
         out, out_np = s.pin_out[s.out_set], s.np_out[s.out_set]
         ctx = s.psys.pool.acquire(s.grid, s.psys.labels_on(self.device), pre.omega, pre.kind, self.dtype,

@@ -245,8 +245,9 @@ def step(state: FlowState, params: SolverParams, psys: PressureSystem, precondit
          profile: InletProfile, advector=None, pcg_tol: float | None = None, _defer=None) -> StepReport:
     """One time-split step (solver.py:407-461); returns per-stage device
     timings (seconds) and the solver statistics.  ``_defer`` (internal):
-    (nu_t_ready, p_ready) CUDA events the step waits for before the first
-    stage that uses that field (``cw_step_defer``)."""
+    (nu_t_ready, p_ready[, k_omega_ready]) CUDA events the step waits for
+    before the first stage that uses that field (``cw_step_defer``,
+    ``cw_step_defer_kw``)."""
     reps = step_many(state, params, psys, preconditioner, profile, 1, pcg_tol, stage_timings=True, _defer=_defer)
     return reps[0] if reps else StepReport()
 
@@ -351,6 +352,8 @@ def step_many(state: FlowState, params: SolverParams, psys: PressureSystem, prec
             lib.cw_set_stage_timing(ctx.h, 1)
         if _defer is not None:
             N.check(lib.cw_step_defer(ctx.h, C.c_void_p(_defer[0].cuda_event), C.c_void_p(_defer[1].cuda_event)))
+            if len(_defer) > 2 and _defer[2] is not None:
+                N.check(lib.cw_step_defer_kw(ctx.h, C.c_void_p(_defer[2].cuda_event)))
         if regions is not None:
             rlo, rhi, rsums, rcounts = regions
             rlo = np.ascontiguousarray(np.atleast_2d(rlo), dtype=np.float64)
