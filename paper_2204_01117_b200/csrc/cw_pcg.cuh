@@ -150,6 +150,15 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, u
 #ifndef CW_L2HINT
 #define CW_L2HINT 1
 #endif
+// which streams are evict_last (bits: 1 z, 2 p, 4 x, 8 codes, 16 r, 32 Ap);
+// the rest evict_first (developer comparisons: CW_L2KEEP=63 keeps all)
+#ifndef CW_L2KEEP
+#define CW_L2KEEP 41
+#endif
+template <int BIT>
+__device__ __forceinline__ uint64_t l2_pol(uint64_t keep, uint64_t drop) {
+  return (CW_L2KEEP & BIT) ? keep : drop;
+}
 __device__ __forceinline__ uint64_t l2_evict_first() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
@@ -509,11 +518,11 @@ __device__ __forceinline__ void issue_A(const PcgArgs<T>& A, uint8_t* ring, uint
   const bool own = c.kk >= c.t.k0 && c.kk < c.t.k1;
   mbar_expect_tx(&full[s], L::BYTES_A_HALO + (own ? L::BYTES_A_X : 0u));
   const uint64_t keep = l2_evict_last(), drop = l2_evict_first();
-  tma_load_3d_hint(st + L::A_Z, &A.tm_z, &full[s], c.t.i0 - Halo<T>::SH, c.t.j0 - 1, c.kk, keep);
-  tma_load_3d_hint(st + L::A_P, tp, &full[s], c.t.i0 - Halo<T>::SH, c.t.j0 - 1, c.kk, drop);
+  tma_load_3d_hint(st + L::A_Z, &A.tm_z, &full[s], c.t.i0 - Halo<T>::SH, c.t.j0 - 1, c.kk, l2_pol<1>(keep, drop));
+  tma_load_3d_hint(st + L::A_P, tp, &full[s], c.t.i0 - Halo<T>::SH, c.t.j0 - 1, c.kk, l2_pol<2>(keep, drop));
   if (own) {
-    tma_load_3d_hint(st + L::A_X, &A.tm_x, &full[s], c.t.i0, c.t.j0, c.kk, drop);
-    tma_load_3d_hint(st + L::A_C, &A.tm_code_own, &full[s], c.t.i0, c.t.j0, c.kk, keep);
+    tma_load_3d_hint(st + L::A_X, &A.tm_x, &full[s], c.t.i0, c.t.j0, c.kk, l2_pol<4>(keep, drop));
+    tma_load_3d_hint(st + L::A_C, &A.tm_code_own, &full[s], c.t.i0, c.t.j0, c.kk, l2_pol<8>(keep, drop));
   }
 }
 
@@ -525,9 +534,10 @@ __device__ __forceinline__ void issue_B(const PcgArgs<T>& A, uint8_t* ring, uint
   uint8_t* st = ring + (size_t)s * L::STAGE;
   mbar_expect_tx(&full[s], L::BYTES_B);
   const uint64_t keep = l2_evict_last(), drop = l2_evict_first();
-  tma_load_3d_hint(st + L::B_R, tr, &full[s], c.t.i0 - Halo<double>::SH, c.t.j0 - 1, c.kk, drop);
-  tma_load_3d_hint(st + L::B_AP, &A.tm_ap, &full[s], c.t.i0 - Halo<T>::SH, c.t.j0 - 1, c.kk, keep);
-  tma_load_3d_hint(st + L::B_C, &A.tm_code, &full[s], c.t.i0 - Halo<uint8_t>::SH, c.t.j0 - 1, c.kk, keep);
+  tma_load_3d_hint(st + L::B_R, tr, &full[s], c.t.i0 - Halo<double>::SH, c.t.j0 - 1, c.kk, l2_pol<16>(keep, drop));
+  tma_load_3d_hint(st + L::B_AP, &A.tm_ap, &full[s], c.t.i0 - Halo<T>::SH, c.t.j0 - 1, c.kk, l2_pol<32>(keep, drop));
+  tma_load_3d_hint(st + L::B_C, &A.tm_code, &full[s], c.t.i0 - Halo<uint8_t>::SH, c.t.j0 - 1, c.kk,
+                   l2_pol<8>(keep, drop));
 }
 
 // A p' per cell.  float32 state: the difference form sum_a w_a (p_i - p_a)
@@ -850,9 +860,9 @@ __device__ void phaseA(const PcgArgs<T>& A, const Blk& blk, double* part, int se
           }
           if (rows && !(CW_ABL & 16)) {
             const int g = (kk - 1) * pplane + e;
-            stg4h<T>(pout + g, pcur, drop);
-            stg4h<T>(apout + g, apv, keep);
-            if (upd_x) stg4h<T>(xout + g, xn, drop);
+            stg4h<T>(pout + g, pcur, l2_pol<2>(keep, drop));
+            stg4h<T>(apout + g, apv, l2_pol<32>(keep, drop));
+            if (upd_x) stg4h<T>(xout + g, xn, l2_pol<4>(keep, drop));
             if (SLABS && A.nslab > 1) {   // boundary planes go to the neighbours' halo planes
               if (kk - 1 == A.o0 && A.lo.Ap) {
                 stg4<T>((pin_sel == 0 ? A.lo.p1 : A.lo.p0) + A.lo.plane_off + e, pcur);
@@ -1075,8 +1085,8 @@ __device__ void phaseB(const PcgArgs<T>& A, const Blk& blk, double* part, int se
             }
             if (rows && !(CW_ABL & 4)) {
               const int g = (kk - 1) * pplane + e;
-              stg4h<T>(zout + g, zv, keep);
-              if (write_r) stg4h<double>(rout + g, pv.r, drop);
+              stg4h<T>(zout + g, zv, l2_pol<1>(keep, drop));
+              if (write_r) stg4h<double>(rout + g, pv.r, l2_pol<16>(keep, drop));
               if (SLABS && A.nslab > 1) {   // boundary planes go to the neighbours' halo planes
                 if (kk - 1 == A.o0 && A.lo.z) {
                   stg4<T>(A.lo.z + A.lo.plane_off + e, zv);
