@@ -144,16 +144,19 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, u
       : "memory");
 }
 // L2 residency: the vectors re-read in the very next phase (z: B -> A, Ap:
-// A -> B) and the operator codes are stored / loaded evict_last so they stay in
-// the 126 MB L2 (36 MB at C3); the streams re-read only an iteration later (p,
-// x, r) are evict_first.  CW_L2HINT=0 drops the hints (developer comparison).
+// A -> B), x (own tile only, read and written once per iteration) and the
+// operator codes are stored / loaded evict_last so they stay in the 126 MB L2
+// (55 MB at C3); p and r (re-read an iteration later, r in fp64) are
+// evict_first.  Measured at C3 (5 steady steps, k_pcg per step): this 3836 us,
+// x evict_first 3868, everything evict_last 3869, r also kept 3846, p also
+// kept 3895, no hints 3913.  CW_L2HINT=0 drops the hints (developer comparison).
 #ifndef CW_L2HINT
 #define CW_L2HINT 1
 #endif
 // which streams are evict_last (bits: 1 z, 2 p, 4 x, 8 codes, 16 r, 32 Ap);
 // the rest evict_first (developer comparisons: CW_L2KEEP=63 keeps all)
 #ifndef CW_L2KEEP
-#define CW_L2KEEP 41
+#define CW_L2KEEP 45
 #endif
 template <int BIT>
 __device__ __forceinline__ uint64_t l2_pol(uint64_t keep, uint64_t drop) {
