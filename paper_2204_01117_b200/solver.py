@@ -263,18 +263,20 @@ class HostStepper:
     field), and overlap across the two copy directions: a piece of step s+1
     starts uploading as soon as the same piece of step s is back in host
     memory, while the later pieces are still coming down.  The step starts
-    once u, v, w, k and omega are up; nu_t and p travel last and the step
-    waits for them only before its first stage that uses them (the diffusion
-    and the first boundary pass, ``cw_step_defer``), so their copies overlap
-    the advection.  ``synchronize()`` waits for the last download.
+    once u, v, w are up; nu_t, p, k and omega travel later and the step
+    waits for each only before its first stage that uses it (the diffusion,
+    the first boundary pass, and for k / omega the upwind step moved behind
+    the projection: ``cw_step_defer``, ``cw_step_defer_kw``), so their copies
+    overlap the step.  ``synchronize()`` waits for the last download.
     """
 
     CHUNKS = 1   # pieces per field (4 measured the same at C3: the duplex link is the limit)
-    LATE = ("nu_t", "p")   # fields whose upload may overlap the start of the step, in use order
+    LATE = ("nu_t", "p", "k", "omega")   # fields whose upload may overlap the step, in use order
 
     def __init__(self, state: FlowState, host: dict):
         from .grid import FIELDS
-        assert set(self.LATE) in (set(), {"nu_t", "p"}), "cw_step_defer knows nu_t and p"
+        assert self.LATE in ((), ("nu_t", "p"), ("nu_t", "p", "k", "omega")), \
+            "cw_step_defer knows nu_t and p, cw_step_defer_kw k and omega"
         self.names = tuple(n for n in FIELDS if n not in self.LATE) + tuple(self.LATE)
         self._n_early = len(self.names) - len(self.LATE)
         self.state = state
@@ -305,7 +307,7 @@ class HostStepper:
                     ev.record(self._up)
                     ready[None if nf == self._n_early else self.names[nf - 1]] = ev
         cur.wait_event(ready[None])
-        defer = (ready["nu_t"], ready["p"]) if "nu_t" in ready and "p" in ready else None
+        defer = (ready["nu_t"], ready["p"], ready.get("omega")) if "nu_t" in ready and "p" in ready else None
         rep = step(self.state, params, psys, preconditioner, profile, pcg_tol=pcg_tol, _defer=defer)
         done = torch.cuda.Event()
         done.record(cur)
