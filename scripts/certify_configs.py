@@ -106,9 +106,57 @@ def certify_objective(name, amp=1e-6, seed=0):
             "oracle_seconds": round(time.perf_counter() - t0, 1)}
 
 
+def certify_eval(name, amp=1e-6, seed=0):
+    """One design evaluation's noise floor: the reference algorithm's loss and
+    region speeds at the golden's design with fp32-level noise on the state
+    after every step, and the per-step PCG counts, against the reference's
+    own evaluate_objective (cfg_<name>.npz from make_golden_configs EVAL)."""
+    sys.path.insert(0, os.path.join(ROOT, "scripts"))
+    import make_golden_configs as mg
+    doc = mg.EVAL[name]()
+    comp = co.Compiled(co.scene_from_dict(doc))
+    theta = np.array([p["initial"] for p in doc["design"]])
+    rng = np.random.default_rng(seed)
+    orig = co.step
+    its = []
+
+    def noisy(st, *a, **k):
+        rep = orig(st, *a, **k)
+        its.append(rep.pcg.iterations)
+        for f in ("u", "v", "w", "k", "omega", "nu_t"):
+            x = getattr(st, f)
+            setattr(st, f, x * (1 + amp * rng.standard_normal(x.shape)))
+        return rep
+
+    co.step = noisy
+    t0 = time.perf_counter()
+    try:
+        res = co.evaluate_objective(comp, theta)
+    finally:
+        co.step = orig
+    loss, speeds = res[0], np.asarray(res[1], float)
+    path = os.path.join(GOLD, f"cfg_{name}.npz")
+    while not os.path.exists(path):   # the reference's own run may still be going
+        time.sleep(60)
+    time.sleep(5)
+    g = np.load(path)
+    gold_its = g["pcg_iterations"].tolist()
+    moved = [i + 1 for i, (a, b) in enumerate(zip(its, gold_its)) if a != b]
+    return {"noise": amp, "loss": loss, "golden_loss": float(g["loss"]),
+            "loss_floor_rel": [abs(loss - float(g["loss"])) / abs(float(g["loss"]))],
+            "speed_floor_rel": (np.abs(speeds - g["region_speeds"]) / np.abs(g["region_speeds"])).tolist(),
+            "mismatched_steps": moved, "certified": not moved,
+            "oracle_seconds": round(time.perf_counter() - t0, 1)}
+
+
 def main():
     for name in sys.argv[1:]:
-        res = certify_objective(name) if name in ("chopt_opt_120", "c4_city_96") else certify(name)
+        if name.endswith("_eval"):
+            res = certify_eval(name)
+        elif name in ("chopt_opt_120", "c4_city_96"):
+            res = certify_objective(name)
+        else:
+            res = certify(name)
         print(name, res, flush=True)
         with open(os.path.join(GOLD, f"cert_{name}.json"), "w") as fh:
             json.dump(res, fh, indent=1, sort_keys=True)

@@ -24,6 +24,8 @@ Fixtures (tests/golden/cfg_<name>.npz; arrays x-fastest, (nz, ny, nx[+1])):
                     max_iter 2 (eps 0.1, lam 1), every FD gradient recorded
     c4_city_96      C4 recipe (16 extent parameters, 6 regions) at 96x96x24,
                     dt 0.2, settle 120: gradient_descent max_iter 1
+* one evaluate_objective of the C4 recipe at 256x256x64 (c4_city_256_eval):
+  loss, region speeds and the per-step PCG counts at the initial design
 
 Reference runs use OPENBLAS_NUM_THREADS=1 and never write into
 the read-only reference tree.
@@ -94,6 +96,13 @@ TRAJ = {
 OPT = {
     "chopt_opt_120": (lambda: chopt(120), 2),
     "c4_city_96": (c4_96, 1),
+}
+# one design evaluation through the reference's own optimize.evaluate_objective
+# at the initial design (per-step PCG counts recorded):
+#   c4_city_256_eval  the C4 recipe at BASELINE.json's 256x256x64 (bench.py's
+#                     design_eval scene), settle 120
+EVAL = {
+    "c4_city_256_eval": lambda: scenes.block_city_design(256, 256, 64, 2.0, 0, 6, 0.2, settle_steps=120),
 }
 
 
@@ -177,14 +186,45 @@ def run_opt(name):
     print(f"{name}: {wall:.1f}s history={res.history} grads={grads} thetas={res.theta_history}")
 
 
+def run_eval(name):
+    import citywind.optimize as opt
+    from citywind.scenario import CompiledScenario, scenario_from_dict
+    doc = EVAL[name]()
+    sc = scenario_from_dict(doc, base_dir=".")
+    comp = CompiledScenario.compile(sc)
+    theta = np.array([p.initial for p in sc.design])
+    its = []
+    orig = opt.step
+
+    def recording(state, *a, **k):
+        rep = orig(state, *a, **k)
+        its.append(rep.pcg.iterations)
+        print(f"{name} step {len(its)}: it={rep.pcg.iterations} kmax={float(state.k.max()):.3g}", flush=True)
+        return rep
+
+    opt.step = recording
+    t0 = time.perf_counter()
+    try:
+        ev = opt.evaluate_objective(comp, theta)
+    finally:
+        opt.step = orig
+    wall = time.perf_counter() - t0
+    np.savez_compressed(os.path.join(OUT, f"cfg_{name}.npz"), doc=np.array(json.dumps(doc)), theta=theta,
+                        loss=np.array(ev.loss), region_speeds=np.array(ev.region_speeds),
+                        pcg_iterations=np.array(its), wall_seconds=np.array(wall))
+    print(f"{name}: {wall:.1f}s loss={ev.loss} speeds={ev.region_speeds} iters={its}")
+
+
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--only", required=True, choices=sorted(TRAJ) + sorted(OPT))
+    ap.add_argument("--only", required=True, choices=sorted(TRAJ) + sorted(OPT) + sorted(EVAL))
     a = ap.parse_args()
     os.makedirs(OUT, exist_ok=True)
     os.chdir(tempfile.mkdtemp())
     if a.only in TRAJ:
         run_traj(a.only)
+    elif a.only in EVAL:
+        run_eval(a.only)
     else:
         run_opt(a.only)
 

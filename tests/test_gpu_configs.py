@@ -12,7 +12,9 @@ against goldens made by the UNMODIFIED reference
 * src/scenarios/channel_opt.json's initial design (translate_x / translate_y
   bindings, scenario.py:394-398), 120 steps;
 * gradient_descent on channel_opt (settle 120) and the C4 16-parameter
-  recipe at 96x96x24 (FD gradient + one update).
+  recipe at 96x96x24 (FD gradient + one update);
+* one evaluate_objective of the C4 recipe at 256x256x64 (bench.py's design
+  evaluation): loss, region speeds and per-step PCG counts.
 
 Gates (north_star, with the SURVEY 8c noise-floor protocol): identical
 per-step PCG iteration counts on every scene the oracle certifies
@@ -188,3 +190,39 @@ def test_c2_canyon_500_steps_against_reference(prec):
     assert its[:horizon] == gold[:horizon]
     assert len(its) == 500
     assert max(kmax[99:]) > 1e10 and float(np.max(g["k_max"][99:])) > 1e10
+
+
+def test_c4_design_evaluation_256_matches_reference():
+    """One design evaluation of the C4 recipe at BASELINE.json's 256x256x64
+    (bench.py's design_eval scene: 16 extent parameters, 6 street regions,
+    settle 120) against the reference's own optimize.evaluate_objective at
+    the initial design (scripts/make_golden_configs.py EVAL): per-step PCG
+    counts identical (within one iteration on the steps the reference itself
+    moves under fp32-level noise, cert_c4_city_256_eval.json), loss and the
+    six trailing-window region speeds within 1e-4 or 5x the reference's own
+    floor."""
+    from paper_2204_01117_b200.optimize import evaluate_objective
+    from paper_2204_01117_b200.scenario import CompiledScenario, scenario_from_dict
+    from paper_2204_01117_b200.solver import make_initial_state, step_many
+    name = "c4_city_256_eval"
+    if not os.path.exists(os.path.join(GOLD, f"cfg_{name}.npz")):
+        pytest.skip("golden not generated")
+    g = _gold(name)
+    cert = _certified(name)
+    sc = scenario_from_dict(json.loads(str(g["doc"])))
+    comp = CompiledScenario.compile(sc)
+    theta = np.asarray(g["theta"], float)
+    ev = evaluate_objective(comp, theta)
+    st = make_initial_state(sc.grid, comp.voxelize_design_device(theta), None, sc.solver, sc.inlet,
+                            mode=sc.init_mode, dtype=comp.dtype, device=comp.device)
+    its = [r.pcg.iterations for r in step_many(st, sc.solver, comp.psys, comp.preconditioner, sc.inlet,
+                                                len(g["pcg_iterations"]), sc.pcg_tol)]
+    gold = g["pcg_iterations"].tolist()
+    moved = set(cert["mismatched_steps"]) if cert else set()
+    for s, (a, b) in enumerate(zip(its, gold), start=1):
+        assert a == b or (s in moved and abs(a - b) <= 1), (s, a, b)
+    lf = max(1e-4, 5.0 * max(cert["loss_floor_rel"])) if cert else 1e-4
+    assert abs(ev.loss - float(g["loss"])) <= lf * abs(float(g["loss"])), (ev.loss, float(g["loss"]), lf)
+    sf = np.maximum(1e-4, 5.0 * np.asarray(cert["speed_floor_rel"])) if cert else 1e-4
+    np.testing.assert_array_less(np.abs(ev.region_speeds - g["region_speeds"]),
+                                 sf * np.abs(g["region_speeds"]) + 1e-300)
