@@ -139,6 +139,8 @@ struct cw_ctx {
   BcOp* bc_ops = nullptr;     // bc_nf independent writes, then bc_no ordered ones
   int bc_nf = -1, bc_no = 0;
   size_t bc_cap[7] = {}, bc_ops_cap = 0;   // grow-only capacities (bytes)
+  void* bc_held = nullptr;    // > 256 * BC_ORD_PER_THREAD ordered writes: their values (k_bc_ord_gather)
+  size_t bc_held_cap = 0;
   // stage timing
   bool timing = false;
   // one-shot waits of the next enqueued step (cw_step_defer): first use of nu_t / p
@@ -439,6 +441,7 @@ extern "C" void cw_ctx_destroy(cw_ctx* c) {
     if (c->bc_list[q]) cudaFree(c->bc_list[q]);
   if (c->bc_count) cudaFree(c->bc_count);
   if (c->bc_ops) cudaFree(c->bc_ops);
+  if (c->bc_held) cudaFree(c->bc_held);
   if (c->ev_made)
     for (auto& e : c->ev) cudaEventDestroy(e);
   for (auto& e : c->pev) cudaEventDestroy(e);
@@ -686,7 +689,7 @@ static void compose_bc(cw_ctx* c, cudaStream_t st) {
   // temporaries in the context's grow-only scratch (slots 24..29; cw_voxelize uses the low slots)
   int* wmap = (int*)cw_internal_scratch(c, 29, (size_t)fo.off[7] * sizeof(int));
   BcOp* ops = (BcOp*)cw_internal_scratch(c, 28, (size_t)tot * sizeof(BcOp));
-  BcOp* outp = (BcOp*)cw_internal_scratch(c, 27, (size_t)(tot + ORD_CAP) * sizeof(BcOp));
+  BcOp* outp = (BcOp*)cw_internal_scratch(c, 27, 2 * (size_t)tot * sizeof(BcOp));
   uint8_t* flag = (uint8_t*)cw_internal_scratch(c, 26, (size_t)tot);
   if (!wmap || !ops || !outp || !flag) return;
   int nc[2] = {0, 0};
@@ -702,15 +705,20 @@ static void compose_bc(cw_ctx* c, cudaStream_t st) {
   }
   k_bc_compose_final<<<std::min(nblk(tot), grid), 256, 0, st>>>(ops, tot, wmap, fo, flag);
   k_bc_compose_conflict<<<std::min(nblk(tot), grid), 256, 0, st>>>(ops, tot, wmap, fo, flag);
-  k_bc_compose_compact<<<std::min(nblk(tot), grid), 256, 0, st>>>(ops, tot, flag, outp, outp + tot, ORD_CAP,
+  k_bc_compose_compact<<<std::min(nblk(tot), grid), 256, 0, st>>>(ops, tot, flag, outp, outp + tot, (int)tot,
                                                                    c->bc_count);
   ok = ok && cudaGetLastError() == cudaSuccess &&
        cudaMemcpyAsync(nc, c->bc_count, sizeof(nc), cudaMemcpyDeviceToHost, st) == cudaSuccess &&
        cudaStreamSynchronize(st) == cudaSuccess;
-  if (!ok || nc[1] > ORD_CAP) {
+  if (!ok) {
     cudaGetLastError();
     return;
   }
+  // more ordered writes than block 0 of the replay holds: a gather launch first
+  if (nc[1] > ORD_CAP && !grow(&c->bc_held, &c->bc_held_cap, (size_t)nc[1] * sizeof(double))) return;
+  if (getenv("CW_BC_DEBUG"))
+    fprintf(stderr, "cw: boundary pass composed: %d independent writes, %d ordered (%s)\n", nc[0], nc[1],
+            nc[1] > ORD_CAP ? "gather launch" : "replay block 0");
   const int n = nc[0];
   if (n + nc[1] > 0) {
     ok = grow((void**)&c->bc_ops, &c->bc_ops_cap, (size_t)(n + nc[1]) * sizeof(BcOp)) &&
@@ -752,11 +760,20 @@ static void launch_bc(cw_ctx* c, BcFields<T> F, const int8_t* lab, long long ver
                       cudaStream_t st, unsigned fmask = BC_ALL) {
   const Dims& d = c->d;
   if (have_bc_lists(c, lab, ver, st)) {
-    if (c->bc_nf >= 0) {   // the composed pass: one launch
+    if (c->bc_nf >= 0) {   // the composed pass: one launch (two with a large ordered set)
+      const T k_in = (T)prm->k_in, om_in = (T)prm->omega_in, nut_in = (T)(prm->k_in / prm->omega_in);
+      const BcOp* oops = c->bc_ops + c->bc_nf;
+      T* held = nullptr;
+      if (c->bc_no > 256 * BC_ORD_PER_THREAD) {
+        held = (T*)c->bc_held;
+        (k_bc_ord_gather<T><<<std::min(nblk(c->bc_no), 8 * c->num_sms), 256, 0, st>>>(
+             F, oops, c->bc_no, (const T*)c->uzx, (const T*)c->uzy, k_in, om_in, nut_in, fmask, held, c->gate),
+         ++c->launches);
+      }
       if (c->bc_nf + c->bc_no > 0)
         (k_bc_replay<T><<<1 + std::max(1, std::min(nblk(c->bc_nf), 8 * c->num_sms)), 256, 0, st>>>(
-             F, c->bc_ops, c->bc_nf, c->bc_ops + c->bc_nf, c->bc_no, (const T*)c->uzx, (const T*)c->uzy,
-             (T)prm->k_in, (T)prm->omega_in, (T)(prm->k_in / prm->omega_in), fmask, c->gate),
+             F, c->bc_ops, c->bc_nf, oops, c->bc_no, (const T*)c->uzx, (const T*)c->uzy, k_in, om_in, nut_in, fmask,
+             c->gate, held),
          ++c->launches);
       return;
     }

@@ -1020,15 +1020,31 @@ __device__ __forceinline__ T bc_value(const BcFields<T>& F, const BcOp& op, cons
 }
 
 constexpr int BC_ORD_PER_THREAD = 8;   // block 0: up to 256 * 8 ordered writes
+// more ordered writes than block 0 holds: their values are read by a launch
+// of their own first (k_bc_ord_gather into `held`), and k_bc_replay stores them
+template <typename T>
+__global__ void k_bc_ord_gather(BcFields<T> F, const BcOp* __restrict__ oops, int no, const T* __restrict__ uzx,
+                                const T* __restrict__ uzy, T k_in, T om_in, T nut_in, unsigned fmask, T* held,
+                                const int* gate) {
+  if (*gate) return;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < no; t += gridDim.x * blockDim.x)
+    if (fmask >> (oops[t].fk & 7) & 1u) held[t] = bc_value<T>(F, oops[t], uzx, uzy, k_in, om_in, nut_in);
+}
+
 // fmask: the fields (bit f) this launch writes -- a pass split by field
 // (cw_step_defer_kw) is the same writes: every op reads its own field only
 template <typename T>
 __global__ void __launch_bounds__(256) k_bc_replay(BcFields<T> F, const BcOp* __restrict__ fops, int nf,
                                                    const BcOp* __restrict__ oops, int no, const T* __restrict__ uzx,
                                                    const T* __restrict__ uzy, T k_in, T om_in, T nut_in,
-                                                   unsigned fmask, const int* gate) {
+                                                   unsigned fmask, const int* gate, const T* __restrict__ held = nullptr) {
   if (*gate) return;
-  if (blockIdx.x == 0) {
+  if (held) {   // the ordered writes' values were read by k_bc_ord_gather
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < no; t += gridDim.x * blockDim.x) {
+      const BcOp op = oops[t];
+      if (fmask >> (op.fk & 7) & 1u) bc_field<T>(F, op.fk & 7)[op.dst] = held[t];
+    }
+  } else if (blockIdx.x == 0) {
     T v[BC_ORD_PER_THREAD];
 #pragma unroll
     for (int s = 0; s < BC_ORD_PER_THREAD; ++s) {
@@ -1046,7 +1062,8 @@ __global__ void __launch_bounds__(256) k_bc_replay(BcFields<T> F, const BcOp* __
     }
     return;
   }
-  for (int t = (blockIdx.x - 1) * blockDim.x + threadIdx.x; t < nf; t += (gridDim.x - 1) * blockDim.x) {
+  const int b0 = held ? 0 : 1;   // without `held`, block 0 took the ordered writes
+  for (int t = (blockIdx.x - b0) * blockDim.x + threadIdx.x; t < nf; t += (gridDim.x - b0) * blockDim.x) {
     const BcOp op = fops[t];
     if (fmask >> (op.fk & 7) & 1u) bc_field<T>(F, op.fk & 7)[op.dst] = bc_value<T>(F, op, uzx, uzy, k_in, om_in, nut_in);
   }

@@ -117,22 +117,33 @@ def test_boundary_full_volume_path_without_labels_version(monkeypatch):
         np.testing.assert_array_equal(got[n], getattr(ost, n), err_msg=n)
 
 
-@pytest.mark.parametrize("layout", ["all_outlets", "mixed"])
-def test_composed_boundary_pass_equals_ordered_lists(layout, monkeypatch):
+@pytest.mark.parametrize("layout", ["all_outlets", "mixed", "random", "random_large"])
+def test_composed_boundary_pass_equals_ordered_lists(layout, monkeypatch, capfd):
     """One boundary pass is ONE k_bc_replay launch of the lists' composition
     (cw_step.cuh k_bc_compose_*): with outlets on every side (every edge and
     corner where a later side reads or overwrites an earlier side's write),
     an inlet face, walls and a wall touching the outlets, the result equals
     the oracle's ordered apply_boundary_conditions (solver.py:330-400) and
     the ordered per-side launches (CW_BC_COMPOSE=0) bit for bit in float64,
-    and bit for bit between the two paths in float32."""
+    and bit for bit between the two paths in float32 -- also on a box whose
+    edge lines carry more ordered writes than the replay's block 0 holds."""
     from oracle import citywind_oracle as co
     from paper_2204_01117_b200 import solver
-    doc = scenes.cuboid(22, 14, 9, 1.0, 0.1)
+    doc = scenes.cuboid(160, 160, 96, 1.0, 0.1) if layout == "random_large" else scenes.cuboid(22, 14, 9, 1.0, 0.1)
     sc = co.scene_from_dict(doc)
     g = sc.grid
     labels = co.classify_boundary(g, sc.faces)           # x-fastest (nz, ny, nx)
-    if layout == "all_outlets":
+    monkeypatch.setenv("CW_BC_DEBUG", "1")
+    if layout.startswith("random"):
+        # random outlet / wall / inlet / air cells on every boundary layer:
+        # edges where a later side's write does not cover an earlier side's
+        # read, i.e. ordered writes in the composition
+        rng = np.random.default_rng(7)
+        lab = rng.choice(np.array([4, 4, 4, 5, 3, 0], np.int8), size=labels.shape)
+        inner = (slice(1, -1),) * 3
+        lab[inner] = labels[inner]
+        labels = lab
+    elif layout == "all_outlets":
         labels[:, :, 0] = 4
         labels[:, :, -1] = 4
         labels[:, 0, :] = 4
@@ -164,3 +175,13 @@ def test_composed_boundary_pass_equals_ordered_lists(layout, monkeypatch):
                     np.testing.assert_array_equal(vals[prec, compose][n], getattr(ost, n), err_msg=f"{compose} {n}")
         for n in FIELDS:
             np.testing.assert_array_equal(vals[prec, "1"][n], vals[prec, "0"][n], err_msg=f"{prec} {n}")
+    # random boundary labels make ordered writes (box-shaped outlet sides
+    # make none: a later side always overwrites what it reads from an
+    # earlier one); block 0 of the replay holds up to 2048 of them, the large
+    # random box has more (a gather launch first)
+    err = capfd.readouterr().err
+    print(err)
+    if layout.startswith("random"):
+        assert "ordered" in err and " 0 ordered" not in err, err[-500:]
+    if layout == "random_large":
+        assert "gather launch" in err, err[-500:]
