@@ -1530,10 +1530,11 @@ __global__ void __launch_bounds__(256) k_turbulence_c(Dims d, const T* __restric
   const T dk = nu + sk, dw = nu + sw;
   const T kn = (kc + dt * (pk + dk * lk)) / ((T)1 + dt * (T)sc.c_mu * wc);
   const T wn = (wc + dt * ((T)2 * (T)sc.alpha * s2 + dw * lw)) / ((T)1 + dt * (T)sc.beta * wc);
-  if (k >= d.o0 && k < d.o1) {   // reference C order over the global grid
+  const bool bad_k = !isfinite(kn), bad_w = !isfinite(wn);
+  if ((bad_k || bad_w) && k >= d.o0 && k < d.o1) {   // reference C order over the global grid
     const long long refi = ((long long)i * d.ny + j) * d.nzg + (k + d.kg0);
-    if (!isfinite(kn)) atomicMin(&rep->bad_index[0], refi);
-    if (!isfinite(wn)) atomicMin(&rep->bad_index[1], refi);
+    if (bad_k) atomicMin(&rep->bad_index[0], refi);
+    if (bad_w) atomicMin(&rep->bad_index[1], refi);
   }
   const T kf = kn > (T)1e-12 ? kn : (T)1e-12;
   const T wf = wn > (T)1e-8 ? wn : (T)1e-8;
