@@ -287,7 +287,7 @@ def zslab_leg(args, dist, rank):
            "--warmup", str(args.warmup), "--dt", str(args.dt)]
     res, ok = {}, 1.0
     try:
-        out = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=900)
+        out = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=300)
         line = next((ln[6:] for ln in out.stdout.splitlines() if ln.startswith("ZSLAB ")), None)
         if out.returncode != 0:
             ok = 0.0
