@@ -256,6 +256,14 @@ int cw_set_max_iter(cw_ctx *ctx, int max_iter);
  * the step.  Synchronises `stream`. */
 int cw_turb_rollback(cw_ctx *ctx, const cw_fields *f, void *stream);
 
+/* After a step reported CW_ERR_PCG or CW_ERR_RHS: the state as the reference
+ * leaves it when project() raises (ref solver.py:272-276, linalg.py:326-327)
+ * -- u, v, w, nu_t, p after the first boundary pass (p is not replaced by a
+ * solve that fails), and with turbulence on, k and omega as advected this step
+ * with their boundary values (copied from the step's upwind buffers).
+ * Synchronises `stream`. */
+int cw_proj_rollback(cw_ctx *ctx, const cw_fields *f, int turbulence, void *stream);
+
 /* Per-stage device timings of the next cw_step call (ms per stage, keys of
  * StepReport.timings, ref solver.py:418-454): enable before, read after. */
 int cw_set_stage_timing(cw_ctx *ctx, int enabled);

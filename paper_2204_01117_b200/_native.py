@@ -134,6 +134,7 @@ SIGNATURES = {
     "cw_pcg_chunks": (C.c_int, [_P, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     "cw_ref_layout": (C.c_int, [_P, C.c_int, C.c_int, _P, _P, _P]),
     "cw_turb_rollback": (C.c_int, [_P, C.POINTER(cw_fields), _P]),
+    "cw_proj_rollback": (C.c_int, [_P, C.POINTER(cw_fields), C.c_int, _P]),
     "cw_set_stage_timing": (C.c_int, [_P, C.c_int]),
     "cw_read_stage_timings": (C.c_int, [_P, C.POINTER(C.c_float)]),
     "cw_pcg_timing": (C.c_int, [_P, C.c_int]),

@@ -757,7 +757,7 @@ constexpr unsigned BC_ALL = 0x7fu, BC_UVWP = 0x47u, BC_KWN = 0x38u;   // fields 
 // fmask != BC_ALL only with composed lists (callers check c->bc_nf >= 0)
 template <typename T>
 static void launch_bc(cw_ctx* c, BcFields<T> F, const int8_t* lab, long long ver, const cw_params* prm,
-                      cudaStream_t st, unsigned fmask = BC_ALL) {
+                      cudaStream_t st, unsigned fmask = BC_ALL, unsigned gate_pass = 0) {
   const Dims& d = c->d;
   if (have_bc_lists(c, lab, ver, st)) {
     if (c->bc_nf >= 0) {   // the composed pass: one launch (two with a large ordered set)
@@ -767,13 +767,14 @@ static void launch_bc(cw_ctx* c, BcFields<T> F, const int8_t* lab, long long ver
       if (c->bc_no > 256 * BC_ORD_PER_THREAD) {
         held = (T*)c->bc_held;
         (k_bc_ord_gather<T><<<std::min(nblk(c->bc_no), 8 * c->num_sms), 256, 0, st>>>(
-             F, oops, c->bc_no, (const T*)c->uzx, (const T*)c->uzy, k_in, om_in, nut_in, fmask, held, c->gate),
+             F, oops, c->bc_no, (const T*)c->uzx, (const T*)c->uzy, k_in, om_in, nut_in, fmask, held, c->gate,
+             gate_pass),
          ++c->launches);
       }
       if (c->bc_nf + c->bc_no > 0)
         (k_bc_replay<T><<<1 + std::max(1, std::min(nblk(c->bc_nf), 8 * c->num_sms)), 256, 0, st>>>(
              F, c->bc_ops, c->bc_nf, oops, c->bc_no, (const T*)c->uzx, (const T*)c->uzy, k_in, om_in, nut_in, fmask,
-             c->gate, held),
+             c->gate, held, gate_pass),
          ++c->launches);
       return;
     }
@@ -1100,12 +1101,16 @@ static int enqueue_step(cw_ctx* c, const cw_fields* f, const cw_params* prm, dou
   int rc = st_project<T>(c, P, f, prm, tol, rep, st);         // "project"
   if (rc) return rc;
   if (defer_kw) {   // the deferred k / omega part of the step, same writes
+    // it also runs after a failed projection (device status 1 or 4): the
+    // reference has advected k, omega and written their boundary values
+    // before project() raises
+    constexpr unsigned PASS = (1u << 1) | (1u << 4);
     CW_CUDA(cudaStreamWaitEvent(st, c->wait_kw, 0));
     c->wait_kw = nullptr;
     if (turb)
       (k_upwind_saved<T><<<g3(c->d.nx, c->d.ny, c->d.nz), B3, 0, st>>>(c->d, acell, P.k, P.om, (T*)c->tk, (T*)c->tw,
-                                                                       (T)prm->dt, c->gate), ++c->launches);
-    launch_bc<T>(c, F1, P.lab, P.lab_ver, prm, st, BC_KWN);
+                                                                       (T)prm->dt, c->gate, PASS), ++c->launches);
+    launch_bc<T>(c, F1, P.lab, P.lab_ver, prm, st, BC_KWN, PASS);
   }
   mark(5);
   if (turb) st_turb<T>(c, P, prm, B.k, B.om, rep, st);        // "turbulence"
@@ -1673,6 +1678,26 @@ extern "C" int cw_turb_rollback(cw_ctx* c, const cw_fields* f, void* stream) {
     (k_turb_rollback<double><<<nb, 256, 0, S(stream)>>>(c->ncell, (const double*)c->tk, (const double*)c->tw,
         (const double*)c->speed, (double*)f->k, (double*)f->omega, (double*)f->nu_t), ++c->launches);
   CW_CUDA(cudaGetLastError());
+  CW_CUDA(cudaStreamSynchronize(S(stream)));
+  return CW_OK;
+}
+
+extern "C" int cw_proj_rollback(cw_ctx* c, const cw_fields* f, int turbulence, void* stream) {
+  if (!c || !f) return fail(CW_ERR_INVALID, "null argument");
+  CW_CUDA(cudaSetDevice(c->device));
+  if (turbulence) {   // k, omega as advected this step (their boundary values written); nu_t untouched
+    const int nb = std::min(nblk(c->ncell), 4 * c->num_sms * 8);
+    if (c->prec == 4)
+      (k_turb_rollback<float><<<nb, 256, 0, S(stream)>>>(c->ncell, (const float*)c->tk, (const float*)c->tw, nullptr,
+                                                          (float*)f->k, (float*)f->omega, (float*)f->nu_t),
+       ++c->launches);
+    else
+      (k_turb_rollback<double><<<nb, 256, 0, S(stream)>>>(c->ncell, (const double*)c->tk, (const double*)c->tw,
+                                                           nullptr, (double*)f->k, (double*)f->omega,
+                                                           (double*)f->nu_t),
+       ++c->launches);
+    CW_CUDA(cudaGetLastError());
+  }
   CW_CUDA(cudaStreamSynchronize(S(stream)));
   return CW_OK;
 }

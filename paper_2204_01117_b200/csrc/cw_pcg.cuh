@@ -766,8 +766,6 @@ __device__ void phase0(const PcgArgs<T>& A, double* part, int set, unsigned seq,
           const double ab = fabs(b), ad = fabs(div);
           bmax = (ab > bmax || ab != ab) ? ab : bmax;
           dmax = (ad > dmax || ad != ad) ? ad : dmax;
-        } else if (i + c < d.nx) {
-          A.state_p[c0 + c] = (T)0;   // project() sets p = 0 off the unknowns (solver.py:278-280)
         }
       }
       stg4<double>(A.r0 + g, rv);
@@ -1158,7 +1156,9 @@ __device__ void phaseB(const PcgArgs<T>& A, const Blk& blk, double* part, int se
   __syncthreads();
 }
 
-// final: state p = x (+ alpha p pending) on the unknowns, x quads (4 planes in flight)
+// final, after a converged solve: state p = x (+ alpha p pending) on the
+// unknowns and 0 elsewhere (project() replaces p, solver.py:278-280); a solve
+// that does not converge leaves p as it was (project() raises first)
 template <typename T>
 __device__ void finish_x(const PcgArgs<T>& A, int unit, T alpha, const T* __restrict__ p, bool zero) {
   const Dims& d = A.d;
@@ -1178,8 +1178,8 @@ __device__ void finish_x(const PcgArgs<T>& A, int unit, T alpha, const T* __rest
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       if (i + q >= d.nx) break;
-      if (zero) A.state_p[c + q] = (T)0;
-      else if ((cw4 >> (8 * q + 6)) & 1u) A.state_p[c + q] = alpha != (T)0 ? xv[q] + alpha * pv[q] : xv[q];
+      if (zero || !((cw4 >> (8 * q + 6)) & 1u)) A.state_p[c + q] = (T)0;
+      else A.state_p[c + q] = alpha != (T)0 ? xv[q] + alpha * pv[q] : xv[q];
     }
   }
 }
@@ -1443,7 +1443,8 @@ __device__ __forceinline__ void pcg_body(const PcgArgs<T>& A, const Blk& blk, ui
   }
   // state p = x, plus the alpha p of the last completed iteration if pending
   const T* plast = psel == 0 ? A.p0 : A.p1;
-  for (int u = blk.id; u < U; u += B) finish_x<T>(A, u, (T)alpha, plast, false);
+  if (converged)
+    for (int u = blk.id; u < U; u += B) finish_x<T>(A, u, (T)alpha, plast, false);
   if (lead) {
     rep->iterations = it;
     rep->converged = converged;

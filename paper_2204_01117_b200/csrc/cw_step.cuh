@@ -129,11 +129,19 @@ __device__ __forceinline__ void upwind_cell(const Dims& d, const T* __restrict__
 }
 
 // the upwind step from a saved cell-centred velocity (cw_step_defer_kw)
+// gate_pass: device statuses (bit s) the launch runs through -- the
+// deferred k / omega part runs after a failed projection too, so the state
+// ends as the reference leaves it when project() raises (advected k, omega)
+__device__ __forceinline__ bool gated(const int* gate, unsigned gate_pass) {
+  const int g = *gate;
+  return g != 0 && !((gate_pass >> (g & 31)) & 1u);
+}
+
 template <typename T>
 __global__ void k_upwind_saved(Dims d, const T* __restrict__ acell, const T* __restrict__ kin,
                                const T* __restrict__ win, T* __restrict__ kout, T* __restrict__ wout, T dt,
-                               const int* gate) {
-  if (*gate) return;
+                               const int* gate, unsigned gate_pass = 0) {
+  if (gated(gate, gate_pass)) return;
   CW_IJK(d.nx, d.ny, d.nz, inb);
   if (!inb) return;
   const long long ncell = (long long)d.nx * d.ny * d.nz;
@@ -1025,8 +1033,8 @@ constexpr int BC_ORD_PER_THREAD = 8;   // block 0: up to 256 * 8 ordered writes
 template <typename T>
 __global__ void k_bc_ord_gather(BcFields<T> F, const BcOp* __restrict__ oops, int no, const T* __restrict__ uzx,
                                 const T* __restrict__ uzy, T k_in, T om_in, T nut_in, unsigned fmask, T* held,
-                                const int* gate) {
-  if (*gate) return;
+                                const int* gate, unsigned gate_pass = 0) {
+  if (gated(gate, gate_pass)) return;
   for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < no; t += gridDim.x * blockDim.x)
     if (fmask >> (oops[t].fk & 7) & 1u) held[t] = bc_value<T>(F, oops[t], uzx, uzy, k_in, om_in, nut_in);
 }
@@ -1037,8 +1045,9 @@ template <typename T>
 __global__ void __launch_bounds__(256) k_bc_replay(BcFields<T> F, const BcOp* __restrict__ fops, int nf,
                                                    const BcOp* __restrict__ oops, int no, const T* __restrict__ uzx,
                                                    const T* __restrict__ uzy, T k_in, T om_in, T nut_in,
-                                                   unsigned fmask, const int* gate, const T* __restrict__ held = nullptr) {
-  if (*gate) return;
+                                                   unsigned fmask, const int* gate, const T* __restrict__ held = nullptr,
+                                                   unsigned gate_pass = 0) {
+  if (gated(gate, gate_pass)) return;
   if (held) {   // the ordered writes' values were read by k_bc_ord_gather
     for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < no; t += gridDim.x * blockDim.x) {
       const BcOp op = oops[t];
@@ -1559,7 +1568,7 @@ __global__ void k_turb_rollback(long long n, const T* __restrict__ k_adv, const 
   CW_GRID_STRIDE(c, n) {
     k[c] = k_adv[c];
     w[c] = w_adv[c];
-    nut[c] = nut_prev[c];
+    if (nut_prev) nut[c] = nut_prev[c];
   }
 }
 

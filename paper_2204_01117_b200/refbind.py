@@ -213,10 +213,26 @@ class RefStepper:
         finally:
             s.psys.pool.release(ctx)
         s.dev.touch()
-        # 2. one device step
-        rep = _dev_step(s.dev, prm, s.psys, pre, _profile(profile), pcg_tol=pcg_tol,
-                        _defer=(late["nu_t"], late["p"], late["omega"]))
-        # 3. device layout -> float64 C order -> pinned host arrays
+        # 2. one device step.  If it raises, the reference's step has already
+        # reassigned the state's arrays (solver.py:423-425 onwards) and left
+        # them as they are at the raise; the device state is rolled back to
+        # exactly that (solver._rollback), so it is downloaded before the
+        # exception propagates, without advancing time / step_count
+        try:
+            rep = _dev_step(s.dev, prm, s.psys, pre, _profile(profile), pcg_tol=pcg_tol,
+                            _defer=(late["nu_t"], late["p"], late["omega"]))
+        except Exception:
+            self._download(s, state, pre)
+            raise
+        self._download(s, state, pre)
+        state.time += prm.dt
+        state.step_count += 1
+        return rep
+
+    def _download(self, s: _Slot, state, pre) -> None:
+        """device layout -> float64 C order -> pinned host arrays assigned to
+        the state's attributes."""
+        lib = N.lib()
         out, out_np = s.pin_out[s.out_set], s.np_out[s.out_set]
         ctx = s.psys.pool.acquire(s.grid, s.psys.labels_on(self.device), pre.omega, pre.kind, self.dtype,
                                   self.device)
@@ -238,9 +254,6 @@ class RefStepper:
             setattr(state, n, out_np[n])
             s.ours[n] = id(out_np[n])
         s.out_set ^= 1
-        state.time += prm.dt
-        state.step_count += 1
-        return rep
 
 
 _default = None

@@ -219,12 +219,19 @@ def _raise_for(rc: int, rep, grid: GridSpec):
     N.check(rc)
 
 
-def _rollback(ctx, f, rep):
-    """A non-finite turbulence update: leave the state as the reference does
-    when update_turbulence raises (turbulence.py:121-131, before it assigns):
-    advected k and omega, the previous nu_t (``cw_turb_rollback``)."""
+def _rollback(ctx, f, rep, step_turbulence=None):
+    """Leave the state as the reference does when a step raises.
+    * A non-finite turbulence update (turbulence.py:121-131, raised before it
+      assigns): advected k and omega, the previous nu_t (``cw_turb_rollback``).
+    * A failed projection inside a full step (solver.py:272-276, ProjectionError
+      or the non-finite right-hand side's ValueError): p untouched by the
+      solve, and with turbulence on the step's advected k and omega
+      (``cw_proj_rollback``); ``step_turbulence`` is None for a stand-alone
+      project(), which touches neither."""
     if rep.status == N.CW_ERR_NONFINITE:
         N.check(N.lib().cw_turb_rollback(ctx.h, C.byref(f), ctx.stream))
+    elif rep.status in (N.CW_ERR_PCG, N.CW_ERR_RHS) and step_turbulence is not None:
+        N.check(N.lib().cw_proj_rollback(ctx.h, C.byref(f), int(bool(step_turbulence)), ctx.stream))
 
 
 def _report_of(r, timings) -> StepReport:
@@ -341,6 +348,7 @@ def step_many(state: FlowState, params: SolverParams, psys: PressureSystem, prec
     if dt == 0.0 or nsteps <= 0:
         return [StepReport() for _ in range(max(nsteps, 0))]
     _warn_cap(state, params, dt)
+    state._turbulence = bool(params.turbulence)   # for finish(): the failed step's rollback
     ctx = _acquire(psys, preconditioner, state)
     state.touch()
     try:
@@ -386,7 +394,7 @@ def step_many(state: FlowState, params: SolverParams, psys: PressureSystem, prec
                 timings = {k: float(ms[i]) * 1e-3 for i, k in enumerate(STAGE_KEYS)}
             for r in reps:
                 if r.status != N.CW_OK:
-                    _rollback(ctx, f, r)
+                    _rollback(ctx, f, r, params.turbulence)
                     _raise_for(r.status, r, state.grid)
                 reports.append(_report_of(r, dict(timings)))
                 state.time += dt
@@ -410,7 +418,7 @@ def finish(state: FlowState, psys: PressureSystem, preconditioner, nsteps: int):
         rc, reps = ctx.read_reports(nsteps)
         for r in reps:
             if r.status != N.CW_OK:
-                _rollback(ctx, ctx.fields(state, state._g, state._has_drag), r)
+                _rollback(ctx, ctx.fields(state, state._g, state._has_drag), r, getattr(state, "_turbulence", True))
                 _raise_for(r.status, r, state.grid)
         return [_report_of(r, {}) for r in reps]
     finally:

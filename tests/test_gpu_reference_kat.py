@@ -320,3 +320,53 @@ def test_singular_system_raises():
                                 "y_min": CellLabel.SOLID_WALL, "y_max": CellLabel.SOLID_WALL})
     with pytest.raises(SingularSystemError):
         build_pressure_matrix(g, lab)
+
+
+@pytest.mark.parametrize("turbulence", [True, False])
+def test_failed_projection_leaves_the_reference_state(turbulence):
+    """A step whose projection does not converge (pcg_tol 0: no criterion is
+    below it, so 10000 iterations, solver.py:272-276) raises ProjectionError
+    with the state as the
+    reference leaves it: u, v, w, nu_t and p after the first boundary pass
+    (the failed solve does not replace p) and k, omega as advected this step
+    (cw_proj_rollback); float64 against the oracle, directly and through the
+    reference-layout binding (refbind, where k / omega are uploaded behind the
+    projection, cw_step_defer_kw)."""
+    import types
+
+    from oracle import citywind_oracle as co
+    from helpers import FIELDS, device_params, device_state, device_system, oracle_compiled
+    from paper_2204_01117_b200 import scenes
+    from paper_2204_01117_b200.errors import ProjectionError
+    from paper_2204_01117_b200.refbind import RefStepper
+    doc = scenes.cuboid(24, 20, 12, 2.0, 0.3)
+    doc["solver"]["turbulence"] = turbulence
+    comp = oracle_compiled(doc)
+    sc = comp.scene
+    ost = comp.make_state()
+    comp.step_state(ost)                                  # a state with a pressure field
+    dst = device_state(ost, torch.float64)
+    ref = lambda a: np.ascontiguousarray(np.asarray(a).transpose(2, 1, 0))   # noqa: E731
+    og = sc.grid
+    rst = types.SimpleNamespace(
+        grid=types.SimpleNamespace(nx=og.nx, ny=og.ny, nz=og.nz, dx=og.dx, dy=og.dy, dz=og.dz, origin=tuple(og.origin)),
+        time=1.0, step_count=1, labels=ref(ost.labels).astype(np.int8),
+        porosity=types.SimpleNamespace(phi=ref(ost.phi), lad=ref(ost.lad)))
+    for n in FIELDS:
+        setattr(rst, n, ref(getattr(ost, n)).astype(np.float64))
+    with pytest.raises(co.ProjectionError):
+        co.step(ost, sc.params, comp.psys, comp.W, sc.inlet, 0.0)
+    psys, pre = device_system(comp)
+    p, prof = device_params(sc)
+    with pytest.raises(ProjectionError):
+        solver.step(dst, p, psys, pre, prof, pcg_tol=0.0)
+    stepper = RefStepper(dtype=torch.float64, ai_omega=sc.ai_omega)
+    with pytest.raises(ProjectionError):
+        stepper.step(rst, p, None, types.SimpleNamespace(name="ai1"), prof, None, 0.0)
+    assert rst.step_count == 1 and rst.time == 1.0
+    for n in FIELDS:
+        want = getattr(ost, n)
+        got = dst.fields[n].cpu().numpy()
+        scale = max(float(np.abs(want).max()), 1e-30)
+        assert float(np.abs(got - want).max()) <= 1e-9 * scale, n
+        assert float(np.abs(ref(getattr(rst, n)) - want).max()) <= 1e-9 * scale, n
