@@ -222,7 +222,10 @@ class RefStepper:
             rep = _dev_step(s.dev, prm, s.psys, pre, _profile(profile), pcg_tol=pcg_tol,
                             _defer=(late["nu_t"], late["p"], late["omega"]))
         except Exception:
-            self._download(s, state, pre)
+            try:
+                self._download(s, state, pre)
+            except Exception:   # a failed download must not mask the step's exception
+                pass
             raise
         self._download(s, state, pre)
         state.time += prm.dt
