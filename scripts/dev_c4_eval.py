@@ -1,4 +1,8 @@
+"""Developer check: one C4 design evaluation at 256x256x64 against the
+reference golden (loss, region speeds, per-step counts); argument fp64 runs
+the device in float64.  Usage: python scripts/dev_c4_eval.py [fp64]"""
 import json, os, sys
+import torch
 import numpy as np
 sys.path.insert(0, "/root/repo")
 from paper_2204_01117_b200.optimize import evaluate_objective
@@ -6,7 +10,7 @@ from paper_2204_01117_b200.scenario import CompiledScenario, scenario_from_dict
 from paper_2204_01117_b200.solver import make_initial_state, step_many
 g = np.load("tests/golden/cfg_c4_city_256_eval.npz")
 sc = scenario_from_dict(json.loads(str(g["doc"])))
-comp = CompiledScenario.compile(sc)
+comp = CompiledScenario.compile(sc, dtype=torch.float64 if "fp64" in sys.argv else torch.float32)
 theta = np.asarray(g["theta"], float)
 ev = evaluate_objective(comp, theta)
 print("loss", ev.loss, float(g["loss"]), "rel", abs(ev.loss - float(g["loss"])) / float(g["loss"]))

@@ -231,3 +231,53 @@ def test_c4_design_evaluation_256_matches_reference():
     sf = np.maximum(1e-4, 5.0 * np.asarray(cert["speed_floor_rel"])) if cert else 1e-4
     np.testing.assert_array_less(np.abs(ev.region_speeds - g["region_speeds"]),
                                  sf * np.abs(g["region_speeds"]) + 1e-300)
+
+
+@pytest.mark.parametrize("name", TRAJ)
+def test_config_trajectory_fp64_tracks_reference(name):
+    """The same device kernels in float64 (the reference's precision) on every
+    config trajectory: identical per-step PCG counts and per-step field L2
+    norms (stored by the golden in float64) within 1e-12 relative at every
+    step (measured: <= 9e-15, scripts/dev_fp64_norms.py) -- C1's 200 steps and
+    the chaotic channel_opt included.  The fp32 deviations gated above are
+    arithmetic precision, not algorithm."""
+    from paper_2204_01117_b200 import solver
+    from paper_2204_01117_b200.scenario import CompiledScenario, scenario_from_dict
+    g = _gold(name)
+    sc = scenario_from_dict(json.loads(str(g["doc"])))
+    comp = CompiledScenario.compile(sc, dtype=torch.float64)
+    st = comp.make_state(g["theta"] if g["theta"].size else None)
+    steps = int(g["steps"])
+    iters, norms = [], {n: [] for n in FIELDS}
+    for _ in range(steps):
+        iters.append(solver.step_many(st, sc.solver, comp.psys, comp.preconditioner, sc.inlet, 1,
+                                      sc.pcg_tol)[0].pcg.iterations)
+        for n in FIELDS:
+            norms[n].append(float(torch.linalg.vector_norm(st.fields[n])))
+    assert iters == g["pcg_iterations"].tolist()
+    for n in FIELDS:
+        np.testing.assert_allclose(norms[n], g[f"norm_{n}"], rtol=1e-12, err_msg=n)
+
+
+def test_c4_design_evaluation_256_fp64_matches_reference_to_machine_precision():
+    """The C4 evaluation at 256x256x64 on the device in float64: all 120
+    per-step PCG counts identical to the reference's, loss and region speeds
+    within 1e-12 relative (measured 1.6e-15, scripts/dev_c4_eval.py fp64)."""
+    from paper_2204_01117_b200.optimize import evaluate_objective
+    from paper_2204_01117_b200.scenario import CompiledScenario, scenario_from_dict
+    from paper_2204_01117_b200.solver import make_initial_state, step_many
+    name = "c4_city_256_eval"
+    if not os.path.exists(os.path.join(GOLD, f"cfg_{name}.npz")):
+        pytest.skip("golden not generated")
+    g = _gold(name)
+    sc = scenario_from_dict(json.loads(str(g["doc"])))
+    comp = CompiledScenario.compile(sc, dtype=torch.float64)
+    theta = np.asarray(g["theta"], float)
+    ev = evaluate_objective(comp, theta)
+    assert abs(ev.loss - float(g["loss"])) <= 1e-12 * abs(float(g["loss"]))
+    np.testing.assert_allclose(ev.region_speeds, g["region_speeds"], rtol=1e-12)
+    st = make_initial_state(sc.grid, comp.voxelize_design_device(theta), None, sc.solver, sc.inlet,
+                            mode=sc.init_mode, dtype=comp.dtype, device=comp.device)
+    its = [r.pcg.iterations for r in step_many(st, sc.solver, comp.psys, comp.preconditioner, sc.inlet,
+                                                len(g["pcg_iterations"]), sc.pcg_tol)]
+    assert its == g["pcg_iterations"].tolist()
