@@ -251,7 +251,10 @@ def zslab_child(args):
     sc = scenario_from_dict(doc)
     comp = CompiledScenario.compile(sc, dtype=torch.float32)
     state = comp.make_state()
-    sol = DistSlabSolver(state, sc.solver, sc.inlet, omega=sc.ai_omega, pcg_tol=sc.pcg_tol)
+    # a 6-plane halo covers the step's reach for max|w| dt/dz < 2 (2 floor(S) + 4,
+    # DESIGN.md 5) when the slabs are deep enough to feed it, else the default 4
+    halo = 6 if sc.grid.nz // world >= 6 else DEFAULT_HALO
+    sol = DistSlabSolver(state, sc.solver, sc.inlet, omega=sc.ai_omega, pcg_tol=sc.pcg_tol, halo=halo)
     del state
     sol.step_many(args.warmup)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -268,7 +271,7 @@ def zslab_child(args):
         print("ZSLAB " + json.dumps({
             "value": ncell * args.steps / (ms * 1e-3), "ms_per_step": ms / args.steps,
             "pcg_iterations": [r.pcg.iterations for r in reps], "slabs": world,
-            "planes_per_slab": [w.k_hi - w.k_lo for w in sol.windows], "halo": DEFAULT_HALO,
+            "planes_per_slab": [w.k_hi - w.k_lo for w in sol.windows], "halo": halo,
             "path": "slabs.DistSlabSolver: NCCL halo exchange, one cooperative PCG launch per GPU with "
                     "boundary planes stored into the neighbours over NVLink (CUDA IPC) and a cross-GPU barrier"}),
               flush=True)
