@@ -161,6 +161,26 @@ def channel_2d(nx: int = 24, ny: int = 16, dt: float = 0.1, speed: float = 2.0) 
     }
 
 
+def karman(resolution: str = "desk", speed: float = 10.0) -> dict:
+    """The 2-D cylinder wake of the paper's validation (the reference's
+    scenarios/karman_desk.json and karman.json): a 46 mm cylinder in a
+    channel, inlet at y = 0, outlet at the top, side walls, seeded initial
+    perturbation 2% of the inlet speed."""
+    n, h, dt, steps = ((256, 384), 0.004, 2e-4, 4000) if resolution == "desk" else ((512, 768), 0.002, 1e-4, 20000)
+    return {
+        "version": 1, "name": "karman-desk" if resolution == "desk" else "karman-full",
+        "grid": {"nx": n[0], "ny": n[1], "nz": 1, "dx": h, "dy": h, "dz": h},
+        "boundaries": {"y_min": "inlet", "y_max": "outlet", "x_min": "solid_wall", "x_max": "solid_wall"},
+        "inlet": {"kind": "uniform", "speed": speed, "direction": [0, 1]},
+        "solver": {"dt": dt, "nu": 1.57e-5, "turbulence": True, "turb_intensity": 0.01, "u_ref": speed,
+                   "length_scale": 0.046},
+        "objects": [{"name": "cylinder", "kind": "building", "shape": "cylinder", "center": [0.512, 0.384],
+                     "radius": 0.023, "phi": 0.0}],
+        "run": {"steps": steps, "snapshot_every": 0 if resolution == "desk" else 4000},
+        "numerics": dict(_NUMERICS, perturb=0.02),
+    }
+
+
 def paint_rasters():
     """Raster and tree mask (ny=40, nx=48) of ``painted_city``: opaque, porous
     and noisy patches, a tree patch over a porous one (non-zero mask = tree)."""
