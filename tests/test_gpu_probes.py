@@ -63,3 +63,14 @@ def test_run_simulation_probes_on_device():
     for pi, p in enumerate(pts):
         assert np.allclose(out["probes"][pi][-1], probe_velocity(out["state"], p), rtol=0, atol=0)
     assert len(out["pcg_iterations"]) == 6
+
+
+def test_probed_run_longer_than_the_report_ring():
+    """run_simulation with probes enqueues steps without reading their reports;
+    a run longer than the device's report ring (4096) is read in batches."""
+    from paper_2204_01117_b200 import scenes
+    from paper_2204_01117_b200.scenario import run_simulation, scenario_from_dict
+    sc = scenario_from_dict(scenes.channel_2d(24, 16, 0.05, 1.0))
+    out = run_simulation(sc, steps=4200, snapshot_every=0, probes=[(10.0, 8.0, 0.5)])
+    assert out["probes"][0].shape == (4200, 3) and len(out["pcg_iterations"]) == 4200
+    assert abs(out["time"] - 4200 * 0.05) < 1e-9
